@@ -61,6 +61,8 @@ def lib():
         L.or_ellip_ke.argtypes = [d, pd, pd]
         L.or_legendre_q.restype = i
         L.or_legendre_q.argtypes = [d, d, i, i, i, pd]
+        L.or_forward_coef.restype = d
+        L.or_forward_coef.argtypes = [i, i]
         L.or_greens.restype = i
         L.or_greens.argtypes = [d, d, d, i, i, pd]
         L.or_rational_tables.restype = None
@@ -127,6 +129,10 @@ def legendre_q(chi: float, kp2: float, forward: bool, nmax: int, miller: int = M
     if rc != 0:
         raise ValueError("or_legendre_q failed")
     return out
+
+
+def forward_coef(nmax: int, miller: int = MILLER_ACCURATE) -> float:
+    return lib().or_forward_coef(nmax, miller)
 
 
 def greens(r: float, r1: float, x: float, nmax: int, miller: int = MILLER_ACCURATE):

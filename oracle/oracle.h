@@ -36,6 +36,9 @@ void or_ellip_ke(double kp2, double *K, double *E);
 /* Q_{n-1/2}(chi), n = 0..nmax.  kp2 = rho_-^2/rho_+^2 (complementary parameter);
  * forward != 0 selects the forward branch (chi < 1.008, R#3).  Returns 0 on success. */
 int or_legendre_q(double chi, double kp2, int forward, int nmax, int miller, double *Q);
+/* 2 t_N of the forward/backward switch chi - 1 < t_N (R#3): 0.016 in the paper mode and for
+ * nmax <= 16; 2 (cosh(ln 64 / (2 nmax)) - 1) beyond in the accurate mode. */
+double or_forward_coef(int nmax, int miller);
 /* G^(n)(r, r1, x), n = 0..nmax. Returns 0, or -1 if r<=0, r1<=0, coincident. */
 int or_greens(double r, double r1, double x, int nmax, int miller, double *G);
 

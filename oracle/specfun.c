@@ -129,6 +129,21 @@ int or_legendre_q(double chi, double kp2, int forward, int nmax, int miller, dou
     return 0;
 }
 
+/* Forward/backward switch (R#3): the paper's chi < 1.008.  In the accurate mode the
+ * forward branch is narrowed for large N so that its rounding growth lambda^{2N} stays below
+ * 2^6 (the paper ran N <= 17; for N <= 16 the rule is the paper's): chi - 1 < t_N with
+ * t_N = min(0.008, cosh(ln(64) / (2N)) - 1).  Returned as 2 t_N, compared as
+ * rho_-^2 < 2 t_N r r1 (chi - 1 = rho_-^2 / (2 r r1)). */
+double or_forward_coef(int nmax, int miller)
+{
+    double t = 0.008;
+    if (miller != OR_MILLER_PAPER && nmax > 0) {
+        double c = cosh(log(64.0) / (2.0 * nmax)) - 1.0;
+        if (c < t) t = c;
+    }
+    return 2.0 * t;
+}
+
 int or_greens(double r, double r1, double x, int nmax, int miller, double *G)
 {
     if (!(r > 0.0) || !(r1 > 0.0)) return -1;
@@ -138,7 +153,7 @@ int or_greens(double r, double r1, double x, int nmax, int miller, double *G)
     if (!(rho_m2 > 0.0)) return -1; /* coincident rings: log singularity */
     double chi = (r * r + r1 * r1 + x * x) / (2.0 * r * r1);
     double kp2 = rho_m2 / rho_p2;
-    int forward = rho_m2 < 0.016 * (r * r1); /* chi < 1.008 (R#3) */
+    int forward = rho_m2 < or_forward_coef(nmax, miller) * (r * r1); /* chi - 1 < t_N (R#3) */
     if (or_legendre_q(chi, kp2, forward, nmax, miller, G) != 0) return -1;
     double inv = 1.0 / (2.0 * M_PI * sqrt(r * r1));
     for (int n = 0; n <= nmax; ++n) G[n] *= inv;

@@ -74,13 +74,29 @@ def test_q_sequence_vs_mpmath(orc, chi, tol):
 
 
 def test_q_forward_branch_amplification_at_switch(orc):
-    # Finding 6: forward recursion just below chi = 1.008 loses ~lambda^(2n) ~ 1e8 at n = 64
+    # Finding 6: the paper's forward recursion just below chi = 1.008 loses ~lambda^(2n) ~ 1e8 at
+    # n = 64 (paper mode pins that the literal rule is kept there); the accurate mode narrows the
+    # forward branch for large N (R#3) and is accurate at the same point.
     r, r1, x, chi = _geom_for_chi(1.0079999)
-    G = orc.greens(r, r1, x, 64)
-    Q = G * 2 * math.pi
     ref = _q_ref(chi, 64)
-    rel = max(abs(Q[n] - float(ref[n])) / float(ref[n]) for n in range(65))
-    assert 1e-11 < rel < 1e-7
+    for miller, lo, hi in [(orc.MILLER_PAPER, 1e-11, 1e-7), (orc.MILLER_ACCURATE, 0.0, 1e-13)]:
+        Q = orc.greens(r, r1, x, 64, miller=miller) * 2 * math.pi
+        rel = max(abs(Q[n] - float(ref[n])) / float(ref[n]) for n in range(65))
+        assert lo <= rel < hi, (miller, rel)
+
+
+def test_forward_switch_rule(orc):
+    # R#3: the paper's chi < 1.008 in the paper mode and for N <= 16; beyond, in the
+    # accurate mode, the switch t_N satisfies lambda(1 + t_N)^(2N) = 64 exactly (closed form).
+    for n in (0, 1, 5, 16):
+        assert orc.forward_coef(n, orc.MILLER_ACCURATE) == 0.016
+    for n in (17, 32, 64, 100, 255):
+        assert orc.forward_coef(n, orc.MILLER_PAPER) == 0.016
+        t = orc.forward_coef(n, orc.MILLER_ACCURATE) / 2
+        assert t < 0.008
+        chi = mp.mpf(1) + t
+        lam = chi + mp.sqrt(chi * chi - 1)
+        assert float(lam ** (2 * n)) == pytest.approx(64.0, rel=1e-9)
 
 
 def test_miller_paper_mode_contamination(orc):
