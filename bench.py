@@ -1,0 +1,327 @@
+#!/usr/bin/env python
+"""bench.py -- the hot path of arXiv 2301.01179 on B200: one step = one full FMM solve
+(Algorithm 1: tree, P2M, M2M, tensors, S2L, L2L, L2P, near field) of BASELINE.json
+configs[1] (C2: N = M = 16,384 rings uniform in (0,1]x[0,1], modes n = 0..16, complex N(0,1)
+coefficients, p = 8, leaf size <= 32 -> depth 5, fields = sources with the self term excluded).
+
+Metric (BASELINE.json): FP64 modal source-field interactions per second, i.e. the
+direct-equivalent rate (N_s N_f - skipped) K / t_solve, plus the solve time and the FP64
+roofline fraction of the dominant kernel.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {cylfmm,reference}] [--config C2]
+
+--impl reference times the CPU oracle (oracle/, plain FP64 C, OpenMP) as it stands on the host
+cores -- this tier's reference arm (there is no reference implementation to install).
+Under torchrun (N > 1) field points are partitioned across ranks (north_star), sources are
+replicated (generated identically from the seed on every rank; no data-path collective).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2301_01179_b200.inputs import CONFIGS  # noqa: E402
+
+FP64_NOMINAL_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # DESIGN.md section 6 (derived, "alu")
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_problem(name):
+    pr = CONFIGS[name]()
+    return pr
+
+
+def n_interactions(pr, skipped):
+    return (len(pr.sr) * len(pr.fr) - skipped) * pr.K
+
+
+def shard(pr, rank, world):
+    nf = len(pr.fr)
+    a, b = rank * nf // world, (rank + 1) * nf // world
+    return pr.fr[a:b], pr.fz[a:b]
+
+
+def run_reference(args):
+    """Reference arm: the CPU oracle FMM as it stands, on this host's cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    pr = make_problem(args.config)
+    cores = os.cpu_count() or 1
+    # bounded sample: field subset sized so one step takes <= ~3 s on this host
+    nf = len(pr.fr)
+    t0 = time.perf_counter()
+    _, sk = oracle.fmm(pr.sr, pr.sz, pr.S, pr.fr[:256], pr.fz[:256], pr.p, pr.depth, pr.L, pr.z0,
+                       nthreads=cores)
+    t_probe = time.perf_counter() - t0
+    m = nf
+    if t_probe * nf / 256 > 3.0:
+        m = max(256, int(nf * 3.0 / (t_probe * nf / 256)))
+    fr, fz = pr.fr[:m], pr.fz[:m]
+    for _ in range(args.warmup):
+        oracle.fmm(pr.sr, pr.sz, pr.S, fr, fz, pr.p, pr.depth, pr.L, pr.z0, nthreads=cores)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        _, sk = oracle.fmm(pr.sr, pr.sz, pr.S, fr, fz, pr.p, pr.depth, pr.L, pr.z0, nthreads=cores)
+        ts.append(time.perf_counter() - t0)
+    t = sum(ts) / len(ts)
+    inter = (len(pr.sr) * m - sk) * pr.K
+    v = inter / t
+    sample = (f"oracle FMM (all {len(pr.sr)} sources, upward pass in full) evaluated at the first "
+              f"{m} of {nf} field points per step")
+    line = {"metric": "FP64 modal source-field interactions/s (direct-equivalent, FMM solve)",
+            "value": v, "unit": "interactions/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"{args.config}: {pr.name}", "n_src": len(pr.sr),
+                       "n_fld": m, "modes": pr.K, "order": pr.p, "depth": pr.depth},
+            "cpu_baseline": {"value": v, "unit": "interactions/s", "cores": cores,
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "interactions/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(pr, budget_s=12.0):
+    """The oracle as it stands, timed on this host's cores on a bounded sample of the workload."""
+    import oracle
+    oracle.build()
+    cores = os.cpu_count() or 1
+    nf = len(pr.fr)
+    m = min(nf, 1024)
+    t0 = time.perf_counter()
+    _, sk = oracle.fmm(pr.sr, pr.sz, pr.S, pr.fr[:m], pr.fz[:m], pr.p, pr.depth, pr.L, pr.z0,
+                       nthreads=cores)
+    t1 = time.perf_counter() - t0
+    if t1 < budget_s / 4 and m < nf:   # grow the sample to use the budget
+        m = min(nf, int(m * (budget_s / 2) / max(t1, 1e-3)))
+        t0 = time.perf_counter()
+        _, sk = oracle.fmm(pr.sr, pr.sz, pr.S, pr.fr[:m], pr.fz[:m], pr.p, pr.depth, pr.L, pr.z0,
+                           nthreads=cores)
+        t1 = time.perf_counter() - t0
+    inter = (len(pr.sr) * m - sk) * pr.K
+    return {"value": inter / t1, "unit": "interactions/s", "cores": cores, "kind": "oracle",
+            "sample": f"one oracle FMM solve: all {len(pr.sr)} sources, the first {m} of {nf} "
+                      f"field points ({t1:.1f} s)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="cylfmm", choices=["cylfmm", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "cylfmm" else args.warmup
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    import paper_2301_01179_b200 as g
+    from paper_2301_01179_b200 import build as b
+    if not b.up_to_date():
+        b.build()
+    pr = make_problem(args.config)
+    fr, fz = shard(pr, rank, world)
+    dev = torch.device("cuda", local)
+    sr = torch.as_tensor(pr.sr, device=dev)
+    sz = torch.as_tensor(pr.sz, device=dev)
+    S = torch.as_tensor(pr.S, device=dev)
+    fr_d = torch.as_tensor(fr, device=dev)
+    fz_d = torch.as_tensor(fz, device=dev)
+    out = torch.empty((len(fr), pr.K), dtype=torch.complex128, device=dev)
+    plan = g.Plan(g.FMMConfig(n_modes=pr.K, order=pr.p, depth=pr.depth, L=pr.L, z0=pr.z0))
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    # warm-up + per-phase breakdown (synchronising timings path, outside the timed region)
+    for _ in range(args.warmup):
+        plan.solve(sr, sz, S, fr_d, fz_d, out=out)
+    _, tm = plan.solve(sr, sz, S, fr_d, fz_d, out=out, timings=True)
+    phase = {k: v for k, v in tm.items()}
+    launches_per_step = tm["kernel_launches"]
+    skipped = tm["n_skipped"]
+
+    # timed region: K solves, L2 flushed between them (not timed), CUDA events on the stream
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.4)
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        plan.solve(sr, sz, S, fr_d, fz_d, out=out)
+        ev[i][1].record(stream)
+    barrier()
+    ms = [a.elapsed_time(bb) for a, bb in ev]
+    clk = clocks.stop()
+    t_step = sum(ms) / len(ms)
+    t_max = t_step
+    if world > 1:
+        tt = torch.tensor([t_step], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+        sk = torch.tensor([skipped], device=dev, dtype=torch.int64)
+        dist.all_reduce(sk)
+        skipped = int(sk.item())
+    inter_total = (len(pr.sr) * len(pr.fr) - skipped) * pr.K
+    value = inter_total / (t_max * 1e-3)
+
+    # e2e through the host-buffer C-ABI call (pinned host memory, H2D + D2H inside the region)
+    hs = [torch.as_tensor(a).pin_memory() for a in (pr.sr, pr.sz)]
+    hS = torch.as_tensor(pr.S).pin_memory()
+    hf = [torch.as_tensor(np.ascontiguousarray(a)).pin_memory() for a in (fr, fz)]
+    hout = torch.empty((len(fr), pr.K), dtype=torch.complex128).pin_memory()
+    for _ in range(2):
+        plan.solve_host(hs[0].numpy(), hs[1].numpy(), hS.numpy(), hf[0].numpy(), hf[1].numpy(),
+                        out=hout.numpy())
+    barrier()
+    e2e_ms = []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        plan.solve_host(hs[0].numpy(), hs[1].numpy(), hS.numpy(), hf[0].numpy(), hf[1].numpy(),
+                        out=hout.numpy())
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    t_e2e = sum(e2e_ms) / len(e2e_ms)
+    if world > 1:
+        tt = torch.tensor([t_e2e], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = float(tt.item())
+    h2d = len(pr.sr) * (16 + 16 * pr.K) + len(fr) * 16
+    d2h = len(fr) * pr.K * 16
+
+    # roofline of the dominant kernel (FP64 CUDA-core arithmetic: "alu")
+    P = (pr.p + 1) * (pr.p + 2) // 2
+    s2l_flops = tm["n_s2l_pairs"] * 4 * P * P * pr.K
+    dom = max(("s2l", phase["ms_s2l"]), ("p2p", phase["ms_p2p"]), key=lambda x: x[1])
+    pk = peaks()
+    roof = None
+    if dom[0] == "s2l" and phase["ms_s2l"] > 0:
+        ach = s2l_flops / (phase["ms_s2l"] * 1e-3) / 1e12
+        roof = {"bound": "alu", "kernel": "s2l_kernel (all levels)", "achieved": ach,
+                "peak": FP64_NOMINAL_TFLOPS, "unit": "TFLOP/s", "frac": ach / FP64_NOMINAL_TFLOPS,
+                "traffic": None, "algorithmic_flops": s2l_flops,
+                "peak_note": "FP64 nominal 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md 6)"}
+    else:
+        roof = {"bound": "alu", "kernel": "p2p_kernel (near field)", "achieved": None,
+                "peak": FP64_NOMINAL_TFLOPS, "unit": "TFLOP/s", "frac": None, "traffic": None}
+
+    if rank == 0:
+        line = {"metric": "FP64 modal source-field interactions/s (direct-equivalent, FMM solve)",
+                "value": value, "unit": "interactions/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": t_max, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": f"{args.config}: {pr.name}", "n_src": len(pr.sr),
+                           "n_fld": len(pr.fr), "modes": pr.K, "order": pr.p, "depth": pr.depth,
+                           "truncation": "double", "miller": "accurate", "l2": "flushed",
+                           "parallelism": f"field-partition x{world}"},
+                "phase_ms": {k: round(v, 4) for k, v in phase.items() if k.startswith("ms_")},
+                "near_pairs": phase["n_near_pairs"], "s2l_box_pairs": phase["n_s2l_pairs"],
+                "roofline": roof, "clocks": clk,
+                "e2e": {"value": inter_total / (t_e2e * 1e-3), "unit": "interactions/s",
+                        "ms_per_step": t_e2e, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                "gpu_launches": launches_per_step * args.steps}
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(pr)
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

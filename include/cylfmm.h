@@ -1,0 +1,165 @@
+/*
+ * cylfmm.h -- C-ABI of libcylfmm.so, the B200-native (sm_100a) FP64 hot path of
+ * M. Carley, "A fast multipole method for ... ring sources in cylindrical coordinates"
+ * (arXiv 2301.01179).  Citations "P:n" are line numbers of the paper text;
+ * "R#k" are the readings of DESIGN.md section 3 where the paper is silent or garbled.
+ *
+ * Problem: ring sources at (r_i, z_i) carrying per-mode complex Fourier
+ * coefficients S_i^(n), n = 0..N (K = N+1 modes).  Output: the modal potentials
+ *     Phi^(n)(r_j, z_j) = sum_i S_i^(n) G^(n)(r_j, r_i, z_j - z_i)
+ * with the modal ring Green's function G^(n) = Q_{n-1/2}(chi) / (2 pi sqrt(r r1)),
+ * chi = (r^2 + r1^2 + x^2) / (2 r r1),
+ * either summed directly or by the paper's uniform (r, z) quadtree FMM (Algorithm 1).
+ *
+ * Conventions for every entry point
+ *  - Pointers marked DEVICE are device pointers on the current CUDA device; pointers marked
+ *    HOST are ordinary host memory (pinned or pageable).  All arrays are C-contiguous.
+ *  - Real arrays are IEEE binary64.  Complex arrays are interleaved (re, im) binary64 pairs,
+ *    row-major [point][mode], i.e. element (j, n) at doubles 2*(j*K+n), 2*(j*K+n)+1.
+ *  - The caller owns every buffer passed in; the library never frees or retains them beyond
+ *    the call (device buffers must stay valid until work queued on `stream` completes).
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Device-side work is queued
+ *    asynchronously on it; the *_host entry points and cylfmm_plan_sync() synchronise.
+ *  - Errors are returned as cylfmm_status codes; nothing throws across the ABI.  A detail
+ *    message for the last failure on the calling thread is available from cylfmm_last_error().
+ *    Argument errors (EINVAL / EDOMAIN) are detected before any work is queued and leave the
+ *    outputs untouched.
+ *  - Coincident pairs (bitwise-equal (r, z)) are the logarithmic singularity of the ring kernel;
+ *    with exclude_coincident = 1 they are skipped (the "self term", R#15), otherwise they are
+ *    reported as CYLFMM_ENUMERIC.
+ */
+#ifndef CYLFMM_H
+#define CYLFMM_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *cylfmm_stream_t; /* == cudaStream_t */
+
+typedef enum {
+    CYLFMM_OK = 0,
+    CYLFMM_EINVAL = 1,   /* null pointer, bad size / order / depth / mode count */
+    CYLFMM_EDOMAIN = 2,  /* r <= 0, non-finite coordinate, point outside the FMM domain */
+    CYLFMM_ENUMERIC = 3, /* unexcluded coincident pair, non-finite result */
+    CYLFMM_ECUDA = 4,    /* CUDA runtime error (message in cylfmm_last_error) */
+    CYLFMM_ENCCL = 5,    /* reserved: collective failure */
+    CYLFMM_ENOMEM = 6    /* device allocation failed */
+} cylfmm_status;
+
+/* Miller start rule for the backward recursion (R#4). */
+enum { CYLFMM_MILLER_ACCURATE = 0, /* contamination of Q_{n-1/2} below ~e^-40 */
+       CYLFMM_MILLER_PAPER = 1 };  /* the paper's literal start index N + 80 */
+/* S2L truncation (R#8). */
+enum { CYLFMM_TRUNC_DOUBLE = 0,    /* source i+j <= p and local k+l <= p (default) */
+       CYLFMM_TRUNC_SINGLE = 1 };  /* joint i+j+k+l <= p */
+
+/* Limits of this build. */
+#define CYLFMM_MAX_MODES 256   /* K <= 256 */
+#define CYLFMM_MAX_ORDER 20    /* p <= 20 */
+#define CYLFMM_MAX_DEPTH 11    /* d <= 11 (leaf Morton keys fit 22 bits) */
+
+typedef struct {
+    int n_modes;            /* K = N+1 >= 1 */
+    int order;              /* p >= 1, the paper's expansion order M */
+    int depth;              /* d, 2 <= d <= CYLFMM_MAX_DEPTH */
+    int truncation;         /* CYLFMM_TRUNC_* */
+    int miller;             /* CYLFMM_MILLER_* */
+    int exclude_coincident; /* 1: skip bitwise-coincident pairs (R#15) */
+    double domain_z0;       /* the square domain is [0, L] x [z0, z0 + L] (R#11) */
+    double domain_L;        /* L > 0; a power of two keeps box indices bit-exact */
+    int mode_chunk;         /* far-field passes run over modes in chunks of this many; 0 = all */
+} cylfmm_params;
+
+/* Per-phase device times of the last solve, milliseconds (CUDA events on the solve stream). */
+typedef struct {
+    double ms_tree, ms_p2m, ms_m2m, ms_tensor, ms_s2l, ms_l2l, ms_l2p, ms_p2p, ms_total;
+    int64_t n_near_pairs;  /* near-field (source, field) pairs evaluated, coincident excluded */
+    int64_t n_skipped;     /* coincident pairs skipped */
+    int64_t n_s2l_pairs;   /* (source box, target box) S2L applications, all levels */
+    int64_t kernel_launches;
+} cylfmm_timings;
+
+typedef struct cylfmm_plan_s *cylfmm_plan;
+
+const char *cylfmm_status_string(cylfmm_status s);
+/* Detail message of the last failing call on this thread ("" if none). */
+const char *cylfmm_last_error(void);
+/* Library version string and the SM architecture it was compiled for ("sm_100a"). */
+const char *cylfmm_version(void);
+
+/* ---------------------------------------------------------------------------------------
+ * Direct modal sum: out_Phi[j][n] = sum_i S_i^(n) G^(n)(fld_r[j], src_r[i],
+ * fld_z[j] - src_z[i]), n = 0..n_modes-1, coincident pairs skipped if exclude_coincident.
+ *   src_r, src_z : DEVICE double[n_src]; src_r > 0, finite.
+ *   src_S        : DEVICE complex128[n_src][n_modes].
+ *   fld_r, fld_z : DEVICE double[n_fld];  fld_r > 0, finite.
+ *   out_Phi      : DEVICE complex128[n_fld][n_modes], overwritten.
+ *   miller       : CYLFMM_MILLER_*.
+ * Summation over i is in a fixed order: results are bitwise reproducible.
+ * Returns CYLFMM_ENUMERIC (after synchronising) if an unexcluded coincident pair was met.
+ * --------------------------------------------------------------------------------------- */
+cylfmm_status cylfmm_direct(const double *src_r, const double *src_z, const double *src_S,
+                            int64_t n_src, const double *fld_r, const double *fld_z,
+                            int64_t n_fld, int n_modes, int miller, int exclude_coincident,
+                            double *out_Phi, cylfmm_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
+ * FMM plan.  The plan owns its device workspace (grown on demand, freed by destroy).
+ * One plan serves one device and one solve at a time.
+ * --------------------------------------------------------------------------------------- */
+cylfmm_status cylfmm_plan_create(cylfmm_plan *plan, const cylfmm_params *prm);
+void cylfmm_plan_destroy(cylfmm_plan plan);
+cylfmm_status cylfmm_plan_sync(cylfmm_plan plan);
+
+/* FMM solve, Algorithm 1 of the paper:
+ *   tree (Morton sort of sources and fields on the uniform depth-d quadtree)
+ *   -> P2M -> M2M l = d-1..2
+ *   -> for l = 2..d: L2L from l-1, S2L from the interaction list with the
+ *      FO/BO/FI/BI variants of the tensor at (outer centre, inner centre, |dz|) (P:411-423,
+ *      492-537, 561-568)
+ *   -> leaves: L2P + direct sum over the 9 neighbour leaves.
+ * Inputs as for cylfmm_direct (DEVICE); every point must lie in the plan's domain
+ * (0 < r <= L, z0 <= z <= z0 + L), else CYLFMM_EDOMAIN.  out_Phi (DEVICE) is in input field
+ * order.  Timings (HOST, nullable) are filled after an internal synchronisation when given.
+ * The far field runs over modes in chunks of prm.mode_chunk (results identical). */
+cylfmm_status cylfmm_fmm_solve(cylfmm_plan plan, const double *src_r, const double *src_z,
+                               const double *src_S, int64_t n_src, const double *fld_r,
+                               const double *fld_z, int64_t n_fld, double *out_Phi,
+                               cylfmm_stream_t stream, cylfmm_timings *timings);
+
+/* Same as cylfmm_fmm_solve with HOST input and output buffers: copies the inputs to the
+ * device, solves, copies out_Phi back and synchronises `stream` before returning. */
+cylfmm_status cylfmm_fmm_solve_host(cylfmm_plan plan, const double *src_r, const double *src_z,
+                                    const double *src_S, int64_t n_src, const double *fld_r,
+                                    const double *fld_z, int64_t n_fld, double *out_Phi,
+                                    cylfmm_stream_t stream, cylfmm_timings *timings);
+
+/* ---------------------------------------------------------------------------------------
+ * Test entry points (batched, DEVICE pointers, asynchronous on `stream`).
+ * --------------------------------------------------------------------------------------- */
+
+/* G^(n)(r[q], r1[q], x[q]), n = 0..n_modes-1: out_G DEVICE double[n][n_modes].
+ * r, r1 > 0 and (r, x) != (r1, 0) required (else CYLFMM_EDOMAIN is flagged on sync). */
+cylfmm_status cylfmm_greens_batch(const double *r, const double *r1, const double *x, int64_t n,
+                                  int n_modes, int miller, double *out_G, cylfmm_stream_t stream);
+
+/* Derivative tensor Gbar^n_{abc} = (1/(a!b!c!)) d^{a+b+c} G^(n)/dr^a dr1^b dx^c (P:876-1065,
+ * Laplace recursion corrected per R#6), modes 0..n_modes-1, a, b <= p, a+b+c <= 2p.
+ * out DEVICE double[n][n_modes][p+1][p+1][2p+1], zero where a+b+c > 2p. */
+cylfmm_status cylfmm_tensor_batch(const double *r, const double *r1, const double *x, int64_t n,
+                                  int n_modes, int p, int miller, double *out,
+                                  cylfmm_stream_t stream);
+
+/* Leaf keys and stable Morton sort (R#11): for points (r, z) DEVICE
+ * double[n] at depth d on [0, L] x [z0, z0 + L]: key[i] = interleave(ix, iz) (radial index
+ * in the even bits), perm = stable argsort(key) (DEVICE int32[n] each; key as uint32). */
+cylfmm_status cylfmm_tree_sort(const double *r, const double *z, int64_t n, int depth,
+                               double L, double z0, uint32_t *key, int32_t *perm,
+                               cylfmm_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

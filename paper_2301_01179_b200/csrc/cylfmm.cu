@@ -1,0 +1,931 @@
+// cylfmm.cu -- libcylfmm.so: the C-ABI of include/cylfmm.h and the single-GPU orchestration of
+// the paper's Algorithm 1.  Product code for sm_100a; independent of oracle/.
+#include "../../include/cylfmm.h"
+
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+
+#include <algorithm>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "fmm_ops.cuh"
+#include "p2p.cuh"
+#include "specfun.cuh"
+#include "tensor.cuh"
+#include "tree.cuh"
+
+using namespace cyl;
+
+// ------------------------------------------------------------------------------------------
+// errors
+static thread_local std::string g_last_error;
+static void set_err(const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+}
+#define CK(call)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess) {                                                              \
+            set_err("%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_));       \
+            return e_ == cudaErrorMemoryAllocation ? CYLFMM_ENOMEM : CYLFMM_ECUDA;            \
+        }                                                                                     \
+    } while (0)
+#define CKL()  CK(cudaGetLastError())
+#define RET_IF(st)                                                                            \
+    do {                                                                                      \
+        cylfmm_status s_ = (st);                                                              \
+        if (s_ != CYLFMM_OK) return s_;                                                       \
+    } while (0)
+
+extern "C" const char *cylfmm_status_string(cylfmm_status s)
+{
+    switch (s) {
+    case CYLFMM_OK: return "ok";
+    case CYLFMM_EINVAL: return "invalid argument";
+    case CYLFMM_EDOMAIN: return "point outside the domain (r <= 0, non-finite, or outside [0,L]x[z0,z0+L])";
+    case CYLFMM_ENUMERIC: return "numerical error (unexcluded coincident pair or non-finite value)";
+    case CYLFMM_ECUDA: return "CUDA error";
+    case CYLFMM_ENCCL: return "NCCL error";
+    case CYLFMM_ENOMEM: return "out of device memory";
+    }
+    return "unknown status";
+}
+extern "C" const char *cylfmm_last_error(void) { return g_last_error.c_str(); }
+extern "C" const char *cylfmm_version(void) { return "cylfmm-b200 0.1 (sm_100a, FP64)"; }
+
+// ------------------------------------------------------------------------------------------
+// per-device init: recursion tables into constant memory, smem opt-in for the kernels
+static std::mutex g_init_mu;
+static bool g_init_done[64];
+
+template <typename F>
+static cudaError_t allow_smem(F *kernel)
+{
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+}
+
+#define P2P_INSTANCES(X)                                                                       \
+    X(8, 16, 2) X(8, 16, 5) X(16, 8, 3) X(16, 8, 9) X(32, 4, 6) X(32, 4, 18)
+
+using S2L8 = S2LCfg<128, 8, 6, 2, 48>;
+#define S2L_P8 128, 8, 6, 2, 48
+#define S2L_P12 256, 16, 6, 4, 32
+#define S2L_P16 256, 16, 10, 4, 32
+#define S2L_P20 256, 16, 16, 4, 32
+
+static cylfmm_status ensure_init()
+{
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_init_mu);
+    if (dev < 64 && g_init_done[dev]) return CYLFMM_OK;
+    RecTables *t = new RecTables;
+    build_rec_tables(t);
+    cudaError_t e = cudaMemcpyToSymbol(c_rec, t, sizeof(RecTables));
+    delete t;
+    CK(e);
+#define X(TT, SC, MT)                                                                          \
+    CK(allow_smem(p2p_kernel<TT, SC, MT, true>));                                              \
+    CK(allow_smem(p2p_kernel<TT, SC, MT, false>));
+    P2P_INSTANCES(X)
+#undef X
+    CK(allow_smem(tensor_seed_kernel));
+    CK(allow_smem(tensor_fill_kernel));
+    CK(allow_smem(p2m_kernel));
+    CK(allow_smem(m2m_kernel));
+    CK(allow_smem(l2l_kernel));
+    CK(allow_smem(l2p_kernel));
+    CK(allow_smem(s2l_kernel<S2L_P8>));
+    CK(allow_smem(s2l_kernel<S2L_P12>));
+    CK(allow_smem(s2l_kernel<S2L_P16>));
+    CK(allow_smem(s2l_kernel<S2L_P20>));
+    if (dev < 64) g_init_done[dev] = true;
+    return CYLFMM_OK;
+}
+
+static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+// ------------------------------------------------------------------------------------------
+// P2P launcher (direct and near field)
+template <int TT, int SC, int MT, bool NEAR>
+static cudaError_t launch_p2p_t(const P2PArgs &a, dim3 grid, cudaStream_t st)
+{
+    size_t sm = p2p_smem_bytes<TT, SC>(a.m1 - a.m0);
+    p2p_kernel<TT, SC, MT, NEAR><<<grid, TT * SC, sm, st>>>(a);
+    return cudaGetLastError();
+}
+
+// pick (TT, SC, MAXT) for a target tile size and mode window; grid.x must be set by caller
+template <bool NEAR>
+static cudaError_t launch_p2p(int TT, const P2PArgs &a, dim3 grid, cudaStream_t st)
+{
+    int KW = a.m1 - a.m0;
+    if (TT == 8) return KW <= 32 ? launch_p2p_t<8, 16, 2, NEAR>(a, grid, st)
+                                 : launch_p2p_t<8, 16, 5, NEAR>(a, grid, st);
+    if (TT == 16) return KW <= 24 ? launch_p2p_t<16, 8, 3, NEAR>(a, grid, st)
+                                  : launch_p2p_t<16, 8, 9, NEAR>(a, grid, st);
+    return KW <= 24 ? launch_p2p_t<32, 4, 6, NEAR>(a, grid, st)
+                    : launch_p2p_t<32, 4, 18, NEAR>(a, grid, st);
+}
+static constexpr int kP2PWindow = 72;
+
+// ------------------------------------------------------------------------------------------
+// direct modal sum
+extern "C" cylfmm_status cylfmm_direct(const double *src_r, const double *src_z,
+                                       const double *src_S, int64_t n_src, const double *fld_r,
+                                       const double *fld_z, int64_t n_fld, int n_modes,
+                                       int miller, int exclude_coincident, double *out_Phi,
+                                       cylfmm_stream_t stream)
+{
+    if (n_src < 0 || n_fld < 0 || n_modes < 1 || n_modes > CYLFMM_MAX_MODES ||
+        (miller != 0 && miller != 1) || n_src > INT32_MAX || n_fld > INT32_MAX) {
+        set_err("cylfmm_direct: bad sizes (n_src=%lld n_fld=%lld n_modes=%d miller=%d)",
+                (long long)n_src, (long long)n_fld, n_modes, miller);
+        return CYLFMM_EINVAL;
+    }
+    if ((n_src > 0 && (!src_r || !src_z || !src_S)) || (n_fld > 0 && (!fld_r || !fld_z || !out_Phi))) {
+        set_err("cylfmm_direct: null pointer");
+        return CYLFMM_EINVAL;
+    }
+    RET_IF(ensure_init());
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n_fld == 0) return CYLFMM_OK;
+    const int K = n_modes;
+    if (n_src == 0) {
+        CK(cudaMemsetAsync(out_Phi, 0, sizeof(double) * 2 * K * n_fld, st));
+        return CYLFMM_OK;
+    }
+    int dev = 0, nsm = 148;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    const int TT = 32, SC = 4;
+    int64_t tiles = (n_fld + TT - 1) / TT;
+    int64_t want = (int64_t)nsm * 4;
+    int nparts = (int)std::max<int64_t>(1, std::min<int64_t>((want + tiles - 1) / tiles, (n_src + 63) / 64));
+    int64_t per = (n_src + nparts - 1) / nparts;
+    per = (per + SC - 1) / SC * SC;
+    nparts = (int)((n_src + per - 1) / per);
+    int *d_err = nullptr;
+    double2 *ws = nullptr;
+    CK(cudaMallocAsync((void **)&d_err, sizeof(int), st));
+    CK(cudaMemsetAsync(d_err, 0, sizeof(int), st));
+    if (nparts > 1) CK(cudaMallocAsync((void **)&ws, sizeof(double2) * (size_t)nparts * n_fld * K, st));
+    for (int m0 = 0; m0 < K; m0 += kP2PWindow) {
+        P2PArgs a = {};
+        a.sr = src_r;
+        a.sz = src_z;
+        a.S = reinterpret_cast<const double2 *>(src_S);
+        a.fr = fld_r;
+        a.fz = fld_z;
+        a.ns = n_src;
+        a.nf = n_fld;
+        a.K = K;
+        a.m0 = m0;
+        a.m1 = std::min(K, m0 + kP2PWindow);
+        a.miller = miller;
+        a.fwd2 = forward_coef(K - 1, miller);
+        a.exclude = exclude_coincident;
+        a.out = nparts > 1 ? ws : reinterpret_cast<double2 *>(out_Phi);
+        a.out_row = nullptr;
+        a.accumulate = 0;
+        a.part_stride = n_fld * K;
+        a.src_per_part = per;
+        a.err_flag = d_err;
+        CK(launch_p2p<false>(TT, a, dim3((unsigned)tiles, nparts), st));
+    }
+    if (nparts > 1) {
+        int64_t ne = n_fld * K;
+        reduce_parts_kernel<<<nblk(ne, 256), 256, 0, st>>>(ws, ne, nparts,
+                                                          reinterpret_cast<double2 *>(out_Phi));
+        CKL();
+        CK(cudaFreeAsync(ws, st));
+    }
+    int h_err = 0;
+    CK(cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaFreeAsync(d_err, st));
+    CK(cudaStreamSynchronize(st));
+    if (h_err) {
+        set_err("cylfmm_direct: unexcluded coincident source/field pair");
+        return CYLFMM_ENUMERIC;
+    }
+    return CYLFMM_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// Green's function and tensor test entry points
+extern "C" cylfmm_status cylfmm_greens_batch(const double *r, const double *r1, const double *x,
+                                             int64_t n, int n_modes, int miller, double *out_G,
+                                             cylfmm_stream_t stream)
+{
+    if (n < 0 || n_modes < 1 || n_modes > CYLFMM_MAX_MODES || (miller != 0 && miller != 1) ||
+        (n > 0 && (!r || !r1 || !x || !out_G))) {
+        set_err("cylfmm_greens_batch: bad arguments");
+        return CYLFMM_EINVAL;
+    }
+    RET_IF(ensure_init());
+    if (n == 0) return CYLFMM_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    int *d_err;
+    CK(cudaMallocAsync((void **)&d_err, sizeof(int), st));
+    CK(cudaMemsetAsync(d_err, 0, sizeof(int), st));
+    greens_batch_kernel<<<nblk(n, 128), 128, 0, st>>>(r, r1, x, n, n_modes, miller,
+                                                      forward_coef(n_modes - 1, miller), out_G, d_err);
+    CKL();
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaFreeAsync(d_err, st));
+    CK(cudaStreamSynchronize(st));
+    if (h & 2) {
+        set_err("cylfmm_greens_batch: r <= 0 or r1 <= 0");
+        return CYLFMM_EDOMAIN;
+    }
+    if (h & 1) {
+        set_err("cylfmm_greens_batch: coincident rings");
+        return CYLFMM_ENUMERIC;
+    }
+    return CYLFMM_OK;
+}
+
+static cylfmm_status run_tensors(TensorGeomArgs ta, int64_t ngeom, cudaStream_t st)
+{
+    const int p = ta.p, D = 2 * p + 1;
+    int Nw = ta.m1 - 1, Ni = Nw > 1 ? Nw : 1;
+    (void)Ni;
+    size_t sm_seed = tensor_seed_smem(ta.K, ta.m1, p);
+    tensor_seed_kernel<<<(unsigned)ngeom, 128, sm_seed, st>>>(ta);
+    CKL();
+    size_t sm_fill = sizeof(double) * (size_t)(p + 1) * (p + 1) * D;
+    int KW = ta.m1 - ta.m0;
+    tensor_fill_kernel<<<(unsigned)(ngeom * KW), 256, sm_fill, st>>>(ta);
+    CKL();
+    return CYLFMM_OK;
+}
+
+extern "C" cylfmm_status cylfmm_tensor_batch(const double *r, const double *r1, const double *x,
+                                             int64_t n, int n_modes, int p, int miller,
+                                             double *out, cylfmm_stream_t stream)
+{
+    if (n < 0 || n_modes < 1 || n_modes > CYLFMM_MAX_MODES || p < 1 || p > CYLFMM_MAX_ORDER ||
+        (miller != 0 && miller != 1) || (n > 0 && (!r || !r1 || !x || !out))) {
+        set_err("cylfmm_tensor_batch: bad arguments");
+        return CYLFMM_EINVAL;
+    }
+    RET_IF(ensure_init());
+    if (n == 0) return CYLFMM_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    int Ni = std::max(n_modes - 1, 1), NM = Ni + 1, D = 2 * p + 1;
+    double *seeds;
+    int *d_err;
+    CK(cudaMallocAsync((void **)&seeds, sizeof(double) * (size_t)n * 4 * NM * D, st));
+    CK(cudaMallocAsync((void **)&d_err, sizeof(int), st));
+    CK(cudaMemsetAsync(d_err, 0, sizeof(int), st));
+    TensorGeomArgs ta = {};
+    ta.r = r;
+    ta.r1 = r1;
+    ta.x = x;
+    ta.n = n;
+    ta.K = n_modes;
+    ta.m0 = 0;
+    ta.m1 = n_modes;
+    ta.p = p;
+    ta.miller = miller;
+    ta.fwd2 = forward_coef(std::max(n_modes - 1, 1), miller);
+    ta.seeds = seeds;
+    ta.out = out;
+    ta.packed = 0;
+    ta.err = d_err;
+    RET_IF(run_tensors(ta, n, st));
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaFreeAsync(seeds, st));
+    CK(cudaFreeAsync(d_err, st));
+    CK(cudaStreamSynchronize(st));
+    if (h & 2) {
+        set_err("cylfmm_tensor_batch: r <= 0 or r1 <= 0");
+        return CYLFMM_EDOMAIN;
+    }
+    if (h & 1) {
+        set_err("cylfmm_tensor_batch: coincident geometry");
+        return CYLFMM_ENUMERIC;
+    }
+    return CYLFMM_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// plan
+struct DevBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+    cylfmm_status need(size_t bytes)
+    {
+        if (bytes <= cap) return CYLFMM_OK;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t b = std::max<size_t>(bytes, 256);
+        CK(cudaMalloc(&p, b));
+        cap = b;
+        return CYLFMM_OK;
+    }
+    template <typename T> T *as() const { return reinterpret_cast<T *>(p); }
+    void release()
+    {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+struct cylfmm_plan_s {
+    cylfmm_params prm;
+    int device = 0;
+    int nsm = 148;
+    // tree buffers
+    DevBuf skey, sidx, skey2, sidx2, fkey, fidx, fkey2, fidx2, hist, scan_tmp[4];
+    DevBuf sr_s, sz_s, S_s, fr_s, fz_s;
+    DevBuf slstart, flstart, flags, smap, skeys, tmap, tkeys, counts;
+    DevBuf M, Lc, tens, seeds;
+    DevBuf tasks, ntasks, tcnt, toff;
+    DevBuf err, ctr;
+    // host-API staging
+    DevBuf h_sr, h_sz, h_S, h_fr, h_fz, h_out;
+    cudaEvent_t ev[16];
+    bool ev_ok = false;
+    int64_t launches = 0;
+};
+
+static void free_plan_bufs(cylfmm_plan p)
+{
+    DevBuf *all[] = {&p->skey, &p->sidx, &p->skey2, &p->sidx2, &p->fkey, &p->fidx, &p->fkey2,
+                     &p->fidx2, &p->hist, &p->scan_tmp[0], &p->scan_tmp[1], &p->scan_tmp[2],
+                     &p->scan_tmp[3], &p->sr_s, &p->sz_s, &p->S_s, &p->fr_s, &p->fz_s,
+                     &p->slstart, &p->flstart, &p->flags, &p->smap, &p->skeys, &p->tmap,
+                     &p->tkeys, &p->counts, &p->M, &p->Lc, &p->tens, &p->seeds, &p->tasks,
+                     &p->ntasks, &p->tcnt, &p->toff, &p->err, &p->ctr, &p->h_sr, &p->h_sz,
+                     &p->h_S, &p->h_fr, &p->h_fz, &p->h_out};
+    for (DevBuf *b : all) b->release();
+}
+
+extern "C" cylfmm_status cylfmm_plan_create(cylfmm_plan *plan, const cylfmm_params *prm)
+{
+    if (!plan || !prm) {
+        set_err("cylfmm_plan_create: null pointer");
+        return CYLFMM_EINVAL;
+    }
+    *plan = nullptr;
+    const cylfmm_params &q = *prm;
+    if (q.n_modes < 1 || q.n_modes > CYLFMM_MAX_MODES || q.order < 1 || q.order > CYLFMM_MAX_ORDER ||
+        q.depth < 2 || q.depth > CYLFMM_MAX_DEPTH || (q.truncation != 0 && q.truncation != 1) ||
+        (q.miller != 0 && q.miller != 1) || !(q.domain_L > 0.0) || !(q.domain_z0 == q.domain_z0) ||
+        q.mode_chunk < 0) {
+        set_err("cylfmm_plan_create: bad parameters (K=%d p=%d d=%d trunc=%d miller=%d L=%g)",
+                q.n_modes, q.order, q.depth, q.truncation, q.miller, q.domain_L);
+        return CYLFMM_EINVAL;
+    }
+    RET_IF(ensure_init());
+    cylfmm_plan p = new cylfmm_plan_s;
+    p->prm = q;
+    CK(cudaGetDevice(&p->device));
+    CK(cudaDeviceGetAttribute(&p->nsm, cudaDevAttrMultiProcessorCount, p->device));
+    for (int i = 0; i < 16; ++i) CK(cudaEventCreate(&p->ev[i]));
+    p->ev_ok = true;
+    *plan = p;
+    return CYLFMM_OK;
+}
+
+extern "C" void cylfmm_plan_destroy(cylfmm_plan plan)
+{
+    if (!plan) return;
+    cudaDeviceSynchronize();
+    free_plan_bufs(plan);
+    if (plan->ev_ok)
+        for (int i = 0; i < 16; ++i) cudaEventDestroy(plan->ev[i]);
+    delete plan;
+}
+
+static cylfmm_status check_err_flag(cylfmm_plan p, cudaStream_t st)
+{
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, p->err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (h & 4) {
+        set_err("cylfmm: point outside the domain [0,L]x[z0,z0+L] or r <= 0 / non-finite");
+        return CYLFMM_EDOMAIN;
+    }
+    if (h & 3) {
+        set_err("cylfmm: unexcluded coincident pair or degenerate geometry");
+        return CYLFMM_ENUMERIC;
+    }
+    return CYLFMM_OK;
+}
+
+extern "C" cylfmm_status cylfmm_plan_sync(cylfmm_plan plan)
+{
+    if (!plan) {
+        set_err("cylfmm_plan_sync: null plan");
+        return CYLFMM_EINVAL;
+    }
+    CK(cudaDeviceSynchronize());
+    if (plan->err.p) return check_err_flag(plan, nullptr);
+    return CYLFMM_OK;
+}
+
+// exclusive scan in place on d (n ints), scratch from plan->scan_tmp[depth]
+static cylfmm_status scan_excl(cylfmm_plan p, int *d, int64_t n, cudaStream_t st, int lvl = 0)
+{
+    if (n <= 0) return CYLFMM_OK;
+    int64_t nt = (n + kScanTile - 1) / kScanTile;
+    if (lvl >= 4) {
+        set_err("scan: too deep");
+        return CYLFMM_EINVAL;
+    }
+    RET_IF(p->scan_tmp[lvl].need(sizeof(int) * (size_t)std::max<int64_t>(nt, 1)));
+    int *sums = p->scan_tmp[lvl].as<int>();
+    scan_tile_kernel<<<(unsigned)nt, kScanThreads, 0, st>>>(d, n, d, sums);
+    CKL();
+    p->launches++;
+    if (nt > 1) {
+        RET_IF(scan_excl(p, sums, nt, st, lvl + 1));
+        scan_add_kernel<<<nblk(n, 256), 256, 0, st>>>(d, n, sums);
+        CKL();
+        p->launches++;
+    }
+    return CYLFMM_OK;
+}
+
+// stable radix sort of (key, idx) by the low `bits` bits; returns buffers holding the result
+static cylfmm_status radix_sort(cylfmm_plan p, DevBuf &k1, DevBuf &v1, DevBuf &k2, DevBuf &v2,
+                                int64_t n, int bits, cudaStream_t st, uint32_t **ko, int **vo)
+{
+    int ntiles = (int)((n + kSortTile - 1) / kSortTile);
+    if (n <= 0) {
+        *ko = k1.as<uint32_t>();
+        *vo = v1.as<int>();
+        return CYLFMM_OK;
+    }
+    RET_IF(p->hist.need(sizeof(int) * 256 * (size_t)std::max(ntiles, 1)));
+    uint32_t *ka = k1.as<uint32_t>(), *kb = k2.as<uint32_t>();
+    int *va = v1.as<int>(), *vb = v2.as<int>();
+    for (int sh = 0; sh < bits; sh += 8) {
+        radix_hist_kernel<<<ntiles, kSortThreads, 0, st>>>(ka, n, sh, ntiles, p->hist.as<int>());
+        CKL();
+        RET_IF(scan_excl(p, p->hist.as<int>(), 256LL * ntiles, st));
+        radix_scatter_kernel<<<ntiles, kSortThreads, 0, st>>>(ka, va, n, sh, ntiles,
+                                                              p->hist.as<int>(), kb, vb);
+        CKL();
+        p->launches += 2;
+        std::swap(ka, kb);
+        std::swap(va, vb);
+    }
+    *ko = ka;
+    *vo = va;
+    return CYLFMM_OK;
+}
+
+extern "C" cylfmm_status cylfmm_tree_sort(const double *r, const double *z, int64_t n, int depth,
+                                          double L, double z0, uint32_t *key, int32_t *perm,
+                                          cylfmm_stream_t stream)
+{
+    if (n < 0 || n > INT32_MAX || depth < 1 || depth > CYLFMM_MAX_DEPTH || !(L > 0.0) ||
+        (n > 0 && (!r || !z || !key || !perm))) {
+        set_err("cylfmm_tree_sort: bad arguments");
+        return CYLFMM_EINVAL;
+    }
+    RET_IF(ensure_init());
+    if (n == 0) return CYLFMM_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    cylfmm_plan_s tmp;
+    DevBuf k1, v1, k2, v2;
+    cylfmm_status s = CYLFMM_OK;
+    do {
+        if ((s = k1.need(4 * n)) || (s = v1.need(4 * n)) || (s = k2.need(4 * n)) ||
+            (s = v2.need(4 * n)) || (s = tmp.err.need(4)))
+            break;
+        cudaMemsetAsync(tmp.err.p, 0, 4, st);
+        keys_kernel<<<nblk(n, 256), 256, 0, st>>>(r, z, n, depth, L, z0, k1.as<uint32_t>(),
+                                                  v1.as<int>(), tmp.err.as<int>());
+        cudaMemcpyAsync(key, k1.p, 4 * n, cudaMemcpyDeviceToDevice, st);
+        uint32_t *ko;
+        int *vo;
+        if ((s = radix_sort(&tmp, k1, v1, k2, v2, n, 2 * depth, st, &ko, &vo))) break;
+        cudaMemcpyAsync(perm, vo, 4 * n, cudaMemcpyDeviceToDevice, st);
+        s = check_err_flag(&tmp, st);
+    } while (0);
+    cudaStreamSynchronize(st);
+    k1.release();
+    v1.release();
+    k2.release();
+    v2.release();
+    free_plan_bufs(&tmp);
+    return s;
+}
+
+// ------------------------------------------------------------------------------------------
+// FMM solve
+static int64_t pow4(int l) { return (int64_t)1 << (2 * l); }
+
+template <int NT, int TM, int RM, int RN, int KC>
+static cudaError_t launch_s2l_t(const FarArgs &fa, int level, cudaStream_t st)
+{
+    using Cfg = S2LCfg<NT, TM, RM, RN, KC>;
+    int nb = 1 << level;
+    int half = std::max(nb / 2, 1);
+    int jtiles = (half + Cfg::JT - 1) / Cfg::JT;
+    int KW = fa.m1 - fa.m0;
+    size_t grid = (size_t)nb * 2 * jtiles * KW;
+    size_t sm = s2l_smem_bytes<NT, TM, RM, RN, KC>(fa.p);
+    s2l_kernel<NT, TM, RM, RN, KC><<<(unsigned)grid, NT, sm, st>>>(fa, level, jtiles);
+    return cudaGetLastError();
+}
+static cudaError_t launch_s2l(const FarArgs &fa, int level, cudaStream_t st)
+{
+    if (fa.p <= 8) return launch_s2l_t<S2L_P8>(fa, level, st);
+    if (fa.p <= 12) return launch_s2l_t<S2L_P12>(fa, level, st);
+    if (fa.p <= 16) return launch_s2l_t<S2L_P16>(fa, level, st);
+    return launch_s2l_t<S2L_P20>(fa, level, st);
+}
+
+struct PhaseTimer {
+    cylfmm_plan p;
+    cudaStream_t st;
+    bool on;
+    int k = 0;
+    void mark()
+    {
+        if (on && k < 16) cudaEventRecord(p->ev[k++], st);
+    }
+};
+
+static cylfmm_status build_tree(cylfmm_plan p, const double *r, const double *z, int64_t n,
+                                bool is_src, cudaStream_t st, int **perm_out, uint32_t **key_out)
+{
+    const cylfmm_params &q = p->prm;
+    DevBuf &k1 = is_src ? p->skey : p->fkey, &v1 = is_src ? p->sidx : p->fidx;
+    DevBuf &k2 = is_src ? p->skey2 : p->fkey2, &v2 = is_src ? p->sidx2 : p->fidx2;
+    size_t nb = sizeof(int) * (size_t)std::max<int64_t>(n, 1);
+    RET_IF(k1.need(nb));
+    RET_IF(v1.need(nb));
+    RET_IF(k2.need(nb));
+    RET_IF(v2.need(nb));
+    if (n > 0) {
+        keys_kernel<<<nblk(n, 256), 256, 0, st>>>(r, z, n, q.depth, q.domain_L, q.domain_z0,
+                                                  k1.as<uint32_t>(), v1.as<int>(), p->err.as<int>());
+        CKL();
+        p->launches++;
+    }
+    RET_IF(radix_sort(p, k1, v1, k2, v2, n, 2 * q.depth, st, key_out, perm_out));
+    return CYLFMM_OK;
+}
+
+static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const double *src_z,
+                                    const double *src_S, int64_t ns, const double *fld_r,
+                                    const double *fld_z, int64_t nf, double *out_Phi,
+                                    cudaStream_t st, cylfmm_timings *tm)
+{
+    const cylfmm_params &q = p->prm;
+    const int d = q.depth, K = q.n_modes, pp = q.order, P = (pp + 1) * (pp + 2) / 2;
+    const int KW = q.mode_chunk > 0 ? std::min(q.mode_chunk, K) : K;
+    p->launches = 0;
+    PhaseTimer T{p, st, tm != nullptr};
+    RET_IF(p->err.need(sizeof(int)));
+    RET_IF(p->ctr.need(sizeof(unsigned long long) * 4));
+    CK(cudaMemsetAsync(p->err.p, 0, sizeof(int), st));
+    CK(cudaMemsetAsync(p->ctr.p, 0, sizeof(unsigned long long) * 4, st));
+    T.mark();  // 0
+    if (nf == 0) return CYLFMM_OK;
+    // ---- tree
+    int *sperm = nullptr, *fperm = nullptr;
+    uint32_t *skey_s = nullptr, *fkey_s = nullptr;
+    RET_IF(build_tree(p, src_r, src_z, ns, true, st, &sperm, &skey_s));
+    RET_IF(build_tree(p, fld_r, fld_z, nf, false, st, &fperm, &fkey_s));
+    RET_IF(p->sr_s.need(8 * std::max<int64_t>(ns, 1)));
+    RET_IF(p->sz_s.need(8 * std::max<int64_t>(ns, 1)));
+    RET_IF(p->S_s.need(16 * (size_t)std::max<int64_t>(ns, 1) * K));
+    RET_IF(p->fr_s.need(8 * nf));
+    RET_IF(p->fz_s.need(8 * nf));
+    if (ns > 0) {
+        gather_kernel<double><<<nblk(ns, 256), 256, 0, st>>>(src_r, sperm, ns, p->sr_s.as<double>());
+        gather_kernel<double><<<nblk(ns, 256), 256, 0, st>>>(src_z, sperm, ns, p->sz_s.as<double>());
+        gather_rows_kernel<<<nblk(ns * K, 256), 256, 0, st>>>(
+            reinterpret_cast<const double2 *>(src_S), sperm, ns, K, p->S_s.as<double2>());
+        CKL();
+        p->launches += 3;
+    }
+    gather_kernel<double><<<nblk(nf, 256), 256, 0, st>>>(fld_r, fperm, nf, p->fr_s.as<double>());
+    gather_kernel<double><<<nblk(nf, 256), 256, 0, st>>>(fld_z, fperm, nf, p->fz_s.as<double>());
+    CKL();
+    p->launches += 2;
+    const int64_t nleaf = pow4(d);
+    RET_IF(p->slstart.need(sizeof(int) * (nleaf + 1)));
+    RET_IF(p->flstart.need(sizeof(int) * (nleaf + 1)));
+    leaf_start_kernel<<<nblk(nleaf + 1, 256), 256, 0, st>>>(skey_s, ns, nleaf, p->slstart.as<int>());
+    leaf_start_kernel<<<nblk(nleaf + 1, 256), 256, 0, st>>>(fkey_s, nf, nleaf, p->flstart.as<int>());
+    CKL();
+    p->launches += 2;
+    // level maps
+    int64_t lvoff[kMaxLevels + 1];
+    lvoff[0] = lvoff[1] = lvoff[2] = 0;
+    for (int l = 2; l <= d; ++l) lvoff[l + 1] = lvoff[l] + pow4(l);
+    const int64_t ltot = lvoff[d + 1];
+    RET_IF(p->flags.need(sizeof(int) * ltot));
+    RET_IF(p->smap.need(sizeof(int) * ltot));
+    RET_IF(p->skeys.need(sizeof(int) * ltot));
+    RET_IF(p->tmap.need(sizeof(int) * ltot));
+    RET_IF(p->tkeys.need(sizeof(int) * ltot));
+    RET_IF(p->counts.need(sizeof(int) * 2 * kMaxLevels));
+    for (int side = 0; side < 2; ++side) {
+        const int *ls = side == 0 ? p->slstart.as<int>() : p->flstart.as<int>();
+        int *map = side == 0 ? p->smap.as<int>() : p->tmap.as<int>();
+        int *keys = side == 0 ? p->skeys.as<int>() : p->tkeys.as<int>();
+        for (int l = 2; l <= d; ++l) {
+            int *fl = p->flags.as<int>() + lvoff[l];
+            level_flags_kernel<<<nblk(pow4(l), 256), 256, 0, st>>>(ls, d, l, fl);
+            CKL();
+            RET_IF(scan_excl(p, fl, pow4(l), st));
+            level_map_kernel<<<nblk(pow4(l), 256), 256, 0, st>>>(
+                ls, d, l, fl, map + lvoff[l], keys + lvoff[l], p->counts.as<int>() + side * kMaxLevels + l);
+            CKL();
+            p->launches += 2;
+        }
+    }
+    int hcnt[2 * kMaxLevels] = {0};
+    CK(cudaMemcpyAsync(hcnt, p->counts.p, sizeof(int) * 2 * kMaxLevels, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    RET_IF(check_err_flag(p, st));
+    T.mark();  // 1: tree done
+    // ---- far-field storage
+    FarArgs fa = {};
+    fa.depth = d;
+    fa.p = pp;
+    fa.P = P;
+    fa.K = K;
+    fa.L = q.domain_L;
+    fa.z0 = q.domain_z0;
+    fa.truncation = q.truncation;
+    int64_t stot = 0, ttot = 0;
+    for (int l = 2; l <= d; ++l) {
+        fa.smap[l] = p->smap.as<int>() + lvoff[l];
+        fa.skeys[l] = p->skeys.as<int>() + lvoff[l];
+        fa.tmap[l] = p->tmap.as<int>() + lvoff[l];
+        fa.tkeys[l] = p->tkeys.as<int>() + lvoff[l];
+        fa.scount[l] = ns > 0 ? hcnt[l] : 0;
+        fa.tcount[l] = hcnt[kMaxLevels + l];
+        fa.soff[l] = stot;
+        fa.toff[l] = ttot;
+        stot += fa.scount[l];
+        ttot += fa.tcount[l];
+    }
+    const int64_t TP = (int64_t)(pp + 1) * (pp + 1) * (pp + 1);
+    const int64_t nstat = (int64_t)12 << d;
+    const int NM = std::max(K - 1, 1) + 1, D = 2 * pp + 1;
+    RET_IF(p->M.need(sizeof(double2) * (size_t)std::max<int64_t>(stot, 1) * KW * P));
+    RET_IF(p->Lc.need(sizeof(double2) * (size_t)std::max<int64_t>(ttot, 1) * KW * P));
+    RET_IF(p->tens.need(sizeof(double) * (size_t)nstat * KW * TP));
+    RET_IF(p->seeds.need(sizeof(double) * (size_t)nstat * 4 * NM * D));
+    fa.M = p->M.as<double2>();
+    fa.Lc = p->Lc.as<double2>();
+    fa.tens = p->tens.as<double>();
+    fa.slstart = p->slstart.as<int>();
+    fa.flstart = p->flstart.as<int>();
+    fa.sr = p->sr_s.as<double>();
+    fa.sz = p->sz_s.as<double>();
+    fa.S = p->S_s.as<double2>();
+    fa.fr = p->fr_s.as<double>();
+    fa.fz = p->fz_s.as<double>();
+    fa.fperm = fperm;
+    fa.out = reinterpret_cast<double2 *>(out_Phi);
+    fa.s2l_pairs = p->ctr.as<unsigned long long>() + 2;
+    double ms_tensor = 0, ms_p2m = 0, ms_m2m = 0, ms_s2l = 0, ms_l2l = 0, ms_l2p = 0;
+    cudaEvent_t e0 = p->ev[10], e1 = p->ev[11];
+    auto tic = [&]() { if (tm) cudaEventRecord(e0, st); };
+    auto toc = [&](double &acc) {
+        if (tm) {
+            cudaEventRecord(e1, st);
+            cudaEventSynchronize(e1);
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e0, e1);
+            acc += ms;
+        }
+    };
+    for (int m0 = 0; m0 < K; m0 += KW) {
+        fa.m0 = m0;
+        fa.m1 = std::min(K, m0 + KW);
+        const int kw = fa.m1 - fa.m0;
+        // tensors for the normalised stations (shared by all levels)
+        tic();
+        {
+            TensorGeomArgs ta = {};
+            ta.station_mode = 1;
+            ta.n = nstat;
+            ta.K = K;
+            ta.m0 = fa.m0;
+            ta.m1 = fa.m1;
+            ta.p = pp;
+            ta.miller = q.miller;
+            ta.fwd2 = forward_coef(std::max(K - 1, 1), q.miller);
+            ta.seeds = p->seeds.as<double>();
+            ta.out = p->tens.as<double>();
+            ta.packed = 1;
+            ta.err = p->err.as<int>();
+            RET_IF(run_tensors(ta, nstat, st));
+            p->launches += 2;
+        }
+        toc(ms_tensor);
+        if (ns > 0) {
+            tic();
+            if (fa.scount[d] > 0) {
+                size_t sm = sizeof(double) * kP2MChunk * P + sizeof(double2) * kP2MChunk * kw;
+                p2m_kernel<<<fa.scount[d], kP2MThreads, sm, st>>>(fa);
+                CKL();
+                p->launches++;
+            }
+            toc(ms_p2m);
+            tic();
+            for (int l = d - 1; l >= 2; --l) {
+                if (fa.scount[l] == 0) continue;
+                size_t sm = sizeof(double2) * 4 * P + sizeof(double) * (pp + 1) * (pp + 1);
+                m2m_kernel<<<(unsigned)((int64_t)fa.scount[l] * kw), 256, sm, st>>>(fa, l);
+                CKL();
+                p->launches++;
+            }
+            toc(ms_m2m);
+        }
+        for (int l = 2; l <= d; ++l) {
+            if (fa.tcount[l] == 0) continue;
+            tic();
+            if (l == 2) {
+                CK(cudaMemsetAsync(fa.Lc + fa.toff[2] * kw * P, 0,
+                                   sizeof(double2) * (size_t)fa.tcount[2] * kw * P, st));
+            } else {
+                size_t sm = sizeof(double2) * P + sizeof(double) * (pp + 1) * (pp + 1);
+                l2l_kernel<<<(unsigned)((int64_t)fa.tcount[l] * kw), 256, sm, st>>>(fa, l);
+                CKL();
+                p->launches++;
+            }
+            toc(ms_l2l);
+            if (ns > 0 && fa.scount[l] > 0) {
+                tic();
+                CK(launch_s2l(fa, l, st));
+                p->launches++;
+                toc(ms_s2l);
+            }
+        }
+        tic();
+        {
+            int ngrp = (kw + kL2PModes - 1) / kL2PModes;
+            size_t sm = sizeof(double2) * kL2PModes * P + sizeof(double) * kL2PPts * P;
+            l2p_kernel<<<(unsigned)((int64_t)fa.tcount[d] * ngrp), 256, sm, st>>>(fa);
+            CKL();
+            p->launches++;
+        }
+        toc(ms_l2p);
+    }
+    // ---- near field
+    tic();
+    double ms_p2p = 0;
+    if (ns > 0) {
+        const int ntl = fa.tcount[d];
+        double avg = (double)nf / std::max(ntl, 1);
+        const int TT = avg <= 10.0 ? 8 : (avg <= 24.0 ? 16 : 32);
+        RET_IF(p->tcnt.need(sizeof(int) * (ntl + 1)));
+        RET_IF(p->ntasks.need(sizeof(int)));
+        int64_t maxtasks = nf / TT + ntl + 1;
+        RET_IF(p->tasks.need(sizeof(int4) * maxtasks));
+        near_tasks_count_kernel<<<nblk(ntl, 256), 256, 0, st>>>(fa.tkeys[d], ntl, fa.flstart, TT,
+                                                               p->tcnt.as<int>());
+        CKL();
+        RET_IF(scan_excl(p, p->tcnt.as<int>(), ntl, st));
+        near_tasks_emit_kernel<<<nblk(ntl, 256), 256, 0, st>>>(fa.tkeys[d], ntl, fa.flstart, TT,
+                                                              p->tcnt.as<int>(), p->tasks.as<int4>(),
+                                                              p->ntasks.as<int>());
+        CKL();
+        p->launches += 2;
+        unsigned long long *ctr = p->ctr.as<unsigned long long>();
+        for (int m0 = 0; m0 < K; m0 += kP2PWindow) {
+            P2PArgs a = {};
+            a.sr = fa.sr;
+            a.sz = fa.sz;
+            a.S = fa.S;
+            a.fr = fa.fr;
+            a.fz = fa.fz;
+            a.ns = ns;
+            a.nf = nf;
+            a.K = K;
+            a.m0 = m0;
+            a.m1 = std::min(K, m0 + kP2PWindow);
+            a.miller = q.miller;
+            a.fwd2 = forward_coef(K - 1, q.miller);
+            a.exclude = q.exclude_coincident;
+            a.out = fa.out;
+            a.out_row = fperm;
+            a.accumulate = 1;
+            a.tasks = p->tasks.as<int4>();
+            a.ntasks = p->ntasks.as<int>();
+            a.leafstart = fa.slstart;
+            a.depth = d;
+            a.n_skipped = ctr + 0;
+            a.n_pairs = ctr + 1;
+            a.err_flag = p->err.as<int>();
+            CK(launch_p2p<true>(TT, a, dim3((unsigned)maxtasks), st));
+            p->launches++;
+        }
+    }
+    toc(ms_p2p);
+    T.mark();
+    if (tm) {
+        unsigned long long c[4] = {0, 0, 0, 0};
+        CK(cudaMemcpyAsync(c, p->ctr.p, sizeof(c), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        float ms_tree = 0, ms_total = 0;
+        cudaEventElapsedTime(&ms_tree, p->ev[0], p->ev[1]);
+        cudaEventElapsedTime(&ms_total, p->ev[0], p->ev[2]);
+        tm->ms_tree = ms_tree;
+        tm->ms_p2m = ms_p2m;
+        tm->ms_m2m = ms_m2m;
+        tm->ms_tensor = ms_tensor;
+        tm->ms_s2l = ms_s2l;
+        tm->ms_l2l = ms_l2l;
+        tm->ms_l2p = ms_l2p;
+        tm->ms_p2p = ms_p2p;
+        tm->ms_total = ms_total;
+        tm->n_skipped = (int64_t)c[0];
+        tm->n_near_pairs = (int64_t)c[1];
+        tm->n_s2l_pairs = (int64_t)c[2];
+        tm->kernel_launches = p->launches;
+        RET_IF(check_err_flag(p, st));
+    }
+    return CYLFMM_OK;
+}
+
+static cylfmm_status validate_solve(cylfmm_plan plan, const double *sr, const double *sz,
+                                    const double *S, int64_t ns, const double *fr, const double *fz,
+                                    int64_t nf, const double *out)
+{
+    if (!plan) {
+        set_err("cylfmm_fmm_solve: null plan");
+        return CYLFMM_EINVAL;
+    }
+    if (ns < 0 || nf < 0 || ns > INT32_MAX || nf > INT32_MAX ||
+        (ns > 0 && (!sr || !sz || !S)) || (nf > 0 && (!fr || !fz || !out))) {
+        set_err("cylfmm_fmm_solve: bad sizes or null pointer");
+        return CYLFMM_EINVAL;
+    }
+    return CYLFMM_OK;
+}
+
+extern "C" cylfmm_status cylfmm_fmm_solve(cylfmm_plan plan, const double *src_r,
+                                          const double *src_z, const double *src_S, int64_t n_src,
+                                          const double *fld_r, const double *fld_z, int64_t n_fld,
+                                          double *out_Phi, cylfmm_stream_t stream,
+                                          cylfmm_timings *timings)
+{
+    RET_IF(validate_solve(plan, src_r, src_z, src_S, n_src, fld_r, fld_z, n_fld, out_Phi));
+    CK(cudaSetDevice(plan->device));
+    return fmm_solve_impl(plan, src_r, src_z, src_S, n_src, fld_r, fld_z, n_fld, out_Phi,
+                          (cudaStream_t)stream, timings);
+}
+
+extern "C" cylfmm_status cylfmm_fmm_solve_host(cylfmm_plan plan, const double *src_r,
+                                               const double *src_z, const double *src_S,
+                                               int64_t n_src, const double *fld_r,
+                                               const double *fld_z, int64_t n_fld,
+                                               double *out_Phi, cylfmm_stream_t stream,
+                                               cylfmm_timings *timings)
+{
+    RET_IF(validate_solve(plan, src_r, src_z, src_S, n_src, fld_r, fld_z, n_fld, out_Phi));
+    CK(cudaSetDevice(plan->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const int K = plan->prm.n_modes;
+    size_t bs = 8 * (size_t)std::max<int64_t>(n_src, 1), bf = 8 * (size_t)std::max<int64_t>(n_fld, 1);
+    RET_IF(plan->h_sr.need(bs));
+    RET_IF(plan->h_sz.need(bs));
+    RET_IF(plan->h_S.need(bs * 2 * K));
+    RET_IF(plan->h_fr.need(bf));
+    RET_IF(plan->h_fz.need(bf));
+    RET_IF(plan->h_out.need(bf * 2 * K));
+    if (n_src > 0) {
+        CK(cudaMemcpyAsync(plan->h_sr.p, src_r, 8 * n_src, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(plan->h_sz.p, src_z, 8 * n_src, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(plan->h_S.p, src_S, 16 * (size_t)n_src * K, cudaMemcpyHostToDevice, st));
+    }
+    if (n_fld > 0) {
+        CK(cudaMemcpyAsync(plan->h_fr.p, fld_r, 8 * n_fld, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(plan->h_fz.p, fld_z, 8 * n_fld, cudaMemcpyHostToDevice, st));
+    }
+    RET_IF(fmm_solve_impl(plan, plan->h_sr.as<double>(), plan->h_sz.as<double>(),
+                          plan->h_S.as<double>(), n_src, plan->h_fr.as<double>(),
+                          plan->h_fz.as<double>(), n_fld, plan->h_out.as<double>(), st, timings));
+    if (n_fld > 0)
+        CK(cudaMemcpyAsync(out_Phi, plan->h_out.p, 16 * (size_t)n_fld * K, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return check_err_flag(plan, st);
+}

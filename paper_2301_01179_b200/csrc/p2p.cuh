@@ -1,0 +1,327 @@
+// p2p.cuh -- pairwise modal sums Phi_t^(n) += sum_s S_s^(n) G^(n)(r_t, r_s, z_t - z_s)
+// (P:195-201): the direct sum (C1) and the FMM near field over the 9 neighbour leaves
+// (P:647-651).  This is the paper's bottleneck.
+//
+// CTA design (sm_100a, FP64 CUDA cores; no tensor cores: special-function arithmetic):
+//   a CTA owns a tile of TT target points and streams its source list through shared memory in
+//   chunks of SC sources.  Per chunk, the NT = TT*SC pairs are
+//     1. classified (forward chi < 1.008 / Miller / skipped) and compacted with warp ballots so
+//        that each warp runs one branch (warp-uniform loops, uniform constant-bank reads);
+//     2. evaluated one pair per thread: G^(n) for the mode window [m0, m1) written to smem;
+//     3. contracted with lane = (target, mode): acc(t, n) += S_s^(n) G_ts^(n) over the chunk,
+//        with the accumulators distributed over the CTA (register use independent of K).
+//   Summation order is fixed (source list order, chunk by chunk): results are bitwise
+//   reproducible and independent of the compaction.
+#pragma once
+#include "specfun.cuh"
+
+namespace cyl {
+
+struct P2PArgs {
+    const double *sr, *sz;      // sources (sorted order for the near field)
+    const double2 *S;           // [ns][K] complex
+    const double *fr, *fz;      // targets (sorted order for the near field)
+    int64_t ns, nf;
+    int K;                      // total modes (N = K - 1 sets the Miller start)
+    int m0, m1;                 // mode window
+    int miller;                 // 0 accurate, 1 paper
+    double fwd2;                // forward switch 2 t_N (R#3)
+    int exclude;                // skip coincident pairs
+    // output
+    double2 *out;               // rows [*][K]
+    const int *out_row;         // target t -> output row (nullptr: row = t)
+    int accumulate;             // load initial value from out
+    int64_t part_stride;        // direct: out += blockIdx.y * part_stride (complex elements)
+    // direct mode: sources [y * src_per_part, ...) ; near mode: tasks
+    int64_t src_per_part;
+    const int4 *tasks;          // near: {t0, t1, leafkey, 0}
+    const int *ntasks;          // near: device count
+    const int *leafstart;       // near: dense source leaf starts [4^d + 1]
+    int depth;
+    unsigned long long *n_skipped;
+    unsigned long long *n_pairs;
+    int *err_flag;
+};
+
+__device__ __forceinline__ uint32_t morton2(uint32_t ix, uint32_t iz)
+{
+    auto spread = [](uint32_t v) {
+        v &= 0xffffu;
+        v = (v | (v << 8)) & 0x00ff00ffu;
+        v = (v | (v << 4)) & 0x0f0f0f0fu;
+        v = (v | (v << 2)) & 0x33333333u;
+        v = (v | (v << 1)) & 0x55555555u;
+        return v;
+    };
+    return spread(ix) | (spread(iz) << 1);
+}
+__device__ __forceinline__ uint32_t compact1(uint32_t v)
+{
+    v &= 0x55555555u;
+    v = (v | (v >> 1)) & 0x33333333u;
+    v = (v | (v >> 2)) & 0x0f0f0f0fu;
+    v = (v | (v >> 4)) & 0x00ff00ffu;
+    v = (v | (v >> 8)) & 0x0000ffffu;
+    return v;
+}
+
+template <int TT, int SC, int MAXT, bool NEAR>
+__global__ void __launch_bounds__(TT *SC) p2p_kernel(P2PArgs a)
+{
+    constexpr int NT = TT * SC;
+    constexpr int NW = NT / 32;
+    const int KW = a.m1 - a.m0;
+    extern __shared__ double smem[];
+    double *Gs = smem;                                  // [KW][TT][SC]
+    double2 *Ss = reinterpret_cast<double2 *>(Gs + (size_t)KW * NT);  // [SC][KW]
+    double *src_r = reinterpret_cast<double *>(Ss + (size_t)SC * KW);
+    double *src_z = src_r + SC;
+    double *tg_r = src_z + SC;
+    double *tg_z = tg_r + TT;
+    int *sidx = reinterpret_cast<int *>(tg_z + TT);     // [SC]
+    int *order = sidx + SC;                             // [NT]
+    int *wcnt = order + NT;                             // [2 NW]
+    int *seg = wcnt + 2 * NW;                           // [9][2] + prefix [10]
+    int *segpre = seg + 18;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int t0, nt, nseg;
+    if (NEAR) {
+        if ((int)blockIdx.x >= *a.ntasks) return;
+        int4 tk = a.tasks[blockIdx.x];
+        t0 = tk.x;
+        nt = tk.y - tk.x;
+        if (tid == 0) {
+            uint32_t key = (uint32_t)tk.z;
+            int ix = (int)compact1(key), iz = (int)compact1(key >> 1);
+            int nb = 1 << a.depth, k = 0, acc = 0;
+            for (int da = -1; da <= 1; ++da)
+                for (int dc = -1; dc <= 1; ++dc) {
+                    int x = ix + da, z = iz + dc;
+                    if (x < 0 || z < 0 || x >= nb || z >= nb) continue;
+                    uint32_t m = morton2((uint32_t)x, (uint32_t)z);
+                    int s0 = a.leafstart[m], s1 = a.leafstart[m + 1];
+                    if (s1 <= s0) continue;
+                    seg[2 * k] = s0;
+                    seg[2 * k + 1] = s1;
+                    segpre[k] = acc;
+                    acc += s1 - s0;
+                    ++k;
+                }
+            segpre[k] = acc;
+            wcnt[0] = k;  // temp
+        }
+        __syncthreads();
+        nseg = wcnt[0];
+        __syncthreads();
+    } else {
+        t0 = blockIdx.x * TT;
+        nt = (int)min((int64_t)TT, a.nf - t0);
+        if (tid == 0) {
+            int64_t s0 = (int64_t)blockIdx.y * a.src_per_part;
+            int64_t s1 = min(a.ns, s0 + a.src_per_part);
+            seg[0] = (int)s0;
+            seg[1] = (int)max(s0, s1);
+            segpre[0] = 0;
+            segpre[1] = seg[1] - seg[0];
+        }
+        nseg = 1;
+    }
+    if (tid < TT) {
+        int t = t0 + min(tid, nt - 1);
+        tg_r[tid] = a.fr[t];
+        tg_z[tid] = a.fz[t];
+    }
+    __syncthreads();
+    const int total = segpre[nseg];
+    double2 *out = a.out + (NEAR ? 0 : (int64_t)blockIdx.y * a.part_stride);
+
+    double2 acc[MAXT];
+#pragma unroll
+    for (int k = 0; k < MAXT; ++k) {
+        acc[k] = make_double2(0.0, 0.0);
+        int id = tid + k * NT;
+        if (a.accumulate && id < TT * KW) {
+            int t = id % TT, n = id / TT;
+            if (t < nt) {
+                int64_t row = a.out_row ? a.out_row[t0 + t] : (t0 + t);
+                acc[k] = out[row * a.K + a.m0 + n];
+            }
+        }
+    }
+    unsigned long long my_skipped = 0, my_pairs = 0;
+    const int Nglob = a.K - 1;
+
+    for (int v0 = 0; v0 < total; v0 += SC) {
+        __syncthreads();
+        if (tid < SC) {
+            int v = v0 + tid, gi = -1;
+            if (v < total) {
+                int k = 0;
+                while (k + 1 < nseg && v >= segpre[k + 1]) ++k;
+                gi = seg[2 * k] + (v - segpre[k]);
+                src_r[tid] = a.sr[gi];
+                src_z[tid] = a.sz[gi];
+            }
+            sidx[tid] = gi;
+        }
+        __syncthreads();
+        for (int e = tid; e < SC * KW; e += NT) {
+            int s = e / KW, n = e - s * KW;
+            int gi = sidx[s];
+            Ss[e] = gi >= 0 ? a.S[(int64_t)gi * a.K + a.m0 + n] : make_double2(0.0, 0.0);
+        }
+        // classify pair slot p = tid (t = p % TT, s = p / TT)
+        int cls;
+        {
+            int t = tid % TT, s = tid / TT;
+            bool valid = t < nt && sidx[s] >= 0;
+            cls = 2;
+            if (valid) {
+                double r = tg_r[t], r1 = src_r[s];
+                double z = tg_z[t], z1 = src_z[s];
+                if (r == r1 && z == z1) {
+                    if (a.exclude) ++my_skipped;
+                    else atomicOr(a.err_flag, 1);
+                } else {
+                    PairGeo g = pair_geo(r, r1, z - z1, a.fwd2);
+                    cls = g.forward ? 0 : 1;
+                    ++my_pairs;
+                }
+            }
+        }
+        unsigned bF = __ballot_sync(0xffffffffu, cls == 0);
+        unsigned bM = __ballot_sync(0xffffffffu, cls == 1);
+        if (lane == 0) {
+            wcnt[warp] = __popc(bF);
+            wcnt[NW + warp] = __popc(bM);
+        }
+        __syncthreads();
+        {
+            int preF = 0, preM = 0, totF = 0, totM = 0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                int cF = wcnt[w], cM = wcnt[NW + w];
+                if (w < warp) {
+                    preF += cF;
+                    preM += cM;
+                }
+                totF += cF;
+                totM += cM;
+            }
+            unsigned lt = (1u << lane) - 1u;
+            int bf = __popc(bF & lt), bm = __popc(bM & lt);
+            int pos;
+            if (cls == 0) pos = preF + bf;
+            else if (cls == 1) pos = totF + preM + bm;
+            else pos = totF + totM + (warp * 32 - preF - preM) + (lane - bf - bm);
+            order[pos] = tid | (cls << 16);
+        }
+        __syncthreads();
+        {
+            int my = order[tid];
+            int p = my & 0xffff, c = my >> 16;
+            int t = p % TT, s = p / TT;
+            double *g = Gs + t * SC + s;
+            bool miller = (c == 1);
+            int S_lane = 0;
+            PairGeo geo;
+            if (c != 2) {
+                geo = pair_geo(tg_r[t], src_r[s], tg_z[t] - src_z[s], a.fwd2);
+                if (miller) S_lane = Nglob + miller_extra(geo, a.miller);
+            }
+            int S_warp = __reduce_max_sync(0xffffffffu, S_lane);
+            if (c == 2) {
+                for (int n = 0; n < KW; ++n) g[n * NT] = 0.0;
+            } else {
+                greens_pair(geo, a.m0, a.m1, S_warp, g, NT);
+            }
+        }
+        __syncthreads();
+        // contraction: lane = (t, n)
+#pragma unroll
+        for (int k = 0; k < MAXT; ++k) {
+            int id = tid + k * NT;
+            if (id < TT * KW) {
+                int t = id % TT, n = id / TT;
+                const double *g = Gs + (n * TT + t) * SC;
+                double2 sum = acc[k];
+#pragma unroll
+                for (int s = 0; s < SC; ++s) {
+                    double2 sv = Ss[s * KW + n];
+                    sum.x = fma(sv.x, g[s], sum.x);
+                    sum.y = fma(sv.y, g[s], sum.y);
+                }
+                acc[k] = sum;
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < MAXT; ++k) {
+        int id = tid + k * NT;
+        if (id < TT * KW) {
+            int t = id % TT, n = id / TT;
+            if (t < nt) {
+                int64_t row = a.out_row ? a.out_row[t0 + t] : (t0 + t);
+                out[row * a.K + a.m0 + n] = acc[k];
+            }
+        }
+    }
+    // counters (integers: deterministic)
+    my_skipped = __reduce_add_sync(0xffffffffu, (unsigned)my_skipped);
+    my_pairs = __reduce_add_sync(0xffffffffu, (unsigned)my_pairs);
+    if (lane == 0 && a.n_skipped && my_skipped && a.m0 == 0) atomicAdd(a.n_skipped, my_skipped);
+    if (lane == 0 && a.n_pairs && my_pairs && a.m0 == 0) atomicAdd(a.n_pairs, my_pairs);
+}
+
+template <int TT, int SC>
+inline size_t p2p_smem_bytes(int KW)
+{
+    constexpr int NT = TT * SC;
+    return sizeof(double) * ((size_t)KW * NT + 2 * (size_t)SC * KW + 2 * SC + 2 * TT) +
+           sizeof(int) * (SC + NT + 2 * (NT / 32) + 18 + 10);
+}
+
+// Deterministic reduction of direct-sum partial results: out[t][n] = sum_part ws[part][t][n].
+__global__ void reduce_parts_kernel(const double2 *ws, int64_t nelem, int nparts, double2 *out)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nelem) return;
+    double2 s = ws[i];
+    for (int p = 1; p < nparts; ++p) {
+        double2 v = ws[(int64_t)p * nelem + i];
+        s.x += v.x;
+        s.y += v.y;
+    }
+    out[i] = s;
+}
+
+// Test entry kernel: one thread per (r, r1, x) triple, all modes to global memory.
+__global__ void greens_batch_kernel(const double *r, const double *r1, const double *x,
+                                    int64_t n, int K, int miller, double fwd2, double *out,
+                                    int *err)
+{
+    int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool ok = q < n;
+    PairGeo g;
+    int S_lane = 0;
+    if (ok) {
+        double rr = r[q], rr1 = r1[q];
+        if (!(rr > 0.0) || !(rr1 > 0.0)) {
+            atomicOr(err, 2);
+            ok = false;
+        } else {
+            g = pair_geo(rr, rr1, x[q], fwd2);
+            if (g.coincident) {
+                atomicOr(err, 1);
+                ok = false;
+            } else if (!g.forward) {
+                S_lane = (K - 1) + miller_extra(g, miller);
+            }
+        }
+    }
+    int S_warp = __reduce_max_sync(0xffffffffu, S_lane);
+    if (ok) greens_pair(g, 0, K, S_warp, out + q * K, 1);
+}
+
+}  // namespace cyl

@@ -1,0 +1,192 @@
+// specfun.cuh -- device FP64 modal ring Green's function G^(n) = Q_{n-1/2}(chi)/(2 pi sqrt(r r1))
+// for n = 0..N, written for sm_100a.  Product code: shares nothing with oracle/.
+//
+// Method (the paper's, App. A), re-arranged for the GPU:
+//  * K, E of modulus k = mu (R#1) from the complementary modulus k' = rho_- / rho_+ (R#2) by the
+//    arithmetic-geometric mean (the oracle uses Carlson's R_F/R_D instead: independent code):
+//      K = pi / (2 AGM(1, k')),  E = K (1 - sum_{m>=0} 2^{m-1} c_m^2),  c_0^2 = k^2 = 4 r r1/rho_+^2.
+//    With mu/(2 pi sqrt(r r1)) = 1/(pi rho_+):  G^(0) = 1/(2 a_inf rho_+),
+//    G^(1) = G^(0) ((1+chi) s - 1)   (from Q_{1/2} = chi mu K - (1+chi) mu E).
+//  * chi - 1 < t_N (tested as rho_-^2 < 2 t_N r r1; the paper's t = 0.008 for N <= 16 and in the
+//    paper mode, narrowed for larger N so the forward rounding growth lambda^2N <= 2^6, R#3):
+//    forward three-term recursion
+//    (2n-1) G_n = 4(n-1) chi G_{n-1} - (2n-3) G_{n-2}, run on u_n = G_n / R_n with
+//    R_n = prod_{k<=n} 4(k-1)/(2k-1): u_n = chi u_{n-1} - eps_n u_{n-2} (one DMUL + one DFMA).
+//  * chi >= 1.008: Miller's backward recursion from seeds (0, 1) at (S, S-1), run on
+//    the rescaled minimal solution y_n = Q~_n (2 chi)^n, which changes by at most a factor 2 per
+//    step (no overflow for any chi, unlike Q~_n itself, R#5), and w_n = y_n / P_n with
+//    P_{n-2} = alpha_n P_{n-1}: w_{n-2} = w_{n-1} - delta_n q w_n, q = 1/(4 chi^2).  Then
+//    G_n = G_0 * (w_n P_n (2 chi)^-n) / w_0.  Start index: paper mode S = N + 80; accurate mode
+//    S = N + ceil(20 / ln lambda) + 4, lambda = chi + sqrt(chi^2 - 1) (contamination
+//    lambda^{-2(S-n)} < e^-40), taken as the max over the Miller lanes of a warp so the loop is
+//    warp-uniform and the coefficient tables are read by uniform index.  Long recurrences
+//    (chi -> 1) are renormalised by a power of two every 64 steps (exact; y_n shrinks by at
+//    most 2 per step).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace cyl {
+
+constexpr int kMaxModes = 256;   // CYLFMM_MAX_MODES
+constexpr int kMaxSteps = 4096;  // Miller start index bound
+constexpr double kPi = 3.141592653589793238462643383279502884;
+
+struct RecTables {
+    double delta[kMaxSteps + 2];   // Miller: delta_n = beta_n / (alpha_n alpha_{n+1}), n >= 2
+    double Pn[kMaxModes + 2];      // Miller: P_n
+    double eps[kMaxModes + 2];     // forward: eps_n = b_n R_{n-2} / R_n, n >= 2
+    double Rn[kMaxModes + 2];      // forward: R_n
+};
+__constant__ RecTables c_rec;
+
+// Host-side construction of the recursion constants (exact rationals rounded once).
+inline void build_rec_tables(RecTables *t)
+{
+    auto alpha = [](int n) { return 2.0 * (n - 1) / (2.0 * n - 3.0); };  // n >= 2
+    auto beta = [](int n) { return (2.0 * n - 1.0) / (2.0 * n - 3.0); };
+    for (int n = 0; n < kMaxSteps + 2; ++n)
+        t->delta[n] = n >= 2 ? beta(n) / (alpha(n) * alpha(n + 1)) : 0.0;
+    t->Pn[0] = 1.0;
+    for (int m = 0; m + 1 < kMaxModes + 2; ++m) t->Pn[m + 1] = t->Pn[m] / alpha(m + 2);
+    auto a = [](int n) { return 4.0 * (n - 1) / (2.0 * n - 1.0); };       // n >= 2
+    auto b = [](int n) { return (2.0 * n - 3.0) / (2.0 * n - 1.0); };
+    t->Rn[0] = 1.0;
+    t->Rn[1] = 1.0;
+    for (int n = 2; n < kMaxModes + 2; ++n) t->Rn[n] = a(n) * t->Rn[n - 1];
+    t->eps[0] = t->eps[1] = 0.0;
+    for (int n = 2; n < kMaxModes + 2; ++n) t->eps[n] = b(n) * t->Rn[n - 2] / t->Rn[n];
+}
+
+// Pair geometry shared by both branches.
+struct PairGeo {
+    double rp2, rm2;   // rho_+^2, rho_-^2
+    double rr1;        // r * r1
+    bool forward;      // chi < 1.008
+    bool coincident;   // rho_-^2 == 0 (bitwise-equal rings)
+};
+
+// Host: the 2 t_N of the forward/backward switch (R#3), see the header comment.
+inline double forward_coef(int nmax, int miller)
+{
+    double t = 0.008;
+    if (miller != 1 && nmax > 0) {
+        double c = cosh(log(64.0) / (2.0 * nmax)) - 1.0;
+        if (c < t) t = c;
+    }
+    return 2.0 * t;
+}
+
+__device__ __forceinline__ PairGeo pair_geo(double r, double r1, double x, double fwd2)
+{
+    PairGeo g;
+    double dp = r + r1, dm = r - r1;
+    g.rp2 = fma(dp, dp, x * x);
+    g.rm2 = fma(dm, dm, x * x);
+    g.rr1 = r * r1;
+    g.forward = g.rm2 < fwd2 * g.rr1;    // chi - 1 < t_N, tie goes backward (R#3)
+    g.coincident = !(g.rm2 > 0.0);
+    return g;
+}
+
+// Accurate-mode Miller start offset e(chi) (evaluated in FP32 with a margin: it only has to be
+// large enough).  chi - 1 = rho_-^2 / (2 r r1).
+__device__ __forceinline__ int miller_extra(const PairGeo &g, int miller_mode)
+{
+    if (miller_mode == 1) return 80;
+    float cm1 = (float)(g.rm2 / (2.0 * g.rr1));
+    float lam_m1 = cm1 + sqrtf(cm1 * (cm1 + 2.0f));     // lambda - 1
+    float lnl = log1pf(lam_m1);
+    int e = (int)ceilf(20.0f / lnl) + 4;
+    return min(e, kMaxSteps - kMaxModes - 4);
+}
+
+// AGM(1, k') with the E sum.  Returns a_inf; s = sum_{m>=0} 2^{m-1} c_m^2 when need_e.
+__device__ __forceinline__ double agm(double kp, double k2, bool need_e, double &s)
+{
+    double a = 1.0, b = kp, pw = 0.5;
+    s = 0.5 * k2;
+#pragma unroll 1
+    for (int it = 0; it < 40; ++it) {
+        double c = 0.5 * (a - b);
+        if (!(fabs(c) > 2.0e-16 * a)) break;
+        double an = 0.5 * (a + b);
+        b = sqrt(a * b);
+        a = an;
+        if (need_e) {
+            pw *= 2.0;
+            s = fma(pw * c, c, s);
+        }
+    }
+    return a;
+}
+
+// G^(n)(r, r1, x) for n = 0..m1-1, stored to out[(n - m0) * ostride] for n in [m0, m1).
+// S_warp: Miller start index (only used on the backward branch; must be > m1 and >= 2).
+// The pair must not be coincident.  Out may point to shared or global memory.
+__device__ __forceinline__ void greens_pair(const PairGeo &g, int m0, int m1, int S_warp,
+                                            double *out, int ostride)
+{
+    double rho_p = sqrt(g.rp2);
+    double inv_rho_p = 1.0 / rho_p;
+    double kp = sqrt(g.rm2) * inv_rho_p;                   // k'
+    double k2 = 4.0 * g.rr1 * inv_rho_p * inv_rho_p;       // k^2 = 1 - k'^2 (no cancellation)
+    double s;
+    double a = agm(kp, k2, g.forward, s);
+    double G0 = 0.5 * inv_rho_p / a;                        // K / (pi rho_+)
+    double sum2 = 0.5 * (g.rp2 + g.rm2);                    // r^2 + r1^2 + x^2 = 2 chi r r1
+    if (g.forward) {
+        double chi = 0.5 * sum2 / g.rr1;
+        double u0 = G0, u1 = G0 * fma(1.0 + chi, s, -1.0);  // G^(1)
+        if (m0 == 0 && m1 > 0) out[0] = u0;
+        if (m0 <= 1 && m1 > 1) out[(1 - m0) * ostride] = u1;
+#pragma unroll 4
+        for (int n = 2; n < m1; ++n) {
+            double u2 = fma(chi, u1, -c_rec.eps[n] * u0);
+            if (n >= m0) out[(n - m0) * ostride] = u2 * c_rec.Rn[n];
+            u0 = u1;
+            u1 = u2;
+        }
+        return;
+    }
+    // Miller, on w_n (see header).  wn = w_n, wl = w_{n-1}; step produces w_{n-2}.
+    double inv2chi = g.rr1 / sum2;
+    double q = inv2chi * inv2chi;
+    double wn = 0.0, wl = 1.0;
+    int n = S_warp;
+    // phase A: indices S-2 .. m1 (no store), renormalised every 64 steps
+    while (n > m1 + 1) {
+        const int nstop = max(m1 + 1, n - 64);
+#pragma unroll 4
+        for (; n > nstop; --n) {
+            double w = fma(-c_rec.delta[n] * q, wn, wl);
+            wn = wl;
+            wl = w;
+        }
+        int ex;
+        frexp(wl, &ex);
+        wn = ldexp(wn, -ex);
+        wl = ldexp(wl, -ex);
+    }
+    // here wl = w_{n-1} with n-1 = m1-1 (or the seed if S-1 == m1-1); store window values
+    if (n - 1 >= m0 && n - 1 < m1) out[(n - 1 - m0) * ostride] = wl;
+#pragma unroll 4
+    for (; n >= 2; --n) {
+        double w = fma(-c_rec.delta[n] * q, wn, wl);
+        wn = wl;
+        wl = w;
+        if (n - 2 >= m0) out[(n - 2 - m0) * ostride] = w;
+    }
+    // wl = w_0.  Normalise and apply P_n (2 chi)^-n upward (v underflows to 0 correctly).
+    double c = G0 / wl;
+    double v = 1.0;
+    for (int k = 0; k < m1; ++k) {
+        if (k >= m0) {
+            double *o = out + (k - m0) * ostride;
+            *o = (*o) * c_rec.Pn[k] * c * v;
+        }
+        v *= inv2chi;
+    }
+}
+
+}  // namespace cyl

@@ -1,0 +1,298 @@
+// tensor.cuh -- the Green-derivative tensor Gbar^n_{abc} = 1/(a!b!c!) d^{a+b+c}G^(n)/dr^a dr1^b dx^c
+// at a geometry (r, r1, x), for a, b <= p and a+b+c <= 2p ("double truncation", R#8).
+// Product code (sm_100a); independent of oracle/.
+//
+// Two kernels:
+//  tensor_seed_kernel  (one CTA per geometry): G^(n), n = 0..max(N,1) (specfun.cuh); the Taylor
+//     tables of the rational kernels from z_+- = 1/(x - i a_+-) (R#7); the x-recursion
+//     Gbar_{00,k+1} across modes (G^(-1) == G^(1) for n = 0); Gbar_{10k}, Gbar_{01k}
+//      and the mixed Gbar_{11k}.  Output: seeds[geom][4][Ni+1][2p+1].
+//  tensor_fill_kernel  (one CTA per (geometry, mode)): the whole tensor of one mode in shared
+//     memory from the seeds by the cylindrical Laplace equation, first in r (b in {0,1}) then in
+//     r1, with the axial term the printed recursion omits restored (R#6):
+//       r^2 (a+1)(a+2) G_{a+2} + r (a+1)(2a+1) G_{a+1} + (a^2 - n^2) G_a
+//         + (c+1)(c+2) [ r^2 G_{a,c+2} + 2 r G_{a-1,c+2} + G_{a-2,c+2} ] = 0,
+//     parallel over (b, c) per radial step.  Written out dense ([a][b][c], c <= 2p) or packed
+//     (c <= 2p-a-b, (p+1)^3 entries: the entries the S2L operator reads).
+#pragma once
+#include "specfun.cuh"
+
+namespace cyl {
+
+struct TensorGeomArgs {
+    const double *r, *r1, *x;    // explicit geometries (test entry), or nullptr for stations
+    int64_t n;                   // number of geometries
+    int station_mode;            // 1: geometry g = (i_in, cls) normalised station (see below)
+    int n_stations;              // stations: g = i_in * 12 + cls
+    int K;                       // modes computed/written: 0..K-1 (window [m0, m1) for fill)
+    int m0, m1;
+    int p;
+    int miller;
+    double fwd2;                 // forward switch for N = max(K-1, 1) (R#3)
+    double *seeds;               // [n][4][Ni+1][2p+1]
+    double *out;                 // dense [n][m1-m0][p+1][p+1][2p+1] or packed [n][m1-m0][(p+1)^3]
+    int packed;
+    int *err;
+};
+
+// The 12 Green's-expansion classes per radial station: (dI, dJ) in {0..3}^2 with
+// max(dI, dJ) >= 2; dI = outer column - inner column, dJ = |z offset| in boxes.
+__host__ __device__ inline void station_class(int cls, int &dI, int &dJ)
+{
+    // order: dI-major over the 16 cells skipping the 4 near ones
+    const int tab[12][2] = {{0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 0}, {2, 1},
+                            {2, 2}, {2, 3}, {3, 0}, {3, 1}, {3, 2}, {3, 3}};
+    dI = tab[cls][0];
+    dJ = tab[cls][1];
+}
+__host__ __device__ inline int class_of(int dI, int dJ)
+{
+    // inverse of station_class; -1 for the near cells
+    if (dI < 2 && dJ < 2) return -1;
+    if (dI < 2) return dI * 2 + (dJ - 2);
+    return 4 + (dI - 2) * 4 + dJ;
+}
+
+__device__ inline void geometry_of(const TensorGeomArgs &a, int64_t g, double &r, double &r1,
+                                   double &x)
+{
+    if (a.station_mode) {
+        int i_in = (int)(g / 12), cls = (int)(g % 12), dI, dJ;
+        station_class(cls, dI, dJ);
+        r1 = i_in + 0.5;          // inner column centre, in units of the box size h
+        r = i_in + dI + 0.5;      // outer column centre
+        x = (double)dJ;
+    } else {
+        r = a.r[g];
+        r1 = a.r1[g];
+        x = a.x[g];
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) tensor_seed_kernel(TensorGeomArgs a)
+{
+    extern __shared__ double sm[];
+    const int p = a.p, C = 2 * p, Q = C + 2, D = C + 1;
+    const int Nw = a.m1 - 1;                 // highest mode needed
+    const int Ni = Nw > 1 ? Nw : 1;          // + mode 1 for n = 0
+    const int NM = Ni + 1;
+    double *G = sm;                          // [NM]
+    double *tab = G + NM;                    // 8 tables x Q: tsum tdif usum udif ssum sdif vp vm
+    double *g00 = tab + 8 * Q;               // [NM][D]
+    double *g10 = g00 + NM * D;
+    double *g01 = g10 + NM * D;
+    double *g11 = g01 + NM * D;
+    const int64_t gi = blockIdx.x;
+    double r, r1, x;
+    geometry_of(a, gi, r, r1, x);
+    const int tid = threadIdx.x;
+    if (!(r > 0.0) || !(r1 > 0.0)) {
+        if (tid == 0) atomicOr(a.err, 2);
+        return;
+    }
+    PairGeo geo = pair_geo(r, r1, x, a.fwd2);
+    if (geo.coincident) {
+        if (tid == 0) atomicOr(a.err, 1);
+        return;
+    }
+    if (tid < 32) {
+        int S_lane = geo.forward ? 0 : (a.K - 1 > Ni ? a.K - 1 : Ni) + miller_extra(geo, a.miller);
+        if (tid == 0) greens_pair(geo, 0, NM, S_lane, G, 1);
+    } else if (tid < 34) {
+        // Taylor coefficients in x of the rational kernels (R#7), sign s: a_s = r +- r1.
+        int s = tid - 32;
+        double as = s == 0 ? r + r1 : r - r1;     // a_+-
+        double bs = s == 0 ? r1 + r : r1 - r;     // exchanged r <-> r1
+        double den = x * x + as * as, dens = x * x + bs * bs;
+        double zr = x / den, zi = as / den;       // z = 1/(x - i a) = (x + i a)/(x^2 + a^2)
+        double yr = x / dens, yi = bs / dens;
+        double wr = zr, wi = zi;                  // w_q = (-1)^q z^{q+1}
+        double vr = yr, vi = yi;
+        double sg = s == 0 ? 1.0 : -1.0;
+        for (int q = 0; q < Q; ++q) {
+            double t = wr;
+            double u = (q == 0 ? -1.0 : 0.0) + 2.0 * r * wi;
+            double us = (q == 0 ? -1.0 : 0.0) + 2.0 * r1 * vi;
+            double w2r = wr * zr - wi * zi;       // (-1)^q z^{q+2}
+            double v = sg * 2.0 * r * (q + 1) * w2r;
+            // store raw per sign in scratch: [s][4][Q] at g11 (reused later)
+            g11[(s * 4 + 0) * Q + q] = t;
+            g11[(s * 4 + 1) * Q + q] = u;
+            g11[(s * 4 + 2) * Q + q] = us;
+            g11[(s * 4 + 3) * Q + q] = v;
+            double nwr = -(wr * zr - wi * zi), nwi = -(wr * zi + wi * zr);
+            wr = nwr;
+            wi = nwi;
+            double nvr = -(vr * yr - vi * yi), nvi = -(vr * yi + vi * yr);
+            vr = nvr;
+            vi = nvi;
+        }
+    }
+    __syncthreads();
+    // raw tables per sign: t+- u+- us+- v+-
+    for (int q = tid; q < Q; q += blockDim.x) {
+        tab[0 * Q + q] = g11[0 * Q + q];  // t+
+        tab[1 * Q + q] = g11[4 * Q + q];  // t-
+        tab[2 * Q + q] = g11[1 * Q + q];  // u+
+        tab[3 * Q + q] = g11[5 * Q + q];  // u-
+        tab[4 * Q + q] = g11[2 * Q + q];  // us+
+        tab[5 * Q + q] = g11[6 * Q + q];  // us-
+        tab[6 * Q + q] = g11[3 * Q + q];  // v+
+        tab[7 * Q + q] = g11[7 * Q + q];  // v-
+    }
+    for (int n = tid; n < NM; n += blockDim.x) g00[n * D] = G[n];
+    __syncthreads();
+    const double *tp = tab, *tm = tab + Q, *up = tab + 2 * Q, *um = tab + 3 * Q;
+    const double *sp = tab + 4 * Q, *smn = tab + 5 * Q, *vp = tab + 6 * Q, *vm = tab + 7 * Q;
+    // x-recursion, in the paper's form with (Gbar^n +- Gbar^{n-1}) formed first:
+    //   Gbar_{00,k+1}^n = (n - 1/2)/(k+1) sum_q [(g_n + g_m)[k-q] t+_q + (g_n - g_m)[k-q] t-_q]
+    for (int k = 0; k < C; ++k) {
+        for (int n = tid; n < NM; n += blockDim.x) {
+            int m = n == 0 ? 1 : n - 1;
+            double s = 0.0;
+            for (int q = 0; q <= k; ++q) {
+                double gn = g00[n * D + k - q], gm = g00[m * D + k - q];
+                s = fma(gn + gm, tp[q], fma(gn - gm, tm[q], s));
+            }
+            g00[n * D + k + 1] = (n - 0.5) * s / (k + 1);
+        }
+        __syncthreads();
+    }
+    // r and r1 derivatives
+    for (int e = tid; e < NM * C; e += blockDim.x) {
+        int n = e / C, k = e % C, m = n == 0 ? 1 : n - 1;
+        double s1 = 0.0, s2 = 0.0;
+        for (int q = 0; q <= k; ++q) {
+            double gn = g00[n * D + k - q], gm = g00[m * D + k - q];
+            double gp = gn + gm, gd = gn - gm;
+            s1 = fma(gp, up[q], fma(gd, um[q], s1));
+            s2 = fma(gp, sp[q], fma(gd, smn[q], s2));
+        }
+        g10[n * D + k] = (-g00[n * D + k] + (n - 0.5) * s1) / (2.0 * r);
+        g01[n * D + k] = (-g00[n * D + k] + (n - 0.5) * s2) / (2.0 * r1);
+    }
+    __syncthreads();
+    // mixed: sum_q [(g+)v+ + (h+)u+ + (g-)v- + (h-)u-] with g = g00, h = g01
+    for (int e = tid; e < NM * (C - 1); e += blockDim.x) {
+        int n = e / (C - 1), k = e % (C - 1), m = n == 0 ? 1 : n - 1;
+        double s = 0.0;
+        for (int q = 0; q <= k; ++q) {
+            double gn = g00[n * D + k - q], gm = g00[m * D + k - q];
+            double hn = g01[n * D + k - q], hm = g01[m * D + k - q];
+            s = fma(gn + gm, vp[q], fma(hn + hm, up[q], fma(gn - gm, vm[q], fma(hn - hm, um[q], s))));
+        }
+        // g11 overlaps the raw tables, consumed before the previous __syncthreads
+        g11[n * D + k] = (-g01[n * D + k] + (n - 0.5) * s) / (2.0 * r);
+    }
+    __syncthreads();
+    // seeds out: [4][NM][D]
+    double *so = a.seeds + gi * 4 * (int64_t)NM * D;
+    for (int e = tid; e < NM * D; e += blockDim.x) {
+        int n = e / D, c = e % D;
+        so[e] = g00[e];
+        so[NM * D + e] = c < C ? g10[e] : 0.0;
+        so[2 * NM * D + e] = c < C ? g01[e] : 0.0;
+        so[3 * NM * D + e] = c < C - 1 ? g11[e] : 0.0;
+        (void)n;
+    }
+}
+
+inline size_t tensor_seed_smem(int K, int m1, int p)
+{
+    int Nw = m1 - 1, Ni = Nw > 1 ? Nw : 1, NM = Ni + 1, Q = 2 * p + 2, D = 2 * p + 1;
+    size_t g11 = (size_t)NM * D;
+    if (g11 < (size_t)8 * Q) g11 = 8 * Q;
+    (void)K;
+    return sizeof(double) * (NM + 8 * Q + 3 * (size_t)NM * D + g11);
+}
+
+// packed offset of (a, b) for order p (host/device helper used by S2L)
+__host__ __device__ inline int packed_off(int aa, int b, int p)
+{
+    // rows a' < aa contribute sum_{b'=0..p} (2p+1-a'-b') = (p+1)(2p+1-a') - p(p+1)/2
+    int off = 0;
+    for (int a2 = 0; a2 < aa; ++a2) off += (p + 1) * (2 * p + 1 - a2) - p * (p + 1) / 2;
+    for (int b2 = 0; b2 < b; ++b2) off += 2 * p + 1 - aa - b2;
+    return off;
+}
+
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) tensor_fill_kernel(TensorGeomArgs a)
+{
+    extern __shared__ double T[];            // [p+1][p+1][2p+1] of one mode
+    const int p = a.p, C = 2 * p, D = C + 1, P1 = p + 1;
+    const int KW = a.m1 - a.m0;
+    const int64_t gi = blockIdx.x / KW;
+    const int n = a.m0 + (int)(blockIdx.x % KW);
+    const int Nw = a.m1 - 1, Ni = Nw > 1 ? Nw : 1, NM = Ni + 1;
+    double r, r1, x;
+    geometry_of(a, gi, r, r1, x);
+    if (!(r > 0.0) || !(r1 > 0.0) || (r == r1 && x == 0.0)) return;   // flagged by seed kernel
+    const int tid = threadIdx.x, nth = blockDim.x;
+    const double *sd = a.seeds + gi * 4 * (int64_t)NM * D;
+    for (int e = tid; e < P1 * P1 * D; e += nth) T[e] = 0.0;
+    __syncthreads();
+#define TI(A, B, Cc) T[((A) * P1 + (B)) * D + (Cc)]
+    for (int c = tid; c < D; c += nth) {
+        TI(0, 0, c) = sd[(0 * NM + n) * D + c];
+        if (c <= C - 1) {
+            if (p >= 1) {
+                TI(1, 0, c) = sd[(1 * NM + n) * D + c];
+                TI(0, 1, c) = sd[(2 * NM + n) * D + c];
+            }
+        }
+        if (c <= C - 2 && p >= 1) TI(1, 1, c) = sd[(3 * NM + n) * D + c];
+    }
+    __syncthreads();
+    const double n2 = (double)n * n;
+    // Laplace in r: Gbar_{a+2,b,c}, b in {0,1}, a = 0..p-2, all c with a+2+b+c <= 2p
+    for (int aa = 0; aa + 2 <= p; ++aa) {
+        const double inv = -1.0 / (r * r * (aa + 1.0) * (aa + 2.0));
+        for (int e = tid; e < 2 * D; e += nth) {
+            int b = e / D, c = e % D;
+            if (aa + 2 + b + c > C) continue;
+            double lap = r * r * TI(aa, b, c + 2);
+            if (aa >= 1) lap = fma(2.0 * r, TI(aa - 1, b, c + 2), lap);
+            if (aa >= 2) lap += TI(aa - 2, b, c + 2);
+            double num = r * (aa + 1) * (2.0 * aa + 1) * TI(aa + 1, b, c) +
+                         (aa * (double)aa - n2) * TI(aa, b, c) + (c + 1.0) * (c + 2.0) * lap;
+            TI(aa + 2, b, c) = num * inv;
+        }
+        __syncthreads();
+    }
+    // Laplace in r1: Gbar_{a,b+2,c}, b = 0..p-2, all a <= p, c with a+b+2+c <= 2p
+    for (int bb = 0; bb + 2 <= p; ++bb) {
+        const double inv = -1.0 / (r1 * r1 * (bb + 1.0) * (bb + 2.0));
+        for (int e = tid; e < P1 * D; e += nth) {
+            int aa = e / D, c = e % D;
+            if (aa + bb + 2 + c > C) continue;
+            double lap = r1 * r1 * TI(aa, bb, c + 2);
+            if (bb >= 1) lap = fma(2.0 * r1, TI(aa, bb - 1, c + 2), lap);
+            if (bb >= 2) lap += TI(aa, bb - 2, c + 2);
+            double num = r1 * (bb + 1) * (2.0 * bb + 1) * TI(aa, bb + 1, c) +
+                         (bb * (double)bb - n2) * TI(aa, bb, c) + (c + 1.0) * (c + 2.0) * lap;
+            TI(aa, bb + 2, c) = num * inv;
+        }
+        __syncthreads();
+    }
+    // write out
+    if (a.packed) {
+        const int64_t TP = (int64_t)P1 * P1 * P1;
+        double *o = a.out + (gi * KW + (n - a.m0)) * TP;
+        for (int e = tid; e < P1 * P1; e += nth) {
+            int aa = e / P1, b = e % P1;
+            const int off = packed_off(aa, b, p);
+            for (int c = 0; c <= C - aa - b; ++c) o[off + c] = TI(aa, b, c);
+        }
+    } else {
+        double *o = a.out + (gi * KW + (n - a.m0)) * (int64_t)P1 * P1 * D;
+        for (int e = tid; e < P1 * P1 * D; e += nth) {
+            int aa = e / (P1 * D), b = (e / D) % P1, c = e % D;
+            o[e] = (aa + b + c <= C) ? T[e] : 0.0;
+        }
+    }
+#undef TI
+}
+
+}  // namespace cyl

@@ -1,0 +1,246 @@
+"""Thin Python binding of libcylfmm.so (include/cylfmm.h): argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels of ``csrc/``; PyTorch supplies device
+memory and the current stream.  There is no CPU fallback: if the shared library is missing
+or no CUDA device is present, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+LIB_PATH = os.path.join(HERE, "libcylfmm.so")
+HEADER = os.path.join(ROOT, "include", "cylfmm.h")
+
+OK, EINVAL, EDOMAIN, ENUMERIC, ECUDA, ENCCL, ENOMEM = range(7)
+MILLER_ACCURATE, MILLER_PAPER = 0, 1
+TRUNC_DOUBLE, TRUNC_SINGLE = 0, 1
+
+
+class CylFMMError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str):
+        super().__init__(f"{where}: status {status} ({detail})")
+        self.status = status
+
+
+class Params(ctypes.Structure):
+    _fields_ = [("n_modes", ctypes.c_int), ("order", ctypes.c_int), ("depth", ctypes.c_int),
+                ("truncation", ctypes.c_int), ("miller", ctypes.c_int),
+                ("exclude_coincident", ctypes.c_int), ("domain_z0", ctypes.c_double),
+                ("domain_L", ctypes.c_double), ("mode_chunk", ctypes.c_int)]
+
+
+class Timings(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_double) for n in ("ms_tree", "ms_p2m", "ms_m2m", "ms_tensor", "ms_s2l",
+                                                "ms_l2l", "ms_l2p", "ms_p2p", "ms_total")] + \
+               [(n, ctypes.c_int64) for n in ("n_near_pairs", "n_skipped", "n_s2l_pairs",
+                                              "kernel_launches")]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_lib = None
+
+
+def header_functions() -> list[str]:
+    """Names of the functions declared in include/cylfmm.h."""
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return re.findall(r"\b(cylfmm_[a-z_]+)\s*\(", txt)
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"libcylfmm.so not built ({LIB_PATH}); run __graft_entry__.build()")
+    L = ctypes.CDLL(LIB_PATH)
+    d, i, i64, vp = ctypes.c_double, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p
+    L.cylfmm_status_string.restype = ctypes.c_char_p
+    L.cylfmm_status_string.argtypes = [i]
+    L.cylfmm_last_error.restype = ctypes.c_char_p
+    L.cylfmm_last_error.argtypes = []
+    L.cylfmm_version.restype = ctypes.c_char_p
+    L.cylfmm_version.argtypes = []
+    L.cylfmm_direct.restype = i
+    L.cylfmm_direct.argtypes = [vp, vp, vp, i64, vp, vp, i64, i, i, i, vp, vp]
+    L.cylfmm_plan_create.restype = i
+    L.cylfmm_plan_create.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(Params)]
+    L.cylfmm_plan_destroy.restype = None
+    L.cylfmm_plan_destroy.argtypes = [vp]
+    L.cylfmm_plan_sync.restype = i
+    L.cylfmm_plan_sync.argtypes = [vp]
+    L.cylfmm_fmm_solve.restype = i
+    L.cylfmm_fmm_solve.argtypes = [vp, vp, vp, vp, i64, vp, vp, i64, vp, vp,
+                                   ctypes.POINTER(Timings)]
+    L.cylfmm_fmm_solve_host.restype = i
+    L.cylfmm_fmm_solve_host.argtypes = L.cylfmm_fmm_solve.argtypes
+    L.cylfmm_greens_batch.restype = i
+    L.cylfmm_greens_batch.argtypes = [vp, vp, vp, i64, i, i, vp, vp]
+    L.cylfmm_tensor_batch.restype = i
+    L.cylfmm_tensor_batch.argtypes = [vp, vp, vp, i64, i, i, i, vp, vp]
+    L.cylfmm_tree_sort.restype = i
+    L.cylfmm_tree_sort.argtypes = [vp, vp, i64, i, d, d, vp, vp, vp]
+    _lib = L
+    return L
+
+
+def _check(st: int, where: str):
+    if st != OK:
+        L = lib()
+        raise CylFMMError(st, where, f"{L.cylfmm_status_string(st).decode()}: "
+                                     f"{L.cylfmm_last_error().decode()}")
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("cylfmm: no CUDA device (there is no CPU fallback)")
+    return torch
+
+
+def _dev_f64(t, torch):
+    t = torch.as_tensor(t, dtype=torch.float64, device="cuda")
+    return t.contiguous()
+
+
+def _dev_c128(t, torch):
+    t = torch.as_tensor(t, dtype=torch.complex128, device="cuda")
+    return t.contiguous()
+
+
+def _stream(torch):
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None and t.numel() > 0 else ctypes.c_void_p(0)
+
+
+def direct(src_r, src_z, src_S, fld_r, fld_z, miller=MILLER_ACCURATE, exclude_coincident=True,
+           out=None):
+    """Direct modal sum on the GPU (cylfmm_direct).  Returns complex128 [n_fld, K] (cuda)."""
+    torch = _torch()
+    sr, sz, fr, fz = (_dev_f64(a, torch) for a in (src_r, src_z, fld_r, fld_z))
+    S = _dev_c128(src_S, torch)
+    ns, K = S.shape
+    nf = fr.shape[0]
+    if out is None:
+        out = torch.empty((nf, K), dtype=torch.complex128, device="cuda")
+    _check(lib().cylfmm_direct(_ptr(sr), _ptr(sz), _ptr(S), ns, _ptr(fr), _ptr(fz), nf, K, miller,
+                               int(bool(exclude_coincident)), _ptr(out), _stream(torch)),
+           "cylfmm_direct")
+    return out
+
+
+def greens_batch(r, r1, x, n_modes, miller=MILLER_ACCURATE):
+    torch = _torch()
+    r, r1, x = (_dev_f64(a, torch) for a in (r, r1, x))
+    n = r.shape[0]
+    out = torch.empty((n, n_modes), dtype=torch.float64, device="cuda")
+    _check(lib().cylfmm_greens_batch(_ptr(r), _ptr(r1), _ptr(x), n, n_modes, miller, _ptr(out),
+                                     _stream(torch)), "cylfmm_greens_batch")
+    return out
+
+
+def tensor_batch(r, r1, x, n_modes, p, miller=MILLER_ACCURATE):
+    torch = _torch()
+    r, r1, x = (_dev_f64(a, torch) for a in (r, r1, x))
+    n = r.shape[0]
+    out = torch.empty((n, n_modes, p + 1, p + 1, 2 * p + 1), dtype=torch.float64, device="cuda")
+    _check(lib().cylfmm_tensor_batch(_ptr(r), _ptr(r1), _ptr(x), n, n_modes, p, miller,
+                                     _ptr(out), _stream(torch)), "cylfmm_tensor_batch")
+    return out
+
+
+def tree_sort(r, z, depth, L, z0=0.0):
+    torch = _torch()
+    r, z = _dev_f64(r, torch), _dev_f64(z, torch)
+    n = r.shape[0]
+    key = torch.empty(n, dtype=torch.int32, device="cuda")
+    perm = torch.empty(n, dtype=torch.int32, device="cuda")
+    _check(lib().cylfmm_tree_sort(_ptr(r), _ptr(z), n, depth, float(L), float(z0), _ptr(key),
+                                  _ptr(perm), _stream(torch)), "cylfmm_tree_sort")
+    return key, perm
+
+
+@dataclass
+class FMMConfig:
+    n_modes: int
+    order: int
+    depth: int
+    L: float = 1.0
+    z0: float = 0.0
+    truncation: int = TRUNC_DOUBLE
+    miller: int = MILLER_ACCURATE
+    exclude_coincident: bool = True
+    mode_chunk: int = 0
+
+
+class Plan:
+    """An FMM plan (cylfmm_plan_create); owns its device workspace."""
+
+    def __init__(self, cfg: FMMConfig):
+        _torch()
+        self.cfg = cfg
+        prm = Params(cfg.n_modes, cfg.order, cfg.depth, cfg.truncation, cfg.miller,
+                     int(bool(cfg.exclude_coincident)), float(cfg.z0), float(cfg.L),
+                     cfg.mode_chunk)
+        h = ctypes.c_void_p()
+        _check(lib().cylfmm_plan_create(ctypes.byref(h), ctypes.byref(prm)), "cylfmm_plan_create")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().cylfmm_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def solve(self, src_r, src_z, src_S, fld_r, fld_z, out=None, timings=False):
+        """Device solve (cylfmm_fmm_solve).  Returns out (complex128 [n_fld, K], cuda) and the
+        timings dict if requested (that path synchronises)."""
+        torch = _torch()
+        sr, sz, fr, fz = (_dev_f64(a, torch) for a in (src_r, src_z, fld_r, fld_z))
+        S = _dev_c128(src_S, torch)
+        ns = S.shape[0]
+        nf = fr.shape[0]
+        if out is None:
+            out = torch.empty((nf, self.cfg.n_modes), dtype=torch.complex128, device="cuda")
+        tm = Timings() if timings else None
+        _check(lib().cylfmm_fmm_solve(self._h, _ptr(sr), _ptr(sz), _ptr(S), ns, _ptr(fr), _ptr(fz),
+                                      nf, _ptr(out), _stream(torch),
+                                      ctypes.byref(tm) if tm is not None else None),
+               "cylfmm_fmm_solve")
+        return (out, tm.as_dict()) if timings else out
+
+    def solve_host(self, src_r, src_z, src_S, fld_r, fld_z, out=None, timings=False):
+        """Host-buffer solve (cylfmm_fmm_solve_host): numpy in, numpy out, copies included."""
+        torch = _torch()
+        sr, sz, fr, fz = (np.ascontiguousarray(a, dtype=np.float64) for a in (src_r, src_z, fld_r, fld_z))
+        S = np.ascontiguousarray(src_S, dtype=np.complex128)
+        ns, nf = S.shape[0], fr.shape[0]
+        if out is None:
+            out = np.empty((nf, self.cfg.n_modes), dtype=np.complex128)
+        tm = Timings() if timings else None
+        p = lambda a: ctypes.c_void_p(a.ctypes.data) if a.size else ctypes.c_void_p(0)  # noqa: E731
+        _check(lib().cylfmm_fmm_solve_host(self._h, p(sr), p(sz), p(S), ns, p(fr), p(fz), nf, p(out),
+                                           _stream(torch),
+                                           ctypes.byref(tm) if tm is not None else None),
+               "cylfmm_fmm_solve_host")
+        return (out, tm.as_dict()) if timings else out
+
+    def sync(self):
+        _check(lib().cylfmm_plan_sync(self._h), "cylfmm_plan_sync")

@@ -1,0 +1,242 @@
+"""GPU parity: every CUDA step of the hot path against the oracle (oracle/, plain FP64 C) on the
+same seeded inputs, through the C-ABI (libcylfmm.so via the ctypes binding).
+
+Metric (reading R#14, the paper's P:697-703): eps^(n) = max_j |A - B| / max_j |B| per mode.
+Tolerances (BASELINE.json north_star): 1e-12 per mode for the direct sum, the Green's function,
+the tensor (per mode and total derivative order) and the FMM against the oracle FMM."""
+import numpy as np
+import pytest
+
+from tests.inputs import config_c1, config_c2, uniform_rings
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2301_01179_b200 import build as b
+    b.build()
+    import paper_2301_01179_b200 as g
+    return g
+
+
+def eps_modes(A, B):
+    A, B = np.asarray(A), np.asarray(B)
+    num = np.abs(A - B).max(axis=0)
+    den = np.abs(B).max(axis=0)
+    return num / np.where(den > 0, den, 1.0)
+
+
+def _geoms(rng, n):
+    r = 0.05 + 2 * rng.random(n)
+    r1 = 0.05 + 2 * rng.random(n)
+    x = rng.standard_normal(n)
+    # near the branch point chi = 1.008 from both sides, near-coincident and very far pairs
+    rr = 0.5 + rng.random(64)
+    chi = np.concatenate([1.008 + np.linspace(-4e-4, 4e-4, 32), 1 + np.logspace(-10, -2, 16),
+                          np.logspace(1, 7, 16)])
+    # r = r1 = rr, x from chi: chi = 1 + x^2 / (2 rr^2)
+    xx = np.sqrt(2 * (chi - 1)) * rr
+    return np.concatenate([r, rr]), np.concatenate([r1, rr]), np.concatenate([x, xx])
+
+
+@pytest.mark.parametrize("K", [1, 2, 9, 17, 65, 100])
+@pytest.mark.parametrize("miller", [0, 1])
+def test_greens_batch_vs_oracle(gpu, orc, K, miller):
+    rng = np.random.default_rng(100 + K)
+    r, r1, x = _geoms(rng, 300)
+    G = gpu.greens_batch(r, r1, x, K, miller).cpu().numpy()
+    for q in range(len(r)):
+        ref = orc.greens(r[q], r1[q], x[q], K - 1, miller)
+        err = np.abs(G[q] - ref).max() / np.abs(ref).max()
+        # forward branch (chi < 1.008): rounding errors grow like the dominant solution,
+        # ~eps lambda^n relative to G^(0) in BOTH codes (SURVEY finding 6); the bound is that
+        # conditioning, not a looser parity (at K <= 17 it is below 1e-12 anyway)
+        chi = (r[q] ** 2 + r1[q] ** 2 + x[q] ** 2) / (2 * r[q] * r1[q])
+        lam = chi + np.sqrt(chi * chi - 1)
+        fwd = (chi - 1) < orc.forward_coef(K - 1, miller) / 2
+        tol = TOL + (8 * 2.2e-16 * lam ** (K - 1) if fwd else 0.0)
+        assert err <= tol, (q, r[q], r1[q], x[q], err)
+
+
+@pytest.mark.parametrize("p,K", [(4, 3), (8, 17), (12, 9), (16, 5)])
+def test_tensor_batch_vs_oracle(gpu, orc, p, K):
+    # normalised station-like geometries (the FMM evaluates tensors at (i+dI+1/2, i+1/2, dJ))
+    geo = [(2.5, 0.5, 0.0), (3.5, 1.5, 2.0), (10.5, 10.5, 2.0), (16.5, 13.5, 3.0),
+           (1.3, 0.7, 0.9), (0.8, 0.8, 0.5), (5.5, 3.5, 1.0)]
+    r, r1, x = (np.array(v) for v in zip(*geo))
+    T = gpu.tensor_batch(r, r1, x, K, p).cpu().numpy()
+    w, order = _s2l_weight(p)
+    for q in range(len(r)):
+        ref = orc.tensor(r[q], r1[q], x[q], K - 1, p)
+        for n in range(min(K, 11)):   # well-conditioned modes; n > 10 in the next test
+            den = np.abs(ref[n] * w).max()
+            err = np.abs((T[q, n] - ref[n]) * w).max() / den
+            assert err <= TOL, (q, n, err)
+    # zero beyond the double-truncation simplex
+    assert np.all(T[:, :, order > 2 * p] == 0)
+
+
+def _s2l_weight(p):
+    """S2L weighting (fmm_ops.cuh, normalised units): entry (a, b, c) multiplies source and
+    target monomials of size <= 2^-(a+b+c) summed over the 2^c (j, l) splits: weight 2^-(a+b)."""
+    a = np.arange(p + 1)[:, None, None]
+    b = np.arange(p + 1)[None, :, None]
+    c = np.arange(2 * p + 1)[None, None, :]
+    order = a + b + c
+    return 2.0 ** -(a + b) * (order <= 2 * p), order
+
+
+def test_tensor_high_modes_no_worse_than_oracle(gpu, orc):
+    """High modes: the paper's cross-mode x-recursion takes differences of adjacent
+    modes and the radial Laplace recursion carries (a^2 - n^2) terms, so rounding is amplified in
+    BOTH FP64 codes (SURVEY APP-E).  Against a 50-digit evaluation of the same recursions the GPU
+    error must stay within 8x the oracle's own rounding error (plus 1e-14)."""
+    from tests.hp_tensor import hp_tensor
+    p, K = 8, 17
+    geo = [(10.5, 10.5, 2.0), (3.5, 1.5, 2.0), (1.3, 0.7, 0.9)]
+    r, r1, x = (np.array(v) for v in zip(*geo))
+    T = gpu.tensor_batch(r, r1, x, K, p).cpu().numpy()
+    w, _ = _s2l_weight(p)
+    for q in range(len(r)):
+        E = hp_tensor(r[q], r1[q], x[q], K - 1, p)
+        O = orc.tensor(r[q], r1[q], x[q], K - 1, p)
+        for n in range(K):
+            den = np.abs(E[n] * w).max()
+            eg = np.abs((T[q, n] - E[n]) * w).max() / den
+            eo = np.abs((O[n] - E[n]) * w).max() / den
+            assert eg <= 8 * eo + 1e-14, (geo[q], n, eg, eo)
+
+
+def test_direct_c1_vs_oracle(gpu, orc):
+    pr = config_c1()
+    ref, sk = orc.direct(pr.sr, pr.sz, pr.S, pr.fr, pr.fz)
+    out = gpu.direct(pr.sr, pr.sz, pr.S, pr.fr, pr.fz).cpu().numpy()
+    e = eps_modes(out, ref)
+    assert e.max() <= TOL, e
+
+
+@pytest.mark.parametrize("ns,nf,K,miller", [(101, 37, 5, 0), (7, 300, 1, 0), (513, 129, 80, 0),
+                                            (257, 65, 17, 1), (3, 3, 2, 1)])
+def test_direct_ragged_vs_oracle(gpu, orc, ns, nf, K, miller):
+    rng = np.random.default_rng(ns * 7 + nf)
+    sr, sz, S = uniform_rings(rng, ns, K)
+    fr, fz, _ = uniform_rings(rng, nf, 1)
+    ref, _ = orc.direct(sr, sz, S, fr, fz, miller=miller)
+    out = gpu.direct(sr, sz, S, fr, fz, miller=miller).cpu().numpy()
+    # K = 80 is beyond every BASELINE config (K <= 65): there the seeds' rounding, carried through
+    # the near-coincident (lambda ~ 1) forward recursion over 80 modes and 513 sources, reaches
+    # ~1e-12 in both codes (R#3); 3e-12 bounds that case only.
+    tol = TOL if K <= 65 else 3e-12
+    assert eps_modes(out, ref).max() <= tol
+
+
+def test_direct_self_exclusion_and_errors(gpu, orc):
+    rng = np.random.default_rng(5)
+    sr, sz, S = uniform_rings(rng, 200, 4)
+    ref, sk = orc.direct(sr, sz, S, sr, sz)
+    assert sk == 200
+    out = gpu.direct(sr, sz, S, sr, sz).cpu().numpy()
+    assert eps_modes(out, ref).max() <= TOL
+    with pytest.raises(gpu.CylFMMError) as ei:
+        gpu.direct(sr, sz, S, sr, sz, exclude_coincident=False)
+    assert ei.value.status == 3
+    # empty source set gives zeros
+    z = gpu.direct(sr[:0], sz[:0], S[:0], sr, sz).cpu().numpy()
+    assert np.all(z == 0)
+
+
+def test_direct_bitwise_deterministic(gpu):
+    pr = config_c1()
+    a = gpu.direct(pr.sr, pr.sz, pr.S, pr.fr, pr.fz).cpu().numpy()
+    b = gpu.direct(pr.sr, pr.sz, pr.S, pr.fr, pr.fz).cpu().numpy()
+    assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("n,depth,L,z0", [(1000, 4, 1.0, 0.0), (70000, 6, 2.0, -1.0), (5, 2, 1.0, 0.0)])
+def test_tree_sort_bit_exact(gpu, orc, n, depth, L, z0):
+    rng = np.random.default_rng(n)
+    r = L * (1 - rng.random(n))
+    z = z0 + L * rng.random(n)
+    r[:3] = L          # closed last box (R#11)
+    z[3:5] = z0 + L
+    key, perm = gpu.tree_sort(r, z, depth, L, z0)
+    k_ref, p_ref = orc.tree_keys(r, z, depth, L, z0)
+    assert np.array_equal(key.cpu().numpy().astype(np.uint32), k_ref)
+    assert np.array_equal(perm.cpu().numpy(), p_ref)
+
+
+def _fmm_case(gpu, orc, sr, sz, S, fr, fz, p, depth, L, z0=0.0, truncation=0, miller=0,
+              mode_chunk=0):
+    K = S.shape[1]
+    ref, sk = orc.fmm(sr, sz, S, fr, fz, p, depth, L, z0, truncation, miller)
+    plan = gpu.Plan(gpu.FMMConfig(n_modes=K, order=p, depth=depth, L=L, z0=z0,
+                                  truncation=truncation, miller=miller, mode_chunk=mode_chunk))
+    out, tm = plan.solve(sr, sz, S, fr, fz, timings=True)
+    assert tm["n_skipped"] == sk
+    return out.cpu().numpy(), ref, plan
+
+
+@pytest.mark.parametrize("n,K,p,depth,L,z0,trunc,miller", [
+    (2000, 5, 6, 4, 1.0, 0.0, 0, 0),
+    (3000, 9, 8, 3, 2.0, -0.5, 0, 1),
+    (1500, 3, 10, 4, 1.0, 0.0, 1, 0),
+    (4000, 17, 12, 4, 1.0, 0.0, 0, 0),
+    (1200, 2, 16, 3, 1.0, 0.0, 0, 0),
+    (800, 1, 5, 2, 1.0, 0.0, 0, 0),
+])
+def test_fmm_small_vs_oracle_fmm(gpu, orc, n, K, p, depth, L, z0, trunc, miller):
+    rng = np.random.default_rng(n + K)
+    sr, sz, S = uniform_rings(rng, n, K, rmax=L, zmax=L)
+    sz = sz + z0
+    out, ref, _ = _fmm_case(gpu, orc, sr, sz, S, sr, sz, p, depth, L, z0, trunc, miller)
+    e = eps_modes(out, ref)
+    assert e.max() <= TOL, e
+
+
+def test_fmm_separate_fields_ragged(gpu, orc):
+    rng = np.random.default_rng(77)
+    sr, sz, S = uniform_rings(rng, 2345, 7)
+    fr, fz, _ = uniform_rings(rng, 333, 1)
+    out, ref, _ = _fmm_case(gpu, orc, sr, sz, S, fr, fz, 8, 4, 1.0)
+    assert eps_modes(out, ref).max() <= TOL
+
+
+def test_fmm_c2_vs_oracle_fmm_and_direct(gpu, orc):
+    pr = config_c2()
+    out, ref, plan = _fmm_case(gpu, orc, pr.sr, pr.sz, pr.S, pr.fr, pr.fz, pr.p, pr.depth, pr.L)
+    e = eps_modes(out, ref)
+    assert e.max() <= TOL, e
+    # against the direct sum: the paper's method at p = 8 (SURVEY APP-I: eps0 7.5e-6, max 3.5e-5)
+    D = gpu.direct(pr.sr, pr.sz, pr.S, pr.fr, pr.fz).cpu().numpy()
+    ed = eps_modes(out, D)
+    assert ed.max() < 1e-4 and ed[0] < 2e-5, ed
+
+
+def test_fmm_mode_chunks_and_host_api_identical(gpu, orc):
+    rng = np.random.default_rng(9)
+    sr, sz, S = uniform_rings(rng, 3000, 11)
+    plan_a = gpu.Plan(gpu.FMMConfig(n_modes=11, order=8, depth=4))
+    plan_b = gpu.Plan(gpu.FMMConfig(n_modes=11, order=8, depth=4, mode_chunk=4))
+    a = plan_a.solve(sr, sz, S, sr, sz).cpu().numpy()
+    b = plan_b.solve(sr, sz, S, sr, sz).cpu().numpy()
+    assert np.array_equal(a, b)
+    h = plan_a.solve_host(sr, sz, S, sr, sz)
+    assert np.array_equal(a, h)
+    c = plan_a.solve(sr, sz, S, sr, sz).cpu().numpy()
+    assert np.array_equal(a, c)   # bitwise reproducible
+
+
+def test_fmm_domain_error(gpu):
+    plan = gpu.Plan(gpu.FMMConfig(n_modes=2, order=4, depth=3))
+    r = np.array([0.5, 1.5])
+    z = np.array([0.5, 0.5])
+    S = np.ones((2, 2), dtype=np.complex128)
+    with pytest.raises(gpu.CylFMMError) as ei:
+        plan.solve(r, z, S, r, z)
+    assert ei.value.status == 2
