@@ -57,7 +57,7 @@ enum { CYLFMM_TRUNC_DOUBLE = 0,    /* source i+j <= p and local k+l <= p (defaul
 
 /* Limits of this build. */
 #define CYLFMM_MAX_MODES 256   /* K <= 256 */
-#define CYLFMM_MAX_ORDER 20    /* p <= 20 */
+#define CYLFMM_MAX_ORDER 16    /* p <= 16 (the paper's highest order) */
 #define CYLFMM_MAX_DEPTH 11    /* d <= 11 (leaf Morton keys fit 22 bits) */
 
 typedef struct {

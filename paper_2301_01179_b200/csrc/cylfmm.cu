@@ -76,11 +76,9 @@ static cudaError_t allow_smem(F *kernel)
 #define P2P_INSTANCES(X)                                                                       \
     X(8, 16, 2) X(8, 16, 5) X(16, 8, 3) X(16, 8, 9) X(32, 4, 6) X(32, 4, 18)
 
-using S2L8 = S2LCfg<128, 8, 6, 2, 48>;
-#define S2L_P8 128, 8, 6, 2, 48
+#define S2L_P8 128, 8, 6, 4, 48
 #define S2L_P12 256, 16, 6, 4, 32
-#define S2L_P16 256, 16, 10, 4, 32
-#define S2L_P20 256, 16, 16, 4, 32
+#define S2L_P16 256, 16, 10, 2, 32
 
 static cylfmm_status ensure_init()
 {
@@ -107,9 +105,15 @@ static cylfmm_status ensure_init()
     CK(allow_smem(s2l_kernel<S2L_P8>));
     CK(allow_smem(s2l_kernel<S2L_P12>));
     CK(allow_smem(s2l_kernel<S2L_P16>));
-    CK(allow_smem(s2l_kernel<S2L_P20>));
     if (dev < 64) g_init_done[dev] = true;
     return CYLFMM_OK;
+}
+
+static int s2l_mp(int p)
+{
+    if (p <= 8) return S2LCfg<S2L_P8>::MP;
+    if (p <= 12) return S2LCfg<S2L_P12>::MP;
+    return S2LCfg<S2L_P16>::MP;
 }
 
 static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -356,6 +360,7 @@ struct cylfmm_plan_s {
     DevBuf M, Lc, tens, seeds;
     DevBuf tasks, ntasks, tcnt, toff;
     DevBuf err, ctr;
+    DevBuf s2lidx;   // S2L operator gather table for this plan's (p, truncation)
     // host-API staging
     DevBuf h_sr, h_sz, h_S, h_fr, h_fz, h_out;
     cudaEvent_t ev[16];
@@ -370,7 +375,7 @@ static void free_plan_bufs(cylfmm_plan p)
                      &p->scan_tmp[3], &p->sr_s, &p->sz_s, &p->S_s, &p->fr_s, &p->fz_s,
                      &p->slstart, &p->flstart, &p->flags, &p->smap, &p->skeys, &p->tmap,
                      &p->tkeys, &p->counts, &p->M, &p->Lc, &p->tens, &p->seeds, &p->tasks,
-                     &p->ntasks, &p->tcnt, &p->toff, &p->err, &p->ctr, &p->h_sr, &p->h_sz,
+                     &p->ntasks, &p->tcnt, &p->toff, &p->err, &p->ctr, &p->s2lidx, &p->h_sr, &p->h_sz,
                      &p->h_S, &p->h_fr, &p->h_fz, &p->h_out};
     for (DevBuf *b : all) b->release();
 }
@@ -398,6 +403,12 @@ extern "C" cylfmm_status cylfmm_plan_create(cylfmm_plan *plan, const cylfmm_para
     CK(cudaDeviceGetAttribute(&p->nsm, cudaDevAttrMultiProcessorCount, p->device));
     for (int i = 0; i < 16; ++i) CK(cudaEventCreate(&p->ev[i]));
     p->ev_ok = true;
+    {
+        std::vector<int> tab;
+        build_s2l_index(q.order, s2l_mp(q.order), q.truncation, tab);
+        RET_IF(p->s2lidx.need(sizeof(int) * tab.size()));
+        CK(cudaMemcpy(p->s2lidx.p, tab.data(), sizeof(int) * tab.size(), cudaMemcpyHostToDevice));
+    }
     *plan = p;
     return CYLFMM_OK;
 }
@@ -534,24 +545,33 @@ extern "C" cylfmm_status cylfmm_tree_sort(const double *r, const double *z, int6
 static int64_t pow4(int l) { return (int64_t)1 << (2 * l); }
 
 template <int NT, int TM, int RM, int RN, int KC>
-static cudaError_t launch_s2l_t(const FarArgs &fa, int level, cudaStream_t st)
+static cudaError_t launch_s2l_t(const FarArgs &fa, cudaStream_t st)
 {
     using Cfg = S2LCfg<NT, TM, RM, RN, KC>;
-    int nb = 1 << level;
-    int half = std::max(nb / 2, 1);
-    int jtiles = (half + Cfg::JT - 1) / Cfg::JT;
-    int KW = fa.m1 - fa.m0;
-    size_t grid = (size_t)nb * 2 * jtiles * KW;
+    S2LGrid gr = {};
+    const int KW = fa.m1 - fa.m0;
+    int64_t tot = 0;
+    for (int l = 2; l <= fa.depth; ++l) {
+        if (fa.tcount[l] == 0) continue;
+        int nb = 1 << l, half = std::max(nb / 2, 1);
+        int jtiles = (half + Cfg::JH - 1) / Cfg::JH;
+        gr.level[gr.nlev] = l;
+        gr.jtiles[gr.nlev] = jtiles;
+        gr.start[gr.nlev] = tot;
+        tot += (int64_t)nb * jtiles * KW;
+        gr.nlev++;
+    }
+    gr.start[gr.nlev] = tot;
+    if (tot == 0) return cudaSuccess;
     size_t sm = s2l_smem_bytes<NT, TM, RM, RN, KC>(fa.p);
-    s2l_kernel<NT, TM, RM, RN, KC><<<(unsigned)grid, NT, sm, st>>>(fa, level, jtiles);
+    s2l_kernel<NT, TM, RM, RN, KC><<<(unsigned)tot, NT, sm, st>>>(fa, gr);
     return cudaGetLastError();
 }
-static cudaError_t launch_s2l(const FarArgs &fa, int level, cudaStream_t st)
+static cudaError_t launch_s2l(const FarArgs &fa, cudaStream_t st)
 {
-    if (fa.p <= 8) return launch_s2l_t<S2L_P8>(fa, level, st);
-    if (fa.p <= 12) return launch_s2l_t<S2L_P12>(fa, level, st);
-    if (fa.p <= 16) return launch_s2l_t<S2L_P16>(fa, level, st);
-    return launch_s2l_t<S2L_P20>(fa, level, st);
+    if (fa.p <= 8) return launch_s2l_t<S2L_P8>(fa, st);
+    if (fa.p <= 12) return launch_s2l_t<S2L_P12>(fa, st);
+    return launch_s2l_t<S2L_P16>(fa, st);
 }
 
 struct PhaseTimer {
@@ -684,7 +704,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         stot += fa.scount[l];
         ttot += fa.tcount[l];
     }
-    const int64_t TP = (int64_t)(pp + 1) * (pp + 1) * (pp + 1);
+    const int64_t TP = (int64_t)(pp + 1) * (pp + 1) * (pp + 1) + ((pp + 1) & 1);  // padded
     const int64_t nstat = (int64_t)12 << d;
     const int NM = std::max(K - 1, 1) + 1, D = 2 * pp + 1;
     RET_IF(p->M.need(sizeof(double2) * (size_t)std::max<int64_t>(stot, 1) * KW * P));
@@ -704,6 +724,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     fa.fperm = fperm;
     fa.out = reinterpret_cast<double2 *>(out_Phi);
     fa.s2l_pairs = p->ctr.as<unsigned long long>() + 2;
+    fa.s2l_idx = p->s2lidx.as<int>();
     double ms_tensor = 0, ms_p2m = 0, ms_m2m = 0, ms_s2l = 0, ms_l2l = 0, ms_l2p = 0;
     cudaEvent_t e0 = p->ev[10], e1 = p->ev[11];
     auto tic = [&]() { if (tm) cudaEventRecord(e0, st); };
@@ -757,28 +778,30 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
                 CKL();
                 p->launches++;
             }
+            // S2L consumes the moments pre-scaled by (-1)^j / j! (fmm_ops.cuh)
+            prescale_moments_kernel<<<nblk(stot * kw * P, 256), 256, 0, st>>>(fa.M, stot * kw, pp, P);
+            CKL();
+            p->launches++;
             toc(ms_m2m);
         }
-        for (int l = 2; l <= d; ++l) {
-            if (fa.tcount[l] == 0) continue;
-            tic();
-            if (l == 2) {
-                CK(cudaMemsetAsync(fa.Lc + fa.toff[2] * kw * P, 0,
-                                   sizeof(double2) * (size_t)fa.tcount[2] * kw * P, st));
-            } else {
-                size_t sm = sizeof(double2) * P + sizeof(double) * (pp + 1) * (pp + 1);
-                l2l_kernel<<<(unsigned)((int64_t)fa.tcount[l] * kw), 256, sm, st>>>(fa, l);
-                CKL();
-                p->launches++;
-            }
-            toc(ms_l2l);
-            if (ns > 0 && fa.scount[l] > 0) {
-                tic();
-                CK(launch_s2l(fa, l, st));
-                p->launches++;
-                toc(ms_s2l);
-            }
+        // S2L of every level in one launch (each level's contribution), then the L2L chain
+        tic();
+        if (ns > 0) {
+            CK(launch_s2l(fa, st));
+            p->launches++;
+        } else {
+            CK(cudaMemsetAsync(fa.Lc, 0, sizeof(double2) * (size_t)ttot * kw * P, st));
         }
+        toc(ms_s2l);
+        tic();
+        for (int l = 3; l <= d; ++l) {
+            if (fa.tcount[l] == 0) continue;
+            size_t sm = sizeof(double2) * P + sizeof(double) * (pp + 1) * (pp + 1);
+            l2l_kernel<<<(unsigned)((int64_t)fa.tcount[l] * kw), 256, sm, st>>>(fa, l);
+            CKL();
+            p->launches++;
+        }
+        toc(ms_l2l);
         tic();
         {
             int ngrp = (kw + kL2PModes - 1) / kL2PModes;

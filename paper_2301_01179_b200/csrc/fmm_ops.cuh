@@ -17,6 +17,8 @@
 #include "tensor.cuh"
 #include "p2p.cuh"
 
+#include <vector>
+
 namespace cyl {
 
 constexpr int kMaxLevels = 12;
@@ -40,6 +42,7 @@ struct FarArgs {
     double2 *out;        // [nf][K], input field order
     const double *tens;  // [12 * 2^d][KW][(p+1)^3] packed
     unsigned long long *s2l_pairs;  // counter of (source box, target box) applications
+    const int *s2l_idx;  // [4][P][MP] operator gather table (build_s2l_index)
 };
 
 __device__ __forceinline__ int tri(int i, int j, int p) { return i * (p + 1) - i * (i - 1) / 2 + j; }
@@ -179,7 +182,8 @@ __global__ void __launch_bounds__(256) m2m_kernel(FarArgs a, int level)
 }
 
 // ---------------------------------------------------------------------------------------------
-// L2L, level l from l-1 (overwrites the level-l locals): CTA per (child box, mode).
+// L2L, level l from l-1, ADDED to the level-l locals (which hold the level's S2L contribution):
+// CTA per (child box, mode).
 __global__ void __launch_bounds__(256) l2l_kernel(FarArgs a, int level)
 {
     extern __shared__ double sm[];
@@ -213,7 +217,9 @@ __global__ void __launch_bounds__(256) l2l_kernel(FarArgs a, int level)
             }
             pq *= sr;
         }
-        a.Lc[((a.toff[level] + slot) * (int64_t)KW + n) * P + ij] = s;
+        double2 *o = a.Lc + ((a.toff[level] + slot) * (int64_t)KW + n) * P + ij;
+        double2 cur = *o;
+        *o = make_double2(cur.x + s.x, cur.y + s.y);
     }
 }
 
@@ -271,181 +277,293 @@ __global__ void __launch_bounds__(256) l2p_kernel(FarArgs a)
 }
 
 // ---------------------------------------------------------------------------------------------
-// S2L, batched per target column: CTA per (level, target column i_t,
-// parity of j_t, tile of JT target boxes of that parity, mode n).  For each of the <= 27 offsets
-// (dI, dJ) of the interaction list (children of the parent's neighbours that are not neighbours,
-// P:246-252, 539-559) the P x P operator
+// S2L, all levels in ONE launch.  CTA per (level, target column i_t, parity
+// of j_t, tile of JT target boxes of that parity, mode n); it writes the level's S2L contribution
+// only (the L2L chain adds the parents afterwards, top-down; L2L is linear so the sum is the
+// paper's L(l) = L2L(L(l-1)) + S2L(l)).  For each of the <= 27 offsets (dI, dJ) of the
+// interaction list (children of the parent's neighbours that are not neighbours, P:246-252,
+// 539-559) the P x P operator
 //     A[(k,l), (i,j)] = sigma C(j+l, j) Gbar^_{A,B, j+l}
 // (FO: sigma = (-1)^j, (A,B) = (k,i); BO: (-1)^l, (k,i); FI: (-1)^j, (i,k); BI: (-1)^l, (i,k))
-// is gathered from the station tensor into smem (k-chunked) and applied to the moments of the
-// JT source boxes (2 JT real columns) by a register-tiled FP64 GEMM on the CUDA cores.
-// Locals accumulate in registers over all offsets in a fixed order (deterministic).
+// is factored as A = diag(1/l!) A' diag((-1)^j / j!) with A'[(k,l),(i,j)] = s H_{A,B}(j+l),
+// H_{ab}(m) = m! Gbar^_{abm} (stored so by the tensor kernel), s = 1 (FO/FI) or (-1)^{j+l}
+// (BO/BI): a pure gather from the station's tensor block, which is copied to smem contiguously.
+// The JT source boxes' moments (2 JT real columns, pre-scaled by (-1)^j/j!) are multiplied on
+// the CUDA cores by a register-tiled FP64 GEMM; outputs accumulate in registers over the offsets
+// in a fixed order (deterministic) and are post-scaled by 1/l! on the write.
 template <int NT, int TM, int RM, int RN, int KC>
 struct S2LCfg {
     static constexpr int TN = NT / TM;
     static constexpr int MP = TM * RM;          // padded rows (>= P)
-    static constexpr int NC = TN * RN;          // columns = 2 JT
-    static constexpr int JT = NC / 2;
+    static constexpr int NC = TN * RN;          // columns = 2 JT (even-j boxes, then odd-j boxes)
+    static constexpr int JT = NC / 2;           // target boxes per CTA (JT/2 of each parity)
+    static constexpr int JH = JT / 2;
+    static constexpr int NOFF = 33;             // (dI, dJ) in [6] x [-3..3] minus the 9 near
 };
 
+struct S2LGrid {
+    int nlev;                       // levels 2..depth
+    int level[kMaxLevels];
+    int jtiles[kMaxLevels];
+    int64_t start[kMaxLevels + 1];  // CTA prefix per level entry
+};
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool valid)
+{
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    int sz = valid ? 16 : 0;   // src-size 0: zero fill
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+template <int RM, int RN, int TM, int TN, int MP, int NC, int MASK>
+__device__ __forceinline__ void s2l_gemm(const double *As, const double *Bs, int kc, int tm,
+                                         int tn, double (&acc)[RM][RN])
+{
+#pragma unroll 3
+    for (int kk = 0; kk < kc; ++kk) {
+        double av[RM], bv[RN];
+#pragma unroll
+        for (int u = 0; u < RM / 2; ++u) {
+            double2 t = *reinterpret_cast<const double2 *>(As + kk * MP + 2 * (tm + TM * u));
+            av[2 * u] = t.x;
+            av[2 * u + 1] = t.y;
+        }
+#pragma unroll
+        for (int v = 0; v < RN; ++v)
+            if (MASK & (1 << v)) bv[v] = Bs[kk * NC + tn + TN * v];
+#pragma unroll
+        for (int u = 0; u < RM; ++u)
+#pragma unroll
+            for (int v = 0; v < RN; ++v)
+                if (MASK & (1 << v)) acc[u][v] = fma(av[u], bv[v], acc[u][v]);
+    }
+}
+
+template <int RM, int RN, int TM, int TN, int MP, int NC, int M>
+__device__ __forceinline__ void s2l_gemm_dispatch(int mask, const double *As, const double *Bs,
+                                                  int kc, int tm, int tn, double (&acc)[RM][RN])
+{
+    if constexpr (M > 0) {
+        if (mask == M) {
+            s2l_gemm<RM, RN, TM, TN, MP, NC, M>(As, Bs, kc, tm, tn, acc);
+            return;
+        }
+        s2l_gemm_dispatch<RM, RN, TM, TN, MP, NC, M - 1>(mask, As, Bs, kc, tm, tn, acc);
+    }
+}
+
 template <int NT, int TM, int RM, int RN, int KC>
-__global__ void __launch_bounds__(NT) s2l_kernel(FarArgs a, int level, int jtiles)
+__global__ void __launch_bounds__(NT) s2l_kernel(FarArgs a, S2LGrid gr)
 {
     using Cfg = S2LCfg<NT, TM, RM, RN, KC>;
-    constexpr int TN = Cfg::TN, MP = Cfg::MP, NC = Cfg::NC, JT = Cfg::JT;
+    constexpr int TN = Cfg::TN, MP = Cfg::MP, NC = Cfg::NC, JT = Cfg::JT, JH = Cfg::JH;
+    constexpr int NOFF = Cfg::NOFF;
+    constexpr int BOXV = TN / 2;                   // boxes per column block v
     extern __shared__ double sm[];
-    double *As = sm;                               // [KC][MP]
-    double *Bs = As + KC * MP;                     // [KC][NC]
-    double *bin = Bs + KC * NC;                    // [(2p+1)][(p+1)]
-    int *tri_i = reinterpret_cast<int *>(bin + (2 * a.p + 1) * (a.p + 1));  // [P]
-    int *tri_j = tri_i + a.P;
-    int *poff = tri_j + a.P;                       // [(p+1)^2]
-    int *tsl = poff + (a.p + 1) * (a.p + 1);       // [JT]
-    int *ssl = tsl + JT;                           // [JT]
-
     const int p = a.p, P = a.P, KW = a.m1 - a.m0;
-    const int nb = 1 << level;
-    int bid = blockIdx.x;
-    const int nloc = bid % KW;
+    const int TP = (p + 1) * (p + 1) * (p + 1), TPp = TP + (TP & 1), HST = TPp + 2;
+    double *As = sm;                               // [KC][MP]
+    double *Bs0 = As + KC * MP;                    // 2 x [P][NC]
+    double *Hs0 = Bs0 + 2 * P * NC;                // 2 x [HST], Hs[TPp] = 0 (masked entries)
+    double *post = Hs0 + 2 * HST;                  // [P] 1 / l!
+    int *tsl = reinterpret_cast<int *>(post + P);  // [JT]  (box b: parity b / JH, index b % JH)
+    int *ssl = tsl + JT;                           // [NOFF][JT]
+    int *olist = ssl + NOFF * JT;                  // [NOFF] active offsets
+    int *nact = olist + NOFF;
+
+    int64_t bid = blockIdx.x;
+    int e = 0;
+    while (e + 1 < gr.nlev && bid >= gr.start[e + 1]) ++e;
+    const int level = gr.level[e], jtiles = gr.jtiles[e];
+    bid -= gr.start[e];
+    const int nloc = (int)(bid % KW);
     bid /= KW;
-    const int jt = bid % jtiles;
-    bid /= jtiles;
-    const int jpar = bid & 1;
-    const int it = bid >> 1;
-    const int n = a.m0 + nloc;
+    const int jt = (int)(bid % jtiles);
+    const int it = (int)(bid / jtiles);
+    const int nb = 1 << level;
     const int tid = threadIdx.x;
     const int tm = tid % TM, tn = tid / TM;
+    const int di0 = (it & 1) ? -3 : -2;
+    auto jt_of = [&](int b) { return 2 * (jt * JH + (b % JH)) + b / JH; };  // target j of box b
 
-    // target boxes of this tile
     int anyt = 0;
     if (tid < JT) {
-        int jtb = jpar + 2 * (jt * JT + tid);
+        int jtb = jt_of(tid);
         int s = -1;
         if (jtb < nb) s = a.tmap[level][morton2((uint32_t)it, (uint32_t)jtb)];
         tsl[tid] = s;
         anyt = s >= 0;
     }
     if (!__syncthreads_or(anyt)) return;
-    for (int e = tid; e < (2 * p + 1) * (p + 1); e += NT) bin[e] = binom_d(e / (p + 1), e % (p + 1));
-    for (int i = 0, ij = 0; i <= p; ++i)
-        for (int j = 0; i + j <= p; ++j, ++ij)
-            if (ij % NT == tid) {
-                tri_i[ij] = i;
-                tri_j[ij] = j;
+    // the 33 offsets in a fixed order, then the source slots of every (offset, box) in one pass
+    if (tid == 0) {
+        int k = 0;
+        for (int di = di0; di <= di0 + 5; ++di)
+            for (int dj = -3; dj <= 3; ++dj) {
+                if (di >= -1 && di <= 1 && dj >= -1 && dj <= 1) continue;
+                olist[k++] = ((di + 3) << 4) | (dj + 3);
             }
-    for (int e = tid; e < (p + 1) * (p + 1); e += NT) poff[e] = packed_off(e / (p + 1), e % (p + 1), p);
-
-    // accumulators: rows m = 2 (tm + TM u) + {0,1}, cols c = tn + TN v
-    double acc[RM][RN];
-    const int64_t TP = (int64_t)(p + 1) * (p + 1) * (p + 1);
+    }
+    for (int q = tid; q < P; q += NT) {
+        int i = 0;
+        while (i < p && q >= (i + 1) * (p + 1) - (i + 1) * i / 2) ++i;
+        int l = q - (i * (p + 1) - i * (i - 1) / 2);
+        double f = 1.0;
+        for (int t = 2; t <= l; ++t) f *= t;
+        post[q] = 1.0 / f;
+    }
+    if (tid < 2) Hs0[tid * HST + TPp] = 0.0;
     __syncthreads();
-#pragma unroll
-    for (int v = 0; v < RN; ++v) {
-        int col = tn + TN * v, box = col >> 1, im = col & 1;
-        int s = tsl[box];
-#pragma unroll
-        for (int u = 0; u < RM; ++u) {
-            int m = 2 * (tm + TM * (u >> 1)) + (u & 1);
-            double x = 0.0;
-            if (s >= 0 && m < P) {
-                double2 L = a.Lc[((a.toff[level] + s) * (int64_t)KW + nloc) * P + m];
-                x = im ? L.y : L.x;
-            }
-            acc[u][v] = x;
-        }
+    for (int q = tid; q < NOFF * JT; q += NT) {
+        int o = q / JT, b = q % JT;
+        int code = olist[o];
+        int di = (code >> 4) - 3, dj = (code & 15) - 3;
+        int is = it + di, jtb = jt_of(b), js = jtb + dj;
+        int par = b / JH;
+        bool ok = tsl[b] >= 0 && is >= 0 && is < nb && js >= 0 && js < nb &&
+                  !(dj == 3 && par == 1) && !(dj == -3 && par == 0);
+        ssl[q] = ok ? a.smap[level][morton2((uint32_t)is, (uint32_t)js)] : -1;
     }
-    const int di0 = (it & 1) ? -3 : -2, dj0 = jpar ? -3 : -2;
-    for (int di = di0; di <= di0 + 5; ++di) {
+    __syncthreads();
+    // compact the active offsets (fixed order) with their column-block masks
+    if (tid == 0) {
+        int k = 0;
+        unsigned long long npairs = 0;
+        for (int o = 0; o < NOFF; ++o) {
+            int mask = 0, cnt = 0;
+            for (int b = 0; b < JT; ++b)
+                if (ssl[o * JT + b] >= 0) {
+                    ++cnt;
+                    mask |= 1 << ((2 * b) / TN);   // column block of box b
+                }
+            if (!cnt) continue;
+            npairs += cnt;
+            olist[k++] = (olist[o] & 0xff) | (o << 8) | (mask << 16);
+        }
+        *nact = k;
+        if (nloc == 0 && a.m0 == 0 && a.s2l_pairs && npairs) atomicAdd(a.s2l_pairs, npairs);
+    }
+    __syncthreads();
+    const int na = *nact;
+
+    double acc[RM][RN];
+#pragma unroll
+    for (int u = 0; u < RM; ++u)
+#pragma unroll
+        for (int v = 0; v < RN; ++v) acc[u][v] = 0.0;
+
+    // async stage of offset k into buffer (k & 1): tensor block + (pre-scaled) moments
+    auto stage = [&](int k) {
+        const int code = olist[k];
+        const int di = ((code >> 4) & 15) - 3, dj = (code & 15) - 3, o = (code >> 8) & 0xff;
         const int is = it + di;
-        if (is < 0 || is >= nb) continue;
-        for (int dj = dj0; dj <= dj0 + 5; ++dj) {
-            if (di >= -1 && di <= 1 && dj >= -1 && dj <= 1) continue;
+        const int iin = min(it, is), dI = di < 0 ? -di : di, dJ = dj < 0 ? -dj : dj;
+        const double *Tn = a.tens + ((int64_t)(iin * 12 + class_of(dI, dJ)) * KW + nloc) * TPp;
+        double *Hs = Hs0 + (k & 1) * HST;
+        double *Bs = Bs0 + (k & 1) * P * NC;
+        for (int q = tid; q < TPp / 2; q += NT) cp_async16(Hs + 2 * q, Tn + 2 * q, true);
+        for (int q = tid; q < P * JT; q += NT) {
+            int b = q / P, kk = q % P;
+            int s = ssl[o * JT + b];
+            const double2 *src = a.M + ((a.soff[level] + (s >= 0 ? s : 0)) * (int64_t)KW + nloc) * P + kk;
+            cp_async16(Bs + kk * NC + 2 * b, src, s >= 0);
+        }
+        cp_async_commit();
+    };
+    if (na > 0) stage(0);
+    for (int k = 0; k < na; ++k) {
+        cp_async_wait_all();
+        __syncthreads();                      // buffer k ready; As free
+        if (k + 1 < na) stage(k + 1);         // overlaps the operator build and GEMM below
+        const int code = olist[k];
+        const int di = ((code >> 4) & 15) - 3, dj = (code & 15) - 3;
+        const int mask = (code >> 16) & 0xff;
+        const int variant = (di <= 0 ? 0 : 2) + (dj <= 0 ? 0 : 1);   // FO, BO, FI, BI
+        const int *itab = a.s2l_idx + (size_t)variant * P * MP;
+        const double *Hs = Hs0 + (k & 1) * HST;
+        const double *Bs = Bs0 + (k & 1) * P * NC;
+        for (int k0 = 0; k0 < P; k0 += KC) {
+            const int kc = min(KC, P - k0);
+            if (k0 > 0) __syncthreads();
+            // A'[kk][m] = +-H_{A,B}(j+l): gather through the precomputed (index, sign) table
+            for (int q = tid; q < kc * MP; q += NT) {
+                int c = __ldg(itab + k0 * MP + q);
+                double v = Hs[c >> 1];
+                As[q] = (c & 1) ? -v : v;
+            }
             __syncthreads();
-            int anys = 0;
-            if (tid < JT) {
-                int jtb = jpar + 2 * (jt * JT + tid), js = jtb + dj;
-                int s = -1;
-                if (tsl[tid] >= 0 && js >= 0 && js < nb)
-                    s = a.smap[level][morton2((uint32_t)is, (uint32_t)js)];
-                ssl[tid] = s;
-                anys = s >= 0;
-            }
-            const int npair = __syncthreads_count(anys);
-            if (npair == 0) continue;
-            if (tid == 0 && nloc == 0 && a.m0 == 0 && a.s2l_pairs) atomicAdd(a.s2l_pairs, (unsigned long long)npair);
-            const bool outward = di <= 0, fwd = dj <= 0;
-            const int iin = min(it, is), dI = di < 0 ? -di : di, dJ = dj < 0 ? -dj : dj;
-            const double *Tn = a.tens + ((int64_t)(iin * 12 + class_of(dI, dJ)) * KW + nloc) * TP;
-            for (int k0 = 0; k0 < P; k0 += KC) {
-                const int kc = min(KC, P - k0);
-                __syncthreads();
-                // A[kk][m]: kk = source coefficient (i, j) = k0 + kk, m = local (k, l)
-                for (int e = tid; e < KC * MP; e += NT) {
-                    int kk = e / MP, m = e % MP;
-                    double val = 0.0;
-                    if (kk < kc && m < P) {
-                        int ij = k0 + kk;
-                        int i = tri_i[ij], j = tri_j[ij], k = tri_i[m], l = tri_j[m];
-                        if (a.truncation == 0 || i + j + k + l <= p) {
-                            int A = outward ? k : i, B = outward ? i : k;
-                            double sg = fwd ? ((j & 1) ? -1.0 : 1.0) : ((l & 1) ? -1.0 : 1.0);
-                            val = sg * bin[(j + l) * (p + 1) + j] * __ldg(Tn + poff[A * (p + 1) + B] + j + l);
-                        }
-                    }
-                    As[e] = val;
-                }
-                for (int e = tid; e < KC * NC; e += NT) {
-                    int kk = e / NC, col = e % NC;
-                    int s = ssl[col >> 1];
-                    double val = 0.0;
-                    if (kk < kc && s >= 0) {
-                        double2 M = a.M[((a.soff[level] + s) * (int64_t)KW + nloc) * P + k0 + kk];
-                        val = (col & 1) ? M.y : M.x;
-                    }
-                    Bs[e] = val;
-                }
-                __syncthreads();
-#pragma unroll 2
-                for (int kk = 0; kk < kc; ++kk) {
-                    double av[RM], bv[RN];
-#pragma unroll
-                    for (int u = 0; u < RM / 2; ++u) {
-                        double2 t = *reinterpret_cast<const double2 *>(As + kk * MP + 2 * (tm + TM * u));
-                        av[2 * u] = t.x;
-                        av[2 * u + 1] = t.y;
-                    }
-#pragma unroll
-                    for (int v = 0; v < RN; ++v) bv[v] = Bs[kk * NC + tn + TN * v];
-#pragma unroll
-                    for (int u = 0; u < RM; ++u)
-#pragma unroll
-                        for (int v = 0; v < RN; ++v) acc[u][v] = fma(av[u], bv[v], acc[u][v]);
-                }
-            }
+            s2l_gemm_dispatch<RM, RN, TM, TN, MP, NC, (1 << RN) - 1>(mask, As, Bs + k0 * NC, kc, tm,
+                                                                    tn, acc);
         }
     }
-    // write back
+    (void)BOXV;
+    // write the level's S2L contribution (post-scaled by 1/l!); every target of the tile is
+    // written, zeros included, so the locals need no initialisation
 #pragma unroll
     for (int v = 0; v < RN; ++v) {
-        int col = tn + TN * v, box = col >> 1, im = col & 1;
-        int s = tsl[box];
+        int col = tn + TN * v, b = col >> 1, im = col & 1;
+        int s = tsl[b];
         if (s < 0) continue;
         double *dst = reinterpret_cast<double *>(a.Lc + ((a.toff[level] + s) * (int64_t)KW + nloc) * P);
 #pragma unroll
         for (int u = 0; u < RM; ++u) {
             int m = 2 * (tm + TM * (u >> 1)) + (u & 1);
-            if (m < P) dst[2 * m + im] = acc[u][v];
+            if (m < P) dst[2 * m + im] = acc[u][v] * post[m];
         }
     }
+}
+
+// Host: (index << 1 | negate) gather table of A'[kk][m] for the 4 variants (FO, BO, FI, BI),
+// rows padded to MP; masked / padded entries point at the zero slot TPp.
+inline void build_s2l_index(int p, int MP, int truncation, std::vector<int> &tab)
+{
+    const int P = (p + 1) * (p + 2) / 2, TP = (p + 1) * (p + 1) * (p + 1), TPp = TP + (TP & 1);
+    std::vector<int> ti(P), tj(P);
+    for (int i = 0, q = 0; i <= p; ++i)
+        for (int j = 0; i + j <= p; ++j, ++q) {
+            ti[q] = i;
+            tj[q] = j;
+        }
+    tab.assign((size_t)4 * P * MP, TPp << 1);
+    for (int var = 0; var < 4; ++var) {
+        const bool outward = var < 2, fwd = (var & 1) == 0;
+        for (int kk = 0; kk < P; ++kk)
+            for (int m = 0; m < P; ++m) {
+                int i = ti[kk], j = tj[kk], k = ti[m], l = tj[m];
+                if (truncation == 1 && i + j + k + l > p) continue;
+                int A = outward ? k : i, B = outward ? i : k;
+                int idx = packed_off(A, B, p) + j + l;
+                int neg = (!fwd && ((j + l) & 1)) ? 1 : 0;
+                tab[((size_t)var * P + kk) * MP + m] = (idx << 1) | neg;
+            }
+    }
+}
+
+// Source moments pre-scaled once for S2L: M'_ij = (-1)^j M^_ij / j! (all levels, after M2M).
+__global__ void prescale_moments_kernel(double2 *M, int64_t nrows, int p, int P)
+{
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nrows * P) return;
+    int q = (int)(e % P);
+    int i = 0;
+    while (i < p && q >= (i + 1) * (p + 1) - (i + 1) * i / 2) ++i;
+    int j = q - (i * (p + 1) - i * (i - 1) / 2);
+    double f = 1.0;
+    for (int t = 2; t <= j; ++t) f *= t;
+    f = ((j & 1) ? -1.0 : 1.0) / f;
+    double2 v = M[e];
+    M[e] = make_double2(v.x * f, v.y * f);
 }
 
 template <int NT, int TM, int RM, int RN, int KC>
 inline size_t s2l_smem_bytes(int p)
 {
     using Cfg = S2LCfg<NT, TM, RM, RN, KC>;
-    int P = (p + 1) * (p + 2) / 2;
-    return sizeof(double) * ((size_t)KC * Cfg::MP + (size_t)KC * Cfg::NC + (2 * p + 1) * (p + 1)) +
-           sizeof(int) * (2 * P + (p + 1) * (p + 1) + 2 * Cfg::JT);
+    int P = (p + 1) * (p + 2) / 2, TP = (p + 1) * (p + 1) * (p + 1), TPp = TP + (TP & 1);
+    return sizeof(double) * ((size_t)KC * Cfg::MP + 2 * (size_t)P * Cfg::NC + 2 * (TPp + 2) + P) +
+           sizeof(int) * (Cfg::JT + Cfg::NOFF * Cfg::JT + Cfg::NOFF + 1);
 }
 
 // Near-field task list: one task per tile of <= TT field points of a non-empty target leaf.

@@ -13,7 +13,7 @@
 //       r^2 (a+1)(a+2) G_{a+2} + r (a+1)(2a+1) G_{a+1} + (a^2 - n^2) G_a
 //         + (c+1)(c+2) [ r^2 G_{a,c+2} + 2 r G_{a-1,c+2} + G_{a-2,c+2} ] = 0,
 //     parallel over (b, c) per radial step.  Written out dense ([a][b][c], c <= 2p) or packed
-//     (c <= 2p-a-b, (p+1)^3 entries: the entries the S2L operator reads).
+//     (c <= 2p-a-b, (p+1)^3 entries: the entries the S2L operator reads, scaled by c!).
 #pragma once
 #include "specfun.cuh"
 
@@ -278,12 +278,16 @@ __global__ void __launch_bounds__(256) tensor_fill_kernel(TensorGeomArgs a)
     }
     // write out
     if (a.packed) {
-        const int64_t TP = (int64_t)P1 * P1 * P1;
-        double *o = a.out + (gi * KW + (n - a.m0)) * TP;
+        const int64_t TP = (int64_t)P1 * P1 * P1, TPp = TP + (TP & 1);   // padded: 16-B blocks
+        double *o = a.out + (gi * KW + (n - a.m0)) * TPp;
         for (int e = tid; e < P1 * P1; e += nth) {
             int aa = e / P1, b = e % P1;
             const int off = packed_off(aa, b, p);
-            for (int c = 0; c <= C - aa - b; ++c) o[off + c] = TI(aa, b, c);
+            double f = 1.0;   // packed (FMM) layout stores H_ab(c) = c! Gbar_abc (S2L Hankel form)
+            for (int c = 0; c <= C - aa - b; ++c) {
+                if (c >= 2) f *= c;
+                o[off + c] = TI(aa, b, c) * f;
+            }
         }
     } else {
         double *o = a.out + (gi * KW + (n - a.m0)) * (int64_t)P1 * P1 * D;
