@@ -773,8 +773,8 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             tic();
             for (int l = d - 1; l >= 2; --l) {
                 if (fa.scount[l] == 0) continue;
-                size_t sm = sizeof(double2) * 4 * P + sizeof(double) * (pp + 1) * (pp + 1);
-                m2m_kernel<<<(unsigned)((int64_t)fa.scount[l] * kw), 256, sm, st>>>(fa, l);
+                unsigned g = (unsigned)((int64_t)fa.scount[l] * ((kw + kMMG - 1) / kMMG));
+                m2m_kernel<<<g, 256, m2m_smem(pp), st>>>(fa, l);
                 CKL();
                 p->launches++;
             }
@@ -796,8 +796,8 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         tic();
         for (int l = 3; l <= d; ++l) {
             if (fa.tcount[l] == 0) continue;
-            size_t sm = sizeof(double2) * P + sizeof(double) * (pp + 1) * (pp + 1);
-            l2l_kernel<<<(unsigned)((int64_t)fa.tcount[l] * kw), 256, sm, st>>>(fa, l);
+            unsigned g = (unsigned)((int64_t)fa.tcount[l] * ((kw + kMMG - 1) / kMMG));
+            l2l_kernel<<<g, 256, l2l_smem(pp), st>>>(fa, l);
             CKL();
             p->launches++;
         }

@@ -134,93 +134,165 @@ __device__ __forceinline__ double binom_d(int n, int k)
 }
 
 // ---------------------------------------------------------------------------------------------
-// M2M, level l from l+1: CTA per (parent box, mode).
+// M2M and L2L: constant binomial recentrings in normalised units, applied separably (r, then z).
+//   M2M (child c -> parent, d = child - parent = (s_r, s_z) h_parent / 4):
+//     T_c[i][j]  = sum_{q<=i} C(i,q) s_r^q 2^-(i+q) M'_c[i-q][j]
+//     M^[i][j]   = sum_c sum_{u<=j} C(j,u) s_z^u 2^-(j+u) T_c[i][j-u]
+//   L2L (parent -> child c), added to the child's S2L contribution:
+//     T[i][m]    = sum_{q: i+q+m<=p} C(i+q,q) s_r^q 2^-(i+2q) L'[i+q][m]
+//     L^[i][j]  += 1/2 sum_{u: i+j+u<=p} C(j+u,u) s_z^u 2^-(j+2u) T[i][j+u]
+// CTA per (box, group of kMMG modes); coefficient tables built in smem.
+constexpr int kMMG = 4;
+
+__device__ inline void recentre_tables(int p, double *cm, double *cl, int tid, int nth)
+{
+    // cm[s][i][q] = C(i,q) s^q 2^-(i+q);  cl[s][i][q] = C(i+q,q) s^q 2^-(i+2q)   (s = -1, +1)
+    const int P1 = p + 1;
+    for (int e = tid; e < 2 * P1 * P1; e += nth) {
+        int sgn = e / (P1 * P1), i = (e / P1) % P1, q = e % P1;
+        double s = sgn ? 1.0 : -1.0;
+        double bm = 0.0, bl = 0.0;
+        if (q <= i) {
+            double c = 1.0;
+            for (int t = 1; t <= q; ++t) c = c * (i - q + t) / t;
+            bm = c;
+        }
+        if (i + q <= p) {
+            double c = 1.0;
+            for (int t = 1; t <= q; ++t) c = c * (i + t) / t;
+            bl = c;
+        }
+        double sq = (q & 1) ? s : 1.0;
+        cm[e] = bm * sq * ldexp(1.0, -(i + q));
+        cl[e] = bl * sq * ldexp(1.0, -(i + 2 * q));
+    }
+}
+
 __global__ void __launch_bounds__(256) m2m_kernel(FarArgs a, int level)
 {
     extern __shared__ double sm[];
-    const int p = a.p, P = a.P, KW = a.m1 - a.m0;
-    const int slot = blockIdx.x / KW, n = blockIdx.x % KW;
-    double2 *ch = reinterpret_cast<double2 *>(sm);   // [4][P]
-    double *bin = reinterpret_cast<double *>(ch + 4 * P);   // [(p+1)^2]
+    const int p = a.p, P = a.P, KW = a.m1 - a.m0, P1 = p + 1;
+    const int ngrp = (KW + kMMG - 1) / kMMG;
+    const int slot = blockIdx.x / ngrp, n0 = (blockIdx.x % ngrp) * kMMG;
+    const int nm = min(kMMG, KW - n0);
+    double *cm = sm, *cl = cm + 2 * P1 * P1;
+    double2 *ch = reinterpret_cast<double2 *>(cl + 2 * P1 * P1);   // [4][nm][P]
+    double2 *T = ch + 4 * kMMG * P;                                  // [4][nm][P]
+    int *tri_i = reinterpret_cast<int *>(T + 4 * kMMG * P);
+    int *tri_j = tri_i + P;
     const uint32_t key = (uint32_t)a.skeys[level][slot];
     int cs[4];
 #pragma unroll
     for (int c = 0; c < 4; ++c) cs[c] = a.smap[level + 1][4 * key + c];
-    for (int e = threadIdx.x; e < (p + 1) * (p + 1); e += blockDim.x)
-        bin[e] = binom_d(e / (p + 1), e % (p + 1));
-    for (int e = threadIdx.x; e < 4 * P; e += blockDim.x) {
-        int c = e / P, ij = e % P;
-        ch[e] = cs[c] >= 0 ? a.M[((a.soff[level + 1] + cs[c]) * (int64_t)KW + n) * P + ij]
+    recentre_tables(p, cm, cl, threadIdx.x, blockDim.x);
+    for (int q = threadIdx.x; q < P; q += blockDim.x) {
+        int i = 0;
+        while (i < p && q >= (i + 1) * (p + 1) - (i + 1) * i / 2) ++i;
+        tri_i[q] = i;
+        tri_j[q] = q - (i * (p + 1) - i * (i - 1) / 2);
+    }
+    for (int e = threadIdx.x; e < 4 * nm * P; e += blockDim.x) {
+        int c = e / (nm * P), r = e % (nm * P);
+        ch[e] = cs[c] >= 0 ? a.M[((a.soff[level + 1] + cs[c]) * (int64_t)KW + n0) * P + r]
                            : make_double2(0.0, 0.0);
     }
     __syncthreads();
-    for (int ij = threadIdx.x; ij < P; ij += blockDim.x) {
-        // decode (i, j)
-        int i = 0;
-        while (tri(i + 1, 0, p) <= ij && i < p) ++i;
-        int j = ij - tri(i, 0, p);
-        double2 s = make_double2(0.0, 0.0);
-        for (int c = 0; c < 4; ++c) {
-            if (cs[c] < 0) continue;
-            double sr = (c & 1) ? 1.0 : -1.0, sz = (c & 2) ? 1.0 : -1.0;
-            const double2 *C = ch + c * P;
-            double pq = 1.0;
+    for (int e = threadIdx.x; e < 4 * nm * P; e += blockDim.x) {
+        int c = e / (nm * P), r = e % (nm * P), n = r / P, ij = r % P;
+        double2 acc = make_double2(0.0, 0.0);
+        if (cs[c] >= 0) {
+            int i = tri_i[ij], j = tri_j[ij];
+            const double *co = cm + ((c & 1) * P1 + i) * P1;
+            const double2 *src = ch + (c * nm + n) * P;
             for (int q = 0; q <= i; ++q) {
-                double pu = pq * bin[i * (p + 1) + q];
-                for (int u = 0; u <= j; ++u) {
-                    double coef = ldexp(pu * bin[j * (p + 1) + u], -(i + j + q + u));
-                    double2 v = C[tri(i - q, j - u, p)];
-                    s.x = fma(coef, v.x, s.x);
-                    s.y = fma(coef, v.y, s.y);
-                    pu *= sz;
-                }
-                pq *= sr;
+                double2 v = src[tri(i - q, j, p)];
+                acc.x = fma(co[q], v.x, acc.x);
+                acc.y = fma(co[q], v.y, acc.y);
             }
         }
-        a.M[((a.soff[level] + slot) * (int64_t)KW + n) * P + ij] = s;
+        T[e] = acc;
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < nm * P; r += blockDim.x) {
+        int n = r / P, ij = r % P, i = tri_i[ij], j = tri_j[ij];
+        double2 acc = make_double2(0.0, 0.0);
+        for (int c = 0; c < 4; ++c) {
+            if (cs[c] < 0) continue;
+            const double *co = cm + (((c >> 1) & 1) * P1 + j) * P1;
+            const double2 *src = T + (c * nm + n) * P;
+            for (int u = 0; u <= j; ++u) {
+                double2 v = src[tri(i, j - u, p)];
+                acc.x = fma(co[u], v.x, acc.x);
+                acc.y = fma(co[u], v.y, acc.y);
+            }
+        }
+        a.M[((a.soff[level] + slot) * (int64_t)KW + n0) * P + r] = acc;
     }
 }
 
-// ---------------------------------------------------------------------------------------------
-// L2L, level l from l-1, ADDED to the level-l locals (which hold the level's S2L contribution):
-// CTA per (child box, mode).
 __global__ void __launch_bounds__(256) l2l_kernel(FarArgs a, int level)
 {
     extern __shared__ double sm[];
-    const int p = a.p, P = a.P, KW = a.m1 - a.m0;
-    const int slot = blockIdx.x / KW, n = blockIdx.x % KW;
-    double2 *par = reinterpret_cast<double2 *>(sm);  // [P]
-    double *bin = reinterpret_cast<double *>(par + P);
+    const int p = a.p, P = a.P, KW = a.m1 - a.m0, P1 = p + 1;
+    const int ngrp = (KW + kMMG - 1) / kMMG;
+    const int slot = blockIdx.x / ngrp, n0 = (blockIdx.x % ngrp) * kMMG;
+    const int nm = min(kMMG, KW - n0);
+    double *cm = sm, *cl = cm + 2 * P1 * P1;
+    double2 *par = reinterpret_cast<double2 *>(cl + 2 * P1 * P1);  // [nm][P]
+    double2 *T = par + kMMG * P;                                   // [nm][P]
+    int *tri_i = reinterpret_cast<int *>(T + kMMG * P);
+    int *tri_j = tri_i + P;
     const uint32_t key = (uint32_t)a.tkeys[level][slot];
     const int ps = a.tmap[level - 1][key >> 2];
-    const int c = key & 3;
-    for (int e = threadIdx.x; e < (p + 1) * (p + 1); e += blockDim.x)
-        bin[e] = binom_d(e / (p + 1), e % (p + 1));
-    for (int e = threadIdx.x; e < P; e += blockDim.x)
-        par[e] = a.Lc[((a.toff[level - 1] + ps) * (int64_t)KW + n) * P + e];
-    __syncthreads();
-    const double sr = (c & 1) ? 1.0 : -1.0, sz = (c & 2) ? 1.0 : -1.0;
-    for (int ij = threadIdx.x; ij < P; ij += blockDim.x) {
+    const int sr = key & 1, sz = (key >> 1) & 1;
+    recentre_tables(p, cm, cl, threadIdx.x, blockDim.x);
+    for (int q = threadIdx.x; q < P; q += blockDim.x) {
         int i = 0;
-        while (tri(i + 1, 0, p) <= ij && i < p) ++i;
-        int j = ij - tri(i, 0, p);
-        double2 s = make_double2(0.0, 0.0);
-        double pq = 1.0;
-        for (int q = 0; i + j + q <= p; ++q) {
-            double pu = pq * bin[(i + q) * (p + 1) + q];
-            for (int u = 0; i + j + q + u <= p; ++u) {
-                double coef = ldexp(pu * bin[(j + u) * (p + 1) + u], -(1 + i + j + 2 * q + 2 * u));
-                double2 v = par[tri(i + q, j + u, p)];
-                s.x = fma(coef, v.x, s.x);
-                s.y = fma(coef, v.y, s.y);
-                pu *= sz;
-            }
-            pq *= sr;
-        }
-        double2 *o = a.Lc + ((a.toff[level] + slot) * (int64_t)KW + n) * P + ij;
-        double2 cur = *o;
-        *o = make_double2(cur.x + s.x, cur.y + s.y);
+        while (i < p && q >= (i + 1) * (p + 1) - (i + 1) * i / 2) ++i;
+        tri_i[q] = i;
+        tri_j[q] = q - (i * (p + 1) - i * (i - 1) / 2);
     }
+    for (int e = threadIdx.x; e < nm * P; e += blockDim.x)
+        par[e] = a.Lc[((a.toff[level - 1] + ps) * (int64_t)KW + n0) * P + e];
+    __syncthreads();
+    for (int e = threadIdx.x; e < nm * P; e += blockDim.x) {
+        int n = e / P, im = e % P, i = tri_i[im], m = tri_j[im];
+        const double *co = cl + (sr * P1 + i) * P1;
+        const double2 *src = par + n * P;
+        double2 acc = make_double2(0.0, 0.0);
+        for (int q = 0; i + q + m <= p; ++q) {
+            double2 v = src[tri(i + q, m, p)];
+            acc.x = fma(co[q], v.x, acc.x);
+            acc.y = fma(co[q], v.y, acc.y);
+        }
+        T[e] = acc;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nm * P; e += blockDim.x) {
+        int n = e / P, ij = e % P, i = tri_i[ij], j = tri_j[ij];
+        const double *co = cl + (sz * P1 + j) * P1;
+        const double2 *src = T + n * P;
+        double2 acc = make_double2(0.0, 0.0);
+        for (int u = 0; i + j + u <= p; ++u) {
+            double2 v = src[tri(i, j + u, p)];
+            acc.x = fma(co[u], v.x, acc.x);
+            acc.y = fma(co[u], v.y, acc.y);
+        }
+        double2 *o = a.Lc + ((a.toff[level] + slot) * (int64_t)KW + n0) * P + e;
+        double2 cur = *o;
+        *o = make_double2(fma(0.5, acc.x, cur.x), fma(0.5, acc.y, cur.y));
+    }
+}
+
+inline size_t m2m_smem(int p)
+{
+    int P = (p + 1) * (p + 2) / 2;
+    return sizeof(double) * 4 * (p + 1) * (p + 1) + sizeof(double2) * 8 * kMMG * P + sizeof(int) * 2 * P;
+}
+inline size_t l2l_smem(int p)
+{
+    int P = (p + 1) * (p + 2) / 2;
+    return sizeof(double) * 4 * (p + 1) * (p + 1) + sizeof(double2) * 2 * kMMG * P + sizeof(int) * 2 * P;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -296,6 +368,7 @@ struct S2LCfg {
     static constexpr int TN = NT / TM;
     static constexpr int MP = TM * RM;          // padded rows (>= P)
     static constexpr int NC = TN * RN;          // columns = 2 JT (even-j boxes, then odd-j boxes)
+    static constexpr int NCP = NC + 2;          // smem row stride of B (breaks 512-B bank aliasing)
     static constexpr int JT = NC / 2;           // target boxes per CTA (JT/2 of each parity)
     static constexpr int JH = JT / 2;
     static constexpr int NOFF = 33;             // (dI, dJ) in [6] x [-3..3] minus the 9 near
@@ -358,7 +431,7 @@ template <int NT, int TM, int RM, int RN, int KC>
 __global__ void __launch_bounds__(NT) s2l_kernel(FarArgs a, S2LGrid gr)
 {
     using Cfg = S2LCfg<NT, TM, RM, RN, KC>;
-    constexpr int TN = Cfg::TN, MP = Cfg::MP, NC = Cfg::NC, JT = Cfg::JT, JH = Cfg::JH;
+    constexpr int TN = Cfg::TN, MP = Cfg::MP, NC = Cfg::NCP, JT = Cfg::JT, JH = Cfg::JH;
     constexpr int NOFF = Cfg::NOFF;
     constexpr int BOXV = TN / 2;                   // boxes per column block v
     extern __shared__ double sm[];
@@ -562,7 +635,7 @@ inline size_t s2l_smem_bytes(int p)
 {
     using Cfg = S2LCfg<NT, TM, RM, RN, KC>;
     int P = (p + 1) * (p + 2) / 2, TP = (p + 1) * (p + 1) * (p + 1), TPp = TP + (TP & 1);
-    return sizeof(double) * ((size_t)KC * Cfg::MP + 2 * (size_t)P * Cfg::NC + 2 * (TPp + 2) + P) +
+    return sizeof(double) * ((size_t)KC * Cfg::MP + 2 * (size_t)P * Cfg::NCP + 2 * (TPp + 2) + P) +
            sizeof(int) * (Cfg::JT + Cfg::NOFF * Cfg::JT + Cfg::NOFF + 1);
 }
 
