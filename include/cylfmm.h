@@ -69,7 +69,8 @@ typedef struct {
     int exclude_coincident; /* 1: skip bitwise-coincident pairs (R#15) */
     double domain_z0;       /* the square domain is [0, L] x [z0, z0 + L] (R#11) */
     double domain_L;        /* L > 0; a power of two keeps box indices bit-exact */
-    int mode_chunk;         /* far-field passes run over modes in chunks of this many; 0 = all */
+    int mode_chunk;         /* far-field passes run over modes in chunks of this many; 0 = auto
+                               (all modes if the workspace fits a third of free memory) */
 } cylfmm_params;
 
 /* Per-phase device times of the last solve, milliseconds (CUDA events on the solve stream). */

@@ -39,6 +39,8 @@ int or_legendre_q(double chi, double kp2, int forward, int nmax, int miller, dou
 /* 2 t_N of the forward/backward switch chi - 1 < t_N (R#3): 0.016 in the paper mode and for
  * nmax <= 16; 2 (cosh(ln 64 / (2 nmax)) - 1) beyond in the accurate mode. */
 double or_forward_coef(int nmax, int miller);
+/* Miller extra steps e(chi) beyond nmax (R#4); the backward recursion starts at nmax + e. */
+int or_miller_extra(double chi, int miller);
 /* G^(n)(r, r1, x), n = 0..nmax. Returns 0, or -1 if r<=0, r1<=0, coincident. */
 int or_greens(double r, double r1, double x, int nmax, int miller, double *G);
 

@@ -89,7 +89,7 @@ void or_ellip_ke(double kp2, double *K, double *E)
 /* Miller extra steps e in the accurate mode (R#4): the backward recursion started at n = N+e
  * contaminates Q_{n-1/2} by ~lambda^{-2(N+e-n)}, lambda = chi + sqrt(chi^2 - 1); we take
  * e = max(80, ceil(20 / ln lambda)) so that the contamination is below e^-40 ~ 4e-18. */
-static int miller_extra(double chi, int miller)
+int or_miller_extra(double chi, int miller)
 {
     if (miller == OR_MILLER_PAPER) return 80;
     double lam = chi + sqrt((chi - 1.0) * (chi + 1.0));
@@ -112,7 +112,7 @@ int or_legendre_q(double chi, double kp2, int forward, int nmax, int miller, dou
         return 0;
     }
     /* Miller: arbitrary seeds Qt[S] = 0, Qt[S-1] = 1 (R#4), recur down to n = 0. */
-    int S = nmax + miller_extra(chi, miller);
+    int S = nmax + or_miller_extra(chi, miller);
     double *Qt = (double *)calloc((size_t)S + 1, sizeof(double));
     if (!Qt) return -1;
     Qt[S] = 0.0;

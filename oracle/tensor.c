@@ -4,7 +4,19 @@
  *
  * Steps, in the paper's order (Appendix A):
  *   1. G^(n), n = 0..max(N,1)  (G^(-1) == G^(1) for n = 0).
- *   2. x-derivatives Gbar_{00,k+1} from (Gbar^n +- Gbar^{n-1}) d^q/dx^q (x/rho_+-^2).
+ *   2. x-derivatives Gbar_{00,c}, c <= 2p (reading R#22):
+ *      a. modes n = 0, 1 by the paper's x-recursion from (Gbar^n +- Gbar^{n-1}) d^q/dx^q
+ *         (x/rho_+-^2) (G^(-1) == G^(1));
+ *      b. modes n >= 2 by the three-term recursion applied to the Taylor series in
+ *         Delta x: chi(x + Delta) = chi + (x/(r r1)) Delta + Delta^2/(2 r r1) exactly, so
+ *         (2n-1) g_n = 4(n-1) chi(Delta) g_{n-1} - (2n-3) g_{n-2} holds coefficient-wise
+ *         (truncated series products).  Forward from g_0, g_1 on the paper's forward branch
+ *         (R#3); on the backward branch Miller's algorithm in ratio form
+ *         rho_n = g_n / g_{n-1}: rho_S = 0, rho_{n-1} = (2n-3) / (4(n-1) chi(Delta) - (2n-1) rho_n)
+ *         (series reciprocal), S = N + e(chi) as for G (R#4), then g_n = g_{n-1} rho_n.
+ *      The paper's cross-mode x-recursion for all n multiplies rounding errors by about
+ *      (n - 1/2)/(k+1) per order when n > k (measured: relative error 4e1 at n = 64, p = 16),
+ *      while the series recursion is as stable as the recursion for G itself.
  *   3. r-derivatives Gbar_{10k}.
  *   4. r1-derivatives Gbar_{01k} by exchanging r and r1.
  *   5. mixed Gbar_{11k}.
@@ -72,11 +84,12 @@ int or_tensor(double r, double r1, double x, int nmax, int p, int miller, double
     const double *tp = tab, *tm = tab + Q, *up = tab + 2 * Q, *um = tab + 3 * Q;
     const double *vp = tab + 4 * Q, *vm = tab + 5 * Q, *sp = tab + 6 * Q, *sm = tab + 7 * Q;
 #define A(arr, n, c) arr[(size_t)(n) * (C + 1) + (c)]
-    /* step 2: x-derivatives, order by order across all modes */
-    for (int n = 0; n <= Ni; ++n) A(g00, n, 0) = G[n];
+    /* step 2a: x-derivatives of modes 0 and 1, order by order */
+    A(g00, 0, 0) = G[0];
+    A(g00, 1, 0) = G[1];
     for (int k = 0; k < C; ++k) {
-        for (int n = 0; n <= Ni; ++n) {
-            int m = n == 0 ? 1 : n - 1;
+        for (int n = 0; n <= 1; ++n) {
+            int m = 1 - n; /* n = 0: G^(-1) == G^(1); n = 1: mode 0 */
             double s = 0.0;
             for (int q = 0; q <= k; ++q) {
                 double gp = A(g00, n, k - q) + A(g00, m, k - q);
@@ -84,6 +97,54 @@ int or_tensor(double r, double r1, double x, int nmax, int p, int miller, double
                 s += gp * tp[q] + gm * tm[q];
             }
             A(g00, n, k + 1) = (n - 0.5) * s / (k + 1);
+        }
+    }
+    /* step 2b: modes n >= 2 by the three-term recursion on Taylor series in Delta x (R#22) */
+    if (Ni >= 2) {
+        const double chi = (r * r + r1 * r1 + x * x) / (2.0 * r * r1);
+        double chis[3] = {chi, x / (r * r1), 1.0 / (2.0 * r * r1)}; /* chi(x + Delta) */
+        double rho_m2 = (r - r1) * (r - r1) + x * x;
+        int forward = rho_m2 < or_forward_coef(Ni, miller) * (r * r1); /* as in or_greens */
+        if (forward) {
+            for (int n = 2; n <= Ni; ++n)
+                for (int c = 0; c <= C; ++c) {
+                    double chig = 0.0; /* [chi(Delta) g_{n-1}]_c */
+                    for (int j = 0; j <= 2 && j <= c; ++j) chig += chis[j] * A(g00, n - 1, c - j);
+                    A(g00, n, c) = (4.0 * (n - 1) * chig - (2.0 * n - 3.0) * A(g00, n - 2, c)) /
+                                   (2.0 * n - 1.0);
+                }
+        } else {
+            int S = Ni + or_miller_extra(chi, miller);
+            double *rho = (double *)calloc((size_t)(C + 1), sizeof(double)); /* rho_S = 0 */
+            double *den = (double *)calloc((size_t)(C + 1), sizeof(double));
+            double *rat = (double *)calloc((size_t)(Ni + 1) * (C + 1), sizeof(double));
+            if (!rho || !den || !rat) {
+                free(rho);
+                free(den);
+                free(rat);
+                goto done;
+            }
+            for (int n = S; n >= 2; --n) {
+                /* den = 4(n-1) chi(Delta) - (2n-1) rho_n ; rho_{n-1} = (2n-3) / den */
+                for (int c = 0; c <= C; ++c)
+                    den[c] = (c <= 2 ? 4.0 * (n - 1) * chis[c] : 0.0) - (2.0 * n - 1.0) * rho[c];
+                for (int c = 0; c <= C; ++c) { /* series reciprocal, triangular */
+                    double s = (c == 0) ? (2.0 * n - 3.0) : 0.0;
+                    for (int j = 0; j < c; ++j) s -= rho[j] * den[c - j];
+                    rho[c] = s / den[0];
+                }
+                if (n - 1 <= Ni)
+                    for (int c = 0; c <= C; ++c) A(rat, n - 1, c) = rho[c];
+            }
+            for (int n = 2; n <= Ni; ++n) /* g_n = g_{n-1} rho_n */
+                for (int c = 0; c <= C; ++c) {
+                    double s = 0.0;
+                    for (int j = 0; j <= c; ++j) s += A(g00, n - 1, j) * A(rat, n, c - j);
+                    A(g00, n, c) = s;
+                }
+            free(rho);
+            free(den);
+            free(rat);
         }
     }
     /* steps 3, 4: r- and r1-derivatives */

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <mutex>
@@ -76,9 +77,19 @@ static cudaError_t allow_smem(F *kernel)
 #define P2P_INSTANCES(X)                                                                       \
     X(8, 16, 2) X(8, 16, 5) X(16, 8, 3) X(16, 8, 9) X(32, 4, 6) X(32, 4, 18)
 
-#define S2L_P8 128, 8, 6, 4, 48
-#define S2L_P12 256, 16, 6, 4, 32
-#define S2L_P16 256, 16, 10, 2, 32
+// S2L tilings (NT, TM, RM, RN, KC, stages); variant 0 of each order class is the default, the
+// others are selectable with CYLFMM_S2L_VARIANT for measurement (same MP = TM RM per class)
+#define S2L_P8 128, 8, 6, 4, 48, 2
+#define S2L_P8_V1 128, 8, 6, 4, 48, 1
+#define S2L_P8_V2 256, 8, 6, 2, 48, 1
+#define S2L_P8_V3 128, 4, 12, 2, 48, 1
+#define S2L_P12 256, 16, 6, 4, 32, 2
+#define S2L_P12_V1 256, 16, 6, 4, 16, 1
+#define S2L_P16 256, 16, 10, 2, 32, 2
+#define S2L_P16_V1 256, 16, 10, 2, 16, 1
+#define S2L_P16_V2 128, 16, 10, 2, 16, 1
+#define S2L_ALL(X) X(S2L_P8) X(S2L_P8_V1) X(S2L_P8_V2) X(S2L_P8_V3) X(S2L_P12) X(S2L_P12_V1) \
+    X(S2L_P16) X(S2L_P16_V1) X(S2L_P16_V2)
 
 static cylfmm_status ensure_init()
 {
@@ -102,9 +113,9 @@ static cylfmm_status ensure_init()
     CK(allow_smem(m2m_kernel));
     CK(allow_smem(l2l_kernel));
     CK(allow_smem(l2p_kernel));
-    CK(allow_smem(s2l_kernel<S2L_P8>));
-    CK(allow_smem(s2l_kernel<S2L_P12>));
-    CK(allow_smem(s2l_kernel<S2L_P16>));
+#define X(...) CK(allow_smem(s2l_kernel<__VA_ARGS__>));
+    S2L_ALL(X)
+#undef X
     if (dev < 64) g_init_done[dev] = true;
     return CYLFMM_OK;
 }
@@ -544,10 +555,10 @@ extern "C" cylfmm_status cylfmm_tree_sort(const double *r, const double *z, int6
 // FMM solve
 static int64_t pow4(int l) { return (int64_t)1 << (2 * l); }
 
-template <int NT, int TM, int RM, int RN, int KC>
+template <int NT, int TM, int RM, int RN, int KC, int ST>
 static cudaError_t launch_s2l_t(const FarArgs &fa, cudaStream_t st)
 {
-    using Cfg = S2LCfg<NT, TM, RM, RN, KC>;
+    using Cfg = S2LCfg<NT, TM, RM, RN, KC, ST>;
     S2LGrid gr = {};
     const int KW = fa.m1 - fa.m0;
     int64_t tot = 0;
@@ -563,14 +574,33 @@ static cudaError_t launch_s2l_t(const FarArgs &fa, cudaStream_t st)
     }
     gr.start[gr.nlev] = tot;
     if (tot == 0) return cudaSuccess;
-    size_t sm = s2l_smem_bytes<NT, TM, RM, RN, KC>(fa.p);
-    s2l_kernel<NT, TM, RM, RN, KC><<<(unsigned)tot, NT, sm, st>>>(fa, gr);
+    size_t sm = s2l_smem_bytes<NT, TM, RM, RN, KC, ST>(fa.p);
+    s2l_kernel<NT, TM, RM, RN, KC, ST><<<(unsigned)tot, NT, sm, st>>>(fa, gr);
     return cudaGetLastError();
+}
+static int s2l_variant()
+{
+    static int v = [] {
+        const char *e = getenv("CYLFMM_S2L_VARIANT");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
 }
 static cudaError_t launch_s2l(const FarArgs &fa, cudaStream_t st)
 {
-    if (fa.p <= 8) return launch_s2l_t<S2L_P8>(fa, st);
-    if (fa.p <= 12) return launch_s2l_t<S2L_P12>(fa, st);
+    const int v = s2l_variant();
+    if (fa.p <= 8) {
+        if (v == 1) return launch_s2l_t<S2L_P8_V1>(fa, st);
+        if (v == 2) return launch_s2l_t<S2L_P8_V2>(fa, st);
+        if (v == 3) return launch_s2l_t<S2L_P8_V3>(fa, st);
+        return launch_s2l_t<S2L_P8>(fa, st);
+    }
+    if (fa.p <= 12) {
+        if (v == 1) return launch_s2l_t<S2L_P12_V1>(fa, st);
+        return launch_s2l_t<S2L_P12>(fa, st);
+    }
+    if (v == 1) return launch_s2l_t<S2L_P16_V1>(fa, st);
+    if (v == 2) return launch_s2l_t<S2L_P16_V2>(fa, st);
     return launch_s2l_t<S2L_P16>(fa, st);
 }
 
@@ -613,7 +643,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
 {
     const cylfmm_params &q = p->prm;
     const int d = q.depth, K = q.n_modes, pp = q.order, P = (pp + 1) * (pp + 2) / 2;
-    const int KW = q.mode_chunk > 0 ? std::min(q.mode_chunk, K) : K;
+    int KW = q.mode_chunk > 0 ? std::min(q.mode_chunk, K) : K;
     p->launches = 0;
     PhaseTimer T{p, st, tm != nullptr};
     RET_IF(p->err.need(sizeof(int)));
@@ -707,6 +737,18 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     const int64_t TP = (int64_t)(pp + 1) * (pp + 1) * (pp + 1) + ((pp + 1) & 1);  // padded
     const int64_t nstat = (int64_t)12 << d;
     const int NM = std::max(K - 1, 1) + 1, D = 2 * pp + 1;
+    if (q.mode_chunk == 0) {
+        // automatic chunk: the far-field workspace (moments, locals, tensors per mode) of one
+        // chunk must fit in a third of the free device memory (C5: 1.8 GB per mode)
+        size_t fmem = 0, tot = 0;
+        CK(cudaMemGetInfo(&fmem, &tot));
+        size_t have = p->M.cap + p->Lc.cap + p->tens.cap;   // reusable current allocations
+        size_t per_mode = sizeof(double2) * (size_t)(stot + ttot) * P + sizeof(double) * nstat * TP;
+        size_t budget = (fmem + have) / 3;
+        int64_t kw = (int64_t)(budget / std::max<size_t>(per_mode, 1));
+        KW = (int)std::max<int64_t>(1, std::min<int64_t>(K, kw));
+        if (KW < K) KW = (K + (K + KW - 1) / KW - 1) / ((K + KW - 1) / KW);  // balanced chunks
+    }
     RET_IF(p->M.need(sizeof(double2) * (size_t)std::max<int64_t>(stot, 1) * KW * P));
     RET_IF(p->Lc.need(sizeof(double2) * (size_t)std::max<int64_t>(ttot, 1) * KW * P));
     RET_IF(p->tens.need(sizeof(double) * (size_t)nstat * KW * TP));

@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(256) l2p_kernel(FarArgs a)
 // The JT source boxes' moments (2 JT real columns, pre-scaled by (-1)^j/j!) are multiplied on
 // the CUDA cores by a register-tiled FP64 GEMM; outputs accumulate in registers over the offsets
 // in a fixed order (deterministic) and are post-scaled by 1/l! on the write.
-template <int NT, int TM, int RM, int RN, int KC>
+template <int NT, int TM, int RM, int RN, int KC, int ST = 2>
 struct S2LCfg {
     static constexpr int TN = NT / TM;
     static constexpr int MP = TM * RM;          // padded rows (>= P)
@@ -372,6 +372,7 @@ struct S2LCfg {
     static constexpr int JT = NC / 2;           // target boxes per CTA (JT/2 of each parity)
     static constexpr int JH = JT / 2;
     static constexpr int NOFF = 33;             // (dI, dJ) in [6] x [-3..3] minus the 9 near
+    static constexpr int STAGES = ST;           // 2: next offset staged behind the GEMM; 1: not
 };
 
 struct S2LGrid {
@@ -427,10 +428,10 @@ __device__ __forceinline__ void s2l_gemm_dispatch(int mask, const double *As, co
     }
 }
 
-template <int NT, int TM, int RM, int RN, int KC>
+template <int NT, int TM, int RM, int RN, int KC, int ST>
 __global__ void __launch_bounds__(NT) s2l_kernel(FarArgs a, S2LGrid gr)
 {
-    using Cfg = S2LCfg<NT, TM, RM, RN, KC>;
+    using Cfg = S2LCfg<NT, TM, RM, RN, KC, ST>;
     constexpr int TN = Cfg::TN, MP = Cfg::MP, NC = Cfg::NCP, JT = Cfg::JT, JH = Cfg::JH;
     constexpr int NOFF = Cfg::NOFF;
     constexpr int BOXV = TN / 2;                   // boxes per column block v
@@ -439,8 +440,8 @@ __global__ void __launch_bounds__(NT) s2l_kernel(FarArgs a, S2LGrid gr)
     const int TP = (p + 1) * (p + 1) * (p + 1), TPp = TP + (TP & 1), HST = TPp + 2;
     double *As = sm;                               // [KC][MP]
     double *Bs0 = As + KC * MP;                    // 2 x [P][NC]
-    double *Hs0 = Bs0 + 2 * P * NC;                // 2 x [HST], Hs[TPp] = 0 (masked entries)
-    double *post = Hs0 + 2 * HST;                  // [P] 1 / l!
+    double *Hs0 = Bs0 + ST * P * NC;               // ST x [HST], Hs[TPp] = 0 (masked entries)
+    double *post = Hs0 + ST * HST;                 // [P] 1 / l!
     int *tsl = reinterpret_cast<int *>(post + P);  // [JT]  (box b: parity b / JH, index b % JH)
     int *ssl = tsl + JT;                           // [NOFF][JT]
     int *olist = ssl + NOFF * JT;                  // [NOFF] active offsets
@@ -487,7 +488,7 @@ __global__ void __launch_bounds__(NT) s2l_kernel(FarArgs a, S2LGrid gr)
         for (int t = 2; t <= l; ++t) f *= t;
         post[q] = 1.0 / f;
     }
-    if (tid < 2) Hs0[tid * HST + TPp] = 0.0;
+    if (tid < ST) Hs0[tid * HST + TPp] = 0.0;
     __syncthreads();
     for (int q = tid; q < NOFF * JT; q += NT) {
         int o = q / JT, b = q % JT;
@@ -527,15 +528,15 @@ __global__ void __launch_bounds__(NT) s2l_kernel(FarArgs a, S2LGrid gr)
 #pragma unroll
         for (int v = 0; v < RN; ++v) acc[u][v] = 0.0;
 
-    // async stage of offset k into buffer (k & 1): tensor block + (pre-scaled) moments
+    // async stage of offset k into buffer (k % ST): tensor block + (pre-scaled) moments
     auto stage = [&](int k) {
         const int code = olist[k];
         const int di = ((code >> 4) & 15) - 3, dj = (code & 15) - 3, o = (code >> 8) & 0xff;
         const int is = it + di;
         const int iin = min(it, is), dI = di < 0 ? -di : di, dJ = dj < 0 ? -dj : dj;
         const double *Tn = a.tens + ((int64_t)(iin * 12 + class_of(dI, dJ)) * KW + nloc) * TPp;
-        double *Hs = Hs0 + (k & 1) * HST;
-        double *Bs = Bs0 + (k & 1) * P * NC;
+        double *Hs = Hs0 + (k % ST) * HST;
+        double *Bs = Bs0 + (k % ST) * P * NC;
         for (int q = tid; q < TPp / 2; q += NT) cp_async16(Hs + 2 * q, Tn + 2 * q, true);
         for (int q = tid; q < P * JT; q += NT) {
             int b = q / P, kk = q % P;
@@ -545,18 +546,22 @@ __global__ void __launch_bounds__(NT) s2l_kernel(FarArgs a, S2LGrid gr)
         }
         cp_async_commit();
     };
-    if (na > 0) stage(0);
+    if (ST == 2 && na > 0) stage(0);
     for (int k = 0; k < na; ++k) {
+        if (ST == 1) {
+            if (k > 0) __syncthreads();       // GEMM k-1 done with the single buffer
+            stage(k);
+        }
         cp_async_wait_all();
         __syncthreads();                      // buffer k ready; As free
-        if (k + 1 < na) stage(k + 1);         // overlaps the operator build and GEMM below
+        if (ST == 2 && k + 1 < na) stage(k + 1);   // overlaps the operator build and GEMM below
         const int code = olist[k];
         const int di = ((code >> 4) & 15) - 3, dj = (code & 15) - 3;
         const int mask = (code >> 16) & 0xff;
         const int variant = (di <= 0 ? 0 : 2) + (dj <= 0 ? 0 : 1);   // FO, BO, FI, BI
         const int *itab = a.s2l_idx + (size_t)variant * P * MP;
-        const double *Hs = Hs0 + (k & 1) * HST;
-        const double *Bs = Bs0 + (k & 1) * P * NC;
+        const double *Hs = Hs0 + (k % ST) * HST;
+        const double *Bs = Bs0 + (k % ST) * P * NC;
         for (int k0 = 0; k0 < P; k0 += KC) {
             const int kc = min(KC, P - k0);
             if (k0 > 0) __syncthreads();
@@ -630,12 +635,12 @@ __global__ void prescale_moments_kernel(double2 *M, int64_t nrows, int p, int P)
     M[e] = make_double2(v.x * f, v.y * f);
 }
 
-template <int NT, int TM, int RM, int RN, int KC>
+template <int NT, int TM, int RM, int RN, int KC, int ST>
 inline size_t s2l_smem_bytes(int p)
 {
-    using Cfg = S2LCfg<NT, TM, RM, RN, KC>;
+    using Cfg = S2LCfg<NT, TM, RM, RN, KC, ST>;
     int P = (p + 1) * (p + 2) / 2, TP = (p + 1) * (p + 1) * (p + 1), TPp = TP + (TP & 1);
-    return sizeof(double) * ((size_t)KC * Cfg::MP + 2 * (size_t)P * Cfg::NCP + 2 * (TPp + 2) + P) +
+    return sizeof(double) * ((size_t)KC * Cfg::MP + ST * (size_t)P * Cfg::NCP + ST * (TPp + 2) + P) +
            sizeof(int) * (Cfg::JT + Cfg::NOFF * Cfg::JT + Cfg::NOFF + 1);
 }
 

@@ -135,3 +135,44 @@ def test_tensor_laplace_residual(orc):
                            + (a * a - n * n) * g(a, c)
                            + (c + 1) * (c + 2) * (r * r * g(a, c + 2) + 2 * r * g(a - 1, c + 2) + g(a - 2, c + 2)))
                     assert abs(res) <= 1e-11 * om[n, a + b + c] * (1 + a + c) ** 2 * r * r
+
+
+@pytest.mark.parametrize("geom", [(6.5, 3.5, 3.0), (2.5, 0.5, 1.0)])
+def test_tensor_high_mode_x_derivatives_vs_mpmath(orc, geom):
+    """Step 2b (reading R#22): Gbar^n_{00c} for modes far above the derivative order, against
+    mpmath's differentiation of Q_{n-1/2}(chi(x)) in x (the definition).  The
+    paper's cross-mode x-recursion alone fails this by many orders of magnitude at n = 40."""
+    mp.mp.dps = 60
+    r, r1, x = geom
+    p = 6
+    T = orc.tensor(r, r1, x, 40, p)
+    for n in (2, 17, 40):
+        f = _G_mp(n)
+        cs = list(range(0, 2 * p + 1, 3))
+        refs = [float(mp.diff(lambda t: f(mp.mpf(r), mp.mpf(r1), t), mp.mpf(x), c) / mp.factorial(c))
+                for c in cs]
+        # per-mode scale: the largest coefficient checked (isolated entries can vanish by
+        # symmetry, e.g. Re (x + i a)^-6 = 0 at x = a, so entry-wise relative error is no measure)
+        scale = max(abs(v) for v in refs)
+        for c, ref in zip(cs, refs):
+            assert abs(T[n, 0, 0, c] - ref) <= 1e-12 * scale, (n, c, T[n, 0, 0, c], ref)
+
+
+@pytest.mark.parametrize("geom", [(130.5, 128.5, 2.0), (20.5, 17.5, 3.0), (3.5, 1.5, 2.0)])
+def test_tensor_all_modes_vs_exact_recursion(orc, geom):
+    """The whole tensor for K = 49 modes at p = 12 against the same recursions evaluated with
+    100 significant digits (tests/hp_tensor.py), where their rounding amplification (up to
+    ~1e22 at high modes) is harmless: the 100-digit values are the exact Taylor coefficients to
+    far below FP64 rounding.  Per mode, in the S2L weighting (entry (a, b, c) scaled by 2^-(a+b))."""
+    from tests.hp_tensor import hp_tensor
+    r, r1, x = geom
+    p, nmax = 12, 48
+    E = hp_tensor(r, r1, x, nmax, p, dps=100)
+    O = orc.tensor(r, r1, x, nmax, p)
+    a = np.arange(p + 1)[:, None, None]
+    b = np.arange(p + 1)[None, :, None]
+    c = np.arange(2 * p + 1)[None, None, :]
+    w = 2.0 ** -(a + b) * ((a + b + c) <= 2 * p)
+    for n in range(nmax + 1):
+        err = np.abs((O[n] - E[n]) * w).max() / np.abs(E[n] * w).max()
+        assert err <= 2e-12, (n, err)
