@@ -13,7 +13,9 @@
  *         (truncated series products).  Forward from g_0, g_1 on the paper's forward branch
  *         (R#3); on the backward branch Miller's algorithm in ratio form
  *         rho_n = g_n / g_{n-1}: rho_S = 0, rho_{n-1} = (2n-3) / (4(n-1) chi(Delta) - (2n-1) rho_n)
- *         (series reciprocal), S = N + e(chi) as for G (R#4), then g_n = g_{n-1} rho_n.
+ *         (series reciprocal), then g_n = g_{n-1} rho_n.  Start S = N + e with e from R#4
+ *         applied to the worst point of the unit disk in Delta (the Taylor coefficients must be
+ *         converged over the S2L offsets |Delta| <= 1, not only at Delta = 0).
  *      The paper's cross-mode x-recursion for all n multiplies rounding errors by about
  *      (n - 1/2)/(k+1) per order when n > k (measured: relative error 4e1 at n = 64, p = 16),
  *      while the series recursion is as stable as the recursion for G itself.
@@ -114,7 +116,23 @@ int or_tensor(double r, double r1, double x, int nmax, int p, int miller, double
                                    (2.0 * n - 1.0);
                 }
         } else {
-            int S = Ni + or_miller_extra(chi, miller);
+            /* start: the contamination lambda^{-2(S-n)} must be small over the whole disk
+             * |Delta| <= 1 (one box size: the S2L offsets) whose Taylor coefficients we need, not
+             * just at Delta = 0 (R#22): e = max(80, ceil(20 / m)), m = min over |Delta| = 1 of
+             * ln|lambda(chi(x + Delta))| (harmonic, so the minimum is on the circle; 256 points) */
+            int e = or_miller_extra(chi, miller);
+            if (miller != OR_MILLER_PAPER) {
+                double m = HUGE_VAL;
+                for (int k = 0; k < 256; ++k) {
+                    double complex d = cexp(I * (2.0 * M_PI * k / 256.0));
+                    double complex z = (r * r + r1 * r1 + (x + d) * (x + d)) / (2.0 * r * r1);
+                    double v = fabs(log(cabs(z + csqrt(z * z - 1.0))));
+                    if (v < m) m = v;
+                }
+                double es = ceil(20.0 / m);
+                if (es > e) e = (int)es;
+            }
+            int S = Ni + e;
             double *rho = (double *)calloc((size_t)(C + 1), sizeof(double)); /* rho_S = 0 */
             double *den = (double *)calloc((size_t)(C + 1), sizeof(double));
             double *rat = (double *)calloc((size_t)(Ni + 1) * (C + 1), sizeof(double));

@@ -4,9 +4,11 @@
 //
 // Two kernels:
 //  tensor_seed_kernel  (one CTA per geometry): G^(n), n = 0..max(N,1) (specfun.cuh); the Taylor
-//     tables of the rational kernels from z_+- = 1/(x - i a_+-) (R#7); the x-recursion
-//     Gbar_{00,k+1} across modes (G^(-1) == G^(1) for n = 0); Gbar_{10k}, Gbar_{01k}
-//      and the mixed Gbar_{11k}.  Output: seeds[geom][4][Ni+1][2p+1].
+//     tables of the rational kernels from z_+- = 1/(x - i a_+-) (R#7); the x-derivatives
+//     Gbar_{00,c}: modes 0, 1 by the paper's x-recursion (G^(-1) == G^(1)), modes
+//     n >= 2 by the three-term recursion on Taylor series in Delta x, forward or Miller-ratio
+//     (reading R#22); Gbar_{10k}, Gbar_{01k} and the mixed Gbar_{11k}
+//     (P:993-1025).  Output: seeds[geom][4][Ni+1][2p+1].
 //  tensor_fill_kernel  (one CTA per (geometry, mode)): the whole tensor of one mode in shared
 //     memory from the seeds by the cylindrical Laplace equation, first in r (b in {0,1}) then in
 //     r1, with the axial term the printed recursion omits restored (R#6):
@@ -83,6 +85,9 @@ __global__ void __launch_bounds__(128) tensor_seed_kernel(TensorGeomArgs a)
     double *g10 = g00 + NM * D;
     double *g01 = g10 + NM * D;
     double *g11 = g01 + NM * D;
+    double *rat = g11 + (NM * D > 8 * Q ? NM * D : 8 * Q);   // [NM][D] Miller ratio series
+    double *rho = rat + NM * D;                              // [D]
+    double *den = rho + D;                                   // [D]
     const int64_t gi = blockIdx.x;
     double r, r1, x;
     geometry_of(a, gi, r, r1, x);
@@ -145,19 +150,116 @@ __global__ void __launch_bounds__(128) tensor_seed_kernel(TensorGeomArgs a)
     __syncthreads();
     const double *tp = tab, *tm = tab + Q, *up = tab + 2 * Q, *um = tab + 3 * Q;
     const double *sp = tab + 4 * Q, *smn = tab + 5 * Q, *vp = tab + 6 * Q, *vm = tab + 7 * Q;
-    // x-recursion, in the paper's form with (Gbar^n +- Gbar^{n-1}) formed first:
+    // x-derivatives (reading R#22).  Modes 0 and 1: the paper's x-recursion with
+    // (Gbar^n +- Gbar^{n-1}) formed first, G^(-1) == G^(1):
     //   Gbar_{00,k+1}^n = (n - 1/2)/(k+1) sum_q [(g_n + g_m)[k-q] t+_q + (g_n - g_m)[k-q] t-_q]
-    for (int k = 0; k < C; ++k) {
-        for (int n = tid; n < NM; n += blockDim.x) {
-            int m = n == 0 ? 1 : n - 1;
+    if (tid < 2) {
+        const int n = tid, m = 1 - tid;
+        for (int k = 0; k < C; ++k) {
             double s = 0.0;
             for (int q = 0; q <= k; ++q) {
                 double gn = g00[n * D + k - q], gm = g00[m * D + k - q];
                 s = fma(gn + gm, tp[q], fma(gn - gm, tm[q], s));
             }
+            __syncwarp(0x3u);
             g00[n * D + k + 1] = (n - 0.5) * s / (k + 1);
+            __syncwarp(0x3u);
         }
-        __syncthreads();
+    }
+    __syncthreads();
+    // Modes n >= 2: the three-term recursion on the Taylor series in Delta x, with
+    // chi(x + Delta) = chi + (x / (r r1)) Delta + Delta^2 / (2 r r1) exactly; the x-recursion
+    // for all modes amplifies rounding by ~(n - 1/2)/(k+1) per order when n > k.
+    if (Ni >= 2) {
+        const double chi0 = 0.5 * (geo.rp2 + geo.rm2) / (2.0 * geo.rr1);
+        const double ch1 = x / geo.rr1, ch2 = 0.5 / geo.rr1;
+        if (geo.forward) {
+            // forward from g_0, g_1: lane c owns coefficient c
+            for (int n = 2; n <= Ni; ++n) {
+                if (tid < D) {
+                    const double *g1 = g00 + (n - 1) * D, *g2 = g00 + (n - 2) * D;
+                    double cg = chi0 * g1[tid];
+                    if (tid >= 1) cg = fma(ch1, g1[tid - 1], cg);
+                    if (tid >= 2) cg = fma(ch2, g1[tid - 2], cg);
+                    g00[n * D + tid] = (4.0 * (n - 1) * cg - (2.0 * n - 3.0) * g2[tid]) / (2.0 * n - 1.0);
+                }
+                __syncthreads();
+            }
+        } else {
+            // Miller in ratio form: rho_S = 0,
+            //   rho_{n-1} = (2n-3) / (4(n-1) chi(Delta) - (2n-1) rho_n)   (series reciprocal),
+            // S = N + e(chi) as for G (R#4); then g_n = g_{n-1} rho_n.
+            // start: the contamination lambda^{-2(S-n)} must be small on the whole disk
+            // |Delta| <= 1 (the S2L offsets) whose Taylor coefficients are used, so e follows from
+            // the minimum of ln|lambda(chi(x + Delta))| on the circle |Delta| = 1 (harmonic)
+            double mloc = 1e300;
+            for (int k = tid; k < 256; k += blockDim.x) {
+                double sn, cs;
+                sincospi(k / 128.0, &sn, &cs);
+                const double xr = x + cs, xi = sn;              // x + Delta
+                const double inv2 = 0.5 / geo.rr1;
+                const double zr = (r * r + r1 * r1 + xr * xr - xi * xi) * inv2, zi = 2.0 * xr * xi * inv2;
+                // w = z + sqrt(z^2 - 1), |ln|w|| (either root gives the same modulus of the log)
+                const double ar = zr * zr - zi * zi - 1.0, ai = 2.0 * zr * zi;
+                const double md = hypot(ar, ai);
+                double sr_ = sqrt(0.5 * (md + fabs(ar))), si_ = ai / (2.0 * (sr_ > 0.0 ? sr_ : 1.0));
+                if (ar < 0.0) {
+                    const double t = fabs(si_);
+                    si_ = ai >= 0.0 ? sr_ : -sr_;
+                    sr_ = t;
+                }
+                const double v = fabs(log(hypot(zr + sr_, zi + si_)));
+                mloc = fmin(mloc, v);
+            }
+            for (int o = 16; o > 0; o >>= 1) mloc = fmin(mloc, __shfl_xor_sync(0xffffffffu, mloc, o));
+            if ((tid & 31) == 0) den[tid >> 5] = mloc;
+            __syncthreads();
+            if (tid == 0) {
+                double m = den[0];
+                for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmin(m, den[w]);
+                int e = miller_extra(geo, a.miller);
+                if (a.miller != 1) {
+                    const double es = ceil(20.0 / (0.97 * m)) + 4.0;
+                    const double cap = (double)(kMaxSteps - kMaxModes - 4);
+                    e = max(e, (int)fmin(es, cap));
+                }
+                const int S = (a.K - 1 > Ni ? a.K - 1 : Ni) + e;
+                for (int c = 0; c < D; ++c) rho[c] = 0.0;
+                for (int n = S; n >= 2; --n) {
+                    const double a4 = 4.0 * (n - 1), b2 = 2.0 * n - 1.0;
+                    den[0] = fma(a4, chi0, -b2 * rho[0]);
+                    if (D > 1) den[1] = fma(a4, ch1, -b2 * rho[1]);
+                    if (D > 2) den[2] = fma(a4, ch2, -b2 * rho[2]);
+                    for (int c = 3; c < D; ++c) den[c] = -b2 * rho[c];
+                    const double inv = 1.0 / den[0];
+                    rho[0] = (2.0 * n - 3.0) * inv;
+                    for (int c = 1; c < D; ++c) {
+                        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+                        int j = 0;
+                        for (; j + 3 < c; j += 4) {
+                            s0 = fma(rho[j], den[c - j], s0);
+                            s1 = fma(rho[j + 1], den[c - j - 1], s1);
+                            s2 = fma(rho[j + 2], den[c - j - 2], s2);
+                            s3 = fma(rho[j + 3], den[c - j - 3], s3);
+                        }
+                        for (; j < c; ++j) s0 = fma(rho[j], den[c - j], s0);
+                        rho[c] = -((s0 + s1) + (s2 + s3)) * inv;
+                    }
+                    if (n - 1 <= Ni)
+                        for (int c = 0; c < D; ++c) rat[(n - 1) * D + c] = rho[c];
+                }
+            }
+            __syncthreads();
+            for (int n = 2; n <= Ni; ++n) {
+                if (tid < D) {
+                    const double *g1 = g00 + (n - 1) * D, *rn = rat + n * D;
+                    double s = 0.0;
+                    for (int j = 0; j <= tid; ++j) s = fma(g1[j], rn[tid - j], s);
+                    g00[n * D + tid] = s;
+                }
+                __syncthreads();
+            }
+        }
     }
     // r and r1 derivatives
     for (int e = tid; e < NM * C; e += blockDim.x) {
@@ -204,7 +306,7 @@ inline size_t tensor_seed_smem(int K, int m1, int p)
     size_t g11 = (size_t)NM * D;
     if (g11 < (size_t)8 * Q) g11 = 8 * Q;
     (void)K;
-    return sizeof(double) * (NM + 8 * Q + 3 * (size_t)NM * D + g11);
+    return sizeof(double) * (NM + 8 * Q + 3 * (size_t)NM * D + g11 + (size_t)NM * D + 2 * D + 4);
 }
 
 // packed offset of (a, b) for order p (host/device helper used by S2L)

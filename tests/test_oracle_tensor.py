@@ -158,7 +158,8 @@ def test_tensor_high_mode_x_derivatives_vs_mpmath(orc, geom):
             assert abs(T[n, 0, 0, c] - ref) <= 1e-12 * scale, (n, c, T[n, 0, 0, c], ref)
 
 
-@pytest.mark.parametrize("geom", [(130.5, 128.5, 2.0), (20.5, 17.5, 3.0), (3.5, 1.5, 2.0)])
+@pytest.mark.parametrize("geom", [(130.5, 128.5, 2.0), (20.5, 17.5, 3.0), (3.5, 1.5, 2.0),
+                                  (10.5, 10.5, 2.0), (11.5, 10.5, 2.0)])
 def test_tensor_all_modes_vs_exact_recursion(orc, geom):
     """The whole tensor for K = 49 modes at p = 12 against the same recursions evaluated with
     100 significant digits (tests/hp_tensor.py), where their rounding amplification (up to
