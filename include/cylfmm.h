@@ -160,6 +160,25 @@ cylfmm_status cylfmm_tree_sort(const double *r, const double *z, int64_t n, int 
                                double L, double z0, uint32_t *key, int32_t *perm,
                                cylfmm_stream_t stream);
 
+/* Field-point partition for a multi-GPU solve (BASELINE north_star: "field points are
+ * partitioned across the GPUs ... sources and the upper tree replicated").
+ * HOST-only (no device needed): every rank calls it with the same replicated inputs and gets
+ * the same answer.  Target leaves of the depth-prm->depth tree (box rule R#11) are cut, in
+ * Morton order, into n_parts contiguous ranges of equal estimated cost
+ *     cost(leaf) = n_t * [ (sum over the 9 neighbour leaves of n_s) * (200 + 9 K)   near field
+ *                          + 4 P K ]                                                L2P
+ *                + (non-empty source boxes in the leaf's S2L list) * 4 P^2 K        S2L
+ * (P = (p+1)(p+2)/2; SURVEY 8(d) work per unit), and every field point gets the part of its
+ * leaf.  part (HOST, int32 [n_fld], out): part index in [0, n_parts) of each field point, input
+ * order.  part_cost (HOST, double [n_parts], out, nullable): estimated flops per part.
+ * Errors: EINVAL (null pointers, n_parts < 1, bad params), EDOMAIN (point outside the domain).
+ * Because the FMM result at a field point depends only on the sources and on its own box
+ * chain, solving each part separately gives bitwise the same values as one solve. */
+cylfmm_status cylfmm_partition_fields(const double *src_r, const double *src_z, int64_t n_src,
+                                      const double *fld_r, const double *fld_z, int64_t n_fld,
+                                      const cylfmm_params *prm, int n_parts, int32_t *part,
+                                      double *part_cost);
+
 #ifdef __cplusplus
 }
 #endif

@@ -117,14 +117,15 @@ int or_tensor(double r, double r1, double x, int nmax, int p, int miller, double
                 }
         } else {
             /* start: the contamination lambda^{-2(S-n)} must be small over the whole disk
-             * |Delta| <= 1 (one box size: the S2L offsets) whose Taylor coefficients we need, not
-             * just at Delta = 0 (R#22): e = max(80, ceil(20 / m)), m = min over |Delta| = 1 of
-             * ln|lambda(chi(x + Delta))| (harmonic, so the minimum is on the circle; 256 points) */
+             * |Delta| <= rho_-/2 whose Taylor coefficients the S2L offsets use (|Delta| <= h and
+             * rho_- >= 2h for every S2L pair), not just at Delta = 0 (R#22):
+             * e = max(80, ceil(20 / m)), m = min over |Delta| = rho_-/2 of ln|lambda(chi(x + Delta))|
+             * (harmonic, so the minimum is on the circle; 256 points) */
             int e = or_miller_extra(chi, miller);
             if (miller != OR_MILLER_PAPER) {
-                double m = HUGE_VAL;
+                double m = HUGE_VAL, R = 0.5 * sqrt(rho_m2);
                 for (int k = 0; k < 256; ++k) {
-                    double complex d = cexp(I * (2.0 * M_PI * k / 256.0));
+                    double complex d = R * cexp(I * (2.0 * M_PI * k / 256.0));
                     double complex z = (r * r + r1 * r1 + (x + d) * (x + d)) / (2.0 * r * r1);
                     double v = fabs(log(cabs(z + csqrt(z * z - 1.0))));
                     if (v < m) m = v;

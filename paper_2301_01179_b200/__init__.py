@@ -2,5 +2,5 @@
 quadtree FMM of arXiv 2301.01179.  The compute path is libcylfmm.so (csrc/, include/cylfmm.h);
 this package is its ctypes binding plus the seeded input generators."""
 from .cylfmm import (MILLER_ACCURATE, MILLER_PAPER, TRUNC_DOUBLE, TRUNC_SINGLE, CylFMMError,  # noqa: F401
-                     FMMConfig, Plan, direct, greens_batch, header_functions, lib, tensor_batch,
-                     tree_sort)
+                     FMMConfig, Plan, direct, greens_batch, header_functions, lib,
+                     partition_fields, tensor_batch, tree_sort)

@@ -8,6 +8,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <cmath>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -79,17 +80,18 @@ static cudaError_t allow_smem(F *kernel)
 
 // S2L tilings (NT, TM, RM, RN, KC, stages); variant 0 of each order class is the default, the
 // others are selectable with CYLFMM_S2L_VARIANT for measurement (same MP = TM RM per class)
-#define S2L_P8 128, 8, 6, 4, 48, 2
-#define S2L_P8_V1 128, 8, 6, 4, 48, 1
-#define S2L_P8_V2 256, 8, 6, 2, 48, 1
-#define S2L_P8_V3 128, 4, 12, 2, 48, 1
-#define S2L_P12 256, 16, 6, 4, 32, 2
-#define S2L_P12_V1 256, 16, 6, 4, 16, 1
-#define S2L_P16 256, 16, 10, 2, 32, 2
-#define S2L_P16_V1 256, 16, 10, 2, 16, 1
-#define S2L_P16_V2 128, 16, 10, 2, 16, 1
+#define S2L_P8 128, 8, 6, 4, 48, 2, 0
+#define S2L_P8_V1 128, 8, 6, 4, 48, 1, 0
+#define S2L_P8_V2 128, 8, 6, 4, 48, 1, 1
+#define S2L_P8_V3 128, 8, 6, 4, 48, 2, 1
+#define S2L_P12 256, 16, 6, 4, 32, 2, 0
+#define S2L_P12_V1 256, 16, 6, 4, 16, 1, 0
+#define S2L_P12_V2 256, 16, 6, 4, 16, 1, 1
+#define S2L_P16 256, 16, 10, 2, 32, 2, 0
+#define S2L_P16_V1 256, 16, 10, 2, 16, 1, 0
+#define S2L_P16_V2 256, 16, 10, 2, 16, 1, 1
 #define S2L_ALL(X) X(S2L_P8) X(S2L_P8_V1) X(S2L_P8_V2) X(S2L_P8_V3) X(S2L_P12) X(S2L_P12_V1) \
-    X(S2L_P16) X(S2L_P16_V1) X(S2L_P16_V2)
+    X(S2L_P12_V2) X(S2L_P16) X(S2L_P16_V1) X(S2L_P16_V2)
 
 static cylfmm_status ensure_init()
 {
@@ -370,6 +372,8 @@ struct cylfmm_plan_s {
     DevBuf slstart, flstart, flags, smap, skeys, tmap, tkeys, counts;
     DevBuf M, Lc, tens, seeds;
     DevBuf tasks, ntasks, tcnt, toff;
+    DevBuf tflag, tpos, tiles, written;   // S2L tile compaction
+    DevBuf need;                          // lazy L2L flags
     DevBuf err, ctr;
     DevBuf s2lidx;   // S2L operator gather table for this plan's (p, truncation)
     // host-API staging
@@ -386,7 +390,7 @@ static void free_plan_bufs(cylfmm_plan p)
                      &p->scan_tmp[3], &p->sr_s, &p->sz_s, &p->S_s, &p->fr_s, &p->fz_s,
                      &p->slstart, &p->flstart, &p->flags, &p->smap, &p->skeys, &p->tmap,
                      &p->tkeys, &p->counts, &p->M, &p->Lc, &p->tens, &p->seeds, &p->tasks,
-                     &p->ntasks, &p->tcnt, &p->toff, &p->err, &p->ctr, &p->s2lidx, &p->h_sr, &p->h_sz,
+                     &p->ntasks, &p->tcnt, &p->toff, &p->tflag, &p->tpos, &p->tiles, &p->written, &p->need, &p->err, &p->ctr, &p->s2lidx, &p->h_sr, &p->h_sz,
                      &p->h_S, &p->h_fr, &p->h_fz, &p->h_out};
     for (DevBuf *b : all) b->release();
 }
@@ -555,28 +559,39 @@ extern "C" cylfmm_status cylfmm_tree_sort(const double *r, const double *z, int6
 // FMM solve
 static int64_t pow4(int l) { return (int64_t)1 << (2 * l); }
 
-template <int NT, int TM, int RM, int RN, int KC, int ST>
-static cudaError_t launch_s2l_t(const FarArgs &fa, cudaStream_t st)
+// S2L tiles of every level 2..depth: (column it, row tile jt of JH boxes per parity)
+static S2LGrid make_s2l_grid(int depth, int JH)
 {
-    using Cfg = S2LCfg<NT, TM, RM, RN, KC, ST>;
     S2LGrid gr = {};
-    const int KW = fa.m1 - fa.m0;
     int64_t tot = 0;
-    for (int l = 2; l <= fa.depth; ++l) {
-        if (fa.tcount[l] == 0) continue;
+    for (int l = 2; l <= depth; ++l) {
         int nb = 1 << l, half = std::max(nb / 2, 1);
-        int jtiles = (half + Cfg::JH - 1) / Cfg::JH;
+        int jtiles = (half + JH - 1) / JH;
         gr.level[gr.nlev] = l;
         gr.jtiles[gr.nlev] = jtiles;
         gr.start[gr.nlev] = tot;
-        tot += (int64_t)nb * jtiles * KW;
+        tot += (int64_t)nb * jtiles;
         gr.nlev++;
     }
     gr.start[gr.nlev] = tot;
-    if (tot == 0) return cudaSuccess;
-    size_t sm = s2l_smem_bytes<NT, TM, RM, RN, KC, ST>(fa.p);
-    s2l_kernel<NT, TM, RM, RN, KC, ST><<<(unsigned)tot, NT, sm, st>>>(fa, gr);
+    return gr;
+}
+
+template <int NT, int TM, int RM, int RN, int KC, int ST, int PF>
+static cudaError_t launch_s2l_t(const FarArgs &fa, int64_t ntiles, cudaStream_t st)
+{
+    using Cfg = S2LCfg<NT, TM, RM, RN, KC, ST, PF>;
+    const int KW = fa.m1 - fa.m0;
+    const S2LGrid gr = make_s2l_grid(fa.depth, Cfg::JH);
+    if (ntiles == 0) return cudaSuccess;
+    size_t sm = s2l_smem_bytes<NT, TM, RM, RN, KC, ST, PF>(fa.p);
+    s2l_kernel<NT, TM, RM, RN, KC, ST, PF><<<(unsigned)(ntiles * KW), NT, sm, st>>>(fa, gr);
     return cudaGetLastError();
+}
+template <int NT, int TM, int RM, int RN, int KC, int ST, int PF>
+static int s2l_jh_t()
+{
+    return S2LCfg<NT, TM, RM, RN, KC, ST, PF>::JH;
 }
 static int s2l_variant()
 {
@@ -586,23 +601,30 @@ static int s2l_variant()
     }();
     return v;
 }
-static cudaError_t launch_s2l(const FarArgs &fa, cudaStream_t st)
+#define S2L_DISPATCH(FN, ...)                                                                  \
+    do {                                                                                       \
+        const int v_ = s2l_variant();                                                          \
+        if (p <= 8) {                                                                          \
+            if (v_ == 1) return FN<S2L_P8_V1>(__VA_ARGS__);                                    \
+            if (v_ == 2) return FN<S2L_P8_V2>(__VA_ARGS__);                                    \
+            if (v_ == 3) return FN<S2L_P8_V3>(__VA_ARGS__);                                    \
+            return FN<S2L_P8>(__VA_ARGS__);                                                    \
+        }                                                                                      \
+        if (p <= 12) {                                                                         \
+            if (v_ == 1) return FN<S2L_P12_V1>(__VA_ARGS__);                                   \
+            if (v_ == 2) return FN<S2L_P12_V2>(__VA_ARGS__);                                   \
+            return FN<S2L_P12>(__VA_ARGS__);                                                   \
+        }                                                                                      \
+        if (v_ == 1) return FN<S2L_P16_V1>(__VA_ARGS__);                                       \
+        if (v_ == 2) return FN<S2L_P16_V2>(__VA_ARGS__);                                       \
+        return FN<S2L_P16>(__VA_ARGS__);                                                       \
+    } while (0)
+static cudaError_t launch_s2l(const FarArgs &fa, int64_t ntiles, cudaStream_t st)
 {
-    const int v = s2l_variant();
-    if (fa.p <= 8) {
-        if (v == 1) return launch_s2l_t<S2L_P8_V1>(fa, st);
-        if (v == 2) return launch_s2l_t<S2L_P8_V2>(fa, st);
-        if (v == 3) return launch_s2l_t<S2L_P8_V3>(fa, st);
-        return launch_s2l_t<S2L_P8>(fa, st);
-    }
-    if (fa.p <= 12) {
-        if (v == 1) return launch_s2l_t<S2L_P12_V1>(fa, st);
-        return launch_s2l_t<S2L_P12>(fa, st);
-    }
-    if (v == 1) return launch_s2l_t<S2L_P16_V1>(fa, st);
-    if (v == 2) return launch_s2l_t<S2L_P16_V2>(fa, st);
-    return launch_s2l_t<S2L_P16>(fa, st);
+    const int p = fa.p;
+    S2L_DISPATCH(launch_s2l_t, fa, ntiles, st);
 }
+static int s2l_jh(int p) { S2L_DISPATCH(s2l_jh_t); }
 
 struct PhaseTimer {
     cylfmm_plan p;
@@ -691,7 +713,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     RET_IF(p->skeys.need(sizeof(int) * ltot));
     RET_IF(p->tmap.need(sizeof(int) * ltot));
     RET_IF(p->tkeys.need(sizeof(int) * ltot));
-    RET_IF(p->counts.need(sizeof(int) * 2 * kMaxLevels));
+    RET_IF(p->counts.need(sizeof(int) * (2 * kMaxLevels + 1)));
     for (int side = 0; side < 2; ++side) {
         const int *ls = side == 0 ? p->slstart.as<int>() : p->flstart.as<int>();
         int *map = side == 0 ? p->smap.as<int>() : p->tmap.as<int>();
@@ -707,8 +729,35 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             p->launches += 2;
         }
     }
-    int hcnt[2 * kMaxLevels] = {0};
-    CK(cudaMemcpyAsync(hcnt, p->counts.p, sizeof(int) * 2 * kMaxLevels, cudaMemcpyDeviceToHost, st));
+    // S2L tiles with at least one interaction (sparse inputs: C4, C5) and the per-box
+    // "written by S2L" flags that L2L / L2P use instead of zero-initialised locals
+    const S2LGrid s2lgr = make_s2l_grid(d, s2l_jh(pp));
+    const int64_t ntiles_all = s2lgr.start[s2lgr.nlev];
+    RET_IF(p->tflag.need(sizeof(int) * std::max<int64_t>(ntiles_all, 1)));
+    RET_IF(p->tpos.need(sizeof(int) * std::max<int64_t>(ntiles_all, 1)));
+    RET_IF(p->tiles.need(sizeof(int) * std::max<int64_t>(ntiles_all, 1)));
+    RET_IF(p->written.need(std::max<int64_t>(ltot, 1)));
+    CK(cudaMemsetAsync(p->counts.as<int>() + 2 * kMaxLevels, 0, sizeof(int), st));
+    if (ntiles_all > 0) {
+        TileArgs ta = {};
+        for (int l = 2; l <= d; ++l) {
+            ta.smap[l] = p->smap.as<int>() + lvoff[l];
+            ta.tmap[l] = p->tmap.as<int>() + lvoff[l];
+            ta.lvoff[l] = lvoff[l];
+        }
+        s2l_tile_flags_kernel<<<nblk(ntiles_all * 32, 256), 256, 0, st>>>(
+            ta, s2lgr, s2l_jh(pp), p->tflag.as<int>(), p->written.as<unsigned char>());
+        CKL();
+        CK(cudaMemcpyAsync(p->tpos.p, p->tflag.p, sizeof(int) * ntiles_all, cudaMemcpyDeviceToDevice, st));
+        RET_IF(scan_excl(p, p->tpos.as<int>(), ntiles_all, st));
+        s2l_tile_emit_kernel<<<nblk(ntiles_all, 256), 256, 0, st>>>(
+            p->tflag.as<int>(), p->tpos.as<int>(), ntiles_all, p->tiles.as<int>(),
+            p->counts.as<int>() + 2 * kMaxLevels);
+        CKL();
+        p->launches += 2;
+    }
+    int hcnt[2 * kMaxLevels + 1] = {0};
+    CK(cudaMemcpyAsync(hcnt, p->counts.p, sizeof(int) * (2 * kMaxLevels + 1), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     RET_IF(check_err_flag(p, st));
     T.mark();  // 1: tree done
@@ -767,6 +816,10 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     fa.out = reinterpret_cast<double2 *>(out_Phi);
     fa.s2l_pairs = p->ctr.as<unsigned long long>() + 2;
     fa.s2l_idx = p->s2lidx.as<int>();
+    fa.s2l_tiles = p->tiles.as<int>();
+    fa.s2l_written = p->written.as<unsigned char>();
+    for (int l = 2; l <= d; ++l) fa.lvoff[l] = lvoff[l];
+    const int64_t ntiles_act = hcnt[2 * kMaxLevels];
     double ms_tensor = 0, ms_p2m = 0, ms_m2m = 0, ms_s2l = 0, ms_l2l = 0, ms_l2p = 0;
     cudaEvent_t e0 = p->ev[10], e1 = p->ev[11];
     auto tic = [&]() { if (tm) cudaEventRecord(e0, st); };
@@ -779,6 +832,15 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             acc += ms;
         }
     };
+    // lazy downward pass: which target locals are materialised (need_kernel, bottom-up)
+    RET_IF(p->need.need(std::max<int64_t>(ltot, 1)));
+    fa.need = p->need.as<unsigned char>();
+    for (int l = d; l >= 2; --l) {
+        if (fa.tcount[l] == 0) continue;
+        need_kernel<<<nblk(fa.tcount[l], 256), 256, 0, st>>>(fa, l, p->need.as<unsigned char>());
+        CKL();
+        p->launches++;
+    }
     for (int m0 = 0; m0 < K; m0 += KW) {
         fa.m0 = m0;
         fa.m1 = std::min(K, m0 + KW);
@@ -828,18 +890,18 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         }
         // S2L of every level in one launch (each level's contribution), then the L2L chain
         tic();
-        if (ns > 0) {
-            CK(launch_s2l(fa, st));
+        if (ns > 0 && ntiles_act > 0) {
+            CK(launch_s2l(fa, ntiles_act, st));
             p->launches++;
-        } else {
-            CK(cudaMemsetAsync(fa.Lc, 0, sizeof(double2) * (size_t)ttot * kw * P, st));
         }
         toc(ms_s2l);
         tic();
         for (int l = 3; l <= d; ++l) {
             if (fa.tcount[l] == 0) continue;
-            unsigned g = (unsigned)((int64_t)fa.tcount[l] * ((kw + kMMG - 1) / kMMG));
-            l2l_kernel<<<g, 256, l2l_smem(pp), st>>>(fa, l);
+            int64_t items = (int64_t)fa.tcount[l] * kw;
+            unsigned g = (unsigned)std::min<int64_t>((items + kL2LWarps - 1) / kL2LWarps,
+                                                     (int64_t)p->nsm * 8);
+            l2l_kernel<<<g, 32 * kL2LWarps, l2l_smem(pp), st>>>(fa, l);
             CKL();
             p->launches++;
         }
@@ -993,4 +1055,100 @@ extern "C" cylfmm_status cylfmm_fmm_solve_host(cylfmm_plan plan, const double *s
         CK(cudaMemcpyAsync(out_Phi, plan->h_out.p, 16 * (size_t)n_fld * K, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     return check_err_flag(plan, st);
+}
+
+// ------------------------------------------------------------------------------------------
+// host-side field partition for multi-GPU solves (include/cylfmm.h)
+static inline uint32_t host_morton(uint32_t ix, uint32_t iz)
+{
+    uint32_t k = 0;
+    for (int b = 0; b < 16; ++b) k |= ((ix >> b) & 1u) << (2 * b) | ((iz >> b) & 1u) << (2 * b + 1);
+    return k;
+}
+static inline bool host_box(double r, double z, int d, double L, double z0, uint32_t &ix, uint32_t &iz)
+{
+    if (!(r > 0.0) || !(r <= L) || !(z >= z0) || !(z <= z0 + L)) return false;
+    const double nb = (double)(1u << d);
+    uint32_t i = (uint32_t)std::floor(r * nb / L), j = (uint32_t)std::floor((z - z0) * nb / L);
+    const uint32_t m = (1u << d) - 1u;
+    ix = std::min(i, m);
+    iz = std::min(j, m);
+    return true;
+}
+
+extern "C" cylfmm_status cylfmm_partition_fields(const double *src_r, const double *src_z,
+                                                 int64_t n_src, const double *fld_r,
+                                                 const double *fld_z, int64_t n_fld,
+                                                 const cylfmm_params *prm, int n_parts,
+                                                 int32_t *part, double *part_cost)
+{
+    if (!prm || n_parts < 1 || n_src < 0 || n_fld < 0 || (n_src > 0 && (!src_r || !src_z)) ||
+        (n_fld > 0 && (!fld_r || !fld_z || !part)) || prm->depth < 2 ||
+        prm->depth > CYLFMM_MAX_DEPTH || prm->order < 1 || prm->n_modes < 1 || !(prm->domain_L > 0.0)) {
+        set_err("cylfmm_partition_fields: bad arguments");
+        return CYLFMM_EINVAL;
+    }
+    const int d = prm->depth, nb = 1 << d, K = prm->n_modes, p = prm->order;
+    const double L = prm->domain_L, z0 = prm->domain_z0, P = (p + 1) * (p + 2) / 2.0;
+    const size_t nleaf = (size_t)nb * nb;
+    std::vector<int64_t> ns(nleaf, 0), nt(nleaf, 0);
+    std::vector<uint32_t> fkey((size_t)n_fld);
+    for (int64_t i = 0; i < n_src; ++i) {
+        uint32_t ix, iz;
+        if (!host_box(src_r[i], src_z[i], d, L, z0, ix, iz)) {
+            set_err("cylfmm_partition_fields: source %lld outside the domain", (long long)i);
+            return CYLFMM_EDOMAIN;
+        }
+        ns[host_morton(ix, iz)]++;
+    }
+    for (int64_t j = 0; j < n_fld; ++j) {
+        uint32_t ix, iz;
+        if (!host_box(fld_r[j], fld_z[j], d, L, z0, ix, iz)) {
+            set_err("cylfmm_partition_fields: field point %lld outside the domain", (long long)j);
+            return CYLFMM_EDOMAIN;
+        }
+        fkey[j] = host_morton(ix, iz);
+        nt[fkey[j]]++;
+    }
+    // cost per target leaf, in Morton order
+    std::vector<double> cost(nleaf, 0.0);
+    const double wpair = 200.0 + 9.0 * K, wl2p = 4.0 * P * K, ws2l = 4.0 * P * P * K;
+    for (int ix = 0; ix < nb; ++ix)
+        for (int iz = 0; iz < nb; ++iz) {
+            const uint32_t k = host_morton((uint32_t)ix, (uint32_t)iz);
+            if (!nt[k]) continue;
+            double near = 0.0, far = 0.0;
+            for (int a = -1; a <= 1; ++a)
+                for (int c = -1; c <= 1; ++c) {
+                    int x = ix + a, z = iz + c;
+                    if (x >= 0 && z >= 0 && x < nb && z < nb)
+                        near += (double)ns[host_morton((uint32_t)x, (uint32_t)z)];
+                }
+            // S2L list at the leaf level: children of the parent's neighbours, not neighbours
+            const int px = ix >> 1, pz = iz >> 1;
+            for (int x = 2 * px - 2; x <= 2 * px + 3; ++x)
+                for (int z = 2 * pz - 2; z <= 2 * pz + 3; ++z) {
+                    if (x < 0 || z < 0 || x >= nb || z >= nb) continue;
+                    if (std::abs(x - ix) <= 1 && std::abs(z - iz) <= 1) continue;
+                    if (ns[host_morton((uint32_t)x, (uint32_t)z)]) far += ws2l;
+                }
+            cost[k] = (double)nt[k] * (near * wpair + wl2p) + far;
+        }
+    double total = 0.0;
+    for (double c : cost) total += c;
+    // contiguous Morton ranges: leaf k goes to part floor(n_parts * (prefix before k + c/2) / total)
+    std::vector<int32_t> leaf_part(nleaf, 0);
+    std::vector<double> pc((size_t)n_parts, 0.0);
+    double acc = 0.0;
+    for (size_t k = 0; k < nleaf; ++k) {
+        int q = total > 0.0 ? (int)((acc + 0.5 * cost[k]) / total * n_parts) : 0;
+        q = std::min(std::max(q, 0), n_parts - 1);
+        leaf_part[k] = q;
+        pc[(size_t)q] += cost[k];
+        acc += cost[k];
+    }
+    for (int64_t j = 0; j < n_fld; ++j) part[j] = leaf_part[fkey[j]];
+    if (part_cost)
+        for (int q = 0; q < n_parts; ++q) part_cost[q] = pc[(size_t)q];
+    return CYLFMM_OK;
 }

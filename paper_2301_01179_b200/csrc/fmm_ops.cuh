@@ -43,6 +43,10 @@ struct FarArgs {
     const double *tens;  // [12 * 2^d][KW][(p+1)^3] packed
     unsigned long long *s2l_pairs;  // counter of (source box, target box) applications
     const int *s2l_idx;  // [4][P][MP] operator gather table (build_s2l_index)
+    const int *s2l_tiles;               // compact list of S2L tiles with >= 1 interaction
+    const unsigned char *s2l_written;   // dense per level [lvoff[l] + key]: local written by S2L
+    int64_t lvoff[kMaxLevels];          // dense per-level offsets (level maps, s2l_written)
+    const unsigned char *need;          // dense per level: local materialised (see need_kernel)
 };
 
 __device__ __forceinline__ int tri(int i, int j, int p) { return i * (p + 1) - i * (i - 1) / 2 + j; }
@@ -230,21 +234,38 @@ __global__ void __launch_bounds__(256) m2m_kernel(FarArgs a, int level)
     }
 }
 
-__global__ void __launch_bounds__(256) l2l_kernel(FarArgs a, int level)
+// Lazy downward pass.  A target box's local is materialised only if it, or a target box below
+// it, receives an S2L contribution (need = written || any child needs); otherwise it equals the
+// re-centred local of its nearest materialised ancestor (L2L is an exact re-centring of a
+// degree-p polynomial), and L2P evaluates that ancestor's local directly.  Uniform
+// inputs (C2, C3) need every box; surface inputs (C5) skip L2L for most of the 700k boxes.
+__global__ void need_kernel(FarArgs a, int level, unsigned char *need)
+{
+    int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= a.tcount[level]) return;
+    const uint32_t key = (uint32_t)a.tkeys[level][s];
+    bool nd = a.s2l_written[a.lvoff[level] + key] != 0;
+    if (level < a.depth)
+        for (int c = 0; c < 4 && !nd; ++c) {
+            const uint32_t ck = 4 * key + c;
+            nd = a.tmap[level + 1][ck] >= 0 && need[a.lvoff[level + 1] + ck] != 0;
+        }
+    need[a.lvoff[level] + key] = nd ? 1 : 0;
+}
+
+// L2L, one warp per (child box, mode), grid-stride over the level's target boxes; separable
+// (r then z) binomial re-centring in normalised units with the tables in shared memory.
+constexpr int kL2LWarps = 8;
+__global__ void __launch_bounds__(32 * kL2LWarps) l2l_kernel(FarArgs a, int level)
 {
     extern __shared__ double sm[];
     const int p = a.p, P = a.P, KW = a.m1 - a.m0, P1 = p + 1;
-    const int ngrp = (KW + kMMG - 1) / kMMG;
-    const int slot = blockIdx.x / ngrp, n0 = (blockIdx.x % ngrp) * kMMG;
-    const int nm = min(kMMG, KW - n0);
     double *cm = sm, *cl = cm + 2 * P1 * P1;
-    double2 *par = reinterpret_cast<double2 *>(cl + 2 * P1 * P1);  // [nm][P]
-    double2 *T = par + kMMG * P;                                   // [nm][P]
-    int *tri_i = reinterpret_cast<int *>(T + kMMG * P);
+    int *tri_i = reinterpret_cast<int *>(cl + 2 * P1 * P1);
     int *tri_j = tri_i + P;
-    const uint32_t key = (uint32_t)a.tkeys[level][slot];
-    const int ps = a.tmap[level - 1][key >> 2];
-    const int sr = key & 1, sz = (key >> 1) & 1;
+    double2 *wbuf = reinterpret_cast<double2 *>(tri_j + P + 2 * (P & 1));   // 16-B aligned
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double2 *par = wbuf + warp * 2 * P, *T = par + P;
     recentre_tables(p, cm, cl, threadIdx.x, blockDim.x);
     for (int q = threadIdx.x; q < P; q += blockDim.x) {
         int i = 0;
@@ -252,47 +273,60 @@ __global__ void __launch_bounds__(256) l2l_kernel(FarArgs a, int level)
         tri_i[q] = i;
         tri_j[q] = q - (i * (p + 1) - i * (i - 1) / 2);
     }
-    for (int e = threadIdx.x; e < nm * P; e += blockDim.x)
-        par[e] = a.Lc[((a.toff[level - 1] + ps) * (int64_t)KW + n0) * P + e];
     __syncthreads();
-    for (int e = threadIdx.x; e < nm * P; e += blockDim.x) {
-        int n = e / P, im = e % P, i = tri_i[im], m = tri_j[im];
-        const double *co = cl + (sr * P1 + i) * P1;
-        const double2 *src = par + n * P;
-        double2 acc = make_double2(0.0, 0.0);
-        for (int q = 0; i + q + m <= p; ++q) {
-            double2 v = src[tri(i + q, m, p)];
-            acc.x = fma(co[q], v.x, acc.x);
-            acc.y = fma(co[q], v.y, acc.y);
+    const int64_t items = (int64_t)a.tcount[level] * KW;
+    for (int64_t it = (int64_t)blockIdx.x * kL2LWarps + warp; it < items;
+         it += (int64_t)gridDim.x * kL2LWarps) {
+        const int slot = (int)(it / KW), n = (int)(it % KW);
+        const uint32_t key = (uint32_t)a.tkeys[level][slot];
+        if (!a.need[a.lvoff[level] + key]) continue;
+        const int ps = a.tmap[level - 1][key >> 2];
+        const int sr = key & 1, sz = (key >> 1) & 1;
+        const bool child_w = a.s2l_written[a.lvoff[level] + key] != 0;
+        const bool par_ok = level - 1 > 2 || a.s2l_written[a.lvoff[level - 1] + (key >> 2)] != 0;
+        const double2 *pg = a.Lc + ((a.toff[level - 1] + ps) * (int64_t)KW + n) * P;
+        for (int e = lane; e < P; e += 32) par[e] = par_ok ? pg[e] : make_double2(0.0, 0.0);
+        __syncwarp();
+        for (int e = lane; e < P; e += 32) {
+            const int i = tri_i[e], m = tri_j[e];
+            const double *co = cl + (sr * P1 + i) * P1;
+            double2 acc = make_double2(0.0, 0.0);
+            for (int q = 0; i + q + m <= p; ++q) {
+                const double2 v = par[tri(i + q, m, p)];
+                acc.x = fma(co[q], v.x, acc.x);
+                acc.y = fma(co[q], v.y, acc.y);
+            }
+            T[e] = acc;
         }
-        T[e] = acc;
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < nm * P; e += blockDim.x) {
-        int n = e / P, ij = e % P, i = tri_i[ij], j = tri_j[ij];
-        const double *co = cl + (sz * P1 + j) * P1;
-        const double2 *src = T + n * P;
-        double2 acc = make_double2(0.0, 0.0);
-        for (int u = 0; i + j + u <= p; ++u) {
-            double2 v = src[tri(i, j + u, p)];
-            acc.x = fma(co[u], v.x, acc.x);
-            acc.y = fma(co[u], v.y, acc.y);
+        __syncwarp();
+        double2 *o = a.Lc + ((a.toff[level] + slot) * (int64_t)KW + n) * P;
+        for (int e = lane; e < P; e += 32) {
+            const int i = tri_i[e], j = tri_j[e];
+            const double *co = cl + (sz * P1 + j) * P1;
+            double2 acc = make_double2(0.0, 0.0);
+            for (int u = 0; i + j + u <= p; ++u) {
+                const double2 v = T[tri(i, j + u, p)];
+                acc.x = fma(co[u], v.x, acc.x);
+                acc.y = fma(co[u], v.y, acc.y);
+            }
+            const double2 cur = child_w ? o[e] : make_double2(0.0, 0.0);
+            o[e] = make_double2(fma(0.5, acc.x, cur.x), fma(0.5, acc.y, cur.y));
         }
-        double2 *o = a.Lc + ((a.toff[level] + slot) * (int64_t)KW + n0) * P + e;
-        double2 cur = *o;
-        *o = make_double2(fma(0.5, acc.x, cur.x), fma(0.5, acc.y, cur.y));
+        __syncwarp();
     }
+}
+
+inline size_t l2l_smem(int p)
+{
+    int P = (p + 1) * (p + 2) / 2;
+    return sizeof(double) * 4 * (p + 1) * (p + 1) + sizeof(int) * (2 * P + 2) +
+           sizeof(double2) * 2 * P * kL2LWarps;
 }
 
 inline size_t m2m_smem(int p)
 {
     int P = (p + 1) * (p + 2) / 2;
     return sizeof(double) * 4 * (p + 1) * (p + 1) + sizeof(double2) * 8 * kMMG * P + sizeof(int) * 2 * P;
-}
-inline size_t l2l_smem(int p)
-{
-    int P = (p + 1) * (p + 2) / 2;
-    return sizeof(double) * 4 * (p + 1) * (p + 1) + sizeof(double2) * 2 * kMMG * P + sizeof(int) * 2 * P;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -310,12 +344,29 @@ __global__ void __launch_bounds__(256) l2p_kernel(FarArgs a)
     double2 *loc = reinterpret_cast<double2 *>(sm);     // [nm][P]
     double *mono = reinterpret_cast<double *>(loc + kL2PModes * P);  // [pts][P]
     const uint32_t key = (uint32_t)a.tkeys[d][slot];
-    double rc, zc, h;
-    box_centre(key, d, a.L, a.z0, rc, zc, h);
-    const double inv_h = 1.0 / h;
     const int t0 = a.flstart[key], t1 = a.flstart[key + 1];
+    // the deepest ancestor (or the leaf) that received an S2L contribution: below it the chain
+    // adds nothing, so the leaf's local is that box's local re-centred (exact) and is
+    // evaluated directly.  Written boxes are always materialised (need_kernel), and the choice
+    // depends only on the leaf's own chain, so results do not depend on the other field points
+    // (a field-partitioned multi-GPU solve is bitwise identical to the 1-GPU one).  None: zero.
+    int la = d;
+    uint32_t ka = key;
+    while (la >= 2 && !a.s2l_written[a.lvoff[la] + ka]) {
+        --la;
+        ka >>= 2;
+    }
+    const bool ok = la >= 2;
+    if (la < 2) {
+        la = 2;
+        ka = key >> (2 * (d - 2));
+    }
+    double rc, zc, h;
+    box_centre(ka, la, a.L, a.z0, rc, zc, h);
+    const double inv_h = 1.0 / h;
+    const int64_t aslot = ok ? a.tmap[la][ka] : 0;
     for (int e = threadIdx.x; e < nm * P; e += blockDim.x)
-        loc[e] = a.Lc[((a.toff[d] + slot) * (int64_t)KW + n0) * P + e];
+        loc[e] = ok ? a.Lc[((a.toff[la] + aslot) * (int64_t)KW + n0) * P + e] : make_double2(0.0, 0.0);
     for (int c0 = t0; c0 < t1; c0 += kL2PPts) {
         const int nc = min(kL2PPts, t1 - c0);
         __syncthreads();
@@ -363,7 +414,7 @@ __global__ void __launch_bounds__(256) l2p_kernel(FarArgs a)
 // The JT source boxes' moments (2 JT real columns, pre-scaled by (-1)^j/j!) are multiplied on
 // the CUDA cores by a register-tiled FP64 GEMM; outputs accumulate in registers over the offsets
 // in a fixed order (deterministic) and are post-scaled by 1/l! on the write.
-template <int NT, int TM, int RM, int RN, int KC, int ST = 2>
+template <int NT, int TM, int RM, int RN, int KC, int ST = 2, int PF = 0>
 struct S2LCfg {
     static constexpr int TN = NT / TM;
     static constexpr int MP = TM * RM;          // padded rows (>= P)
@@ -379,8 +430,64 @@ struct S2LGrid {
     int nlev;                       // levels 2..depth
     int level[kMaxLevels];
     int jtiles[kMaxLevels];
-    int64_t start[kMaxLevels + 1];  // CTA prefix per level entry
+    int64_t start[kMaxLevels + 1];  // tile prefix per level entry; tile = (column it, row tile jt)
 };
+
+// Tile activity for S2L: one warp per tile (level, target column it, row tile jt of JT = 2 JH
+// target boxes, JH of each parity).  A tile is active iff some target box in it has a non-empty
+// source box in its interaction list (children of the parent's neighbours that are not
+// neighbours); every target box of an active tile is written by S2L, the
+// others are marked unwritten (their S2L contribution is zero).
+struct TileArgs {
+    const int *smap[kMaxLevels], *tmap[kMaxLevels];
+    int64_t lvoff[kMaxLevels];
+};
+__global__ void s2l_tile_flags_kernel(TileArgs ta, S2LGrid gr, int JH, int *active,
+                                      unsigned char *written)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (t >= gr.start[gr.nlev]) return;
+    int e = 0;
+    while (e + 1 < gr.nlev && t >= gr.start[e + 1]) ++e;
+    const int level = gr.level[e], jtiles = gr.jtiles[e];
+    const int64_t tl = t - gr.start[e];
+    const int jt = (int)(tl % jtiles), it = (int)(tl / jtiles);
+    const int nb = 1 << level, JT = 2 * JH;
+    const int di0 = (it & 1) ? -3 : -2;
+    const int *tmap = ta.tmap[level], *smap = ta.smap[level];
+    bool any = false;
+    for (int q = lane; q < 42 * JT && !any; q += 32) {
+        const int o = q / JT, b = q % JT;
+        const int di = di0 + o / 7, dj = o % 7 - 3;
+        if (di >= -1 && di <= 1 && dj >= -1 && dj <= 1) continue;
+        const int par = b / JH, jtb = 2 * (jt * JH + (b % JH)) + par;
+        const int is = it + di, js = jtb + dj;
+        if (jtb >= nb || is < 0 || is >= nb || js < 0 || js >= nb) continue;
+        if ((dj == 3 && par == 1) || (dj == -3 && par == 0)) continue;
+        if (tmap[morton2((uint32_t)it, (uint32_t)jtb)] < 0) continue;
+        if (smap[morton2((uint32_t)is, (uint32_t)js)] >= 0) any = true;
+    }
+    any = __any_sync(0xffffffffu, any);
+    if (lane == 0) active[t] = any ? 1 : 0;
+    for (int b = lane; b < JT; b += 32) {
+        const int jtb = 2 * (jt * JH + (b % JH)) + b / JH;
+        if (jtb < nb) {
+            const uint32_t key = morton2((uint32_t)it, (uint32_t)jtb);
+            if (tmap[key] >= 0) written[ta.lvoff[level] + key] = any ? 1 : 0;
+        }
+    }
+}
+
+// compact list of active tiles (pos = exclusive scan of active)
+__global__ void s2l_tile_emit_kernel(const int *active, const int *pos, int64_t ntiles, int *tiles,
+                                     int *count)
+{
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ntiles) return;
+    if (active[t]) tiles[pos[t]] = (int)t;
+    if (t == ntiles - 1) *count = pos[t] + active[t];
+}
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool valid)
 {
@@ -391,10 +498,49 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool va
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
-template <int RM, int RN, int TM, int TN, int MP, int NC, int MASK>
+template <int RM, int RN, int TM, int TN, int MP, int NC, int MASK, int PF>
 __device__ __forceinline__ void s2l_gemm(const double *As, const double *Bs, int kc, int tm,
                                          int tn, double (&acc)[RM][RN])
 {
+    if constexpr (PF) {
+        // register double buffer: fragments of kk + 1 are loaded before the FMAs of kk
+        double av[2][RM], bv[2][RN];
+        auto load = [&](int kk, int b) {
+#pragma unroll
+            for (int u = 0; u < RM / 2; ++u) {
+                double2 t = *reinterpret_cast<const double2 *>(As + kk * MP + 2 * (tm + TM * u));
+                av[b][2 * u] = t.x;
+                av[b][2 * u + 1] = t.y;
+            }
+#pragma unroll
+            for (int v = 0; v < RN; ++v)
+                if (MASK & (1 << v)) bv[b][v] = Bs[kk * NC + tn + TN * v];
+        };
+        load(0, 0);
+        int kk = 0;
+        for (; kk + 1 < kc; kk += 2) {
+            load(kk + 1, 1);
+#pragma unroll
+            for (int u = 0; u < RM; ++u)
+#pragma unroll
+                for (int v = 0; v < RN; ++v)
+                    if (MASK & (1 << v)) acc[u][v] = fma(av[0][u], bv[0][v], acc[u][v]);
+            if (kk + 2 < kc) load(kk + 2, 0);
+#pragma unroll
+            for (int u = 0; u < RM; ++u)
+#pragma unroll
+                for (int v = 0; v < RN; ++v)
+                    if (MASK & (1 << v)) acc[u][v] = fma(av[1][u], bv[1][v], acc[u][v]);
+        }
+        if (kk < kc) {
+#pragma unroll
+            for (int u = 0; u < RM; ++u)
+#pragma unroll
+                for (int v = 0; v < RN; ++v)
+                    if (MASK & (1 << v)) acc[u][v] = fma(av[0][u], bv[0][v], acc[u][v]);
+        }
+        return;
+    }
 #pragma unroll 3
     for (int kk = 0; kk < kc; ++kk) {
         double av[RM], bv[RN];
@@ -415,23 +561,23 @@ __device__ __forceinline__ void s2l_gemm(const double *As, const double *Bs, int
     }
 }
 
-template <int RM, int RN, int TM, int TN, int MP, int NC, int M>
+template <int RM, int RN, int TM, int TN, int MP, int NC, int M, int PF>
 __device__ __forceinline__ void s2l_gemm_dispatch(int mask, const double *As, const double *Bs,
                                                   int kc, int tm, int tn, double (&acc)[RM][RN])
 {
     if constexpr (M > 0) {
         if (mask == M) {
-            s2l_gemm<RM, RN, TM, TN, MP, NC, M>(As, Bs, kc, tm, tn, acc);
+            s2l_gemm<RM, RN, TM, TN, MP, NC, M, PF>(As, Bs, kc, tm, tn, acc);
             return;
         }
-        s2l_gemm_dispatch<RM, RN, TM, TN, MP, NC, M - 1>(mask, As, Bs, kc, tm, tn, acc);
+        s2l_gemm_dispatch<RM, RN, TM, TN, MP, NC, M - 1, PF>(mask, As, Bs, kc, tm, tn, acc);
     }
 }
 
-template <int NT, int TM, int RM, int RN, int KC, int ST>
+template <int NT, int TM, int RM, int RN, int KC, int ST, int PF>
 __global__ void __launch_bounds__(NT) s2l_kernel(FarArgs a, S2LGrid gr)
 {
-    using Cfg = S2LCfg<NT, TM, RM, RN, KC, ST>;
+    using Cfg = S2LCfg<NT, TM, RM, RN, KC, ST, PF>;
     constexpr int TN = Cfg::TN, MP = Cfg::MP, NC = Cfg::NCP, JT = Cfg::JT, JH = Cfg::JH;
     constexpr int NOFF = Cfg::NOFF;
     constexpr int BOXV = TN / 2;                   // boxes per column block v
@@ -447,13 +593,12 @@ __global__ void __launch_bounds__(NT) s2l_kernel(FarArgs a, S2LGrid gr)
     int *olist = ssl + NOFF * JT;                  // [NOFF] active offsets
     int *nact = olist + NOFF;
 
-    int64_t bid = blockIdx.x;
+    const int nloc = (int)(blockIdx.x % KW);
+    int64_t bid = a.s2l_tiles[blockIdx.x / KW];      // active tile (s2l_tile_flags_kernel)
     int e = 0;
     while (e + 1 < gr.nlev && bid >= gr.start[e + 1]) ++e;
     const int level = gr.level[e], jtiles = gr.jtiles[e];
     bid -= gr.start[e];
-    const int nloc = (int)(bid % KW);
-    bid /= KW;
     const int jt = (int)(bid % jtiles);
     const int it = (int)(bid / jtiles);
     const int nb = 1 << level;
@@ -572,8 +717,8 @@ __global__ void __launch_bounds__(NT) s2l_kernel(FarArgs a, S2LGrid gr)
                 As[q] = (c & 1) ? -v : v;
             }
             __syncthreads();
-            s2l_gemm_dispatch<RM, RN, TM, TN, MP, NC, (1 << RN) - 1>(mask, As, Bs + k0 * NC, kc, tm,
-                                                                    tn, acc);
+            s2l_gemm_dispatch<RM, RN, TM, TN, MP, NC, (1 << RN) - 1, PF>(mask, As, Bs + k0 * NC, kc,
+                                                                        tm, tn, acc);
         }
     }
     (void)BOXV;
@@ -635,10 +780,10 @@ __global__ void prescale_moments_kernel(double2 *M, int64_t nrows, int p, int P)
     M[e] = make_double2(v.x * f, v.y * f);
 }
 
-template <int NT, int TM, int RM, int RN, int KC, int ST>
+template <int NT, int TM, int RM, int RN, int KC, int ST, int PF>
 inline size_t s2l_smem_bytes(int p)
 {
-    using Cfg = S2LCfg<NT, TM, RM, RN, KC, ST>;
+    using Cfg = S2LCfg<NT, TM, RM, RN, KC, ST, PF>;
     int P = (p + 1) * (p + 2) / 2, TP = (p + 1) * (p + 1) * (p + 1), TPp = TP + (TP & 1);
     return sizeof(double) * ((size_t)KC * Cfg::MP + ST * (size_t)P * Cfg::NCP + ST * (TPp + 2) + P) +
            sizeof(int) * (Cfg::JT + Cfg::NOFF * Cfg::JT + Cfg::NOFF + 1);

@@ -190,13 +190,15 @@ __global__ void __launch_bounds__(128) tensor_seed_kernel(TensorGeomArgs a)
             //   rho_{n-1} = (2n-3) / (4(n-1) chi(Delta) - (2n-1) rho_n)   (series reciprocal),
             // S = N + e(chi) as for G (R#4); then g_n = g_{n-1} rho_n.
             // start: the contamination lambda^{-2(S-n)} must be small on the whole disk
-            // |Delta| <= 1 (the S2L offsets) whose Taylor coefficients are used, so e follows from
-            // the minimum of ln|lambda(chi(x + Delta))| on the circle |Delta| = 1 (harmonic)
+            // |Delta| <= rho_-/2 whose Taylor coefficients the S2L offsets use (|Delta| <= h,
+            // rho_- >= 2h), so e follows from the minimum of ln|lambda(chi(x + Delta))| on the
+            // circle |Delta| = rho_-/2 (harmonic)
             double mloc = 1e300;
+            const double Rd = 0.5 * sqrt(geo.rm2);
             for (int k = tid; k < 256; k += blockDim.x) {
                 double sn, cs;
                 sincospi(k / 128.0, &sn, &cs);
-                const double xr = x + cs, xi = sn;              // x + Delta
+                const double xr = fma(Rd, cs, x), xi = Rd * sn;   // x + Delta
                 const double inv2 = 0.5 / geo.rr1;
                 const double zr = (r * r + r1 * r1 + xr * xr - xi * xi) * inv2, zi = 2.0 * xr * xi * inv2;
                 // w = z + sqrt(z^2 - 1), |ln|w|| (either root gives the same modulus of the log)

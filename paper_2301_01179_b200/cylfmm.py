@@ -89,6 +89,9 @@ def lib():
     L.cylfmm_tensor_batch.argtypes = [vp, vp, vp, i64, i, i, i, vp, vp]
     L.cylfmm_tree_sort.restype = i
     L.cylfmm_tree_sort.argtypes = [vp, vp, i64, i, d, d, vp, vp, vp]
+    L.cylfmm_partition_fields.restype = i
+    L.cylfmm_partition_fields.argtypes = [vp, vp, i64, vp, vp, i64, ctypes.POINTER(Params), i,
+                                          vp, vp]
     _lib = L
     return L
 
@@ -244,3 +247,19 @@ class Plan:
 
     def sync(self):
         _check(lib().cylfmm_plan_sync(self._h), "cylfmm_plan_sync")
+
+
+def partition_fields(src_r, src_z, fld_r, fld_z, cfg: "FMMConfig", n_parts: int):
+    """Cost-weighted Morton partition of the field points over n_parts GPUs
+    (cylfmm_partition_fields, host-only: no device needed).  Returns (part int32 [n_fld],
+    estimated flops per part float64 [n_parts])."""
+    a = [np.ascontiguousarray(v, dtype=np.float64) for v in (src_r, src_z, fld_r, fld_z)]
+    part = np.empty(a[2].shape[0], dtype=np.int32)
+    cost = np.empty(n_parts, dtype=np.float64)
+    prm = Params(cfg.n_modes, cfg.order, cfg.depth, cfg.truncation, cfg.miller,
+                 int(bool(cfg.exclude_coincident)), float(cfg.z0), float(cfg.L), cfg.mode_chunk)
+    p = lambda x: ctypes.c_void_p(x.ctypes.data) if x.size else ctypes.c_void_p(0)  # noqa: E731
+    _check(lib().cylfmm_partition_fields(p(a[0]), p(a[1]), a[0].shape[0], p(a[2]), p(a[3]),
+                                         a[2].shape[0], ctypes.byref(prm), int(n_parts), p(part),
+                                         p(cost)), "cylfmm_partition_fields")
+    return part, cost

@@ -231,6 +231,30 @@ def test_fmm_mode_chunks_and_host_api_identical(gpu, orc):
     assert np.array_equal(a, c)   # bitwise reproducible
 
 
+@pytest.mark.parametrize("depth,p,K", [(5, 8, 9), (6, 10, 5), (2, 6, 3)])
+def test_fmm_sparse_sources_vs_oracle_fmm(gpu, orc, depth, p, K):
+    """C5-like layout at small size: sources on a torus + sphere generating curve, fields on a
+    separate grid covering the domain, so most target boxes get no S2L contribution (skipped
+    tiles, lazily materialised locals evaluated from an ancestor)."""
+    from tests.inputs import surface_sources
+    sr, sz = surface_sources(2500)
+    rng = np.random.default_rng(depth)
+    S = rng.standard_normal((len(sr), K)) + 1j * rng.standard_normal((len(sr), K))
+    g = np.arange(1, 41) / 40
+    fr = np.repeat(g, 80)
+    fz = np.tile(2.0 * np.arange(80) / 79, 40)
+    out, ref, _ = _fmm_case(gpu, orc, sr, sz, S, fr, fz, p, depth, 2.0)
+    assert eps_modes(out, ref).max() <= TOL
+
+
+def test_fmm_no_sources_gives_zero(gpu):
+    plan = gpu.Plan(gpu.FMMConfig(n_modes=3, order=4, depth=3))
+    fr = np.array([0.25, 0.75])
+    fz = np.array([0.5, 0.1])
+    out = plan.solve(np.zeros(0), np.zeros(0), np.zeros((0, 3), dtype=np.complex128), fr, fz)
+    assert np.all(out.cpu().numpy() == 0)
+
+
 def test_fmm_domain_error(gpu):
     plan = gpu.Plan(gpu.FMMConfig(n_modes=2, order=4, depth=3))
     r = np.array([0.5, 1.5])
