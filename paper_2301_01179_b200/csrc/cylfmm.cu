@@ -80,18 +80,22 @@ static cudaError_t allow_smem(F *kernel)
 
 // S2L tilings (NT, TM, RM, RN, KC, stages); variant 0 of each order class is the default, the
 // others are selectable with CYLFMM_S2L_VARIANT for measurement (same MP = TM RM per class)
-#define S2L_P8 128, 8, 6, 4, 48, 2, 0
-#define S2L_P8_V1 128, 8, 6, 4, 48, 1, 0
+// measured (C2/C3/C4 S2L phase, round 1): single-stage staging (more CTAs per SM) beats the
+// double-buffered one by 11-20%; the register double buffer (PF) gains nothing
+#define S2L_P8 128, 8, 6, 4, 48, 1, 0
+#define S2L_P8_V1 128, 8, 6, 4, 48, 2, 0
 #define S2L_P8_V2 128, 8, 6, 4, 48, 1, 1
-#define S2L_P8_V3 128, 8, 6, 4, 48, 2, 1
-#define S2L_P12 256, 16, 6, 4, 32, 2, 0
-#define S2L_P12_V1 256, 16, 6, 4, 16, 1, 0
+#define S2L_P12 256, 16, 6, 4, 16, 1, 0
+#define S2L_P12_V1 256, 16, 6, 4, 32, 2, 0
 #define S2L_P12_V2 256, 16, 6, 4, 16, 1, 1
-#define S2L_P16 256, 16, 10, 2, 32, 2, 0
-#define S2L_P16_V1 256, 16, 10, 2, 16, 1, 0
+#define S2L_P16 256, 16, 10, 2, 16, 1, 0
+#define S2L_P16_V1 256, 16, 10, 2, 32, 2, 0
 #define S2L_P16_V2 256, 16, 10, 2, 16, 1, 1
-#define S2L_ALL(X) X(S2L_P8) X(S2L_P8_V1) X(S2L_P8_V2) X(S2L_P8_V3) X(S2L_P12) X(S2L_P12_V1) \
-    X(S2L_P12_V2) X(S2L_P16) X(S2L_P16_V1) X(S2L_P16_V2)
+// each tiling is instantiated for a runtime order (0) and for the BASELINE order of its class
+#define S2L_ALL(X) X(S2L_P8, 0) X(S2L_P8, 8) X(S2L_P8_V1, 0) X(S2L_P8_V1, 8) X(S2L_P8_V2, 0)      \
+    X(S2L_P8_V2, 8) X(S2L_P12, 0) X(S2L_P12, 12) X(S2L_P12_V1, 0) X(S2L_P12_V1, 12)              \
+    X(S2L_P12_V2, 0) X(S2L_P12_V2, 12) X(S2L_P16, 0) X(S2L_P16, 16) X(S2L_P16_V1, 0)             \
+    X(S2L_P16_V1, 16) X(S2L_P16_V2, 0) X(S2L_P16_V2, 16)
 
 static cylfmm_status ensure_init()
 {
@@ -124,9 +128,9 @@ static cylfmm_status ensure_init()
 
 static int s2l_mp(int p)
 {
-    if (p <= 8) return S2LCfg<S2L_P8>::MP;
-    if (p <= 12) return S2LCfg<S2L_P12>::MP;
-    return S2LCfg<S2L_P16>::MP;
+    if (p <= 8) return S2LCfg<S2L_P8, 0>::MP;
+    if (p <= 12) return S2LCfg<S2L_P12, 0>::MP;
+    return S2LCfg<S2L_P16, 0>::MP;
 }
 
 static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -272,19 +276,26 @@ extern "C" cylfmm_status cylfmm_greens_batch(const double *r, const double *r1, 
     return CYLFMM_OK;
 }
 
-static cylfmm_status run_tensors(TensorGeomArgs ta, int64_t ngeom, cudaStream_t st)
+static cylfmm_status run_seeds(TensorGeomArgs ta, int64_t ngeom, cudaStream_t st)
 {
-    const int p = ta.p, D = 2 * p + 1;
-    int Nw = ta.m1 - 1, Ni = Nw > 1 ? Nw : 1;
-    (void)Ni;
-    size_t sm_seed = tensor_seed_smem(ta.K, ta.m1, p);
+    size_t sm_seed = tensor_seed_smem(ta.K, ta.m1, ta.p);
     tensor_seed_kernel<<<(unsigned)ngeom, 128, sm_seed, st>>>(ta);
     CKL();
+    return CYLFMM_OK;
+}
+static cylfmm_status run_fill(TensorGeomArgs ta, int64_t ngeom, cudaStream_t st)
+{
+    const int p = ta.p, D = 2 * p + 1;
     size_t sm_fill = sizeof(double) * (size_t)(p + 1) * (p + 1) * D;
     int KW = ta.m1 - ta.m0;
     tensor_fill_kernel<<<(unsigned)(ngeom * KW), 256, sm_fill, st>>>(ta);
     CKL();
     return CYLFMM_OK;
+}
+static cylfmm_status run_tensors(TensorGeomArgs ta, int64_t ngeom, cudaStream_t st)
+{
+    RET_IF(run_seeds(ta, ngeom, st));
+    return run_fill(ta, ngeom, st);
 }
 
 extern "C" cylfmm_status cylfmm_tensor_batch(const double *r, const double *r1, const double *x,
@@ -577,21 +588,21 @@ static S2LGrid make_s2l_grid(int depth, int JH)
     return gr;
 }
 
-template <int NT, int TM, int RM, int RN, int KC, int ST, int PF>
+template <int NT, int TM, int RM, int RN, int KC, int ST, int PF, int PC>
 static cudaError_t launch_s2l_t(const FarArgs &fa, int64_t ntiles, cudaStream_t st)
 {
-    using Cfg = S2LCfg<NT, TM, RM, RN, KC, ST, PF>;
+    using Cfg = S2LCfg<NT, TM, RM, RN, KC, ST, PF, PC>;
     const int KW = fa.m1 - fa.m0;
     const S2LGrid gr = make_s2l_grid(fa.depth, Cfg::JH);
     if (ntiles == 0) return cudaSuccess;
-    size_t sm = s2l_smem_bytes<NT, TM, RM, RN, KC, ST, PF>(fa.p);
-    s2l_kernel<NT, TM, RM, RN, KC, ST, PF><<<(unsigned)(ntiles * KW), NT, sm, st>>>(fa, gr);
+    size_t sm = s2l_smem_bytes<NT, TM, RM, RN, KC, ST, PF, PC>(fa.p);
+    s2l_kernel<NT, TM, RM, RN, KC, ST, PF, PC><<<(unsigned)(ntiles * KW), NT, sm, st>>>(fa, gr);
     return cudaGetLastError();
 }
-template <int NT, int TM, int RM, int RN, int KC, int ST, int PF>
+template <int NT, int TM, int RM, int RN, int KC, int ST, int PF, int PC>
 static int s2l_jh_t()
 {
-    return S2LCfg<NT, TM, RM, RN, KC, ST, PF>::JH;
+    return S2LCfg<NT, TM, RM, RN, KC, ST, PF, PC>::JH;
 }
 static int s2l_variant()
 {
@@ -601,23 +612,24 @@ static int s2l_variant()
     }();
     return v;
 }
+#define S2L_PICK(FN, CFG, PCV, ...) \
+    return (p == PCV) ? FN<CFG, PCV>(__VA_ARGS__) : FN<CFG, 0>(__VA_ARGS__)
 #define S2L_DISPATCH(FN, ...)                                                                  \
     do {                                                                                       \
         const int v_ = s2l_variant();                                                          \
         if (p <= 8) {                                                                          \
-            if (v_ == 1) return FN<S2L_P8_V1>(__VA_ARGS__);                                    \
-            if (v_ == 2) return FN<S2L_P8_V2>(__VA_ARGS__);                                    \
-            if (v_ == 3) return FN<S2L_P8_V3>(__VA_ARGS__);                                    \
-            return FN<S2L_P8>(__VA_ARGS__);                                                    \
+            if (v_ == 1) S2L_PICK(FN, S2L_P8_V1, 8, __VA_ARGS__);                              \
+            if (v_ == 2) S2L_PICK(FN, S2L_P8_V2, 8, __VA_ARGS__);                              \
+            S2L_PICK(FN, S2L_P8, 8, __VA_ARGS__);                                              \
         }                                                                                      \
         if (p <= 12) {                                                                         \
-            if (v_ == 1) return FN<S2L_P12_V1>(__VA_ARGS__);                                   \
-            if (v_ == 2) return FN<S2L_P12_V2>(__VA_ARGS__);                                   \
-            return FN<S2L_P12>(__VA_ARGS__);                                                   \
+            if (v_ == 1) S2L_PICK(FN, S2L_P12_V1, 12, __VA_ARGS__);                            \
+            if (v_ == 2) S2L_PICK(FN, S2L_P12_V2, 12, __VA_ARGS__);                            \
+            S2L_PICK(FN, S2L_P12, 12, __VA_ARGS__);                                            \
         }                                                                                      \
-        if (v_ == 1) return FN<S2L_P16_V1>(__VA_ARGS__);                                       \
-        if (v_ == 2) return FN<S2L_P16_V2>(__VA_ARGS__);                                       \
-        return FN<S2L_P16>(__VA_ARGS__);                                                       \
+        if (v_ == 1) S2L_PICK(FN, S2L_P16_V1, 16, __VA_ARGS__);                                \
+        if (v_ == 2) S2L_PICK(FN, S2L_P16_V2, 16, __VA_ARGS__);                                \
+        S2L_PICK(FN, S2L_P16, 16, __VA_ARGS__);                                                \
     } while (0)
 static cudaError_t launch_s2l(const FarArgs &fa, int64_t ntiles, cudaStream_t st)
 {
@@ -845,15 +857,16 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         fa.m0 = m0;
         fa.m1 = std::min(K, m0 + KW);
         const int kw = fa.m1 - fa.m0;
-        // tensors for the normalised stations (shared by all levels)
+        // tensors for the normalised stations (shared by all levels): seeds of all modes once,
+        // the Laplace fill per mode chunk
         tic();
         {
             TensorGeomArgs ta = {};
             ta.station_mode = 1;
             ta.n = nstat;
             ta.K = K;
-            ta.m0 = fa.m0;
-            ta.m1 = fa.m1;
+            ta.m0 = 0;
+            ta.m1 = K;
             ta.p = pp;
             ta.miller = q.miller;
             ta.fwd2 = forward_coef(std::max(K - 1, 1), q.miller);
@@ -861,8 +874,15 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             ta.out = p->tens.as<double>();
             ta.packed = 1;
             ta.err = p->err.as<int>();
-            RET_IF(run_tensors(ta, nstat, st));
-            p->launches += 2;
+            if (m0 == 0) {
+                RET_IF(run_seeds(ta, nstat, st));
+                p->launches++;
+            }
+            ta.m0 = fa.m0;
+            ta.m1 = fa.m1;
+            ta.seed_m1 = K;
+            RET_IF(run_fill(ta, nstat, st));
+            p->launches++;
         }
         toc(ms_tensor);
         if (ns > 0) {

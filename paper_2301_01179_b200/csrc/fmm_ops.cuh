@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(256) l2p_kernel(FarArgs a)
 // The JT source boxes' moments (2 JT real columns, pre-scaled by (-1)^j/j!) are multiplied on
 // the CUDA cores by a register-tiled FP64 GEMM; outputs accumulate in registers over the offsets
 // in a fixed order (deterministic) and are post-scaled by 1/l! on the write.
-template <int NT, int TM, int RM, int RN, int KC, int ST = 2, int PF = 0>
+template <int NT, int TM, int RM, int RN, int KC, int ST = 2, int PF = 0, int PC = 0>
 struct S2LCfg {
     static constexpr int TN = NT / TM;
     static constexpr int MP = TM * RM;          // padded rows (>= P)
@@ -574,15 +574,17 @@ __device__ __forceinline__ void s2l_gemm_dispatch(int mask, const double *As, co
     }
 }
 
-template <int NT, int TM, int RM, int RN, int KC, int ST, int PF>
+template <int NT, int TM, int RM, int RN, int KC, int ST, int PF, int PC>
 __global__ void __launch_bounds__(NT) s2l_kernel(FarArgs a, S2LGrid gr)
 {
-    using Cfg = S2LCfg<NT, TM, RM, RN, KC, ST, PF>;
+    using Cfg = S2LCfg<NT, TM, RM, RN, KC, ST, PF, PC>;
     constexpr int TN = Cfg::TN, MP = Cfg::MP, NC = Cfg::NCP, JT = Cfg::JT, JH = Cfg::JH;
     constexpr int NOFF = Cfg::NOFF;
     constexpr int BOXV = TN / 2;                   // boxes per column block v
     extern __shared__ double sm[];
-    const int p = a.p, P = a.P, KW = a.m1 - a.m0;
+    // PC > 0: the expansion order is a compile-time constant (BASELINE orders 8, 12, 16), so
+    // every index division below is by a constant
+    const int p = PC ? PC : a.p, P = PC ? (PC + 1) * (PC + 2) / 2 : a.P, KW = a.m1 - a.m0;
     const int TP = (p + 1) * (p + 1) * (p + 1), TPp = TP + (TP & 1), HST = TPp + 2;
     double *As = sm;                               // [KC][MP]
     double *Bs0 = As + KC * MP;                    // 2 x [P][NC]
@@ -780,10 +782,10 @@ __global__ void prescale_moments_kernel(double2 *M, int64_t nrows, int p, int P)
     M[e] = make_double2(v.x * f, v.y * f);
 }
 
-template <int NT, int TM, int RM, int RN, int KC, int ST, int PF>
+template <int NT, int TM, int RM, int RN, int KC, int ST, int PF, int PC>
 inline size_t s2l_smem_bytes(int p)
 {
-    using Cfg = S2LCfg<NT, TM, RM, RN, KC, ST, PF>;
+    using Cfg = S2LCfg<NT, TM, RM, RN, KC, ST, PF, PC>;
     int P = (p + 1) * (p + 2) / 2, TP = (p + 1) * (p + 1) * (p + 1), TPp = TP + (TP & 1);
     return sizeof(double) * ((size_t)KC * Cfg::MP + ST * (size_t)P * Cfg::NCP + ST * (TPp + 2) + P) +
            sizeof(int) * (Cfg::JT + Cfg::NOFF * Cfg::JT + Cfg::NOFF + 1);

@@ -68,9 +68,10 @@ def test_greens_batch_vs_oracle(gpu, orc, K, miller):
 def test_tensor_batch_vs_oracle(gpu, orc, p, K):
     # normalised station-like geometries (the FMM evaluates tensors at (i+dI+1/2, i+1/2, dJ)),
     # forward and Miller branches, near the axis and deep (r ~ 700 h, C5's leaf level)
-    geo = [(2.5, 0.5, 0.0), (3.5, 1.5, 2.0), (10.5, 10.5, 2.0), (16.5, 13.5, 3.0),
-           (1.3, 0.7, 0.9), (0.8, 0.8, 0.5), (5.5, 3.5, 1.0), (130.5, 128.5, 2.0),
+    geo = [(10.5, 10.5, 2.0), (16.5, 13.5, 3.0), (5.5, 3.5, 1.0), (130.5, 128.5, 2.0),
            (702.5, 700.5, 3.0), (20.5, 17.5, 3.0)]
+    if p <= 12:   # near the axis only at moderate order: see test_tensor_near_axis_vs_exact
+        geo += [(3.5, 1.5, 2.0), (2.5, 0.5, 0.0), (1.3, 0.7, 0.9), (0.8, 0.8, 0.5)]
     r, r1, x = (np.array(v) for v in zip(*geo))
     T = gpu.tensor_batch(r, r1, x, K, p).cpu().numpy()
     w, order = _s2l_weight(p)
@@ -110,6 +111,29 @@ def test_tensor_high_modes_vs_exact(gpu):
             den = np.abs(E[n] * w).max()
             eg = np.abs((T[q, n] - E[n]) * w).max() / den
             assert eg <= 2e-12, (geo[q], n, eg)
+
+
+def test_tensor_near_axis_vs_exact(gpu, orc):
+    """Near-axis stations (inner radius h/2) at p = 16: the radial Laplace recursion
+     carries (b^2 - n^2)/r1^2 and amplifies rounding through its parasitic r1^-n
+    solution (SURVEY APP-E), in BOTH FP64 codes (up to ~1e-7 of the per-mode weighted max at
+    n ~ 15).  Against the exact coefficients (100-digit recursion) the GPU must be no worse than
+    8x the oracle's own rounding error (plus 1e-14).  In the FMM these stations carry
+    contributions that are tiny at high modes (max-normalised metric)."""
+    from tests.hp_tensor import hp_tensor
+    p, K = 16, 25
+    geo = [(0.5, 0.5, 3.0), (2.5, 0.5, 0.0), (1.5, 0.5, 3.0), (1.3, 0.7, 0.9), (3.5, 1.5, 2.0)]
+    r, r1, x = (np.array(v) for v in zip(*geo))
+    T = gpu.tensor_batch(r, r1, x, K, p).cpu().numpy()
+    w, _ = _s2l_weight(p)
+    for q in range(len(r)):
+        E = hp_tensor(r[q], r1[q], x[q], K - 1, p, dps=60)
+        O = orc.tensor(r[q], r1[q], x[q], K - 1, p)
+        for n in range(K):
+            den = np.abs(E[n] * w).max()
+            eg = np.abs((T[q, n] - E[n]) * w).max() / den
+            eo = np.abs((O[n] - E[n]) * w).max() / den
+            assert eg <= 8 * eo + 1e-14, (geo[q], n, eg, eo)
 
 
 def test_direct_c1_vs_oracle(gpu, orc):
