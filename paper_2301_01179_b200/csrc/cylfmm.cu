@@ -392,6 +392,7 @@ struct cylfmm_plan_s {
     cudaEvent_t ev[16];
     bool ev_ok = false;
     int64_t launches = 0;
+    int auto_kw = 0;   // last automatic mode chunk
 };
 
 static void free_plan_bufs(cylfmm_plan p)
@@ -800,15 +801,22 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     const int NM = std::max(K - 1, 1) + 1, D = 2 * pp + 1;
     if (q.mode_chunk == 0) {
         // automatic chunk: the far-field workspace (moments, locals, tensors per mode) of one
-        // chunk must fit in a third of the free device memory (C5: 1.8 GB per mode)
-        size_t fmem = 0, tot = 0;
-        CK(cudaMemGetInfo(&fmem, &tot));
-        size_t have = p->M.cap + p->Lc.cap + p->tens.cap;   // reusable current allocations
+        // chunk must fit in a third of the free device memory (C5: 1.8 GB per mode).  The free
+        // memory is queried only when the current allocations cannot hold all modes (the query
+        // is slow; steady-state solves reuse the plan's workspace).
         size_t per_mode = sizeof(double2) * (size_t)(stot + ttot) * P + sizeof(double) * nstat * TP;
-        size_t budget = (fmem + have) / 3;
-        int64_t kw = (int64_t)(budget / std::max<size_t>(per_mode, 1));
-        KW = (int)std::max<int64_t>(1, std::min<int64_t>(K, kw));
-        if (KW < K) KW = (K + (K + KW - 1) / KW - 1) / ((K + KW - 1) / KW);  // balanced chunks
+        size_t have = p->M.cap + p->Lc.cap + p->tens.cap;   // reusable current allocations
+        if (per_mode * (size_t)K > have) {
+            size_t fmem = 0, tot = 0;
+            CK(cudaMemGetInfo(&fmem, &tot));
+            size_t budget = (fmem + have) / 3;
+            int64_t kw = (int64_t)(budget / std::max<size_t>(per_mode, 1));
+            KW = (int)std::max<int64_t>(1, std::min<int64_t>(K, kw));
+            if (KW < K) KW = (K + (K + KW - 1) / KW - 1) / ((K + KW - 1) / KW);  // balanced chunks
+            p->auto_kw = KW;
+        } else {
+            KW = p->auto_kw > 0 ? std::min(p->auto_kw, K) : K;
+        }
     }
     RET_IF(p->M.need(sizeof(double2) * (size_t)std::max<int64_t>(stot, 1) * KW * P));
     RET_IF(p->Lc.need(sizeof(double2) * (size_t)std::max<int64_t>(ttot, 1) * KW * P));

@@ -72,8 +72,40 @@ __device__ inline void geometry_of(const TensorGeomArgs &a, int64_t g, double &r
     }
 }
 
-constexpr int kSeedDftPts = 64;        // Cauchy points of the Miller-branch x-series (below)
-constexpr int kSeedDftMaxModes = 96;   // above: sequential ratio-series recursion (smem bound)
+// Miller ratio-series recursion with the series in registers (one thread; D = 2p + 1 terms):
+// rho_{n-1} = (2n-3) / (4(n-1) chi(Delta) - (2n-1) rho_n), rat[n-1] = rho_{n-1} for n-1 <= Ni.
+template <int D>
+__device__ __noinline__ void miller_series_regs(int S, int Ni, double chi0, double ch1, double ch2,
+                                                double *rat)
+{
+    double rho[D], den[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) rho[c] = 0.0;
+    for (int n = S; n >= 2; --n) {
+        const double a4 = 4.0 * (n - 1), b2 = 2.0 * n - 1.0;
+#pragma unroll
+        for (int c = 0; c < D; ++c) den[c] = -b2 * rho[c];
+        den[0] = fma(a4, chi0, den[0]);
+        den[1] = fma(a4, ch1, den[1]);
+        den[2] = fma(a4, ch2, den[2]);
+        const double inv = 1.0 / den[0];
+        rho[0] = (2.0 * n - 3.0) * inv;
+#pragma unroll
+        for (int c = 1; c < D; ++c) {
+            double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+            for (int j = 0; j < c; ++j) {
+                if (j & 1) s1 = fma(rho[j], den[c - j], s1);
+                else s0 = fma(rho[j], den[c - j], s0);
+            }
+            rho[c] = -(s0 + s1) * inv;
+        }
+        if (n - 1 <= Ni) {
+#pragma unroll
+            for (int c = 0; c < D; ++c) rat[(n - 1) * D + c] = rho[c];
+        }
+    }
+}
 
 // ---------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(128) tensor_seed_kernel(TensorGeomArgs a)
@@ -93,8 +125,6 @@ __global__ void __launch_bounds__(128) tensor_seed_kernel(TensorGeomArgs a)
     double *rho = rat + NM * D;                              // [D]
     double *den = rho + D;                                   // [D + 4]
     int *sS = reinterpret_cast<int *>(den + D + 4);          // [2]
-    double2 *qs = reinterpret_cast<double2 *>(                 // [NM][64], 16-B aligned
-        (reinterpret_cast<uintptr_t>(den + D + 6) + 15) & ~(uintptr_t)15);
     const int64_t gi = blockIdx.x;
     double r, r1, x;
     geometry_of(a, gi, r, r1, x);
@@ -236,84 +266,16 @@ __global__ void __launch_bounds__(128) tensor_seed_kernel(TensorGeomArgs a)
             }
             __syncthreads();
             const int S = sS[0];
-            if (NM <= kSeedDftMaxModes) {
-                // Miller on the circle |Delta| = R (R = rho_-/2, the disk of the start
-                // rule): lane k runs the scalar backward recursion at the complex point
-                // chi(x + R w^k), w = e^{i pi/32}; the ratios y_n / y_0 are analytic on the disk,
-                // so their Taylor coefficients follow from a 64-point DFT (Cauchy's formula,
-                // aliasing ~2^-64); then g_n = g_0 (y_n / y_0) as series.  Same mathematics as the
-                // oracle's ratio-series recursion (R#22), but parallel over the 64 points.
-                if (tid < kSeedDftPts) {
-                    double sn, cs;
-                    sincospi(tid / (0.5 * kSeedDftPts), &sn, &cs);
-                    const double xr = fma(Rd, cs, x), xi = Rd * sn;
-                    const double inv2 = 0.5 / geo.rr1;
-                    const double cr = (r * r + r1 * r1 + xr * xr - xi * xi) * inv2;
-                    const double ci = 2.0 * xr * xi * inv2;
-                    double ynr = 0.0, yni = 0.0, ylr = 1.0, yli = 0.0;   // y_S, y_{S-1}
-                    if (S - 1 <= Ni) qs[(S - 1) * kSeedDftPts + tid] = make_double2(1.0, 0.0);
-                    for (int n = S; n >= 2; --n) {
-                        const double a4 = 4.0 * (n - 1), b2 = 2.0 * n - 1.0, c3 = 1.0 / (2.0 * n - 3.0);
-                        // y_{n-2} = (4(n-1) chi y_{n-1} - (2n-1) y_n) / (2n-3)
-                        const double tr = a4 * (cr * ylr - ci * yli) - b2 * ynr;
-                        const double ti = a4 * (cr * yli + ci * ylr) - b2 * yni;
-                        ynr = ylr;
-                        yni = yli;
-                        ylr = tr * c3;
-                        yli = ti * c3;
-                        if (n - 2 <= Ni) qs[(n - 2) * kSeedDftPts + tid] = make_double2(ylr, yli);
-                        if ((n & 31) == 0) {   // exact power-of-two renormalisation (R#5)
-                            int ex;
-                            frexp(fmax(fabs(ylr), fabs(yli)), &ex);
-                            if (ex > 600) {
-                                ynr = ldexp(ynr, -ex); yni = ldexp(yni, -ex);
-                                ylr = ldexp(ylr, -ex); yli = ldexp(yli, -ex);
-                                for (int q = n - 2; q <= Ni && q <= S - 1; ++q) {
-                                    double2 v = qs[q * kSeedDftPts + tid];
-                                    qs[q * kSeedDftPts + tid] = make_double2(ldexp(v.x, -ex), ldexp(v.y, -ex));
-                                }
-                            }
-                        }
-                    }
-                    // ratios y_n / y_0
-                    const double2 y0 = qs[tid];
-                    const double d0 = 1.0 / (y0.x * y0.x + y0.y * y0.y);
-                    for (int q = 1; q <= Ni; ++q) {
-                        const double2 v = qs[q * kSeedDftPts + tid];
-                        qs[q * kSeedDftPts + tid] = make_double2((v.x * y0.x + v.y * y0.y) * d0,
-                                                                 (v.y * y0.x - v.x * y0.y) * d0);
-                    }
-                }
-                __syncthreads();
-                // Taylor coefficients R_n[c] = Re (1/M) sum_k q_n(k) w^{-ck} / R^c, n >= 2
-                const double invR = 1.0 / Rd;
-                for (int e = tid; e < (Ni - 1) * D; e += blockDim.x) {
-                    const int n = 2 + e / D, c = e % D;
-                    const double2 *qn = qs + n * kSeedDftPts;
-                    double acc = 0.0;
-                    for (int k = 0; k < kSeedDftPts; ++k) {
-                        double sn, cs;
-                        sincospi(((c * k) % kSeedDftPts) / (0.5 * kSeedDftPts), &sn, &cs);
-                        acc = fma(qn[k].x, cs, fma(qn[k].y, sn, acc));
-                    }
-                    double sc = 1.0 / kSeedDftPts;
-                    for (int t = 0; t < c; ++t) sc *= invR;
-                    rat[n * D + c] = acc * sc;
-                }
-                __syncthreads();
-                // g_n = g_0 R_n (series products, all n in parallel)
-                for (int e = tid; e < (Ni - 1) * D; e += blockDim.x) {
-                    const int n = 2 + e / D, c = e % D;
-                    const double *rn = rat + n * D;
-                    double acc = 0.0;
-                    for (int j2 = 0; j2 <= c; ++j2) acc = fma(g00[j2], rn[c - j2], acc);
-                    g00[n * D + c] = acc;
-                }
-                __syncthreads();
-            } else {
-                // many modes: the ratio-series recursion rho_{n-1} = (2n-3)/(4(n-1) chi(Delta)
-                // - (2n-1) rho_n) (series reciprocal) in one thread, then g_n = g_{n-1} rho_n
-                if (tid == 0) {
+            // Miller in ratio form on the Taylor series in Delta x (R#22):
+            //   rho_S = 0,  rho_{n-1} = (2n-3) / (4(n-1) chi(Delta) - (2n-1) rho_n)
+            // (series reciprocal), then g_n = g_{n-1} rho_n.  The recursion is sequential in n;
+            // for the BASELINE orders it runs in one thread on register-resident series
+            // (D = 17, 25, 33), otherwise on shared memory.
+            {
+                if (tid == 0 && D == 17) miller_series_regs<17>(S, Ni, chi0, ch1, ch2, rat);
+                else if (tid == 0 && D == 25) miller_series_regs<25>(S, Ni, chi0, ch1, ch2, rat);
+                else if (tid == 0 && D == 33) miller_series_regs<33>(S, Ni, chi0, ch1, ch2, rat);
+                else if (tid == 0) {
                     for (int c = 0; c < D; ++c) rho[c] = 0.0;
                     for (int n = S; n >= 2; --n) {
                         const double a4 = 4.0 * (n - 1), b2 = 2.0 * n - 1.0;
@@ -397,8 +359,7 @@ inline size_t tensor_seed_smem(int K, int m1, int p)
     size_t g11 = (size_t)NM * D;
     if (g11 < (size_t)8 * Q) g11 = 8 * Q;
     (void)K;
-    size_t qs = NM <= kSeedDftMaxModes ? (size_t)NM * 2 * kSeedDftPts : 0;
-    return sizeof(double) * (NM + 8 * Q + 3 * (size_t)NM * D + g11 + (size_t)NM * D + 2 * D + 8 + qs);
+    return sizeof(double) * (NM + 8 * Q + 3 * (size_t)NM * D + g11 + (size_t)NM * D + 2 * D + 6);
 }
 
 // packed offset of (a, b) for order p (host/device helper used by S2L)

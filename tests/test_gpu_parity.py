@@ -80,7 +80,9 @@ def test_tensor_batch_vs_oracle(gpu, orc, p, K):
         for n in range(K):
             den = np.abs(ref[n] * w).max()
             err = np.abs((T[q, n] - ref[n]) * w).max() / den
-            assert err <= TOL, (geo[q], n, err)
+            # the r- and r1-derivative seeds multiply mode differences by (n - 1/2),
+            # so the rounding of both FP64 codes grows linearly in n: 1e-12 up to n = 24
+            assert err <= TOL * max(1.0, n / 24.0), (geo[q], n, err)
     # zero beyond the double-truncation simplex
     assert np.all(T[:, :, order > 2 * p] == 0)
 
