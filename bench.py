@@ -12,8 +12,11 @@ roofline fraction of the dominant kernel.
 
 --impl reference times the CPU oracle (oracle/, plain FP64 C, OpenMP) as it stands on the host
 cores -- this tier's reference arm (there is no reference implementation to install).
-Under torchrun (N > 1) field points are partitioned across ranks (north_star), sources are
-replicated (generated identically from the seed on every rank; no data-path collective).
+Under torchrun (N > 1, one process per GPU, NCCL) the field points are partitioned across ranks
+by cost-weighted contiguous Morton ranges (cylfmm_partition_fields; north_star), each rank owns a
+contiguous shard of the sources, and every timed step replicates the sources with an NCCL
+all-gather before the rank's solve; the total problem is fixed ("scaling": "strong") and the
+step time is the max over ranks.  Outputs stay sharded (each rank's potentials in its rows).
 """
 from __future__ import annotations
 
@@ -104,12 +107,6 @@ def make_problem(name):
 
 def n_interactions(pr, skipped):
     return (len(pr.sr) * len(pr.fr) - skipped) * pr.K
-
-
-def shard(pr, rank, world):
-    nf = len(pr.fr)
-    a, b = rank * nf // world, (rank + 1) * nf // world
-    return pr.fr[a:b], pr.fz[a:b]
 
 
 def run_reference(args):
@@ -209,25 +206,46 @@ def main():
 
     import paper_2301_01179_b200 as g
     from paper_2301_01179_b200 import build as b
+    from paper_2301_01179_b200 import distributed as dd
     if not b.up_to_date():
         b.build()
     pr = make_problem(args.config)
-    fr, fz = shard(pr, rank, world)
     dev = torch.device("cuda", local)
-    sr = torch.as_tensor(pr.sr, device=dev)
-    sz = torch.as_tensor(pr.sz, device=dev)
-    S = torch.as_tensor(pr.S, device=dev)
-    fr_d = torch.as_tensor(fr, device=dev)
-    fz_d = torch.as_tensor(fz, device=dev)
+    cfg = g.FMMConfig(n_modes=pr.K, order=pr.p, depth=pr.depth, L=pr.L, z0=pr.z0)
+    # fields: all of them on one GPU; on N GPUs the cost-weighted contiguous Morton range of this
+    # rank (cylfmm_partition_fields, identical on every rank: planning, outside the timed region)
+    if world > 1:
+        part, _ = g.partition_fields(pr.sr, pr.sz, pr.fr, pr.fz, cfg, world)
+        fidx = dd.my_fields(part, rank)
+    else:
+        fidx = np.arange(len(pr.fr))
+    # sources: each rank owns a contiguous shard; N > 1 replicates them with an all-gather
+    # (NCCL over NVLink) inside every timed step -- the north_star's source replication
+    sl = dd.source_shard(len(pr.sr), rank, world)
+    sr_loc = torch.as_tensor(pr.sr[sl], device=dev)
+    sz_loc = torch.as_tensor(pr.sz[sl], device=dev)
+    S_loc = torch.as_tensor(pr.S[sl], device=dev)
+    same = pr.fields_are_sources and world == 1       # fields ARE the sources (C2-C4)
+    fr, fz = pr.fr[fidx], pr.fz[fidx]
+    fr_d = torch.as_tensor(np.ascontiguousarray(fr), device=dev)
+    fz_d = torch.as_tensor(np.ascontiguousarray(fz), device=dev)
     out = torch.empty((len(fr), pr.K), dtype=torch.complex128, device=dev)
-    plan = g.Plan(g.FMMConfig(n_modes=pr.K, order=pr.p, depth=pr.depth, L=pr.L, z0=pr.z0))
+    plan = g.Plan(cfg)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
     stream = torch.cuda.current_stream()
 
+    def step(timings=False):
+        if world > 1:
+            sr, sz, S = dd.allgather_sources((sr_loc, sz_loc, S_loc))
+        else:
+            sr, sz, S = sr_loc, sz_loc, S_loc
+        a, bb = (sr, sz) if same else (fr_d, fz_d)
+        return plan.solve(sr, sz, S, a, bb, out=out, timings=timings)
+
     # warm-up + per-phase breakdown (synchronising timings path, outside the timed region)
     for _ in range(args.warmup):
-        plan.solve(sr, sz, S, fr_d, fz_d, out=out)
-    _, tm = plan.solve(sr, sz, S, fr_d, fz_d, out=out, timings=True)
+        step()
+    _, tm = step(timings=True)
     phase = {k: v for k, v in tm.items()}
     launches_per_step = tm["kernel_launches"]
     skipped = tm["n_skipped"]
@@ -242,7 +260,7 @@ def main():
     for i in range(args.steps):
         flush.zero_()
         ev[i][0].record(stream)
-        plan.solve(sr, sz, S, fr_d, fz_d, out=out)
+        step()
         ev[i][1].record(stream)
     barrier()
     ms = [a.elapsed_time(bb) for a, bb in ev]
@@ -259,10 +277,11 @@ def main():
     inter_total = (len(pr.sr) * len(pr.fr) - skipped) * pr.K
     value = inter_total / (t_max * 1e-3)
 
-    # e2e through the host-buffer C-ABI call (pinned host memory, H2D + D2H inside the region)
+    # e2e through the host-buffer C-ABI call (pinned host memory, H2D + D2H inside the region):
+    # the full source set and this rank's field points in, this rank's potentials out
     hs = [torch.as_tensor(a).pin_memory() for a in (pr.sr, pr.sz)]
     hS = torch.as_tensor(pr.S).pin_memory()
-    hf = [torch.as_tensor(np.ascontiguousarray(a)).pin_memory() for a in (fr, fz)]
+    hf = hs if same else [torch.as_tensor(np.ascontiguousarray(a)).pin_memory() for a in (fr, fz)]
     hout = torch.empty((len(fr), pr.K), dtype=torch.complex128).pin_memory()
     for _ in range(2):
         plan.solve_host(hs[0].numpy(), hs[1].numpy(), hS.numpy(), hf[0].numpy(), hf[1].numpy(),
@@ -281,7 +300,7 @@ def main():
         tt = torch.tensor([t_e2e], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_e2e = float(tt.item())
-    h2d = len(pr.sr) * (16 + 16 * pr.K) + len(fr) * 16
+    h2d = len(pr.sr) * (16 + 16 * pr.K) + (0 if same else len(fr) * 16)
     d2h = len(fr) * pr.K * 16
 
     # roofline of the dominant kernel (FP64 CUDA-core arithmetic: "alu")
@@ -308,7 +327,8 @@ def main():
                 "config": {"workload": f"{args.config}: {pr.name}", "n_src": len(pr.sr),
                            "n_fld": len(pr.fr), "modes": pr.K, "order": pr.p, "depth": pr.depth,
                            "truncation": "double", "miller": "accurate", "l2": "flushed",
-                           "parallelism": f"field-partition x{world}"},
+                           "parallelism": (f"field-partition x{world} (cost-weighted Morton ranges, "
+                                           "source all-gather)") if world > 1 else "single GPU"},
                 "phase_ms": {k: round(v, 4) for k, v in phase.items() if k.startswith("ms_")},
                 "near_pairs": phase["n_near_pairs"], "s2l_box_pairs": phase["n_s2l_pairs"],
                 "roofline": roof, "clocks": clk,

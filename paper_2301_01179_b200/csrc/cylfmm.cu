@@ -690,8 +690,15 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     // ---- tree
     int *sperm = nullptr, *fperm = nullptr;
     uint32_t *skey_s = nullptr, *fkey_s = nullptr;
+    // fields == sources (C2-C4: "field points equal to source points"): one tree serves both
+    const bool same = fld_r == src_r && fld_z == src_z && nf == ns;
     RET_IF(build_tree(p, src_r, src_z, ns, true, st, &sperm, &skey_s));
-    RET_IF(build_tree(p, fld_r, fld_z, nf, false, st, &fperm, &fkey_s));
+    if (same) {
+        fperm = sperm;
+        fkey_s = skey_s;
+    } else {
+        RET_IF(build_tree(p, fld_r, fld_z, nf, false, st, &fperm, &fkey_s));
+    }
     RET_IF(p->sr_s.need(8 * std::max<int64_t>(ns, 1)));
     RET_IF(p->sz_s.need(8 * std::max<int64_t>(ns, 1)));
     RET_IF(p->S_s.need(16 * (size_t)std::max<int64_t>(ns, 1) * K));
@@ -705,17 +712,28 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         CKL();
         p->launches += 3;
     }
-    gather_kernel<double><<<nblk(nf, 256), 256, 0, st>>>(fld_r, fperm, nf, p->fr_s.as<double>());
-    gather_kernel<double><<<nblk(nf, 256), 256, 0, st>>>(fld_z, fperm, nf, p->fz_s.as<double>());
-    CKL();
-    p->launches += 2;
+    const double *fr_sorted = p->sr_s.as<double>(), *fz_sorted = p->sz_s.as<double>();
+    if (!same) {
+        gather_kernel<double><<<nblk(nf, 256), 256, 0, st>>>(fld_r, fperm, nf, p->fr_s.as<double>());
+        gather_kernel<double><<<nblk(nf, 256), 256, 0, st>>>(fld_z, fperm, nf, p->fz_s.as<double>());
+        CKL();
+        p->launches += 2;
+        fr_sorted = p->fr_s.as<double>();
+        fz_sorted = p->fz_s.as<double>();
+    }
     const int64_t nleaf = pow4(d);
     RET_IF(p->slstart.need(sizeof(int) * (nleaf + 1)));
     RET_IF(p->flstart.need(sizeof(int) * (nleaf + 1)));
     leaf_start_kernel<<<nblk(nleaf + 1, 256), 256, 0, st>>>(skey_s, ns, nleaf, p->slstart.as<int>());
-    leaf_start_kernel<<<nblk(nleaf + 1, 256), 256, 0, st>>>(fkey_s, nf, nleaf, p->flstart.as<int>());
     CKL();
-    p->launches += 2;
+    p->launches++;
+    const int *flstart = p->slstart.as<int>();
+    if (!same) {
+        leaf_start_kernel<<<nblk(nleaf + 1, 256), 256, 0, st>>>(fkey_s, nf, nleaf, p->flstart.as<int>());
+        CKL();
+        p->launches++;
+        flstart = p->flstart.as<int>();
+    }
     // level maps
     int64_t lvoff[kMaxLevels + 1];
     lvoff[0] = lvoff[1] = lvoff[2] = 0;
@@ -727,8 +745,10 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     RET_IF(p->tmap.need(sizeof(int) * ltot));
     RET_IF(p->tkeys.need(sizeof(int) * ltot));
     RET_IF(p->counts.need(sizeof(int) * (2 * kMaxLevels + 1)));
-    for (int side = 0; side < 2; ++side) {
-        const int *ls = side == 0 ? p->slstart.as<int>() : p->flstart.as<int>();
+    int *tmap_b = same ? p->smap.as<int>() : p->tmap.as<int>();
+    int *tkeys_b = same ? p->skeys.as<int>() : p->tkeys.as<int>();
+    for (int side = 0; side < (same ? 1 : 2); ++side) {
+        const int *ls = side == 0 ? p->slstart.as<int>() : flstart;
         int *map = side == 0 ? p->smap.as<int>() : p->tmap.as<int>();
         int *keys = side == 0 ? p->skeys.as<int>() : p->tkeys.as<int>();
         for (int l = 2; l <= d; ++l) {
@@ -755,7 +775,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         TileArgs ta = {};
         for (int l = 2; l <= d; ++l) {
             ta.smap[l] = p->smap.as<int>() + lvoff[l];
-            ta.tmap[l] = p->tmap.as<int>() + lvoff[l];
+            ta.tmap[l] = tmap_b + lvoff[l];
             ta.lvoff[l] = lvoff[l];
         }
         s2l_tile_flags_kernel<<<nblk(ntiles_all * 32, 256), 256, 0, st>>>(
@@ -773,6 +793,8 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     CK(cudaMemcpyAsync(hcnt, p->counts.p, sizeof(int) * (2 * kMaxLevels + 1), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     RET_IF(check_err_flag(p, st));
+    if (same)
+        for (int l = 0; l < kMaxLevels; ++l) hcnt[kMaxLevels + l] = hcnt[l];
     T.mark();  // 1: tree done
     // ---- far-field storage
     FarArgs fa = {};
@@ -787,8 +809,8 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     for (int l = 2; l <= d; ++l) {
         fa.smap[l] = p->smap.as<int>() + lvoff[l];
         fa.skeys[l] = p->skeys.as<int>() + lvoff[l];
-        fa.tmap[l] = p->tmap.as<int>() + lvoff[l];
-        fa.tkeys[l] = p->tkeys.as<int>() + lvoff[l];
+        fa.tmap[l] = tmap_b + lvoff[l];
+        fa.tkeys[l] = tkeys_b + lvoff[l];
         fa.scount[l] = ns > 0 ? hcnt[l] : 0;
         fa.tcount[l] = hcnt[kMaxLevels + l];
         fa.soff[l] = stot;
@@ -826,12 +848,12 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     fa.Lc = p->Lc.as<double2>();
     fa.tens = p->tens.as<double>();
     fa.slstart = p->slstart.as<int>();
-    fa.flstart = p->flstart.as<int>();
+    fa.flstart = flstart;
     fa.sr = p->sr_s.as<double>();
     fa.sz = p->sz_s.as<double>();
     fa.S = p->S_s.as<double2>();
-    fa.fr = p->fr_s.as<double>();
-    fa.fz = p->fz_s.as<double>();
+    fa.fr = fr_sorted;
+    fa.fz = fz_sorted;
     fa.fperm = fperm;
     fa.out = reinterpret_cast<double2 *>(out_Phi);
     fa.s2l_pairs = p->ctr.as<unsigned long long>() + 2;
@@ -1072,13 +1094,17 @@ extern "C" cylfmm_status cylfmm_fmm_solve_host(cylfmm_plan plan, const double *s
         CK(cudaMemcpyAsync(plan->h_sz.p, src_z, 8 * n_src, cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(plan->h_S.p, src_S, 16 * (size_t)n_src * K, cudaMemcpyHostToDevice, st));
     }
-    if (n_fld > 0) {
+    // fields == sources (same host arrays): copied once, one tree serves both
+    const bool same = fld_r == src_r && fld_z == src_z && n_fld == n_src;
+    if (n_fld > 0 && !same) {
         CK(cudaMemcpyAsync(plan->h_fr.p, fld_r, 8 * n_fld, cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(plan->h_fz.p, fld_z, 8 * n_fld, cudaMemcpyHostToDevice, st));
     }
+    const double *dfr = same ? plan->h_sr.as<double>() : plan->h_fr.as<double>();
+    const double *dfz = same ? plan->h_sz.as<double>() : plan->h_fz.as<double>();
     RET_IF(fmm_solve_impl(plan, plan->h_sr.as<double>(), plan->h_sz.as<double>(),
-                          plan->h_S.as<double>(), n_src, plan->h_fr.as<double>(),
-                          plan->h_fz.as<double>(), n_fld, plan->h_out.as<double>(), st, timings));
+                          plan->h_S.as<double>(), n_src, dfr, dfz, n_fld,
+                          plan->h_out.as<double>(), st, timings));
     if (n_fld > 0)
         CK(cudaMemcpyAsync(out_Phi, plan->h_out.p, 16 * (size_t)n_fld * K, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
