@@ -496,6 +496,49 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool va
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+// Bulk (TMA, 1-D) global -> shared copies completing on an mbarrier (sm_90+/sm_100a).
+__device__ __forceinline__ unsigned smem_u32(const void *p)
+{
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async()
+{
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_mbar_init()
+{
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
 template <int RM, int RN, int TM, int TN, int MP, int NC, int MASK, int PF>
@@ -574,8 +617,67 @@ __device__ __forceinline__ void s2l_gemm_dispatch(int mask, const double *As, co
     }
 }
 
+// Blocked-column GEMM (PF == 2): thread tn owns the RN consecutive columns tn*RN.. (RN/2 whole
+// boxes), so B fragments load as 16-byte vectors and a whole warp can skip an offset none of its
+// boxes interacts with (warp-uniform branch, no mask instantiations).
+template <int RM, int RN, int TM, int MP, int NC>
+__device__ __forceinline__ void s2l_gemm_blk(const double *As, const double *Bs, int kc, int tm,
+                                             int tn, double (&acc)[RM][RN])
+{
+#pragma unroll 2
+    for (int kk = 0; kk < kc; ++kk) {
+        double av[RM], bv[RN];
+#pragma unroll
+        for (int u = 0; u < RM / 2; ++u) {
+            double2 t = *reinterpret_cast<const double2 *>(As + kk * MP + 2 * (tm + TM * u));
+            av[2 * u] = t.x;
+            av[2 * u + 1] = t.y;
+        }
+#pragma unroll
+        for (int v = 0; v < RN / 2; ++v) {
+            double2 t = *reinterpret_cast<const double2 *>(Bs + kk * NC + tn * RN + 2 * v);
+            bv[2 * v] = t.x;
+            bv[2 * v + 1] = t.y;
+        }
+#pragma unroll
+        for (int u = 0; u < RM; ++u)
+#pragma unroll
+            for (int v = 0; v < RN; ++v) acc[u][v] = fma(av[u], bv[v], acc[u][v]);
+    }
+}
+
+// Box-major GEMM (PF == 3): B staged by bulk copies as [box][BPS] complex rows (BPS odd: the
+// four boxes a warp reads per step fall in distinct bank groups); thread tn owns boxes
+// tn*RN/2 .. +RN/2-1 (both re and im columns of each).
+template <int RM, int RN, int TM, int MP>
+__device__ __forceinline__ void s2l_gemm_box(const double *As, const double2 *Bs, int BPS, int kc,
+                                             int tm, int tn, double (&acc)[RM][RN])
+{
+    const double2 *Bt = Bs + (tn * RN / 2) * BPS;
+#pragma unroll 2
+    for (int kk = 0; kk < kc; ++kk) {
+        double av[RM], bv[RN];
+#pragma unroll
+        for (int u = 0; u < RM / 2; ++u) {
+            double2 t = *reinterpret_cast<const double2 *>(As + kk * MP + 2 * (tm + TM * u));
+            av[2 * u] = t.x;
+            av[2 * u + 1] = t.y;
+        }
+#pragma unroll
+        for (int v = 0; v < RN / 2; ++v) {
+            double2 t = Bt[v * BPS + kk];
+            bv[2 * v] = t.x;
+            bv[2 * v + 1] = t.y;
+        }
+#pragma unroll
+        for (int u = 0; u < RM; ++u)
+#pragma unroll
+            for (int v = 0; v < RN; ++v) acc[u][v] = fma(av[u], bv[v], acc[u][v]);
+    }
+}
+
 template <int NT, int TM, int RM, int RN, int KC, int ST, int PF, int PC>
-__global__ void __launch_bounds__(NT) s2l_kernel(FarArgs a, S2LGrid gr)
+__global__ void __launch_bounds__(NT, (RM * RN >= 40 ? 256 : 512) / NT) s2l_kernel(FarArgs a, S2LGrid gr)
 {
     using Cfg = S2LCfg<NT, TM, RM, RN, KC, ST, PF, PC>;
     constexpr int TN = Cfg::TN, MP = Cfg::MP, NC = Cfg::NCP, JT = Cfg::JT, JH = Cfg::JH;
@@ -586,14 +688,21 @@ __global__ void __launch_bounds__(NT) s2l_kernel(FarArgs a, S2LGrid gr)
     // every index division below is by a constant
     const int p = PC ? PC : a.p, P = PC ? (PC + 1) * (PC + 2) / 2 : a.P, KW = a.m1 - a.m0;
     const int TP = (p + 1) * (p + 1) * (p + 1), TPp = TP + (TP & 1), HST = TPp + 2;
+    constexpr bool TMA = PF == 3;                  // box-major B staged by bulk copies
+    const int BPS = P | 1;                         // TMA: complex row stride per box (odd)
     double *As = sm;                               // [KC][MP]
-    double *Bs0 = As + KC * MP;                    // 2 x [P][NC]
-    double *Hs0 = Bs0 + ST * P * NC;               // ST x [HST], Hs[TPp] = 0 (masked entries)
-    double *post = Hs0 + ST * HST;                 // [P] 1 / l!
+    double *Bs0 = As + KC * MP;                    // ST x [P][NC] (TMA: [JT][BPS] complex)
+    double *Hs0 = Bs0 + (TMA ? 2 * JT * BPS : ST * P * NC);   // ST x [HST], Hs[TPp] = 0
+    uint64_t *bar = reinterpret_cast<uint64_t *>(Hs0 + ST * HST);   // TMA completion barrier
+    double *post = reinterpret_cast<double *>(bar + 1);            // [P] 1 / l!
     int *tsl = reinterpret_cast<int *>(post + P);  // [JT]  (box b: parity b / JH, index b % JH)
     int *ssl = tsl + JT;                           // [NOFF][JT]
     int *olist = ssl + NOFF * JT;                  // [NOFF] active offsets
     int *nact = olist + NOFF;
+    unsigned *omask = reinterpret_cast<unsigned *>(nact + 1);   // [NOFF] boxes with a source
+    constexpr bool BLK = PF >= 2;                  // blocked columns (box-aligned per thread)
+    static_assert(!BLK || JT <= 32, "box bit masks are 32-bit");
+    static_assert(!TMA || ST == 1, "bulk-copy staging is single-stage");
 
     const int nloc = (int)(blockIdx.x % KW);
     int64_t bid = a.s2l_tiles[blockIdx.x / KW];      // active tile (s2l_tile_flags_kernel)
@@ -636,6 +745,10 @@ __global__ void __launch_bounds__(NT) s2l_kernel(FarArgs a, S2LGrid gr)
         post[q] = 1.0 / f;
     }
     if (tid < ST) Hs0[tid * HST + TPp] = 0.0;
+    if (TMA && tid == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
     __syncthreads();
     for (int q = tid; q < NOFF * JT; q += NT) {
         int o = q / JT, b = q % JT;
@@ -649,18 +762,39 @@ __global__ void __launch_bounds__(NT) s2l_kernel(FarArgs a, S2LGrid gr)
     }
     __syncthreads();
     // compact the active offsets (fixed order) with their column-block masks
-    if (tid == 0) {
+    if (BLK && tid < 32) {
+        // warp 0: one ballot per offset over the (<= 32) boxes
+        int k = 0;
+        unsigned long long npairs = 0;
+        for (int o = 0; o < NOFF; ++o) {
+            const unsigned bm = __ballot_sync(0xffffffffu, tid < JT && ssl[o * JT + tid] >= 0);
+            if (!bm) continue;
+            npairs += __popc(bm);
+            if (tid == 0) {
+                omask[k] = bm;
+                olist[k] = (olist[o] & 0xff) | (o << 8);
+            }
+            ++k;
+        }
+        if (tid == 0) {
+            *nact = k;
+            if (nloc == 0 && a.m0 == 0 && a.s2l_pairs && npairs) atomicAdd(a.s2l_pairs, npairs);
+        }
+    } else if (!BLK && tid == 0) {
         int k = 0;
         unsigned long long npairs = 0;
         for (int o = 0; o < NOFF; ++o) {
             int mask = 0, cnt = 0;
+            unsigned bm = 0;
             for (int b = 0; b < JT; ++b)
                 if (ssl[o * JT + b] >= 0) {
                     ++cnt;
-                    mask |= 1 << ((2 * b) / TN);   // column block of box b
+                    mask |= 1 << ((2 * b) / TN);   // column block of box b (strided layout)
+                    bm |= 1u << b;                  // box bit (blocked layout)
                 }
             if (!cnt) continue;
             npairs += cnt;
+            omask[k] = bm;
             olist[k++] = (olist[o] & 0xff) | (o << 8) | (mask << 16);
         }
         *nact = k;
@@ -674,6 +808,14 @@ __global__ void __launch_bounds__(NT) s2l_kernel(FarArgs a, S2LGrid gr)
     for (int u = 0; u < RM; ++u)
 #pragma unroll
         for (int v = 0; v < RN; ++v) acc[u][v] = 0.0;
+    // boxes covered by this warp (blocked layout: thread tn owns boxes tn*RN/2 .. +RN/2-1)
+    unsigned wbox = 0;
+    if constexpr (BLK) {
+        unsigned mine = 0;
+#pragma unroll
+        for (int v = 0; v < RN; v += 2) mine |= 1u << ((tn * RN + v) >> 1);
+        wbox = __reduce_or_sync(0xffffffffu, mine);
+    }
 
     // async stage of offset k into buffer (k % ST): tensor block + (pre-scaled) moments
     auto stage = [&](int k) {
@@ -693,15 +835,47 @@ __global__ void __launch_bounds__(NT) s2l_kernel(FarArgs a, S2LGrid gr)
         }
         cp_async_commit();
     };
-    if (ST == 2 && na > 0) stage(0);
+    // TMA stage of offset k: the station's tensor block and one bulk copy per source box
+    // (rows of boxes without a source at this offset are zeroed by plain stores)
+    auto stage_tma = [&](int k) {
+        const int code = olist[k];
+        const int di = ((code >> 4) & 15) - 3, dj = (code & 15) - 3, o = (code >> 8) & 0xff;
+        const int is = it + di;
+        const int iin = min(it, is), dI = di < 0 ? -di : di, dJ = dj < 0 ? -dj : dj;
+        const double *Tn = a.tens + ((int64_t)(iin * 12 + class_of(dI, dJ)) * KW + nloc) * TPp;
+        double2 *Bs = reinterpret_cast<double2 *>(Bs0);
+        const unsigned bm = omask[k];
+        if (tid < 32) {
+            if (tid == 0) {
+                fence_proxy_async();
+                mbar_arrive_expect_tx(bar, (unsigned)(TPp * 8 + __popc(bm) * P * 16));
+                bulk_g2s(Hs0, Tn, (unsigned)(TPp * 8), bar);
+            }
+            __syncwarp();
+            if (tid < JT && ((bm >> tid) & 1u)) {
+                const int sl = ssl[o * JT + tid];
+                bulk_g2s(Bs + tid * BPS, a.M + ((a.soff[level] + sl) * (int64_t)KW + nloc) * P,
+                         (unsigned)(P * 16), bar);
+            }
+        }
+        for (int q = tid; q < JT * P; q += NT) {
+            const int b = q / P;
+            if (!((bm >> b) & 1u)) Bs[b * BPS + (q - b * P)] = make_double2(0.0, 0.0);
+        }
+        mbar_wait(bar, (unsigned)(k & 1));
+    };
+    if (!TMA && ST == 2 && na > 0) stage(0);
     for (int k = 0; k < na; ++k) {
-        if (ST == 1) {
+        if (TMA) {
+            __syncthreads();                  // GEMM k-1 done with As, Bs, Hs
+            stage_tma(k);
+        } else if (ST == 1) {
             if (k > 0) __syncthreads();       // GEMM k-1 done with the single buffer
             stage(k);
         }
-        cp_async_wait_all();
+        if (!TMA) cp_async_wait_all();
         __syncthreads();                      // buffer k ready; As free
-        if (ST == 2 && k + 1 < na) stage(k + 1);   // overlaps the operator build and GEMM below
+        if (!TMA && ST == 2 && k + 1 < na) stage(k + 1);   // overlaps the build and GEMM below
         const int code = olist[k];
         const int di = ((code >> 4) & 15) - 3, dj = (code & 15) - 3;
         const int mask = (code >> 16) & 0xff;
@@ -719,8 +893,16 @@ __global__ void __launch_bounds__(NT) s2l_kernel(FarArgs a, S2LGrid gr)
                 As[q] = (c & 1) ? -v : v;
             }
             __syncthreads();
-            s2l_gemm_dispatch<RM, RN, TM, TN, MP, NC, (1 << RN) - 1, PF>(mask, As, Bs + k0 * NC, kc,
-                                                                        tm, tn, acc);
+            if constexpr (TMA) {
+                if (omask[k] & wbox)
+                    s2l_gemm_box<RM, RN, TM, MP>(As, reinterpret_cast<const double2 *>(Bs0) + k0, BPS,
+                                                 kc, tm, tn, acc);
+            } else if constexpr (BLK) {
+                if (omask[k] & wbox) s2l_gemm_blk<RM, RN, TM, MP, NC>(As, Bs + k0 * NC, kc, tm, tn, acc);
+            } else {
+                s2l_gemm_dispatch<RM, RN, TM, TN, MP, NC, (1 << RN) - 1, PF>(mask, As, Bs + k0 * NC,
+                                                                            kc, tm, tn, acc);
+            }
         }
     }
     (void)BOXV;
@@ -728,7 +910,7 @@ __global__ void __launch_bounds__(NT) s2l_kernel(FarArgs a, S2LGrid gr)
     // written, zeros included, so the locals need no initialisation
 #pragma unroll
     for (int v = 0; v < RN; ++v) {
-        int col = tn + TN * v, b = col >> 1, im = col & 1;
+        int col = BLK ? tn * RN + v : tn + TN * v, b = col >> 1, im = col & 1;
         int s = tsl[b];
         if (s < 0) continue;
         double *dst = reinterpret_cast<double *>(a.Lc + ((a.toff[level] + s) * (int64_t)KW + nloc) * P);
@@ -787,8 +969,9 @@ inline size_t s2l_smem_bytes(int p)
 {
     using Cfg = S2LCfg<NT, TM, RM, RN, KC, ST, PF, PC>;
     int P = (p + 1) * (p + 2) / 2, TP = (p + 1) * (p + 1) * (p + 1), TPp = TP + (TP & 1);
-    return sizeof(double) * ((size_t)KC * Cfg::MP + ST * (size_t)P * Cfg::NCP + ST * (TPp + 2) + P) +
-           sizeof(int) * (Cfg::JT + Cfg::NOFF * Cfg::JT + Cfg::NOFF + 1);
+    const size_t bsz = PF == 3 ? (size_t)2 * Cfg::JT * (P | 1) : ST * (size_t)P * Cfg::NCP;
+    return sizeof(double) * ((size_t)KC * Cfg::MP + bsz + ST * (TPp + 2) + 1 + P) +
+           sizeof(int) * (Cfg::JT + Cfg::NOFF * Cfg::JT + 2 * Cfg::NOFF + 1);
 }
 
 // Near-field task list: one task per tile of <= TT field points of a non-empty target leaf.
