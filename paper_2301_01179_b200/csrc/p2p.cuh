@@ -66,7 +66,7 @@ __device__ __forceinline__ uint32_t compact1(uint32_t v)
 }
 
 template <int TT, int SC, int MAXT, bool NEAR>
-__global__ void __launch_bounds__(TT *SC) p2p_kernel(P2PArgs a)
+__global__ void __launch_bounds__(TT *SC, (MAXT > 6 ? 4 : 8)) p2p_kernel(P2PArgs a)
 {
     constexpr int NT = TT * SC;
     constexpr int NW = NT / 32;
