@@ -396,6 +396,11 @@ struct cylfmm_plan_s {
     bool ev_ok = false;
     int64_t launches = 0;
     int auto_kw = 0;   // last automatic mode chunk
+    // concurrency: the data-independent tensors and the near field run on their own streams,
+    // joined to the caller's stream by events (aev: start, tree, tensors, near, s2l)
+    cudaStream_t aux[2] = {nullptr, nullptr};
+    cudaEvent_t aev[5];
+    bool aux_ok = false;
 };
 
 static void free_plan_bufs(cylfmm_plan p)
@@ -433,6 +438,9 @@ extern "C" cylfmm_status cylfmm_plan_create(cylfmm_plan *plan, const cylfmm_para
     CK(cudaDeviceGetAttribute(&p->nsm, cudaDevAttrMultiProcessorCount, p->device));
     for (int i = 0; i < 16; ++i) CK(cudaEventCreate(&p->ev[i]));
     p->ev_ok = true;
+    for (int i = 0; i < 2; ++i) CK(cudaStreamCreateWithFlags(&p->aux[i], cudaStreamNonBlocking));
+    for (int i = 0; i < 5; ++i) CK(cudaEventCreateWithFlags(&p->aev[i], cudaEventDisableTiming));
+    p->aux_ok = true;
     {
         std::vector<int> tab;
         build_s2l_index(q.order, s2l_mp(q.order), q.truncation, tab);
@@ -450,6 +458,10 @@ extern "C" void cylfmm_plan_destroy(cylfmm_plan plan)
     free_plan_bufs(plan);
     if (plan->ev_ok)
         for (int i = 0; i < 16; ++i) cudaEventDestroy(plan->ev[i]);
+    if (plan->aux_ok) {
+        for (int i = 0; i < 2; ++i) cudaStreamDestroy(plan->aux[i]);
+        for (int i = 0; i < 5; ++i) cudaEventDestroy(plan->aev[i]);
+    }
     delete plan;
 }
 
@@ -690,6 +702,42 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     CK(cudaMemsetAsync(p->ctr.p, 0, sizeof(unsigned long long) * 4, st));
     T.mark();  // 0
     if (nf == 0) return CYLFMM_OK;
+    // Streams: the timings path runs every phase on `st` (clean per-phase events); otherwise the
+    // tensors (independent of the data: normalised stations) and the near field (independent of
+    // the far field) run on the plan's auxiliary streams and are joined by events.
+    const bool overlap = tm == nullptr && p->aux_ok;
+    cudaStream_t st_t = overlap ? p->aux[0] : st, st_n = overlap ? p->aux[1] : st;
+    const int64_t nstat = (int64_t)12 << d;
+    const int NM = std::max(K - 1, 1) + 1, D = 2 * pp + 1;
+    RET_IF(p->seeds.need(sizeof(double) * (size_t)nstat * 4 * NM * D));
+    TensorGeomArgs ta = {};
+    ta.station_mode = 1;
+    ta.n = nstat;
+    ta.K = K;
+    ta.m0 = 0;
+    ta.m1 = K;
+    ta.p = pp;
+    ta.miller = q.miller;
+    ta.fwd2 = forward_coef(std::max(K - 1, 1), q.miller);
+    ta.seeds = p->seeds.as<double>();
+    ta.packed = 1;
+    ta.err = p->err.as<int>();
+    double ms_seed = 0;
+    if (overlap) {
+        CK(cudaEventRecord(p->aev[0], st));
+        CK(cudaStreamWaitEvent(st_t, p->aev[0], 0));
+    } else if (tm) {
+        cudaEventRecord(p->ev[12], st);
+    }
+    RET_IF(run_seeds(ta, nstat, st_t));   // seeds of all modes once, behind the tree build
+    p->launches++;
+    if (tm) {
+        cudaEventRecord(p->ev[13], st);
+        cudaEventSynchronize(p->ev[13]);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, p->ev[12], p->ev[13]);
+        ms_seed = ms;
+    }
     // ---- tree
     int *sperm = nullptr, *fperm = nullptr;
     uint32_t *skey_s = nullptr, *fkey_s = nullptr;
@@ -822,8 +870,6 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         ttot += fa.tcount[l];
     }
     const int64_t TP = (int64_t)(pp + 1) * (pp + 1) * (pp + 1) + ((pp + 1) & 1);  // padded
-    const int64_t nstat = (int64_t)12 << d;
-    const int NM = std::max(K - 1, 1) + 1, D = 2 * pp + 1;
     if (q.mode_chunk == 0) {
         // automatic chunk: the far-field workspace (moments, locals, tensors per mode) of one
         // chunk must fit in a third of the free device memory (C5: 1.8 GB per mode).  The free
@@ -846,7 +892,6 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     RET_IF(p->M.need(sizeof(double2) * (size_t)std::max<int64_t>(stot, 1) * KW * P));
     RET_IF(p->Lc.need(sizeof(double2) * (size_t)std::max<int64_t>(ttot, 1) * KW * P));
     RET_IF(p->tens.need(sizeof(double) * (size_t)nstat * KW * TP));
-    RET_IF(p->seeds.need(sizeof(double) * (size_t)nstat * 4 * NM * D));
     fa.M = p->M.as<double2>();
     fa.Lc = p->Lc.as<double2>();
     fa.tens = p->tens.as<double>();
@@ -865,7 +910,8 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     fa.s2l_written = p->written.as<unsigned char>();
     for (int l = 2; l <= d; ++l) fa.lvoff[l] = lvoff[l];
     const int64_t ntiles_act = hcnt[2 * kMaxLevels];
-    double ms_tensor = 0, ms_p2m = 0, ms_m2m = 0, ms_s2l = 0, ms_l2l = 0, ms_l2p = 0;
+    fa.l2p_accumulate = ns > 0;   // L2P adds the far field onto the near field's rows
+    double ms_tensor = ms_seed, ms_p2m = 0, ms_m2m = 0, ms_s2l = 0, ms_l2l = 0, ms_l2p = 0;
     cudaEvent_t e0 = p->ev[10], e1 = p->ev[11];
     auto tic = [&]() { if (tm) cudaEventRecord(e0, st); };
     auto toc = [&](double &acc) {
@@ -886,6 +932,62 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         CKL();
         p->launches++;
     }
+    // ---- near field: writes every field row (the far field is added by L2P)
+    tic();
+    double ms_p2p = 0;
+    if (ns > 0) {
+        if (overlap) {
+            CK(cudaEventRecord(p->aev[1], st));
+            CK(cudaStreamWaitEvent(st_n, p->aev[1], 0));
+        }
+        const int ntl = fa.tcount[d];
+        double avg = (double)nf / std::max(ntl, 1);
+        const int TT = avg <= 10.0 ? 8 : (avg <= 24.0 ? 16 : 32);
+        RET_IF(p->tcnt.need(sizeof(int) * (ntl + 1)));
+        RET_IF(p->ntasks.need(sizeof(int)));
+        int64_t maxtasks = nf / TT + ntl + 1;
+        RET_IF(p->tasks.need(sizeof(int4) * maxtasks));
+        near_tasks_count_kernel<<<nblk(ntl, 256), 256, 0, st_n>>>(fa.tkeys[d], ntl, fa.flstart, TT,
+                                                               p->tcnt.as<int>());
+        CKL();
+        RET_IF(scan_excl(p, p->tcnt.as<int>(), ntl, st_n));
+        near_tasks_emit_kernel<<<nblk(ntl, 256), 256, 0, st_n>>>(fa.tkeys[d], ntl, fa.flstart, TT,
+                                                              p->tcnt.as<int>(), p->tasks.as<int4>(),
+                                                              p->ntasks.as<int>());
+        CKL();
+        p->launches += 2;
+        unsigned long long *ctr = p->ctr.as<unsigned long long>();
+        for (int m0 = 0; m0 < K; m0 += kP2PWindow) {
+            P2PArgs a = {};
+            a.sr = fa.sr;
+            a.sz = fa.sz;
+            a.S = fa.S;
+            a.fr = fa.fr;
+            a.fz = fa.fz;
+            a.ns = ns;
+            a.nf = nf;
+            a.K = K;
+            a.m0 = m0;
+            a.m1 = std::min(K, m0 + kP2PWindow);
+            a.miller = q.miller;
+            a.fwd2 = forward_coef(K - 1, q.miller);
+            a.exclude = q.exclude_coincident;
+            a.out = fa.out;
+            a.out_row = fperm;
+            a.accumulate = 0;
+            a.tasks = p->tasks.as<int4>();
+            a.ntasks = p->ntasks.as<int>();
+            a.leafstart = fa.slstart;
+            a.depth = d;
+            a.n_skipped = ctr + 0;
+            a.n_pairs = ctr + 1;
+            a.err_flag = p->err.as<int>();
+            CK(launch_p2p<true>(TT, a, dim3((unsigned)maxtasks), st_n));
+            p->launches++;
+        }
+        if (overlap) CK(cudaEventRecord(p->aev[3], st_n));
+    }
+    toc(ms_p2p);
     for (int m0 = 0; m0 < K; m0 += KW) {
         fa.m0 = m0;
         fa.m1 = std::min(K, m0 + KW);
@@ -894,28 +996,14 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         // the Laplace fill per mode chunk
         tic();
         {
-            TensorGeomArgs ta = {};
-            ta.station_mode = 1;
-            ta.n = nstat;
-            ta.K = K;
-            ta.m0 = 0;
-            ta.m1 = K;
-            ta.p = pp;
-            ta.miller = q.miller;
-            ta.fwd2 = forward_coef(std::max(K - 1, 1), q.miller);
-            ta.seeds = p->seeds.as<double>();
             ta.out = p->tens.as<double>();
-            ta.packed = 1;
-            ta.err = p->err.as<int>();
-            if (m0 == 0) {
-                RET_IF(run_seeds(ta, nstat, st));
-                p->launches++;
-            }
             ta.m0 = fa.m0;
             ta.m1 = fa.m1;
             ta.seed_m1 = K;
-            RET_IF(run_fill(ta, nstat, st));
+            if (overlap && m0 > 0) CK(cudaStreamWaitEvent(st_t, p->aev[4], 0));  // previous S2L done
+            RET_IF(run_fill(ta, nstat, st_t));
             p->launches++;
+            if (overlap) CK(cudaEventRecord(p->aev[2], st_t));
         }
         toc(ms_tensor);
         if (ns > 0) {
@@ -943,10 +1031,12 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         }
         // S2L of every level in one launch (each level's contribution), then the L2L chain
         tic();
+        if (overlap) CK(cudaStreamWaitEvent(st, p->aev[2], 0));   // tensors of this chunk ready
         if (ns > 0 && ntiles_act > 0) {
             CK(launch_s2l(fa, ntiles_act, st));
             p->launches++;
         }
+        if (overlap) CK(cudaEventRecord(p->aev[4], st));
         toc(ms_s2l);
         tic();
         for (int l = 3; l <= d; ++l) {
@@ -960,6 +1050,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         }
         toc(ms_l2l);
         tic();
+        if (overlap && ns > 0 && m0 == 0) CK(cudaStreamWaitEvent(st, p->aev[3], 0));  // near field
         {
             int ngrp = (kw + kL2PModes - 1) / kL2PModes;
             size_t sm = sizeof(double2) * kL2PModes * P + sizeof(double) * kL2PPts * P;
@@ -969,57 +1060,6 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         }
         toc(ms_l2p);
     }
-    // ---- near field
-    tic();
-    double ms_p2p = 0;
-    if (ns > 0) {
-        const int ntl = fa.tcount[d];
-        double avg = (double)nf / std::max(ntl, 1);
-        const int TT = avg <= 10.0 ? 8 : (avg <= 24.0 ? 16 : 32);
-        RET_IF(p->tcnt.need(sizeof(int) * (ntl + 1)));
-        RET_IF(p->ntasks.need(sizeof(int)));
-        int64_t maxtasks = nf / TT + ntl + 1;
-        RET_IF(p->tasks.need(sizeof(int4) * maxtasks));
-        near_tasks_count_kernel<<<nblk(ntl, 256), 256, 0, st>>>(fa.tkeys[d], ntl, fa.flstart, TT,
-                                                               p->tcnt.as<int>());
-        CKL();
-        RET_IF(scan_excl(p, p->tcnt.as<int>(), ntl, st));
-        near_tasks_emit_kernel<<<nblk(ntl, 256), 256, 0, st>>>(fa.tkeys[d], ntl, fa.flstart, TT,
-                                                              p->tcnt.as<int>(), p->tasks.as<int4>(),
-                                                              p->ntasks.as<int>());
-        CKL();
-        p->launches += 2;
-        unsigned long long *ctr = p->ctr.as<unsigned long long>();
-        for (int m0 = 0; m0 < K; m0 += kP2PWindow) {
-            P2PArgs a = {};
-            a.sr = fa.sr;
-            a.sz = fa.sz;
-            a.S = fa.S;
-            a.fr = fa.fr;
-            a.fz = fa.fz;
-            a.ns = ns;
-            a.nf = nf;
-            a.K = K;
-            a.m0 = m0;
-            a.m1 = std::min(K, m0 + kP2PWindow);
-            a.miller = q.miller;
-            a.fwd2 = forward_coef(K - 1, q.miller);
-            a.exclude = q.exclude_coincident;
-            a.out = fa.out;
-            a.out_row = fperm;
-            a.accumulate = 1;
-            a.tasks = p->tasks.as<int4>();
-            a.ntasks = p->ntasks.as<int>();
-            a.leafstart = fa.slstart;
-            a.depth = d;
-            a.n_skipped = ctr + 0;
-            a.n_pairs = ctr + 1;
-            a.err_flag = p->err.as<int>();
-            CK(launch_p2p<true>(TT, a, dim3((unsigned)maxtasks), st));
-            p->launches++;
-        }
-    }
-    toc(ms_p2p);
     T.mark();
     if (tm) {
         unsigned long long c[4] = {0, 0, 0, 0};
@@ -1028,7 +1068,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         float ms_tree = 0, ms_total = 0;
         cudaEventElapsedTime(&ms_tree, p->ev[0], p->ev[1]);
         cudaEventElapsedTime(&ms_total, p->ev[0], p->ev[2]);
-        tm->ms_tree = ms_tree;
+        tm->ms_tree = ms_tree - ms_seed;   // the seeds ran first on st in the timed path
         tm->ms_p2m = ms_p2m;
         tm->ms_m2m = ms_m2m;
         tm->ms_tensor = ms_tensor;

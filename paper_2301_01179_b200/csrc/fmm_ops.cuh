@@ -47,6 +47,7 @@ struct FarArgs {
     const unsigned char *s2l_written;   // dense per level [lvoff[l] + key]: local written by S2L
     int64_t lvoff[kMaxLevels];          // dense per-level offsets (level maps, s2l_written)
     const unsigned char *need;          // dense per level: local materialised (see need_kernel)
+    int l2p_accumulate;                 // L2P adds onto out (the near field wrote it first)
 };
 
 __device__ __forceinline__ int tri(int i, int j, int p) { return i * (p + 1) - i * (i - 1) / 2 + j; }
@@ -394,7 +395,13 @@ __global__ void __launch_bounds__(256) l2p_kernel(FarArgs a)
                 sy = fma(lo[kl].y, mo[kl], sy);
             }
             int64_t row = a.fperm[c0 + t];
-            a.out[row * a.K + a.m0 + n0 + n] = make_double2(sx * inv_h, sy * inv_h);
+            double2 *o = a.out + row * a.K + a.m0 + n0 + n;
+            if (a.l2p_accumulate) {
+                const double2 cur = *o;
+                *o = make_double2(fma(sx, inv_h, cur.x), fma(sy, inv_h, cur.y));
+            } else {
+                *o = make_double2(sx * inv_h, sy * inv_h);
+            }
         }
     }
 }
