@@ -84,16 +84,17 @@ static cudaError_t allow_smem(F *kernel)
 // double-buffered one by 11-20%; a register double buffer gains nothing; blocked columns with
 // warp-level offset skipping (PF 2) beat the strided/masked layout (PF 0) by 3-23%.
 // PF 3 = blocked + box-major B staged by TMA bulk copies on an mbarrier (default: C2 S2L
-// 0.49 -> 0.45 ms, C3 21.7 -> 20.2 ms, C4 98.6 -> 93.8 ms).
+// 0.49 -> 0.45 ms, C3 21.7 -> 20.2 ms, C4 98.6 -> 93.8 ms); double-buffering the TMA stages
+// (ST 2, V1) halves the resident CTAs and is 20-50% slower.
 #define S2L_P8 128, 8, 6, 4, 48, 1, 3
-#define S2L_P8_V1 128, 8, 6, 4, 48, 1, 2
-#define S2L_P8_V2 128, 8, 6, 4, 48, 1, 0
+#define S2L_P8_V1 128, 8, 6, 4, 48, 2, 3
+#define S2L_P8_V2 128, 8, 6, 4, 48, 1, 2
 #define S2L_P12 256, 16, 6, 4, 16, 1, 3
-#define S2L_P12_V1 256, 16, 6, 4, 16, 1, 2
-#define S2L_P12_V2 256, 16, 6, 4, 16, 1, 0
+#define S2L_P12_V1 256, 16, 6, 4, 16, 2, 3
+#define S2L_P12_V2 256, 16, 6, 4, 16, 1, 2
 #define S2L_P16 256, 16, 10, 2, 16, 1, 3
-#define S2L_P16_V1 256, 16, 10, 2, 16, 1, 2
-#define S2L_P16_V2 256, 16, 10, 2, 16, 1, 0
+#define S2L_P16_V1 256, 16, 10, 2, 16, 2, 3
+#define S2L_P16_V2 256, 16, 10, 2, 16, 1, 2
 // each tiling is instantiated for a runtime order (0) and for the BASELINE order of its class
 #define S2L_ALL(X) X(S2L_P8, 0) X(S2L_P8, 8) X(S2L_P8_V1, 0) X(S2L_P8_V1, 8) X(S2L_P8_V2, 0)      \
     X(S2L_P8_V2, 8) X(S2L_P12, 0) X(S2L_P12, 12) X(S2L_P12_V1, 0) X(S2L_P12_V1, 12)              \

@@ -699,9 +699,9 @@ __global__ void __launch_bounds__(NT, (RM * RN >= 40 ? 256 : 512) / NT) s2l_kern
     const int BPS = P | 1;                         // TMA: complex row stride per box (odd)
     double *As = sm;                               // [KC][MP]
     double *Bs0 = As + KC * MP;                    // ST x [P][NC] (TMA: [JT][BPS] complex)
-    double *Hs0 = Bs0 + (TMA ? 2 * JT * BPS : ST * P * NC);   // ST x [HST], Hs[TPp] = 0
-    uint64_t *bar = reinterpret_cast<uint64_t *>(Hs0 + ST * HST);   // TMA completion barrier
-    double *post = reinterpret_cast<double *>(bar + 1);            // [P] 1 / l!
+    double *Hs0 = Bs0 + (TMA ? ST * 2 * JT * BPS : ST * P * NC);   // ST x [HST], Hs[TPp] = 0
+    uint64_t *bar = reinterpret_cast<uint64_t *>(Hs0 + ST * HST);   // TMA barriers, one per stage
+    double *post = reinterpret_cast<double *>(bar + 2);            // [P] 1 / l!
     int *tsl = reinterpret_cast<int *>(post + P);  // [JT]  (box b: parity b / JH, index b % JH)
     int *ssl = tsl + JT;                           // [NOFF][JT]
     int *olist = ssl + NOFF * JT;                  // [NOFF] active offsets
@@ -709,7 +709,6 @@ __global__ void __launch_bounds__(NT, (RM * RN >= 40 ? 256 : 512) / NT) s2l_kern
     unsigned *omask = reinterpret_cast<unsigned *>(nact + 1);   // [NOFF] boxes with a source
     constexpr bool BLK = PF >= 2;                  // blocked columns (box-aligned per thread)
     static_assert(!BLK || JT <= 32, "box bit masks are 32-bit");
-    static_assert(!TMA || ST == 1, "bulk-copy staging is single-stage");
 
     const int nloc = (int)(blockIdx.x % KW);
     int64_t bid = a.s2l_tiles[blockIdx.x / KW];      // active tile (s2l_tile_flags_kernel)
@@ -753,7 +752,7 @@ __global__ void __launch_bounds__(NT, (RM * RN >= 40 ? 256 : 512) / NT) s2l_kern
     }
     if (tid < ST) Hs0[tid * HST + TPp] = 0.0;
     if (TMA && tid == 0) {
-        mbar_init(bar, 1);
+        for (int b = 0; b < ST; ++b) mbar_init(bar + b, 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -842,54 +841,61 @@ __global__ void __launch_bounds__(NT, (RM * RN >= 40 ? 256 : 512) / NT) s2l_kern
         }
         cp_async_commit();
     };
-    // TMA stage of offset k: the station's tensor block and one bulk copy per source box
-    // (rows of boxes without a source at this offset are zeroed by plain stores)
-    auto stage_tma = [&](int k) {
+    // TMA stage of offset k into buffer bf: the station's tensor block and one bulk copy per
+    // source box; rows of boxes without a source at this offset are zeroed by plain stores.
+    // The caller guarantees no thread still reads buffer bf (a block barrier precedes).
+    auto tma_issue = [&](int k, int bf) {
         const int code = olist[k];
         const int di = ((code >> 4) & 15) - 3, dj = (code & 15) - 3, o = (code >> 8) & 0xff;
         const int is = it + di;
         const int iin = min(it, is), dI = di < 0 ? -di : di, dJ = dj < 0 ? -dj : dj;
         const double *Tn = a.tens + ((int64_t)(iin * 12 + class_of(dI, dJ)) * KW + nloc) * TPp;
-        double2 *Bs = reinterpret_cast<double2 *>(Bs0);
+        double2 *Bs = reinterpret_cast<double2 *>(Bs0) + (size_t)bf * JT * BPS;
         const unsigned bm = omask[k];
         if (tid < 32) {
             if (tid == 0) {
                 fence_proxy_async();
-                mbar_arrive_expect_tx(bar, (unsigned)(TPp * 8 + __popc(bm) * P * 16));
-                bulk_g2s(Hs0, Tn, (unsigned)(TPp * 8), bar);
+                mbar_arrive_expect_tx(bar + bf, (unsigned)(TPp * 8 + __popc(bm) * P * 16));
+                bulk_g2s(Hs0 + bf * HST, Tn, (unsigned)(TPp * 8), bar + bf);
             }
             __syncwarp();
             if (tid < JT && ((bm >> tid) & 1u)) {
                 const int sl = ssl[o * JT + tid];
                 bulk_g2s(Bs + tid * BPS, a.M + ((a.soff[level] + sl) * (int64_t)KW + nloc) * P,
-                         (unsigned)(P * 16), bar);
+                         (unsigned)(P * 16), bar + bf);
             }
         }
-        for (int q = tid; q < JT * P; q += NT) {
-            const int b = q / P;
-            if (!((bm >> b) & 1u)) Bs[b * BPS + (q - b * P)] = make_double2(0.0, 0.0);
-        }
-        mbar_wait(bar, (unsigned)(k & 1));
+        for (int b = tid >> 5; b < JT; b += NT / 32)
+            if (!((bm >> b) & 1u))
+                for (int kk = tid & 31; kk < P; kk += 32) Bs[b * BPS + kk] = make_double2(0.0, 0.0);
     };
+    if (TMA && na > 0) tma_issue(0, 0);
     if (!TMA && ST == 2 && na > 0) stage(0);
     for (int k = 0; k < na; ++k) {
+        const int buf = ST == 2 ? (k & 1) : 0;
         if (TMA) {
-            __syncthreads();                  // GEMM k-1 done with As, Bs, Hs
-            stage_tma(k);
-        } else if (ST == 1) {
-            if (k > 0) __syncthreads();       // GEMM k-1 done with the single buffer
-            stage(k);
+            if (ST == 1 && k > 0) {
+                __syncthreads();              // GEMM k-1 done with the single buffer and As
+                tma_issue(k, 0);
+            }
+            mbar_wait(bar + buf, (unsigned)((ST == 2 ? (k >> 1) : k) & 1));
+        } else {
+            if (ST == 1) {
+                if (k > 0) __syncthreads();   // GEMM k-1 done with the single buffer
+                stage(k);
+            }
+            cp_async_wait_all();
         }
-        if (!TMA) cp_async_wait_all();
-        __syncthreads();                      // buffer k ready; As free
+        __syncthreads();                      // buffer k ready (zero rows visible); As free
         if (!TMA && ST == 2 && k + 1 < na) stage(k + 1);   // overlaps the build and GEMM below
         const int code = olist[k];
         const int di = ((code >> 4) & 15) - 3, dj = (code & 15) - 3;
         const int mask = (code >> 16) & 0xff;
         const int variant = (di <= 0 ? 0 : 2) + (dj <= 0 ? 0 : 1);   // FO, BO, FI, BI
         const int *itab = a.s2l_idx + (size_t)variant * P * MP;
-        const double *Hs = Hs0 + (k % ST) * HST;
-        const double *Bs = Bs0 + (k % ST) * P * NC;
+        const double *Hs = Hs0 + buf * HST;
+        const double *Bs = Bs0 + buf * P * NC;
+        const double2 *Bt = reinterpret_cast<const double2 *>(Bs0) + (size_t)buf * JT * BPS;
         for (int k0 = 0; k0 < P; k0 += KC) {
             const int kc = min(KC, P - k0);
             if (k0 > 0) __syncthreads();
@@ -900,10 +906,12 @@ __global__ void __launch_bounds__(NT, (RM * RN >= 40 ? 256 : 512) / NT) s2l_kern
                 As[q] = (c & 1) ? -v : v;
             }
             __syncthreads();
+            // double-buffered TMA: the next offset's copies start now (every thread is past the
+            // GEMM that read buffer (k+1) & 1) and land behind this GEMM
+            if (TMA && ST == 2 && k0 == 0 && k + 1 < na) tma_issue(k + 1, (k + 1) & 1);
             if constexpr (TMA) {
                 if (omask[k] & wbox)
-                    s2l_gemm_box<RM, RN, TM, MP>(As, reinterpret_cast<const double2 *>(Bs0) + k0, BPS,
-                                                 kc, tm, tn, acc);
+                    s2l_gemm_box<RM, RN, TM, MP>(As, Bt + k0, BPS, kc, tm, tn, acc);
             } else if constexpr (BLK) {
                 if (omask[k] & wbox) s2l_gemm_blk<RM, RN, TM, MP, NC>(As, Bs + k0 * NC, kc, tm, tn, acc);
             } else {
@@ -911,6 +919,7 @@ __global__ void __launch_bounds__(NT, (RM * RN >= 40 ? 256 : 512) / NT) s2l_kern
                                                                             kc, tm, tn, acc);
             }
         }
+        if (TMA && ST == 2) __syncthreads();  // As is rebuilt for the next offset
     }
     (void)BOXV;
     // write the level's S2L contribution (post-scaled by 1/l!); every target of the tile is
@@ -976,8 +985,8 @@ inline size_t s2l_smem_bytes(int p)
 {
     using Cfg = S2LCfg<NT, TM, RM, RN, KC, ST, PF, PC>;
     int P = (p + 1) * (p + 2) / 2, TP = (p + 1) * (p + 1) * (p + 1), TPp = TP + (TP & 1);
-    const size_t bsz = PF == 3 ? (size_t)2 * Cfg::JT * (P | 1) : ST * (size_t)P * Cfg::NCP;
-    return sizeof(double) * ((size_t)KC * Cfg::MP + bsz + ST * (TPp + 2) + 1 + P) +
+    const size_t bsz = PF == 3 ? (size_t)ST * 2 * Cfg::JT * (P | 1) : ST * (size_t)P * Cfg::NCP;
+    return sizeof(double) * ((size_t)KC * Cfg::MP + bsz + ST * (TPp + 2) + 2 + P) +
            sizeof(int) * (Cfg::JT + Cfg::NOFF * Cfg::JT + 2 * Cfg::NOFF + 1);
 }
 
