@@ -796,7 +796,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     RET_IF(p->skeys.need(sizeof(int) * ltot));
     RET_IF(p->tmap.need(sizeof(int) * ltot));
     RET_IF(p->tkeys.need(sizeof(int) * ltot));
-    RET_IF(p->counts.need(sizeof(int) * (2 * kMaxLevels + 1)));
+    RET_IF(p->counts.need(sizeof(int) * (2 * kMaxLevels + 2)));
     int *tmap_b = same ? p->smap.as<int>() : p->tmap.as<int>();
     int *tkeys_b = same ? p->skeys.as<int>() : p->tkeys.as<int>();
     for (int side = 0; side < (same ? 1 : 2); ++side) {
@@ -822,7 +822,13 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     RET_IF(p->tpos.need(sizeof(int) * std::max<int64_t>(ntiles_all, 1)));
     RET_IF(p->tiles.need(sizeof(int) * std::max<int64_t>(ntiles_all, 1)));
     RET_IF(p->written.need(std::max<int64_t>(ltot, 1)));
-    CK(cudaMemsetAsync(p->counts.as<int>() + 2 * kMaxLevels, 0, sizeof(int), st));
+    CK(cudaMemsetAsync(p->counts.as<int>() + 2 * kMaxLevels, 0, 2 * sizeof(int), st));
+    if (ns > 0) {   // the largest source column at the leaf level bounds the stations S2L reads
+        max_col_kernel<<<nblk(std::min<int64_t>(ns, pow4(d)), 256), 256, 0, st>>>(
+            p->skeys.as<int>() + lvoff[d], p->counts.as<int>() + d, p->counts.as<int>() + 2 * kMaxLevels + 1);
+        CKL();
+        p->launches++;
+    }
     if (ntiles_all > 0) {
         TileArgs ta = {};
         for (int l = 2; l <= d; ++l) {
@@ -841,8 +847,8 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         CKL();
         p->launches += 2;
     }
-    int hcnt[2 * kMaxLevels + 1] = {0};
-    CK(cudaMemcpyAsync(hcnt, p->counts.p, sizeof(int) * (2 * kMaxLevels + 1), cudaMemcpyDeviceToHost, st));
+    int hcnt[2 * kMaxLevels + 2] = {0};
+    CK(cudaMemcpyAsync(hcnt, p->counts.p, sizeof(int) * (2 * kMaxLevels + 2), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     RET_IF(check_err_flag(p, st));
     if (same)
@@ -1002,7 +1008,9 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             ta.m1 = fa.m1;
             ta.seed_m1 = K;
             if (overlap && m0 > 0) CK(cudaStreamWaitEvent(st_t, p->aev[4], 0));  // previous S2L done
-            RET_IF(run_fill(ta, nstat, st_t));
+            // stations i_in <= the largest source column (C5: 35% of them) are the only ones read
+            const int64_t nstat_used = ns > 0 ? 12 * std::min<int64_t>(1 << d, hcnt[2 * kMaxLevels + 1] + 1) : 0;
+            if (nstat_used > 0) RET_IF(run_fill(ta, nstat_used, st_t));
             p->launches++;
             if (overlap) CK(cudaEventRecord(p->aev[2], st_t));
         }
@@ -1010,8 +1018,8 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         if (ns > 0) {
             tic();
             if (fa.scount[d] > 0) {
-                size_t sm = sizeof(double) * kP2MChunk * P + sizeof(double2) * kP2MChunk * kw;
-                p2m_kernel<<<fa.scount[d], kP2MThreads, sm, st>>>(fa);
+                const int nmb = (kw + kP2MModes - 1) / kP2MModes;
+                p2m_kernel<<<(unsigned)((int64_t)fa.scount[d] * nmb), kP2MThreads, p2m_smem(P), st>>>(fa);
                 CKL();
                 p->launches++;
             }

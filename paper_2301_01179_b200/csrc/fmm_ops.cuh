@@ -61,72 +61,90 @@ __device__ __forceinline__ void box_centre(uint32_t key, int level, double L, do
 }
 
 // ---------------------------------------------------------------------------------------------
-// P2M at the leaves: CTA per non-empty source leaf.  Outputs (n, ij) spread over threads, sources
-// streamed through smem in chunks of 32 with their monomials.
+// P2M at the leaves, as a small complex-by-real GEMM per leaf:
+//   M^(n)_ij = sum_q S_q^(n) mono_q[ij],  mono_q[ij] = ((r_q - r_c)/h)^i ((z_q - z_c)/h)^j.
+// CTA per (source leaf, block of kP2MModes modes); sources streamed through shared memory in
+// chunks of kP2MSrc (monomials computed once per chunk); thread tile = 2 modes x kP2MRC
+// coefficients in registers (20 DFMA per 7 shared loads per source).
 constexpr int kP2MThreads = 256;
-constexpr int kP2MChunk = 32;
-constexpr int kP2MOut = 4;
+constexpr int kP2MSrc = 32;
+constexpr int kP2MModes = 16;
+constexpr int kP2MRC = 5;
 
 __global__ void __launch_bounds__(kP2MThreads) p2m_kernel(FarArgs a)
 {
     extern __shared__ double sm[];
     const int p = a.p, P = a.P, KW = a.m1 - a.m0, d = a.depth;
-    double *mono = sm;                                           // [chunk][P]
-    double2 *Sx = reinterpret_cast<double2 *>(mono + kP2MChunk * P);  // [chunk][KW]
-    const int slot = blockIdx.x;
+    const int nmb = (KW + kP2MModes - 1) / kP2MModes;
+    const int slot = blockIdx.x / nmb, n0 = (blockIdx.x % nmb) * kP2MModes;
+    const int nm = min(kP2MModes, KW - n0);
+    double *mono = sm;                                                  // [kP2MSrc][P]
+    double2 *Sx = reinterpret_cast<double2 *>(mono + kP2MSrc * P);      // [kP2MSrc][kP2MModes]
     const uint32_t key = (uint32_t)a.skeys[d][slot];
     double rc, zc, h;
     box_centre(key, d, a.L, a.z0, rc, zc, h);
+    const double inv_h = 1.0 / h;
     const int q0 = a.slstart[key], q1 = a.slstart[key + 1];
-    double2 *Mo = a.M + (a.soff[d] + slot) * (int64_t)KW * P;
-    const int nout = KW * P;
-    for (int g0 = 0; g0 < nout; g0 += kP2MThreads * kP2MOut) {
-        double2 acc[kP2MOut];
+    const int tn = threadIdx.x % (kP2MModes / 2), tc = threadIdx.x / (kP2MModes / 2);
+    const int c0 = tc * kP2MRC;
+    const bool active = c0 < P;
+    double2 acc[2][kP2MRC];
 #pragma unroll
-        for (int k = 0; k < kP2MOut; ++k) acc[k] = make_double2(0.0, 0.0);
-        for (int c0 = q0; c0 < q1; c0 += kP2MChunk) {
-            const int nc = min(kP2MChunk, q1 - c0);
-            __syncthreads();
-            if (threadIdx.x < nc) {
-                int q = c0 + threadIdx.x;
-                double dr = (a.sr[q] - rc) / h, dz = (a.sz[q] - zc) / h;
-                double pr = 1.0;
-                for (int i = 0; i <= p; ++i) {
-                    double pz = pr;
-                    for (int j = 0; i + j <= p; ++j) {
-                        mono[threadIdx.x * P + tri(i, j, p)] = pz;
-                        pz *= dz;
-                    }
-                    pr *= dr;
-                }
-            }
-            for (int e = threadIdx.x; e < nc * KW; e += kP2MThreads) {
-                int q = e / KW, n = e % KW;
-                Sx[e] = a.S[(int64_t)(c0 + q) * a.K + a.m0 + n];
-            }
-            __syncthreads();
+    for (int v = 0; v < 2; ++v)
 #pragma unroll
-            for (int k = 0; k < kP2MOut; ++k) {
-                int o = g0 + threadIdx.x + k * kP2MThreads;
-                if (o < nout) {
-                    int n = o / P, ij = o % P;
-                    double2 s = acc[k];
-                    for (int q = 0; q < nc; ++q) {
-                        double m = mono[q * P + ij];
-                        double2 sv = Sx[q * KW + n];
-                        s.x = fma(sv.x, m, s.x);
-                        s.y = fma(sv.y, m, s.y);
-                    }
-                    acc[k] = s;
+        for (int u = 0; u < kP2MRC; ++u) acc[v][u] = make_double2(0.0, 0.0);
+    for (int s0 = q0; s0 < q1; s0 += kP2MSrc) {
+        const int nc = min(kP2MSrc, q1 - s0);
+        __syncthreads();
+        if (threadIdx.x < nc) {
+            const int q = s0 + threadIdx.x;
+            const double dr = (a.sr[q] - rc) * inv_h, dz = (a.sz[q] - zc) * inv_h;
+            double pr = 1.0;
+            for (int i = 0; i <= p; ++i) {
+                double pz = pr;
+                for (int j = 0; i + j <= p; ++j) {
+                    mono[threadIdx.x * P + tri(i, j, p)] = pz;
+                    pz *= dz;
                 }
+                pr *= dr;
             }
         }
+        for (int e = threadIdx.x; e < nc * kP2MModes; e += kP2MThreads) {
+            const int q = e / kP2MModes, n = e % kP2MModes;
+            Sx[e] = n < nm ? a.S[(int64_t)(s0 + q) * a.K + a.m0 + n0 + n] : make_double2(0.0, 0.0);
+        }
+        __syncthreads();
+        if (active) {
+            for (int q = 0; q < nc; ++q) {
+                const double2 sa = Sx[q * kP2MModes + 2 * tn], sb = Sx[q * kP2MModes + 2 * tn + 1];
+                const double *mq = mono + q * P + c0;
 #pragma unroll
-        for (int k = 0; k < kP2MOut; ++k) {
-            int o = g0 + threadIdx.x + k * kP2MThreads;
-            if (o < nout) Mo[o] = acc[k];
+                for (int u = 0; u < kP2MRC; ++u) {
+                    const double m = c0 + u < P ? mq[u] : 0.0;
+                    acc[0][u].x = fma(sa.x, m, acc[0][u].x);
+                    acc[0][u].y = fma(sa.y, m, acc[0][u].y);
+                    acc[1][u].x = fma(sb.x, m, acc[1][u].x);
+                    acc[1][u].y = fma(sb.y, m, acc[1][u].y);
+                }
+            }
         }
     }
+    if (active) {
+        double2 *Mo = a.M + (a.soff[d] + slot) * (int64_t)KW * P;
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+            const int n = n0 + 2 * tn + v;
+            if (2 * tn + v >= nm) continue;
+#pragma unroll
+            for (int u = 0; u < kP2MRC; ++u)
+                if (c0 + u < P) Mo[(int64_t)n * P + c0 + u] = acc[v][u];
+        }
+    }
+}
+
+inline size_t p2m_smem(int P)
+{
+    return sizeof(double) * kP2MSrc * P + sizeof(double2) * kP2MSrc * kP2MModes;
 }
 
 // binomial C(n, k) for n <= 2 * 20 (exact in FP64)

@@ -199,6 +199,19 @@ __global__ void level_map_kernel(const int *lstart, int depth, int level, const 
     if (b == nbox - 1) *count = s + (ne ? 1 : 0);
 }
 
+// largest radial box index among the non-empty boxes of a level (stations beyond it are unused)
+__global__ void max_col_kernel(const int *keys, const int *count, int *out)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= *count) return;
+    uint32_t v = (uint32_t)keys[i] & 0x55555555u;   // radial bits (even positions)
+    v = (v | (v >> 1)) & 0x33333333u;
+    v = (v | (v >> 2)) & 0x0f0f0f0fu;
+    v = (v | (v >> 4)) & 0x00ff00ffu;
+    v = (v | (v >> 8)) & 0x0000ffffu;
+    atomicMax(out, (int)v);
+}
+
 template <typename T>
 __global__ void gather_kernel(const T *in, const int *perm, int64_t n, T *out)
 {

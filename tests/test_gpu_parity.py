@@ -326,3 +326,22 @@ def test_fmm_full_size_sampled_vs_oracle_fmm(gpu, orc, name, sample):
     ref, _ = orc.fmm(pr.sr, pr.sz, pr.S, pr.fr[idx], pr.fz[idx], pr.p, pr.depth, pr.L, pr.z0)
     e = eps_modes(F, ref)
     assert e.max() <= TOL, (name, e)
+
+
+def test_edge_max_modes_min_order_max_depth(gpu, orc):
+    """Limits of the C-ABI (include/cylfmm.h): K = 256 modes (CYLFMM_MAX_MODES) in the direct sum,
+    order p = 1 and depth d = 11 (CYLFMM_MAX_DEPTH) in the FMM, a single source, and a field set
+    that is not the source set -- each against the oracle."""
+    rng = np.random.default_rng(11)
+    sr, sz, S = uniform_rings(rng, 64, 256)
+    fr, fz, _ = uniform_rings(rng, 40, 1)
+    ref, _ = orc.direct(sr, sz, S, fr, fz)
+    out = gpu.direct(sr, sz, S, fr, fz).cpu().numpy()
+    # K = 256: the forward branch (R#3 narrowed to lambda^(2N) <= 2^6) and Miller (start N + e)
+    assert eps_modes(out, ref).max() <= 3e-12
+    sr, sz, S = uniform_rings(rng, 900, 3)
+    for p, depth in [(1, 4), (3, 11)]:
+        out, ref, _ = _fmm_case(gpu, orc, sr, sz, S, fr, fz, p, depth, 1.0)
+        assert eps_modes(out, ref).max() <= TOL, (p, depth)
+    out, ref, _ = _fmm_case(gpu, orc, sr[:1], sz[:1], S[:1], fr, fz, 6, 3, 1.0)
+    assert eps_modes(out, ref).max() <= TOL
