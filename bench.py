@@ -309,11 +309,20 @@ def main():
     dom = max(("s2l", phase["ms_s2l"]), ("p2p", phase["ms_p2p"]), key=lambda x: x[1])
     pk = peaks()
     roof = None
+    traffic = None
+    try:   # dram read + write bytes per launch of the dominant kernel from the committed capture
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f)["per_launch_dram_bytes"].get("s2l_kernel")
+    except Exception:
+        pass
     if dom[0] == "s2l" and phase["ms_s2l"] > 0:
         ach = s2l_flops / (phase["ms_s2l"] * 1e-3) / 1e12
         roof = {"bound": "alu", "kernel": "s2l_kernel (all levels)", "achieved": ach,
                 "peak": FP64_NOMINAL_TFLOPS, "unit": "TFLOP/s", "frac": ach / FP64_NOMINAL_TFLOPS,
-                "traffic": None, "algorithmic_flops": s2l_flops,
+                "traffic": traffic if pr.name.startswith("C2") else None,
+                "traffic_note": "ncu dram__bytes_read.sum + dram__bytes_write.sum per launch "
+                                "(profiles/ncu_traffic.json); flop-bound kernel",
+                "algorithmic_flops": s2l_flops,
                 "peak_note": "FP64 nominal 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md 6)"}
     else:
         roof = {"bound": "alu", "kernel": "p2p_kernel (near field)", "achieved": None,
