@@ -82,9 +82,9 @@ def lib():
         L.or_l2p.restype = None
         L.or_l2p.argtypes = [pd, i, i, d, d, d, d, pd]
         L.or_s2l.restype = i
-        L.or_s2l.argtypes = [pd, i, i, d, d, d, d, i, i, pd]
+        L.or_s2l.argtypes = [pd, i, i, i, d, d, d, d, i, i, pd]
         L.or_fmm.restype = i64
-        L.or_fmm.argtypes = [pd, pd, pd, i64, pd, pd, i64, i, i, i, d, d, i, i, pd, i]
+        L.or_fmm.argtypes = [pd, pd, pd, i64, pd, pd, i64, i, i, i, i, d, d, i, i, pd, i]
         _lib = L
     return _lib
 
@@ -209,25 +209,29 @@ def l2p(Lc, p, rc, zc, r, z):
     return out
 
 
-def s2l(M, p, rs, zs, rt, zt, truncation=TRUNC_DOUBLE, miller=MILLER_ACCURATE):
+def s2l(M, p, rs, zs, rt, zt, truncation=TRUNC_DOUBLE, miller=MILLER_ACCURATE, pl=None):
+    """Source moments M [K, P(p)] -> local contribution [K, P(pl)] (pl defaults to p)."""
     M = _c128(M)
-    out = np.zeros_like(M)
-    rc = lib().or_s2l(_pd(M.view(np.float64)), M.shape[0], p, rs, zs, rt, zt, truncation, miller,
-                      _pd(out.view(np.float64)))
+    pl = p if pl is None else pl
+    out = np.zeros((M.shape[0], tri_size(pl)), dtype=np.complex128)
+    rc = lib().or_s2l(_pd(M.view(np.float64)), M.shape[0], p, pl, rs, zs, rt, zt, truncation,
+                      miller, _pd(out.view(np.float64)))
     if rc != 0:
         raise ValueError("or_s2l failed")
     return out
 
 
 def fmm(sr, sz, S, fr, fz, p, depth, L, z0=0.0, truncation=TRUNC_DOUBLE,
-        miller=MILLER_ACCURATE, nthreads: int = 0):
+        miller=MILLER_ACCURATE, nthreads: int = 0, pl=None):
+    """Algorithm 1: source/moment order p, local order pl (default p)."""
     sr, sz, fr, fz = _f64(sr), _f64(sz), _f64(fr), _f64(fz)
     S = _c128(S)
     ns, K = S.shape
     nf = fr.shape[0]
     Phi = np.zeros((nf, K), dtype=np.complex128)
     sk = lib().or_fmm(_pd(sr), _pd(sz), _pd(S.view(np.float64)), ns, _pd(fr), _pd(fz), nf, K, p,
-                      depth, L, z0, truncation, miller, _pd(Phi.view(np.float64)), nthreads)
+                      0 if pl is None else pl, depth, L, z0, truncation, miller,
+                      _pd(Phi.view(np.float64)), nthreads)
     if sk < 0:
         raise ValueError("or_fmm: invalid input")
     return Phi, int(sk)

@@ -148,40 +148,43 @@ void or_l2p(const double *Lc, int nmodes, int p, double rc, double zc, double r,
             }
 }
 
-int or_s2l(const double *M, int nmodes, int p, double rs, double zs, double rt, double zt,
-           int truncation, int miller, double *Lacc)
+int or_s2l(const double *M, int nmodes, int p, int pl, double rs, double zs, double rt,
+           double zt, int truncation, int miller, double *Lacc)
 {
-    int P = tri_size(p);
+    /* p: source (moment) order, pl: local order (they may differ); the tensor is
+     * computed to a, b <= max(p, pl), a + b + c <= 2 max(p, pl), which contains every entry
+     * the double-truncated operator reads (A, B <= max, c = j + l <= p + pl - A - B) */
+    int P = tri_size(p), Pl = tri_size(pl), pt = p > pl ? p : pl;
     int outward = rt >= rs;       /* target at equal or larger radius: FO/BO (R#10) */
     int forward = zt >= zs;       /* target at equal or larger z: FO/FI */
     double r = outward ? rt : rs; /* tensor at r >= r1, x >= 0 */
     double r1 = outward ? rs : rt;
     double x = fabs(zt - zs);
-    int D = 2 * p + 1;
-    size_t tsz = (size_t)nmodes * (p + 1) * (p + 1) * D;
+    int D = 2 * pt + 1;
+    size_t tsz = (size_t)nmodes * (pt + 1) * (pt + 1) * D;
     double *T = (double *)malloc(sizeof(double) * tsz);
     if (!T) return -1;
-    if (or_tensor(r, r1, x, nmodes - 1, p, miller, T) != 0) {
+    if (or_tensor(r, r1, x, nmodes - 1, pt, miller, T) != 0) {
         free(T);
         return -1;
     }
     for (int m = 0; m < nmodes; ++m)
-        for (int k = 0; k <= p; ++k)
-            for (int l = 0; k + l <= p; ++l) {
+        for (int k = 0; k <= pl; ++k)
+            for (int l = 0; k + l <= pl; ++l) {
                 double re = 0.0, im = 0.0;
                 for (int i = 0; i <= p; ++i)
                     for (int j = 0; i + j <= p; ++j) {
                         if (truncation == OR_TRUNC_SINGLE && i + j + k + l > p) continue;
                         double sigma = forward ? ((j & 1) ? -1.0 : 1.0) : ((l & 1) ? -1.0 : 1.0);
                         int a = outward ? k : i, b = outward ? i : k;
-                        double g = T[(((size_t)m * (p + 1) + a) * (p + 1) + b) * D + (j + l)];
+                        double g = T[(((size_t)m * (pt + 1) + a) * (pt + 1) + b) * D + (j + l)];
                         double c = sigma * binom(j + l, j) * g;
                         const double *s = M + 2 * ((size_t)m * P + tri_idx(i, j, p));
                         re += c * s[0];
                         im += c * s[1];
                     }
-                Lacc[2 * ((size_t)m * P + tri_idx(k, l, p))] += re;
-                Lacc[2 * ((size_t)m * P + tri_idx(k, l, p)) + 1] += im;
+                Lacc[2 * ((size_t)m * Pl + tri_idx(k, l, pl))] += re;
+                Lacc[2 * ((size_t)m * Pl + tri_idx(k, l, pl)) + 1] += im;
             }
     free(T);
     return 0;
@@ -242,9 +245,11 @@ static void demorton(uint32_t key, uint32_t *ix, uint32_t *iz)
 }
 
 int64_t or_fmm(const double *sr, const double *sz, const double *S, int64_t ns,
-               const double *fr, const double *fz, int64_t nf, int nmodes, int p, int depth,
-               double L, double z0, int truncation, int miller, double *Phi, int nthreads)
+               const double *fr, const double *fz, int64_t nf, int nmodes, int p, int pl,
+               int depth, double L, double z0, int truncation, int miller, double *Phi,
+               int nthreads)
 {
+    if (pl <= 0) pl = p; /* local order defaults to the source order */
     if (depth < 2 || depth > 15 || p < 1 || nmodes < 1 || !(L > 0.0)) return -1;
 #ifdef _OPENMP
     if (nthreads > 0) omp_set_num_threads(nthreads);
@@ -256,8 +261,9 @@ int64_t or_fmm(const double *sr, const double *sz, const double *S, int64_t ns,
     for (int64_t j = 0; j < nf; ++j)
         if (!(fr[j] > 0.0) || !(fr[j] <= L) || !(fz[j] >= z0) || !(fz[j] <= z0 + L)) return -1;
 
-    int P = tri_size(p);
-    size_t per_box = (size_t)2 * nmodes * P;
+    int P = tri_size(p), Pl = tri_size(pl);
+    size_t per_box = (size_t)2 * nmodes * P;     /* source boxes: moments of order p */
+    size_t per_tbox = (size_t)2 * nmodes * Pl;   /* target boxes: locals of order pl */
     int64_t skipped = 0;
     int err = 0;
 
@@ -278,7 +284,7 @@ int64_t or_fmm(const double *sr, const double *sz, const double *S, int64_t ns,
     memset(tgt, 0, sizeof(tgt));
     for (int l = 2; l <= depth; ++l) {
         if (level_from_leaf_keys(&src[l], l, depth, skey_sorted, ns, per_box) != 0) err = 1;
-        if (level_from_leaf_keys(&tgt[l], l, depth, fkey_sorted, nf, per_box) != 0) err = 1;
+        if (level_from_leaf_keys(&tgt[l], l, depth, fkey_sorted, nf, per_tbox) != 0) err = 1;
     }
     /* leaf ranges of sorted sources: start[slot], end[slot] */
     int64_t nleaf = src[depth].count;
@@ -338,14 +344,14 @@ int64_t or_fmm(const double *sr, const double *sz, const double *S, int64_t ns,
             uint32_t key = tgt[l].keys[b], ix, iz;
             demorton(key, &ix, &iz);
             double tr = (ix + 0.5) * h, tz = z0 + (iz + 0.5) * h;
-            double *Lb = tgt[l].data + (size_t)b * per_box;
+            double *Lb = tgt[l].data + (size_t)b * per_tbox;
             if (l >= 3) { /* shift parent local expansion */
                 uint32_t px, pz;
                 demorton(key >> 2, &px, &pz);
                 double hp = 2.0 * h;
                 double pr = (px + 0.5) * hp, pzc = z0 + (pz + 0.5) * hp;
                 int32_t ps = tgt[l - 1].map[key >> 2];
-                or_l2l(tgt[l - 1].data + (size_t)ps * per_box, nmodes, p, tr - pr, tz - pzc, Lb);
+                or_l2l(tgt[l - 1].data + (size_t)ps * per_tbox, nmodes, pl, tr - pr, tz - pzc, Lb);
             }
             /* S2L list: children of the parent's neighbours that are not neighbours */
             int px = (int)(ix >> 1), pz = (int)(iz >> 1);
@@ -359,8 +365,8 @@ int64_t or_fmm(const double *sr, const double *sz, const double *S, int64_t ns,
                             int32_t ss = src[l].map[morton((uint32_t)ci, (uint32_t)cj)];
                             if (ss < 0) continue;
                             double sr0 = (ci + 0.5) * h, sz0 = z0 + (cj + 0.5) * h;
-                            if (or_s2l(src[l].data + (size_t)ss * per_box, nmodes, p, sr0, sz0, tr,
-                                       tz, truncation, miller, Lb) != 0)
+                            if (or_s2l(src[l].data + (size_t)ss * per_box, nmodes, p, pl, sr0, sz0,
+                                       tr, tz, truncation, miller, Lb) != 0)
                                 err_l = 1;
                         }
                 }
@@ -381,7 +387,7 @@ int64_t or_fmm(const double *sr, const double *sz, const double *S, int64_t ns,
                 demorton(fkey[j], &ix, &iz);
                 double rc = (ix + 0.5) * hd, zc = z0 + (iz + 0.5) * hd;
                 int32_t ts = tgt[depth].map[fkey[j]];
-                or_l2p(tgt[depth].data + (size_t)ts * per_box, nmodes, p, rc, zc, fr[j], fz[j], out);
+                or_l2p(tgt[depth].data + (size_t)ts * per_tbox, nmodes, pl, rc, zc, fr[j], fz[j], out);
                 for (int a = (int)ix - 1; a <= (int)ix + 1; ++a)
                     for (int c = (int)iz - 1; c <= (int)iz + 1; ++c) {
                         if (a < 0 || c < 0 || a >= (int)nb || c >= (int)nb) continue;

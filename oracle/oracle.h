@@ -76,14 +76,15 @@ void or_l2p(const double *Lc, int nmodes, int p, double rc, double zc, double r,
             double *phi_accum);
 /* S2L from source box centre (rs, zs) to target box centre (rt, zt): computes the tensor at
  * (outer centre, inner centre, |dz|) and applies the FO/BO/FI/BI variant. */
-int or_s2l(const double *M, int nmodes, int p, double rs, double zs, double rt, double zt,
-           int truncation, int miller, double *L_accum);
+int or_s2l(const double *M, int nmodes, int p, int pl, double rs, double zs, double rt,
+           double zt, int truncation, int miller, double *L_accum);
 
 /* Reference FMM, Algorithm 1 step by step.  Domain [0,L] x [z0, z0+L].
  * Returns number of skipped coincident near-field pairs, or -1 on error. */
 int64_t or_fmm(const double *sr, const double *sz, const double *S, int64_t ns,
-               const double *fr, const double *fz, int64_t nf, int nmodes, int p, int depth,
-               double L, double z0, int truncation, int miller, double *Phi, int nthreads);
+               const double *fr, const double *fz, int64_t nf, int nmodes, int p, int pl,
+               int depth, double L, double z0, int truncation, int miller, double *Phi,
+               int nthreads);
 
 #ifdef __cplusplus
 }

@@ -204,7 +204,8 @@ def test_fmm_converges_to_direct(orc):
         assert np.all(eps[p] > eps[p + 4])
 
 
-def test_fmm_equals_direct_expansion_form(orc):
+@pytest.mark.parametrize("p,pl", [(6, 6), (5, 8), (8, 4)])
+def test_fmm_equals_direct_expansion_form(orc, p, pl):
     """Algorithm 1 (with M2M and L2L) vs the direct-expansion form assembled here from the same
     single-box operators: moments of each S2L-list box taken directly from its sources, S2L to
     the target's ancestor at each level, evaluated at the target; plus the near field (R#21).
@@ -212,8 +213,8 @@ def test_fmm_equals_direct_expansion_form(orc):
     rng = np.random.default_rng(21)
     sr, sz, S = uniform_rings(rng, 400, 3)
     fr, fz, _ = uniform_rings(rng, 12, 1)
-    p, d, L = 6, 3, 1.0
-    F, _ = orc.fmm(sr, sz, S, fr, fz, p, d, L)
+    d, L = 3, 1.0
+    F, _ = orc.fmm(sr, sz, S, fr, fz, p, d, L, pl=pl)
     nb = 2 ** d
     six = np.minimum(np.floor(sr * nb / L), nb - 1).astype(int)
     siz = np.minimum(np.floor(sz * nb / L), nb - 1).astype(int)
@@ -232,9 +233,34 @@ def test_fmm_equals_direct_expansion_form(orc):
                     continue
                 rs, zs = (a + 0.5) * h, (c + 0.5) * h
                 M = orc.p2m(sr[sel], sz[sel], S[sel], p, rs, zs)
-                Lc = orc.s2l(M, p, rs, zs, rt, zt)
-                out[t] += orc.l2p(Lc, p, rt, zt, fr[t], fz[t])
+                Lc = orc.s2l(M, p, rs, zs, rt, zt, pl=pl)
+                out[t] += orc.l2p(Lc, pl, rt, zt, fr[t], fz[t])
         near = (np.abs(six - tx) <= 1) & (np.abs(siz - tz) <= 1)
         Dn, _ = orc.direct(sr[near], sz[near], S[near], fr[t:t + 1], fz[t:t + 1])
         out[t] += Dn[0]
     assert np.max(np.abs(out - F)) <= 1e-13 * np.max(np.abs(F))
+
+
+def test_s2l_separate_orders_converge(orc):
+    """Independent source and local orders: S2L from moments of
+    order p to a local of order pl, evaluated in the target box, converges to the direct field as
+    min(p, pl) grows, and raising one order alone is bounded by the other."""
+    rng = np.random.default_rng(17)
+    h, K = 1.0 / 16, 3
+    rs, zs, rt, zt = 6.5 * h, 5.5 * h, 8.5 * h, 7.5 * h
+    r = rs + (rng.random(10) - 0.5) * h
+    z = zs + (rng.random(10) - 0.5) * h
+    S = rng.standard_normal((10, K)) + 1j * rng.standard_normal((10, K))
+    tr = rt + (rng.random(6) - 0.5) * h
+    tz = zt + (rng.random(6) - 0.5) * h
+    D, _ = orc.direct(r, z, S, tr, tz)
+
+    def err(p, pl):
+        M = orc.p2m(r, z, S, p, rs, zs)
+        Lc = orc.s2l(M, p, rs, zs, rt, zt, pl=pl)
+        F = np.array([orc.l2p(Lc, pl, rt, zt, tr[k], tz[k]) for k in range(6)])
+        return np.max(np.abs(F - D)) / np.max(np.abs(D))
+
+    assert err(10, 10) < err(6, 10) and err(10, 10) < err(10, 6)
+    assert err(6, 12) < 10 * err(6, 6) and err(12, 6) < 10 * err(6, 6)
+    assert err(12, 12) < 1e-6
