@@ -71,6 +71,8 @@ typedef struct {
     double domain_L;        /* L > 0; a power of two keeps box indices bit-exact */
     int mode_chunk;         /* far-field passes run over modes in chunks of this many; 0 = auto
                                (all modes if the workspace fits a third of free memory) */
+    int order_local;        /* local-expansion order pl (the source and local orders
+                               may differ); 0 = the source order `order`.  1 <= pl <= 16 */
 } cylfmm_params;
 
 /* Per-phase device times of the last solve, milliseconds (CUDA events on the solve stream). */

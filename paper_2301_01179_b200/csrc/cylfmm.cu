@@ -425,6 +425,7 @@ extern "C" cylfmm_status cylfmm_plan_create(cylfmm_plan *plan, const cylfmm_para
     *plan = nullptr;
     const cylfmm_params &q = *prm;
     if (q.n_modes < 1 || q.n_modes > CYLFMM_MAX_MODES || q.order < 1 || q.order > CYLFMM_MAX_ORDER ||
+        q.order_local < 0 || q.order_local > CYLFMM_MAX_ORDER ||
         q.depth < 2 || q.depth > CYLFMM_MAX_DEPTH || (q.truncation != 0 && q.truncation != 1) ||
         (q.miller != 0 && q.miller != 1) || !(q.domain_L > 0.0) || !(q.domain_z0 == q.domain_z0) ||
         q.mode_chunk < 0) {
@@ -444,7 +445,8 @@ extern "C" cylfmm_status cylfmm_plan_create(cylfmm_plan *plan, const cylfmm_para
     p->aux_ok = true;
     {
         std::vector<int> tab;
-        build_s2l_index(q.order, s2l_mp(q.order), q.truncation, tab);
+        const int pl = q.order_local > 0 ? q.order_local : q.order;
+        build_s2l_index(q.order, pl, s2l_mp(pl), q.truncation, tab);
         RET_IF(p->s2lidx.need(sizeof(int) * tab.size()));
         CK(cudaMemcpy(p->s2lidx.p, tab.data(), sizeof(int) * tab.size(), cudaMemcpyHostToDevice));
     }
@@ -612,7 +614,7 @@ static cudaError_t launch_s2l_t(const FarArgs &fa, int64_t ntiles, cudaStream_t 
     const int KW = fa.m1 - fa.m0;
     const S2LGrid gr = make_s2l_grid(fa.depth, Cfg::JH);
     if (ntiles == 0) return cudaSuccess;
-    size_t sm = s2l_smem_bytes<NT, TM, RM, RN, KC, ST, PF, PC>(fa.p);
+    size_t sm = s2l_smem_bytes<NT, TM, RM, RN, KC, ST, PF, PC>(fa.p, fa.pl);
     s2l_kernel<NT, TM, RM, RN, KC, ST, PF, PC><<<(unsigned)(ntiles * KW), NT, sm, st>>>(fa, gr);
     return cudaGetLastError();
 }
@@ -629,17 +631,19 @@ static int s2l_variant()
     }();
     return v;
 }
+// class by the local order `cls` (GEMM rows <= MP); the compile-time order PC only when the
+// source and local orders are both PCV (`pcm`)
 #define S2L_PICK(FN, CFG, PCV, ...) \
-    return (p == PCV) ? FN<CFG, PCV>(__VA_ARGS__) : FN<CFG, 0>(__VA_ARGS__)
+    return (pcm == PCV) ? FN<CFG, PCV>(__VA_ARGS__) : FN<CFG, 0>(__VA_ARGS__)
 #define S2L_DISPATCH(FN, ...)                                                                  \
     do {                                                                                       \
         const int v_ = s2l_variant();                                                          \
-        if (p <= 8) {                                                                          \
+        if (cls <= 8) {                                                                        \
             if (v_ == 1) S2L_PICK(FN, S2L_P8_V1, 8, __VA_ARGS__);                              \
             if (v_ == 2) S2L_PICK(FN, S2L_P8_V2, 8, __VA_ARGS__);                              \
             S2L_PICK(FN, S2L_P8, 8, __VA_ARGS__);                                              \
         }                                                                                      \
-        if (p <= 12) {                                                                         \
+        if (cls <= 12) {                                                                       \
             if (v_ == 1) S2L_PICK(FN, S2L_P12_V1, 12, __VA_ARGS__);                            \
             if (v_ == 2) S2L_PICK(FN, S2L_P12_V2, 12, __VA_ARGS__);                            \
             S2L_PICK(FN, S2L_P12, 12, __VA_ARGS__);                                            \
@@ -650,10 +654,14 @@ static int s2l_variant()
     } while (0)
 static cudaError_t launch_s2l(const FarArgs &fa, int64_t ntiles, cudaStream_t st)
 {
-    const int p = fa.p;
+    const int cls = fa.pl, pcm = fa.p == fa.pl ? fa.p : -1;
     S2L_DISPATCH(launch_s2l_t, fa, ntiles, st);
 }
-static int s2l_jh(int p) { S2L_DISPATCH(s2l_jh_t); }
+static int s2l_jh(int cls)
+{
+    const int pcm = -1;
+    S2L_DISPATCH(s2l_jh_t);
+}
 
 struct PhaseTimer {
     cylfmm_plan p;
@@ -694,6 +702,9 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
 {
     const cylfmm_params &q = p->prm;
     const int d = q.depth, K = q.n_modes, pp = q.order, P = (pp + 1) * (pp + 2) / 2;
+    // local order (0 = the source order) and the tensor order max(p, pl)
+    const int pl = q.order_local > 0 ? q.order_local : pp, Pl = (pl + 1) * (pl + 2) / 2;
+    const int pt = std::max(pp, pl);
     int KW = q.mode_chunk > 0 ? std::min(q.mode_chunk, K) : K;
     p->launches = 0;
     PhaseTimer T{p, st, tm != nullptr};
@@ -709,7 +720,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     const bool overlap = tm == nullptr && p->aux_ok;
     cudaStream_t st_t = overlap ? p->aux[0] : st, st_n = overlap ? p->aux[1] : st;
     const int64_t nstat = (int64_t)12 << d;
-    const int NM = std::max(K - 1, 1) + 1, D = 2 * pp + 1;
+    const int NM = std::max(K - 1, 1) + 1, D = 2 * pt + 1;
     RET_IF(p->seeds.need(sizeof(double) * (size_t)nstat * 4 * NM * D));
     TensorGeomArgs ta = {};
     ta.station_mode = 1;
@@ -717,7 +728,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     ta.K = K;
     ta.m0 = 0;
     ta.m1 = K;
-    ta.p = pp;
+    ta.p = pt;
     ta.miller = q.miller;
     ta.fwd2 = forward_coef(std::max(K - 1, 1), q.miller);
     ta.seeds = p->seeds.as<double>();
@@ -816,7 +827,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     }
     // S2L tiles with at least one interaction (sparse inputs: C4, C5) and the per-box
     // "written by S2L" flags that L2L / L2P use instead of zero-initialised locals
-    const S2LGrid s2lgr = make_s2l_grid(d, s2l_jh(pp));
+    const S2LGrid s2lgr = make_s2l_grid(d, s2l_jh(pl));
     const int64_t ntiles_all = s2lgr.start[s2lgr.nlev];
     RET_IF(p->tflag.need(sizeof(int) * std::max<int64_t>(ntiles_all, 1)));
     RET_IF(p->tpos.need(sizeof(int) * std::max<int64_t>(ntiles_all, 1)));
@@ -837,7 +848,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             ta.lvoff[l] = lvoff[l];
         }
         s2l_tile_flags_kernel<<<nblk(ntiles_all * 32, 256), 256, 0, st>>>(
-            ta, s2lgr, s2l_jh(pp), p->tflag.as<int>(), p->written.as<unsigned char>());
+            ta, s2lgr, s2l_jh(pl), p->tflag.as<int>(), p->written.as<unsigned char>());
         CKL();
         CK(cudaMemcpyAsync(p->tpos.p, p->tflag.p, sizeof(int) * ntiles_all, cudaMemcpyDeviceToDevice, st));
         RET_IF(scan_excl(p, p->tpos.as<int>(), ntiles_all, st));
@@ -859,6 +870,9 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     fa.depth = d;
     fa.p = pp;
     fa.P = P;
+    fa.pl = pl;
+    fa.Pl = Pl;
+    fa.pt = pt;
     fa.K = K;
     fa.L = q.domain_L;
     fa.z0 = q.domain_z0;
@@ -876,13 +890,13 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         stot += fa.scount[l];
         ttot += fa.tcount[l];
     }
-    const int64_t TP = (int64_t)(pp + 1) * (pp + 1) * (pp + 1) + ((pp + 1) & 1);  // padded
+    const int64_t TP = (int64_t)(pt + 1) * (pt + 1) * (pt + 1) + ((pt + 1) & 1);  // padded
     if (q.mode_chunk == 0) {
         // automatic chunk: the far-field workspace (moments, locals, tensors per mode) of one
         // chunk must fit in a third of the free device memory (C5: 1.8 GB per mode).  The free
         // memory is queried only when the current allocations cannot hold all modes (the query
         // is slow; steady-state solves reuse the plan's workspace).
-        size_t per_mode = sizeof(double2) * (size_t)(stot + ttot) * P + sizeof(double) * nstat * TP;
+        size_t per_mode = sizeof(double2) * ((size_t)stot * P + (size_t)ttot * Pl) + sizeof(double) * nstat * TP;
         size_t have = p->M.cap + p->Lc.cap + p->tens.cap;   // reusable current allocations
         if (per_mode * (size_t)K > have) {
             size_t fmem = 0, tot = 0;
@@ -897,7 +911,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         }
     }
     RET_IF(p->M.need(sizeof(double2) * (size_t)std::max<int64_t>(stot, 1) * KW * P));
-    RET_IF(p->Lc.need(sizeof(double2) * (size_t)std::max<int64_t>(ttot, 1) * KW * P));
+    RET_IF(p->Lc.need(sizeof(double2) * (size_t)std::max<int64_t>(ttot, 1) * KW * Pl));
     RET_IF(p->tens.need(sizeof(double) * (size_t)nstat * KW * TP));
     fa.M = p->M.as<double2>();
     fa.Lc = p->Lc.as<double2>();
@@ -1053,7 +1067,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             int64_t items = (int64_t)fa.tcount[l] * kw;
             unsigned g = (unsigned)std::min<int64_t>((items + kL2LWarps - 1) / kL2LWarps,
                                                      (int64_t)p->nsm * 8);
-            l2l_kernel<<<g, 32 * kL2LWarps, l2l_smem(pp), st>>>(fa, l);
+            l2l_kernel<<<g, 32 * kL2LWarps, l2l_smem(pl), st>>>(fa, l);
             CKL();
             p->launches++;
         }
@@ -1062,7 +1076,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         if (overlap && ns > 0 && m0 == 0) CK(cudaStreamWaitEvent(st, p->aev[3], 0));  // near field
         {
             int ngrp = (kw + kL2PModes - 1) / kL2PModes;
-            size_t sm = sizeof(double2) * kL2PModes * P + sizeof(double) * kL2PPts * P;
+            size_t sm = sizeof(double2) * kL2PModes * Pl + sizeof(double) * kL2PPts * Pl;
             l2p_kernel<<<(unsigned)((int64_t)fa.tcount[d] * ngrp), 256, sm, st>>>(fa);
             CKL();
             p->launches++;

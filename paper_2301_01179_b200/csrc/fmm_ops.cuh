@@ -24,7 +24,8 @@ namespace cyl {
 constexpr int kMaxLevels = 12;
 
 struct FarArgs {
-    int depth, p, P, K, m0, m1;
+    int depth, p, P, K, m0, m1;   // p, P: source (moment) order and size
+    int pl, Pl, pt;               // local order and size; tensor order max(p, pl)
     double L, z0;
     int truncation;
     // per level l (2..depth): compact box lists
@@ -278,7 +279,7 @@ constexpr int kL2LWarps = 8;
 __global__ void __launch_bounds__(32 * kL2LWarps) l2l_kernel(FarArgs a, int level)
 {
     extern __shared__ double sm[];
-    const int p = a.p, P = a.P, KW = a.m1 - a.m0, P1 = p + 1;
+    const int p = a.pl, P = a.Pl, KW = a.m1 - a.m0, P1 = p + 1;   // local order
     double *cm = sm, *cl = cm + 2 * P1 * P1;
     int *tri_i = reinterpret_cast<int *>(cl + 2 * P1 * P1);
     int *tri_j = tri_i + P;
@@ -356,7 +357,7 @@ constexpr int kL2PPts = 16;
 __global__ void __launch_bounds__(256) l2p_kernel(FarArgs a)
 {
     extern __shared__ double sm[];
-    const int p = a.p, P = a.P, KW = a.m1 - a.m0, d = a.depth;
+    const int p = a.pl, P = a.Pl, KW = a.m1 - a.m0, d = a.depth;   // local order
     const int ngrp = (KW + kL2PModes - 1) / kL2PModes;
     const int slot = blockIdx.x / ngrp, g = blockIdx.x % ngrp;
     const int n0 = g * kL2PModes, nm = min(kL2PModes, KW - n0);
@@ -711,16 +712,19 @@ __global__ void __launch_bounds__(NT, (RM * RN >= 40 ? 256 : 512) / NT) s2l_kern
     extern __shared__ double sm[];
     // PC > 0: the expansion order is a compile-time constant (BASELINE orders 8, 12, 16), so
     // every index division below is by a constant
+    // p, P: source order and size (GEMM depth); pl, Pl: local order and size (GEMM rows, <= MP);
+    // pt = max(p, pl): tensor order.  PC > 0 implies p = pl = PC.
     const int p = PC ? PC : a.p, P = PC ? (PC + 1) * (PC + 2) / 2 : a.P, KW = a.m1 - a.m0;
-    const int TP = (p + 1) * (p + 1) * (p + 1), TPp = TP + (TP & 1), HST = TPp + 2;
+    const int pl = PC ? PC : a.pl, Pl = PC ? P : a.Pl, pt = PC ? PC : a.pt;
+    const int TP = (pt + 1) * (pt + 1) * (pt + 1), TPp = TP + (TP & 1), HST = TPp + 2;
     constexpr bool TMA = PF == 3;                  // box-major B staged by bulk copies
     const int BPS = P | 1;                         // TMA: complex row stride per box (odd)
     double *As = sm;                               // [KC][MP]
     double *Bs0 = As + KC * MP;                    // ST x [P][NC] (TMA: [JT][BPS] complex)
     double *Hs0 = Bs0 + (TMA ? ST * 2 * JT * BPS : ST * P * NC);   // ST x [HST], Hs[TPp] = 0
     uint64_t *bar = reinterpret_cast<uint64_t *>(Hs0 + ST * HST);   // TMA barriers, one per stage
-    double *post = reinterpret_cast<double *>(bar + 2);            // [P] 1 / l!
-    int *tsl = reinterpret_cast<int *>(post + P);  // [JT]  (box b: parity b / JH, index b % JH)
+    double *post = reinterpret_cast<double *>(bar + 2);            // [Pl] 1 / l!
+    int *tsl = reinterpret_cast<int *>(post + Pl); // [JT]  (box b: parity b / JH, index b % JH)
     int *ssl = tsl + JT;                           // [NOFF][JT]
     int *olist = ssl + NOFF * JT;                  // [NOFF] active offsets
     int *nact = olist + NOFF;
@@ -760,10 +764,10 @@ __global__ void __launch_bounds__(NT, (RM * RN >= 40 ? 256 : 512) / NT) s2l_kern
                 olist[k++] = ((di + 3) << 4) | (dj + 3);
             }
     }
-    for (int q = tid; q < P; q += NT) {
+    for (int q = tid; q < Pl; q += NT) {   // target coefficient (k, l), local order pl
         int i = 0;
-        while (i < p && q >= (i + 1) * (p + 1) - (i + 1) * i / 2) ++i;
-        int l = q - (i * (p + 1) - i * (i - 1) / 2);
+        while (i < pl && q >= (i + 1) * (pl + 1) - (i + 1) * i / 2) ++i;
+        int l = q - (i * (pl + 1) - i * (i - 1) / 2);
         double f = 1.0;
         for (int t = 2; t <= l; ++t) f *= t;
         post[q] = 1.0 / f;
@@ -947,35 +951,44 @@ __global__ void __launch_bounds__(NT, (RM * RN >= 40 ? 256 : 512) / NT) s2l_kern
         int col = BLK ? tn * RN + v : tn + TN * v, b = col >> 1, im = col & 1;
         int s = tsl[b];
         if (s < 0) continue;
-        double *dst = reinterpret_cast<double *>(a.Lc + ((a.toff[level] + s) * (int64_t)KW + nloc) * P);
+        double *dst = reinterpret_cast<double *>(a.Lc + ((a.toff[level] + s) * (int64_t)KW + nloc) * Pl);
 #pragma unroll
         for (int u = 0; u < RM; ++u) {
             int m = 2 * (tm + TM * (u >> 1)) + (u & 1);
-            if (m < P) dst[2 * m + im] = acc[u][v] * post[m];
+            if (m < Pl) dst[2 * m + im] = acc[u][v] * post[m];
         }
     }
 }
 
 // Host: (index << 1 | negate) gather table of A'[kk][m] for the 4 variants (FO, BO, FI, BI),
 // rows padded to MP; masked / padded entries point at the zero slot TPp.
-inline void build_s2l_index(int p, int MP, int truncation, std::vector<int> &tab)
+inline void build_s2l_index(int p, int pl, int MP, int truncation, std::vector<int> &tab)
 {
-    const int P = (p + 1) * (p + 2) / 2, TP = (p + 1) * (p + 1) * (p + 1), TPp = TP + (TP & 1);
-    std::vector<int> ti(P), tj(P);
+    // rows kk = (i, j): source coefficients of order p; columns m = (k, l): local order pl;
+    // entries H_{A,B}(j + l) of the tensor of order pt = max(p, pl) (packed layout)
+    const int pt = p > pl ? p : pl;
+    const int P = (p + 1) * (p + 2) / 2, Pl = (pl + 1) * (pl + 2) / 2;
+    const int TP = (pt + 1) * (pt + 1) * (pt + 1), TPp = TP + (TP & 1);
+    std::vector<int> ti(P), tj(P), tk(Pl), tl(Pl);
     for (int i = 0, q = 0; i <= p; ++i)
         for (int j = 0; i + j <= p; ++j, ++q) {
             ti[q] = i;
             tj[q] = j;
         }
+    for (int k = 0, q = 0; k <= pl; ++k)
+        for (int l = 0; k + l <= pl; ++l, ++q) {
+            tk[q] = k;
+            tl[q] = l;
+        }
     tab.assign((size_t)4 * P * MP, TPp << 1);
     for (int var = 0; var < 4; ++var) {
         const bool outward = var < 2, fwd = (var & 1) == 0;
         for (int kk = 0; kk < P; ++kk)
-            for (int m = 0; m < P; ++m) {
-                int i = ti[kk], j = tj[kk], k = ti[m], l = tj[m];
+            for (int m = 0; m < Pl; ++m) {
+                int i = ti[kk], j = tj[kk], k = tk[m], l = tl[m];
                 if (truncation == 1 && i + j + k + l > p) continue;
                 int A = outward ? k : i, B = outward ? i : k;
-                int idx = packed_off(A, B, p) + j + l;
+                int idx = packed_off(A, B, pt) + j + l;
                 int neg = (!fwd && ((j + l) & 1)) ? 1 : 0;
                 tab[((size_t)var * P + kk) * MP + m] = (idx << 1) | neg;
             }
@@ -999,10 +1012,12 @@ __global__ void prescale_moments_kernel(double2 *M, int64_t nrows, int p, int P)
 }
 
 template <int NT, int TM, int RM, int RN, int KC, int ST, int PF, int PC>
-inline size_t s2l_smem_bytes(int p)
+inline size_t s2l_smem_bytes(int p, int pl)
 {
     using Cfg = S2LCfg<NT, TM, RM, RN, KC, ST, PF, PC>;
-    int P = (p + 1) * (p + 2) / 2, TP = (p + 1) * (p + 1) * (p + 1), TPp = TP + (TP & 1);
+    const int pt = p > pl ? p : pl;
+    int P = (p + 1) * (p + 2) / 2, TP = (pt + 1) * (pt + 1) * (pt + 1), TPp = TP + (TP & 1);
+    P = P > (pl + 1) * (pl + 2) / 2 ? P : (pl + 1) * (pl + 2) / 2;   // post[] of Pl, B rows of P
     const size_t bsz = PF == 3 ? (size_t)ST * 2 * Cfg::JT * (P | 1) : ST * (size_t)P * Cfg::NCP;
     return sizeof(double) * ((size_t)KC * Cfg::MP + bsz + ST * (TPp + 2) + 2 + P) +
            sizeof(int) * (Cfg::JT + Cfg::NOFF * Cfg::JT + 2 * Cfg::NOFF + 1);

@@ -33,7 +33,8 @@ class Params(ctypes.Structure):
     _fields_ = [("n_modes", ctypes.c_int), ("order", ctypes.c_int), ("depth", ctypes.c_int),
                 ("truncation", ctypes.c_int), ("miller", ctypes.c_int),
                 ("exclude_coincident", ctypes.c_int), ("domain_z0", ctypes.c_double),
-                ("domain_L", ctypes.c_double), ("mode_chunk", ctypes.c_int)]
+                ("domain_L", ctypes.c_double), ("mode_chunk", ctypes.c_int),
+                ("order_local", ctypes.c_int)]
 
 
 class Timings(ctypes.Structure):
@@ -186,6 +187,7 @@ class FMMConfig:
     miller: int = MILLER_ACCURATE
     exclude_coincident: bool = True
     mode_chunk: int = 0
+    order_local: int = 0      # local-expansion order (0: = order)
 
 
 class Plan:
@@ -196,7 +198,7 @@ class Plan:
         self.cfg = cfg
         prm = Params(cfg.n_modes, cfg.order, cfg.depth, cfg.truncation, cfg.miller,
                      int(bool(cfg.exclude_coincident)), float(cfg.z0), float(cfg.L),
-                     cfg.mode_chunk)
+                     cfg.mode_chunk, cfg.order_local)
         h = ctypes.c_void_p()
         _check(lib().cylfmm_plan_create(ctypes.byref(h), ctypes.byref(prm)), "cylfmm_plan_create")
         self._h = h
@@ -257,7 +259,8 @@ def partition_fields(src_r, src_z, fld_r, fld_z, cfg: "FMMConfig", n_parts: int)
     part = np.empty(a[2].shape[0], dtype=np.int32)
     cost = np.empty(n_parts, dtype=np.float64)
     prm = Params(cfg.n_modes, cfg.order, cfg.depth, cfg.truncation, cfg.miller,
-                 int(bool(cfg.exclude_coincident)), float(cfg.z0), float(cfg.L), cfg.mode_chunk)
+                 int(bool(cfg.exclude_coincident)), float(cfg.z0), float(cfg.L), cfg.mode_chunk,
+                 cfg.order_local)
     p = lambda x: ctypes.c_void_p(x.ctypes.data) if x.size else ctypes.c_void_p(0)  # noqa: E731
     _check(lib().cylfmm_partition_fields(p(a[0]), p(a[1]), a[0].shape[0], p(a[2]), p(a[3]),
                                          a[2].shape[0], ctypes.byref(prm), int(n_parts), p(part),

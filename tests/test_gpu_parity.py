@@ -211,11 +211,12 @@ def test_tree_sort_bit_exact(gpu, orc, n, depth, L, z0):
 
 
 def _fmm_case(gpu, orc, sr, sz, S, fr, fz, p, depth, L, z0=0.0, truncation=0, miller=0,
-              mode_chunk=0):
+              mode_chunk=0, pl=0):
     K = S.shape[1]
-    ref, sk = orc.fmm(sr, sz, S, fr, fz, p, depth, L, z0, truncation, miller)
+    ref, sk = orc.fmm(sr, sz, S, fr, fz, p, depth, L, z0, truncation, miller, pl=pl or None)
     plan = gpu.Plan(gpu.FMMConfig(n_modes=K, order=p, depth=depth, L=L, z0=z0,
-                                  truncation=truncation, miller=miller, mode_chunk=mode_chunk))
+                                  truncation=truncation, miller=miller, mode_chunk=mode_chunk,
+                                  order_local=pl))
     out, tm = plan.solve(sr, sz, S, fr, fz, timings=True)
     assert tm["n_skipped"] == sk
     return out.cpu().numpy(), ref, plan
@@ -344,4 +345,17 @@ def test_edge_max_modes_min_order_max_depth(gpu, orc):
         out, ref, _ = _fmm_case(gpu, orc, sr, sz, S, fr, fz, p, depth, 1.0)
         assert eps_modes(out, ref).max() <= TOL, (p, depth)
     out, ref, _ = _fmm_case(gpu, orc, sr[:1], sz[:1], S[:1], fr, fz, 6, 3, 1.0)
+    assert eps_modes(out, ref).max() <= TOL
+
+
+@pytest.mark.parametrize("p,pl,K,depth", [(6, 9, 5, 4), (9, 6, 5, 4), (8, 12, 9, 4), (12, 16, 3, 3),
+                                         (16, 10, 3, 3)])
+def test_fmm_separate_source_local_orders(gpu, orc, p, pl, K, depth):
+    """Independent source and local orders: moments of order p,
+    locals of order pl, tensor of order max(p, pl), against the oracle FMM with the same orders;
+    the S2L tiling class follows pl and mixed orders use the runtime-order kernels."""
+    rng = np.random.default_rng(p * 31 + pl)
+    sr, sz, S = uniform_rings(rng, 2500, K)
+    fr, fz, _ = uniform_rings(rng, 700, 1)
+    out, ref, _ = _fmm_case(gpu, orc, sr, sz, S, fr, fz, p, depth, 1.0, pl=pl)
     assert eps_modes(out, ref).max() <= TOL
