@@ -84,7 +84,11 @@ def lib():
         L.or_s2l.restype = i
         L.or_s2l.argtypes = [pd, i, i, i, d, d, d, d, i, i, pd]
         L.or_fmm.restype = i64
-        L.or_fmm.argtypes = [pd, pd, pd, i64, pd, pd, i64, i, i, i, i, d, d, i, i, pd, i]
+        L.or_fmm.argtypes = [pd, pd, pd, i64, pd, pd, i64, i, i, i, i, d, d, i, i, pd, pd, pd, i]
+        L.or_greens_grad.restype = i
+        L.or_greens_grad.argtypes = [d, d, d, i, i, pd, pd, pd]
+        L.or_direct_grad.restype = i64
+        L.or_direct_grad.argtypes = [pd, pd, pd, i64, pd, pd, i64, i, i, i, pd, pd, pd, i]
         _lib = L
     return _lib
 
@@ -169,6 +173,30 @@ def direct(sr, sz, S, fr, fz, miller: int = MILLER_ACCURATE, exclude_coincident:
     return Phi, int(sk)
 
 
+def greens_grad(r, r1, x, nmax, miller: int = MILLER_ACCURATE):
+    """G^(n), dG/dr, dG/dx (field point) for n = 0..nmax."""
+    G, Gr, Gx = (np.zeros(nmax + 1) for _ in range(3))
+    if lib().or_greens_grad(r, r1, x, nmax, miller, _pd(G), _pd(Gr), _pd(Gx)) != 0:
+        raise ValueError("or_greens_grad failed")
+    return G, Gr, Gx
+
+
+def direct_grad(sr, sz, S, fr, fz, miller: int = MILLER_ACCURATE, exclude_coincident: bool = True,
+                nthreads: int = 0):
+    """Direct sum with field gradients: (Phi, dPhi/dr, dPhi/dz, skipped)."""
+    sr, sz, fr, fz = _f64(sr), _f64(sz), _f64(fr), _f64(fz)
+    S = _c128(S)
+    ns, K = S.shape
+    nf = fr.shape[0]
+    out = [np.zeros((nf, K), dtype=np.complex128) for _ in range(3)]
+    sk = lib().or_direct_grad(_pd(sr), _pd(sz), _pd(S.view(np.float64)), ns, _pd(fr), _pd(fz), nf,
+                              K, miller, int(exclude_coincident),
+                              *[_pd(o.view(np.float64)) for o in out], nthreads)
+    if sk < 0:
+        raise ValueError("or_direct_grad: domain error or unexcluded coincident pair")
+    return out[0], out[1], out[2], int(sk)
+
+
 def tree_keys(r, z, depth, L, z0):
     r, z = _f64(r), _f64(z)
     n = r.shape[0]
@@ -222,19 +250,25 @@ def s2l(M, p, rs, zs, rt, zt, truncation=TRUNC_DOUBLE, miller=MILLER_ACCURATE, p
 
 
 def fmm(sr, sz, S, fr, fz, p, depth, L, z0=0.0, truncation=TRUNC_DOUBLE,
-        miller=MILLER_ACCURATE, nthreads: int = 0, pl=None):
-    """Algorithm 1: source/moment order p, local order pl (default p)."""
+        miller=MILLER_ACCURATE, nthreads: int = 0, pl=None, grad=False):
+    """Algorithm 1: source/moment order p, local order pl (default p).
+    grad=True also returns the field gradients dPhi/dr, dPhi/dz: (Phi, dPr, dPz, skipped)."""
     sr, sz, fr, fz = _f64(sr), _f64(sz), _f64(fr), _f64(fz)
     S = _c128(S)
     ns, K = S.shape
     nf = fr.shape[0]
     Phi = np.zeros((nf, K), dtype=np.complex128)
+    grad = bool(grad)
+    Gr = np.zeros((nf, K), dtype=np.complex128) if grad else None
+    Gz = np.zeros((nf, K), dtype=np.complex128) if grad else None
+    nul = ctypes.POINTER(ctypes.c_double)()
     sk = lib().or_fmm(_pd(sr), _pd(sz), _pd(S.view(np.float64)), ns, _pd(fr), _pd(fz), nf, K, p,
                       0 if pl is None else pl, depth, L, z0, truncation, miller,
-                      _pd(Phi.view(np.float64)), nthreads)
+                      _pd(Phi.view(np.float64)), _pd(Gr.view(np.float64)) if grad else nul,
+                      _pd(Gz.view(np.float64)) if grad else nul, nthreads)
     if sk < 0:
         raise ValueError("or_fmm: invalid input")
-    return Phi, int(sk)
+    return (Phi, Gr, Gz, int(sk)) if grad else (Phi, int(sk))
 
 
 def eps_per_mode(A: np.ndarray, B: np.ndarray) -> np.ndarray:

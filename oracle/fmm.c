@@ -134,6 +134,25 @@ void or_l2l(const double *Lp, int nmodes, int p, double dr, double dz, double *L
             }
 }
 
+/* gradient of the local expansion at (r, z): d/dr and d/dz of sum Phi_kl dr^k dz^l */
+void or_l2p_grad(const double *Lc, int nmodes, int p, double rc, double zc, double r, double z,
+                 double *gr, double *gz)
+{
+    int P = tri_size(p);
+    double dr = r - rc, dz = z - zc;
+    for (int m = 0; m < nmodes; ++m)
+        for (int k = 0; k <= p; ++k)
+            for (int l = 0; k + l <= p; ++l) {
+                double mr = k > 0 ? k * pow(dr, k - 1) * pow(dz, l) : 0.0;
+                double mz = l > 0 ? l * pow(dr, k) * pow(dz, l - 1) : 0.0;
+                const double *c = Lc + 2 * ((size_t)m * P + tri_idx(k, l, p));
+                gr[2 * m] += c[0] * mr;
+                gr[2 * m + 1] += c[1] * mr;
+                gz[2 * m] += c[0] * mz;
+                gz[2 * m + 1] += c[1] * mz;
+            }
+}
+
 void or_l2p(const double *Lc, int nmodes, int p, double rc, double zc, double r, double z,
             double *phi)
 {
@@ -247,8 +266,11 @@ static void demorton(uint32_t key, uint32_t *ix, uint32_t *iz)
 int64_t or_fmm(const double *sr, const double *sz, const double *S, int64_t ns,
                const double *fr, const double *fz, int64_t nf, int nmodes, int p, int pl,
                int depth, double L, double z0, int truncation, int miller, double *Phi,
-               int nthreads)
+               double *dPr, double *dPz, int nthreads)
 {
+    /* dPr, dPz (nullable, both or neither): the field gradients, from the gradient of the local
+     * expansion at the point plus the near field with the derivative relations of G (or_greens_grad) */
+    const int grad = dPr != NULL && dPz != NULL;
     if (pl <= 0) pl = p; /* local order defaults to the source order */
     if (depth < 2 || depth > 15 || p < 1 || nmodes < 1 || !(L > 0.0)) return -1;
 #ifdef _OPENMP
@@ -378,16 +400,26 @@ int64_t or_fmm(const double *sr, const double *sz, const double *S, int64_t ns,
         uint32_t nb = 1u << depth;
 #pragma omp parallel reduction(+ : skipped) reduction(| : err)
         {
-            double *G = (double *)malloc(sizeof(double) * nmodes);
+            double *G = (double *)malloc(sizeof(double) * 3 * nmodes);
+            double *Gr = G + nmodes, *Gx = Gr + nmodes;
 #pragma omp for schedule(dynamic, 16)
             for (int64_t j = 0; j < nf; ++j) {
                 double *out = Phi + 2 * (size_t)j * nmodes;
+                double *outr = grad ? dPr + 2 * (size_t)j * nmodes : NULL;
+                double *outz = grad ? dPz + 2 * (size_t)j * nmodes : NULL;
                 memset(out, 0, sizeof(double) * 2 * nmodes);
+                if (grad) {
+                    memset(outr, 0, sizeof(double) * 2 * nmodes);
+                    memset(outz, 0, sizeof(double) * 2 * nmodes);
+                }
                 uint32_t ix, iz;
                 demorton(fkey[j], &ix, &iz);
                 double rc = (ix + 0.5) * hd, zc = z0 + (iz + 0.5) * hd;
                 int32_t ts = tgt[depth].map[fkey[j]];
                 or_l2p(tgt[depth].data + (size_t)ts * per_tbox, nmodes, pl, rc, zc, fr[j], fz[j], out);
+                if (grad)
+                    or_l2p_grad(tgt[depth].data + (size_t)ts * per_tbox, nmodes, pl, rc, zc, fr[j],
+                                fz[j], outr, outz);
                 for (int a = (int)ix - 1; a <= (int)ix + 1; ++a)
                     for (int c = (int)iz - 1; c <= (int)iz + 1; ++c) {
                         if (a < 0 || c < 0 || a >= (int)nb || c >= (int)nb) continue;
@@ -399,7 +431,10 @@ int64_t or_fmm(const double *sr, const double *sz, const double *S, int64_t ns,
                                 ++skipped;
                                 continue;
                             }
-                            if (or_greens(fr[j], sr[i], fz[j] - sz[i], nmodes - 1, miller, G) != 0) {
+                            int rc2 = grad ? or_greens_grad(fr[j], sr[i], fz[j] - sz[i], nmodes - 1,
+                                                            miller, G, Gr, Gx)
+                                           : or_greens(fr[j], sr[i], fz[j] - sz[i], nmodes - 1, miller, G);
+                            if (rc2 != 0) {
                                 err = 1;
                                 continue;
                             }
@@ -407,6 +442,12 @@ int64_t or_fmm(const double *sr, const double *sz, const double *S, int64_t ns,
                             for (int n = 0; n < nmodes; ++n) {
                                 out[2 * n] += Si[2 * n] * G[n];
                                 out[2 * n + 1] += Si[2 * n + 1] * G[n];
+                                if (grad) {
+                                    outr[2 * n] += Si[2 * n] * Gr[n];
+                                    outr[2 * n + 1] += Si[2 * n + 1] * Gr[n];
+                                    outz[2 * n] += Si[2 * n] * Gx[n];
+                                    outz[2 * n + 1] += Si[2 * n + 1] * Gx[n];
+                                }
                             }
                         }
                     }
