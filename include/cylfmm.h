@@ -162,6 +162,18 @@ cylfmm_status cylfmm_tree_sort(const double *r, const double *z, int64_t n, int 
                                double L, double z0, uint32_t *key, int32_t *perm,
                                cylfmm_stream_t stream);
 
+/* FMM solve with the potential gradients (the paper's motivating
+ * application): as cylfmm_fmm_solve, plus out_dPhi_dr and out_dPhi_dz (DEVICE,
+ * complex128 [n_fld][n_modes], input field order), the derivatives of Phi^(n) with respect to
+ * the field point's r and z.  Far field: derivative of the local expansion; near field: the
+ * paper's first-order relations dG/dx and dG/dr, G^(-1) == G^(1).
+ * Errors: as cylfmm_fmm_solve; EINVAL for null gradient outputs or n_modes > 72. */
+cylfmm_status cylfmm_fmm_solve_grad(cylfmm_plan plan, const double *src_r, const double *src_z,
+                                    const double *src_S, int64_t n_src, const double *fld_r,
+                                    const double *fld_z, int64_t n_fld, double *out_Phi,
+                                    double *out_dPhi_dr, double *out_dPhi_dz,
+                                    cylfmm_stream_t stream, cylfmm_timings *timings);
+
 /* Field-point partition for a multi-GPU solve (BASELINE north_star: "field points are
  * partitioned across the GPUs ... sources and the upper tree replicated").
  * HOST-only (no device needed): every rank calls it with the same replicated inputs and gets

@@ -114,6 +114,7 @@ static cylfmm_status ensure_init()
     CK(e);
 #define X(TT, SC, MT)                                                                          \
     CK(allow_smem(p2p_kernel<TT, SC, MT, true>));                                              \
+    CK(allow_smem(p2p_kernel<TT, SC, MT, true, true>));                                        \
     CK(allow_smem(p2p_kernel<TT, SC, MT, false>));
     P2P_INSTANCES(X)
 #undef X
@@ -122,7 +123,8 @@ static cylfmm_status ensure_init()
     CK(allow_smem(p2m_kernel));
     CK(allow_smem(m2m_kernel));
     CK(allow_smem(l2l_kernel));
-    CK(allow_smem(l2p_kernel));
+    CK(allow_smem(l2p_kernel<false>));
+    CK(allow_smem(l2p_kernel<true>));
 #define X(...) CK(allow_smem(s2l_kernel<__VA_ARGS__>));
     S2L_ALL(X)
 #undef X
@@ -141,25 +143,25 @@ static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / 
 
 // ------------------------------------------------------------------------------------------
 // P2P launcher (direct and near field)
-template <int TT, int SC, int MT, bool NEAR>
+template <int TT, int SC, int MT, bool NEAR, bool GRAD>
 static cudaError_t launch_p2p_t(const P2PArgs &a, dim3 grid, cudaStream_t st)
 {
-    size_t sm = p2p_smem_bytes<TT, SC>(a.m1 - a.m0);
-    p2p_kernel<TT, SC, MT, NEAR><<<grid, TT * SC, sm, st>>>(a);
+    size_t sm = p2p_smem_bytes<TT, SC, GRAD>(a.m1 - a.m0);
+    p2p_kernel<TT, SC, MT, NEAR, GRAD><<<grid, TT * SC, sm, st>>>(a);
     return cudaGetLastError();
 }
 
 // pick (TT, SC, MAXT) for a target tile size and mode window; grid.x must be set by caller
-template <bool NEAR>
+template <bool NEAR, bool GRAD = false>
 static cudaError_t launch_p2p(int TT, const P2PArgs &a, dim3 grid, cudaStream_t st)
 {
     int KW = a.m1 - a.m0;
-    if (TT == 8) return KW <= 32 ? launch_p2p_t<8, 16, 2, NEAR>(a, grid, st)
-                                 : launch_p2p_t<8, 16, 5, NEAR>(a, grid, st);
-    if (TT == 16) return KW <= 24 ? launch_p2p_t<16, 8, 3, NEAR>(a, grid, st)
-                                  : launch_p2p_t<16, 8, 9, NEAR>(a, grid, st);
-    return KW <= 24 ? launch_p2p_t<32, 4, 6, NEAR>(a, grid, st)
-                    : launch_p2p_t<32, 4, 18, NEAR>(a, grid, st);
+    if (TT == 8) return KW <= 32 ? launch_p2p_t<8, 16, 2, NEAR, GRAD>(a, grid, st)
+                                 : launch_p2p_t<8, 16, 5, NEAR, GRAD>(a, grid, st);
+    if (TT == 16) return KW <= 24 ? launch_p2p_t<16, 8, 3, NEAR, GRAD>(a, grid, st)
+                                  : launch_p2p_t<16, 8, 9, NEAR, GRAD>(a, grid, st);
+    return KW <= 24 ? launch_p2p_t<32, 4, 6, NEAR, GRAD>(a, grid, st)
+                    : launch_p2p_t<32, 4, 18, NEAR, GRAD>(a, grid, st);
 }
 static constexpr int kP2PWindow = 72;
 
@@ -698,8 +700,10 @@ static cylfmm_status build_tree(cylfmm_plan p, const double *r, const double *z,
 static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const double *src_z,
                                     const double *src_S, int64_t ns, const double *fld_r,
                                     const double *fld_z, int64_t nf, double *out_Phi,
-                                    cudaStream_t st, cylfmm_timings *tm)
+                                    cudaStream_t st, cylfmm_timings *tm,
+                                    double *out_dr = nullptr, double *out_dz = nullptr)
 {
+    const bool grad = out_dr != nullptr && out_dz != nullptr;
     const cylfmm_params &q = p->prm;
     const int d = q.depth, K = q.n_modes, pp = q.order, P = (pp + 1) * (pp + 2) / 2;
     // local order (0 = the source order) and the tensor order max(p, pl)
@@ -932,6 +936,8 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     for (int l = 2; l <= d; ++l) fa.lvoff[l] = lvoff[l];
     const int64_t ntiles_act = hcnt[2 * kMaxLevels];
     fa.l2p_accumulate = ns > 0;   // L2P adds the far field onto the near field's rows
+    fa.outr = grad ? reinterpret_cast<double2 *>(out_dr) : nullptr;
+    fa.outz = grad ? reinterpret_cast<double2 *>(out_dz) : nullptr;
     double ms_tensor = ms_seed, ms_p2m = 0, ms_m2m = 0, ms_s2l = 0, ms_l2l = 0, ms_l2p = 0;
     cudaEvent_t e0 = p->ev[10], e1 = p->ev[11];
     auto tic = [&]() { if (tm) cudaEventRecord(e0, st); };
@@ -994,6 +1000,8 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             a.fwd2 = forward_coef(K - 1, q.miller);
             a.exclude = q.exclude_coincident;
             a.out = fa.out;
+            a.outr = fa.outr;
+            a.outz = fa.outz;
             a.out_row = fperm;
             a.accumulate = 0;
             a.tasks = p->tasks.as<int4>();
@@ -1003,7 +1011,9 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             a.n_skipped = ctr + 0;
             a.n_pairs = ctr + 1;
             a.err_flag = p->err.as<int>();
-            CK(launch_p2p<true>(TT, a, dim3((unsigned)maxtasks), st_n));
+            const dim3 grid((unsigned)maxtasks);
+            if (grad) CK((launch_p2p<true, true>(TT, a, grid, st_n)));
+            else CK(launch_p2p<true>(TT, a, grid, st_n));
             p->launches++;
         }
         if (overlap) CK(cudaEventRecord(p->aev[3], st_n));
@@ -1076,8 +1086,9 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         if (overlap && ns > 0 && m0 == 0) CK(cudaStreamWaitEvent(st, p->aev[3], 0));  // near field
         {
             int ngrp = (kw + kL2PModes - 1) / kL2PModes;
-            size_t sm = sizeof(double2) * kL2PModes * Pl + sizeof(double) * kL2PPts * Pl;
-            l2p_kernel<<<(unsigned)((int64_t)fa.tcount[d] * ngrp), 256, sm, st>>>(fa);
+            size_t sm = sizeof(double2) * kL2PModes * Pl + sizeof(double) * kL2PPts * Pl * (grad ? 3 : 1);
+            if (grad) l2p_kernel<true><<<(unsigned)((int64_t)fa.tcount[d] * ngrp), 256, sm, st>>>(fa);
+            else l2p_kernel<false><<<(unsigned)((int64_t)fa.tcount[d] * ngrp), 256, sm, st>>>(fa);
             CKL();
             p->launches++;
         }
@@ -1135,6 +1146,28 @@ extern "C" cylfmm_status cylfmm_fmm_solve(cylfmm_plan plan, const double *src_r,
     CK(cudaSetDevice(plan->device));
     return fmm_solve_impl(plan, src_r, src_z, src_S, n_src, fld_r, fld_z, n_fld, out_Phi,
                           (cudaStream_t)stream, timings);
+}
+
+extern "C" cylfmm_status cylfmm_fmm_solve_grad(cylfmm_plan plan, const double *src_r,
+                                               const double *src_z, const double *src_S,
+                                               int64_t n_src, const double *fld_r,
+                                               const double *fld_z, int64_t n_fld,
+                                               double *out_Phi, double *out_dPhi_dr,
+                                               double *out_dPhi_dz, cylfmm_stream_t stream,
+                                               cylfmm_timings *timings)
+{
+    RET_IF(validate_solve(plan, src_r, src_z, src_S, n_src, fld_r, fld_z, n_fld, out_Phi));
+    if (n_fld > 0 && (!out_dPhi_dr || !out_dPhi_dz)) {
+        set_err("cylfmm_fmm_solve_grad: null gradient output");
+        return CYLFMM_EINVAL;
+    }
+    if (plan->prm.n_modes > kP2PWindow) {
+        set_err("cylfmm_fmm_solve_grad: gradients support n_modes <= %d", kP2PWindow);
+        return CYLFMM_EINVAL;
+    }
+    CK(cudaSetDevice(plan->device));
+    return fmm_solve_impl(plan, src_r, src_z, src_S, n_src, fld_r, fld_z, n_fld, out_Phi,
+                          (cudaStream_t)stream, timings, out_dPhi_dr, out_dPhi_dz);
 }
 
 extern "C" cylfmm_status cylfmm_fmm_solve_host(cylfmm_plan plan, const double *src_r,

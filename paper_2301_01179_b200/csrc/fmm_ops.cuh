@@ -49,6 +49,7 @@ struct FarArgs {
     int64_t lvoff[kMaxLevels];          // dense per-level offsets (level maps, s2l_written)
     const unsigned char *need;          // dense per level: local materialised (see need_kernel)
     int l2p_accumulate;                 // L2P adds onto out (the near field wrote it first)
+    double2 *outr, *outz;               // gradient rows (nullable): dPhi/dr, dPhi/dz
 };
 
 __device__ __forceinline__ int tri(int i, int j, int p) { return i * (p + 1) - i * (i - 1) / 2 + j; }
@@ -354,6 +355,9 @@ inline size_t m2m_smem(int p)
 constexpr int kL2PModes = 16;
 constexpr int kL2PPts = 16;
 
+// GRAD: also d/dr and d/dz of the local polynomial from the derivative
+// monomials k dr^(k-1) dz^l and l dr^k dz^(l-1) (normalised units: an extra 1/h).
+template <bool GRAD>
 __global__ void __launch_bounds__(256) l2p_kernel(FarArgs a)
 {
     extern __shared__ double sm[];
@@ -363,6 +367,7 @@ __global__ void __launch_bounds__(256) l2p_kernel(FarArgs a)
     const int n0 = g * kL2PModes, nm = min(kL2PModes, KW - n0);
     double2 *loc = reinterpret_cast<double2 *>(sm);     // [nm][P]
     double *mono = reinterpret_cast<double *>(loc + kL2PModes * P);  // [pts][P]
+    double *monr = mono + kL2PPts * P, *monz = monr + kL2PPts * P;   // GRAD: derivative monomials
     const uint32_t key = (uint32_t)a.tkeys[d][slot];
     const int t0 = a.flstart[key], t1 = a.flstart[key + 1];
     // the deepest ancestor (or the leaf) that received an S2L contribution: below it the chain
@@ -393,13 +398,20 @@ __global__ void __launch_bounds__(256) l2p_kernel(FarArgs a)
         if (threadIdx.x < nc) {
             int t = c0 + threadIdx.x;
             double dr = (a.fr[t] - rc) / h, dz = (a.fz[t] - zc) / h;
-            double pr = 1.0;
+            double pr = 1.0, prm = 0.0;   // dr^i and i dr^(i-1)
             for (int i = 0; i <= p; ++i) {
-                double pz = pr;
+                double pz = pr, pzm = 0.0, pzr = prm;   // dr^i dz^j, j dr^i dz^(j-1), i dr^(i-1) dz^j
                 for (int j = 0; i + j <= p; ++j) {
                     mono[threadIdx.x * P + tri(i, j, p)] = pz;
+                    if (GRAD) {
+                        monr[threadIdx.x * P + tri(i, j, p)] = pzr;
+                        monz[threadIdx.x * P + tri(i, j, p)] = pzm;
+                    }
+                    pzm = (j + 1) * pz;
                     pz *= dz;
+                    pzr *= dz;
                 }
+                prm = (i + 1) * pr;
                 pr *= dr;
             }
         }
@@ -414,6 +426,26 @@ __global__ void __launch_bounds__(256) l2p_kernel(FarArgs a)
                 sy = fma(lo[kl].y, mo[kl], sy);
             }
             int64_t row = a.fperm[c0 + t];
+            if (GRAD) {
+                const double *mr = monr + t * P, *mz = monz + t * P;
+                double rx = 0.0, ry = 0.0, zx = 0.0, zy = 0.0;
+                for (int kl = 0; kl < P; ++kl) {
+                    rx = fma(lo[kl].x, mr[kl], rx);
+                    ry = fma(lo[kl].y, mr[kl], ry);
+                    zx = fma(lo[kl].x, mz[kl], zx);
+                    zy = fma(lo[kl].y, mz[kl], zy);
+                }
+                const double s2 = inv_h * inv_h;
+                double2 *orr = a.outr + row * a.K + a.m0 + n0 + n, *oz = a.outz + row * a.K + a.m0 + n0 + n;
+                if (a.l2p_accumulate) {
+                    const double2 cr = *orr, cz = *oz;
+                    *orr = make_double2(fma(rx, s2, cr.x), fma(ry, s2, cr.y));
+                    *oz = make_double2(fma(zx, s2, cz.x), fma(zy, s2, cz.y));
+                } else {
+                    *orr = make_double2(rx * s2, ry * s2);
+                    *oz = make_double2(zx * s2, zy * s2);
+                }
+            }
             double2 *o = a.out + row * a.K + a.m0 + n0 + n;
             if (a.l2p_accumulate) {
                 const double2 cur = *o;

@@ -29,6 +29,7 @@ struct P2PArgs {
     int exclude;                // skip coincident pairs
     // output
     double2 *out;               // rows [*][K]
+    double2 *outr, *outz;       // gradient rows dPhi/dr, dPhi/dz (GRAD kernels only)
     const int *out_row;         // target t -> output row (nullptr: row = t)
     int accumulate;             // load initial value from out
     int64_t part_stride;        // direct: out += blockIdx.y * part_stride (complex elements)
@@ -65,20 +66,26 @@ __device__ __forceinline__ uint32_t compact1(uint32_t v)
     return v;
 }
 
-template <int TT, int SC, int MAXT, bool NEAR>
+// GRAD (near field, one mode window from mode 0): also the field gradients, from the paper's
+// first-order derivative relations (P:917-923 in x, P:958-966 in r; G^(-1) == G^(1)):
+//   dG^n/dx = (n - 1/2) x q_n,   dG^n/dr = -G^n/(2r) + (n - 1/2) u q_n,
+//   q_n = (G^n + G^{n-1}) / rho_+^2 + (G^n - G^{n-1}) / rho_-^2,   u = (r^2 - r1^2 - x^2)/(2r).
+template <int TT, int SC, int MAXT, bool NEAR, bool GRAD = false>
 __global__ void __launch_bounds__(TT *SC, (MAXT > 6 ? 4 : 8)) p2p_kernel(P2PArgs a)
 {
     constexpr int NT = TT * SC;
     constexpr int NW = NT / 32;
     const int KW = a.m1 - a.m0;
+    const int KG = GRAD && KW < 2 ? 2 : KW;              // GRAD needs G^1 for mode 0
     extern __shared__ double smem[];
-    double *Gs = smem;                                  // [KW][TT][SC]
-    double2 *Ss = reinterpret_cast<double2 *>(Gs + (size_t)KW * NT);  // [SC][KW]
+    double *Gs = smem;                                  // [KG][TT][SC]
+    double2 *Ss = reinterpret_cast<double2 *>(Gs + (size_t)KG * NT);  // [SC][KW]
     double *src_r = reinterpret_cast<double *>(Ss + (size_t)SC * KW);
     double *src_z = src_r + SC;
     double *tg_r = src_z + SC;
     double *tg_z = tg_r + TT;
-    int *sidx = reinterpret_cast<int *>(tg_z + TT);     // [SC]
+    double *pf = tg_z + TT;                             // GRAD: [4][NT] 1/rho+^2, 1/rho-^2, x, u
+    int *sidx = reinterpret_cast<int *>(pf + (GRAD ? 4 * NT : 0));     // [SC]
     int *order = sidx + SC;                             // [NT]
     int *wcnt = order + NT;                             // [2 NW]
     int *seg = wcnt + 2 * NW;                           // [9][2] + prefix [10]
@@ -136,16 +143,24 @@ __global__ void __launch_bounds__(TT *SC, (MAXT > 6 ? 4 : 8)) p2p_kernel(P2PArgs
     const int total = segpre[nseg];
     double2 *out = a.out + (NEAR ? 0 : (int64_t)blockIdx.y * a.part_stride);
 
-    double2 acc[MAXT];
+    double2 acc[MAXT], accr[GRAD ? MAXT : 1], accz[GRAD ? MAXT : 1];
 #pragma unroll
     for (int k = 0; k < MAXT; ++k) {
         acc[k] = make_double2(0.0, 0.0);
+        if constexpr (GRAD) {
+            accr[k] = make_double2(0.0, 0.0);
+            accz[k] = make_double2(0.0, 0.0);
+        }
         int id = tid + k * NT;
         if (a.accumulate && id < TT * KW) {
             int t = id % TT, n = id / TT;
             if (t < nt) {
                 int64_t row = a.out_row ? a.out_row[t0 + t] : (t0 + t);
                 acc[k] = out[row * a.K + a.m0 + n];
+                if constexpr (GRAD) {
+                    accr[k] = a.outr[row * a.K + a.m0 + n];
+                    accz[k] = a.outz[row * a.K + a.m0 + n];
+                }
             }
         }
     }
@@ -232,9 +247,21 @@ __global__ void __launch_bounds__(TT *SC, (MAXT > 6 ? 4 : 8)) p2p_kernel(P2PArgs
             }
             int S_warp = __reduce_max_sync(0xffffffffu, S_lane);
             if (c == 2) {
-                for (int n = 0; n < KW; ++n) g[n * NT] = 0.0;
+                for (int n = 0; n < KG; ++n) g[n * NT] = 0.0;
             } else {
-                greens_pair(geo, a.m0, a.m1, S_warp, g, NT);
+                greens_pair(geo, a.m0, a.m0 + KG, S_warp, g, NT);
+            }
+            if constexpr (GRAD) {
+                const int q = t * SC + s;
+                if (c == 2) {
+                    pf[q] = pf[NT + q] = pf[2 * NT + q] = pf[3 * NT + q] = 0.0;
+                } else {
+                    const double r = tg_r[t], r1 = src_r[s], x = tg_z[t] - src_z[s];
+                    pf[q] = 1.0 / geo.rp2;
+                    pf[NT + q] = 1.0 / geo.rm2;
+                    pf[2 * NT + q] = x;
+                    pf[3 * NT + q] = (r * r - r1 * r1 - x * x) / (2.0 * r);
+                }
             }
         }
         __syncthreads();
@@ -246,11 +273,35 @@ __global__ void __launch_bounds__(TT *SC, (MAXT > 6 ? 4 : 8)) p2p_kernel(P2PArgs
                 int t = id % TT, n = id / TT;
                 const double *g = Gs + (n * TT + t) * SC;
                 double2 sum = acc[k];
+                if constexpr (GRAD) {
+                    const int nm1 = a.m0 + n == 0 ? 1 : n - 1;     // G^(-1) == G^(1)
+                    const double *gm = Gs + (nm1 * TT + t) * SC;
+                    const double hn = a.m0 + n - 0.5, inv2r = 0.5 / tg_r[t];
+                    double2 sr_ = accr[k], sz_ = accz[k];
 #pragma unroll
-                for (int s = 0; s < SC; ++s) {
-                    double2 sv = Ss[s * KW + n];
-                    sum.x = fma(sv.x, g[s], sum.x);
-                    sum.y = fma(sv.y, g[s], sum.y);
+                    for (int s = 0; s < SC; ++s) {
+                        const int q = t * SC + s;
+                        const double G = g[s], Gm = gm[s];
+                        const double qn = hn * fma(G + Gm, pf[q], (G - Gm) * pf[NT + q]);
+                        const double dz = qn * pf[2 * NT + q];
+                        const double dr = fma(qn, pf[3 * NT + q], -G * inv2r);
+                        double2 sv = Ss[s * KW + n];
+                        sum.x = fma(sv.x, G, sum.x);
+                        sum.y = fma(sv.y, G, sum.y);
+                        sr_.x = fma(sv.x, dr, sr_.x);
+                        sr_.y = fma(sv.y, dr, sr_.y);
+                        sz_.x = fma(sv.x, dz, sz_.x);
+                        sz_.y = fma(sv.y, dz, sz_.y);
+                    }
+                    accr[k] = sr_;
+                    accz[k] = sz_;
+                } else {
+#pragma unroll
+                    for (int s = 0; s < SC; ++s) {
+                        double2 sv = Ss[s * KW + n];
+                        sum.x = fma(sv.x, g[s], sum.x);
+                        sum.y = fma(sv.y, g[s], sum.y);
+                    }
                 }
                 acc[k] = sum;
             }
@@ -264,6 +315,10 @@ __global__ void __launch_bounds__(TT *SC, (MAXT > 6 ? 4 : 8)) p2p_kernel(P2PArgs
             if (t < nt) {
                 int64_t row = a.out_row ? a.out_row[t0 + t] : (t0 + t);
                 out[row * a.K + a.m0 + n] = acc[k];
+                if constexpr (GRAD) {
+                    a.outr[row * a.K + a.m0 + n] = accr[k];
+                    a.outz[row * a.K + a.m0 + n] = accz[k];
+                }
             }
         }
     }
@@ -274,11 +329,13 @@ __global__ void __launch_bounds__(TT *SC, (MAXT > 6 ? 4 : 8)) p2p_kernel(P2PArgs
     if (lane == 0 && a.n_pairs && my_pairs && a.m0 == 0) atomicAdd(a.n_pairs, my_pairs);
 }
 
-template <int TT, int SC>
+template <int TT, int SC, bool GRAD = false>
 inline size_t p2p_smem_bytes(int KW)
 {
     constexpr int NT = TT * SC;
-    return sizeof(double) * ((size_t)KW * NT + 2 * (size_t)SC * KW + 2 * SC + 2 * TT) +
+    const int KG = GRAD && KW < 2 ? 2 : KW;
+    return sizeof(double) * ((size_t)KG * NT + 2 * (size_t)SC * KW + 2 * SC + 2 * TT +
+                             (GRAD ? 4 * NT : 0)) +
            sizeof(int) * (SC + NT + 2 * (NT / 32) + 18 + 10);
 }
 

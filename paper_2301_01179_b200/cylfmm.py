@@ -84,6 +84,9 @@ def lib():
                                    ctypes.POINTER(Timings)]
     L.cylfmm_fmm_solve_host.restype = i
     L.cylfmm_fmm_solve_host.argtypes = L.cylfmm_fmm_solve.argtypes
+    L.cylfmm_fmm_solve_grad.restype = i
+    L.cylfmm_fmm_solve_grad.argtypes = [vp, vp, vp, vp, i64, vp, vp, i64, vp, vp, vp, vp,
+                                        ctypes.POINTER(Timings)]
     L.cylfmm_greens_batch.restype = i
     L.cylfmm_greens_batch.argtypes = [vp, vp, vp, i64, i, i, vp, vp]
     L.cylfmm_tensor_batch.restype = i
@@ -230,6 +233,22 @@ class Plan:
                                       ctypes.byref(tm) if tm is not None else None),
                "cylfmm_fmm_solve")
         return (out, tm.as_dict()) if timings else out
+
+    def solve_grad(self, src_r, src_z, src_S, fld_r, fld_z, timings=False):
+        """Device solve with potential gradients (cylfmm_fmm_solve_grad): returns (Phi, dPhi/dr,
+        dPhi/dz), complex128 [n_fld, K] each (cuda), and the timings dict if requested."""
+        torch = _torch()
+        sr, sz, fr, fz = (_dev_f64(a, torch) for a in (src_r, src_z, fld_r, fld_z))
+        S = _dev_c128(src_S, torch)
+        ns, nf = S.shape[0], fr.shape[0]
+        outs = [torch.empty((nf, self.cfg.n_modes), dtype=torch.complex128, device="cuda")
+                for _ in range(3)]
+        tm = Timings() if timings else None
+        _check(lib().cylfmm_fmm_solve_grad(self._h, _ptr(sr), _ptr(sz), _ptr(S), ns, _ptr(fr),
+                                           _ptr(fz), nf, *[_ptr(o) for o in outs], _stream(torch),
+                                           ctypes.byref(tm) if tm is not None else None),
+               "cylfmm_fmm_solve_grad")
+        return (tuple(outs), tm.as_dict()) if timings else tuple(outs)
 
     def solve_host(self, src_r, src_z, src_S, fld_r, fld_z, out=None, timings=False):
         """Host-buffer solve (cylfmm_fmm_solve_host): numpy in, numpy out, copies included."""

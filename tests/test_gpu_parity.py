@@ -359,3 +359,26 @@ def test_fmm_separate_source_local_orders(gpu, orc, p, pl, K, depth):
     fr, fz, _ = uniform_rings(rng, 700, 1)
     out, ref, _ = _fmm_case(gpu, orc, sr, sz, S, fr, fz, p, depth, 1.0, pl=pl)
     assert eps_modes(out, ref).max() <= TOL
+
+
+@pytest.mark.parametrize("n,K,p,depth,same", [(2000, 5, 8, 4, True), (1500, 1, 6, 3, False),
+                                              (3000, 17, 12, 4, True)])
+def test_fmm_gradients_vs_oracle_fmm(gpu, orc, n, K, p, depth, same):
+    """Potential gradients: dPhi/dr and dPhi/dz from the GPU solve against
+    the oracle's Algorithm 1 with gradients (local-expansion gradient + near-field derivative
+    relations P:917-923, 958-966), in the same metric and tolerance as Phi."""
+    rng = np.random.default_rng(n + K)
+    sr, sz, S = uniform_rings(rng, n, K)
+    if same:
+        fr, fz = sr, sz
+    else:
+        fr, fz, _ = uniform_rings(rng, 400, 1)
+    ref, refr, refz, sk = orc.fmm(sr, sz, S, fr, fz, p, depth, 1.0, grad=True)
+    plan = gpu.Plan(gpu.FMMConfig(n_modes=K, order=p, depth=depth))
+    (F, Fr, Fz), tm = plan.solve_grad(sr, sz, S, fr, fz, timings=True)
+    assert tm["n_skipped"] == sk
+    assert eps_modes(F.cpu().numpy(), ref).max() <= TOL
+    assert eps_modes(Fr.cpu().numpy(), refr).max() <= TOL
+    assert eps_modes(Fz.cpu().numpy(), refz).max() <= TOL
+    # and Phi from the gradient solve equals the plain solve bitwise
+    assert np.array_equal(F.cpu().numpy(), plan.solve(sr, sz, S, fr, fz).cpu().numpy())
