@@ -2,8 +2,10 @@
 // for n = 0..N, written for sm_100a.  Product code: shares nothing with oracle/.
 //
 // Method (the paper's, App. A), re-arranged for the GPU:
-//  * K, E of modulus k = mu (R#1) from the complementary modulus k' = rho_- / rho_+ (R#2) by the
-//    arithmetic-geometric mean (the oracle uses Carlson's R_F/R_D instead: independent code):
+//  * K, E of modulus k = mu (R#1) from the complementary modulus k' = rho_- / rho_+ (R#2): on the
+//    forward branch (k'^2 <= 0.004) by the small-k' series of DLMF 19.12.1-2 (ke_small), on the
+//    Miller branch by the arithmetic-geometric mean (the oracle uses Carlson's R_F/R_D instead:
+//    independent code):
 //      K = pi / (2 AGM(1, k')),  E = K (1 - sum_{m>=0} 2^{m-1} c_m^2),  c_0^2 = k^2 = 4 r r1/rho_+^2.
 //    With mu/(2 pi sqrt(r r1)) = 1/(pi rho_+):  G^(0) = 1/(2 a_inf rho_+),
 //    G^(1) = G^(0) ((1+chi) s - 1)   (from Q_{1/2} = chi mu K - (1+chi) mu E).
@@ -32,11 +34,15 @@ constexpr int kMaxModes = 256;   // CYLFMM_MAX_MODES
 constexpr int kMaxSteps = 4096;  // Miller start index bound
 constexpr double kPi = 3.141592653589793238462643383279502884;
 
+constexpr int kKESeries = 8;      // terms of the small-k' series of K and E (forward branch)
+
 struct RecTables {
     double delta[kMaxSteps + 2];   // Miller: delta_n = beta_n / (alpha_n alpha_{n+1}), n >= 2
     double Pn[kMaxModes + 2];      // Miller: P_n
     double eps[kMaxModes + 2];     // forward: eps_n = b_n R_{n-2} / R_n, n >= 2
     double Rn[kMaxModes + 2];      // forward: R_n
+    // K = L P1(k'^2) + P2(k'^2),  E = 1 + k'^2 (L P3(k'^2) + P4(k'^2)),  L = ln(1/k')
+    double ke[4][kKESeries];
 };
 __constant__ RecTables c_rec;
 
@@ -56,6 +62,38 @@ inline void build_rec_tables(RecTables *t)
     for (int n = 2; n < kMaxModes + 2; ++n) t->Rn[n] = a(n) * t->Rn[n - 1];
     t->eps[0] = t->eps[1] = 0.0;
     for (int n = 2; n < kMaxModes + 2; ++n) t->eps[n] = b(n) * t->Rn[n - 2] / t->Rn[n];
+    // small-k' expansions of the complete elliptic integrals (DLMF 19.12.1-2):
+    //   K = sum_m [(1/2)_m / m!]^2 k'^{2m} (L + d_m),
+    //   E = 1 + 1/2 sum_m (1/2)_m (3/2)_m / ((2)_m m!) k'^{2m+2} (L + d_m - 1/((2m+1)(2m+2))),
+    //   d_0 = 2 ln 2, d_{m+1} = d_m - 1/((m+1)(2m+1))   (long double, rounded once)
+    long double am = 1.0L, bm = 1.0L, dm = 2.0L * logl(2.0L);
+    for (int m = 0; m < kKESeries; ++m) {
+        t->ke[0][m] = (double)(am * am);
+        t->ke[1][m] = (double)(am * am * dm);
+        t->ke[2][m] = (double)(0.5L * am * bm);
+        t->ke[3][m] = (double)(0.5L * am * bm * (dm - 1.0L / ((2.0L * m + 1.0L) * (2.0L * m + 2.0L))));
+        am *= (m + 0.5L) / (m + 1.0L);
+        bm *= (m + 1.5L) / (m + 2.0L);
+        dm -= 1.0L / ((m + 1.0L) * (2.0L * m + 1.0L));
+    }
+}
+
+// K(k) and E(k) for small k'^2 = 1 - k^2 (forward branch: k'^2 <= t/(2+t) <= 0.004, truncation
+// after kKESeries terms < 4e-20 relative); replaces the AGM there (one log, 4 short Horner sums).
+__device__ __forceinline__ void ke_small(double kp2, double &K, double &E)
+{
+    const double L = -0.5 * log(kp2);
+    double p1 = c_rec.ke[0][kKESeries - 1], p2 = c_rec.ke[1][kKESeries - 1];
+    double p3 = c_rec.ke[2][kKESeries - 1], p4 = c_rec.ke[3][kKESeries - 1];
+#pragma unroll
+    for (int m = kKESeries - 2; m >= 0; --m) {
+        p1 = fma(p1, kp2, c_rec.ke[0][m]);
+        p2 = fma(p2, kp2, c_rec.ke[1][m]);
+        p3 = fma(p3, kp2, c_rec.ke[2][m]);
+        p4 = fma(p4, kp2, c_rec.ke[3][m]);
+    }
+    K = fma(L, p1, p2);
+    E = fma(kp2, fma(L, p3, p4), 1.0);
 }
 
 // Pair geometry shared by both branches.
@@ -129,15 +167,15 @@ __device__ __forceinline__ void greens_pair(const PairGeo &g, int m0, int m1, in
 {
     double rho_p = sqrt(g.rp2);
     double inv_rho_p = 1.0 / rho_p;
-    double kp = sqrt(g.rm2) * inv_rho_p;                   // k'
-    double k2 = 4.0 * g.rr1 * inv_rho_p * inv_rho_p;       // k^2 = 1 - k'^2 (no cancellation)
-    double s;
-    double a = agm(kp, k2, g.forward, s);
-    double G0 = 0.5 * inv_rho_p / a;                        // K / (pi rho_+)
     double sum2 = 0.5 * (g.rp2 + g.rm2);                    // r^2 + r1^2 + x^2 = 2 chi r r1
     if (g.forward) {
+        // K, E from the small-k' series (k'^2 = rho_-^2 / rho_+^2 <= 0.004 here)
+        double Kk, Ek;
+        ke_small(g.rm2 * inv_rho_p * inv_rho_p, Kk, Ek);
+        const double G0 = Kk * inv_rho_p * (1.0 / kPi);     // K / (pi rho_+)
         double chi = 0.5 * sum2 / g.rr1;
-        double u0 = G0, u1 = G0 * fma(1.0 + chi, s, -1.0);  // G^(1)
+        // G^(1) / G^(0) = Q_{1/2}/Q_{-1/2} = chi - (1 + chi) E/K
+        double u0 = G0, u1 = G0 * fma(-(1.0 + chi), Ek / Kk, chi);
         if (m0 == 0 && m1 > 0) out[0] = u0;
         if (m0 <= 1 && m1 > 1) out[(1 - m0) * ostride] = u1;
 #pragma unroll 4
@@ -149,6 +187,11 @@ __device__ __forceinline__ void greens_pair(const PairGeo &g, int m0, int m1, in
         }
         return;
     }
+    double kp = sqrt(g.rm2) * inv_rho_p;                   // k'
+    double k2 = 4.0 * g.rr1 * inv_rho_p * inv_rho_p;       // k^2 = 1 - k'^2 (no cancellation)
+    double s;
+    double a = agm(kp, k2, false, s);
+    double G0 = 0.5 * inv_rho_p / a;                        // K / (pi rho_+)
     // Miller, on w_n (see header).  wn = w_n, wl = w_{n-1}; step produces w_{n-2}.
     double inv2chi = g.rr1 / sum2;
     double q = inv2chi * inv2chi;
