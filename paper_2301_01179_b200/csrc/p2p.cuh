@@ -87,8 +87,8 @@ __global__ void __launch_bounds__(TT *SC, (MAXT > 6 ? 4 : 8)) p2p_kernel(P2PArgs
     double *pf = tg_z + TT;                             // GRAD: [4][NT] 1/rho+^2, 1/rho-^2, x, u
     int *sidx = reinterpret_cast<int *>(pf + (GRAD ? 4 * NT : 0));     // [SC]
     int *order = sidx + SC;                             // [NT]
-    int *wcnt = order + NT;                             // [2 NW]
-    int *seg = wcnt + 2 * NW;                           // [9][2] + prefix [10]
+    int *wcnt = order + NT;                             // [3 NW]
+    int *seg = wcnt + 3 * NW;                           // [9][2] + prefix [10]
     int *segpre = seg + 18;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -200,36 +200,42 @@ __global__ void __launch_bounds__(TT *SC, (MAXT > 6 ? 4 : 8)) p2p_kernel(P2PArgs
                     else atomicOr(a.err_flag, 1);
                 } else {
                     PairGeo g = pair_geo(r, r1, z - z1, a.fwd2);
-                    cls = g.forward ? 0 : 1;
+                    cls = g.forward ? 0 : (g.far ? 3 : 1);   // forward / Miller / far
                     ++my_pairs;
                 }
             }
         }
+        // order: forward, far, Miller, skipped (warps then run one evaluation path each)
         unsigned bF = __ballot_sync(0xffffffffu, cls == 0);
+        unsigned bX = __ballot_sync(0xffffffffu, cls == 3);
         unsigned bM = __ballot_sync(0xffffffffu, cls == 1);
         if (lane == 0) {
             wcnt[warp] = __popc(bF);
-            wcnt[NW + warp] = __popc(bM);
+            wcnt[NW + warp] = __popc(bX);
+            wcnt[2 * NW + warp] = __popc(bM);
         }
         __syncthreads();
         {
-            int preF = 0, preM = 0, totF = 0, totM = 0;
+            int preF = 0, preX = 0, preM = 0, totF = 0, totX = 0, totM = 0;
 #pragma unroll
             for (int w = 0; w < NW; ++w) {
-                int cF = wcnt[w], cM = wcnt[NW + w];
+                int cF = wcnt[w], cX = wcnt[NW + w], cM = wcnt[2 * NW + w];
                 if (w < warp) {
                     preF += cF;
+                    preX += cX;
                     preM += cM;
                 }
                 totF += cF;
+                totX += cX;
                 totM += cM;
             }
             unsigned lt = (1u << lane) - 1u;
-            int bf = __popc(bF & lt), bm = __popc(bM & lt);
+            int bf = __popc(bF & lt), bx = __popc(bX & lt), bm = __popc(bM & lt);
             int pos;
             if (cls == 0) pos = preF + bf;
-            else if (cls == 1) pos = totF + preM + bm;
-            else pos = totF + totM + (warp * 32 - preF - preM) + (lane - bf - bm);
+            else if (cls == 3) pos = totF + preX + bx;
+            else if (cls == 1) pos = totF + totX + preM + bm;
+            else pos = totF + totX + totM + (warp * 32 - preF - preX - preM) + (lane - bf - bx - bm);
             order[pos] = tid | (cls << 16);
         }
         __syncthreads();
@@ -336,7 +342,7 @@ inline size_t p2p_smem_bytes(int KW)
     const int KG = GRAD && KW < 2 ? 2 : KW;
     return sizeof(double) * ((size_t)KG * NT + 2 * (size_t)SC * KW + 2 * SC + 2 * TT +
                              (GRAD ? 4 * NT : 0)) +
-           sizeof(int) * (SC + NT + 2 * (NT / 32) + 18 + 10);
+           sizeof(int) * (SC + NT + 3 * (NT / 32) + 18 + 10);
 }
 
 // Deterministic reduction of direct-sum partial results: out[t][n] = sum_part ws[part][t][n].

@@ -43,7 +43,12 @@ struct RecTables {
     double Rn[kMaxModes + 2];      // forward: R_n
     // K = L P1(k'^2) + P2(k'^2),  E = 1 + k'^2 (L P3(k'^2) + P4(k'^2)),  L = ln(1/k')
     double ke[4][kKESeries];
+    // far branch (chi >= kFarChi): A_n = Gamma(n+1/2)/(2 sqrt(pi) Gamma(n+1)) and the term ratios
+    // of 2F1((2n+1)/4, (2n+3)/4; n+1; 1/chi^2)
+    double farA[kMaxModes + 2];
+    double farT[kMaxModes + 2][4];
 };
+constexpr double kFarChi = 1.0e3;        // far branch from chi = 1000 (4 hypergeometric terms)
 __constant__ RecTables c_rec;
 
 // Host-side construction of the recursion constants (exact rationals rounded once).
@@ -76,6 +81,14 @@ inline void build_rec_tables(RecTables *t)
         bm *= (m + 1.5L) / (m + 2.0L);
         dm -= 1.0L / ((m + 1.0L) * (2.0L * m + 1.0L));
     }
+    long double A = 0.5L;
+    for (int n = 0; n < kMaxModes + 2; ++n) {
+        if (n > 0) A *= (n - 0.5L) / n;
+        t->farA[n] = (double)A;
+        const long double a = (2.0L * n + 1.0L) / 4.0L, b = (2.0L * n + 3.0L) / 4.0L, c = n + 1.0L;
+        for (int k = 0; k < 4; ++k)
+            t->farT[n][k] = (double)((a + k) * (b + k) / ((c + k) * (k + 1.0L)));
+    }
 }
 
 // K(k) and E(k) for small k'^2 = 1 - k^2 (forward branch: k'^2 <= t/(2+t) <= 0.004, truncation
@@ -101,6 +114,7 @@ struct PairGeo {
     double rp2, rm2;   // rho_+^2, rho_-^2
     double rr1;        // r * r1
     bool forward;      // chi < 1.008
+    bool far;          // chi >= kFarChi: hypergeometric series in 1/chi^2 (greens_far)
     bool coincident;   // rho_-^2 == 0 (bitwise-equal rings)
 };
 
@@ -123,6 +137,7 @@ __device__ __forceinline__ PairGeo pair_geo(double r, double r1, double x, doubl
     g.rm2 = fma(dm, dm, x * x);
     g.rr1 = r * r1;
     g.forward = g.rm2 < fwd2 * g.rr1;    // chi - 1 < t_N, tie goes backward (R#3)
+    g.far = g.rm2 >= 2.0 * (kFarChi - 1.0) * g.rr1;
     g.coincident = !(g.rm2 > 0.0);
     return g;
 }
@@ -159,12 +174,39 @@ __device__ __forceinline__ double agm(double kp, double k2, bool need_e, double 
     return a;
 }
 
+// Far pairs (chi >= 1000, e.g. a ring near the axis seen from a neighbouring ring): the
+// hypergeometric form of Q_nu (DLMF 14.3.7) with nu = n - 1/2,
+//   G^(n) = A_n q^n F_n(4 q^2) / sqrt(r^2 + r1^2 + x^2),  q = 1/(2 chi) = r r1 / (r^2 + r1^2 + x^2),
+//   F_n(z) = 2F1((2n+1)/4, (2n+3)/4; n+1; z), four terms (relative truncation < 2e-17 for
+//   z <= 4e-6, n <= 256); the same function the Miller recursion evaluates, without
+//   its loop.  q^n underflows to 0 for the highest modes of very distant pairs (correct).
+__device__ __forceinline__ void greens_far(const PairGeo &g, int m0, int m1, double *out, int ostride)
+{
+    const double sum2 = 0.5 * (g.rp2 + g.rm2);
+    const double q = g.rr1 / sum2, z = 4.0 * q * q;
+    double qn = 1.0 / sqrt(sum2);
+    for (int n = 0; n < m1; ++n) {
+        if (n > 0) qn *= q;
+        if (n >= m0) {
+            double t = z * c_rec.farT[n][3];
+            t = z * c_rec.farT[n][2] * (1.0 + t);
+            t = z * c_rec.farT[n][1] * (1.0 + t);
+            t = z * c_rec.farT[n][0] * (1.0 + t);
+            out[(n - m0) * ostride] = c_rec.farA[n] * qn * (1.0 + t);
+        }
+    }
+}
+
 // G^(n)(r, r1, x) for n = 0..m1-1, stored to out[(n - m0) * ostride] for n in [m0, m1).
 // S_warp: Miller start index (only used on the backward branch; must be > m1 and >= 2).
 // The pair must not be coincident.  Out may point to shared or global memory.
 __device__ __forceinline__ void greens_pair(const PairGeo &g, int m0, int m1, int S_warp,
                                             double *out, int ostride)
 {
+    if (g.far) {
+        greens_far(g, m0, m1, out, ostride);
+        return;
+    }
     double rho_p = sqrt(g.rp2);
     double inv_rho_p = 1.0 / rho_p;
     double sum2 = 0.5 * (g.rp2 + g.rm2);                    // r^2 + r1^2 + x^2 = 2 chi r r1
