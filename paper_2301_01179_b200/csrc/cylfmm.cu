@@ -772,19 +772,19 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     RET_IF(p->fr_s.need(8 * nf));
     RET_IF(p->fz_s.need(8 * nf));
     if (ns > 0) {
-        gather_kernel<double><<<nblk(ns, 256), 256, 0, st>>>(src_r, sperm, ns, p->sr_s.as<double>());
-        gather_kernel<double><<<nblk(ns, 256), 256, 0, st>>>(src_z, sperm, ns, p->sz_s.as<double>());
-        gather_rows_kernel<<<nblk(ns * K, 256), 256, 0, st>>>(
-            reinterpret_cast<const double2 *>(src_S), sperm, ns, K, p->S_s.as<double2>());
+        gather_points_kernel<<<nblk(ns * std::max(K, 1), 256), 256, 0, st>>>(
+            src_r, src_z, reinterpret_cast<const double2 *>(src_S), sperm, ns, K,
+            p->sr_s.as<double>(), p->sz_s.as<double>(), p->S_s.as<double2>());
         CKL();
-        p->launches += 3;
+        p->launches++;
     }
     const double *fr_sorted = p->sr_s.as<double>(), *fz_sorted = p->sz_s.as<double>();
     if (!same) {
-        gather_kernel<double><<<nblk(nf, 256), 256, 0, st>>>(fld_r, fperm, nf, p->fr_s.as<double>());
-        gather_kernel<double><<<nblk(nf, 256), 256, 0, st>>>(fld_z, fperm, nf, p->fz_s.as<double>());
+        gather_points_kernel<<<nblk(nf, 256), 256, 0, st>>>(fld_r, fld_z, nullptr, fperm, nf, 0,
+                                                            p->fr_s.as<double>(), p->fz_s.as<double>(),
+                                                            nullptr);
         CKL();
-        p->launches += 2;
+        p->launches++;
         fr_sorted = p->fr_s.as<double>();
         fz_sorted = p->fz_s.as<double>();
     }
@@ -814,11 +814,30 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     RET_IF(p->counts.need(sizeof(int) * (2 * kMaxLevels + 2)));
     int *tmap_b = same ? p->smap.as<int>() : p->tmap.as<int>();
     int *tkeys_b = same ? p->skeys.as<int>() : p->tkeys.as<int>();
-    for (int side = 0; side < (same ? 1 : 2); ++side) {
+    const int nside = same ? 1 : 2;
+    int lsmall = 1;   // levels 2..lsmall in one launch (4^l <= kSmallLevelBoxes)
+    while (lsmall + 1 <= d && pow4(lsmall + 1) <= kSmallLevelBoxes) ++lsmall;
+    if (lsmall >= 2) {
+        SmallLevelArgs sa = {};
+        for (int side = 0; side < nside; ++side) {
+            sa.ls[side] = side == 0 ? p->slstart.as<int>() : flstart;
+            sa.map[side] = side == 0 ? p->smap.as<int>() : p->tmap.as<int>();
+            sa.keys[side] = side == 0 ? p->skeys.as<int>() : p->tkeys.as<int>();
+            sa.count[side] = p->counts.as<int>() + side * kMaxLevels;
+        }
+        for (int l = 0; l <= d + 1 && l < 17; ++l) sa.lvoff[l] = lvoff[l];
+        sa.depth = d;
+        sa.lmin = 2;
+        sa.nlev = lsmall - 1;
+        level_maps_small_kernel<<<nside * sa.nlev, 1024, 0, st>>>(sa);
+        CKL();
+        p->launches++;
+    }
+    for (int side = 0; side < nside; ++side) {
         const int *ls = side == 0 ? p->slstart.as<int>() : flstart;
         int *map = side == 0 ? p->smap.as<int>() : p->tmap.as<int>();
         int *keys = side == 0 ? p->skeys.as<int>() : p->tkeys.as<int>();
-        for (int l = 2; l <= d; ++l) {
+        for (int l = lsmall + 1; l <= d; ++l) {
             int *fl = p->flags.as<int>() + lvoff[l];
             level_flags_kernel<<<nblk(pow4(l), 256), 256, 0, st>>>(ls, d, l, fl);
             CKL();

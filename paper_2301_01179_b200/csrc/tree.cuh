@@ -212,6 +212,62 @@ __global__ void max_col_kernel(const int *keys, const int *count, int *out)
     atomicMax(out, (int)v);
 }
 
+// Level maps of the small levels (4^l <= 4096) for both point sets in ONE launch: CTA per
+// (side, level), flags + block-wide exclusive scan in shared memory (replaces the per-level
+// flags / scan / map launches, which dominate the tree phase of small problems such as C2).
+constexpr int kSmallLevelBoxes = 4096;
+struct SmallLevelArgs {
+    const int *ls[2];          // dense leaf starts per side
+    int *map[2], *keys[2];     // dense level maps / compact key lists (level offsets below)
+    int *count[2];             // per side: count[l]
+    int64_t lvoff[17];
+    int depth, lmin, nlev;     // levels lmin .. lmin + nlev - 1
+};
+__global__ void __launch_bounds__(1024) level_maps_small_kernel(SmallLevelArgs a)
+{
+    __shared__ int wsum[32];
+    const int side = blockIdx.x / a.nlev, level = a.lmin + blockIdx.x % a.nlev;
+    const int nbox = 1 << (2 * level), sh = 2 * (a.depth - level);
+    const int *ls = a.ls[side];
+    int *map = a.map[side] + a.lvoff[level], *keys = a.keys[side] + a.lvoff[level];
+    constexpr int PER = kSmallLevelBoxes / 1024;
+    const int b0 = threadIdx.x * PER;
+    int f[PER], c = 0;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        const int b = b0 + k;
+        f[k] = b < nbox && ls[(int64_t)(b + 1) << sh] > ls[(int64_t)b << sh];
+        c += f[k];
+    }
+    // block exclusive scan of c
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int x = c;
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        int v = wsum[lane];
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += y;
+        }
+        wsum[lane] = v;   // inclusive per warp
+    }
+    __syncthreads();
+    int pos = x - c + (w > 0 ? wsum[w - 1] : 0);
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        const int b = b0 + k;
+        if (b >= nbox) break;
+        map[b] = f[k] ? pos : -1;
+        if (f[k]) keys[pos++] = b;
+    }
+    if (threadIdx.x == 1023) a.count[side][level] = wsum[31];
+}
+
 template <typename T>
 __global__ void gather_kernel(const T *in, const int *perm, int64_t n, T *out)
 {
@@ -228,6 +284,24 @@ __global__ void gather_rows_kernel(const double2 *in, const int *perm, int64_t n
     int64_t i = e / K;
     int k = (int)(e - i * K);
     out[e] = in[(int64_t)perm[i] * K + k];
+}
+
+// sorted copies of a point set in one pass: r, z (and the coefficient rows when S != nullptr)
+__global__ void gather_points_kernel(const double *r, const double *z, const double2 *S,
+                                     const int *perm, int64_t n, int K, double *rs, double *zs,
+                                     double2 *Ss)
+{
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < n) {
+        const int pi = perm[e];
+        rs[e] = r[pi];
+        zs[e] = z[pi];
+    }
+    if (S && e < n * K) {
+        const int64_t i = e / K;
+        const int k = (int)(e - i * K);
+        Ss[e] = S[(int64_t)perm[i] * K + k];
+    }
 }
 
 }  // namespace cyl
