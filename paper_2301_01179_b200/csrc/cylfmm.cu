@@ -15,6 +15,7 @@
 
 #include "fmm_ops.cuh"
 #include "p2p.cuh"
+#include "p2p_warp.cuh"
 #include "specfun.cuh"
 #include "tensor.cuh"
 #include "tree.cuh"
@@ -75,6 +76,8 @@ static cudaError_t allow_smem(F *kernel)
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
 }
 
+#define P2PW_INSTANCES(X) X(9, true, false) X(17, true, false) X(17, true, true) X(33, true, false) \
+    X(9, false, false) X(17, false, false) X(33, false, false)
 #define P2P_INSTANCES(X)                                                                       \
     X(8, 16, 2) X(8, 16, 5) X(16, 8, 3) X(16, 8, 9) X(32, 4, 6) X(32, 4, 18)
 
@@ -112,6 +115,9 @@ static cylfmm_status ensure_init()
     cudaError_t e = cudaMemcpyToSymbol(c_rec, t, sizeof(RecTables));
     delete t;
     CK(e);
+#define X(KT, E, W) CK(allow_smem(p2p_warp_kernel<KT, E, W>));
+    P2PW_INSTANCES(X)
+#undef X
 #define X(TT, SC, MT)                                                                          \
     CK(allow_smem(p2p_kernel<TT, SC, MT, true>));                                              \
     CK(allow_smem(p2p_kernel<TT, SC, MT, true, true>));                                        \
@@ -164,6 +170,40 @@ static cudaError_t launch_p2p(int TT, const P2PArgs &a, dim3 grid, cudaStream_t 
                     : launch_p2p_t<32, 4, 18, NEAR, GRAD>(a, grid, st);
 }
 static constexpr int kP2PWindow = 72;
+
+// warp-task near field (p2p_warp.cuh): compile-time mode bound KT >= K
+static int p2pw_kt(int K)
+{
+    if (K <= 9) return 9;
+    if (K <= 17) return 17;
+    if (K <= 33) return 33;
+    return 0;
+}
+static bool p2pw_enabled(int K, bool grad)
+{
+    if (grad || p2pw_kt(K) == 0) return false;
+    const char *e = getenv("CYLFMM_P2P_VARIANT");
+    return !(e && atoi(e) == 1);
+}
+static cudaError_t launch_p2pw(const P2PArgs &a, cudaStream_t st)
+{
+    const char *e = getenv("CYLFMM_P2P_VARIANT");
+    const int kt = p2pw_kt(a.K);
+    const bool wsm = e && atoi(e) == 2;
+    const bool exact = a.K == kt && !(e && atoi(e) == 3);
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+#define X(KT, E, W)                                                                            \
+    if (kt == KT && exact == E && wsm == W) {                                                  \
+        p2p_warp_kernel<KT, E, W><<<nsm * p2pw_min_blocks<KT, W>(), 128,                       \
+                                    p2pw_smem_bytes<KT, W>(), st>>>(a);                        \
+        return cudaGetLastError();                                                             \
+    }
+    P2PW_INSTANCES(X)
+#undef X
+    return cudaErrorInvalidValue;
+}
 
 // ------------------------------------------------------------------------------------------
 // direct modal sum
@@ -989,17 +1029,29 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         const int ntl = fa.tcount[d];
         double avg = (double)nf / std::max(ntl, 1);
         const int TT = avg <= 10.0 ? 8 : (avg <= 24.0 ? 16 : 32);
+        const bool wk = p2pw_enabled(K, grad);
         RET_IF(p->tcnt.need(sizeof(int) * (ntl + 1)));
-        RET_IF(p->ntasks.need(sizeof(int)));
-        int64_t maxtasks = nf / TT + ntl + 1;
+        RET_IF(p->ntasks.need(kTaskCtrInts * sizeof(int)));
+        // warp tasks: <= nf/32 full pieces + <= 5 power-of-two pieces per leaf
+        int64_t maxtasks = wk ? nf / 32 + 6 * (int64_t)ntl + 1 : nf / TT + ntl + 1;
         RET_IF(p->tasks.need(sizeof(int4) * maxtasks));
-        near_tasks_count_kernel<<<nblk(ntl, 256), 256, 0, st_n>>>(fa.tkeys[d], ntl, fa.flstart, TT,
-                                                               p->tcnt.as<int>());
-        CKL();
-        RET_IF(scan_excl(p, p->tcnt.as<int>(), ntl, st_n));
-        near_tasks_emit_kernel<<<nblk(ntl, 256), 256, 0, st_n>>>(fa.tkeys[d], ntl, fa.flstart, TT,
-                                                              p->tcnt.as<int>(), p->tasks.as<int4>(),
-                                                              p->ntasks.as<int>());
+        if (wk) {
+            CK(cudaMemsetAsync(p->ntasks.as<int>(), 0, kTaskCtrInts * sizeof(int), st_n));
+            near_wtasks_count_kernel<<<nblk(ntl, 256), 256, 0, st_n>>>(fa.tkeys[d], ntl, fa.flstart,
+                                                                    fa.slstart, d, p->ntasks.as<int>());
+            CKL();
+            near_wtasks_emit_kernel<<<nblk(ntl, 256), 256, 0, st_n>>>(fa.tkeys[d], ntl, fa.flstart,
+                                                                   fa.slstart, d, p->tasks.as<int4>(),
+                                                                   p->ntasks.as<int>());
+        } else {
+            near_tasks_count_kernel<<<nblk(ntl, 256), 256, 0, st_n>>>(fa.tkeys[d], ntl, fa.flstart, TT,
+                                                                   p->tcnt.as<int>());
+            CKL();
+            RET_IF(scan_excl(p, p->tcnt.as<int>(), ntl, st_n));
+            near_tasks_emit_kernel<<<nblk(ntl, 256), 256, 0, st_n>>>(fa.tkeys[d], ntl, fa.flstart, TT,
+                                                                  p->tcnt.as<int>(), p->tasks.as<int4>(),
+                                                                  p->ntasks.as<int>());
+        }
         CKL();
         p->launches += 2;
         unsigned long long *ctr = p->ctr.as<unsigned long long>();
@@ -1031,7 +1083,9 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             a.n_pairs = ctr + 1;
             a.err_flag = p->err.as<int>();
             const dim3 grid((unsigned)maxtasks);
-            if (grad) CK((launch_p2p<true, true>(TT, a, grid, st_n)));
+            a.task_ctr = p->ntasks.as<int>() + 1;
+            if (wk) CK(launch_p2pw(a, st_n));
+            else if (grad) CK((launch_p2p<true, true>(TT, a, grid, st_n)));
             else CK(launch_p2p<true>(TT, a, grid, st_n));
             p->launches++;
         }

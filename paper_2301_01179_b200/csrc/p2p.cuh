@@ -37,6 +37,7 @@ struct P2PArgs {
     int64_t src_per_part;
     const int4 *tasks;          // near: {t0, t1, leafkey, 0}
     const int *ntasks;          // near: device count
+    int *task_ctr;              // near, warp-task kernel: dynamic task counter (zeroed)
     const int *leafstart;       // near: dense source leaf starts [4^d + 1]
     int depth;
     unsigned long long *n_skipped;

@@ -1,0 +1,434 @@
+// p2p_warp.cuh -- FMM near field with warp-autonomous tasks: the paper's bottleneck
+// (P:582-584, 729-733, 799-802), Phi_t^(n) += sum_s S_s^(n) G^(n)(r_t, r_s, z_t - z_s) over the
+// sources of the 9 neighbour leaves of t's leaf, bitwise-coincident pairs skipped (R#15).
+//
+// Design (sm_100a, FP64 CUDA cores).  The CTA-wide variant (p2p.cuh) classifies and compacts
+// pairs across the CTA and therefore synchronises four times per 128 pairs; on C2 a third of its
+// stall samples were barrier waits and most issue slots went to index arithmetic.  Here every
+// warp owns one task (<= 32 targets of one leaf) and never waits for another warp:
+//   * lanes = (target tl, source slot sl), TW x SL = 32, TW = the task's target count rounded up
+//     to a power of two (tasks are emitted as power-of-two-sized pieces of a leaf);
+//   * the task's source rows (r, z and the K-mode coefficient row) are staged by the warp into
+//     its own shared-memory slice, 32 sources per stage (odd row stride: the SL rows read by one
+//     LDS.128 fall into distinct bank quads), __syncwarp only;
+//   * per stage each lane classifies its pairs (forward chi < 1.008 / Miller / far chi >= 1000 /
+//     skipped, R#3) and walks them class by class (forward, far, then Miller: iteration i of
+//     the warp runs the same branch on as many lanes as the per-lane class counts allow);
+//   * G^(n) is produced in registers and contracted at once into the lane's register
+//     accumulators acc[n] (forward and far upward in n; Miller downward into w[n], normalised
+//     upward by G^(0) = K/(pi rho_+) from the AGM);
+//   * the SL partial sums of a target are combined by a fixed xor-shuffle tree, so results are
+//     bitwise reproducible.
+// Mode window: all K <= KT modes in one pass (KT compile-time: register arrays).
+#pragma once
+#include "p2p.cuh"
+
+namespace cyl {
+
+constexpr int kWarpCH = 32;   // sources per warp stage
+constexpr int kWarps = 4;     // warps per CTA (one task per CTA, the source list split in four)
+
+template <int KT>
+__host__ __device__ constexpr int p2pw_row() { return KT | 1; }   // odd double2 row stride
+
+// WSM ("wide occupancy"): four resident CTAs per SM (register cap 128) instead of three
+template <int KT, bool WSM>
+inline size_t p2pw_smem_bytes()
+{
+    return (size_t)kWarps * (sizeof(double2) * kWarpCH * p2pw_row<KT>() + sizeof(double) * 2 * kWarpCH +
+                             sizeof(int) * kWarpCH) +
+           sizeof(int) * 19;
+}
+template <int KT, bool WSM>
+__host__ __device__ constexpr int p2pw_min_blocks()
+{
+    return KT <= 9 ? 4 : (KT <= 17 ? (WSM ? 4 : 3) : 2);
+}
+
+__device__ __forceinline__ double2 cfma(double2 s, double g, double2 acc)
+{
+    acc.x = fma(s.x, g, acc.x);
+    acc.y = fma(s.y, g, acc.y);
+    return acc;
+}
+
+// A CTA works on one task at a time (<= 32 targets of one leaf); warp w takes the w-th quarter
+// of the task's source list; the four partial sums are added in warp order at the end
+// (deterministic).  Persistent CTAs fetch tasks from *a.task_ctr (zeroed before the launch).
+// EXACT: the mode count equals KT (no per-mode guards).
+template <int KT, bool EXACT, bool WSM>
+__global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_kernel(P2PArgs a)
+{
+    constexpr int CH = kWarpCH, ROW = p2pw_row<KT>();
+    extern __shared__ double smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // layout: S rows [kWarps][CH][ROW] double2 | r, z [kWarps][2 CH] | source index [kWarps][CH] |
+    //         segments: starts [9], prefixes [9], total
+    double2 *stS0 = reinterpret_cast<double2 *>(smem);
+    double2 *stS = stS0 + (size_t)warp * CH * ROW;
+    double *stR = reinterpret_cast<double *>(stS0 + (size_t)kWarps * CH * ROW) + warp * 2 * CH;
+    double *stZ = stR + CH;
+    double *wbase = reinterpret_cast<double *>(stS0 + (size_t)kWarps * CH * ROW) + kWarps * 2 * CH;
+    int *stG = reinterpret_cast<int *>(wbase) + warp * CH;
+    int *segS0 = reinterpret_cast<int *>(wbase) + kWarps * CH;
+    int *segPre = segS0 + 9;
+
+    unsigned my_skipped = 0, my_pairs = 0;
+    const int ntasks = *a.ntasks;
+    for (;;) {                                           // persistent: fetch tasks heaviest first
+    if (threadIdx.x == 0) segS0[18] = atomicAdd(a.task_ctr, 1);
+    __syncthreads();
+    const int task = segS0[18];
+    __syncthreads();
+    if (task >= ntasks) break;                           // CTA-uniform
+    const int4 tk = a.tasks[task];
+    const int t0 = tk.x, nt = tk.y - tk.x;
+    const int TW = nt <= 1 ? 1 : 1 << (32 - __clz(nt - 1));   // next power of two >= nt
+    const int lgTW = __ffs(TW) - 1;
+    const int SL = 32 >> lgTW;
+    const int tl = lane & (TW - 1), sl = lane >> lgTW;
+    const bool tvalid = tl < nt;
+    const int KW = EXACT ? KT : a.m1 - a.m0;            // m0 = 0
+
+    // neighbour source segments (warp 0, lane k < 9 = neighbour k), prefix by shuffles
+    if (warp == 0) {
+        int s0 = 0, len = 0;
+        const uint32_t key = (uint32_t)tk.z;
+        const int ix = (int)compact1(key), iz = (int)compact1(key >> 1), nb = 1 << a.depth;
+        if (lane < 9) {
+            const int x = ix + lane / 3 - 1, z = iz + lane % 3 - 1;
+            if (x >= 0 && z >= 0 && x < nb && z < nb) {
+                const uint32_t m = morton2((uint32_t)x, (uint32_t)z);
+                s0 = a.leafstart[m];
+                len = a.leafstart[m + 1] - s0;
+            }
+        }
+        int incl = len;
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) {
+            int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        if (lane < 9) {
+            segS0[lane] = s0;
+            segPre[lane] = incl - len;
+        }
+        if (lane == 8) segS0[18] = incl;                 // total (after segS0[9], segPre[9])
+    }
+    __syncthreads();
+    const int total = segS0[18];
+    const int vb = (int)(((int64_t)total * warp) / kWarps), ve = (int)(((int64_t)total * (warp + 1)) / kWarps);
+
+    const double tr = a.fr[t0 + min(tl, nt - 1)], tz = a.fz[t0 + min(tl, nt - 1)];
+    double2 acc[KT];
+#pragma unroll
+    for (int j = 0; j < KT; ++j) acc[j] = make_double2(0.0, 0.0);
+    const int Nglob = a.K - 1;
+    const double fwd2 = a.fwd2;
+
+    for (int v0 = vb; v0 < ve; v0 += CH) {
+        const int nch = min(CH, ve - v0);
+        __syncwarp();
+        if (lane < nch) {
+            const int v = v0 + lane;
+            int k = 0;
+#pragma unroll
+            for (int kk = 1; kk < 9; ++kk) k += (v >= segPre[kk]);
+            const int gi = segS0[k] + (v - segPre[k]);
+            stG[lane] = gi;
+            stR[lane] = a.sr[gi];
+            stZ[lane] = a.sz[gi];
+        }
+        __syncwarp();
+        // coefficient rows: element e = s KW + n, lanes stride 32 elements
+        {
+            int s = lane / KW, n = lane - s * KW;
+            const int ds = 32 / KW, dn = 32 - ds * KW;
+#pragma unroll 4
+            for (int e = lane; e < nch * KW; e += 32) {
+                stS[s * ROW + n] = a.S[(int64_t)stG[s] * a.K + n];
+                s += ds;
+                n += dn;
+                if (n >= KW) {
+                    n -= KW;
+                    ++s;
+                }
+            }
+        }
+        __syncwarp();
+        // classify this lane's pairs c = sl + SL i
+        unsigned mF = 0, mX = 0, mM = 0;
+        const int npl = (nch - sl + SL - 1) / SL;    // pairs of this lane (may be <= 0)
+        if (tvalid) {
+            for (int i = 0; i < npl; ++i) {
+                const int c = sl + SL * i;
+                const double r1 = stR[c], z1 = stZ[c];
+                if (tr == r1 && tz == z1) {
+                    if (a.exclude) ++my_skipped;
+                    else atomicOr(a.err_flag, 1);
+                    continue;
+                }
+                const PairGeo g = pair_geo(tr, r1, tz - z1, fwd2);
+                if (g.forward) mF |= 1u << i;
+                else if (g.far) mX |= 1u << i;
+                else mM |= 1u << i;
+            }
+        }
+        const int nF = __popc(mF), nX = __popc(mX), nM = __popc(mM);
+        my_pairs += nF + nX + nM;
+        // forward and far pairs, one per lane and iteration
+        const int itFX = __reduce_max_sync(0xffffffffu, nF + nX);
+        for (int it = 0; it < itFX; ++it) {
+            int cls = 2, idx = 0;
+            if (mF) { cls = 0; idx = __ffs(mF) - 1; mF &= mF - 1; }
+            else if (mX) { cls = 3; idx = __ffs(mX) - 1; mX &= mX - 1; }
+            const int c = sl + SL * idx;
+            const PairGeo g = pair_geo(tr, stR[c], tz - stZ[c], fwd2);
+            const double2 *Srow = stS + c * ROW;
+            if (cls == 0) {
+                // forward on u_n = G_n / R_n, K, E by the small-k' series
+                const double inv_rho_p = 1.0 / sqrt(g.rp2);
+                double Kk, Ek;
+                ke_small(g.rm2 * inv_rho_p * inv_rho_p, Kk, Ek);
+                const double G0 = Kk * inv_rho_p * (1.0 / kPi);
+                const double chi = 0.25 * (g.rp2 + g.rm2) / g.rr1;
+                double u0 = G0, u1 = G0 * fma(-(1.0 + chi), Ek / Kk, chi);
+                acc[0] = cfma(Srow[0], u0, acc[0]);
+                if (KW > 1) acc[1] = cfma(Srow[1], u1, acc[1]);
+#pragma unroll
+                for (int n = 2; n < KT; ++n) {
+                    if (n < KW) {
+                        const double u2 = fma(chi, u1, -c_rec.eps[n] * u0);
+                        acc[n] = cfma(Srow[n], u2 * c_rec.Rn[n], acc[n]);
+                        u0 = u1;
+                        u1 = u2;
+                    }
+                }
+            } else if (cls == 3) {
+                // far (chi >= 1000): hypergeometric form (DLMF 14.3.7), see greens_far
+                const double sum2 = 0.5 * (g.rp2 + g.rm2);
+                const double q = g.rr1 / sum2, z = 4.0 * q * q;
+                double qn = 1.0 / sqrt(sum2);
+#pragma unroll
+                for (int n = 0; n < KT; ++n) {
+                    if (n < KW) {
+                        if (n > 0) qn *= q;
+                        double t = z * c_rec.farT[n][3];
+                        t = z * c_rec.farT[n][2] * (1.0 + t);
+                        t = z * c_rec.farT[n][1] * (1.0 + t);
+                        t = z * c_rec.farT[n][0] * (1.0 + t);
+                        acc[n] = cfma(Srow[n], c_rec.farA[n] * qn * (1.0 + t), acc[n]);
+                    }
+                }
+            }
+        }
+        // Miller pairs, two per lane and iteration in lockstep (two independent
+        // dependency chains per lane: the recursion is latency-bound).  w_n is recomputed in a
+        // second pass over the last KW steps instead of being stored: pass 1 yields w_0 and the
+        // normalisation c = G^(0) / w_0, pass 2 contracts G_n = w_n P_n c (2 chi)^-n downward.
+        const int itM = __reduce_max_sync(0xffffffffu, (nM + 1) >> 1);
+        for (int it = 0; it < itM; ++it) {
+            int ia = -1, ib = -1;
+            if (mM) { ia = __ffs(mM) - 1; mM &= mM - 1; }
+            if (mM) { ib = __ffs(mM) - 1; mM &= mM - 1; }
+            const bool va = ia >= 0, vb = ib >= 0;
+            const int ca = sl + SL * (va ? ia : 0), cb = vb ? sl + SL * ib : ca;
+            const PairGeo gA = pair_geo(tr, stR[ca], tz - stZ[ca], fwd2);
+            const PairGeo gB = pair_geo(tr, stR[cb], tz - stZ[cb], fwd2);
+            const int S_lane = va ? Nglob + max(miller_extra(gA, a.miller), miller_extra(gB, a.miller)) : 0;
+            const int S_warp = __reduce_max_sync(0xffffffffu, S_lane);
+            if (va) {
+                const double ipA = 1.0 / sqrt(gA.rp2), ipB = 1.0 / sqrt(gB.rp2);
+                // AGM(1, k') of both pairs (K = pi / (2 AGM)); a converged pair is frozen
+                double a1 = 1.0, b1 = sqrt(gA.rm2) * ipA, a2 = 1.0, b2 = sqrt(gB.rm2) * ipB;
+#pragma unroll 1
+                for (int k = 0; k < 40; ++k) {
+                    const bool uA = fabs(0.5 * (a1 - b1)) > 2.0e-16 * a1;
+                    const bool uB = fabs(0.5 * (a2 - b2)) > 2.0e-16 * a2;
+                    if (!uA && !uB) break;
+                    const double nA = 0.5 * (a1 + b1), nB = 0.5 * (a2 + b2);
+                    const double sA = sqrt(a1 * b1), sB = sqrt(a2 * b2);
+                    if (uA) { a1 = nA; b1 = sA; }
+                    if (uB) { a2 = nB; b2 = sB; }
+                }
+                const double G0A = 0.5 * ipA / a1, G0B = 0.5 * ipB / a2;
+                const double sumA = 0.5 * (gA.rp2 + gA.rm2), sumB = 0.5 * (gB.rp2 + gB.rm2);
+                const double i2A = gA.rr1 / sumA, i2B = gB.rr1 / sumB;      // 1 / (2 chi)
+                const double qA = i2A * i2A, qB = i2B * i2B;
+                double wnA = 0.0, wlA = 1.0, wnB = 0.0, wlB = 1.0;
+                int n = S_warp;
+                while (n > KW + 1) {
+                    const int nstop = max(KW + 1, n - 64);
+#pragma unroll 4
+                    for (; n > nstop; --n) {
+                        const double d = c_rec.delta[n];
+                        const double wA = fma(-d * qA, wnA, wlA);
+                        const double wB = fma(-d * qB, wnB, wlB);
+                        wnA = wlA;
+                        wlA = wA;
+                        wnB = wlB;
+                        wlB = wB;
+                    }
+                    int ex;
+                    frexp(wlA, &ex);
+                    wnA = ldexp(wnA, -ex);
+                    wlA = ldexp(wlA, -ex);
+                    frexp(wlB, &ex);
+                    wnB = ldexp(wnB, -ex);
+                    wlB = ldexp(wlB, -ex);
+                }
+                // pass 1: w_0 of both chains (wl = w_KW, wn = w_{KW+1} here)
+                double xnA = wnA, xlA = wlA, xnB = wnB, xlB = wlB;
+                double cvA = 1.0, cvB = 1.0;
+#pragma unroll
+                for (int j = KT - 1; j >= 0; --j) {
+                    if (j < KW) {
+                        const double d = c_rec.delta[j + 2];
+                        const double wA = fma(-d * qA, xnA, xlA);
+                        const double wB = fma(-d * qB, xnB, xlB);
+                        xnA = xlA;
+                        xlA = wA;
+                        xnB = xlB;
+                        xlB = wB;
+                        if (j > 0) {
+                            cvA *= i2A;
+                            cvB *= i2B;
+                        }
+                    }
+                }
+                cvA *= G0A / xlA;                        // c (2 chi)^-(KW-1)
+                cvB = vb ? cvB * (G0B / xlB) : 0.0;
+                const double tcA = sumA / gA.rr1, tcB = sumB / gB.rr1;   // 2 chi
+                // pass 2: G_j = w_j P_j c (2 chi)^-j, j = KW-1 .. 0
+#pragma unroll
+                for (int j = KT - 1; j >= 0; --j) {
+                    if (j < KW) {
+                        const double d = c_rec.delta[j + 2];
+                        const double wA = fma(-d * qA, wnA, wlA);
+                        const double wB = fma(-d * qB, wnB, wlB);
+                        wnA = wlA;
+                        wlA = wA;
+                        wnB = wlB;
+                        wlB = wB;
+                        const double2 SA = stS[ca * ROW + j], SB = stS[cb * ROW + j];
+                        acc[j] = cfma(SA, wA * c_rec.Pn[j] * cvA, acc[j]);
+                        acc[j] = cfma(SB, wB * c_rec.Pn[j] * cvB, acc[j]);
+                        cvA *= tcA;
+                        cvB *= tcB;
+                    }
+                }
+            }
+        }
+    }
+    // combine the SL partial sums of each target (fixed xor tree), then the four warps in order
+    for (int o = TW; o < 32; o <<= 1) {
+#pragma unroll
+        for (int j = 0; j < KT; ++j) {
+            acc[j].x += __shfl_xor_sync(0xffffffffu, acc[j].x, o);
+            acc[j].y += __shfl_xor_sync(0xffffffffu, acc[j].y, o);
+        }
+    }
+    __syncthreads();                                     // staging buffers are free
+    double2 *red = stS0;                                 // [kWarps][KT][32] <= [kWarps][CH][ROW]
+    if (sl == 0) {
+#pragma unroll
+        for (int j = 0; j < KT; ++j)
+            if (j < KW) red[(warp * KT + j) * 32 + tl] = acc[j];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nt * KW; e += 32 * kWarps) {
+        const int t = e / KW, j = e - t * KW;
+        double2 v = red[j * 32 + t];
+#pragma unroll
+        for (int w = 1; w < kWarps; ++w) {
+            const double2 p = red[(w * KT + j) * 32 + t];
+            v.x += p.x;
+            v.y += p.y;
+        }
+        const int64_t row = a.out_row ? a.out_row[t0 + t] : (t0 + t);
+        double2 *o = a.out + row * a.K + a.m0 + j;
+        if (a.accumulate) {
+            const double2 p = *o;
+            v.x += p.x;
+            v.y += p.y;
+        }
+        *o = v;
+    }
+    }   // task loop
+    my_skipped = __reduce_add_sync(0xffffffffu, my_skipped);
+    my_pairs = __reduce_add_sync(0xffffffffu, my_pairs);
+    if (lane == 0 && a.n_skipped && my_skipped) atomicAdd(a.n_skipped, (unsigned long long)my_skipped);
+    if (lane == 0 && a.n_pairs && my_pairs) atomicAdd(a.n_pairs, (unsigned long long)my_pairs);
+}
+
+// Near-field tasks for the warp kernel: each target leaf is cut into pieces of 32 targets, the
+// remainder r < 32 into power-of-two pieces unless r fills >= 3/4 of the next power of two.
+// Tasks are emitted heaviest first (32 buckets by log2 of lanes x sources; the task order
+// does not affect any result: every task owns its output rows), so the persistent CTAs finish
+// together.  ctr layout: [0] ntasks, [1] fetch counter, [2..33] bucket counts, [34..65] fill.
+// size of the next piece of a leaf with nt >= 1 remaining targets
+__device__ __forceinline__ int piece_size(int nt)
+{
+    if (nt >= 32) return 32;
+    const int p = nt <= 1 ? 1 : 1 << (32 - __clz(nt - 1));
+    return (4 * nt >= 3 * p) ? nt : p / 2;
+}
+constexpr int kTaskCtrInts = 66;
+__device__ __forceinline__ int near_sources(int key, const int *slstart, int depth)
+{
+    const int ix = (int)compact1((uint32_t)key), iz = (int)compact1((uint32_t)key >> 1), nb = 1 << depth;
+    int tot = 0;
+    for (int da = -1; da <= 1; ++da)
+        for (int dc = -1; dc <= 1; ++dc) {
+            const int x = ix + da, z = iz + dc;
+            if (x < 0 || z < 0 || x >= nb || z >= nb) continue;
+            const uint32_t m = morton2((uint32_t)x, (uint32_t)z);
+            tot += slstart[m + 1] - slstart[m];
+        }
+    return tot;
+}
+__device__ __forceinline__ int task_bucket(int nt, int nsrc)
+{
+    const int tw = nt <= 1 ? 1 : 1 << (32 - __clz(nt - 1));
+    const unsigned cost = (unsigned)tw * (unsigned)max(nsrc, 1);
+    return 31 - __clz(cost);
+}
+__global__ void near_wtasks_count_kernel(const int *tkeys, int nleaf, const int *flstart,
+                                         const int *slstart, int depth, int *ctr)
+{
+    int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nleaf) return;
+    const int key = tkeys[s];
+    const int nsrc = near_sources(key, slstart, depth);
+    for (int nt = flstart[key + 1] - flstart[key]; nt > 0;) {
+        const int take = piece_size(nt);
+        atomicAdd(&ctr[2 + task_bucket(take, nsrc)], 1);
+        nt -= take;
+    }
+}
+__global__ void near_wtasks_emit_kernel(const int *tkeys, int nleaf, const int *flstart,
+                                        const int *slstart, int depth, int4 *tasks, int *ctr)
+{
+    __shared__ int off[32];
+    if (threadIdx.x < 32) {
+        int o = 0;                                       // buckets in descending order
+        for (int b = 31; b > (int)threadIdx.x; --b) o += ctr[2 + b];
+        off[threadIdx.x] = o;
+        if (blockIdx.x == 0 && threadIdx.x == 0) ctr[0] = o + ctr[2];
+    }
+    __syncthreads();
+    int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nleaf) return;
+    const int key = tkeys[s];
+    const int nsrc = near_sources(key, slstart, depth);
+    int t = flstart[key], nt = flstart[key + 1] - t;
+    while (nt > 0) {
+        const int take = piece_size(nt);
+        const int b = task_bucket(take, nsrc);
+        tasks[off[b] + atomicAdd(&ctr[34 + b], 1)] = make_int4(t, t + take, key, 0);
+        t += take;
+        nt -= take;
+    }
+}
+
+}  // namespace cyl
