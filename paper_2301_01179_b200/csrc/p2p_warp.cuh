@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
         }
         __syncwarp();
         // classify this lane's pairs c = sl + SL i
-        unsigned mF = 0, mX = 0, mM = 0;
+        unsigned mF = 0, mX = 0, mM = 0, mL = 0;     // forward, far, Miller short / long
         const int npl = (nch - sl + SL - 1) / SL;    // pairs of this lane (may be <= 0)
         if (tvalid) {
             for (int i = 0; i < npl; ++i) {
@@ -171,10 +171,11 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
                 const PairGeo g = pair_geo(tr, r1, tz - z1, fwd2);
                 if (g.forward) mF |= 1u << i;
                 else if (g.far) mX |= 1u << i;
+                else if (g.rm2 < 0.1122 * g.rr1) mL |= 1u << i;   // chi < 1.0561: e >= 64
                 else mM |= 1u << i;
             }
         }
-        const int nF = __popc(mF), nX = __popc(mX), nM = __popc(mM);
+        const int nF = __popc(mF), nX = __popc(mX), nM = __popc(mM) + __popc(mL);
         my_pairs += nF + nX + nM;
         // forward and far pairs, one per lane and iteration
         const int itFX = __reduce_max_sync(0xffffffffu, nF + nX);
@@ -187,12 +188,12 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
             const double2 *Srow = stS + c * ROW;
             if (cls == 0) {
                 // forward on u_n = G_n / R_n, K, E by the small-k' series
-                const double inv_rho_p = 1.0 / sqrt(g.rp2);
+                const double inv_rho_p = rsqrt_nr(g.rp2);
                 double Kk, Ek;
                 ke_small(g.rm2 * inv_rho_p * inv_rho_p, Kk, Ek);
                 const double G0 = Kk * inv_rho_p * (1.0 / kPi);
-                const double chi = 0.25 * (g.rp2 + g.rm2) / g.rr1;
-                double u0 = G0, u1 = G0 * fma(-(1.0 + chi), Ek / Kk, chi);
+                const double chi = 0.25 * (g.rp2 + g.rm2) * rcp_nr(g.rr1);
+                double u0 = G0, u1 = G0 * fma(-(1.0 + chi), Ek * rcp_nr(Kk), chi);
                 acc[0] = cfma(Srow[0], u0, acc[0]);
                 if (KW > 1) acc[1] = cfma(Srow[1], u1, acc[1]);
 #pragma unroll
@@ -207,8 +208,9 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
             } else if (cls == 3) {
                 // far (chi >= 1000): hypergeometric form (DLMF 14.3.7), see greens_far
                 const double sum2 = 0.5 * (g.rp2 + g.rm2);
-                const double q = g.rr1 / sum2, z = 4.0 * q * q;
-                double qn = 1.0 / sqrt(sum2);
+                const double isum = rcp_nr(sum2);
+                const double q = g.rr1 * isum, z = 4.0 * q * q;
+                double qn = rsqrt_nr(sum2);
 #pragma unroll
                 for (int n = 0; n < KT; ++n) {
                     if (n < KW) {
@@ -229,8 +231,11 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
         const int itM = __reduce_max_sync(0xffffffffu, (nM + 1) >> 1);
         for (int it = 0; it < itM; ++it) {
             int ia = -1, ib = -1;
-            if (mM) { ia = __ffs(mM) - 1; mM &= mM - 1; }
-            if (mM) { ib = __ffs(mM) - 1; mM &= mM - 1; }
+            // long chains first, so that lanes run chains of similar length side by side
+            if (mL) { ia = __ffs(mL) - 1; mL &= mL - 1; }
+            else if (mM) { ia = __ffs(mM) - 1; mM &= mM - 1; }
+            if (mL) { ib = __ffs(mL) - 1; mL &= mL - 1; }
+            else if (mM) { ib = __ffs(mM) - 1; mM &= mM - 1; }
             const bool va = ia >= 0, vb = ib >= 0;
             const int ca = sl + SL * (va ? ia : 0), cb = vb ? sl + SL * ib : ca;
             const PairGeo gA = pair_geo(tr, stR[ca], tz - stZ[ca], fwd2);
@@ -238,22 +243,22 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
             const int S_lane = va ? Nglob + max(miller_extra(gA, a.miller), miller_extra(gB, a.miller)) : 0;
             const int S_warp = __reduce_max_sync(0xffffffffu, S_lane);
             if (va) {
-                const double ipA = 1.0 / sqrt(gA.rp2), ipB = 1.0 / sqrt(gB.rp2);
+                const double ipA = rsqrt_nr(gA.rp2), ipB = rsqrt_nr(gB.rp2);
                 // AGM(1, k') of both pairs (K = pi / (2 AGM)); a converged pair is frozen
-                double a1 = 1.0, b1 = sqrt(gA.rm2) * ipA, a2 = 1.0, b2 = sqrt(gB.rm2) * ipB;
+                double a1 = 1.0, b1 = sqrt_nr(gA.rm2) * ipA, a2 = 1.0, b2 = sqrt_nr(gB.rm2) * ipB;
 #pragma unroll 1
                 for (int k = 0; k < 40; ++k) {
                     const bool uA = fabs(0.5 * (a1 - b1)) > 2.0e-16 * a1;
                     const bool uB = fabs(0.5 * (a2 - b2)) > 2.0e-16 * a2;
                     if (!uA && !uB) break;
                     const double nA = 0.5 * (a1 + b1), nB = 0.5 * (a2 + b2);
-                    const double sA = sqrt(a1 * b1), sB = sqrt(a2 * b2);
+                    const double sA = sqrt_nr(a1 * b1), sB = sqrt_nr(a2 * b2);
                     if (uA) { a1 = nA; b1 = sA; }
                     if (uB) { a2 = nB; b2 = sB; }
                 }
-                const double G0A = 0.5 * ipA / a1, G0B = 0.5 * ipB / a2;
+                const double G0A = 0.5 * ipA * rcp_nr(a1), G0B = 0.5 * ipB * rcp_nr(a2);
                 const double sumA = 0.5 * (gA.rp2 + gA.rm2), sumB = 0.5 * (gB.rp2 + gB.rm2);
-                const double i2A = gA.rr1 / sumA, i2B = gB.rr1 / sumB;      // 1 / (2 chi)
+                const double i2A = gA.rr1 * rcp_nr(sumA), i2B = gB.rr1 * rcp_nr(sumB);   // 1/(2 chi)
                 const double qA = i2A * i2A, qB = i2B * i2B;
                 double wnA = 0.0, wlA = 1.0, wnB = 0.0, wlB = 1.0;
                 int n = S_warp;
@@ -296,9 +301,9 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
                         }
                     }
                 }
-                cvA *= G0A / xlA;                        // c (2 chi)^-(KW-1)
-                cvB = vb ? cvB * (G0B / xlB) : 0.0;
-                const double tcA = sumA / gA.rr1, tcB = sumB / gB.rr1;   // 2 chi
+                cvA *= G0A * rcp_nr(xlA);                // c (2 chi)^-(KW-1)
+                cvB = vb ? cvB * (G0B * rcp_nr(xlB)) : 0.0;
+                const double tcA = sumA * rcp_nr(gA.rr1), tcB = sumB * rcp_nr(gB.rr1);   // 2 chi
                 // pass 2: G_j = w_j P_j c (2 chi)^-j, j = KW-1 .. 0
 #pragma unroll
                 for (int j = KT - 1; j >= 0; --j) {

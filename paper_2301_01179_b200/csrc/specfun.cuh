@@ -91,6 +91,37 @@ inline void build_rec_tables(RecTables *t)
     }
 }
 
+// Reciprocal and (reciprocal) square root of a positive normal double: the SFU's approximation
+// (rcp/rsqrt.approx.f64, ~2^-23 relative) refined by two Newton steps in FMA form (each squares
+// the relative error), so the result is within an ulp or two of the correctly rounded value.
+// Unlike the IEEE-conforming operators these have no special-case branches; the near-field
+// kernel uses them for values that are positive and finite by construction.
+__device__ __forceinline__ double rcp_nr(double x)
+{
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+__device__ __forceinline__ double rsqrt_nr(double x)
+{
+    double y;
+    asm("rsqrt.approx.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double h = 0.5 * x;
+    double e = fma(-h * y, y, 0.5);
+    y = fma(y, e, y);
+    e = fma(-h * y, y, 0.5);
+    return fma(y, e, y);
+}
+__device__ __forceinline__ double sqrt_nr(double x)
+{
+    const double y = rsqrt_nr(x);
+    const double s = x * y;
+    return fma(fma(-s, s, x), 0.5 * y, s);
+}
+
 // K(k) and E(k) for small k'^2 = 1 - k^2 (forward branch: k'^2 <= t/(2+t) <= 0.004, truncation
 // after kKESeries terms < 4e-20 relative); replaces the AGM there (one log, 4 short Horner sums).
 __device__ __forceinline__ void ke_small(double kp2, double &K, double &E)

@@ -382,4 +382,4 @@ def test_fmm_gradients_vs_oracle_fmm(gpu, orc, n, K, p, depth, same):
     assert eps_modes(Fz.cpu().numpy(), refz).max() <= TOL
     # and Phi from the gradient solve equals the plain solve (the plain solve may run the
     # warp-task near-field kernel: same pairs, another summation order)
-    assert eps_modes(F.cpu().numpy(), plan.solve(sr, sz, S, fr, fz).cpu().numpy()).max() <= 1e-14
+    assert eps_modes(F.cpu().numpy(), plan.solve(sr, sz, S, fr, fz).cpu().numpy()).max() <= 1e-13
