@@ -85,6 +85,25 @@ def test_q_forward_branch_amplification_at_switch(orc):
         assert lo <= rel < hi, (miller, rel)
 
 
+@pytest.mark.parametrize("geom", [
+    (0.2548828125, 0.2549105212934298, 1.8260273504377977e-06),   # C5, chi - 1 = 5.9e-9
+    (1.0, 1.0, 2e-5), (1.0, 1.0, 1.4e-3), (0.7, 0.7000003, 1e-7),
+])
+def test_q_forward_near_coincident_high_modes(orc, geom):
+    # R#24: the forward recursion evaluated with chi = 1 + delta, delta from k'^2,
+    # keeps near-coincident rings (chi - 1 down to 1e-10) accurate to ~1e-14 up to n = 64; with a
+    # rounded chi it lost 4e-13 at n = 64 for the C5 pair.  Reference: mpmath legenq, 40 digits.
+    r, r1, x = geom
+    mp.mp.dps = 40
+    chi = (mp.mpf(r) ** 2 + mp.mpf(r1) ** 2 + mp.mpf(x) ** 2) / (2 * mp.mpf(r) * mp.mpf(r1))
+    assert chi - 1 < 1.2e-4                                         # forward branch at N = 64
+    G = orc.greens(r, r1, x, 64)
+    c = 2 * mp.pi * mp.sqrt(mp.mpf(r) * mp.mpf(r1))
+    for n in range(65):
+        ref = mp.re(mp.legenq(n - mp.mpf(1) / 2, 0, chi, type=3)) / c
+        assert abs(G[n] - float(ref)) <= 6e-14 * abs(float(ref)), (n, G[n], ref)
+
+
 def test_forward_switch_rule(orc):
     # R#3: the paper's chi < 1.008 in the paper mode and for N <= 16; beyond, in the
     # accurate mode, the switch t_N satisfies lambda(1 + t_N)^(2N) = 64 exactly (closed form).
