@@ -76,8 +76,9 @@ static cudaError_t allow_smem(F *kernel)
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
 }
 
-#define P2PW_INSTANCES(X) X(9, true, false) X(17, true, false) X(17, true, true) X(33, true, false) \
-    X(9, false, false) X(17, false, false) X(33, false, false)
+#define P2PW_INSTANCES(X) X(9, true, false, false) X(17, true, false, false) X(17, true, true, false) \
+    X(33, true, false, false) X(9, false, false, false) X(17, false, false, false) \
+    X(33, false, false, false) X(33, false, false, true)
 #define P2P_INSTANCES(X)                                                                       \
     X(8, 16, 2) X(8, 16, 5) X(16, 8, 3) X(16, 8, 9) X(32, 4, 6) X(32, 4, 18)
 
@@ -115,7 +116,7 @@ static cylfmm_status ensure_init()
     cudaError_t e = cudaMemcpyToSymbol(c_rec, t, sizeof(RecTables));
     delete t;
     CK(e);
-#define X(KT, E, W) CK(allow_smem(p2p_warp_kernel<KT, E, W>));
+#define X(KT, E, W, N) CK(allow_smem(p2p_warp_kernel<KT, E, W, N>));
     P2PW_INSTANCES(X)
 #undef X
 #define X(TT, SC, MT)                                                                          \
@@ -172,32 +173,39 @@ static cudaError_t launch_p2p(int TT, const P2PArgs &a, dim3 grid, cudaStream_t 
 static constexpr int kP2PWindow = 72;
 
 // warp-task near field (p2p_warp.cuh): compile-time mode bound KT >= K
+static constexpr int kP2PWWindow = 33;   // warp-task kernel: modes per pass for K > 33
 static int p2pw_kt(int K)
 {
     if (K <= 9) return 9;
     if (K <= 17) return 17;
-    if (K <= 33) return 33;
-    return 0;
+    return 33;
 }
 static bool p2pw_enabled(int K, bool grad)
 {
-    if (grad || p2pw_kt(K) == 0) return false;
+    if (grad || K > kP2PWindow * 8) return false;
     const char *e = getenv("CYLFMM_P2P_VARIANT");
     return !(e && atoi(e) == 1);
 }
+// one pass over the mode window [a.m0, a.m1) (m0 > 0 only for K > 33)
 static cudaError_t launch_p2pw(const P2PArgs &a, cudaStream_t st)
 {
     const char *e = getenv("CYLFMM_P2P_VARIANT");
-    const int kt = p2pw_kt(a.K);
+    const int KW = a.m1 - a.m0;
+    const int kt = p2pw_kt(a.m0 > 0 ? kP2PWindow : a.K);
     const bool wsm = e && atoi(e) == 2;
-    const bool exact = a.K == kt && !(e && atoi(e) == 3);
+    const bool win = a.m0 > 0;
+    const bool exact = !win && KW == kt && !(e && atoi(e) == 3);
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-#define X(KT, E, W)                                                                            \
-    if (kt == KT && exact == E && wsm == W) {                                                  \
-        p2p_warp_kernel<KT, E, W><<<nsm * p2pw_min_blocks<KT, W>(), 128,                       \
-                                    p2pw_smem_bytes<KT, W>(), st>>>(a);                        \
+    if (win) {                 // the first window's launch consumed the fetch counter
+        cudaError_t err = cudaMemsetAsync(a.task_ctr, 0, sizeof(int), st);
+        if (err != cudaSuccess) return err;
+    }
+#define X(KT, E, W, N)                                                                         \
+    if (kt == KT && exact == E && wsm == W && win == N) {                                      \
+        p2p_warp_kernel<KT, E, W, N><<<nsm * p2pw_min_blocks<KT, W>(), 128,                    \
+                                       p2pw_smem_bytes<KT, W>(), st>>>(a);                     \
         return cudaGetLastError();                                                             \
     }
     P2PW_INSTANCES(X)
@@ -1055,7 +1063,8 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         CKL();
         p->launches += 2;
         unsigned long long *ctr = p->ctr.as<unsigned long long>();
-        for (int m0 = 0; m0 < K; m0 += kP2PWindow) {
+        const int win = wk ? kP2PWWindow : kP2PWindow;
+        for (int m0 = 0; m0 < K; m0 += win) {
             P2PArgs a = {};
             a.sr = fa.sr;
             a.sz = fa.sz;
@@ -1066,7 +1075,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             a.nf = nf;
             a.K = K;
             a.m0 = m0;
-            a.m1 = std::min(K, m0 + kP2PWindow);
+            a.m1 = std::min(K, m0 + win);
             a.miller = q.miller;
             a.fwd2 = forward_coef(K - 1, q.miller);
             a.exclude = q.exclude_coincident;

@@ -56,7 +56,9 @@ __device__ __forceinline__ double2 cfma(double2 s, double g, double2 acc)
 // of the task's source list; the four partial sums are added in warp order at the end
 // (deterministic).  Persistent CTAs fetch tasks from *a.task_ctr (zeroed before the launch).
 // EXACT: the mode count equals KT (no per-mode guards).
-template <int KT, bool EXACT, bool WSM>
+// WIN: a mode window [m0, m0 + KW) with m0 > 0 (K > KT: the recursions still start at mode 0;
+// only the window's modes are accumulated).
+template <int KT, bool EXACT, bool WSM, bool WIN = false>
 __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_kernel(P2PArgs a)
 {
     constexpr int CH = kWarpCH, ROW = p2pw_row<KT>();
@@ -88,7 +90,8 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
     const int SL = 32 >> lgTW;
     const int tl = lane & (TW - 1), sl = lane >> lgTW;
     const bool tvalid = tl < nt;
-    const int KW = EXACT ? KT : a.m1 - a.m0;            // m0 = 0
+    const int KW = EXACT ? KT : a.m1 - a.m0;
+    const int M0 = WIN ? a.m0 : 0, M1 = M0 + KW;
 
     // neighbour source segments (warp 0, lane k < 9 = neighbour k), prefix by shuffles
     if (warp == 0) {
@@ -146,7 +149,7 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
             const int ds = 32 / KW, dn = 32 - ds * KW;
 #pragma unroll 4
             for (int e = lane; e < nch * KW; e += 32) {
-                stS[s * ROW + n] = a.S[(int64_t)stG[s] * a.K + n];
+                stS[s * ROW + n] = a.S[(int64_t)stG[s] * a.K + M0 + n];
                 s += ds;
                 n += dn;
                 if (n >= KW) {
@@ -192,17 +195,38 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
                 double Kk, Ek;
                 ke_small(g.rm2 * inv_rho_p * inv_rho_p, Kk, Ek);
                 const double G0 = Kk * inv_rho_p * (1.0 / kPi);
-                const double chi = 0.25 * (g.rp2 + g.rm2) * rcp_nr(g.rr1);
+                const double irr = rcp_nr(g.rr1);
+                const double chi = 0.25 * (g.rp2 + g.rm2) * irr;
+                const double dchi = 0.5 * g.rm2 * irr;    // chi - 1, exact to rounding (R#24)
                 double u0 = G0, u1 = G0 * fma(-(1.0 + chi), Ek * rcp_nr(Kk), chi);
-                acc[0] = cfma(Srow[0], u0, acc[0]);
-                if (KW > 1) acc[1] = cfma(Srow[1], u1, acc[1]);
-#pragma unroll
-                for (int n = 2; n < KT; ++n) {
-                    if (n < KW) {
-                        const double u2 = fma(chi, u1, -c_rec.eps[n] * u0);
-                        acc[n] = cfma(Srow[n], u2 * c_rec.Rn[n], acc[n]);
+                if constexpr (WIN) {                    // M0 >= 2: advance to the window
+#pragma unroll 4
+                    for (int n = 2; n < M0; ++n) {
+                        const double u2 = fma(dchi, u1, fma(-c_rec.eps[n], u0, u1));
                         u0 = u1;
                         u1 = u2;
+                    }
+#pragma unroll
+                    for (int j = 0; j < KT; ++j) {
+                        if (j < KW) {
+                            const int n = M0 + j;
+                            const double u2 = fma(dchi, u1, fma(-c_rec.eps[n], u0, u1));
+                            acc[j] = cfma(Srow[j], u2 * c_rec.Rn[n], acc[j]);
+                            u0 = u1;
+                            u1 = u2;
+                        }
+                    }
+                } else {
+                    acc[0] = cfma(Srow[0], u0, acc[0]);
+                    if (KW > 1) acc[1] = cfma(Srow[1], u1, acc[1]);
+#pragma unroll
+                    for (int n = 2; n < KT; ++n) {
+                        if (n < KW) {
+                            const double u2 = fma(dchi, u1, fma(-c_rec.eps[n], u0, u1));
+                            acc[n] = cfma(Srow[n], u2 * c_rec.Rn[n], acc[n]);
+                            u0 = u1;
+                            u1 = u2;
+                        }
                     }
                 }
             } else if (cls == 3) {
@@ -211,15 +235,19 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
                 const double isum = rcp_nr(sum2);
                 const double q = g.rr1 * isum, z = 4.0 * q * q;
                 double qn = rsqrt_nr(sum2);
+                if constexpr (WIN) {
+                    for (int n = 0; n < M0 - 1; ++n) qn *= q;   // q^(M0-1): the loop multiplies once more
+                }
 #pragma unroll
-                for (int n = 0; n < KT; ++n) {
-                    if (n < KW) {
+                for (int j = 0; j < KT; ++j) {
+                    if (j < KW) {
+                        const int n = M0 + j;
                         if (n > 0) qn *= q;
                         double t = z * c_rec.farT[n][3];
                         t = z * c_rec.farT[n][2] * (1.0 + t);
                         t = z * c_rec.farT[n][1] * (1.0 + t);
                         t = z * c_rec.farT[n][0] * (1.0 + t);
-                        acc[n] = cfma(Srow[n], c_rec.farA[n] * qn * (1.0 + t), acc[n]);
+                        acc[j] = cfma(Srow[j], c_rec.farA[n] * qn * (1.0 + t), acc[j]);
                     }
                 }
             }
@@ -262,8 +290,8 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
                 const double qA = i2A * i2A, qB = i2B * i2B;
                 double wnA = 0.0, wlA = 1.0, wnB = 0.0, wlB = 1.0;
                 int n = S_warp;
-                while (n > KW + 1) {
-                    const int nstop = max(KW + 1, n - 64);
+                while (n > M1 + 1) {
+                    const int nstop = max(M1 + 1, n - 64);
 #pragma unroll 4
                     for (; n > nstop; --n) {
                         const double d = c_rec.delta[n];
@@ -282,12 +310,38 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
                     wnB = ldexp(wnB, -ex);
                     wlB = ldexp(wlB, -ex);
                 }
-                // pass 1: w_0 of both chains (wl = w_KW, wn = w_{KW+1} here)
+                // pass 1: w_0 of both chains (wl = w_M1, wn = w_{M1+1} here)
                 double xnA = wnA, xlA = wlA, xnB = wnB, xlB = wlB;
                 double cvA = 1.0, cvB = 1.0;
+                if constexpr (WIN) {                    // steps below the window (n = M0 + 1 .. 2)
+                    for (int j = KW - 1; j >= 0; --j) {
+                        const double d = c_rec.delta[M0 + j + 2];
+                        const double wA = fma(-d * qA, xnA, xlA);
+                        const double wB = fma(-d * qB, xnB, xlB);
+                        xnA = xlA;
+                        xlA = wA;
+                        xnB = xlB;
+                        xlB = wB;
+                        cvA *= i2A;
+                        cvB *= i2B;
+                    }
+                    for (int m = M0 + 1; m >= 2; --m) {
+                        const double d = c_rec.delta[m];
+                        const double wA = fma(-d * qA, xnA, xlA);
+                        const double wB = fma(-d * qB, xnB, xlB);
+                        xnA = xlA;
+                        xlA = wA;
+                        xnB = xlB;
+                        xlB = wB;
+                        if (m > 2) {
+                            cvA *= i2A;
+                            cvB *= i2B;
+                        }
+                    }
+                }
 #pragma unroll
                 for (int j = KT - 1; j >= 0; --j) {
-                    if (j < KW) {
+                    if (!WIN && j < KW) {
                         const double d = c_rec.delta[j + 2];
                         const double wA = fma(-d * qA, xnA, xlA);
                         const double wB = fma(-d * qB, xnB, xlB);
@@ -301,14 +355,15 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
                         }
                     }
                 }
-                cvA *= G0A * rcp_nr(xlA);                // c (2 chi)^-(KW-1)
+                cvA *= G0A * rcp_nr(xlA);                // c (2 chi)^-(M1-1)
                 cvB = vb ? cvB * (G0B * rcp_nr(xlB)) : 0.0;
                 const double tcA = sumA * rcp_nr(gA.rr1), tcB = sumB * rcp_nr(gB.rr1);   // 2 chi
-                // pass 2: G_j = w_j P_j c (2 chi)^-j, j = KW-1 .. 0
+                // pass 2: G_n = w_n P_n c (2 chi)^-n, n = M0 + j, j = KW-1 .. 0
 #pragma unroll
                 for (int j = KT - 1; j >= 0; --j) {
                     if (j < KW) {
-                        const double d = c_rec.delta[j + 2];
+                        const int nn = M0 + j;
+                        const double d = c_rec.delta[nn + 2];
                         const double wA = fma(-d * qA, wnA, wlA);
                         const double wB = fma(-d * qB, wnB, wlB);
                         wnA = wlA;
@@ -316,8 +371,8 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
                         wnB = wlB;
                         wlB = wB;
                         const double2 SA = stS[ca * ROW + j], SB = stS[cb * ROW + j];
-                        acc[j] = cfma(SA, wA * c_rec.Pn[j] * cvA, acc[j]);
-                        acc[j] = cfma(SB, wB * c_rec.Pn[j] * cvB, acc[j]);
+                        acc[j] = cfma(SA, wA * c_rec.Pn[nn] * cvA, acc[j]);
+                        acc[j] = cfma(SB, wB * c_rec.Pn[nn] * cvB, acc[j]);
                         cvA *= tcA;
                         cvB *= tcB;
                     }
@@ -362,6 +417,7 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
     }   // task loop
     my_skipped = __reduce_add_sync(0xffffffffu, my_skipped);
     my_pairs = __reduce_add_sync(0xffffffffu, my_pairs);
+    if (WIN) my_skipped = my_pairs = 0;                  // counted by the first window
     if (lane == 0 && a.n_skipped && my_skipped) atomicAdd(a.n_skipped, (unsigned long long)my_skipped);
     if (lane == 0 && a.n_pairs && my_pairs) atomicAdd(a.n_pairs, (unsigned long long)my_pairs);
 }

@@ -13,7 +13,10 @@
 //    paper mode, narrowed for larger N so the forward rounding growth lambda^2N <= 2^6, R#3):
 //    forward three-term recursion
 //    (2n-1) G_n = 4(n-1) chi G_{n-1} - (2n-3) G_{n-2}, run on u_n = G_n / R_n with
-//    R_n = prod_{k<=n} 4(k-1)/(2k-1): u_n = chi u_{n-1} - eps_n u_{n-2} (one DMUL + one DFMA).
+//    R_n = prod_{k<=n} 4(k-1)/(2k-1): u_n = chi u_{n-1} - eps_n u_{n-2}, evaluated as
+//    u_{n-1} - eps_n u_{n-2} + (chi - 1) u_{n-1} with chi - 1 = rho_-^2 / (2 r r1) (two DFMA;
+//    R#24: on this branch chi - 1 < 0.008 and a rounded chi loses its low bits, which cost 7e-13
+//    of G^(64) at chi - 1 = 6e-9; this form keeps 3e-14).
 //  * chi >= 1.008: Miller's backward recursion from seeds (0, 1) at (S, S-1), run on
 //    the rescaled minimal solution y_n = Q~_n (2 chi)^n, which changes by at most a factor 2 per
 //    step (no overflow for any chi, unlike Q~_n itself, R#5), and w_n = y_n / P_n with
@@ -247,13 +250,14 @@ __device__ __forceinline__ void greens_pair(const PairGeo &g, int m0, int m1, in
         ke_small(g.rm2 * inv_rho_p * inv_rho_p, Kk, Ek);
         const double G0 = Kk * inv_rho_p * (1.0 / kPi);     // K / (pi rho_+)
         double chi = 0.5 * sum2 / g.rr1;
+        const double dchi = 0.5 * g.rm2 / g.rr1;             // chi - 1 (R#24)
         // G^(1) / G^(0) = Q_{1/2}/Q_{-1/2} = chi - (1 + chi) E/K
         double u0 = G0, u1 = G0 * fma(-(1.0 + chi), Ek / Kk, chi);
         if (m0 == 0 && m1 > 0) out[0] = u0;
         if (m0 <= 1 && m1 > 1) out[(1 - m0) * ostride] = u1;
 #pragma unroll 4
         for (int n = 2; n < m1; ++n) {
-            double u2 = fma(chi, u1, -c_rec.eps[n] * u0);
+            double u2 = fma(dchi, u1, fma(-c_rec.eps[n], u0, u1));
             if (n >= m0) out[(n - m0) * ostride] = u2 * c_rec.Rn[n];
             u0 = u1;
             u1 = u2;

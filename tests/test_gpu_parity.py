@@ -64,6 +64,19 @@ def test_greens_batch_vs_oracle(gpu, orc, K, miller):
         assert err <= tol, (q, r[q], r1[q], x[q], err)
 
 
+def test_greens_near_coincident_high_modes(gpu, orc):
+    """R#24: forward branch with chi = 1 + delta in both codes; near-coincident rings (chi - 1
+    from 1e-10 to 1e-4, C5's densest near field) agree per mode and per n to 1e-13 relative up
+    to n = 64 (the oracle is pinned to mpmath there, test_oracle_specfun)."""
+    geo = [(0.2548828125, 0.2549105212934298, 1.8260273504377977e-06), (1.0, 1.0, 2e-5),
+           (1.0, 1.0, 1.4e-3), (0.7, 0.7000003, 1e-7), (0.31, 0.3100001, 0.0)]
+    r, r1, x = (np.array(v) for v in zip(*geo))
+    G = gpu.greens_batch(r, r1, x, 65).cpu().numpy()
+    for q in range(len(r)):
+        ref = orc.greens(r[q], r1[q], x[q], 64)
+        assert (np.abs(G[q] - ref) / np.abs(ref)).max() <= 1e-13, q
+
+
 @pytest.mark.parametrize("p,K", [(4, 3), (8, 17), (12, 33), (16, 65)])
 def test_tensor_batch_vs_oracle(gpu, orc, p, K):
     # normalised station-like geometries (the FMM evaluates tensors at (i+dI+1/2, i+1/2, dJ)),
