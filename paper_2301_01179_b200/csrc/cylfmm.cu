@@ -452,6 +452,10 @@ struct cylfmm_plan_s {
     cudaStream_t aux[2] = {nullptr, nullptr};
     cudaEvent_t aev[5];
     bool aux_ok = false;
+    // host-buffer solves: the coefficient rows are copied on their own stream behind the tree
+    // build (hev: previous work on the caller's stream done, coefficients resident)
+    cudaStream_t hcp = nullptr;
+    cudaEvent_t hev[2];
 };
 
 static void free_plan_bufs(cylfmm_plan p)
@@ -492,6 +496,8 @@ extern "C" cylfmm_status cylfmm_plan_create(cylfmm_plan *plan, const cylfmm_para
     p->ev_ok = true;
     for (int i = 0; i < 2; ++i) CK(cudaStreamCreateWithFlags(&p->aux[i], cudaStreamNonBlocking));
     for (int i = 0; i < 5; ++i) CK(cudaEventCreateWithFlags(&p->aev[i], cudaEventDisableTiming));
+    CK(cudaStreamCreateWithFlags(&p->hcp, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&p->hev[i], cudaEventDisableTiming));
     p->aux_ok = true;
     {
         std::vector<int> tab;
@@ -514,6 +520,8 @@ extern "C" void cylfmm_plan_destroy(cylfmm_plan plan)
     if (plan->aux_ok) {
         for (int i = 0; i < 2; ++i) cudaStreamDestroy(plan->aux[i]);
         for (int i = 0; i < 5; ++i) cudaEventDestroy(plan->aev[i]);
+        cudaStreamDestroy(plan->hcp);
+        for (int i = 0; i < 2; ++i) cudaEventDestroy(plan->hev[i]);
     }
     delete plan;
 }
@@ -749,7 +757,8 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
                                     const double *src_S, int64_t ns, const double *fld_r,
                                     const double *fld_z, int64_t nf, double *out_Phi,
                                     cudaStream_t st, cylfmm_timings *tm,
-                                    double *out_dr = nullptr, double *out_dz = nullptr)
+                                    double *out_dr = nullptr, double *out_dz = nullptr,
+                                    cudaEvent_t s_ready = nullptr)
 {
     const bool grad = out_dr != nullptr && out_dz != nullptr;
     const cylfmm_params &q = p->prm;
@@ -820,6 +829,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     RET_IF(p->fr_s.need(8 * nf));
     RET_IF(p->fz_s.need(8 * nf));
     if (ns > 0) {
+        if (s_ready) CK(cudaStreamWaitEvent(st, s_ready, 0));   // host solve: S copied behind the sort
         gather_points_kernel<<<nblk(ns * std::max(K, 1), 256), 256, 0, st>>>(
             src_r, src_z, reinterpret_cast<const double2 *>(src_S), sperm, ns, K,
             p->sr_s.as<double>(), p->sz_s.as<double>(), p->S_s.as<double2>());
@@ -1273,7 +1283,12 @@ extern "C" cylfmm_status cylfmm_fmm_solve_host(cylfmm_plan plan, const double *s
     if (n_src > 0) {
         CK(cudaMemcpyAsync(plan->h_sr.p, src_r, 8 * n_src, cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(plan->h_sz.p, src_z, 8 * n_src, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(plan->h_S.p, src_S, 16 * (size_t)n_src * K, cudaMemcpyHostToDevice, st));
+        // the K-mode coefficient rows (the bulk of the input) on their own stream: they are
+        // first read by the gather after the Morton sort, so the copy overlaps the tree build
+        CK(cudaEventRecord(plan->hev[0], st));
+        CK(cudaStreamWaitEvent(plan->hcp, plan->hev[0], 0));
+        CK(cudaMemcpyAsync(plan->h_S.p, src_S, 16 * (size_t)n_src * K, cudaMemcpyHostToDevice, plan->hcp));
+        CK(cudaEventRecord(plan->hev[1], plan->hcp));
     }
     // fields == sources (same host arrays): copied once, one tree serves both
     const bool same = fld_r == src_r && fld_z == src_z && n_fld == n_src;
@@ -1285,7 +1300,8 @@ extern "C" cylfmm_status cylfmm_fmm_solve_host(cylfmm_plan plan, const double *s
     const double *dfz = same ? plan->h_sz.as<double>() : plan->h_fz.as<double>();
     RET_IF(fmm_solve_impl(plan, plan->h_sr.as<double>(), plan->h_sz.as<double>(),
                           plan->h_S.as<double>(), n_src, dfr, dfz, n_fld,
-                          plan->h_out.as<double>(), st, timings));
+                          plan->h_out.as<double>(), st, timings, nullptr, nullptr,
+                          n_src > 0 ? plan->hev[1] : nullptr));
     if (n_fld > 0)
         CK(cudaMemcpyAsync(out_Phi, plan->h_out.p, 16 * (size_t)n_fld * K, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));

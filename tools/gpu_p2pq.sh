@@ -1,0 +1,4 @@
+cd "${GRAFT_REPO_ROOT:-/root/repo}"; mkdir -p gpurun_out
+rm -f gpurun_out/p2pq.jsonl
+for c in C2 C3 C4 C5; do timeout 600 python tools/phase_bench.py $c --reps 4 >> gpurun_out/p2pq.jsonl 2>>gpurun_out/p2pq.err; done
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "fmm or near or greens" > gpurun_out/pytest_p.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_p.log
