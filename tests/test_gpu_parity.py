@@ -252,6 +252,22 @@ def test_fmm_small_vs_oracle_fmm(gpu, orc, n, K, p, depth, L, z0, trunc, miller)
     assert e.max() <= TOL, e
 
 
+@pytest.mark.parametrize("K", [1, 2, 9, 17, 20, 33, 34, 66])
+def test_near_field_warp_kernel_modes_and_pieces(gpu, orc, K):
+    """Warp-task near field (p2p_warp.cuh): every compile-time mode bound (9, 17, 33, exact or
+    not), mode windows for K > 33 (34: 33 + 1, 66: 33 + 33), and leaves cut into 32-target and
+    power-of-two pieces (a dense cluster: leaves of 1..~200 targets), against the oracle FMM at
+    a shallow depth (near-field dominated) with coincident pairs (fields = sources)."""
+    rng = np.random.default_rng(500 + K)
+    sr, sz, S = uniform_rings(rng, 1200, K)
+    cr, cz = 0.3 + 0.02 * rng.standard_normal(900), 0.6 + 0.02 * rng.standard_normal(900)
+    sr = np.concatenate([sr, np.clip(cr, 1e-3, 1.0)])
+    sz = np.concatenate([sz, np.clip(cz, 0.0, 1.0)])
+    S = np.concatenate([S, rng.standard_normal((900, K)) + 1j * rng.standard_normal((900, K))])
+    out, ref, _ = _fmm_case(gpu, orc, sr, sz, S, sr, sz, 4, 3, 1.0)
+    assert eps_modes(out, ref).max() <= TOL
+
+
 def test_fmm_separate_fields_ragged(gpu, orc):
     rng = np.random.default_rng(77)
     sr, sz, S = uniform_rings(rng, 2345, 7)
