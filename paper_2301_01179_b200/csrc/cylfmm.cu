@@ -76,9 +76,12 @@ static cudaError_t allow_smem(F *kernel)
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
 }
 
-#define P2PW_INSTANCES(X) X(9, true, false, false) X(17, true, false, false) X(17, true, true, false) \
-    X(33, true, false, false) X(9, false, false, false) X(17, false, false, false) \
-    X(33, false, false, false) X(33, false, false, true)
+#define P2PW_INSTANCES(X) X(9, true, false, false, false) X(17, true, false, false, false)              \
+    X(17, true, true, false, false) X(33, true, false, false, false) X(9, false, false, false, false) \
+    X(17, false, false, false, false) X(33, false, false, false, false) X(33, false, false, true, false) \
+    X(9, true, false, false, true) X(17, true, false, false, true) X(33, true, false, false, true)     \
+    X(9, false, false, false, true) X(17, false, false, false, true) X(33, false, false, false, true) \
+    X(33, false, false, true, true)
 #define P2P_INSTANCES(X)                                                                       \
     X(8, 16, 2) X(8, 16, 5) X(16, 8, 3) X(16, 8, 9) X(32, 4, 6) X(32, 4, 18)
 
@@ -116,7 +119,7 @@ static cylfmm_status ensure_init()
     cudaError_t e = cudaMemcpyToSymbol(c_rec, t, sizeof(RecTables));
     delete t;
     CK(e);
-#define X(KT, E, W, N) CK(allow_smem(p2p_warp_kernel<KT, E, W, N>));
+#define X(KT, E, W, N, DR) CK(allow_smem(p2p_warp_kernel<KT, E, W, N, DR>));
     P2PW_INSTANCES(X)
 #undef X
 #define X(TT, SC, MT)                                                                          \
@@ -186,26 +189,26 @@ static bool p2pw_enabled(int K, bool grad)
     const char *e = getenv("CYLFMM_P2P_VARIANT");
     return !(e && atoi(e) == 1);
 }
-// one pass over the mode window [a.m0, a.m1) (m0 > 0 only for K > 33)
-static cudaError_t launch_p2pw(const P2PArgs &a, cudaStream_t st)
+// one pass over the mode window [a.m0, a.m1) (m0 > 0 only for K > 33); direct: the direct sum
+static cudaError_t launch_p2pw(const P2PArgs &a, cudaStream_t st, bool direct = false)
 {
     const char *e = getenv("CYLFMM_P2P_VARIANT");
     const int KW = a.m1 - a.m0;
-    const int kt = p2pw_kt(a.m0 > 0 ? kP2PWindow : a.K);
-    const bool wsm = e && atoi(e) == 2;
+    const int kt = p2pw_kt(a.m0 > 0 ? kP2PWWindow : a.K);
+    const bool wsm = !direct && e && atoi(e) == 2;
     const bool win = a.m0 > 0;
     const bool exact = !win && KW == kt && !(e && atoi(e) == 3);
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (win) {                 // the first window's launch consumed the fetch counter
+    if (win || direct) {       // the previous launch consumed the fetch counter
         cudaError_t err = cudaMemsetAsync(a.task_ctr, 0, sizeof(int), st);
         if (err != cudaSuccess) return err;
     }
-#define X(KT, E, W, N)                                                                         \
-    if (kt == KT && exact == E && wsm == W && win == N) {                                      \
-        p2p_warp_kernel<KT, E, W, N><<<nsm * p2pw_min_blocks<KT, W>(), 128,                    \
-                                       p2pw_smem_bytes<KT, W>(), st>>>(a);                     \
+#define X(KT, E, W, N, DR)                                                                     \
+    if (kt == KT && exact == E && wsm == W && win == N && direct == DR) {                      \
+        p2p_warp_kernel<KT, E, W, N, DR><<<nsm * p2pw_min_blocks<KT, W>(), 128,                \
+                                           p2pw_smem_bytes<KT, W>(), st>>>(a);                 \
         return cudaGetLastError();                                                             \
     }
     P2PW_INSTANCES(X)
@@ -242,19 +245,24 @@ extern "C" cylfmm_status cylfmm_direct(const double *src_r, const double *src_z,
     int dev = 0, nsm = 148;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    // warp-task kernel (p2p_warp.cuh): tasks = (32-target tile, source partition of >= 128),
+    // ~12 tasks per resident CTA slot; CYLFMM_P2P_VARIANT=1 keeps the CTA-wide kernel
+    const bool wk = p2pw_enabled(K, false);
     const int TT = 32, SC = 4;
     int64_t tiles = (n_fld + TT - 1) / TT;
-    int64_t want = (int64_t)nsm * 4;
-    int nparts = (int)std::max<int64_t>(1, std::min<int64_t>((want + tiles - 1) / tiles, (n_src + 63) / 64));
+    int64_t want = (int64_t)nsm * (wk ? 12 * 3 : 4);
+    int nparts = (int)std::max<int64_t>(1, std::min<int64_t>((want + tiles - 1) / tiles,
+                                                             (n_src + (wk ? 127 : 63)) / (wk ? 128 : 64)));
     int64_t per = (n_src + nparts - 1) / nparts;
     per = (per + SC - 1) / SC * SC;
     nparts = (int)((n_src + per - 1) / per);
     int *d_err = nullptr;
     double2 *ws = nullptr;
-    CK(cudaMallocAsync((void **)&d_err, sizeof(int), st));
-    CK(cudaMemsetAsync(d_err, 0, sizeof(int), st));
+    CK(cudaMallocAsync((void **)&d_err, 2 * sizeof(int), st));
+    CK(cudaMemsetAsync(d_err, 0, 2 * sizeof(int), st));
     if (nparts > 1) CK(cudaMallocAsync((void **)&ws, sizeof(double2) * (size_t)nparts * n_fld * K, st));
-    for (int m0 = 0; m0 < K; m0 += kP2PWindow) {
+    const int win = wk ? kP2PWWindow : kP2PWindow;
+    for (int m0 = 0; m0 < K; m0 += win) {
         P2PArgs a = {};
         a.sr = src_r;
         a.sz = src_z;
@@ -265,7 +273,7 @@ extern "C" cylfmm_status cylfmm_direct(const double *src_r, const double *src_z,
         a.nf = n_fld;
         a.K = K;
         a.m0 = m0;
-        a.m1 = std::min(K, m0 + kP2PWindow);
+        a.m1 = std::min(K, m0 + win);
         a.miller = miller;
         a.fwd2 = forward_coef(K - 1, miller);
         a.exclude = exclude_coincident;
@@ -275,7 +283,9 @@ extern "C" cylfmm_status cylfmm_direct(const double *src_r, const double *src_z,
         a.part_stride = n_fld * K;
         a.src_per_part = per;
         a.err_flag = d_err;
-        CK(launch_p2p<false>(TT, a, dim3((unsigned)tiles, nparts), st));
+        a.task_ctr = d_err + 1;
+        if (wk) CK(launch_p2pw(a, st, true));
+        else CK(launch_p2p<false>(TT, a, dim3((unsigned)tiles, nparts), st));
     }
     if (nparts > 1) {
         int64_t ne = n_fld * K;

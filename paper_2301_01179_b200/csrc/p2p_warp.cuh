@@ -58,7 +58,9 @@ __device__ __forceinline__ double2 cfma(double2 s, double g, double2 acc)
 // EXACT: the mode count equals KT (no per-mode guards).
 // WIN: a mode window [m0, m0 + KW) with m0 > 0 (K > KT: the recursions still start at mode 0;
 // only the window's modes are accumulated).
-template <int KT, bool EXACT, bool WSM, bool WIN = false>
+// DIRECT: the direct sum: task = (tile of 32 targets, source partition), the
+// partition's partial sums written to out + part * part_stride (reduced in fixed order after).
+template <int KT, bool EXACT, bool WSM, bool WIN = false, bool DIRECT = false>
 __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_kernel(P2PArgs a)
 {
     constexpr int CH = kWarpCH, ROW = p2pw_row<KT>();
@@ -76,14 +78,21 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
     int *segPre = segS0 + 9;
 
     unsigned my_skipped = 0, my_pairs = 0;
-    const int ntasks = *a.ntasks;
+    const int nparts = DIRECT ? (int)((a.ns + a.src_per_part - 1) / a.src_per_part) : 1;
+    const int ntasks = DIRECT ? (int)((a.nf + 31) / 32) * nparts : *a.ntasks;
     for (;;) {                                           // persistent: fetch tasks heaviest first
     if (threadIdx.x == 0) segS0[18] = atomicAdd(a.task_ctr, 1);
     __syncthreads();
     const int task = segS0[18];
     __syncthreads();
     if (task >= ntasks) break;                           // CTA-uniform
-    const int4 tk = a.tasks[task];
+    int4 tk;
+    if (DIRECT) {
+        const int tile = task / nparts, part = task % nparts;
+        tk = make_int4(tile * 32, (int)min(a.nf, (int64_t)tile * 32 + 32), part, 0);
+    } else {
+        tk = a.tasks[task];
+    }
     const int t0 = tk.x, nt = tk.y - tk.x;
     const int TW = nt <= 1 ? 1 : 1 << (32 - __clz(nt - 1));   // next power of two >= nt
     const int lgTW = __ffs(TW) - 1;
@@ -93,8 +102,16 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
     const int KW = EXACT ? KT : a.m1 - a.m0;
     const int M0 = WIN ? a.m0 : 0, M1 = M0 + KW;
 
-    // neighbour source segments (warp 0, lane k < 9 = neighbour k), prefix by shuffles
-    if (warp == 0) {
+    // neighbour source segments (warp 0, lane k < 9 = neighbour k), prefix by shuffles; the
+    // direct sum has one segment, the partition
+    if (DIRECT && warp == 0) {
+        const int64_t s0 = (int64_t)tk.z * a.src_per_part, s1 = min(a.ns, s0 + a.src_per_part);
+        if (lane < 9) {
+            segS0[lane] = lane == 0 ? (int)s0 : 0;
+            segPre[lane] = lane == 0 ? 0 : (int)(s1 - s0);
+        }
+        if (lane == 8) segS0[18] = (int)(s1 - s0);
+    } else if (warp == 0) {
         int s0 = 0, len = 0;
         const uint32_t key = (uint32_t)tk.z;
         const int ix = (int)compact1(key), iz = (int)compact1(key >> 1), nb = 1 << a.depth;
@@ -406,7 +423,7 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
             v.y += p.y;
         }
         const int64_t row = a.out_row ? a.out_row[t0 + t] : (t0 + t);
-        double2 *o = a.out + row * a.K + a.m0 + j;
+        double2 *o = a.out + (DIRECT ? tk.z * a.part_stride : 0) + row * a.K + a.m0 + j;
         if (a.accumulate) {
             const double2 p = *o;
             v.x += p.x;
