@@ -15,7 +15,8 @@ echo "ncu1 rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"s2l_kernel|p2p_warp" -s 6 -c 2 \
    -o gpurun_out/prof $CMD > gpurun_out/ncu_full.log 2>&1
 echo "ncu2 rc=$?"
-timeout 900 python tools/diag_c5b.py > gpurun_out/diag_c5.log 2>&1
+timeout 900 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
+timeout 900 python tools/direct_speedup.py C2 C3 > gpurun_out/speedup.jsonl 2> gpurun_out/speedup.err
 for c in C2 C3 C4 C5; do
   timeout 1200 python tools/run_config.py $c --sample 96 > gpurun_out/cfg_$c.json 2> gpurun_out/cfg_$c.err; echo "$c rc=$?"
 done
