@@ -45,6 +45,22 @@ __host__ __device__ constexpr int p2pw_min_blocks()
     return KT <= 9 ? 4 : (KT <= 17 ? (WSM ? 4 : 3) : 2);
 }
 
+// asynchronous global -> shared copies (LDGSTS): a stage's loads are all in flight at once
+__device__ __forceinline__ void pw_async8(void *smem, const void *gmem)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+                 "l"(gmem));
+}
+__device__ __forceinline__ void pw_async16(void *smem, const void *gmem)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+                 "l"(gmem));
+}
+__device__ __forceinline__ void pw_async_wait()
+{
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
 __device__ __forceinline__ double2 cfma(double2 s, double g, double2 acc)
 {
     acc.x = fma(s.x, g, acc.x);
@@ -156,8 +172,8 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
             for (int kk = 1; kk < 9; ++kk) k += (v >= segPre[kk]);
             const int gi = segS0[k] + (v - segPre[k]);
             stG[lane] = gi;
-            stR[lane] = a.sr[gi];
-            stZ[lane] = a.sz[gi];
+            pw_async8(stR + lane, a.sr + gi);
+            pw_async8(stZ + lane, a.sz + gi);
         }
         __syncwarp();
         // coefficient rows: element e = s KW + n, lanes stride 32 elements
@@ -166,7 +182,7 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
             const int ds = 32 / KW, dn = 32 - ds * KW;
 #pragma unroll 4
             for (int e = lane; e < nch * KW; e += 32) {
-                stS[s * ROW + n] = a.S[(int64_t)stG[s] * a.K + M0 + n];
+                pw_async16(stS + s * ROW + n, a.S + (int64_t)stG[s] * a.K + M0 + n);
                 s += ds;
                 n += dn;
                 if (n >= KW) {
@@ -175,6 +191,7 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
                 }
             }
         }
+        pw_async_wait();
         __syncwarp();
         // classify this lane's pairs c = sl + SL i
         unsigned mF = 0, mX = 0, mM = 0, mL = 0;     // forward, far, Miller short / long
