@@ -352,7 +352,12 @@ static cylfmm_status run_fill(TensorGeomArgs ta, int64_t ngeom, cudaStream_t st)
     const int p = ta.p, D = 2 * p + 1;
     size_t sm_fill = sizeof(double) * (size_t)(p + 1) * (p + 1) * D;
     int KW = ta.m1 - ta.m0;
-    tensor_fill_kernel<<<(unsigned)(ngeom * KW), 256, sm_fill, st>>>(ta);
+    // threads per (station, mode): the widest radial step has (p + 1)(2p + 1) entries (153 at
+    // p = 8); narrower CTAs let more of them overlap their barrier-bound steps
+    // (CYLFMM_FILL_THREADS overrides, for measurement)
+    static const int fth = getenv("CYLFMM_FILL_THREADS") ? atoi(getenv("CYLFMM_FILL_THREADS")) : 0;
+    const int nth = fth > 0 ? fth : (p <= 8 ? 64 : (p <= 12 ? 128 : 256));
+    tensor_fill_kernel<<<(unsigned)(ngeom * KW), nth, sm_fill, st>>>(ta);
     CKL();
     return CYLFMM_OK;
 }
