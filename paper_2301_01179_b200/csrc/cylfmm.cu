@@ -343,7 +343,9 @@ extern "C" cylfmm_status cylfmm_greens_batch(const double *r, const double *r1, 
 static cylfmm_status run_seeds(TensorGeomArgs ta, int64_t ngeom, cudaStream_t st)
 {
     size_t sm_seed = tensor_seed_smem(ta.K, ta.m1, ta.p);
-    tensor_seed_kernel<<<(unsigned)ngeom, 128, sm_seed, st>>>(ta);
+    // >= 64 threads: lanes over the 2p + 1 <= 33 series coefficients plus the two table threads
+    static const int sth = getenv("CYLFMM_SEED_THREADS") ? atoi(getenv("CYLFMM_SEED_THREADS")) : 64;
+    tensor_seed_kernel<<<(unsigned)ngeom, sth >= 64 ? sth : 64, sm_seed, st>>>(ta);
     CKL();
     return CYLFMM_OK;
 }
@@ -1159,7 +1161,8 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             for (int l = d - 1; l >= 2; --l) {
                 if (fa.scount[l] == 0) continue;
                 unsigned g = (unsigned)((int64_t)fa.scount[l] * ((kw + kMMG - 1) / kMMG));
-                m2m_kernel<<<g, 256, m2m_smem(pp), st>>>(fa, l);
+                static const int mth = getenv("CYLFMM_M2M_THREADS") ? atoi(getenv("CYLFMM_M2M_THREADS")) : 256;
+                m2m_kernel<<<g, mth, m2m_smem(pp), st>>>(fa, l);
                 CKL();
                 p->launches++;
             }
