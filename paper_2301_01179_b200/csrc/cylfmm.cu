@@ -1197,8 +1197,16 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         {
             int ngrp = (kw + kL2PModes - 1) / kL2PModes;
             size_t sm = sizeof(double2) * kL2PModes * Pl + sizeof(double) * kL2PPts * Pl * (grad ? 3 : 1);
-            if (grad) l2p_kernel<true><<<(unsigned)((int64_t)fa.tcount[d] * ngrp), 256, sm, st>>>(fa);
-            else l2p_kernel<false><<<(unsigned)((int64_t)fa.tcount[d] * ngrp), 256, sm, st>>>(fa);
+            // leaves per CTA: one when the leaves hold >= kL2PPts points on average (C2-C4), up to
+            // 64 when they are many and small (C5: 1M leaves of 4 points), so that a CTA reuses the
+            // evaluating box's local over a run of leaves
+            const int ntl = fa.tcount[d];
+            fa.l2p_lc = nf >= (int64_t)kL2PPts * ntl
+                            ? 1
+                            : (int)std::min<int64_t>(64, std::max<int64_t>(1, ntl / ((int64_t)p->nsm * 8)));
+            const int64_t nch = (ntl + fa.l2p_lc - 1) / fa.l2p_lc;
+            if (grad) l2p_kernel<true><<<(unsigned)(nch * ngrp), 256, sm, st>>>(fa);
+            else l2p_kernel<false><<<(unsigned)(nch * ngrp), 256, sm, st>>>(fa);
             CKL();
             p->launches++;
         }

@@ -49,6 +49,7 @@ struct FarArgs {
     int64_t lvoff[kMaxLevels];          // dense per-level offsets (level maps, s2l_written)
     const unsigned char *need;          // dense per level: local materialised (see need_kernel)
     int l2p_accumulate;                 // L2P adds onto out (the near field wrote it first)
+    int l2p_lc;                         // L2P: consecutive target leaves per CTA (>= 1)
     double2 *outr, *outz;               // gradient rows (nullable): dPhi/dr, dPhi/dz
 };
 
@@ -363,26 +364,45 @@ __global__ void __launch_bounds__(256) l2p_kernel(FarArgs a)
     extern __shared__ double sm[];
     const int p = a.pl, P = a.Pl, KW = a.m1 - a.m0, d = a.depth;   // local order
     const int ngrp = (KW + kL2PModes - 1) / kL2PModes;
-    const int slot = blockIdx.x / ngrp, g = blockIdx.x % ngrp;
+    const int chunk = blockIdx.x / ngrp, g = blockIdx.x % ngrp;
     const int n0 = g * kL2PModes, nm = min(kL2PModes, KW - n0);
     double2 *loc = reinterpret_cast<double2 *>(sm);     // [nm][P]
     double *mono = reinterpret_cast<double *>(loc + kL2PModes * P);  // [pts][P]
     double *monr = mono + kL2PPts * P, *monz = monr + kL2PPts * P;   // GRAD: derivative monomials
-    const uint32_t key = (uint32_t)a.tkeys[d][slot];
-    const int t0 = a.flstart[key], t1 = a.flstart[key + 1];
+    // a CTA takes l2p_lc consecutive target leaves (Morton order, so their field points are one
+    // contiguous sorted range) and walks them in runs that share the evaluating box: the local is
+    // loaded once per run (C5: leaves of 4 points under coarse boxes)
+    const int nleaf = a.tcount[d];
+    const int l0 = chunk * a.l2p_lc, l1 = min(nleaf, l0 + a.l2p_lc);
     // the deepest ancestor (or the leaf) that received an S2L contribution: below it the chain
     // adds nothing, so the leaf's local is that box's local re-centred (exact) and is
     // evaluated directly.  Written boxes are always materialised (need_kernel), and the choice
     // depends only on the leaf's own chain, so results do not depend on the other field points
     // (a field-partitioned multi-GPU solve is bitwise identical to the 1-GPU one).  None: zero.
-    int la = d;
-    uint32_t ka = key;
-    while (la >= 2 && !a.s2l_written[a.lvoff[la] + ka]) {
-        --la;
-        ka >>= 2;
+    auto owner = [&](int leaf, int &la, uint32_t &ka) {
+        la = d;
+        ka = (uint32_t)a.tkeys[d][leaf];
+        while (la >= 2 && !a.s2l_written[a.lvoff[la] + ka]) {
+            --la;
+            ka >>= 2;
+        }
+        if (la < 2) la = -1;                            // nothing written: zero local
+    };
+    for (int li = l0; li < l1;) {
+    int la;
+    uint32_t ka;
+    owner(li, la, ka);
+    int lj = li + 1;
+    for (; lj < l1; ++lj) {
+        int lb;
+        uint32_t kb;
+        owner(lj, lb, kb);
+        if (lb != la || (la >= 2 && kb != ka)) break;
     }
+    const uint32_t key = (uint32_t)a.tkeys[d][li], keyl = (uint32_t)a.tkeys[d][lj - 1];
+    const int t0 = a.flstart[key], t1 = a.flstart[keyl + 1];
     const bool ok = la >= 2;
-    if (la < 2) {
+    if (!ok) {
         la = 2;
         ka = key >> (2 * (d - 2));
     }
@@ -390,6 +410,7 @@ __global__ void __launch_bounds__(256) l2p_kernel(FarArgs a)
     box_centre(ka, la, a.L, a.z0, rc, zc, h);
     const double inv_h = 1.0 / h;
     const int64_t aslot = ok ? a.tmap[la][ka] : 0;
+    __syncthreads();                                    // the previous run is done with loc
     for (int e = threadIdx.x; e < nm * P; e += blockDim.x)
         loc[e] = ok ? a.Lc[((a.toff[la] + aslot) * (int64_t)KW + n0) * P + e] : make_double2(0.0, 0.0);
     for (int c0 = t0; c0 < t1; c0 += kL2PPts) {
@@ -455,6 +476,8 @@ __global__ void __launch_bounds__(256) l2p_kernel(FarArgs a)
             }
         }
     }
+    li = lj;
+    }   // runs
 }
 
 // ---------------------------------------------------------------------------------------------
