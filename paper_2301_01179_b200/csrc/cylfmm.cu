@@ -667,9 +667,13 @@ static int64_t pow4(int l) { return (int64_t)1 << (2 * l); }
 // S2L tiles of every level 2..depth: (column it, row tile jt of JH boxes per parity)
 static S2LGrid make_s2l_grid(int depth, int JH)
 {
+    // deepest level first: its tiles carry the most boxes (the longest CTAs), so they start in
+    // the first wave and the short coarse-level CTAs fill the tail
     S2LGrid gr = {};
     int64_t tot = 0;
-    for (int l = 2; l <= depth; ++l) {
+    static const bool asc = getenv("CYLFMM_S2L_ASC") && atoi(getenv("CYLFMM_S2L_ASC")) == 1;
+    for (int li = 2; li <= depth; ++li) {
+        const int l = asc ? li : depth + 2 - li;
         int nb = 1 << l, half = std::max(nb / 2, 1);
         int jtiles = (half + JH - 1) / JH;
         gr.level[gr.nlev] = l;
