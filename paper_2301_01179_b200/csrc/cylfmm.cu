@@ -458,6 +458,8 @@ struct cylfmm_plan_s {
     DevBuf need;                          // lazy L2L flags
     DevBuf err, ctr;
     DevBuf s2lidx;   // S2L operator gather table for this plan's (p, truncation)
+    DevBuf rtab;     // M2M / L2L recentring tables: [rtab(p) | rtab(pl)] doubles, then tri ints
+    size_t rtab_nm = 0, rtab_nd = 0, rtab_ntm = 0;
     // host-API staging
     DevBuf h_sr, h_sz, h_S, h_fr, h_fz, h_out;
     cudaEvent_t ev[16];
@@ -482,7 +484,7 @@ static void free_plan_bufs(cylfmm_plan p)
                      &p->scan_tmp[3], &p->sr_s, &p->sz_s, &p->S_s, &p->fr_s, &p->fz_s,
                      &p->slstart, &p->flstart, &p->flags, &p->smap, &p->skeys, &p->tmap,
                      &p->tkeys, &p->counts, &p->M, &p->Lc, &p->tens, &p->seeds, &p->tasks,
-                     &p->ntasks, &p->tcnt, &p->toff, &p->tflag, &p->tpos, &p->tiles, &p->written, &p->need, &p->err, &p->ctr, &p->s2lidx, &p->h_sr, &p->h_sz,
+                     &p->ntasks, &p->tcnt, &p->toff, &p->tflag, &p->tpos, &p->tiles, &p->written, &p->need, &p->err, &p->ctr, &p->s2lidx, &p->rtab, &p->h_sr, &p->h_sz,
                      &p->h_S, &p->h_fr, &p->h_fz, &p->h_out};
     for (DevBuf *b : all) b->release();
 }
@@ -522,6 +524,22 @@ extern "C" cylfmm_status cylfmm_plan_create(cylfmm_plan *plan, const cylfmm_para
         build_s2l_index(q.order, pl, s2l_mp(pl), q.truncation, tab);
         RET_IF(p->s2lidx.need(sizeof(int) * tab.size()));
         CK(cudaMemcpy(p->s2lidx.p, tab.data(), sizeof(int) * tab.size(), cudaMemcpyHostToDevice));
+        // recentring tables for the source order (M2M) and the local order (L2L), once per plan
+        std::vector<double> rm, rl;
+        std::vector<int> tm_, tl_;
+        recentre_tables_host(q.order, rm, tm_);
+        recentre_tables_host(pl, rl, tl_);
+        const size_t nd = rm.size() + rl.size(), ni = tm_.size() + tl_.size();
+        RET_IF(p->rtab.need(sizeof(double) * nd + sizeof(int) * ni));
+        std::vector<char> blob(sizeof(double) * nd + sizeof(int) * ni);
+        memcpy(blob.data(), rm.data(), sizeof(double) * rm.size());
+        memcpy(blob.data() + sizeof(double) * rm.size(), rl.data(), sizeof(double) * rl.size());
+        memcpy(blob.data() + sizeof(double) * nd, tm_.data(), sizeof(int) * tm_.size());
+        memcpy(blob.data() + sizeof(double) * nd + sizeof(int) * tm_.size(), tl_.data(), sizeof(int) * tl_.size());
+        CK(cudaMemcpy(p->rtab.p, blob.data(), blob.size(), cudaMemcpyHostToDevice));
+        p->rtab_nm = rm.size();
+        p->rtab_nd = nd;
+        p->rtab_ntm = tm_.size();
     }
     *plan = p;
     return CYLFMM_OK;
@@ -1029,6 +1047,10 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     fa.out = reinterpret_cast<double2 *>(out_Phi);
     fa.s2l_pairs = p->ctr.as<unsigned long long>() + 2;
     fa.s2l_idx = p->s2lidx.as<int>();
+    fa.rtab_m = p->rtab.as<double>();
+    fa.rtab_l = p->rtab.as<double>() + p->rtab_nm;
+    fa.tritab_m = reinterpret_cast<const int *>(p->rtab.as<double>() + p->rtab_nd);
+    fa.tritab_l = fa.tritab_m + p->rtab_ntm;
     fa.s2l_tiles = p->tiles.as<int>();
     fa.s2l_written = p->written.as<unsigned char>();
     for (int l = 2; l <= d; ++l) fa.lvoff[l] = lvoff[l];

@@ -17,6 +17,7 @@
 #include "tensor.cuh"
 #include "p2p.cuh"
 
+#include <cmath>
 #include <vector>
 
 namespace cyl {
@@ -50,6 +51,10 @@ struct FarArgs {
     const unsigned char *need;          // dense per level: local materialised (see need_kernel)
     int l2p_accumulate;                 // L2P adds onto out (the near field wrote it first)
     int l2p_lc;                         // L2P: consecutive target leaves per CTA (>= 1)
+    // recentring tables (host-built once per plan, recentre_tables_host): [cm | cl] 4 (p+1)^2
+    // doubles and [tri_i | tri_j] 2 P ints, for the source order (M2M) and the local order (L2L)
+    const double *rtab_m, *rtab_l;
+    const int *tritab_m, *tritab_l;
     double2 *outr, *outz;               // gradient rows (nullable): dPhi/dr, dPhi/dz
 };
 
@@ -170,11 +175,14 @@ __device__ __forceinline__ double binom_d(int n, int k)
 // CTA per (box, group of kMMG modes); coefficient tables built in smem.
 constexpr int kMMG = 4;
 
-__device__ inline void recentre_tables(int p, double *cm, double *cl, int tid, int nth)
+// Recentring tables, built once per plan on the host (exact binomials times powers of two):
+//   cm[s][i][q] = C(i,q) s^q 2^-(i+q);  cl[s][i][q] = C(i+q,q) s^q 2^-(i+2q)   (s = -1, +1)
+// out = [cm | cl] (4 (p+1)^2), tri = [tri_i | tri_j] (2 P).
+inline void recentre_tables_host(int p, std::vector<double> &out, std::vector<int> &tri)
 {
-    // cm[s][i][q] = C(i,q) s^q 2^-(i+q);  cl[s][i][q] = C(i+q,q) s^q 2^-(i+2q)   (s = -1, +1)
-    const int P1 = p + 1;
-    for (int e = tid; e < 2 * P1 * P1; e += nth) {
+    const int P1 = p + 1, P = (p + 1) * (p + 2) / 2;
+    out.assign((size_t)4 * P1 * P1, 0.0);
+    for (int e = 0; e < 2 * P1 * P1; ++e) {
         int sgn = e / (P1 * P1), i = (e / P1) % P1, q = e % P1;
         double s = sgn ? 1.0 : -1.0;
         double bm = 0.0, bl = 0.0;
@@ -189,10 +197,27 @@ __device__ inline void recentre_tables(int p, double *cm, double *cl, int tid, i
             bl = c;
         }
         double sq = (q & 1) ? s : 1.0;
-        cm[e] = bm * sq * ldexp(1.0, -(i + q));
-        cl[e] = bl * sq * ldexp(1.0, -(i + 2 * q));
+        out[e] = bm * sq * std::ldexp(1.0, -(i + q));
+        out[2 * P1 * P1 + e] = bl * sq * std::ldexp(1.0, -(i + 2 * q));
+    }
+    tri.assign((size_t)2 * P, 0);
+    for (int i = 0, q = 0; i <= p; ++i)
+        for (int j = 0; i + j <= p; ++j, ++q) {
+            tri[q] = i;
+            tri[P + q] = j;
+        }
+}
+__device__ __forceinline__ void load_recentre_tables(int p, const double *rtab, const int *tritab,
+                                                     double *cm, int *tri_i, int *tri_j)
+{
+    const int P1 = p + 1, P = (p + 1) * (p + 2) / 2;
+    for (int e = threadIdx.x; e < 4 * P1 * P1; e += blockDim.x) cm[e] = __ldg(rtab + e);   // cm, cl
+    for (int q = threadIdx.x; q < P; q += blockDim.x) {
+        tri_i[q] = __ldg(tritab + q);
+        tri_j[q] = __ldg(tritab + P + q);
     }
 }
+
 
 __global__ void __launch_bounds__(256) m2m_kernel(FarArgs a, int level)
 {
@@ -210,13 +235,7 @@ __global__ void __launch_bounds__(256) m2m_kernel(FarArgs a, int level)
     int cs[4];
 #pragma unroll
     for (int c = 0; c < 4; ++c) cs[c] = a.smap[level + 1][4 * key + c];
-    recentre_tables(p, cm, cl, threadIdx.x, blockDim.x);
-    for (int q = threadIdx.x; q < P; q += blockDim.x) {
-        int i = 0;
-        while (i < p && q >= (i + 1) * (p + 1) - (i + 1) * i / 2) ++i;
-        tri_i[q] = i;
-        tri_j[q] = q - (i * (p + 1) - i * (i - 1) / 2);
-    }
+    load_recentre_tables(p, a.rtab_m, a.tritab_m, cm, tri_i, tri_j);   // cl = cm + 2 (p+1)^2
     for (int e = threadIdx.x; e < 4 * nm * P; e += blockDim.x) {
         int c = e / (nm * P), r = e % (nm * P);
         ch[e] = cs[c] >= 0 ? a.M[((a.soff[level + 1] + cs[c]) * (int64_t)KW + n0) * P + r]
@@ -288,13 +307,7 @@ __global__ void __launch_bounds__(32 * kL2LWarps) l2l_kernel(FarArgs a, int leve
     double2 *wbuf = reinterpret_cast<double2 *>(tri_j + P + 2 * (P & 1));   // 16-B aligned
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double2 *par = wbuf + warp * 2 * P, *T = par + P;
-    recentre_tables(p, cm, cl, threadIdx.x, blockDim.x);
-    for (int q = threadIdx.x; q < P; q += blockDim.x) {
-        int i = 0;
-        while (i < p && q >= (i + 1) * (p + 1) - (i + 1) * i / 2) ++i;
-        tri_i[q] = i;
-        tri_j[q] = q - (i * (p + 1) - i * (i - 1) / 2);
-    }
+    load_recentre_tables(p, a.rtab_l, a.tritab_l, cm, tri_i, tri_j);   // local order
     __syncthreads();
     const int64_t items = (int64_t)a.tcount[level] * KW;
     for (int64_t it = (int64_t)blockIdx.x * kL2LWarps + warp; it < items;
