@@ -529,6 +529,14 @@ extern "C" cylfmm_status cylfmm_plan_create(cylfmm_plan *plan, const cylfmm_para
         std::vector<int> tm_, tl_;
         recentre_tables_host(q.order, rm, tm_);
         recentre_tables_host(pl, rl, tl_);
+        // S2L moment prescale (-1)^j / j! per source coefficient (i, j) (fmm_ops.cuh)
+        const int Pm = (q.order + 1) * (q.order + 2) / 2;
+        for (int qq = 0; qq < Pm; ++qq) {
+            const int j = tm_[Pm + qq];
+            double f = 1.0;
+            for (int t = 2; t <= j; ++t) f *= t;
+            rl.push_back(((j & 1) ? -1.0 : 1.0) / f);
+        }
         const size_t nd = rm.size() + rl.size(), ni = tm_.size() + tl_.size();
         RET_IF(p->rtab.need(sizeof(double) * nd + sizeof(int) * ni));
         std::vector<char> blob(sizeof(double) * nd + sizeof(int) * ni);
@@ -1051,6 +1059,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     fa.rtab_l = p->rtab.as<double>() + p->rtab_nm;
     fa.tritab_m = reinterpret_cast<const int *>(p->rtab.as<double>() + p->rtab_nd);
     fa.tritab_l = fa.tritab_m + p->rtab_ntm;
+    fa.pscale = p->rtab.as<double>() + p->rtab_nd - (pp + 1) * (pp + 2) / 2;
     fa.s2l_tiles = p->tiles.as<int>();
     fa.s2l_written = p->written.as<unsigned char>();
     for (int l = 2; l <= d; ++l) fa.lvoff[l] = lvoff[l];
@@ -1193,7 +1202,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
                 p->launches++;
             }
             // S2L consumes the moments pre-scaled by (-1)^j / j! (fmm_ops.cuh)
-            prescale_moments_kernel<<<nblk(stot * kw * P, 256), 256, 0, st>>>(fa.M, stot * kw, pp, P);
+            prescale_moments_kernel<<<nblk(stot * kw * P, 256), 256, 0, st>>>(fa.M, stot * kw, P, fa.pscale);
             CKL();
             p->launches++;
             toc(ms_m2m);

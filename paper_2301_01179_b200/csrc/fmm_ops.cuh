@@ -55,6 +55,7 @@ struct FarArgs {
     // doubles and [tri_i | tri_j] 2 P ints, for the source order (M2M) and the local order (L2L)
     const double *rtab_m, *rtab_l;
     const int *tritab_m, *tritab_l;
+    const double *pscale;               // [P] (-1)^j / j! per source coefficient (S2L prescale)
     double2 *outr, *outz;               // gradient rows (nullable): dPhi/dr, dPhi/dz
 };
 
@@ -551,7 +552,9 @@ __global__ void s2l_tile_flags_kernel(TileArgs ta, S2LGrid gr, int JH, int *acti
     const int di0 = (it & 1) ? -3 : -2;
     const int *tmap = ta.tmap[level], *smap = ta.smap[level];
     bool any = false;
-    for (int q = lane; q < 42 * JT && !any; q += 32) {
+    // no early exit: the unrolled loop keeps several map lookups in flight per lane
+#pragma unroll 6
+    for (int q = lane; q < 42 * JT; q += 32) {
         const int o = q / JT, b = q % JT;
         const int di = di0 + o / 7, dj = o % 7 - 3;
         if (di >= -1 && di <= 1 && dj >= -1 && dj <= 1) continue;
@@ -1064,17 +1067,11 @@ inline void build_s2l_index(int p, int pl, int MP, int truncation, std::vector<i
 }
 
 // Source moments pre-scaled once for S2L: M'_ij = (-1)^j M^_ij / j! (all levels, after M2M).
-__global__ void prescale_moments_kernel(double2 *M, int64_t nrows, int p, int P)
+__global__ void prescale_moments_kernel(double2 *M, int64_t nrows, int P, const double *pscale)
 {
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= nrows * P) return;
-    int q = (int)(e % P);
-    int i = 0;
-    while (i < p && q >= (i + 1) * (p + 1) - (i + 1) * i / 2) ++i;
-    int j = q - (i * (p + 1) - i * (i - 1) / 2);
-    double f = 1.0;
-    for (int t = 2; t <= j; ++t) f *= t;
-    f = ((j & 1) ? -1.0 : 1.0) / f;
+    const double f = __ldg(pscale + (int)(e % P));   // (-1)^j / j! of coefficient (i, j)
     double2 v = M[e];
     M[e] = make_double2(v.x * f, v.y * f);
 }
