@@ -623,7 +623,8 @@ static cylfmm_status scan_excl(cylfmm_plan p, int *d, int64_t n, cudaStream_t st
 static cylfmm_status radix_sort(cylfmm_plan p, DevBuf &k1, DevBuf &v1, DevBuf &k2, DevBuf &v2,
                                 int64_t n, int bits, cudaStream_t st, uint32_t **ko, int **vo)
 {
-    int ntiles = (int)((n + kSortTile - 1) / kSortTile);
+    const int items = sort_items(n), tile = kSortThreads * items;
+    int ntiles = (int)((n + tile - 1) / tile);
     if (n <= 0) {
         *ko = k1.as<uint32_t>();
         *vo = v1.as<int>();
@@ -633,11 +634,11 @@ static cylfmm_status radix_sort(cylfmm_plan p, DevBuf &k1, DevBuf &v1, DevBuf &k
     uint32_t *ka = k1.as<uint32_t>(), *kb = k2.as<uint32_t>();
     int *va = v1.as<int>(), *vb = v2.as<int>();
     for (int sh = 0; sh < bits; sh += 8) {
-        radix_hist_kernel<<<ntiles, kSortThreads, 0, st>>>(ka, n, sh, ntiles, p->hist.as<int>());
+        radix_hist_kernel<<<ntiles, kSortThreads, 0, st>>>(ka, n, sh, ntiles, p->hist.as<int>(), items);
         CKL();
         RET_IF(scan_excl(p, p->hist.as<int>(), 256LL * ntiles, st));
         radix_scatter_kernel<<<ntiles, kSortThreads, 0, st>>>(ka, va, n, sh, ntiles,
-                                                              p->hist.as<int>(), kb, vb);
+                                                              p->hist.as<int>(), kb, vb, items);
         CKL();
         p->launches += 2;
         std::swap(ka, kb);

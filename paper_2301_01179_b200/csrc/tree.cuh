@@ -36,18 +36,21 @@ __global__ void keys_kernel(const double *r, const double *z, int64_t n, int dep
 }
 
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 8;
+constexpr int kSortItems = 8;                         // keys per thread for large inputs
 constexpr int kSortTile = kSortThreads * kSortItems;  // 2048
+// keys per thread: 4 for small inputs (16k keys: 16 CTAs of 4 serial rounds instead of 8 of 8;
+// measured on the C2 step: 1 and 2 keys per thread are slower, the histogram scan grows), else 8
+inline int sort_items(int64_t n) { return n <= 65536 ? 4 : kSortItems; }
 
 __global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(const uint32_t *key, int64_t n,
                                                                   int shift, int ntiles,
-                                                                  int *hist)
+                                                                  int *hist, int items)
 {
     __shared__ int cnt[256];
     cnt[threadIdx.x] = 0;
     __syncthreads();
-    int64_t base = (int64_t)blockIdx.x * kSortTile;
-    for (int k = 0; k < kSortItems; ++k) {
+    int64_t base = (int64_t)blockIdx.x * kSortThreads * items;
+    for (int k = 0; k < items; ++k) {
         int64_t i = base + k * kSortThreads + threadIdx.x;
         if (i < n) atomicAdd(&cnt[(key[i] >> shift) & 255u], 1);
     }
@@ -57,7 +60,7 @@ __global__ void __launch_bounds__(kSortThreads) radix_hist_kernel(const uint32_t
 
 __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
     const uint32_t *key_in, const int *val_in, int64_t n, int shift, int ntiles,
-    const int *offsets, uint32_t *key_out, int *val_out)
+    const int *offsets, uint32_t *key_out, int *val_out, int items)
 {
     __shared__ int wcount[kSortThreads / 32][257];
     __shared__ int running[256];
@@ -65,8 +68,8 @@ __global__ void __launch_bounds__(kSortThreads) radix_scatter_kernel(
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     running[tid] = 0;
     base[tid] = offsets[(int64_t)tid * ntiles + blockIdx.x];
-    const int64_t tbase = (int64_t)blockIdx.x * kSortTile;
-    for (int rnd = 0; rnd < kSortItems; ++rnd) {
+    const int64_t tbase = (int64_t)blockIdx.x * kSortThreads * items;
+    for (int rnd = 0; rnd < items; ++rnd) {
         for (int e = tid; e < (kSortThreads / 32) * 257; e += kSortThreads) (&wcount[0][0])[e] = 0;
         __syncthreads();
         int64_t i = tbase + rnd * kSortThreads + tid;
