@@ -80,6 +80,13 @@ constexpr int kP2MSrc = 32;
 constexpr int kP2MModes = 16;
 constexpr int kP2MRC = 5;
 
+// 16-byte asynchronous global -> shared copy (zero fill when !valid)
+__device__ __forceinline__ void p2m_async16(void *smem, const void *gmem, bool valid)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+                 "l"(gmem), "r"(valid ? 16 : 0));
+}
+
 __global__ void __launch_bounds__(kP2MThreads) p2m_kernel(FarArgs a)
 {
     extern __shared__ double sm[];
@@ -118,10 +125,13 @@ __global__ void __launch_bounds__(kP2MThreads) p2m_kernel(FarArgs a)
                 pr *= dr;
             }
         }
+        // coefficient rows by asynchronous copies (in flight while the monomials are formed)
         for (int e = threadIdx.x; e < nc * kP2MModes; e += kP2MThreads) {
             const int q = e / kP2MModes, n = e % kP2MModes;
-            Sx[e] = n < nm ? a.S[(int64_t)(s0 + q) * a.K + a.m0 + n0 + n] : make_double2(0.0, 0.0);
+            const bool v = n < nm;
+            p2m_async16(Sx + e, v ? a.S + (int64_t)(s0 + q) * a.K + a.m0 + n0 + n : a.S, v);
         }
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
         __syncthreads();
         if (active) {
             for (int q = 0; q < nc; ++q) {
