@@ -1083,9 +1083,15 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     // lazy downward pass: which target locals are materialised (need_kernel, bottom-up)
     RET_IF(p->need.need(std::max<int64_t>(ltot, 1)));
     fa.need = p->need.as<unsigned char>();
+    // tree done: the near field and the need flags start behind it on their own streams (the
+    // need flags on the tensor stream: S2L waits for that stream, L2L runs after S2L)
+    if (overlap) {
+        CK(cudaEventRecord(p->aev[1], st));
+        CK(cudaStreamWaitEvent(st_t, p->aev[1], 0));
+    }
     for (int l = d; l >= 2; --l) {
         if (fa.tcount[l] == 0) continue;
-        need_kernel<<<nblk(fa.tcount[l], 256), 256, 0, st>>>(fa, l, p->need.as<unsigned char>());
+        need_kernel<<<nblk(fa.tcount[l], 256), 256, 0, st_t>>>(fa, l, p->need.as<unsigned char>());
         CKL();
         p->launches++;
     }
@@ -1093,10 +1099,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     tic();
     double ms_p2p = 0;
     if (ns > 0) {
-        if (overlap) {
-            CK(cudaEventRecord(p->aev[1], st));
-            CK(cudaStreamWaitEvent(st_n, p->aev[1], 0));
-        }
+        if (overlap) CK(cudaStreamWaitEvent(st_n, p->aev[1], 0));
         const int ntl = fa.tcount[d];
         double avg = (double)nf / std::max(ntl, 1);
         const int TT = avg <= 10.0 ? 8 : (avg <= 24.0 ? 16 : 32);
