@@ -837,10 +837,13 @@ __global__ void __launch_bounds__(NT, (RM * RN >= 40 ? 256 : 512) / NT) s2l_kern
     }
     if (!__syncthreads_or(anyt)) return;
     // the 33 offsets in a fixed order, then the source slots of every (offset, box) in one pass
+    // (dj = 0, -1, +1, -2, +2, -3, +3 per column: the forward / backward partners of a column
+    // are adjacent, so the backward one can reuse the gathered operator, see below)
     if (tid == 0) {
         int k = 0;
         for (int di = di0; di <= di0 + 5; ++di)
-            for (int dj = -3; dj <= 3; ++dj) {
+            for (int t = 0; t < 7; ++t) {
+                const int dj = (t & 1) ? -((t + 1) >> 1) : (t >> 1);
                 if (di >= -1 && di <= 1 && dj >= -1 && dj <= 1) continue;
                 olist[k++] = ((di + 3) << 4) | (dj + 3);
             }
@@ -926,6 +929,31 @@ __global__ void __launch_bounds__(NT, (RM * RN >= 40 ? 256 : 512) / NT) s2l_kern
         wbox = __reduce_or_sync(0xffffffffu, mine);
     }
 
+    // reuse masks: moment coefficients kk with odd j; this thread's accumulator rows with odd l
+    unsigned long long oddj = 0;
+    unsigned oddl = 0;
+    if (PF == 3 && ST == 1 && P <= KC) {
+        for (int i = 0, q = 0; i <= p; ++i)
+            for (int j = 0; i + j <= p; ++j, ++q)
+                if (j & 1) oddj |= 1ull << q;
+#pragma unroll
+        for (int r = 0; r < RM; ++r) {
+            const int m = 2 * (tm + TM * (r >> 1)) + (r & 1);
+            if (m < Pl) {
+                int kq = 0;
+                while (kq < pl && m >= (kq + 1) * (pl + 1) - (kq + 1) * kq / 2) ++kq;
+                if ((m - (kq * (pl + 1) - kq * (kq - 1) / 2)) & 1) oddl |= 1u << r;
+            }
+        }
+    }
+    auto negate_oddl = [&]() {
+#pragma unroll
+        for (int r = 0; r < RM; ++r)
+            if ((oddl >> r) & 1u) {
+#pragma unroll
+                for (int v = 0; v < RN; ++v) acc[r][v] = -acc[r][v];
+            }
+    };
     // async stage of offset k into buffer (k % ST): tensor block + (pre-scaled) moments
     auto stage = [&](int k) {
         const int code = olist[k];
@@ -947,6 +975,16 @@ __global__ void __launch_bounds__(NT, (RM * RN >= 40 ? 256 : 512) / NT) s2l_kern
     // TMA stage of offset k into buffer bf: the station's tensor block and one bulk copy per
     // source box; rows of boxes without a source at this offset are zeroed by plain stores.
     // The caller guarantees no thread still reads buffer bf (a block barrier precedes).
+    // Operator reuse (single-stage TMA path, whole operator in As): a backward offset (di, +a)
+    // right after its forward partner (di, -a) has the same station tensor and the same gathered
+    // A' up to the sign (-1)^{j+l} = (-1)^j (-1)^l: it negates the odd-j moment
+    // coefficients and the odd-l accumulator rows around its GEMM instead of re-gathering.
+    auto reuse_of = [&](int k) -> bool {
+        if (!(PF == 3 && ST == 1) || P > KC || k == 0) return false;
+        const int c = olist[k], cq = olist[k - 1];
+        const int dj = (c & 15) - 3, djq = (cq & 15) - 3;
+        return ((c >> 4) & 15) == ((cq >> 4) & 15) && dj > 0 && dj == -djq;
+    };
     auto tma_issue = [&](int k, int bf) {
         const int code = olist[k];
         const int di = ((code >> 4) & 15) - 3, dj = (code & 15) - 3, o = (code >> 8) & 0xff;
@@ -955,11 +993,12 @@ __global__ void __launch_bounds__(NT, (RM * RN >= 40 ? 256 : 512) / NT) s2l_kern
         const double *Tn = a.tens + ((int64_t)(iin * 12 + class_of(dI, dJ)) * KW + nloc) * TPp;
         double2 *Bs = reinterpret_cast<double2 *>(Bs0) + (size_t)bf * JT * BPS;
         const unsigned bm = omask[k];
+        const bool ru = reuse_of(k);
         if (tid < 32) {
             if (tid == 0) {
                 fence_proxy_async();
-                mbar_arrive_expect_tx(bar + bf, (unsigned)(TPp * 8 + __popc(bm) * P * 16));
-                bulk_g2s(Hs0 + bf * HST, Tn, (unsigned)(TPp * 8), bar + bf);
+                mbar_arrive_expect_tx(bar + bf, (unsigned)((ru ? 0 : TPp * 8) + __popc(bm) * P * 16));
+                if (!ru) bulk_g2s(Hs0 + bf * HST, Tn, (unsigned)(TPp * 8), bar + bf);
             }
             __syncwarp();
             if (tid < JT && ((bm >> tid) & 1u)) {
@@ -999,16 +1038,31 @@ __global__ void __launch_bounds__(NT, (RM * RN >= 40 ? 256 : 512) / NT) s2l_kern
         const double *Hs = Hs0 + buf * HST;
         const double *Bs = Bs0 + buf * P * NC;
         const double2 *Bt = reinterpret_cast<const double2 *>(Bs0) + (size_t)buf * JT * BPS;
+        const bool ru = reuse_of(k);
+        if (ru) {                             // A' of the forward partner stays in As
+            double2 *Bw = reinterpret_cast<double2 *>(Bs0) + (size_t)buf * JT * BPS;
+            for (int q = tid; q < JT * P; q += NT) {
+                const int b = q / P, kk = q - b * P;
+                if ((oddj >> kk) & 1ull) {
+                    const double2 v = Bw[b * BPS + kk];
+                    Bw[b * BPS + kk] = make_double2(-v.x, -v.y);
+                }
+            }
+            __syncthreads();
+            negate_oddl();
+        }
         for (int k0 = 0; k0 < P; k0 += KC) {
             const int kc = min(KC, P - k0);
             if (k0 > 0) __syncthreads();
             // A'[kk][m] = +-H_{A,B}(j+l): gather through the precomputed (index, sign) table
+            if (!ru) {
             for (int q = tid; q < kc * MP; q += NT) {
                 int c = __ldg(itab + k0 * MP + q);
                 double v = Hs[c >> 1];
                 As[q] = (c & 1) ? -v : v;
             }
             __syncthreads();
+            }
             // double-buffered TMA: the next offset's copies start now (every thread is past the
             // GEMM that read buffer (k+1) & 1) and land behind this GEMM
             if (TMA && ST == 2 && k0 == 0 && k + 1 < na) tma_issue(k + 1, (k + 1) & 1);
@@ -1022,6 +1076,7 @@ __global__ void __launch_bounds__(NT, (RM * RN >= 40 ? 256 : 512) / NT) s2l_kern
                                                                             kc, tm, tn, acc);
             }
         }
+        if (ru) negate_oddl();                // back to the forward sign
         if (TMA && ST == 2) __syncthreads();  // As is rebuilt for the next offset
     }
     (void)BOXV;
