@@ -153,7 +153,13 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
     }
     __syncthreads();
     const int total = segS0[18];
-    const int vb = (int)(((int64_t)total * warp) / kWarps), ve = (int)(((int64_t)total * (warp + 1)) / kWarps);
+    // the warps' shares of the source list interleave in chunks of 8 (chunk c goes to warp
+    // c mod 4): every warp sees all neighbour leaves, so the Miller / forward mix, and with it
+    // the warps' durations, are alike (contiguous quarters left warps waiting at the final
+    // barrier).  Warp-local index u -> source v = (4 (u / 8) + warp) 8 + u % 8.
+    constexpr int ICH = 8;
+    const int rem = total % (kWarps * ICH);
+    const int vb = 0, ve = ICH * (total / (kWarps * ICH)) + min(max(rem - ICH * warp, 0), ICH);
 
     const double tr = a.fr[t0 + min(tl, nt - 1)], tz = a.fz[t0 + min(tl, nt - 1)];
     double2 acc[KT];
@@ -166,7 +172,8 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
         const int nch = min(CH, ve - v0);
         __syncwarp();
         if (lane < nch) {
-            const int v = v0 + lane;
+            const int uu = v0 + lane;
+            const int v = (kWarps * (uu / ICH) + warp) * ICH + uu % ICH;
             int k = 0;
 #pragma unroll
             for (int kk = 1; kk < 9; ++kk) k += (v >= segPre[kk]);
