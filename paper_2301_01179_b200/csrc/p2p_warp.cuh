@@ -156,7 +156,8 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
     // the warps' shares of the source list interleave in chunks of 4 (chunk c goes to warp
     // c mod 4): every warp sees all neighbour leaves, so the Miller / forward mix, and with it
     // the warps' durations, are alike (contiguous quarters left warps waiting at the final
-    // barrier).  Warp-local index u -> source v = (4 (u / 4) + warp) 4 + u % 4 (chunks of 1, 2, 4, 8, 16 measured: 1-4 alike, 16 slower).
+    // barrier).  Warp-local index u -> source v = (4 (u / 4) + warp) 4 + u % 4 (chunks of 1,
+    // 2, 4, 8, 16 measured: 1-4 alike, 8 and 16 slower).
     constexpr int ICH = 4;
     const int rem = total % (kWarps * ICH);
     const int vb = 0, ve = ICH * (total / (kWarps * ICH)) + min(max(rem - ICH * warp, 0), ICH);
