@@ -193,6 +193,34 @@ cylfmm_status cylfmm_partition_fields(const double *src_r, const double *src_z, 
                                       const cylfmm_params *prm, int n_parts, int32_t *part,
                                       double *part_cost);
 
+/* Error-driven choice of the expansion order and the tree depth (the paper
+ * fixes neither: its error "scales approximately as C^{-0.4M} with weak dependence on tree
+ * depth", read as eps(p) = CYLFMM_EPS_C * 10^(-0.4 p), R#25).  HOST-only.
+ *  - order: the smallest p in [1, CYLFMM_MAX_ORDER] with eps(p) <= tol (CYLFMM_MAX_ORDER if
+ *    none); order_local = 0 (equal orders, as in the paper's runs).
+ *  - depth: the d in [depth_min, depth_max] (clamped to [2, CYLFMM_MAX_DEPTH]) minimising the
+ *    modelled solve time
+ *        T(d) = [ near(d) * (200 + 9 K) / e_near  +  s2l(d) * 4 P^2 K / e_s2l
+ *               + 12 * 2^d * K * (12 (2p+1)^2 + 12 (p+1)^3) / e_tens ] / F64_peak
+ *    (SURVEY 8(d) work per unit; e_* = round-1 measured fractions of the FP64 peak), where
+ *    near(d) = sum over non-empty target leaves t of n_t * (sources in the 9 leaves around t)
+ *    (coincident pairs included) and s2l(d) = sum over levels 2..d of (non-empty target box,
+ *    non-empty source box in its interaction list) pairs: the exact counts a
+ *    depth-d solve reports as n_near_pairs + n_skipped and n_s2l_pairs.
+ * prm (in/out): n_modes, domain_L, domain_z0 read (checked as for plan_create); order, depth
+ * and order_local written; other fields untouched.  tol > 0 (per-mode relative error).
+ * near_pairs, s2l_pairs (HOST int64 [depth_max - depth_min + 1], nullable), est_ms (HOST double
+ * [same], nullable): the per-depth counts and modelled times (-1 for depths outside [2, 11]).
+ * eps_model (HOST, nullable): eps(order).
+ * Errors: EINVAL (null prm, tol <= 0 or not finite, depth_min > depth_max, bad prm fields),
+ * EDOMAIN (point outside the domain). */
+#define CYLFMM_EPS_C 0.1
+cylfmm_status cylfmm_select_params(const double *src_r, const double *src_z, int64_t n_src,
+                                   const double *fld_r, const double *fld_z, int64_t n_fld,
+                                   double tol, int depth_min, int depth_max, cylfmm_params *prm,
+                                   int64_t *near_pairs, int64_t *s2l_pairs, double *est_ms,
+                                   double *eps_model);
+
 #ifdef __cplusplus
 }
 #endif

@@ -3,4 +3,4 @@ quadtree FMM of arXiv 2301.01179.  The compute path is libcylfmm.so (csrc/, incl
 this package is its ctypes binding plus the seeded input generators."""
 from .cylfmm import (MILLER_ACCURATE, MILLER_PAPER, TRUNC_DOUBLE, TRUNC_SINGLE, CylFMMError,  # noqa: F401
                      FMMConfig, Plan, direct, greens_batch, header_functions, lib,
-                     partition_fields, tensor_batch, tree_sort)
+                     partition_fields, select_params, tensor_batch, tree_sort)

@@ -1468,3 +1468,126 @@ extern "C" cylfmm_status cylfmm_partition_fields(const double *src_r, const doub
         for (int q = 0; q < n_parts; ++q) part_cost[q] = pc[(size_t)q];
     return CYLFMM_OK;
 }
+
+// ------------------------------------------------------------------------------------------
+// host-side error-driven order and depth selection (include/cylfmm.h, R#25)
+namespace {
+// round-1 measured fractions of the FP64 peak: near field ~0.12,
+// S2L GEMM ~0.3, tensor seeds + fill ~0.05; F64 nominal 37.2 TF/s
+constexpr double kEffNear = 0.12, kEffS2L = 0.30, kEffTens = 0.05, kF64 = 37.2e12;
+}
+
+extern "C" cylfmm_status cylfmm_select_params(const double *src_r, const double *src_z,
+                                              int64_t n_src, const double *fld_r,
+                                              const double *fld_z, int64_t n_fld, double tol,
+                                              int depth_min, int depth_max, cylfmm_params *prm,
+                                              int64_t *near_pairs, int64_t *s2l_pairs,
+                                              double *est_ms, double *eps_model)
+{
+    if (!prm || !(tol > 0.0) || !std::isfinite(tol) || depth_min > depth_max || n_src < 0 ||
+        n_fld < 0 || (n_src > 0 && (!src_r || !src_z)) || (n_fld > 0 && (!fld_r || !fld_z)) ||
+        prm->n_modes < 1 || prm->n_modes > CYLFMM_MAX_MODES || !(prm->domain_L > 0.0) ||
+        !std::isfinite(prm->domain_L) || !std::isfinite(prm->domain_z0)) {
+        set_err("cylfmm_select_params: bad arguments");
+        return CYLFMM_EINVAL;
+    }
+    const int K = prm->n_modes;
+    const double L = prm->domain_L, z0 = prm->domain_z0;
+    // order: smallest p with CYLFMM_EPS_C 10^(-0.4 p) <= tol
+    int p = 1;
+    while (p < CYLFMM_MAX_ORDER && CYLFMM_EPS_C * std::pow(10.0, -0.4 * p) > tol) ++p;
+    const double P = (p + 1) * (p + 2) / 2.0;
+    const int d0 = std::max(depth_min, 2), d1 = std::min(depth_max, CYLFMM_MAX_DEPTH);
+    const int nd = depth_max - depth_min + 1;
+    if (d0 > d1) {
+        set_err("cylfmm_select_params: no depth in [%d, %d] within [2, %d]", depth_min, depth_max,
+                CYLFMM_MAX_DEPTH);
+        return CYLFMM_EINVAL;
+    }
+    // finest-level box of every point (Morton key at d1); coarser keys by shifting
+    const int D = d1;
+    std::vector<uint32_t> skey((size_t)n_src), fkey((size_t)n_fld);
+    for (int64_t i = 0; i < n_src; ++i) {
+        uint32_t ix, iz;
+        if (!host_box(src_r[i], src_z[i], D, L, z0, ix, iz)) {
+            set_err("cylfmm_select_params: source %lld outside the domain", (long long)i);
+            return CYLFMM_EDOMAIN;
+        }
+        skey[i] = host_morton(ix, iz);
+    }
+    for (int64_t j = 0; j < n_fld; ++j) {
+        uint32_t ix, iz;
+        if (!host_box(fld_r[j], fld_z[j], D, L, z0, ix, iz)) {
+            set_err("cylfmm_select_params: field point %lld outside the domain", (long long)j);
+            return CYLFMM_EDOMAIN;
+        }
+        fkey[j] = host_morton(ix, iz);
+    }
+    // per level l = 2..D: source / target counts per box (dense, Morton-indexed), the level's
+    // S2L pair count, and (l in [d0, d1]) the near-pair count with leaves at level l
+    std::vector<int64_t> s2l_lev((size_t)D + 1, 0), near_lev((size_t)D + 1, 0);
+    std::vector<int64_t> ns, nt;
+    for (int l = 2; l <= D; ++l) {
+        const int nb = 1 << l, sh = 2 * (D - l);
+        ns.assign((size_t)nb * nb, 0);
+        nt.assign((size_t)nb * nb, 0);
+        for (uint32_t k : skey) ns[k >> sh]++;
+        for (uint32_t k : fkey) nt[k >> sh]++;
+        int64_t s2l = 0, near = 0;
+        for (int ix = 0; ix < nb; ++ix)
+            for (int iz = 0; iz < nb; ++iz) {
+                const int64_t t = nt[host_morton((uint32_t)ix, (uint32_t)iz)];
+                if (!t) continue;
+                // interaction list: children of the parent's neighbours that are not neighbours
+                const int px = ix >> 1, pz = iz >> 1;
+                for (int x = 2 * px - 2; x <= 2 * px + 3; ++x)
+                    for (int z = 2 * pz - 2; z <= 2 * pz + 3; ++z) {
+                        if (x < 0 || z < 0 || x >= nb || z >= nb) continue;
+                        if (std::abs(x - ix) <= 1 && std::abs(z - iz) <= 1) continue;
+                        if (ns[host_morton((uint32_t)x, (uint32_t)z)]) ++s2l;
+                    }
+                if (l < d0) continue;
+                int64_t s9 = 0;
+                for (int a = -1; a <= 1; ++a)
+                    for (int c = -1; c <= 1; ++c) {
+                        const int x = ix + a, z = iz + c;
+                        if (x >= 0 && z >= 0 && x < nb && z < nb)
+                            s9 += ns[host_morton((uint32_t)x, (uint32_t)z)];
+                    }
+                near += t * s9;
+            }
+        s2l_lev[l] = s2l;
+        near_lev[l] = near;
+    }
+    int best = -1;
+    double best_ms = 0.0;
+    const double wpair = (200.0 + 9.0 * K) / kEffNear, ws2l = 4.0 * P * P * K / kEffS2L;
+    const double wtens = 12.0 * K * (12.0 * (2 * p + 1) * (2 * p + 1) + 12.0 * (p + 1) * (p + 1) * (p + 1)) / kEffTens;
+    int64_t s2l_cum = 0;
+    for (int d = 2; d <= D; ++d) {
+        s2l_cum += s2l_lev[d];
+        if (d < d0 || d > d1) continue;
+        const double ms = 1e3 * ((double)near_lev[d] * wpair + (double)s2l_cum * ws2l +
+                                 (double)(1 << d) * wtens) / kF64;
+        const int q = d - depth_min;
+        if (near_pairs) near_pairs[q] = near_lev[d];
+        if (s2l_pairs) s2l_pairs[q] = s2l_cum;
+        if (est_ms) est_ms[q] = ms;
+        if (best < 0 || ms < best_ms) {
+            best = d;
+            best_ms = ms;
+        }
+    }
+    for (int q = 0; q < nd; ++q) {
+        const int d = depth_min + q;
+        if (d >= d0 && d <= d1) continue;
+        if (near_pairs) near_pairs[q] = -1;
+        if (s2l_pairs) s2l_pairs[q] = -1;
+        if (est_ms) est_ms[q] = -1.0;
+    }
+    prm->order = p;
+    prm->order_local = 0;
+    prm->depth = best;
+    if (eps_model) *eps_model = CYLFMM_EPS_C * std::pow(10.0, -0.4 * p);
+    return CYLFMM_OK;
+}

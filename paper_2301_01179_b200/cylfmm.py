@@ -96,6 +96,9 @@ def lib():
     L.cylfmm_partition_fields.restype = i
     L.cylfmm_partition_fields.argtypes = [vp, vp, i64, vp, vp, i64, ctypes.POINTER(Params), i,
                                           vp, vp]
+    L.cylfmm_select_params.restype = i
+    L.cylfmm_select_params.argtypes = [vp, vp, i64, vp, vp, i64, d, i, i, ctypes.POINTER(Params),
+                                       vp, vp, vp, vp]
     _lib = L
     return L
 
@@ -285,3 +288,27 @@ def partition_fields(src_r, src_z, fld_r, fld_z, cfg: "FMMConfig", n_parts: int)
                                          a[2].shape[0], ctypes.byref(prm), int(n_parts), p(part),
                                          p(cost)), "cylfmm_partition_fields")
     return part, cost
+
+
+def select_params(src_r, src_z, fld_r, fld_z, n_modes: int, tol: float, L: float = 1.0,
+                  z0: float = 0.0, depth_min: int = 2, depth_max: int = 11):
+    """Error-driven order and depth (cylfmm_select_params, host-only): the smallest order whose
+    modelled error CYLFMM_EPS_C 10^(-0.4 p) meets tol (R#25), and the depth in
+    [depth_min, depth_max] minimising the modelled solve time.  Returns (FMMConfig, info) with
+    info = {"eps_model", "depths", "near_pairs", "s2l_pairs", "est_ms"} (per-depth arrays)."""
+    a = [np.ascontiguousarray(v, dtype=np.float64) for v in (src_r, src_z, fld_r, fld_z)]
+    nd = max(depth_max - depth_min + 1, 0)
+    near = np.zeros(nd, dtype=np.int64)
+    s2l = np.zeros(nd, dtype=np.int64)
+    ms = np.zeros(nd, dtype=np.float64)
+    eps = ctypes.c_double(0.0)
+    prm = Params(int(n_modes), 1, 2, TRUNC_DOUBLE, MILLER_ACCURATE, 1, float(z0), float(L), 0, 0)
+    p = lambda x: ctypes.c_void_p(x.ctypes.data) if x.size else ctypes.c_void_p(0)  # noqa: E731
+    _check(lib().cylfmm_select_params(p(a[0]), p(a[1]), a[0].shape[0], p(a[2]), p(a[3]),
+                                      a[2].shape[0], float(tol), int(depth_min), int(depth_max),
+                                      ctypes.byref(prm), p(near), p(s2l), p(ms),
+                                      ctypes.byref(eps)), "cylfmm_select_params")
+    cfg = FMMConfig(n_modes=int(n_modes), order=prm.order, depth=prm.depth, L=float(L), z0=float(z0))
+    info = {"eps_model": eps.value, "depths": np.arange(depth_min, depth_max + 1),
+            "near_pairs": near, "s2l_pairs": s2l, "est_ms": ms}
+    return cfg, info
