@@ -879,14 +879,29 @@ __global__ void __launch_bounds__(NT, (RM * RN >= 40 ? 256 : 512) / NT) s2l_kern
         int k = 0;
         unsigned long long npairs = 0;
         for (int o = 0; o < NOFF; ++o) {
-            const unsigned bm = __ballot_sync(0xffffffffu, tid < JT && ssl[o * JT + tid] >= 0);
-            if (!bm) continue;
-            npairs += __popc(bm);
-            if (tid == 0) {
-                omask[k] = bm;
-                olist[k] = (olist[o] & 0xff) | (o << 8);
+            // TMA path: (di, -3) reaches only odd target boxes and (di, +3) only even ones
+            // (parity rule of the interaction list), so the pair is one merged offset: the odd
+            // boxes' sources from (di, -3), the even boxes' from (di, +3) (signs: see `mg`)
+            const int oc = olist[o];
+            const bool mrg = TMA && (oc & 15) == 0;
+            bool has = tid < JT && ssl[o * JT + tid] >= 0;
+            if (mrg && tid < JT) {
+                const int sp = ssl[(o + 1) * JT + tid];
+                if (sp >= 0) {
+                    ssl[o * JT + tid] = sp;
+                    has = true;
+                }
             }
-            ++k;
+            const unsigned bm = __ballot_sync(0xffffffffu, has);
+            if (bm) {
+                npairs += __popc(bm);
+                if (tid == 0) {
+                    omask[k] = bm;
+                    olist[k] = (oc & 0xff) | (o << 8) | (mrg ? 1 << 24 : 0);
+                }
+                ++k;
+            }
+            if (mrg) ++o;
         }
         if (tid == 0) {
             *nact = k;
@@ -932,10 +947,10 @@ __global__ void __launch_bounds__(NT, (RM * RN >= 40 ? 256 : 512) / NT) s2l_kern
     // reuse masks: moment coefficients kk with odd j; this thread's accumulator rows with odd l
     unsigned long long oddj = 0;
     unsigned oddl = 0;
-    if (PF == 3 && ST == 1 && P <= KC) {
+    if (PF == 3) {
         for (int i = 0, q = 0; i <= p; ++i)
             for (int j = 0; i + j <= p; ++j, ++q)
-                if (j & 1) oddj |= 1ull << q;
+                if ((j & 1) && q < 64) oddj |= 1ull << q;   // used only when P <= 64 (reuse)
 #pragma unroll
         for (int r = 0; r < RM; ++r) {
             const int m = 2 * (tm + TM * (r >> 1)) + (r & 1);
@@ -1039,6 +1054,24 @@ __global__ void __launch_bounds__(NT, (RM * RN >= 40 ? 256 : 512) / NT) s2l_kern
         const double *Bs = Bs0 + buf * P * NC;
         const double2 *Bt = reinterpret_cast<const double2 *>(Bs0) + (size_t)buf * JT * BPS;
         const bool ru = reuse_of(k);
+        // merged (di, -3) / (di, +3) offset: the operator is the forward one; the even boxes'
+        // (+3) part is its backward partner, (-1)^j on their moments and (-1)^l on their
+        // accumulator rows around the GEMM, as for the operator reuse below
+        const bool mg = TMA && ((code >> 24) & 1);
+        const bool evenT = (tn * RN / 2) < JH;
+        if (mg) {
+            double2 *Bw = reinterpret_cast<double2 *>(Bs0) + (size_t)buf * JT * BPS;
+            for (int q = tid; q < JH * (p + 1); q += NT) {
+                const int b = q / (p + 1), i = q - b * (p + 1);
+                const int q0 = i * (p + 1) - i * (i - 1) / 2;
+                for (int j = 1; i + j <= p; j += 2) {
+                    const double2 v = Bw[b * BPS + q0 + j];
+                    Bw[b * BPS + q0 + j] = make_double2(-v.x, -v.y);
+                }
+            }
+            __syncthreads();
+            if (evenT) negate_oddl();
+        }
         if (ru) {                             // A' of the forward partner stays in As
             double2 *Bw = reinterpret_cast<double2 *>(Bs0) + (size_t)buf * JT * BPS;
             for (int q = tid; q < JT * P; q += NT) {
@@ -1076,7 +1109,7 @@ __global__ void __launch_bounds__(NT, (RM * RN >= 40 ? 256 : 512) / NT) s2l_kern
                                                                             kc, tm, tn, acc);
             }
         }
-        if (ru) negate_oddl();                // back to the forward sign
+        if (ru || (mg && evenT)) negate_oddl();   // back to the forward sign
         if (TMA && ST == 2) __syncthreads();  // As is rebuilt for the next offset
     }
     (void)BOXV;
