@@ -1043,7 +1043,11 @@ __global__ void __launch_bounds__(NT, (RM * RN >= 40 ? 256 : 512) / NT) s2l_kern
             }
             cp_async_wait_all();
         }
-        __syncthreads();                      // buffer k ready (zero rows visible); As free
+        // buffer k ready (zero rows visible); As free.  Single-stage TMA: As is free since the
+        // barrier before tma_issue, the bulk copies are visible after mbar_wait, and the zero
+        // rows (stored by tma_issue) become visible at the barrier after the gather / negation
+        // below, before any GEMM reads them (negations touch only TMA-written rows)
+        if (!(TMA && ST == 1)) __syncthreads();
         if (!TMA && ST == 2 && k + 1 < na) stage(k + 1);   // overlaps the build and GEMM below
         const int code = olist[k];
         const int di = ((code >> 4) & 15) - 3, dj = (code & 15) - 3;
@@ -1061,8 +1065,10 @@ __global__ void __launch_bounds__(NT, (RM * RN >= 40 ? 256 : 512) / NT) s2l_kern
         const bool evenT = (tn * RN / 2) < JH;
         if (mg) {
             double2 *Bw = reinterpret_cast<double2 *>(Bs0) + (size_t)buf * JT * BPS;
+            const unsigned bmk = omask[k];
             for (int q = tid; q < JH * (p + 1); q += NT) {
                 const int b = q / (p + 1), i = q - b * (p + 1);
+                if (!((bmk >> b) & 1u)) continue;
                 const int q0 = i * (p + 1) - i * (i - 1) / 2;
                 for (int j = 1; i + j <= p; j += 2) {
                     const double2 v = Bw[b * BPS + q0 + j];
@@ -1074,9 +1080,10 @@ __global__ void __launch_bounds__(NT, (RM * RN >= 40 ? 256 : 512) / NT) s2l_kern
         }
         if (ru) {                             // A' of the forward partner stays in As
             double2 *Bw = reinterpret_cast<double2 *>(Bs0) + (size_t)buf * JT * BPS;
+            const unsigned bmk = omask[k];
             for (int q = tid; q < JT * P; q += NT) {
                 const int b = q / P, kk = q - b * P;
-                if ((oddj >> kk) & 1ull) {
+                if (((oddj >> kk) & 1ull) && ((bmk >> b) & 1u)) {
                     const double2 v = Bw[b * BPS + kk];
                     Bw[b * BPS + kk] = make_double2(-v.x, -v.y);
                 }
