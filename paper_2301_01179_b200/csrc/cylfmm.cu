@@ -96,12 +96,15 @@ static cudaError_t allow_smem(F *kernel)
 #define S2L_P8 128, 8, 6, 4, 48, 1, 3
 #define S2L_P8_V1 128, 8, 6, 4, 48, 2, 3
 #define S2L_P8_V2 128, 8, 6, 4, 48, 1, 2
-#define S2L_P12 256, 16, 6, 4, 16, 1, 3
-#define S2L_P12_V1 256, 16, 6, 4, 16, 2, 3
-#define S2L_P12_V2 256, 16, 6, 4, 16, 1, 2
-#define S2L_P16 256, 16, 10, 2, 16, 1, 3
-#define S2L_P16_V1 256, 16, 10, 2, 16, 2, 3
-#define S2L_P16_V2 256, 16, 10, 2, 16, 1, 2
+// depth chunk KC: the largest that keeps two CTAs per SM (one barrier pair per chunk; measured
+// C3 / C4 S2L: KC 16 -> 48 at p = 12: 18.5 -> 17.3 ms; KC 16 -> 24 at p = 16: 87.0 -> 85.6 ms;
+// KC 32 at p = 12: 17.6 ms; KC 8 at p = 16: 98.8 ms)
+#define S2L_P12 256, 16, 6, 4, 48, 1, 3
+#define S2L_P12_V1 256, 16, 6, 4, 16, 1, 3
+#define S2L_P12_V2 256, 16, 6, 4, 32, 1, 3
+#define S2L_P16 256, 16, 10, 2, 24, 1, 3
+#define S2L_P16_V1 256, 16, 10, 2, 16, 1, 3
+#define S2L_P16_V2 256, 16, 10, 2, 8, 1, 3
 // each tiling is instantiated for a runtime order (0) and for the BASELINE order of its class
 #define S2L_ALL(X) X(S2L_P8, 0) X(S2L_P8, 8) X(S2L_P8_V1, 0) X(S2L_P8_V1, 8) X(S2L_P8_V2, 0)      \
     X(S2L_P8_V2, 8) X(S2L_P12, 0) X(S2L_P12, 12) X(S2L_P12_V1, 0) X(S2L_P12_V1, 12)              \

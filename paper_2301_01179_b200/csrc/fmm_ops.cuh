@@ -995,7 +995,7 @@ __global__ void __launch_bounds__(NT, (RM * RN >= 40 ? 256 : 512) / NT) s2l_kern
     // A' up to the sign (-1)^{j+l} = (-1)^j (-1)^l: it negates the odd-j moment
     // coefficients and the odd-l accumulator rows around its GEMM instead of re-gathering.
     auto reuse_of = [&](int k) -> bool {
-        if (!(PF == 3 && ST == 1) || P > KC || k == 0) return false;
+        if (!(PF == 3 && ST == 1) || P > KC || P > 64 || k == 0) return false;   // oddj: 64 bits
         const int c = olist[k], cq = olist[k - 1];
         const int dj = (c & 15) - 3, djq = (cq & 15) - 3;
         return ((c >> 4) & 15) == ((cq >> 4) & 15) && dj > 0 && dj == -djq;
