@@ -92,7 +92,7 @@ static cudaError_t allow_smem(F *kernel)
 // warp-level offset skipping (PF 2) beat the strided/masked layout (PF 0) by 3-23%.
 // PF 3 = blocked + box-major B staged by TMA bulk copies on an mbarrier (default: C2 S2L
 // 0.49 -> 0.45 ms, C3 21.7 -> 20.2 ms, C4 98.6 -> 93.8 ms); double-buffering the TMA stages
-// (ST 2, V1) halves the resident CTAs and is 20-50% slower.
+// (ST 2; S2L_P8_V1 keeps it) halves the resident CTAs and is 20-50% slower.
 #define S2L_P8 128, 8, 6, 4, 48, 1, 3
 #define S2L_P8_V1 128, 8, 6, 4, 48, 2, 3
 #define S2L_P8_V2 128, 8, 6, 4, 48, 1, 2
