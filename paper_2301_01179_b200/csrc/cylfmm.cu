@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "fmm_ops.cuh"
+#include "s2l.cuh"
 #include "p2p.cuh"
 #include "p2p_warp.cuh"
 #include "specfun.cuh"
@@ -85,31 +86,12 @@ static cudaError_t allow_smem(F *kernel)
 #define P2P_INSTANCES(X)                                                                       \
     X(8, 16, 2) X(8, 16, 5) X(16, 8, 3) X(16, 8, 9) X(32, 4, 6) X(32, 4, 18)
 
-// S2L tilings (NT, TM, RM, RN, KC, stages); variant 0 of each order class is the default, the
-// others are selectable with CYLFMM_S2L_VARIANT for measurement (same MP = TM RM per class)
-// measured (C2/C3/C4 S2L phase, round 1): single-stage staging (more CTAs per SM) beats the
-// double-buffered one by 11-20%; a register double buffer gains nothing; blocked columns with
-// warp-level offset skipping (PF 2) beat the strided/masked layout (PF 0) by 3-23%.
-// PF 3 = blocked + box-major B staged by TMA bulk copies on an mbarrier (default: C2 S2L
-// 0.49 -> 0.45 ms, C3 21.7 -> 20.2 ms, C4 98.6 -> 93.8 ms); double-buffering the TMA stages
-// (ST 2; S2L_P8_V1 keeps it) halves the resident CTAs and is 20-50% slower.
-#define S2L_P8 128, 8, 6, 4, 48, 1, 3
-#define S2L_P8_V1 128, 8, 6, 4, 48, 2, 3
-#define S2L_P8_V2 128, 8, 6, 4, 48, 1, 2
-// depth chunk KC: the largest that keeps two CTAs per SM (one barrier pair per chunk; measured
-// C3 / C4 S2L: KC 16 -> 48 at p = 12: 18.5 -> 17.3 ms; KC 16 -> 24 at p = 16: 87.0 -> 85.6 ms;
-// KC 32 at p = 12: 17.6 ms; KC 8 at p = 16: 98.8 ms)
-#define S2L_P12 256, 16, 6, 4, 48, 1, 3
-#define S2L_P12_V1 256, 16, 6, 4, 16, 1, 3
-#define S2L_P12_V2 256, 16, 6, 4, 32, 1, 3
-#define S2L_P16 256, 16, 10, 2, 24, 1, 3
-#define S2L_P16_V1 256, 16, 10, 2, 16, 1, 3
-#define S2L_P16_V2 256, 16, 10, 2, 8, 1, 3
-// each tiling is instantiated for a runtime order (0) and for the BASELINE order of its class
-#define S2L_ALL(X) X(S2L_P8, 0) X(S2L_P8, 8) X(S2L_P8_V1, 0) X(S2L_P8_V1, 8) X(S2L_P8_V2, 0)      \
-    X(S2L_P8_V2, 8) X(S2L_P12, 0) X(S2L_P12, 12) X(S2L_P12_V1, 0) X(S2L_P12_V1, 12)              \
-    X(S2L_P12_V2, 0) X(S2L_P12_V2, 12) X(S2L_P16, 0) X(S2L_P16, 16) X(S2L_P16_V1, 0)             \
-    X(S2L_P16_V1, 16) X(S2L_P16_V2, 0) X(S2L_P16_V2, 16)
+// S2L batch shapes (R rows per unit, C pairs per thread, NU units >= units(pl, R), CG column
+// groups) per local-order class; JT = CG C pairs per batch
+#define S2L_P8 4, 4, 16, 8
+#define S2L_P12 4, 4, 32, 8
+#define S2L_P16 4, 4, 48, 4
+#define S2L_ALL(X) X(S2L_P8) X(S2L_P12) X(S2L_P16)
 
 static cylfmm_status ensure_init()
 {
@@ -138,18 +120,18 @@ static cylfmm_status ensure_init()
     CK(allow_smem(l2l_kernel));
     CK(allow_smem(l2p_kernel<false>));
     CK(allow_smem(l2p_kernel<true>));
-#define X(...) CK(allow_smem(s2l_kernel<__VA_ARGS__>));
+#define X(...) CK(allow_smem(s2l_batch_kernel<__VA_ARGS__>));
     S2L_ALL(X)
 #undef X
     if (dev < 64) g_init_done[dev] = true;
     return CYLFMM_OK;
 }
 
-static int s2l_mp(int p)
+static int s2l_jt(int pl)
 {
-    if (p <= 8) return S2LCfg<S2L_P8, 0>::MP;
-    if (p <= 12) return S2LCfg<S2L_P12, 0>::MP;
-    return S2LCfg<S2L_P16, 0>::MP;
+    if (pl <= 8) return S2LCfg<S2L_P8>::JT;
+    if (pl <= 12) return S2LCfg<S2L_P12>::JT;
+    return S2LCfg<S2L_P16>::JT;
 }
 
 static inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -457,10 +439,10 @@ struct cylfmm_plan_s {
     DevBuf slstart, flstart, flags, smap, skeys, tmap, tkeys, counts;
     DevBuf M, Lc, tens, seeds;
     DevBuf tasks, ntasks, tcnt, toff;
-    DevBuf tflag, tpos, tiles, written;   // S2L tile compaction
+    DevBuf written;                       // per-box 'local written by S2L' flags
+    DevBuf pcnt, poff, khist, kstart, kcur, bstart, pairs, batches, wlist, pairbuf;   // S2L lists
     DevBuf need;                          // lazy L2L flags
     DevBuf err, ctr;
-    DevBuf s2lidx;   // S2L operator gather table for this plan's (p, truncation)
     DevBuf rtab;     // M2M / L2L recentring tables: [rtab(p) | rtab(pl)] doubles, then tri ints
     size_t rtab_nm = 0, rtab_nd = 0, rtab_ntm = 0;
     // host-API staging
@@ -487,7 +469,7 @@ static void free_plan_bufs(cylfmm_plan p)
                      &p->scan_tmp[3], &p->sr_s, &p->sz_s, &p->S_s, &p->fr_s, &p->fz_s,
                      &p->slstart, &p->flstart, &p->flags, &p->smap, &p->skeys, &p->tmap,
                      &p->tkeys, &p->counts, &p->M, &p->Lc, &p->tens, &p->seeds, &p->tasks,
-                     &p->ntasks, &p->tcnt, &p->toff, &p->tflag, &p->tpos, &p->tiles, &p->written, &p->need, &p->err, &p->ctr, &p->s2lidx, &p->rtab, &p->h_sr, &p->h_sz,
+                     &p->ntasks, &p->tcnt, &p->toff, &p->written, &p->pcnt, &p->poff, &p->khist, &p->kstart, &p->kcur, &p->bstart, &p->pairs, &p->batches, &p->wlist, &p->pairbuf, &p->need, &p->err, &p->ctr, &p->rtab, &p->h_sr, &p->h_sz,
                      &p->h_S, &p->h_fr, &p->h_fz, &p->h_out};
     for (DevBuf *b : all) b->release();
 }
@@ -522,11 +504,7 @@ extern "C" cylfmm_status cylfmm_plan_create(cylfmm_plan *plan, const cylfmm_para
     for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&p->hev[i], cudaEventDisableTiming));
     p->aux_ok = true;
     {
-        std::vector<int> tab;
         const int pl = q.order_local > 0 ? q.order_local : q.order;
-        build_s2l_index(q.order, pl, s2l_mp(pl), q.truncation, tab);
-        RET_IF(p->s2lidx.need(sizeof(int) * tab.size()));
-        CK(cudaMemcpy(p->s2lidx.p, tab.data(), sizeof(int) * tab.size(), cudaMemcpyHostToDevice));
         // recentring tables for the source order (M2M) and the local order (L2L), once per plan
         std::vector<double> rm, rl;
         std::vector<int> tm_, tl_;
@@ -694,82 +672,21 @@ extern "C" cylfmm_status cylfmm_tree_sort(const double *r, const double *z, int6
 // FMM solve
 static int64_t pow4(int l) { return (int64_t)1 << (2 * l); }
 
-// S2L tiles of every level 2..depth: (column it, row tile jt of JH boxes per parity)
-static S2LGrid make_s2l_grid(int depth, int JH)
+template <int R, int C, int NU, int CG>
+static cudaError_t launch_s2l_t(const S2LArgs &sa, int64_t nbatches, cudaStream_t st)
 {
-    // deepest level first: its tiles carry the most boxes (the longest CTAs), so they start in
-    // the first wave and the short coarse-level CTAs fill the tail
-    S2LGrid gr = {};
-    int64_t tot = 0;
-    static const bool asc = getenv("CYLFMM_S2L_ASC") && atoi(getenv("CYLFMM_S2L_ASC")) == 1;
-    for (int li = 2; li <= depth; ++li) {
-        const int l = asc ? li : depth + 2 - li;
-        int nb = 1 << l, half = std::max(nb / 2, 1);
-        int jtiles = (half + JH - 1) / JH;
-        gr.level[gr.nlev] = l;
-        gr.jtiles[gr.nlev] = jtiles;
-        gr.start[gr.nlev] = tot;
-        tot += (int64_t)nb * jtiles;
-        gr.nlev++;
-    }
-    gr.start[gr.nlev] = tot;
-    return gr;
-}
-
-template <int NT, int TM, int RM, int RN, int KC, int ST, int PF, int PC>
-static cudaError_t launch_s2l_t(const FarArgs &fa, int64_t ntiles, cudaStream_t st)
-{
-    using Cfg = S2LCfg<NT, TM, RM, RN, KC, ST, PF, PC>;
-    const int KW = fa.m1 - fa.m0;
-    const S2LGrid gr = make_s2l_grid(fa.depth, Cfg::JH);
-    if (ntiles == 0) return cudaSuccess;
-    size_t sm = s2l_smem_bytes<NT, TM, RM, RN, KC, ST, PF, PC>(fa.p, fa.pl);
-    s2l_kernel<NT, TM, RM, RN, KC, ST, PF, PC><<<(unsigned)(ntiles * KW), NT, sm, st>>>(fa, gr);
+    const int KW = sa.m1 - sa.m0;
+    if (nbatches == 0) return cudaSuccess;
+    size_t sm = s2l_smem_bytes<R, C, NU, CG>(sa.p, sa.pl);
+    s2l_batch_kernel<R, C, NU, CG><<<(unsigned)(nbatches * KW), NU * CG, sm, st>>>(sa);
     return cudaGetLastError();
 }
-template <int NT, int TM, int RM, int RN, int KC, int ST, int PF, int PC>
-static int s2l_jh_t()
+// class by the local order (units(pl, R) <= NU)
+static cudaError_t launch_s2l(const S2LArgs &sa, int64_t nbatches, cudaStream_t st)
 {
-    return S2LCfg<NT, TM, RM, RN, KC, ST, PF, PC>::JH;
-}
-static int s2l_variant()
-{
-    static int v = [] {
-        const char *e = getenv("CYLFMM_S2L_VARIANT");
-        return e ? atoi(e) : 0;
-    }();
-    return v;
-}
-// class by the local order `cls` (GEMM rows <= MP); the compile-time order PC only when the
-// source and local orders are both PCV (`pcm`)
-#define S2L_PICK(FN, CFG, PCV, ...) \
-    return (pcm == PCV) ? FN<CFG, PCV>(__VA_ARGS__) : FN<CFG, 0>(__VA_ARGS__)
-#define S2L_DISPATCH(FN, ...)                                                                  \
-    do {                                                                                       \
-        const int v_ = s2l_variant();                                                          \
-        if (cls <= 8) {                                                                        \
-            if (v_ == 1) S2L_PICK(FN, S2L_P8_V1, 8, __VA_ARGS__);                              \
-            if (v_ == 2) S2L_PICK(FN, S2L_P8_V2, 8, __VA_ARGS__);                              \
-            S2L_PICK(FN, S2L_P8, 8, __VA_ARGS__);                                              \
-        }                                                                                      \
-        if (cls <= 12) {                                                                       \
-            if (v_ == 1) S2L_PICK(FN, S2L_P12_V1, 12, __VA_ARGS__);                            \
-            if (v_ == 2) S2L_PICK(FN, S2L_P12_V2, 12, __VA_ARGS__);                            \
-            S2L_PICK(FN, S2L_P12, 12, __VA_ARGS__);                                            \
-        }                                                                                      \
-        if (v_ == 1) S2L_PICK(FN, S2L_P16_V1, 16, __VA_ARGS__);                                \
-        if (v_ == 2) S2L_PICK(FN, S2L_P16_V2, 16, __VA_ARGS__);                                \
-        S2L_PICK(FN, S2L_P16, 16, __VA_ARGS__);                                                \
-    } while (0)
-static cudaError_t launch_s2l(const FarArgs &fa, int64_t ntiles, cudaStream_t st)
-{
-    const int cls = fa.pl, pcm = fa.p == fa.pl ? fa.p : -1;
-    S2L_DISPATCH(launch_s2l_t, fa, ntiles, st);
-}
-static int s2l_jh(int cls)
-{
-    const int pcm = -1;
-    S2L_DISPATCH(s2l_jh_t);
+    if (sa.pl <= 8) return launch_s2l_t<S2L_P8>(sa, nbatches, st);
+    if (sa.pl <= 12) return launch_s2l_t<S2L_P12>(sa, nbatches, st);
+    return launch_s2l_t<S2L_P16>(sa, nbatches, st);
 }
 
 struct PhaseTimer {
@@ -920,7 +837,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     RET_IF(p->skeys.need(sizeof(int) * ltot));
     RET_IF(p->tmap.need(sizeof(int) * ltot));
     RET_IF(p->tkeys.need(sizeof(int) * ltot));
-    RET_IF(p->counts.need(sizeof(int) * (2 * kMaxLevels + 2)));
+    RET_IF(p->counts.need(sizeof(int) * (2 * kMaxLevels + 4)));
     int *tmap_b = same ? p->smap.as<int>() : p->tmap.as<int>();
     int *tkeys_b = same ? p->skeys.as<int>() : p->tkeys.as<int>();
     const int nside = same ? 1 : 2;
@@ -957,45 +874,80 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             p->launches += 2;
         }
     }
-    // S2L tiles with at least one interaction (sparse inputs: C4, C5) and the per-box
-    // "written by S2L" flags that L2L / L2P use instead of zero-initialised locals
-    const S2LGrid s2lgr = make_s2l_grid(d, s2l_jh(pl));
-    const int64_t ntiles_all = s2lgr.start[s2lgr.nlev];
-    RET_IF(p->tflag.need(sizeof(int) * std::max<int64_t>(ntiles_all, 1)));
-    RET_IF(p->tpos.need(sizeof(int) * std::max<int64_t>(ntiles_all, 1)));
-    RET_IF(p->tiles.need(sizeof(int) * std::max<int64_t>(ntiles_all, 1)));
+    // S2L interaction lists (s2l.cuh): every (target box, source box) pair of every level,
+    // counted per target (dense index) and per station key; the per-box "written by S2L" flags
+    // that L2L / L2P use instead of zero-initialised locals
+    const int nkeys = 2 * 12 * (1 << d), JT = s2l_jt(pl);
     RET_IF(p->written.need(std::max<int64_t>(ltot, 1)));
-    CK(cudaMemsetAsync(p->counts.as<int>() + 2 * kMaxLevels, 0, 2 * sizeof(int), st));
+    RET_IF(p->pcnt.need(sizeof(int) * std::max<int64_t>(ltot, 1)));
+    RET_IF(p->poff.need(sizeof(int) * std::max<int64_t>(ltot, 1)));
+    RET_IF(p->wlist.need(sizeof(int) * std::max<int64_t>(ltot, 1)));
+    RET_IF(p->khist.need(sizeof(int) * nkeys));
+    RET_IF(p->kstart.need(sizeof(int) * nkeys));
+    RET_IF(p->kcur.need(sizeof(int) * nkeys));
+    RET_IF(p->bstart.need(sizeof(int) * nkeys));
+    int *cnt_ex = p->counts.as<int>() + 2 * kMaxLevels;   // [0] written targets, [1] max source
+                                                          // column, [2] pairs, [3] batches
+    CK(cudaMemsetAsync(cnt_ex, 0, 4 * sizeof(int), st));
     if (ns > 0) {   // the largest source column at the leaf level bounds the stations S2L reads
         max_col_kernel<<<nblk(std::min<int64_t>(ns, pow4(d)), 256), 256, 0, st>>>(
-            p->skeys.as<int>() + lvoff[d], p->counts.as<int>() + d, p->counts.as<int>() + 2 * kMaxLevels + 1);
+            p->skeys.as<int>() + lvoff[d], p->counts.as<int>() + d, cnt_ex + 1);
         CKL();
         p->launches++;
     }
-    if (ntiles_all > 0) {
-        TileArgs ta = {};
-        for (int l = 2; l <= d; ++l) {
-            ta.smap[l] = p->smap.as<int>() + lvoff[l];
-            ta.tmap[l] = tmap_b + lvoff[l];
-            ta.lvoff[l] = lvoff[l];
-        }
-        s2l_tile_flags_kernel<<<nblk(ntiles_all * 32, 256), 256, 0, st>>>(
-            ta, s2lgr, s2l_jh(pl), p->tflag.as<int>(), p->written.as<unsigned char>());
-        CKL();
-        CK(cudaMemcpyAsync(p->tpos.p, p->tflag.p, sizeof(int) * ntiles_all, cudaMemcpyDeviceToDevice, st));
-        RET_IF(scan_excl(p, p->tpos.as<int>(), ntiles_all, st));
-        s2l_tile_emit_kernel<<<nblk(ntiles_all, 256), 256, 0, st>>>(
-            p->tflag.as<int>(), p->tpos.as<int>(), ntiles_all, p->tiles.as<int>(),
-            p->counts.as<int>() + 2 * kMaxLevels);
-        CKL();
-        p->launches += 2;
+    S2LListArgs la = {};
+    la.depth = d;
+    for (int l = 2; l <= d; ++l) {
+        la.smap[l] = p->smap.as<int>() + lvoff[l];
+        la.tmap[l] = tmap_b + lvoff[l];
     }
-    int hcnt[2 * kMaxLevels + 2] = {0};
-    CK(cudaMemcpyAsync(hcnt, p->counts.p, sizeof(int) * (2 * kMaxLevels + 2), cudaMemcpyDeviceToHost, st));
+    for (int l = 0; l <= d + 1; ++l) la.lvoff[l] = lvoff[l];
+    la.nkeys = nkeys;
+    la.JT = JT;
+    la.pcnt = p->pcnt.as<int>();
+    la.poff = p->poff.as<int>();
+    la.khist = p->khist.as<int>();
+    la.kstart = p->kstart.as<int>();
+    la.kcur = p->kcur.as<int>();
+    la.bstart = p->bstart.as<int>();
+    la.written = p->written.as<unsigned char>();
+    la.wlist = p->wlist.as<int>();
+    la.wcount = cnt_ex;
+    la.totals = cnt_ex + 2;
+    CK(cudaMemsetAsync(la.khist, 0, sizeof(int) * nkeys, st));
+    CK(cudaMemsetAsync(la.kcur, 0, sizeof(int) * nkeys, st));
+    s2l_count_kernel<<<nblk(ltot, 256), 256, 0, st>>>(la);
+    CKL();
+    s2l_nbatch_kernel<<<nblk(nkeys, 256), 256, 0, st>>>(la);
+    CKL();
+    CK(cudaMemcpyAsync(la.poff, la.pcnt, sizeof(int) * ltot, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(la.kstart, la.khist, sizeof(int) * nkeys, cudaMemcpyDeviceToDevice, st));
+    RET_IF(scan_excl(p, la.poff, ltot, st));
+    RET_IF(scan_excl(p, la.kstart, nkeys, st));
+    RET_IF(scan_excl(p, la.bstart, nkeys, st));
+    s2l_totals_kernel<<<1, 32, 0, st>>>(la);
+    CKL();
+    p->launches += 3;
+    int hcnt[2 * kMaxLevels + 4] = {0};
+    CK(cudaMemcpyAsync(hcnt, p->counts.p, sizeof(int) * (2 * kMaxLevels + 4), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     RET_IF(check_err_flag(p, st));
     if (same)
         for (int l = 0; l < kMaxLevels; ++l) hcnt[kMaxLevels + l] = hcnt[l];
+    // the pair lists, now that their sizes are known
+    const int64_t npairs = hcnt[2 * kMaxLevels + 2], nbatches = hcnt[2 * kMaxLevels + 3];
+    const int nwritten = hcnt[2 * kMaxLevels];
+    RET_IF(p->pairs.need(sizeof(int4) * std::max<int64_t>(npairs, 1)));
+    RET_IF(p->batches.need(sizeof(int4) * std::max<int64_t>(nbatches, 1)));
+    la.pairs = p->pairs.as<int4>();
+    la.batches = p->batches.as<int4>();
+    if (npairs > 0) {
+        s2l_emit_kernel<<<nblk(ltot, 256), 256, 0, st>>>(la);
+        CKL();
+        s2l_batch_emit_kernel<<<nblk(nkeys, 256), 256, 0, st>>>(la);
+        CKL();
+        p->launches += 2;
+    }
     T.mark();  // 1: tree done
     // ---- far-field storage
     FarArgs fa = {};
@@ -1028,8 +980,9 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         // chunk must fit in a third of the free device memory (C5: 1.8 GB per mode).  The free
         // memory is queried only when the current allocations cannot hold all modes (the query
         // is slow; steady-state solves reuse the plan's workspace).
-        size_t per_mode = sizeof(double2) * ((size_t)stot * P + (size_t)ttot * Pl) + sizeof(double) * nstat * TP;
-        size_t have = p->M.cap + p->Lc.cap + p->tens.cap;   // reusable current allocations
+        size_t per_mode = sizeof(double2) * ((size_t)stot * P + (size_t)(ttot + npairs) * Pl) +
+                          sizeof(double) * nstat * TP;
+        size_t have = p->M.cap + p->Lc.cap + p->tens.cap + p->pairbuf.cap;   // reusable allocations
         if (per_mode * (size_t)K > have) {
             size_t fmem = 0, tot = 0;
             CK(cudaMemGetInfo(&fmem, &tot));
@@ -1045,6 +998,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     RET_IF(p->M.need(sizeof(double2) * (size_t)std::max<int64_t>(stot, 1) * KW * P));
     RET_IF(p->Lc.need(sizeof(double2) * (size_t)std::max<int64_t>(ttot, 1) * KW * Pl));
     RET_IF(p->tens.need(sizeof(double) * (size_t)nstat * KW * TP));
+    RET_IF(p->pairbuf.need(sizeof(double2) * (size_t)std::max<int64_t>(npairs, 1) * KW * Pl));
     fa.M = p->M.as<double2>();
     fa.Lc = p->Lc.as<double2>();
     fa.tens = p->tens.as<double>();
@@ -1057,17 +1011,42 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     fa.fz = fz_sorted;
     fa.fperm = fperm;
     fa.out = reinterpret_cast<double2 *>(out_Phi);
-    fa.s2l_pairs = p->ctr.as<unsigned long long>() + 2;
-    fa.s2l_idx = p->s2lidx.as<int>();
     fa.rtab_m = p->rtab.as<double>();
     fa.rtab_l = p->rtab.as<double>() + p->rtab_nm;
     fa.tritab_m = reinterpret_cast<const int *>(p->rtab.as<double>() + p->rtab_nd);
     fa.tritab_l = fa.tritab_m + p->rtab_ntm;
     fa.pscale = p->rtab.as<double>() + p->rtab_nd - (pp + 1) * (pp + 2) / 2;
-    fa.s2l_tiles = p->tiles.as<int>();
     fa.s2l_written = p->written.as<unsigned char>();
     for (int l = 2; l <= d; ++l) fa.lvoff[l] = lvoff[l];
-    const int64_t ntiles_act = hcnt[2 * kMaxLevels];
+    // S2L batch GEMM and reduction arguments (s2l.cuh)
+    S2LArgs sa = {};
+    sa.p = pp;
+    sa.P = P;
+    sa.pl = pl;
+    sa.Pl = Pl;
+    sa.pt = pt;
+    sa.K = K;
+    sa.tens = p->tens.as<double>();
+    sa.M = p->M.as<double2>();
+    sa.pairs = p->pairs.as<int4>();
+    sa.batches = p->batches.as<int4>();
+    for (int l = 2; l <= d; ++l) sa.soff[l] = fa.soff[l];
+    sa.truncation = q.truncation;
+    sa.pairbuf = p->pairbuf.as<double2>();
+    S2LReduceArgs ra = {};
+    ra.depth = d;
+    ra.nw = nwritten;
+    ra.Pl = Pl;
+    for (int l = 0; l <= d + 1; ++l) ra.lvoff[l] = lvoff[l];
+    for (int l = 2; l <= d; ++l) {
+        ra.toff[l] = fa.toff[l];
+        ra.tmap[l] = fa.tmap[l];
+    }
+    ra.wlist = p->wlist.as<int>();
+    ra.poff = p->poff.as<int>();
+    ra.pcnt = p->pcnt.as<int>();
+    ra.pairbuf = sa.pairbuf;
+    ra.Lc = fa.Lc;
     fa.l2p_accumulate = ns > 0;   // L2P adds the far field onto the near field's rows
     fa.outr = grad ? reinterpret_cast<double2 *>(out_dr) : nullptr;
     fa.outz = grad ? reinterpret_cast<double2 *>(out_dz) : nullptr;
@@ -1217,8 +1196,15 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         // S2L of every level in one launch (each level's contribution), then the L2L chain
         tic();
         if (overlap) CK(cudaStreamWaitEvent(st, p->aev[2], 0));   // tensors of this chunk ready
-        if (ns > 0 && ntiles_act > 0) {
-            CK(launch_s2l(fa, ntiles_act, st));
+        if (ns > 0 && npairs > 0) {
+            sa.m0 = fa.m0;
+            sa.m1 = fa.m1;
+            ra.KW = kw;
+            CK(launch_s2l(sa, nbatches, st));
+            const int64_t witems = (int64_t)nwritten * kw;
+            s2l_reduce_kernel<<<(unsigned)std::min<int64_t>((witems + 7) / 8, (int64_t)p->nsm * 16), 256, 0, st>>>(ra);
+            CKL();
+            p->launches++;
             p->launches++;
         }
         if (overlap) CK(cudaEventRecord(p->aev[4], st));
@@ -1273,7 +1259,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         tm->ms_total = ms_total;
         tm->n_skipped = (int64_t)c[0];
         tm->n_near_pairs = (int64_t)c[1];
-        tm->n_s2l_pairs = (int64_t)c[2];
+        tm->n_s2l_pairs = npairs;
         tm->kernel_launches = p->launches;
         RET_IF(check_err_flag(p, st));
     }
