@@ -118,8 +118,11 @@ static cylfmm_status ensure_init()
     CK(allow_smem(p2m_kernel));
     CK(allow_smem(m2m_kernel));
     CK(allow_smem(l2l_kernel));
-    CK(allow_smem(l2p_kernel<false>));
-    CK(allow_smem(l2p_kernel<true>));
+    CK(allow_smem(l2p_kernel<4, false>));
+    CK(allow_smem(l2p_kernel<9, false>));
+    CK(allow_smem(l2p_kernel<13, false>));
+    CK(allow_smem(l2p_kernel<16, false>));
+    CK(allow_smem(l2p_kernel<16, true>));
 #define X(...) CK(allow_smem(s2l_batch_kernel<__VA_ARGS__>));
     S2L_ALL(X)
 #undef X
@@ -441,7 +444,8 @@ struct cylfmm_plan_s {
     DevBuf tasks, ntasks, tcnt, toff;
     DevBuf written;                       // per-box 'local written by S2L' flags
     DevBuf pcnt, poff, khist, kstart, kcur, bstart, pairs, batches, wlist, pairbuf;   // S2L lists
-    DevBuf need;                          // lazy L2L flags
+    DevBuf need, lrow;                    // lazy L2L flags, compact local rows
+    DevBuf l2pown, l2pflag, l2ppos, l2ptask, l2pntask;   // L2P evaluating boxes and tasks
     DevBuf err, ctr;
     DevBuf rtab;     // M2M / L2L recentring tables: [rtab(p) | rtab(pl)] doubles, then tri ints
     size_t rtab_nm = 0, rtab_nd = 0, rtab_ntm = 0;
@@ -469,7 +473,7 @@ static void free_plan_bufs(cylfmm_plan p)
                      &p->scan_tmp[3], &p->sr_s, &p->sz_s, &p->S_s, &p->fr_s, &p->fz_s,
                      &p->slstart, &p->flstart, &p->flags, &p->smap, &p->skeys, &p->tmap,
                      &p->tkeys, &p->counts, &p->M, &p->Lc, &p->tens, &p->seeds, &p->tasks,
-                     &p->ntasks, &p->tcnt, &p->toff, &p->written, &p->pcnt, &p->poff, &p->khist, &p->kstart, &p->kcur, &p->bstart, &p->pairs, &p->batches, &p->wlist, &p->pairbuf, &p->need, &p->err, &p->ctr, &p->rtab, &p->h_sr, &p->h_sz,
+                     &p->ntasks, &p->tcnt, &p->toff, &p->written, &p->pcnt, &p->poff, &p->khist, &p->kstart, &p->kcur, &p->bstart, &p->pairs, &p->batches, &p->wlist, &p->pairbuf, &p->need, &p->lrow, &p->l2pown, &p->l2pflag, &p->l2ppos, &p->l2ptask, &p->l2pntask, &p->err, &p->ctr, &p->rtab, &p->h_sr, &p->h_sz,
                      &p->h_S, &p->h_fr, &p->h_fz, &p->h_out};
     for (DevBuf *b : all) b->release();
 }
@@ -837,7 +841,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     RET_IF(p->skeys.need(sizeof(int) * ltot));
     RET_IF(p->tmap.need(sizeof(int) * ltot));
     RET_IF(p->tkeys.need(sizeof(int) * ltot));
-    RET_IF(p->counts.need(sizeof(int) * (2 * kMaxLevels + 4)));
+    RET_IF(p->counts.need(sizeof(int) * (2 * kMaxLevels + 5)));
     int *tmap_b = same ? p->smap.as<int>() : p->tmap.as<int>();
     int *tkeys_b = same ? p->skeys.as<int>() : p->tkeys.as<int>();
     const int nside = same ? 1 : 2;
@@ -887,8 +891,9 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     RET_IF(p->kcur.need(sizeof(int) * nkeys));
     RET_IF(p->bstart.need(sizeof(int) * nkeys));
     int *cnt_ex = p->counts.as<int>() + 2 * kMaxLevels;   // [0] written targets, [1] max source
-                                                          // column, [2] pairs, [3] batches
-    CK(cudaMemsetAsync(cnt_ex, 0, 4 * sizeof(int), st));
+                                                          // column, [2] pairs, [3] batches,
+                                                          // [4] materialised locals
+    CK(cudaMemsetAsync(cnt_ex, 0, 5 * sizeof(int), st));
     if (ns > 0) {   // the largest source column at the leaf level bounds the stations S2L reads
         max_col_kernel<<<nblk(std::min<int64_t>(ns, pow4(d)), 256), 256, 0, st>>>(
             p->skeys.as<int>() + lvoff[d], p->counts.as<int>() + d, cnt_ex + 1);
@@ -928,8 +933,31 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     s2l_totals_kernel<<<1, 32, 0, st>>>(la);
     CKL();
     p->launches += 3;
-    int hcnt[2 * kMaxLevels + 4] = {0};
-    CK(cudaMemcpyAsync(hcnt, p->counts.p, sizeof(int) * (2 * kMaxLevels + 4), cudaMemcpyDeviceToHost, st));
+    // lazy downward pass: which target locals are materialised (need = written or a child
+    // needs, bottom-up, fmm_ops.cuh); only those get a row of the local storage (compact lrow)
+    RET_IF(p->need.need(std::max<int64_t>(ltot, 1)));
+    RET_IF(p->lrow.need(sizeof(int) * std::max<int64_t>(ltot, 1)));
+    {
+        NeedArgs na = {};
+        na.depth = d;
+        for (int l = 2; l <= d; ++l) na.tmap[l] = tmap_b + lvoff[l];
+        for (int l = 0; l <= d + 1; ++l) na.lvoff[l] = lvoff[l];
+        na.written = la.written;
+        na.need = p->need.as<unsigned char>();
+        na.needi = p->lrow.as<int>();
+        for (int l = d; l >= 2; --l) {
+            need_kernel<<<nblk(pow4(l), 256), 256, 0, st>>>(na, l);
+            CKL();
+            p->launches++;
+        }
+        RET_IF(scan_excl(p, p->lrow.as<int>(), ltot, st));
+        count_total_kernel<<<1, 32, 0, st>>>(p->lrow.as<int>(), p->need.as<unsigned char>(), ltot,
+                                             cnt_ex + 4);
+        CKL();
+        p->launches++;
+    }
+    int hcnt[2 * kMaxLevels + 5] = {0};
+    CK(cudaMemcpyAsync(hcnt, p->counts.p, sizeof(int) * (2 * kMaxLevels + 5), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     RET_IF(check_err_flag(p, st));
     if (same)
@@ -937,6 +965,9 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     // the pair lists, now that their sizes are known
     const int64_t npairs = hcnt[2 * kMaxLevels + 2], nbatches = hcnt[2 * kMaxLevels + 3];
     const int nwritten = hcnt[2 * kMaxLevels];
+    const int64_t nlc = hcnt[2 * kMaxLevels + 4];   // materialised locals (Lc rows)
+    // stations i_in <= the largest source column (C5: 35% of them) are the only ones S2L reads
+    const int64_t nstat_used = ns > 0 ? 12 * std::min<int64_t>(1 << d, hcnt[2 * kMaxLevels + 1] + 1) : 0;
     RET_IF(p->pairs.need(sizeof(int4) * std::max<int64_t>(npairs, 1)));
     RET_IF(p->batches.need(sizeof(int4) * std::max<int64_t>(nbatches, 1)));
     la.pairs = p->pairs.as<int4>();
@@ -980,8 +1011,8 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         // chunk must fit in a third of the free device memory (C5: 1.8 GB per mode).  The free
         // memory is queried only when the current allocations cannot hold all modes (the query
         // is slow; steady-state solves reuse the plan's workspace).
-        size_t per_mode = sizeof(double2) * ((size_t)stot * P + (size_t)(ttot + npairs) * Pl) +
-                          sizeof(double) * nstat * TP;
+        size_t per_mode = sizeof(double2) * ((size_t)stot * P + (size_t)(nlc + npairs) * Pl) +
+                          sizeof(double) * nstat_used * TP;
         size_t have = p->M.cap + p->Lc.cap + p->tens.cap + p->pairbuf.cap;   // reusable allocations
         if (per_mode * (size_t)K > have) {
             size_t fmem = 0, tot = 0;
@@ -996,8 +1027,8 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         }
     }
     RET_IF(p->M.need(sizeof(double2) * (size_t)std::max<int64_t>(stot, 1) * KW * P));
-    RET_IF(p->Lc.need(sizeof(double2) * (size_t)std::max<int64_t>(ttot, 1) * KW * Pl));
-    RET_IF(p->tens.need(sizeof(double) * (size_t)nstat * KW * TP));
+    RET_IF(p->Lc.need(sizeof(double2) * (size_t)std::max<int64_t>(nlc, 1) * KW * Pl));
+    RET_IF(p->tens.need(sizeof(double) * (size_t)std::max<int64_t>(nstat_used, 1) * KW * TP));
     RET_IF(p->pairbuf.need(sizeof(double2) * (size_t)std::max<int64_t>(npairs, 1) * KW * Pl));
     fa.M = p->M.as<double2>();
     fa.Lc = p->Lc.as<double2>();
@@ -1038,16 +1069,19 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     ra.nw = nwritten;
     ra.Pl = Pl;
     for (int l = 0; l <= d + 1; ++l) ra.lvoff[l] = lvoff[l];
-    for (int l = 2; l <= d; ++l) {
-        ra.toff[l] = fa.toff[l];
-        ra.tmap[l] = fa.tmap[l];
-    }
+    ra.lrow = p->lrow.as<int>();
     ra.wlist = p->wlist.as<int>();
     ra.poff = p->poff.as<int>();
     ra.pcnt = p->pcnt.as<int>();
     ra.pairbuf = sa.pairbuf;
     ra.Lc = fa.Lc;
     fa.l2p_accumulate = ns > 0;   // L2P adds the far field onto the near field's rows
+    fa.tfield = nf;
+    RET_IF(p->l2pown.need(sizeof(int) * std::max(hcnt[kMaxLevels + d], 1)));
+    RET_IF(p->l2pflag.need(sizeof(int) * nf));
+    RET_IF(p->l2ppos.need(sizeof(int) * nf));
+    RET_IF(p->l2ptask.need(sizeof(int) * (nf / 16 + hcnt[kMaxLevels + d] + 1)));
+    RET_IF(p->l2pntask.need(sizeof(int)));
     fa.outr = grad ? reinterpret_cast<double2 *>(out_dr) : nullptr;
     fa.outz = grad ? reinterpret_cast<double2 *>(out_dz) : nullptr;
     double ms_tensor = ms_seed, ms_p2m = 0, ms_m2m = 0, ms_s2l = 0, ms_l2l = 0, ms_l2p = 0;
@@ -1062,20 +1096,12 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             acc += ms;
         }
     };
-    // lazy downward pass: which target locals are materialised (need_kernel, bottom-up)
-    RET_IF(p->need.need(std::max<int64_t>(ltot, 1)));
     fa.need = p->need.as<unsigned char>();
-    // tree done: the near field and the need flags start behind it on their own streams (the
-    // need flags on the tensor stream: S2L waits for that stream, L2L runs after S2L)
+    fa.lrow = p->lrow.as<int>();
+    // tree done: the near field starts behind it on its own stream
     if (overlap) {
         CK(cudaEventRecord(p->aev[1], st));
         CK(cudaStreamWaitEvent(st_t, p->aev[1], 0));
-    }
-    for (int l = d; l >= 2; --l) {
-        if (fa.tcount[l] == 0) continue;
-        need_kernel<<<nblk(fa.tcount[l], 256), 256, 0, st_t>>>(fa, l, p->need.as<unsigned char>());
-        CKL();
-        p->launches++;
     }
     // ---- near field: writes every field row (the far field is added by L2P)
     tic();
@@ -1163,7 +1189,6 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             ta.seed_m1 = K;
             if (overlap && m0 > 0) CK(cudaStreamWaitEvent(st_t, p->aev[4], 0));  // previous S2L done
             // stations i_in <= the largest source column (C5: 35% of them) are the only ones read
-            const int64_t nstat_used = ns > 0 ? 12 * std::min<int64_t>(1 << d, hcnt[2 * kMaxLevels + 1] + 1) : 0;
             if (nstat_used > 0) RET_IF(run_fill(ta, nstat_used, st_t));
             p->launches++;
             if (overlap) CK(cudaEventRecord(p->aev[2], st_t));
@@ -1173,7 +1198,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             tic();
             if (fa.scount[d] > 0) {
                 const int nmb = (kw + kP2MModes - 1) / kP2MModes;
-                p2m_kernel<<<(unsigned)((int64_t)fa.scount[d] * nmb), kP2MThreads, p2m_smem(P), st>>>(fa);
+                p2m_kernel<<<(unsigned)((int64_t)fa.scount[d] * nmb), kP2MThreads, p2m_smem(P, pp), st>>>(fa);
                 CKL();
                 p->launches++;
             }
@@ -1223,18 +1248,42 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         tic();
         if (overlap && ns > 0 && m0 == 0) CK(cudaStreamWaitEvent(st, p->aev[3], 0));  // near field
         {
-            int ngrp = (kw + kL2PModes - 1) / kL2PModes;
-            size_t sm = sizeof(double2) * kL2PModes * Pl + sizeof(double) * kL2PPts * Pl * (grad ? 3 : 1);
-            // leaves per CTA: one when the leaves hold >= kL2PPts points on average (C2-C4), up to
-            // 64 when they are many and small (C5: 1M leaves of 4 points), so that a CTA reuses the
-            // evaluating box's local over a run of leaves
+            // tasks: runs of <= TP sorted field points sharing their evaluating box; TP from the
+            // points per target leaf (C5's leaves hold 4 points but share coarse boxes: 128)
             const int ntl = fa.tcount[d];
-            fa.l2p_lc = nf >= (int64_t)kL2PPts * ntl
-                            ? 1
-                            : (int)std::min<int64_t>(64, std::max<int64_t>(1, ntl / ((int64_t)p->nsm * 8)));
-            const int64_t nch = (ntl + fa.l2p_lc - 1) / fa.l2p_lc;
-            if (grad) l2p_kernel<true><<<(unsigned)(nch * ngrp), 256, sm, st>>>(fa);
-            else l2p_kernel<false><<<(unsigned)(nch * ngrp), 256, sm, st>>>(fa);
+            const int64_t ppl = nf / std::max(ntl, 1);
+            fa.l2p_tp = ppl < 8 ? 128 : (int)std::min<int64_t>(128, std::max<int64_t>(16, (int64_t)1 << (63 - __builtin_clzll(ppl))));
+            const int gpc = kL2PThreads / fa.l2p_tp;
+            const int64_t ub_tasks = nf / fa.l2p_tp + ntl + 1;
+            if (m0 == 0) {   // evaluating box of every target leaf (written flags are per solve)
+                l2p_owner_kernel<<<nblk(ntl, 256), 256, 0, st>>>(fa, p->l2pown.as<int>());
+                CKL();
+                int *flag = p->l2pflag.as<int>(), *pos = p->l2ppos.as<int>();
+                l2p_task_flags_kernel<<<nblk(nf, 256), 256, 0, st>>>(fa, fkey_s, p->l2pown.as<int>(), flag);
+                CKL();
+                CK(cudaMemcpyAsync(pos, flag, sizeof(int) * nf, cudaMemcpyDeviceToDevice, st));
+                RET_IF(scan_excl(p, pos, nf, st));
+                l2p_task_emit_kernel<<<nblk(nf, 256), 256, 0, st>>>(nf, flag, pos, p->l2ptask.as<int>());
+                CKL();
+                l2p_ntasks_kernel<<<1, 32, 0, st>>>(pos, flag, nf, p->l2pntask.as<int>());
+                CKL();
+                p->launches += 5;
+            }
+            // modes per thread: the groups of a task fill the CTA (gpc groups per item)
+            int ngrp = (kw + 15) / 16;
+            if (gpc > 1) ngrp = std::max(ngrp, std::min(kw, gpc * ((ngrp + gpc - 1) / gpc)));
+            const int mb = (kw + ngrp - 1) / ngrp;
+            const int64_t items = ub_tasks * ((ngrp + gpc - 1) / gpc);
+            // persistent CTAs over the items (the task count stays on the device)
+            const unsigned grid = (unsigned)std::min<int64_t>(items, (int64_t)p->nsm * 16);
+            const uint32_t *fk = fkey_s;
+            const int *own = p->l2pown.as<int>(), *tst = p->l2ptask.as<int>(), *ntk = p->l2pntask.as<int>();
+            const int tp = fa.l2p_tp;
+            if (grad) l2p_kernel<16, true><<<grid, kL2PThreads, l2p_smem<16>(Pl, kw, tp), st>>>(fa, fk, own, tst, ntk, ngrp);
+            else if (mb <= 4) l2p_kernel<4, false><<<grid, kL2PThreads, l2p_smem<4>(Pl, kw, tp), st>>>(fa, fk, own, tst, ntk, ngrp);
+            else if (mb <= 9) l2p_kernel<9, false><<<grid, kL2PThreads, l2p_smem<9>(Pl, kw, tp), st>>>(fa, fk, own, tst, ntk, ngrp);
+            else if (mb <= 13) l2p_kernel<13, false><<<grid, kL2PThreads, l2p_smem<13>(Pl, kw, tp), st>>>(fa, fk, own, tst, ntk, ngrp);
+            else l2p_kernel<16, false><<<grid, kL2PThreads, l2p_smem<16>(Pl, kw, tp), st>>>(fa, fk, own, tst, ntk, ngrp);
             CKL();
             p->launches++;
         }

@@ -35,7 +35,7 @@ struct FarArgs {
     int scount[kMaxLevels], tcount[kMaxLevels];
     int64_t soff[kMaxLevels], toff[kMaxLevels];  // box offsets into M / Lc
     double2 *M;          // moments  [box][KW][P]
-    double2 *Lc;         // locals   [box][KW][P]
+    double2 *Lc;         // locals   [materialised box (lrow)][KW][Pl]
     const int *slstart, *flstart;
     const double *sr, *sz;
     const double2 *S;    // sorted sources [ns][K]
@@ -46,8 +46,10 @@ struct FarArgs {
     const unsigned char *s2l_written;   // dense per level [lvoff[l] + key]: local written by S2L
     int64_t lvoff[kMaxLevels];          // dense per-level offsets (level maps, s2l_written)
     const unsigned char *need;          // dense per level: local materialised (see need_kernel)
+    const int *lrow;                    // dense per level: Lc row of a materialised local
     int l2p_accumulate;                 // L2P adds onto out (the near field wrote it first)
-    int l2p_lc;                         // L2P: consecutive target leaves per CTA (>= 1)
+    int64_t tfield;                     // field points (L2P)
+    int l2p_tp;                         // L2P task size (points)
     // recentring tables (host-built once per plan, recentre_tables_host): [cm | cl] 4 (p+1)^2
     // doubles and [tri_i | tri_j] 2 P ints, for the source order (M2M) and the local order (L2L)
     const double *rtab_m, *rtab_l;
@@ -93,6 +95,15 @@ __global__ void __launch_bounds__(kP2MThreads) p2m_kernel(FarArgs a)
     const int nm = min(kP2MModes, KW - n0);
     double *mono = sm;                                                  // [kP2MSrc][P]
     double2 *Sx = reinterpret_cast<double2 *>(mono + kP2MSrc * P);      // [kP2MSrc][kP2MModes]
+    double *pw = reinterpret_cast<double *>(Sx + kP2MSrc * kP2MModes);  // [kP2MSrc][2][p+1]
+    int *mi = reinterpret_cast<int *>(pw + kP2MSrc * 2 * (p + 1));      // [P] i, then [P] j
+    int *mj = mi + P;
+    for (int c = threadIdx.x; c < P; c += kP2MThreads) {
+        int i = 0;
+        while (i < p && c >= (i + 1) * (p + 1) - (i + 1) * i / 2) ++i;
+        mi[c] = i;
+        mj[c] = c - (i * (p + 1) - i * (i - 1) / 2);
+    }
     const uint32_t key = (uint32_t)a.skeys[d][slot];
     double rc, zc, h;
     box_centre(key, d, a.L, a.z0, rc, zc, h);
@@ -109,18 +120,24 @@ __global__ void __launch_bounds__(kP2MThreads) p2m_kernel(FarArgs a)
     for (int s0 = q0; s0 < q1; s0 += kP2MSrc) {
         const int nc = min(kP2MSrc, q1 - s0);
         __syncthreads();
-        if (threadIdx.x < nc) {
-            const int q = s0 + threadIdx.x;
-            const double dr = (a.sr[q] - rc) * inv_h, dz = (a.sz[q] - zc) * inv_h;
-            double pr = 1.0;
-            for (int i = 0; i <= p; ++i) {
-                double pz = pr;
-                for (int j = 0; i + j <= p; ++j) {
-                    mono[threadIdx.x * P + tri(i, j, p)] = pz;
-                    pz *= dz;
+        // powers dr^i, dz^j of every source of the chunk, one thread per (source, axis)
+        if (threadIdx.x < 2 * kP2MSrc) {
+            const int qq = threadIdx.x >> 1, ax = threadIdx.x & 1;
+            if (qq < nc) {
+                const int q = s0 + qq;
+                const double v = ax ? (a.sz[q] - zc) * inv_h : (a.sr[q] - rc) * inv_h;
+                double pv = 1.0;
+                for (int i = 0; i <= p; ++i) {
+                    pw[(qq * 2 + ax) * (p + 1) + i] = pv;
+                    pv *= v;
                 }
-                pr *= dr;
             }
+        }
+        __syncthreads();
+        // monomials dr^i dz^j, all threads
+        for (int e = threadIdx.x; e < nc * P; e += kP2MThreads) {
+            const int qq = e / P, c = e - qq * P;
+            mono[qq * P + c] = pw[(qq * 2) * (p + 1) + mi[c]] * pw[(qq * 2 + 1) * (p + 1) + mj[c]];
         }
         // coefficient rows by asynchronous copies (in flight while the monomials are formed)
         for (int e = threadIdx.x; e < nc * kP2MModes; e += kP2MThreads) {
@@ -158,9 +175,10 @@ __global__ void __launch_bounds__(kP2MThreads) p2m_kernel(FarArgs a)
     }
 }
 
-inline size_t p2m_smem(int P)
+inline size_t p2m_smem(int P, int p)
 {
-    return sizeof(double) * kP2MSrc * P + sizeof(double2) * kP2MSrc * kP2MModes;
+    return sizeof(double) * kP2MSrc * P + sizeof(double2) * kP2MSrc * kP2MModes +
+           sizeof(double) * kP2MSrc * 2 * (p + 1) + sizeof(int) * 2 * P;
 }
 
 // binomial C(n, k) for n <= 2 * 20 (exact in FP64)
@@ -288,18 +306,29 @@ __global__ void __launch_bounds__(256) m2m_kernel(FarArgs a, int level)
 // re-centred local of its nearest materialised ancestor (L2L is an exact re-centring of a
 // degree-p polynomial), and L2P evaluates that ancestor's local directly.  Uniform
 // inputs (C2, C3) need every box; surface inputs (C5) skip L2L for most of the 700k boxes.
-__global__ void need_kernel(FarArgs a, int level, unsigned char *need)
+// Dense form (thread per position of the level, before the host knows the level counts):
+// need[g] for g = lvoff[l] + key, and needi[g] = need as int (scanned into the compact Lc row).
+struct NeedArgs {
+    int depth;
+    const int *tmap[kMaxLevels];
+    int64_t lvoff[kMaxLevels + 1];
+    const unsigned char *written;
+    unsigned char *need;
+    int *needi;
+};
+__global__ void need_kernel(NeedArgs a, int level)
 {
-    int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= a.tcount[level]) return;
-    const uint32_t key = (uint32_t)a.tkeys[level][s];
-    bool nd = a.s2l_written[a.lvoff[level] + key] != 0;
-    if (level < a.depth)
-        for (int c = 0; c < 4 && !nd; ++c) {
-            const uint32_t ck = 4 * key + c;
-            nd = a.tmap[level + 1][ck] >= 0 && need[a.lvoff[level + 1] + ck] != 0;
-        }
-    need[a.lvoff[level] + key] = nd ? 1 : 0;
+    const int64_t key = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (key >= ((int64_t)1 << (2 * level))) return;
+    const int64_t g = a.lvoff[level] + key;
+    bool nd = false;
+    if (a.tmap[level][key] >= 0) {
+        nd = a.written[g] != 0;
+        if (level < a.depth)
+            for (int c = 0; c < 4 && !nd; ++c) nd = a.need[a.lvoff[level + 1] + 4 * key + c] != 0;
+    }
+    a.need[g] = nd ? 1 : 0;
+    a.needi[g] = nd ? 1 : 0;
 }
 
 // L2L, one warp per (child box, mode), grid-stride over the level's target boxes; separable
@@ -327,7 +356,7 @@ __global__ void __launch_bounds__(32 * kL2LWarps) l2l_kernel(FarArgs a, int leve
         const int sr = key & 1, sz = (key >> 1) & 1;
         const bool child_w = a.s2l_written[a.lvoff[level] + key] != 0;
         const bool par_ok = level - 1 > 2 || a.s2l_written[a.lvoff[level - 1] + (key >> 2)] != 0;
-        const double2 *pg = a.Lc + ((a.toff[level - 1] + ps) * (int64_t)KW + n) * P;
+        const double2 *pg = a.Lc + ((int64_t)a.lrow[a.lvoff[level - 1] + (key >> 2)] * KW + n) * P;
         for (int e = lane; e < P; e += 32) par[e] = par_ok ? pg[e] : make_double2(0.0, 0.0);
         __syncwarp();
         for (int e = lane; e < P; e += 32) {
@@ -342,7 +371,7 @@ __global__ void __launch_bounds__(32 * kL2LWarps) l2l_kernel(FarArgs a, int leve
             T[e] = acc;
         }
         __syncwarp();
-        double2 *o = a.Lc + ((a.toff[level] + slot) * (int64_t)KW + n) * P;
+        double2 *o = a.Lc + ((int64_t)a.lrow[a.lvoff[level] + key] * KW + n) * P;
         for (int e = lane; e < P; e += 32) {
             const int i = tri_i[e], j = tri_j[e];
             const double *co = cl + (sz * P1 + j) * P1;
@@ -372,133 +401,210 @@ inline size_t m2m_smem(int p)
     return sizeof(double) * 4 * (p + 1) * (p + 1) + sizeof(double2) * 8 * kMMG * P + sizeof(int) * 2 * P;
 }
 
-// ---------------------------------------------------------------------------------------------
-// L2P at the leaves: CTA per (target leaf, mode group of <= 16); writes out rows (input order).
-constexpr int kL2PModes = 16;
-constexpr int kL2PPts = 16;
+// one-shot TMA bulk copy on an mbarrier (L2P local staging)
+__device__ __forceinline__ void l2p_mbar_init(uint64_t *bar)
+{
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(b));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+// generic-proxy reads of a buffer (previous item) before an async-proxy (TMA) write to it
+__device__ __forceinline__ void l2p_fence_proxy()
+{
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void l2p_bulk(void *dst, const void *src, unsigned bytes, uint64_t *bar)
+{
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(dst)),
+                 "l"(src), "r"(bytes), "r"(b)
+                 : "memory");
+}
+__device__ __forceinline__ void l2p_mbar_wait(uint64_t *bar, unsigned phase)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(phase)
+        : "memory");
+}
 
-// GRAD: also d/dr and d/dz of the local polynomial from the derivative
-// monomials k dr^(k-1) dz^l and l dr^k dz^(l-1) (normalised units: an extra 1/h).
-template <bool GRAD>
-__global__ void __launch_bounds__(256) l2p_kernel(FarArgs a)
+// ---------------------------------------------------------------------------------------------
+// L2P at the leaves: Phi^(n)(r, z) += sum_{k+l<=p} Phi_kl (r - r_c)^k (z - z_c)^l.
+// The local evaluated is that of the deepest ancestor (or the leaf itself) whose local was
+// written by S2L: below it the chain adds nothing, so the leaf's local is that box's local
+// re-centred (exact) and is evaluated directly.  Written boxes are always
+// materialised (need_kernel), and the choice depends only on the leaf's own chain, so results
+// do not depend on the other field points.  None written: the far field is zero.
+// owner[s] for target leaf slot s: (level << 24) | Lc row of the evaluating box, or -1.
+__global__ void l2p_owner_kernel(FarArgs a, int *owner)
+{
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    const int d = a.depth;
+    if (s >= a.tcount[d]) return;
+    int la = d;
+    uint32_t ka = (uint32_t)a.tkeys[d][s];
+    while (la >= 2 && !a.s2l_written[a.lvoff[la] + ka]) {
+        --la;
+        ka >>= 2;
+    }
+    owner[s] = la < 2 ? -1 : (la << 24) | a.lrow[a.lvoff[la] + ka];
+}
+
+// L2P tasks: runs of <= TP consecutive sorted field points with the same evaluating box (a task
+// starts where the owner changes or at a multiple of TP; TP = a.l2p_tp in {16, 32, 64, 128}).
+// C5: 4M points in ~15k runs, most of them hundreds of points under a coarse written box;
+// C2 / C3: leaves of ~16 points, each its own evaluating box.
+constexpr int kL2PThreads = 128;
+__device__ __forceinline__ int point_owner(const FarArgs &a, const uint32_t *fkey, const int *owner,
+                                           int64_t t)
+{
+    return owner[a.tmap[a.depth][fkey[t]]];
+}
+__global__ void l2p_task_flags_kernel(FarArgs a, const uint32_t *fkey, const int *owner, int *flag)
+{
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= a.tfield) return;
+    flag[t] = (t % a.l2p_tp == 0 || point_owner(a, fkey, owner, t) != point_owner(a, fkey, owner, t - 1)) ? 1 : 0;
+}
+__global__ void l2p_task_emit_kernel(int64_t nf, const int *flag, const int *pos, int *tstart)
+{
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < nf && flag[t]) tstart[pos[t]] = (int)t;
+}
+
+// CTA item = (task, gpc = 128 / TP consecutive groups of <= MB modes): the evaluating box's
+// local (the groups' modes, one contiguous block of the compact local storage) arrives by one TMA
+// bulk copy; thread = (field point, mode group), monomials (r - r_c)^k (z - z_c)^l / h^(k+l)
+// generated in registers in the coefficient order (k-major), the local's coefficients read as
+// shared-memory broadcasts (the points of a task evaluate the same box): MB vector loads for
+// 2 MB DFMA per coefficient.  GRAD: also d/dr and d/dz of the local polynomial (SURVEY 8(f)
+// item 3), from k dr^(k-1) dz^l and l dr^k dz^(l-1).
+template <int MB, bool GRAD>
+__global__ void __launch_bounds__(kL2PThreads) l2p_kernel(FarArgs a, const uint32_t *fkey, const int *owner,
+                                                          const int *tstart, const int *ntasks, int ngrp)
 {
     extern __shared__ double sm[];
     const int p = a.pl, P = a.Pl, KW = a.m1 - a.m0, d = a.depth;   // local order
-    const int ngrp = (KW + kL2PModes - 1) / kL2PModes;
-    const int chunk = blockIdx.x / ngrp, g = blockIdx.x % ngrp;
-    const int n0 = g * kL2PModes, nm = min(kL2PModes, KW - n0);
-    double2 *loc = reinterpret_cast<double2 *>(sm);     // [nm][P]
-    double *mono = reinterpret_cast<double *>(loc + kL2PModes * P);  // [pts][P]
-    double *monr = mono + kL2PPts * P, *monz = monr + kL2PPts * P;   // GRAD: derivative monomials
-    // a CTA takes l2p_lc consecutive target leaves (Morton order, so their field points are one
-    // contiguous sorted range) and walks them in runs that share the evaluating box: the local is
-    // loaded once per run (C5: leaves of 4 points under coarse boxes)
-    const int nleaf = a.tcount[d];
-    const int l0 = chunk * a.l2p_lc, l1 = min(nleaf, l0 + a.l2p_lc);
-    // the deepest ancestor (or the leaf) that received an S2L contribution: below it the chain
-    // adds nothing, so the leaf's local is that box's local re-centred (exact) and is
-    // evaluated directly.  Written boxes are always materialised (need_kernel), and the choice
-    // depends only on the leaf's own chain, so results do not depend on the other field points
-    // (a field-partitioned multi-GPU solve is bitwise identical to the 1-GPU one).  None: zero.
-    auto owner = [&](int leaf, int &la, uint32_t &ka) {
-        la = d;
-        ka = (uint32_t)a.tkeys[d][leaf];
-        while (la >= 2 && !a.s2l_written[a.lvoff[la] + ka]) {
-            --la;
-            ka >>= 2;
+    const int TP = a.l2p_tp, gpc = kL2PThreads / TP;
+    const int ngi = (ngrp + gpc - 1) / gpc;                          // CTA items per task
+    double2 *loc = reinterpret_cast<double2 *>(sm);                 // [staged modes][Pl]
+    uint64_t *bar = reinterpret_cast<uint64_t *>(loc + (size_t)min(KW, gpc * MB) * P);
+    const int nt = *ntasks;
+    if (threadIdx.x == 0) l2p_mbar_init(bar);
+    __syncthreads();
+    unsigned phase = 0;
+    const int ip = threadIdx.x % TP, jg = threadIdx.x / TP;
+    // persistent CTAs over (task, group block) items
+    for (int64_t item = blockIdx.x; item < (int64_t)nt * ngi; item += gridDim.x) {
+    const int task = (int)(item / ngi), G0 = (int)(item - (int64_t)task * ngi) * gpc;
+    const int nG = min(gpc, ngrp - G0);
+    const int64_t t0 = tstart[task], t1 = task + 1 < nt ? tstart[task + 1] : a.tfield;
+    const int nA = (KW * G0) / ngrp, nB = (KW * (G0 + nG)) / ngrp;    // staged modes [nA, nB)
+    const int g = G0 + jg;
+    const int n0 = (KW * g) / ngrp, nm = jg < nG ? (KW * (g + 1)) / ngrp - n0 : 0;   // <= MB
+    const int own = point_owner(a, fkey, owner, t0);
+    const int64_t t = t0 + ip;
+    double inv_h = 0.0, dr = 0.0, dz = 0.0;
+    if (own >= 0) {
+        if (threadIdx.x == 0) {
+            l2p_fence_proxy();
+            l2p_bulk(loc, a.Lc + ((int64_t)(own & 0xffffff) * KW + nA) * P, (unsigned)((nB - nA) * P * 16), bar);
         }
-        if (la < 2) la = -1;                            // nothing written: zero local
-    };
-    for (int li = l0; li < l1;) {
-    int la;
-    uint32_t ka;
-    owner(li, la, ka);
-    int lj = li + 1;
-    for (; lj < l1; ++lj) {
-        int lb;
-        uint32_t kb;
-        owner(lj, lb, kb);
-        if (lb != la || (la >= 2 && kb != ka)) break;
+        const int la = own >> 24;
+        double rc, zc, h;
+        box_centre(fkey[t0] >> (2 * (d - la)), la, a.L, a.z0, rc, zc, h);
+        inv_h = 1.0 / h;
+        if (t < t1) {
+            dr = (a.fr[t] - rc) * inv_h;
+            dz = (a.fz[t] - zc) * inv_h;
+        }
+        l2p_mbar_wait(bar, phase);
+        phase ^= 1u;
     }
-    const uint32_t key = (uint32_t)a.tkeys[d][li], keyl = (uint32_t)a.tkeys[d][lj - 1];
-    const int t0 = a.flstart[key], t1 = a.flstart[keyl + 1];
-    const bool ok = la >= 2;
-    if (!ok) {
-        la = 2;
-        ka = key >> (2 * (d - 2));
+    const double2 *lg = loc + (size_t)(n0 - nA) * P;
+    if (t < t1 && nm > 0) {
+    const int64_t row = a.fperm[t];
+    double2 acc[MB], accr[GRAD ? MB : 1], accz[GRAD ? MB : 1];
+#pragma unroll
+    for (int m = 0; m < MB; ++m) acc[m] = make_double2(0.0, 0.0);
+    if (GRAD) {
+#pragma unroll
+        for (int m = 0; m < MB; ++m) accr[GRAD ? m : 0] = accz[GRAD ? m : 0] = make_double2(0.0, 0.0);
     }
-    double rc, zc, h;
-    box_centre(ka, la, a.L, a.z0, rc, zc, h);
-    const double inv_h = 1.0 / h;
-    const int64_t aslot = ok ? a.tmap[la][ka] : 0;
-    __syncthreads();                                    // the previous run is done with loc
-    for (int e = threadIdx.x; e < nm * P; e += blockDim.x)
-        loc[e] = ok ? a.Lc[((a.toff[la] + aslot) * (int64_t)KW + n0) * P + e] : make_double2(0.0, 0.0);
-    for (int c0 = t0; c0 < t1; c0 += kL2PPts) {
-        const int nc = min(kL2PPts, t1 - c0);
-        __syncthreads();
-        if (threadIdx.x < nc) {
-            int t = c0 + threadIdx.x;
-            double dr = (a.fr[t] - rc) / h, dz = (a.fz[t] - zc) / h;
-            double pr = 1.0, prm = 0.0;   // dr^i and i dr^(i-1)
-            for (int i = 0; i <= p; ++i) {
-                double pz = pr, pzm = 0.0, pzr = prm;   // dr^i dz^j, j dr^i dz^(j-1), i dr^(i-1) dz^j
-                for (int j = 0; i + j <= p; ++j) {
-                    mono[threadIdx.x * P + tri(i, j, p)] = pz;
-                    if (GRAD) {
-                        monr[threadIdx.x * P + tri(i, j, p)] = pzr;
-                        monz[threadIdx.x * P + tri(i, j, p)] = pzm;
+    if (own >= 0) {
+        double pr = 1.0, prm = 0.0;   // dr^k and k dr^(k-1)
+        int q = 0;
+        for (int k = 0; k <= p; ++k) {
+            double pz = pr, pzr = prm, pzm = 0.0;   // dr^k dz^l, k dr^(k-1) dz^l, l dr^k dz^(l-1)
+            for (int l = 0; k + l <= p; ++l, ++q) {
+#pragma unroll
+                for (int m = 0; m < MB; ++m) {
+                    if (m < nm) {
+                        const double2 c = lg[m * P + q];
+                        acc[m].x = fma(c.x, pz, acc[m].x);
+                        acc[m].y = fma(c.y, pz, acc[m].y);
+                        if (GRAD) {
+                            accr[GRAD ? m : 0].x = fma(c.x, pzr, accr[GRAD ? m : 0].x);
+                            accr[GRAD ? m : 0].y = fma(c.y, pzr, accr[GRAD ? m : 0].y);
+                            accz[GRAD ? m : 0].x = fma(c.x, pzm, accz[GRAD ? m : 0].x);
+                            accz[GRAD ? m : 0].y = fma(c.y, pzm, accz[GRAD ? m : 0].y);
+                        }
                     }
-                    pzm = (j + 1) * pz;
-                    pz *= dz;
+                }
+                if (GRAD) {
+                    pzm = (l + 1) * pz;
                     pzr *= dz;
                 }
-                prm = (i + 1) * pr;
-                pr *= dr;
+                pz *= dz;
             }
+            if (GRAD) prm = (k + 1) * pr;
+            pr *= dr;
         }
-        __syncthreads();
-        for (int e = threadIdx.x; e < nc * nm; e += blockDim.x) {
-            int t = e / nm, n = e % nm;
-            const double *mo = mono + t * P;
-            const double2 *lo = loc + n * P;
-            double sx = 0.0, sy = 0.0;
-            for (int kl = 0; kl < P; ++kl) {
-                sx = fma(lo[kl].x, mo[kl], sx);
-                sy = fma(lo[kl].y, mo[kl], sy);
-            }
-            int64_t row = a.fperm[c0 + t];
-            if (GRAD) {
-                const double *mr = monr + t * P, *mz = monz + t * P;
-                double rx = 0.0, ry = 0.0, zx = 0.0, zy = 0.0;
-                for (int kl = 0; kl < P; ++kl) {
-                    rx = fma(lo[kl].x, mr[kl], rx);
-                    ry = fma(lo[kl].y, mr[kl], ry);
-                    zx = fma(lo[kl].x, mz[kl], zx);
-                    zy = fma(lo[kl].y, mz[kl], zy);
-                }
-                const double s2 = inv_h * inv_h;
-                double2 *orr = a.outr + row * a.K + a.m0 + n0 + n, *oz = a.outz + row * a.K + a.m0 + n0 + n;
-                if (a.l2p_accumulate) {
-                    const double2 cr = *orr, cz = *oz;
-                    *orr = make_double2(fma(rx, s2, cr.x), fma(ry, s2, cr.y));
-                    *oz = make_double2(fma(zx, s2, cz.x), fma(zy, s2, cz.y));
-                } else {
-                    *orr = make_double2(rx * s2, ry * s2);
-                    *oz = make_double2(zx * s2, zy * s2);
-                }
-            }
-            double2 *o = a.out + row * a.K + a.m0 + n0 + n;
+    }
+    // (the normalised local is h^(1+k+l) Phi_kl: divide by h once; gradients by h^2)
+    double2 *o = a.out + row * a.K + a.m0 + n0;
+#pragma unroll
+    for (int m = 0; m < MB; ++m) {
+        if (m >= nm) break;
+        double2 v = make_double2(acc[m].x * inv_h, acc[m].y * inv_h);
+        if (a.l2p_accumulate) {
+            const double2 cur = o[m];
+            v = make_double2(fma(acc[m].x, inv_h, cur.x), fma(acc[m].y, inv_h, cur.y));
+        }
+        o[m] = v;
+    }
+    if (GRAD) {
+        const double s2 = inv_h * inv_h;
+        double2 *orr = a.outr + row * a.K + a.m0 + n0, *oz = a.outz + row * a.K + a.m0 + n0;
+#pragma unroll
+        for (int m = 0; m < MB; ++m) {
+            if (m >= nm) break;
+            const double2 ar = accr[GRAD ? m : 0], az = accz[GRAD ? m : 0];
             if (a.l2p_accumulate) {
-                const double2 cur = *o;
-                *o = make_double2(fma(sx, inv_h, cur.x), fma(sy, inv_h, cur.y));
+                const double2 cr = orr[m], cz = oz[m];
+                orr[m] = make_double2(fma(ar.x, s2, cr.x), fma(ar.y, s2, cr.y));
+                oz[m] = make_double2(fma(az.x, s2, cz.x), fma(az.y, s2, cz.y));
             } else {
-                *o = make_double2(sx * inv_h, sy * inv_h);
+                orr[m] = make_double2(ar.x * s2, ar.y * s2);
+                oz[m] = make_double2(az.x * s2, az.y * s2);
             }
         }
     }
-    li = lj;
-    }   // runs
+    }
+    __syncthreads();   // every thread is done with loc before the next item's copy
+    }
+}
+template <int MB>
+inline size_t l2p_smem(int Pl, int KW, int TP)
+{
+    const int gpc = kL2PThreads / TP;
+    return sizeof(double2) * (size_t)std::min(KW, gpc * MB) * Pl + 2 * sizeof(uint64_t);
 }
 
 // Near-field task list: one task per tile of <= TT field points of a non-empty target leaf.

@@ -364,8 +364,8 @@ inline size_t s2l_smem_bytes(int p, int pl)
 // fixed offset order, of their pair-buffer rows
 struct S2LReduceArgs {
     int depth, nw, KW, Pl;
-    int64_t lvoff[kMaxLevels + 1], toff[kMaxLevels];
-    const int *tmap[kMaxLevels];
+    int64_t lvoff[kMaxLevels + 1];
+    const int *lrow;   // dense: Lc row of a materialised local
     const int *wlist, *poff, *pcnt;
     const double2 *pairbuf;
     double2 *Lc;
@@ -377,8 +377,7 @@ __global__ void __launch_bounds__(256) s2l_reduce_kernel(S2LReduceArgs a)
     for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < items;
          it += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int g = a.wlist[it / KW], n = (int)(it % KW);
-        const int l = dense_level(a.lvoff, a.depth, g);
-        const int64_t row = a.toff[l] + a.tmap[l][g - a.lvoff[l]];
+        const int64_t row = a.lrow[g];
         const int o = a.poff[g], c = a.pcnt[g];
         for (int e = lane; e < Pl; e += 32) {
             double2 s = a.pairbuf[((int64_t)o * KW + n) * Pl + e];

@@ -203,6 +203,18 @@ __global__ void level_map_kernel(const int *lstart, int depth, int level, const 
 }
 
 // largest radial box index among the non-empty boxes of a level (stations beyond it are unused)
+// out = scan[n-1] + flag[n-1] (the total of an exclusive scan of 0/1 flags)
+__global__ void count_total_kernel(const int *scan, const unsigned char *flag, int64_t n, int *out)
+{
+    if (threadIdx.x == 0) *out = n > 0 ? scan[n - 1] + (flag[n - 1] ? 1 : 0) : 0;
+}
+
+// *out = scan[n-1] + flag[n-1] for int flags
+__global__ void l2p_ntasks_kernel(const int *scan, const int *flag, int64_t n, int *out)
+{
+    if (threadIdx.x == 0) *out = n > 0 ? scan[n - 1] + flag[n - 1] : 0;
+}
+
 __global__ void max_col_kernel(const int *keys, const int *count, int *out)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
