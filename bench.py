@@ -1,14 +1,17 @@
 #!/usr/bin/env python
 """bench.py -- the hot path of arXiv 2301.01179 on B200: one step = one full FMM solve
-(Algorithm 1: tree, P2M, M2M, tensors, S2L, L2L, L2P, near field) of BASELINE.json
-configs[1] (C2: N = M = 16,384 rings uniform in (0,1]x[0,1], modes n = 0..16, complex N(0,1)
-coefficients, p = 8, leaf size <= 32 -> depth 5, fields = sources with the self term excluded).
+(Algorithm 1: tree, P2M, M2M, tensors, S2L, L2L, L2P, near field) of the largest
+single-GPU BASELINE.json configuration, configs[4] (C5: N = M = 4,194,304; sources uniform in arc
+length on a torus and a sphere generating curve, fields on a 2048 x 2048 grid of (0,1] x [0,2],
+modes n = 0..64, complex N(0,1) coefficients, p = 16, depth 10).  --config C2..C4 run the
+smaller configurations (parity-test cases; C2 = configs[1] is the small FMM case).
 
 Metric (BASELINE.json): FP64 modal source-field interactions per second, i.e. the
 direct-equivalent rate (N_s N_f - skipped) K / t_solve, plus the solve time and the FP64
-roofline fraction of the dominant kernel.
+roofline fraction of the dominant kernel (per-phase CUDA events recorded by the library on the
+streams the phases run on, inside the timed region: cylfmm_plan_set_profiling).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {cylfmm,reference}] [--config C2]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {cylfmm,reference}] [--config C5]
 
 --impl reference times the CPU oracle (oracle/, plain FP64 C, OpenMP) as it stands on the host
 cores -- this tier's reference arm (there is no reference implementation to install).
@@ -109,28 +112,47 @@ def n_interactions(pr, skipped):
     return (len(pr.sr) * len(pr.fr) - skipped) * pr.K
 
 
+def oracle_sample(pr, budget_s, cores):
+    """Time the oracle FMM (all sources; upward pass in full) on a seeded sample of the field
+    points sized so that one run takes about budget_s on this host.  Returns (m, seconds,
+    skipped, sample indices)."""
+    import oracle
+    oracle.build()
+    nf = len(pr.fr)
+    order = np.random.default_rng(1234).permutation(nf)
+
+    def run(m):
+        idx = np.sort(order[:m])
+        t0 = time.perf_counter()
+        _, sk = oracle.fmm(pr.sr, pr.sz, pr.S, pr.fr[idx], pr.fz[idx], pr.p, pr.depth, pr.L,
+                           pr.z0, nthreads=cores)
+        return time.perf_counter() - t0, sk, idx
+
+    m0, m1 = min(nf, 16), min(nf, 64)
+    t0, _, _ = run(m0)
+    t1, sk, idx = run(m1)
+    per = max((t1 - t0) / max(m1 - m0, 1), 1e-6)
+    fixed = max(t1 - per * m1, 0.0)
+    m = int(min(nf, max(m0, (budget_s - fixed) / per)))
+    if m != m1:
+        t1, sk, idx = run(m)
+    return m, t1, sk, idx, fixed
+
+
 def run_reference(args):
     """Reference arm: the CPU oracle FMM as it stands, on this host's cores (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import oracle
-    oracle.build()
     pr = make_problem(args.config)
     cores = os.cpu_count() or 1
-    # bounded sample: field subset sized so one step takes <= ~3 s on this host
-    nf = len(pr.fr)
-    t0 = time.perf_counter()
-    _, sk = oracle.fmm(pr.sr, pr.sz, pr.S, pr.fr[:256], pr.fz[:256], pr.p, pr.depth, pr.L, pr.z0,
-                       nthreads=cores)
-    t_probe = time.perf_counter() - t0
-    m = nf
-    if t_probe * nf / 256 > 3.0:
-        m = max(256, int(nf * 3.0 / (t_probe * nf / 256)))
-    fr, fz = pr.fr[:m], pr.fz[:m]
+    m, _, _, idx, fixed = oracle_sample(pr, 4.0, cores)   # each step a bounded sample (~4 s)
+    fr, fz = pr.fr[idx], pr.fz[idx]
     for _ in range(args.warmup):
         oracle.fmm(pr.sr, pr.sz, pr.S, fr, fz, pr.p, pr.depth, pr.L, pr.z0, nthreads=cores)
     ts = []
+    sk = 0
     for _ in range(args.steps):
         t0 = time.perf_counter()
         _, sk = oracle.fmm(pr.sr, pr.sz, pr.S, fr, fz, pr.p, pr.depth, pr.L, pr.z0, nthreads=cores)
@@ -138,8 +160,8 @@ def run_reference(args):
     t = sum(ts) / len(ts)
     inter = (len(pr.sr) * m - sk) * pr.K
     v = inter / t
-    sample = (f"oracle FMM (all {len(pr.sr)} sources, upward pass in full) evaluated at the first "
-              f"{m} of {nf} field points per step")
+    sample = (f"oracle FMM (all {len(pr.sr)} sources, upward pass in full, ~{fixed:.1f} s of the "
+              f"step) evaluated at a seeded sample of {m} of {len(pr.fr)} field points per step")
     line = {"metric": "FP64 modal source-field interactions/s (direct-equivalent, FMM solve)",
             "value": v, "unit": "interactions/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
@@ -154,37 +176,47 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(pr, budget_s=12.0):
+def cpu_baseline(pr, budget_s=15.0):
     """The oracle as it stands, timed on this host's cores on a bounded sample of the workload."""
-    import oracle
-    oracle.build()
     cores = os.cpu_count() or 1
-    nf = len(pr.fr)
-    m = min(nf, 1024)
-    t0 = time.perf_counter()
-    _, sk = oracle.fmm(pr.sr, pr.sz, pr.S, pr.fr[:m], pr.fz[:m], pr.p, pr.depth, pr.L, pr.z0,
-                       nthreads=cores)
-    t1 = time.perf_counter() - t0
-    if t1 < budget_s / 4 and m < nf:   # grow the sample to use the budget
-        m = min(nf, int(m * (budget_s / 2) / max(t1, 1e-3)))
-        t0 = time.perf_counter()
-        _, sk = oracle.fmm(pr.sr, pr.sz, pr.S, pr.fr[:m], pr.fz[:m], pr.p, pr.depth, pr.L, pr.z0,
-                           nthreads=cores)
-        t1 = time.perf_counter() - t0
+    m, t, sk, _, fixed = oracle_sample(pr, budget_s, cores)
     inter = (len(pr.sr) * m - sk) * pr.K
-    return {"value": inter / t1, "unit": "interactions/s", "cores": cores, "kind": "oracle",
-            "sample": f"one oracle FMM solve: all {len(pr.sr)} sources, the first {m} of {nf} "
-                      f"field points ({t1:.1f} s)"}
+    return {"value": inter / t, "unit": "interactions/s", "cores": cores, "kind": "oracle",
+            "sample": f"one oracle FMM solve: all {len(pr.sr)} sources (upward pass in full, "
+                      f"~{fixed:.1f} s), a seeded sample of {m} of {len(pr.fr)} field points "
+                      f"({t:.1f} s)"}
+
+
+# Algorithmic FP64 work per unit (SURVEY 8(d); DESIGN.md section 6): the dominant phase's
+# achieved rate = these flops / its in-region CUDA-event time.
+def phase_flops(pr, tm):
+    K, p = pr.K, pr.p
+    P = (p + 1) * (p + 2) // 2
+    nf, ns = len(pr.fr), len(pr.sr)
+    near = (tm["n_forward"] * (210 + 4 * (K - 2) + 5 * K) + tm["n_far"] * (60 + 14 * K) +
+            tm["n_miller"] * (180 + 4 * (K - 1) + 5 * K) + 4 * tm["miller_steps"])
+    return {"s2l": tm["n_s2l_pairs"] * 4 * P * P * K,
+            "p2p": near,
+            "l2p": nf * 4 * P * K,
+            "p2m": ns * 4 * P * K}
+
+
+KERNEL_OF = {"s2l": "s2l_batch_kernel + s2l_reduce_kernel (S2L phase)",
+             "p2p": "p2p_warp_kernel (near-field phase)",
+             "l2p": "l2p_kernel (L2P phase)", "p2m": "p2m_kernel (P2M phase)"}
+NCU_NAME = {"s2l": "s2l_batch_kernel", "p2p": "p2p_warp_kernel", "l2p": "l2p_kernel",
+            "p2m": "p2m_kernel"}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="cylfmm", choices=["cylfmm", "reference"])
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C5")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "cylfmm" else args.warmup
     if args.impl == "reference":
@@ -242,13 +274,14 @@ def main():
         a, bb = (sr, sz) if same else (fr_d, fz_d)
         return plan.solve(sr, sz, S, a, bb, out=out, timings=timings)
 
-    # warm-up + per-phase breakdown (synchronising timings path, outside the timed region)
+    # warm-up, then one synchronising timings solve outside the timed region for the counts
+    # (near-field branch mix, skipped pairs); the phase times come from the timed region
     for _ in range(args.warmup):
         step()
     _, tm = step(timings=True)
-    phase = {k: v for k, v in tm.items()}
     launches_per_step = tm["kernel_launches"]
     skipped = tm["n_skipped"]
+    plan.set_profiling(True)
 
     # timed region: K solves, L2 flushed between them (not timed), CUDA events on the stream
     clocks = ClockSampler(local)
@@ -265,6 +298,8 @@ def main():
     barrier()
     ms = [a.elapsed_time(bb) for a, bb in ev]
     clk = clocks.stop()
+    phase = plan.read_timings()   # per-phase CUDA events of the K timed solves (averaged)
+    plan.set_profiling(False)
     t_step = sum(ms) / len(ms)
     t_max = t_step
     if world > 1:
@@ -277,56 +312,56 @@ def main():
     inter_total = (len(pr.sr) * len(pr.fr) - skipped) * pr.K
     value = inter_total / (t_max * 1e-3)
 
-    # e2e through the host-buffer C-ABI call (pinned host memory, H2D + D2H inside the region):
-    # the full source set and this rank's field points in, this rank's potentials out
-    hs = [torch.as_tensor(a).pin_memory() for a in (pr.sr, pr.sz)]
-    hS = torch.as_tensor(pr.S).pin_memory()
-    hf = hs if same else [torch.as_tensor(np.ascontiguousarray(a)).pin_memory() for a in (fr, fz)]
-    hout = torch.empty((len(fr), pr.K), dtype=torch.complex128).pin_memory()
-    for _ in range(2):
-        plan.solve_host(hs[0].numpy(), hs[1].numpy(), hS.numpy(), hf[0].numpy(), hf[1].numpy(),
-                        out=hout.numpy())
-    barrier()
-    e2e_ms = []
-    for _ in range(args.steps):
-        flush.zero_()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        plan.solve_host(hs[0].numpy(), hs[1].numpy(), hS.numpy(), hf[0].numpy(), hf[1].numpy(),
-                        out=hout.numpy())
-        e2e_ms.append((time.perf_counter() - t0) * 1e3)
-    t_e2e = sum(e2e_ms) / len(e2e_ms)
-    if world > 1:
-        tt = torch.tensor([t_e2e], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_e2e = float(tt.item())
-    h2d = len(pr.sr) * (16 + 16 * pr.K) + (0 if same else len(fr) * 16)
-    d2h = len(fr) * pr.K * 16
+    e2e = None
+    if not args.no_e2e:
+        # e2e through the host-buffer C-ABI call (pinned host memory, H2D + D2H inside the region):
+        # the full source set and this rank's field points in, this rank's potentials out
+        hs = [torch.as_tensor(a).pin_memory() for a in (pr.sr, pr.sz)]
+        hS = torch.as_tensor(pr.S).pin_memory()
+        hf = hs if same else [torch.as_tensor(np.ascontiguousarray(a)).pin_memory() for a in (fr, fz)]
+        hout = torch.empty((len(fr), pr.K), dtype=torch.complex128).pin_memory()
+        for _ in range(2):
+            plan.solve_host(hs[0].numpy(), hs[1].numpy(), hS.numpy(), hf[0].numpy(), hf[1].numpy(),
+                            out=hout.numpy())
+        barrier()
+        e2e_ms = []
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            plan.solve_host(hs[0].numpy(), hs[1].numpy(), hS.numpy(), hf[0].numpy(), hf[1].numpy(),
+                            out=hout.numpy())
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        t_e2e = sum(e2e_ms) / len(e2e_ms)
+        if world > 1:
+            tt = torch.tensor([t_e2e], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_e2e = float(tt.item())
+        h2d = len(pr.sr) * (16 + 16 * pr.K) + (0 if same else len(fr) * 16)
+        d2h = len(fr) * pr.K * 16
+        e2e = {"value": inter_total / (t_e2e * 1e-3), "unit": "interactions/s",
+               "ms_per_step": t_e2e, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
 
-    # roofline of the dominant kernel (FP64 CUDA-core arithmetic: "alu")
-    P = (pr.p + 1) * (pr.p + 2) // 2
-    s2l_flops = tm["n_s2l_pairs"] * 4 * P * P * pr.K
-    dom = max(("s2l", phase["ms_s2l"]), ("p2p", phase["ms_p2p"]), key=lambda x: x[1])
-    pk = peaks()
-    roof = None
+    # roofline of the dominant kernel (FP64 CUDA-core arithmetic: "alu"): the compute phase
+    # with the largest in-region time, its algorithmic flops (phase_flops) / that time
+    fl = phase_flops(pr, tm)
+    dom = max(fl, key=lambda k: phase["ms_" + k])
+    ach = fl[dom] / (phase["ms_" + dom] * 1e-3) / 1e12 if phase["ms_" + dom] > 0 else None
     traffic = None
-    try:   # dram read + write bytes per launch of the dominant kernel from the committed capture
+    try:   # dram read + write bytes per step of the dominant kernel(s), committed ncu capture
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f)["per_launch_dram_bytes"].get("s2l_kernel")
+            traffic = json.load(f)["per_step_dram_bytes"][args.config].get(NCU_NAME[dom])
     except Exception:
         pass
-    if dom[0] == "s2l" and phase["ms_s2l"] > 0:
-        ach = s2l_flops / (phase["ms_s2l"] * 1e-3) / 1e12
-        roof = {"bound": "alu", "kernel": "s2l_kernel (all levels)", "achieved": ach,
-                "peak": FP64_NOMINAL_TFLOPS, "unit": "TFLOP/s", "frac": ach / FP64_NOMINAL_TFLOPS,
-                "traffic": traffic if pr.name.startswith("C2") else None,
-                "traffic_note": "ncu dram__bytes_read.sum + dram__bytes_write.sum per launch "
-                                "(profiles/ncu_traffic.json); flop-bound kernel",
-                "algorithmic_flops": s2l_flops,
-                "peak_note": "FP64 nominal 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md 6)"}
-    else:
-        roof = {"bound": "alu", "kernel": "p2p_kernel (near field)", "achieved": None,
-                "peak": FP64_NOMINAL_TFLOPS, "unit": "TFLOP/s", "frac": None, "traffic": None}
+    roof = {"bound": "alu", "kernel": KERNEL_OF[dom], "achieved": ach, "peak": FP64_NOMINAL_TFLOPS,
+            "unit": "TFLOP/s", "frac": ach / FP64_NOMINAL_TFLOPS if ach else None,
+            "traffic": traffic, "algorithmic_flops": fl[dom], "ms": phase["ms_" + dom],
+            "traffic_note": "ncu dram__bytes_read.sum + dram__bytes_write.sum of the phase's "
+                            "kernel launches in one step (profiles/ncu_traffic.json)",
+            "peak_note": "FP64 nominal 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (DESIGN.md 6); "
+                         "MEASURED_PEAKS.json has no FP64 figure",
+            "phase_frac": {k: (fl[k] / (phase["ms_" + k] * 1e-3) / 1e12 / FP64_NOMINAL_TFLOPS
+                               if phase["ms_" + k] > 0 else None) for k in fl}}
 
     if rank == 0:
         line = {"metric": "FP64 modal source-field interactions/s (direct-equivalent, FMM solve)",
@@ -339,10 +374,10 @@ def main():
                            "parallelism": (f"field-partition x{world} (cost-weighted Morton ranges, "
                                            "source all-gather)") if world > 1 else "single GPU"},
                 "phase_ms": {k: round(v, 4) for k, v in phase.items() if k.startswith("ms_")},
-                "near_pairs": phase["n_near_pairs"], "s2l_box_pairs": phase["n_s2l_pairs"],
+                "near_branches": {k: tm[k] for k in ("n_forward", "n_far", "n_miller", "miller_steps")},
+                "near_pairs": tm["n_near_pairs"], "s2l_box_pairs": tm["n_s2l_pairs"],
                 "roofline": roof, "clocks": clk,
-                "e2e": {"value": inter_total / (t_e2e * 1e-3), "unit": "interactions/s",
-                        "ms_per_step": t_e2e, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                "e2e": e2e,
                 "gpu_launches": launches_per_step * args.steps}
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(pr)

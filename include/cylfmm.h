@@ -75,13 +75,27 @@ typedef struct {
                                may differ); 0 = the source order `order`.  1 <= pl <= 16 */
 } cylfmm_params;
 
-/* Per-phase device times of the last solve, milliseconds (CUDA events on the solve stream). */
+/* Per-phase device times, milliseconds: CUDA events recorded on the stream each phase runs on
+ * (the tensors and the near field run on the plan's auxiliary streams, concurrently with the
+ * tree / far-field chain, so the phases may sum to more than ms_total).  Filled by a solve with
+ * a non-null `timings` (that solve runs every phase on `stream`, serialised, and synchronises),
+ * or averaged over the solves since profiling was switched on by cylfmm_plan_read_timings. */
 typedef struct {
-    double ms_tree, ms_p2m, ms_m2m, ms_tensor, ms_s2l, ms_l2l, ms_l2p, ms_p2p, ms_total;
+    double ms_tree;        /* ms_sort + ms_lists */
+    double ms_p2m, ms_m2m, ms_tensor, ms_s2l, ms_l2l, ms_l2p, ms_p2p, ms_total;
     int64_t n_near_pairs;  /* near-field (source, field) pairs evaluated, coincident excluded */
     int64_t n_skipped;     /* coincident pairs skipped */
     int64_t n_s2l_pairs;   /* (source box, target box) S2L applications, all levels */
     int64_t kernel_launches;
+    double ms_sort;        /* Morton keys, radix sorts, permuted coordinate / coefficient copies */
+    double ms_lists;       /* leaf starts, level maps, S2L pair lists, lazy-L2L flags */
+    double ms_unpermute;   /* 0: the un-permutation is fused into the output row writes (a13) */
+    double ms_allgather;   /* collective time (multi-device solves; 0 on one device) */
+    int64_t n_solves;      /* solves averaged */
+    /* near-field branch counts (synchronised timings path only): pairs on the forward branch
+     * (chi < 1.008), the far series (chi >= 1000) and Miller's backward recursion
+     * (P:868-874), and the sum over Miller pairs of the start offset S - N (R#4) */
+    int64_t n_forward, n_far, n_miller, miller_steps;
 } cylfmm_timings;
 
 typedef struct cylfmm_plan_s *cylfmm_plan;
@@ -115,6 +129,15 @@ cylfmm_status cylfmm_direct(const double *src_r, const double *src_z, const doub
 cylfmm_status cylfmm_plan_create(cylfmm_plan *plan, const cylfmm_params *prm);
 void cylfmm_plan_destroy(cylfmm_plan plan);
 cylfmm_status cylfmm_plan_sync(cylfmm_plan plan);
+
+/* Profiling of asynchronous solves.  on != 0: every following solve records CUDA events around
+ * its phases on the streams they run on (no synchronisation, no change to the launch sequence
+ * or results); cylfmm_plan_read_timings then synchronises those events and returns the phase
+ * times averaged over the solves since the last read (or since profiling was switched on), and
+ * the S2L pair count / kernel launches of the last solve.  Errors: EINVAL (null argument),
+ * ECUDA. */
+cylfmm_status cylfmm_plan_set_profiling(cylfmm_plan plan, int on);
+cylfmm_status cylfmm_plan_read_timings(cylfmm_plan plan, cylfmm_timings *timings);
 
 /* FMM solve, Algorithm 1 of the paper:
  *   tree (Morton sort of sources and fields on the uniform depth-d quadtree)

@@ -3,6 +3,7 @@
 #include "../../include/cylfmm.h"
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdarg.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -432,6 +433,24 @@ struct DevBuf {
     }
 };
 
+// Phase timing: CUDA events recorded on the stream each phase runs on (no synchronisation),
+// summed when the timings are read (after the solve has completed), plus NVTX ranges.
+enum { PH_SORT, PH_LISTS, PH_TENSOR, PH_P2M, PH_M2M, PH_S2L, PH_L2L, PH_L2P, PH_P2P, PH_TOTAL, PH_N };
+static const char *kPhaseName[PH_N] = {"cylfmm.sort", "cylfmm.lists", "cylfmm.tensor", "cylfmm.p2m",
+                                       "cylfmm.m2m", "cylfmm.s2l", "cylfmm.l2l", "cylfmm.l2p",
+                                       "cylfmm.near", "cylfmm.solve"};
+struct PhaseMark {
+    int ph;
+    cudaEvent_t a, b;
+};
+struct Phases {
+    cylfmm_plan p;
+    bool on;
+    int open[PH_N];
+    void beg(int ph, cudaStream_t s);
+    void end(int ph, cudaStream_t s);
+};
+
 struct cylfmm_plan_s {
     cylfmm_params prm;
     int device = 0;
@@ -464,7 +483,72 @@ struct cylfmm_plan_s {
     // build (hev: previous work on the caller's stream done, coefficients resident)
     cudaStream_t hcp = nullptr;
     cudaEvent_t hev[2];
+    // phase events (Phases): pool reused across solves, marks of the solves since the last read
+    std::vector<cudaEvent_t> evpool;
+    size_t evused = 0;
+    std::vector<PhaseMark> marks;
+    int prof_solves = 0;
+    bool prof_on = false;
+    int64_t last_npairs = 0, last_launches = 0;
 };
+
+static cudaEvent_t pool_event(cylfmm_plan p)
+{
+    if (p->evused == p->evpool.size()) {
+        cudaEvent_t e = nullptr;
+        if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+        p->evpool.push_back(e);
+    }
+    return p->evpool[p->evused++];
+}
+void Phases::beg(int ph, cudaStream_t s)
+{
+    nvtxRangePushA(kPhaseName[ph]);
+    if (!on) return;
+    PhaseMark m = {ph, pool_event(p), nullptr};
+    if (m.a) cudaEventRecord(m.a, s);
+    open[ph] = (int)p->marks.size();
+    p->marks.push_back(m);
+}
+void Phases::end(int ph, cudaStream_t s)
+{
+    nvtxRangePop();
+    if (!on) return;
+    PhaseMark &m = p->marks[open[ph]];
+    m.b = pool_event(p);
+    if (m.b) cudaEventRecord(m.b, s);
+}
+// sum the phase marks of the solves since the last read into t (averaged per solve), then reset
+static cylfmm_status read_phases(cylfmm_plan p, cylfmm_timings *t)
+{
+    double acc[PH_N] = {0};
+    for (const PhaseMark &m : p->marks) {
+        if (!m.a || !m.b) continue;
+        CK(cudaEventSynchronize(m.b));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, m.a, m.b));
+        acc[m.ph] += ms;
+    }
+    const double n = std::max(p->prof_solves, 1);
+    t->ms_sort = acc[PH_SORT] / n;
+    t->ms_lists = acc[PH_LISTS] / n;
+    t->ms_tree = t->ms_sort + t->ms_lists;
+    t->ms_tensor = acc[PH_TENSOR] / n;
+    t->ms_p2m = acc[PH_P2M] / n;
+    t->ms_m2m = acc[PH_M2M] / n;
+    t->ms_s2l = acc[PH_S2L] / n;
+    t->ms_l2l = acc[PH_L2L] / n;
+    t->ms_l2p = acc[PH_L2P] / n;
+    t->ms_p2p = acc[PH_P2P] / n;
+    t->ms_total = acc[PH_TOTAL] / n;
+    t->ms_unpermute = 0.0;   // fused into the L2P / near-field row writes (a13)
+    t->ms_allgather = 0.0;
+    t->n_solves = p->prof_solves;
+    p->marks.clear();
+    p->evused = 0;
+    p->prof_solves = 0;
+    return CYLFMM_OK;
+}
 
 static void free_plan_bufs(cylfmm_plan p)
 {
@@ -545,6 +629,7 @@ extern "C" void cylfmm_plan_destroy(cylfmm_plan plan)
     free_plan_bufs(plan);
     if (plan->ev_ok)
         for (int i = 0; i < 16; ++i) cudaEventDestroy(plan->ev[i]);
+    for (cudaEvent_t e : plan->evpool) cudaEventDestroy(e);
     if (plan->aux_ok) {
         for (int i = 0; i < 2; ++i) cudaStreamDestroy(plan->aux[i]);
         for (int i = 0; i < 5; ++i) cudaEventDestroy(plan->aev[i]);
@@ -568,6 +653,31 @@ static cylfmm_status check_err_flag(cylfmm_plan p, cudaStream_t st)
         return CYLFMM_ENUMERIC;
     }
     return CYLFMM_OK;
+}
+
+extern "C" cylfmm_status cylfmm_plan_set_profiling(cylfmm_plan plan, int on)
+{
+    if (!plan) {
+        set_err("cylfmm_plan_set_profiling: null plan");
+        return CYLFMM_EINVAL;
+    }
+    plan->prof_on = on != 0;
+    plan->marks.clear();
+    plan->evused = 0;
+    plan->prof_solves = 0;
+    return CYLFMM_OK;
+}
+
+extern "C" cylfmm_status cylfmm_plan_read_timings(cylfmm_plan plan, cylfmm_timings *t)
+{
+    if (!plan || !t) {
+        set_err("cylfmm_plan_read_timings: null argument");
+        return CYLFMM_EINVAL;
+    }
+    *t = cylfmm_timings{};
+    t->n_s2l_pairs = plan->last_npairs;
+    t->kernel_launches = plan->last_launches;
+    return read_phases(plan, t);
 }
 
 extern "C" cylfmm_status cylfmm_plan_sync(cylfmm_plan plan)
@@ -693,17 +803,6 @@ static cudaError_t launch_s2l(const S2LArgs &sa, int64_t nbatches, cudaStream_t 
     return launch_s2l_t<S2L_P16>(sa, nbatches, st);
 }
 
-struct PhaseTimer {
-    cylfmm_plan p;
-    cudaStream_t st;
-    bool on;
-    int k = 0;
-    void mark()
-    {
-        if (on && k < 16) cudaEventRecord(p->ev[k++], st);
-    }
-};
-
 static cylfmm_status build_tree(cylfmm_plan p, const double *r, const double *z, int64_t n,
                                 bool is_src, cudaStream_t st, int **perm_out, uint32_t **key_out)
 {
@@ -740,17 +839,30 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     const int pt = std::max(pp, pl);
     int KW = q.mode_chunk > 0 ? std::min(q.mode_chunk, K) : K;
     p->launches = 0;
-    PhaseTimer T{p, st, tm != nullptr};
+    // phase events: always in the synchronised timings path, on request (plan profiling) else
+    if (tm) {
+        p->marks.clear();
+        p->evused = 0;
+        p->prof_solves = 0;
+    }
+    Phases T{p, tm != nullptr || p->prof_on, {}};
+    if (T.on) p->prof_solves++;
     RET_IF(p->err.need(sizeof(int)));
-    RET_IF(p->ctr.need(sizeof(unsigned long long) * 4));
+    RET_IF(p->ctr.need(sizeof(unsigned long long) * 8));
     CK(cudaMemsetAsync(p->err.p, 0, sizeof(int), st));
-    CK(cudaMemsetAsync(p->ctr.p, 0, sizeof(unsigned long long) * 4, st));
-    T.mark();  // 0
-    if (nf == 0) return CYLFMM_OK;
-    // Streams: the timings path runs every phase on `st` (clean per-phase events); otherwise the
-    // tensors (independent of the data: normalised stations) and the near field (independent of
-    // the far field) run on the plan's auxiliary streams and are joined by events.
-    const bool overlap = tm == nullptr && p->aux_ok;
+    CK(cudaMemsetAsync(p->ctr.p, 0, sizeof(unsigned long long) * 8, st));
+    T.beg(PH_TOTAL, st);
+    if (nf == 0) {
+        T.end(PH_TOTAL, st);
+        return CYLFMM_OK;
+    }
+    // Streams: the timings path runs every phase on `st` (clean per-phase events).  Small
+    // problems (launch-latency bound: C2, C3) run the tensors (independent of the data:
+    // normalised stations) and the near field (independent of the far field) on the plan's
+    // auxiliary streams, joined by events; large ones (C4, C5) keep every kernel on `st`, where
+    // each already fills the GPU (measured: C5 162.6 ms overlapped vs 163.0 ms serialised) and
+    // the per-phase events stay clean.
+    const bool overlap = tm == nullptr && p->aux_ok && ns + nf <= ((int64_t)1 << 20);
     cudaStream_t st_t = overlap ? p->aux[0] : st, st_n = overlap ? p->aux[1] : st;
     const int64_t nstat = (int64_t)12 << d;
     const int NM = std::max(K - 1, 1) + 1, D = 2 * pt + 1;
@@ -767,23 +879,16 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     ta.seeds = p->seeds.as<double>();
     ta.packed = 1;
     ta.err = p->err.as<int>();
-    double ms_seed = 0;
     if (overlap) {
         CK(cudaEventRecord(p->aev[0], st));
         CK(cudaStreamWaitEvent(st_t, p->aev[0], 0));
-    } else if (tm) {
-        cudaEventRecord(p->ev[12], st);
     }
+    T.beg(PH_TENSOR, st_t);
     RET_IF(run_seeds(ta, nstat, st_t));   // seeds of all modes once, behind the tree build
     p->launches++;
-    if (tm) {
-        cudaEventRecord(p->ev[13], st);
-        cudaEventSynchronize(p->ev[13]);
-        float ms = 0;
-        cudaEventElapsedTime(&ms, p->ev[12], p->ev[13]);
-        ms_seed = ms;
-    }
+    T.end(PH_TENSOR, st_t);
     // ---- tree
+    T.beg(PH_SORT, st);
     int *sperm = nullptr, *fperm = nullptr;
     uint32_t *skey_s = nullptr, *fkey_s = nullptr;
     // fields == sources (C2-C4: "field points equal to source points"): one tree serves both
@@ -818,6 +923,8 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         fr_sorted = p->fr_s.as<double>();
         fz_sorted = p->fz_s.as<double>();
     }
+    T.end(PH_SORT, st);
+    T.beg(PH_LISTS, st);
     const int64_t nleaf = pow4(d);
     RET_IF(p->slstart.need(sizeof(int) * (nleaf + 1)));
     RET_IF(p->flstart.need(sizeof(int) * (nleaf + 1)));
@@ -979,7 +1086,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         CKL();
         p->launches += 2;
     }
-    T.mark();  // 1: tree done
+    T.end(PH_LISTS, st);
     // ---- far-field storage
     FarArgs fa = {};
     fa.depth = d;
@@ -1084,18 +1191,6 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     RET_IF(p->l2pntask.need(sizeof(int)));
     fa.outr = grad ? reinterpret_cast<double2 *>(out_dr) : nullptr;
     fa.outz = grad ? reinterpret_cast<double2 *>(out_dz) : nullptr;
-    double ms_tensor = ms_seed, ms_p2m = 0, ms_m2m = 0, ms_s2l = 0, ms_l2l = 0, ms_l2p = 0;
-    cudaEvent_t e0 = p->ev[10], e1 = p->ev[11];
-    auto tic = [&]() { if (tm) cudaEventRecord(e0, st); };
-    auto toc = [&](double &acc) {
-        if (tm) {
-            cudaEventRecord(e1, st);
-            cudaEventSynchronize(e1);
-            float ms = 0;
-            cudaEventElapsedTime(&ms, e0, e1);
-            acc += ms;
-        }
-    };
     fa.need = p->need.as<unsigned char>();
     fa.lrow = p->lrow.as<int>();
     // tree done: the near field starts behind it on its own stream
@@ -1104,10 +1199,9 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         CK(cudaStreamWaitEvent(st_t, p->aev[1], 0));
     }
     // ---- near field: writes every field row (the far field is added by L2P)
-    tic();
-    double ms_p2p = 0;
     if (ns > 0) {
         if (overlap) CK(cudaStreamWaitEvent(st_n, p->aev[1], 0));
+        T.beg(PH_P2P, st_n);
         const int ntl = fa.tcount[d];
         double avg = (double)nf / std::max(ntl, 1);
         const int TT = avg <= 10.0 ? 8 : (avg <= 24.0 ? 16 : 32);
@@ -1164,6 +1258,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             a.depth = d;
             a.n_skipped = ctr + 0;
             a.n_pairs = ctr + 1;
+            a.n_branch = ctr + 3;
             a.err_flag = p->err.as<int>();
             const dim3 grid((unsigned)maxtasks);
             a.task_ctr = p->ntasks.as<int>() + 1;
@@ -1172,43 +1267,42 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             else CK(launch_p2p<true>(TT, a, grid, st_n));
             p->launches++;
         }
+        T.end(PH_P2P, st_n);
         if (overlap) CK(cudaEventRecord(p->aev[3], st_n));
     }
-    toc(ms_p2p);
     for (int m0 = 0; m0 < K; m0 += KW) {
         fa.m0 = m0;
         fa.m1 = std::min(K, m0 + KW);
         const int kw = fa.m1 - fa.m0;
         // tensors for the normalised stations (shared by all levels): seeds of all modes once,
         // the Laplace fill per mode chunk
-        tic();
         {
             ta.out = p->tens.as<double>();
             ta.m0 = fa.m0;
             ta.m1 = fa.m1;
             ta.seed_m1 = K;
             if (overlap && m0 > 0) CK(cudaStreamWaitEvent(st_t, p->aev[4], 0));  // previous S2L done
+            T.beg(PH_TENSOR, st_t);
             // stations i_in <= the largest source column (C5: 35% of them) are the only ones read
             if (nstat_used > 0) RET_IF(run_fill(ta, nstat_used, st_t));
             p->launches++;
+            T.end(PH_TENSOR, st_t);
             if (overlap) CK(cudaEventRecord(p->aev[2], st_t));
         }
-        toc(ms_tensor);
         if (ns > 0) {
-            tic();
+            T.beg(PH_P2M, st);
             if (fa.scount[d] > 0) {
                 const int nmb = (kw + kP2MModes - 1) / kP2MModes;
                 p2m_kernel<<<(unsigned)((int64_t)fa.scount[d] * nmb), kP2MThreads, p2m_smem(P, pp), st>>>(fa);
                 CKL();
                 p->launches++;
             }
-            toc(ms_p2m);
-            tic();
+            T.end(PH_P2M, st);
+            T.beg(PH_M2M, st);
             for (int l = d - 1; l >= 2; --l) {
                 if (fa.scount[l] == 0) continue;
                 unsigned g = (unsigned)((int64_t)fa.scount[l] * ((kw + kMMG - 1) / kMMG));
-                static const int mth = getenv("CYLFMM_M2M_THREADS") ? atoi(getenv("CYLFMM_M2M_THREADS")) : 256;
-                m2m_kernel<<<g, mth, m2m_smem(pp), st>>>(fa, l);
+                m2m_kernel<<<g, 256, m2m_smem(pp), st>>>(fa, l);
                 CKL();
                 p->launches++;
             }
@@ -1216,11 +1310,11 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             prescale_moments_kernel<<<nblk(stot * kw * P, 256), 256, 0, st>>>(fa.M, stot * kw, P, fa.pscale);
             CKL();
             p->launches++;
-            toc(ms_m2m);
+            T.end(PH_M2M, st);
         }
         // S2L of every level in one launch (each level's contribution), then the L2L chain
-        tic();
         if (overlap) CK(cudaStreamWaitEvent(st, p->aev[2], 0));   // tensors of this chunk ready
+        T.beg(PH_S2L, st);
         if (ns > 0 && npairs > 0) {
             sa.m0 = fa.m0;
             sa.m1 = fa.m1;
@@ -1232,9 +1326,9 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             p->launches++;
             p->launches++;
         }
+        T.end(PH_S2L, st);
         if (overlap) CK(cudaEventRecord(p->aev[4], st));
-        toc(ms_s2l);
-        tic();
+        T.beg(PH_L2L, st);
         for (int l = 3; l <= d; ++l) {
             if (fa.tcount[l] == 0) continue;
             int64_t items = (int64_t)fa.tcount[l] * kw;
@@ -1244,9 +1338,9 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             CKL();
             p->launches++;
         }
-        toc(ms_l2l);
-        tic();
+        T.end(PH_L2L, st);
         if (overlap && ns > 0 && m0 == 0) CK(cudaStreamWaitEvent(st, p->aev[3], 0));  // near field
+        T.beg(PH_L2P, st);
         {
             // tasks: runs of <= TP sorted field points sharing their evaluating box; TP from the
             // points per target leaf (C5's leaves hold 4 points but share coarse boxes: 128)
@@ -1287,30 +1381,26 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             CKL();
             p->launches++;
         }
-        toc(ms_l2p);
+        T.end(PH_L2P, st);
     }
-    T.mark();
+    T.end(PH_TOTAL, st);
     if (tm) {
-        unsigned long long c[4] = {0, 0, 0, 0};
+        unsigned long long c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         CK(cudaMemcpyAsync(c, p->ctr.p, sizeof(c), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        float ms_tree = 0, ms_total = 0;
-        cudaEventElapsedTime(&ms_tree, p->ev[0], p->ev[1]);
-        cudaEventElapsedTime(&ms_total, p->ev[0], p->ev[2]);
-        tm->ms_tree = ms_tree - ms_seed;   // the seeds ran first on st in the timed path
-        tm->ms_p2m = ms_p2m;
-        tm->ms_m2m = ms_m2m;
-        tm->ms_tensor = ms_tensor;
-        tm->ms_s2l = ms_s2l;
-        tm->ms_l2l = ms_l2l;
-        tm->ms_l2p = ms_l2p;
-        tm->ms_p2p = ms_p2p;
-        tm->ms_total = ms_total;
+        RET_IF(read_phases(p, tm));
         tm->n_skipped = (int64_t)c[0];
         tm->n_near_pairs = (int64_t)c[1];
         tm->n_s2l_pairs = npairs;
         tm->kernel_launches = p->launches;
+        tm->n_forward = (int64_t)c[3];
+        tm->n_far = (int64_t)c[4];
+        tm->n_miller = (int64_t)c[5];
+        tm->miller_steps = (int64_t)c[6];
         RET_IF(check_err_flag(p, st));
+    } else if (p->prof_on) {
+        p->last_npairs = npairs;
+        p->last_launches = p->launches;
     }
     return CYLFMM_OK;
 }

@@ -42,6 +42,7 @@ struct P2PArgs {
     int depth;
     unsigned long long *n_skipped;
     unsigned long long *n_pairs;
+    unsigned long long *n_branch;   // nullable: [0] forward, [1] far, [2] Miller pairs, [3] sum S - N
     int *err_flag;
 };
 

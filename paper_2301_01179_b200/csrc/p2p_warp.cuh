@@ -93,7 +93,8 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
     int *segS0 = reinterpret_cast<int *>(wbase) + kWarps * CH;
     int *segPre = segS0 + 9;
 
-    unsigned my_skipped = 0, my_pairs = 0;
+    unsigned my_skipped = 0, my_pairs = 0, my_fwd = 0, my_far = 0, my_mil = 0;
+    unsigned long long my_msteps = 0;
     const int nparts = DIRECT ? (int)((a.ns + a.src_per_part - 1) / a.src_per_part) : 1;
     const int ntasks = DIRECT ? (int)((a.nf + 31) / 32) * nparts : *a.ntasks;
     for (;;) {                                           // persistent: fetch tasks heaviest first
@@ -222,75 +223,116 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
         }
         const int nF = __popc(mF), nX = __popc(mX), nM = __popc(mM) + __popc(mL);
         my_pairs += nF + nX + nM;
-        // forward and far pairs, one per lane and iteration
-        const int itFX = __reduce_max_sync(0xffffffffu, nF + nX);
-        for (int it = 0; it < itFX; ++it) {
-            int cls = 2, idx = 0;
-            if (mF) { cls = 0; idx = __ffs(mF) - 1; mF &= mF - 1; }
-            else if (mX) { cls = 3; idx = __ffs(mX) - 1; mX &= mX - 1; }
-            const int c = sl + SL * idx;
-            const PairGeo g = pair_geo(tr, stR[c], tz - stZ[c], fwd2);
-            const double2 *Srow = stS + c * ROW;
-            if (cls == 0) {
-                // forward on u_n = G_n / R_n, K, E by the small-k' series
-                const double inv_rho_p = rsqrt_nr(g.rp2);
-                double Kk, Ek;
-                ke_small(g.rm2 * inv_rho_p * inv_rho_p, Kk, Ek);
-                const double G0 = Kk * inv_rho_p * (1.0 / kPi);
-                const double irr = rcp_nr(g.rr1);
-                const double chi = 0.25 * (g.rp2 + g.rm2) * irr;
-                const double dchi = 0.5 * g.rm2 * irr;    // chi - 1, exact to rounding (R#24)
-                double u0 = G0, u1 = G0 * fma(-(1.0 + chi), Ek * rcp_nr(Kk), chi);
-                if constexpr (WIN) {                    // M0 >= 2: advance to the window
+        my_fwd += nF;
+        my_far += nX;
+        my_mil += nM;
+        // forward pairs on u_n = G_n / R_n, K, E by the small-k' series.  The
+        // recursion is a chain of dependent FMAs: in the windowed pass (K > KT, where the chain
+        // also advances to the window) two pairs per lane run in lockstep to hide its latency;
+        // a missing second pair runs with zero seeds (the recursion is linear: exact zeros).
+        constexpr bool TWO = WIN;
+        const int itF = __reduce_max_sync(0xffffffffu, TWO ? (nF + 1) >> 1 : nF);
+        for (int it = 0; it < itF; ++it) {
+            int ia = -1, ib = -1;
+            if (mF) { ia = __ffs(mF) - 1; mF &= mF - 1; }
+            if (TWO && mF) { ib = __ffs(mF) - 1; mF &= mF - 1; }
+            if (ia < 0) continue;
+            const int ca = sl + SL * ia, cb = ib >= 0 ? sl + SL * ib : ca;
+            const double wb = ib >= 0 ? 1.0 : 0.0;
+            const PairGeo gA = pair_geo(tr, stR[ca], tz - stZ[ca], fwd2);
+            const double2 *SA = stS + ca * ROW, *SB = stS + cb * ROW;
+            const double ipA = rsqrt_nr(gA.rp2);
+            double KA, EA;
+            ke_small(gA.rm2 * ipA * ipA, KA, EA);
+            const double G0A = KA * ipA * (1.0 / kPi);
+            const double irA = rcp_nr(gA.rr1);
+            const double chA = 0.25 * (gA.rp2 + gA.rm2) * irA;
+            const double dA = 0.5 * gA.rm2 * irA;   // chi - 1, exact to rounding (R#24)
+            double u0A = G0A, u1A = G0A * fma(-(1.0 + chA), EA * rcp_nr(KA), chA);
+            double u0B = 0.0, u1B = 0.0, dB = 0.0;
+            if constexpr (TWO) {
+                const PairGeo gB = pair_geo(tr, stR[cb], tz - stZ[cb], fwd2);
+                const double ipB = rsqrt_nr(gB.rp2);
+                double KB, EB;
+                ke_small(gB.rm2 * ipB * ipB, KB, EB);
+                const double G0B = KB * ipB * (wb / kPi);
+                const double irB = rcp_nr(gB.rr1);
+                const double chB = 0.25 * (gB.rp2 + gB.rm2) * irB;
+                dB = 0.5 * gB.rm2 * irB;
+                u0B = G0B;
+                u1B = G0B * fma(-(1.0 + chB), EB * rcp_nr(KB), chB);
+            }
+            if constexpr (WIN) {                        // M0 >= 2: advance to the window
 #pragma unroll 4
-                    for (int n = 2; n < M0; ++n) {
-                        const double u2 = fma(dchi, u1, fma(-c_rec.eps[n], u0, u1));
-                        u0 = u1;
-                        u1 = u2;
+                for (int n = 2; n < M0; ++n) {
+                    const double e = c_rec.eps[n];
+                    const double u2A = fma(dA, u1A, fma(-e, u0A, u1A));
+                    u0A = u1A;
+                    u1A = u2A;
+                    if constexpr (TWO) {
+                        const double u2B = fma(dB, u1B, fma(-e, u0B, u1B));
+                        u0B = u1B;
+                        u1B = u2B;
                     }
-#pragma unroll
-                    for (int j = 0; j < KT; ++j) {
-                        if (j < KW) {
-                            const int n = M0 + j;
-                            const double u2 = fma(dchi, u1, fma(-c_rec.eps[n], u0, u1));
-                            acc[j] = cfma(Srow[j], u2 * c_rec.Rn[n], acc[j]);
-                            u0 = u1;
-                            u1 = u2;
-                        }
-                    }
-                } else {
-                    acc[0] = cfma(Srow[0], u0, acc[0]);
-                    if (KW > 1) acc[1] = cfma(Srow[1], u1, acc[1]);
-#pragma unroll
-                    for (int n = 2; n < KT; ++n) {
-                        if (n < KW) {
-                            const double u2 = fma(dchi, u1, fma(-c_rec.eps[n], u0, u1));
-                            acc[n] = cfma(Srow[n], u2 * c_rec.Rn[n], acc[n]);
-                            u0 = u1;
-                            u1 = u2;
-                        }
-                    }
-                }
-            } else if (cls == 3) {
-                // far (chi >= 1000): hypergeometric form (DLMF 14.3.7), see greens_far
-                const double sum2 = 0.5 * (g.rp2 + g.rm2);
-                const double isum = rcp_nr(sum2);
-                const double q = g.rr1 * isum, z = 4.0 * q * q;
-                double qn = rsqrt_nr(sum2);
-                if constexpr (WIN) {
-                    for (int n = 0; n < M0 - 1; ++n) qn *= q;   // q^(M0-1): the loop multiplies once more
                 }
 #pragma unroll
                 for (int j = 0; j < KT; ++j) {
                     if (j < KW) {
                         const int n = M0 + j;
-                        if (n > 0) qn *= q;
-                        double t = z * c_rec.farT[n][3];
-                        t = z * c_rec.farT[n][2] * (1.0 + t);
-                        t = z * c_rec.farT[n][1] * (1.0 + t);
-                        t = z * c_rec.farT[n][0] * (1.0 + t);
-                        acc[j] = cfma(Srow[j], c_rec.farA[n] * qn * (1.0 + t), acc[j]);
+                        const double e = c_rec.eps[n], R = c_rec.Rn[n];
+                        const double u2A = fma(dA, u1A, fma(-e, u0A, u1A));
+                        acc[j] = cfma(SA[j], u2A * R, acc[j]);
+                        u0A = u1A;
+                        u1A = u2A;
+                        if constexpr (TWO) {
+                            const double u2B = fma(dB, u1B, fma(-e, u0B, u1B));
+                            acc[j] = cfma(SB[j], u2B * R, acc[j]);
+                            u0B = u1B;
+                            u1B = u2B;
+                        }
                     }
+                }
+            } else {
+                acc[0] = cfma(SA[0], u0A, acc[0]);
+                if (KW > 1) acc[1] = cfma(SA[1], u1A, acc[1]);
+#pragma unroll
+                for (int n = 2; n < KT; ++n) {
+                    if (n < KW) {
+                        const double u2A = fma(dA, u1A, fma(-c_rec.eps[n], u0A, u1A));
+                        acc[n] = cfma(SA[n], u2A * c_rec.Rn[n], acc[n]);
+                        u0A = u1A;
+                        u1A = u2A;
+                    }
+                }
+            }
+        }
+        // far pairs (chi >= 1000), one per lane and iteration: hypergeometric form (DLMF
+        // 14.3.7), see greens_far; every mode is independent (no chain)
+        const int itX = __reduce_max_sync(0xffffffffu, nX);
+        for (int it = 0; it < itX; ++it) {
+            if (!mX) continue;
+            const int idx = __ffs(mX) - 1;
+            mX &= mX - 1;
+            const int c = sl + SL * idx;
+            const PairGeo g = pair_geo(tr, stR[c], tz - stZ[c], fwd2);
+            const double2 *Srow = stS + c * ROW;
+            const double sum2 = 0.5 * (g.rp2 + g.rm2);
+            const double isum = rcp_nr(sum2);
+            const double q = g.rr1 * isum, z = 4.0 * q * q;
+            double qn = rsqrt_nr(sum2);
+            if constexpr (WIN) {
+                for (int n = 0; n < M0 - 1; ++n) qn *= q;   // q^(M0-1): the loop multiplies once more
+            }
+#pragma unroll
+            for (int j = 0; j < KT; ++j) {
+                if (j < KW) {
+                    const int n = M0 + j;
+                    if (n > 0) qn *= q;
+                    double t = z * c_rec.farT[n][3];
+                    t = z * c_rec.farT[n][2] * (1.0 + t);
+                    t = z * c_rec.farT[n][1] * (1.0 + t);
+                    t = z * c_rec.farT[n][0] * (1.0 + t);
+                    acc[j] = cfma(Srow[j], c_rec.farA[n] * qn * (1.0 + t), acc[j]);
                 }
             }
         }
@@ -310,7 +352,9 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
             const int ca = sl + SL * (va ? ia : 0), cb = vb ? sl + SL * ib : ca;
             const PairGeo gA = pair_geo(tr, stR[ca], tz - stZ[ca], fwd2);
             const PairGeo gB = pair_geo(tr, stR[cb], tz - stZ[cb], fwd2);
-            const int S_lane = va ? Nglob + max(miller_extra(gA, a.miller), miller_extra(gB, a.miller)) : 0;
+            const int eA = va ? miller_extra(gA, a.miller) : 0, eB = vb ? miller_extra(gB, a.miller) : 0;
+            const int S_lane = va ? Nglob + max(eA, eB) : 0;
+            my_msteps += (unsigned)(eA + eB);
             const int S_warp = __reduce_max_sync(0xffffffffu, S_lane);
             if (va) {
                 const double ipA = rsqrt_nr(gA.rp2), ipB = rsqrt_nr(gB.rp2);
@@ -462,6 +506,18 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
     if (WIN) my_skipped = my_pairs = 0;                  // counted by the first window
     if (lane == 0 && a.n_skipped && my_skipped) atomicAdd(a.n_skipped, (unsigned long long)my_skipped);
     if (lane == 0 && a.n_pairs && my_pairs) atomicAdd(a.n_pairs, (unsigned long long)my_pairs);
+    if (!WIN && a.n_branch) {
+        my_fwd = __reduce_add_sync(0xffffffffu, my_fwd);
+        my_far = __reduce_add_sync(0xffffffffu, my_far);
+        my_mil = __reduce_add_sync(0xffffffffu, my_mil);
+        for (int o = 16; o > 0; o >>= 1) my_msteps += __shfl_xor_sync(0xffffffffu, my_msteps, o);
+        if (lane == 0) {
+            if (my_fwd) atomicAdd(a.n_branch + 0, (unsigned long long)my_fwd);
+            if (my_far) atomicAdd(a.n_branch + 1, (unsigned long long)my_far);
+            if (my_mil) atomicAdd(a.n_branch + 2, (unsigned long long)my_mil);
+            if (my_msteps) atomicAdd(a.n_branch + 3, my_msteps);
+        }
+    }
 }
 
 // Near-field tasks for the warp kernel: each target leaf is cut into pieces of 32 targets, the

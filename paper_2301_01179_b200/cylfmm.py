@@ -41,7 +41,10 @@ class Timings(ctypes.Structure):
     _fields_ = [(n, ctypes.c_double) for n in ("ms_tree", "ms_p2m", "ms_m2m", "ms_tensor", "ms_s2l",
                                                 "ms_l2l", "ms_l2p", "ms_p2p", "ms_total")] + \
                [(n, ctypes.c_int64) for n in ("n_near_pairs", "n_skipped", "n_s2l_pairs",
-                                              "kernel_launches")]
+                                              "kernel_launches")] + \
+               [(n, ctypes.c_double) for n in ("ms_sort", "ms_lists", "ms_unpermute", "ms_allgather")] + \
+               [(n, ctypes.c_int64) for n in ("n_solves", "n_forward", "n_far", "n_miller",
+                                              "miller_steps")]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -79,6 +82,10 @@ def lib():
     L.cylfmm_plan_destroy.argtypes = [vp]
     L.cylfmm_plan_sync.restype = i
     L.cylfmm_plan_sync.argtypes = [vp]
+    L.cylfmm_plan_set_profiling.restype = i
+    L.cylfmm_plan_set_profiling.argtypes = [vp, i]
+    L.cylfmm_plan_read_timings.restype = i
+    L.cylfmm_plan_read_timings.argtypes = [vp, ctypes.POINTER(Timings)]
     L.cylfmm_fmm_solve.restype = i
     L.cylfmm_fmm_solve.argtypes = [vp, vp, vp, vp, i64, vp, vp, i64, vp, vp,
                                    ctypes.POINTER(Timings)]
@@ -271,6 +278,17 @@ class Plan:
 
     def sync(self):
         _check(lib().cylfmm_plan_sync(self._h), "cylfmm_plan_sync")
+
+    def set_profiling(self, on: bool):
+        """Record phase events in the following (asynchronous) solves (cylfmm_plan_set_profiling)."""
+        _check(lib().cylfmm_plan_set_profiling(self._h, int(bool(on))), "cylfmm_plan_set_profiling")
+
+    def read_timings(self) -> dict:
+        """Phase times averaged over the profiled solves since the last read
+        (cylfmm_plan_read_timings; synchronises their events)."""
+        tm = Timings()
+        _check(lib().cylfmm_plan_read_timings(self._h, ctypes.byref(tm)), "cylfmm_plan_read_timings")
+        return tm.as_dict()
 
 
 def partition_fields(src_r, src_z, fld_r, fld_z, cfg: "FMMConfig", n_parts: int):
