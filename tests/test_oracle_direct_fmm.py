@@ -264,3 +264,39 @@ def test_s2l_separate_orders_converge(orc):
     assert err(10, 10) < err(6, 10) and err(10, 10) < err(10, 6)
     assert err(6, 12) < 10 * err(6, 6) and err(12, 6) < 10 * err(6, 6)
     assert err(12, 12) < 1e-6
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 5, 6, 7])
+def test_s2l_truncation_order_by_scaling(orc, p):
+    """External pin of the S2L truncation boundary (R#8), single (i+j+k+l <= p) and double
+    (i+j <= p, k+l <= p): S2L + L2P is a truncated Taylor expansion of G^(n)(r_t, r_s, z_t - z_s)
+    in the source offset (r_s, z_s) - c_s and the target offset (r_t, z_t) - c_t.  In
+    both truncations the lowest dropped terms have total degree p + 1, so shrinking BOTH offsets
+    by a factor 2 must shrink the error against the exact G (oracle.greens, pinned to mpmath
+    legenq in test_oracle_specfun) by 2^(p+1): a '>=' for '>' slip (one degree too few) gives
+    2^p, one degree too many 2^(p+2).  Generic box pairs (no row / diagonal symmetry, which can
+    cancel the leading term), outward and inward, forward and backward.  Single truncation drops
+    terms double truncation keeps, so its error is the larger (SURVEY APP-F: 3x-30x)."""
+    h = 1.0 / 32
+    K = 4
+    S = np.array([1.0 + 0.5j, -0.7 + 0.2j, 0.3 - 0.9j, 0.8 + 0.1j])
+    for (si, sj, ti, tj) in [(10, 12, 13, 9), (13, 9, 10, 12), (9, 11, 12, 8), (12, 8, 9, 11)]:
+        cs = ((si + 0.5) * h, (sj + 0.5) * h)
+        ct = ((ti + 0.5) * h, (tj + 0.5) * h)
+        errs = {0: [], 1: []}
+        for lam in (0.5, 0.25, 0.125):
+            rs, zs = cs[0] + lam * 0.31 * h, cs[1] - lam * 0.42 * h
+            rt, zt = ct[0] - lam * 0.37 * h, ct[1] + lam * 0.26 * h
+            exact = orc.greens(rt, rs, zt - zs, K - 1) * S
+            M = orc.p2m([rs], [zs], S[None, :], p, cs[0], cs[1])
+            for trunc in (0, 1):
+                L = orc.s2l(M, p, cs[0], cs[1], ct[0], ct[1], truncation=trunc)
+                F = orc.l2p(L, p, ct[0], ct[1], rt, zt)
+                errs[trunc].append(np.abs(F - exact).max() / np.abs(exact).max())
+        for trunc, tol in ((1, 0.25), (0, 0.5)):
+            if trunc == 0 and p > 6:
+                continue   # double truncation at p = 7 reaches rounding at the smallest offset
+            e = errs[trunc]
+            rates = [math.log2(e[k] / e[k + 1]) for k in range(2)]
+            assert all(abs(r - (p + 1)) < tol for r in rates), ((si, sj, ti, tj), p, trunc, e, rates)
+        assert all(a > b for a, b in zip(errs[1], errs[0])), (errs[1], errs[0])
