@@ -79,7 +79,7 @@ static cudaError_t allow_smem(F *kernel)
 }
 
 #define P2PW_INSTANCES(X) X(9, true, false, false, false) X(17, true, false, false, false)              \
-    X(17, true, true, false, false) X(33, true, false, false, false) X(9, false, false, false, false) \
+    X(33, true, false, false, false) X(9, false, false, false, false) \
     X(17, false, false, false, false) X(33, false, false, false, false) X(33, false, false, true, false) \
     X(9, true, false, false, true) X(17, true, false, false, true) X(33, true, false, false, true)     \
     X(9, false, false, false, true) X(17, false, false, false, true) X(33, false, false, false, true) \
@@ -172,21 +172,16 @@ static int p2pw_kt(int K)
     if (K <= 17) return 17;
     return 33;
 }
-static bool p2pw_enabled(int K, bool grad)
-{
-    if (grad || K > kP2PWindow * 8) return false;
-    const char *e = getenv("CYLFMM_P2P_VARIANT");
-    return !(e && atoi(e) == 1);
-}
+// the warp-task kernel serves every potential solve; the CTA-wide kernel (p2p.cuh) the gradients
+static bool p2pw_enabled(int K, bool grad) { return !grad && K <= kP2PWindow * 8; }
 // one pass over the mode window [a.m0, a.m1) (m0 > 0 only for K > 33); direct: the direct sum
 static cudaError_t launch_p2pw(const P2PArgs &a, cudaStream_t st, bool direct = false)
 {
-    const char *e = getenv("CYLFMM_P2P_VARIANT");
     const int KW = a.m1 - a.m0;
     const int kt = p2pw_kt(a.m0 > 0 ? kP2PWWindow : a.K);
-    const bool wsm = !direct && e && atoi(e) == 2;
+    const bool wsm = false;
     const bool win = a.m0 > 0;
-    const bool exact = !win && KW == kt && !(e && atoi(e) == 3);
+    const bool exact = !win && KW == kt;
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -247,6 +242,15 @@ extern "C" cylfmm_status cylfmm_direct(const double *src_r, const double *src_z,
     nparts = (int)((n_src + per - 1) / per);
     int *d_err = nullptr;
     double2 *ws = nullptr;
+    // stream-ordered frees on every return path (including CK failures below)
+    struct AsyncFree {
+        void **q;
+        cudaStream_t s;
+        ~AsyncFree()
+        {
+            if (*q) cudaFreeAsync(*q, s);
+        }
+    } free_err{(void **)&d_err, st}, free_ws{(void **)&ws, st};
     CK(cudaMallocAsync((void **)&d_err, 2 * sizeof(int), st));
     CK(cudaMemsetAsync(d_err, 0, 2 * sizeof(int), st));
     if (nparts > 1) CK(cudaMallocAsync((void **)&ws, sizeof(double2) * (size_t)nparts * n_fld * K, st));
@@ -281,11 +285,9 @@ extern "C" cylfmm_status cylfmm_direct(const double *src_r, const double *src_z,
         reduce_parts_kernel<<<nblk(ne, 256), 256, 0, st>>>(ws, ne, nparts,
                                                           reinterpret_cast<double2 *>(out_Phi));
         CKL();
-        CK(cudaFreeAsync(ws, st));
     }
     int h_err = 0;
     CK(cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaFreeAsync(d_err, st));
     CK(cudaStreamSynchronize(st));
     if (h_err) {
         set_err("cylfmm_direct: unexcluded coincident source/field pair");
@@ -332,9 +334,8 @@ extern "C" cylfmm_status cylfmm_greens_batch(const double *r, const double *r1, 
 static cylfmm_status run_seeds(TensorGeomArgs ta, int64_t ngeom, cudaStream_t st)
 {
     size_t sm_seed = tensor_seed_smem(ta.K, ta.m1, ta.p);
-    // >= 64 threads: lanes over the 2p + 1 <= 33 series coefficients plus the two table threads
-    static const int sth = getenv("CYLFMM_SEED_THREADS") ? atoi(getenv("CYLFMM_SEED_THREADS")) : 64;
-    tensor_seed_kernel<<<(unsigned)ngeom, sth >= 64 ? sth : 64, sm_seed, st>>>(ta);
+    // 64 threads: lanes over the 2p + 1 <= 33 series coefficients plus the two table threads
+    tensor_seed_kernel<<<(unsigned)ngeom, 64, sm_seed, st>>>(ta);
     CKL();
     return CYLFMM_OK;
 }
@@ -345,9 +346,7 @@ static cylfmm_status run_fill(TensorGeomArgs ta, int64_t ngeom, cudaStream_t st)
     int KW = ta.m1 - ta.m0;
     // threads per (station, mode): the widest radial step has (p + 1)(2p + 1) entries (153 at
     // p = 8); narrower CTAs let more of them overlap their barrier-bound steps
-    // (CYLFMM_FILL_THREADS overrides, for measurement)
-    static const int fth = getenv("CYLFMM_FILL_THREADS") ? atoi(getenv("CYLFMM_FILL_THREADS")) : 0;
-    const int nth = fth > 0 ? fth : (p <= 8 ? 64 : (p <= 12 ? 128 : 256));
+    const int nth = p <= 8 ? 64 : (p <= 12 ? 128 : 256);
     tensor_fill_kernel<<<(unsigned)(ngeom * KW), nth, sm_fill, st>>>(ta);
     CKL();
     return CYLFMM_OK;
@@ -470,19 +469,19 @@ struct cylfmm_plan_s {
     size_t rtab_nm = 0, rtab_nd = 0, rtab_ntm = 0;
     // host-API staging
     DevBuf h_sr, h_sz, h_S, h_fr, h_fz, h_out;
-    cudaEvent_t ev[16];
+    cudaEvent_t ev[16] = {};
     bool ev_ok = false;
     int64_t launches = 0;
     int auto_kw = 0;   // last automatic mode chunk
     // concurrency: the data-independent tensors and the near field run on their own streams,
     // joined to the caller's stream by events (aev: start, tree, tensors, near, s2l)
     cudaStream_t aux[2] = {nullptr, nullptr};
-    cudaEvent_t aev[5];
+    cudaEvent_t aev[5] = {};
     bool aux_ok = false;
     // host-buffer solves: the coefficient rows are copied on their own stream behind the tree
     // build (hev: previous work on the caller's stream done, coefficients resident)
     cudaStream_t hcp = nullptr;
-    cudaEvent_t hev[2];
+    cudaEvent_t hev[2] = {};
     // phase events (Phases): pool reused across solves, marks of the solves since the last read
     std::vector<cudaEvent_t> evpool;
     size_t evused = 0;
@@ -562,6 +561,8 @@ static void free_plan_bufs(cylfmm_plan p)
     for (DevBuf *b : all) b->release();
 }
 
+static cylfmm_status plan_init(cylfmm_plan p, const cylfmm_params &q);
+
 extern "C" cylfmm_status cylfmm_plan_create(cylfmm_plan *plan, const cylfmm_params *prm)
 {
     if (!plan || !prm) {
@@ -581,6 +582,17 @@ extern "C" cylfmm_status cylfmm_plan_create(cylfmm_plan *plan, const cylfmm_para
     }
     RET_IF(ensure_init());
     cylfmm_plan p = new cylfmm_plan_s;
+    const cylfmm_status st = plan_init(p, q);
+    if (st != CYLFMM_OK) {
+        cylfmm_plan_destroy(p);   // releases whatever was created before the failure
+        return st;
+    }
+    *plan = p;
+    return CYLFMM_OK;
+}
+
+static cylfmm_status plan_init(cylfmm_plan p, const cylfmm_params &q)
+{
     p->prm = q;
     CK(cudaGetDevice(&p->device));
     CK(cudaDeviceGetAttribute(&p->nsm, cudaDevAttrMultiProcessorCount, p->device));
@@ -618,7 +630,6 @@ extern "C" cylfmm_status cylfmm_plan_create(cylfmm_plan *plan, const cylfmm_para
         p->rtab_nd = nd;
         p->rtab_ntm = tm_.size();
     }
-    *plan = p;
     return CYLFMM_OK;
 }
 
@@ -627,15 +638,17 @@ extern "C" void cylfmm_plan_destroy(cylfmm_plan plan)
     if (!plan) return;
     cudaDeviceSynchronize();
     free_plan_bufs(plan);
-    if (plan->ev_ok)
-        for (int i = 0; i < 16; ++i) cudaEventDestroy(plan->ev[i]);
+    // every handle is null until created, so a partly built plan is released too
+    for (cudaEvent_t e : plan->ev)
+        if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : plan->evpool) cudaEventDestroy(e);
-    if (plan->aux_ok) {
-        for (int i = 0; i < 2; ++i) cudaStreamDestroy(plan->aux[i]);
-        for (int i = 0; i < 5; ++i) cudaEventDestroy(plan->aev[i]);
-        cudaStreamDestroy(plan->hcp);
-        for (int i = 0; i < 2; ++i) cudaEventDestroy(plan->hev[i]);
-    }
+    for (cudaStream_t x : plan->aux)
+        if (x) cudaStreamDestroy(x);
+    for (cudaEvent_t e : plan->aev)
+        if (e) cudaEventDestroy(e);
+    if (plan->hcp) cudaStreamDestroy(plan->hcp);
+    for (cudaEvent_t e : plan->hev)
+        if (e) cudaEventDestroy(e);
     delete plan;
 }
 
@@ -1398,7 +1411,12 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         tm->n_miller = (int64_t)c[5];
         tm->miller_steps = (int64_t)c[6];
         RET_IF(check_err_flag(p, st));
-    } else if (p->prof_on) {
+    } else if (!q.exclude_coincident && ns > 0) {
+        // coincident pairs are an error in this mode: the near-field flag is checked here
+        // (one synchronisation), as cylfmm_direct does, not deferred to cylfmm_plan_sync
+        RET_IF(check_err_flag(p, st));
+    }
+    if (!tm && p->prof_on) {
         p->last_npairs = npairs;
         p->last_launches = p->launches;
     }
