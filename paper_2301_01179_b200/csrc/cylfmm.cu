@@ -463,6 +463,7 @@ struct cylfmm_plan_s {
     DevBuf written;                       // per-box 'local written by S2L' flags
     DevBuf pcnt, poff, khist, kstart, kcur, bstart, pairs, batches, wlist, pairbuf;   // S2L lists
     DevBuf need, lrow;                    // lazy L2L flags, compact local rows
+    DevBuf stflag, stlist;                // stations with an S2L pair
     DevBuf l2pown, l2pflag, l2ppos, l2ptask, l2pntask;   // L2P evaluating boxes and tasks
     DevBuf err, ctr;
     DevBuf rtab;     // M2M / L2L recentring tables: [rtab(p) | rtab(pl)] doubles, then tri ints
@@ -556,7 +557,7 @@ static void free_plan_bufs(cylfmm_plan p)
                      &p->scan_tmp[3], &p->sr_s, &p->sz_s, &p->S_s, &p->fr_s, &p->fz_s,
                      &p->slstart, &p->flstart, &p->flags, &p->smap, &p->skeys, &p->tmap,
                      &p->tkeys, &p->counts, &p->M, &p->Lc, &p->tens, &p->seeds, &p->tasks,
-                     &p->ntasks, &p->tcnt, &p->toff, &p->written, &p->pcnt, &p->poff, &p->khist, &p->kstart, &p->kcur, &p->bstart, &p->pairs, &p->batches, &p->wlist, &p->pairbuf, &p->need, &p->lrow, &p->l2pown, &p->l2pflag, &p->l2ppos, &p->l2ptask, &p->l2pntask, &p->err, &p->ctr, &p->rtab, &p->h_sr, &p->h_sz,
+                     &p->ntasks, &p->tcnt, &p->toff, &p->written, &p->pcnt, &p->poff, &p->khist, &p->kstart, &p->kcur, &p->bstart, &p->pairs, &p->batches, &p->wlist, &p->pairbuf, &p->need, &p->lrow, &p->stflag, &p->stlist, &p->l2pown, &p->l2pflag, &p->l2ppos, &p->l2ptask, &p->l2pntask, &p->err, &p->ctr, &p->rtab, &p->h_sr, &p->h_sz,
                      &p->h_S, &p->h_fr, &p->h_fz, &p->h_out};
     for (DevBuf *b : all) b->release();
 }
@@ -892,14 +893,6 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     ta.seeds = p->seeds.as<double>();
     ta.packed = 1;
     ta.err = p->err.as<int>();
-    if (overlap) {
-        CK(cudaEventRecord(p->aev[0], st));
-        CK(cudaStreamWaitEvent(st_t, p->aev[0], 0));
-    }
-    T.beg(PH_TENSOR, st_t);
-    RET_IF(run_seeds(ta, nstat, st_t));   // seeds of all modes once, behind the tree build
-    p->launches++;
-    T.end(PH_TENSOR, st_t);
     // ---- tree
     T.beg(PH_SORT, st);
     int *sperm = nullptr, *fperm = nullptr;
@@ -961,7 +954,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     RET_IF(p->skeys.need(sizeof(int) * ltot));
     RET_IF(p->tmap.need(sizeof(int) * ltot));
     RET_IF(p->tkeys.need(sizeof(int) * ltot));
-    RET_IF(p->counts.need(sizeof(int) * (2 * kMaxLevels + 5)));
+    RET_IF(p->counts.need(sizeof(int) * (2 * kMaxLevels + 6)));
     int *tmap_b = same ? p->smap.as<int>() : p->tmap.as<int>();
     int *tkeys_b = same ? p->skeys.as<int>() : p->tkeys.as<int>();
     const int nside = same ? 1 : 2;
@@ -1012,8 +1005,9 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     RET_IF(p->bstart.need(sizeof(int) * nkeys));
     int *cnt_ex = p->counts.as<int>() + 2 * kMaxLevels;   // [0] written targets, [1] max source
                                                           // column, [2] pairs, [3] batches,
-                                                          // [4] materialised locals
-    CK(cudaMemsetAsync(cnt_ex, 0, 5 * sizeof(int), st));
+                                                          // [4] materialised locals,
+                                                          // [5] stations with a pair
+    CK(cudaMemsetAsync(cnt_ex, 0, 6 * sizeof(int), st));
     if (ns > 0) {   // the largest source column at the leaf level bounds the stations S2L reads
         max_col_kernel<<<nblk(std::min<int64_t>(ns, pow4(d)), 256), 256, 0, st>>>(
             p->skeys.as<int>() + lvoff[d], p->counts.as<int>() + d, cnt_ex + 1);
@@ -1053,6 +1047,22 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     s2l_totals_kernel<<<1, 32, 0, st>>>(la);
     CKL();
     p->launches += 3;
+    // the stations S2L reads (a key with a pair), a compact list for the tensor kernels
+    RET_IF(p->stflag.need(sizeof(int) * nstat));
+    RET_IF(p->stlist.need(sizeof(int) * nstat));
+    {
+        int *fl = p->stflag.as<int>(), *ps = p->kcur.as<int>();   // kcur is free until the emit
+        s2l_station_flags_kernel<<<nblk(nstat, 256), 256, 0, st>>>(la.khist, (int)nstat, fl);
+        CKL();
+        CK(cudaMemcpyAsync(ps, fl, sizeof(int) * nstat, cudaMemcpyDeviceToDevice, st));
+        RET_IF(scan_excl(p, ps, nstat, st));
+        s2l_station_emit_kernel<<<nblk(nstat, 256), 256, 0, st>>>(fl, ps, (int)nstat, p->stlist.as<int>());
+        CKL();
+        l2p_ntasks_kernel<<<1, 32, 0, st>>>(ps, fl, nstat, cnt_ex + 5);
+        CKL();
+        CK(cudaMemsetAsync(la.kcur, 0, sizeof(int) * nkeys, st));
+        p->launches += 3;
+    }
     // lazy downward pass: which target locals are materialised (need = written or a child
     // needs, bottom-up, fmm_ops.cuh); only those get a row of the local storage (compact lrow)
     RET_IF(p->need.need(std::max<int64_t>(ltot, 1)));
@@ -1076,8 +1086,8 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         CKL();
         p->launches++;
     }
-    int hcnt[2 * kMaxLevels + 5] = {0};
-    CK(cudaMemcpyAsync(hcnt, p->counts.p, sizeof(int) * (2 * kMaxLevels + 5), cudaMemcpyDeviceToHost, st));
+    int hcnt[2 * kMaxLevels + 6] = {0};
+    CK(cudaMemcpyAsync(hcnt, p->counts.p, sizeof(int) * (2 * kMaxLevels + 6), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     RET_IF(check_err_flag(p, st));
     if (same)
@@ -1088,6 +1098,8 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     const int64_t nlc = hcnt[2 * kMaxLevels + 4];   // materialised locals (Lc rows)
     // stations i_in <= the largest source column (C5: 35% of them) are the only ones S2L reads
     const int64_t nstat_used = ns > 0 ? 12 * std::min<int64_t>(1 << d, hcnt[2 * kMaxLevels + 1] + 1) : 0;
+    const int64_t nstu = hcnt[2 * kMaxLevels + 5];   // stations with a pair (<= nstat_used)
+    ta.glist = p->stlist.as<int>();
     RET_IF(p->pairs.need(sizeof(int4) * std::max<int64_t>(npairs, 1)));
     RET_IF(p->batches.need(sizeof(int4) * std::max<int64_t>(nbatches, 1)));
     la.pairs = p->pairs.as<int4>();
@@ -1206,10 +1218,16 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     fa.outz = grad ? reinterpret_cast<double2 *>(out_dz) : nullptr;
     fa.need = p->need.as<unsigned char>();
     fa.lrow = p->lrow.as<int>();
-    // tree done: the near field starts behind it on its own stream
+    // tree done: the near field and the tensors start behind it on their own streams
     if (overlap) {
         CK(cudaEventRecord(p->aev[1], st));
         CK(cudaStreamWaitEvent(st_t, p->aev[1], 0));
+    }
+    if (nstu > 0) {   // seeds of all modes once, for the stations with a pair
+        T.beg(PH_TENSOR, st_t);
+        RET_IF(run_seeds(ta, nstu, st_t));
+        p->launches++;
+        T.end(PH_TENSOR, st_t);
     }
     // ---- near field: writes every field row (the far field is added by L2P)
     if (ns > 0) {
@@ -1296,8 +1314,9 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             ta.seed_m1 = K;
             if (overlap && m0 > 0) CK(cudaStreamWaitEvent(st_t, p->aev[4], 0));  // previous S2L done
             T.beg(PH_TENSOR, st_t);
-            // stations i_in <= the largest source column (C5: 35% of them) are the only ones read
-            if (nstat_used > 0) RET_IF(run_fill(ta, nstat_used, st_t));
+            // the stations with a pair are the only ones S2L reads (dense layout, i_in <= the
+            // largest source column)
+            if (nstu > 0) RET_IF(run_fill(ta, nstu, st_t));
             p->launches++;
             T.end(PH_TENSOR, st_t);
             if (overlap) CK(cudaEventRecord(p->aev[2], st_t));

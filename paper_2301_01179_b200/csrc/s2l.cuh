@@ -122,6 +122,18 @@ __global__ void s2l_batch_emit_kernel(S2LListArgs a)
     for (int q = 0; q < n; q += a.JT) a.batches[b++] = make_int4(s0 + q, min(a.JT, n - q), k, 0);
 }
 
+// stations (i_in, class) with at least one pair (either in/out key): the only tensors S2L reads
+__global__ void s2l_station_flags_kernel(const int *khist, int nstat, int *flag)
+{
+    const int st = blockIdx.x * blockDim.x + threadIdx.x;
+    if (st < nstat) flag[st] = (khist[2 * st] + khist[2 * st + 1]) > 0 ? 1 : 0;
+}
+__global__ void s2l_station_emit_kernel(const int *flag, const int *pos, int nstat, int *list)
+{
+    const int st = blockIdx.x * blockDim.x + threadIdx.x;
+    if (st < nstat && flag[st]) list[pos[st]] = st;
+}
+
 // totals of the scanned counts (one thread): pairs, batches
 __global__ void s2l_totals_kernel(S2LListArgs a)
 {

@@ -36,6 +36,7 @@ struct TensorGeomArgs {
     double *out;                 // dense [n][m1-m0][p+1][p+1][2p+1] or packed [n][m1-m0][(p+1)^3]
     int packed;
     int *err;
+    const int *glist;            // nullable: CTA b works on geometry glist[b] (used stations)
 };
 
 // The 12 Green's-expansion classes per radial station: (dI, dJ) in {0..3}^2 with
@@ -125,7 +126,7 @@ __global__ void __launch_bounds__(128) tensor_seed_kernel(TensorGeomArgs a)
     double *rho = rat + NM * D;                              // [D]
     double *den = rho + D;                                   // [D + 4]
     int *sS = reinterpret_cast<int *>(den + D + 4);          // [2]
-    const int64_t gi = blockIdx.x;
+    const int64_t gi = a.glist ? a.glist[blockIdx.x] : blockIdx.x;
     double r, r1, x;
     geometry_of(a, gi, r, r1, x);
     const int tid = threadIdx.x;
@@ -380,7 +381,7 @@ __global__ void __launch_bounds__(256) tensor_fill_kernel(TensorGeomArgs a)
     extern __shared__ double T[];            // [p+1][p+1][2p+1] of one mode
     const int p = a.p, C = 2 * p, D = C + 1, P1 = p + 1;
     const int KW = a.m1 - a.m0;
-    const int64_t gi = blockIdx.x / KW;
+    const int64_t gi = a.glist ? a.glist[blockIdx.x / KW] : blockIdx.x / KW;
     const int n = a.m0 + (int)(blockIdx.x % KW);
     const int Nw = (a.seed_m1 ? a.seed_m1 : a.m1) - 1, Ni = Nw > 1 ? Nw : 1, NM = Ni + 1;
     double r, r1, x;
