@@ -115,7 +115,6 @@ static cylfmm_status ensure_init()
     P2P_INSTANCES(X)
 #undef X
     CK(allow_smem(tensor_seed_kernel));
-    CK(allow_smem(tensor_fill_kernel));
     CK(allow_smem(p2m_kernel));
     CK(allow_smem(m2m_kernel));
     CK(allow_smem(l2l_kernel));
@@ -341,13 +340,9 @@ static cylfmm_status run_seeds(TensorGeomArgs ta, int64_t ngeom, cudaStream_t st
 }
 static cylfmm_status run_fill(TensorGeomArgs ta, int64_t ngeom, cudaStream_t st)
 {
-    const int p = ta.p, D = 2 * p + 1;
-    size_t sm_fill = sizeof(double) * (size_t)(p + 1) * (p + 1) * D;
-    int KW = ta.m1 - ta.m0;
-    // threads per (station, mode): the widest radial step has (p + 1)(2p + 1) entries (153 at
-    // p = 8); narrower CTAs let more of them overlap their barrier-bound steps
-    const int nth = p <= 8 ? 64 : (p <= 12 ? 128 : 256);
-    tensor_fill_kernel<<<(unsigned)(ngeom * KW), nth, sm_fill, st>>>(ta);
+    // warp per (station, mode), 4 warps per CTA (tensor.cuh)
+    ta.nwork = ngeom * (ta.m1 - ta.m0);
+    tensor_fill_kernel<<<nblk(ta.nwork, 4), 128, 0, st>>>(ta);
     CKL();
     return CYLFMM_OK;
 }

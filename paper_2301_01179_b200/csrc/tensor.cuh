@@ -9,9 +9,9 @@
 //     n >= 2 by the three-term recursion on Taylor series in Delta x, forward or Miller-ratio
 //     (reading R#22); Gbar_{10k}, Gbar_{01k} and the mixed Gbar_{11k}
 //     (P:993-1025).  Output: seeds[geom][4][Ni+1][2p+1].
-//  tensor_fill_kernel  (one CTA per (geometry, mode)): the whole tensor of one mode in shared
-//     memory from the seeds by the cylindrical Laplace equation, first in r (b in {0,1}) then in
-//     r1, with the axial term the printed recursion omits restored (R#6):
+//  tensor_fill_kernel  (one warp per (geometry, mode), registers and shuffles only): the tensor
+//     of one mode from the seeds by the cylindrical Laplace equation in r (b in {0,1}) and in r1
+//     (P:1027-1065), with the axial term the printed recursion omits restored (R#6):
 //       r^2 (a+1)(a+2) G_{a+2} + r (a+1)(2a+1) G_{a+1} + (a^2 - n^2) G_a
 //         + (c+1)(c+2) [ r^2 G_{a,c+2} + 2 r G_{a-1,c+2} + G_{a-2,c+2} ] = 0,
 //     parallel over (b, c) per radial step.  Written out dense ([a][b][c], c <= 2p) or packed
@@ -37,6 +37,7 @@ struct TensorGeomArgs {
     int packed;
     int *err;
     const int *glist;            // nullable: CTA b works on geometry glist[b] (used stations)
+    int64_t nwork;               // fill: (geometry, mode) items
 };
 
 // The 12 Green's-expansion classes per radial station: (dI, dJ) in {0..3}^2 with
@@ -374,87 +375,124 @@ __host__ __device__ inline int packed_off(int aa, int b, int p)
 }
 
 // ---------------------------------------------------------------------------------------------
-// CTA per (geometry, mode).  (A warp-per-(geometry, mode) variant with __syncwarp steps was
-// measured 60 us slower on C2: its 11 KB per warp halves the resident warps.)
-__global__ void __launch_bounds__(256) tensor_fill_kernel(TensorGeomArgs a)
+// Warp per (geometry, mode), no shared memory and no barriers.  Lane c holds column c of the
+// current rows (c = lane, and c = lane + 32 in a second register: only column 2p = 32 of row
+// (0, 0) at p = 16 needs it).  The Laplace recursion in r (b in {0, 1}, advancing a) and, for
+// every a as soon as its b = 0, 1 rows exist, the recursion in r1 (advancing b) keep the three
+// previous rows in registers; the (c + 2) terms come from lane c + 2 by shuffles.  Each row is
+// written out as soon as it is formed (one coalesced store per row).  Entries with a + b + c > 2p
+// are never read by a valid entry, so lanes past the end of a row carry don't-care values.
+struct Row {                 // column c (lo) and c + 32 (hi) of one tensor row
+    double lo, hi;
+};
+__device__ __forceinline__ double col_plus2(const Row &v, int lane)
 {
-    extern __shared__ double T[];            // [p+1][p+1][2p+1] of one mode
+    const double a = __shfl_down_sync(0xffffffffu, v.lo, 2);
+    const double b = __shfl_sync(0xffffffffu, v.hi, lane - 30);   // lanes 30, 31: c + 2 >= 32
+    return lane < 30 ? a : b;
+}
+
+__global__ void __launch_bounds__(128) tensor_fill_kernel(TensorGeomArgs a)
+{
     const int p = a.p, C = 2 * p, D = C + 1, P1 = p + 1;
     const int KW = a.m1 - a.m0;
-    const int64_t gi = a.glist ? a.glist[blockIdx.x / KW] : blockIdx.x / KW;
-    const int n = a.m0 + (int)(blockIdx.x % KW);
+    const int lane = threadIdx.x & 31;
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (w >= a.nwork) return;
+    const int64_t gi = a.glist ? a.glist[w / KW] : w / KW;
+    const int n = a.m0 + (int)(w % KW);
     const int Nw = (a.seed_m1 ? a.seed_m1 : a.m1) - 1, Ni = Nw > 1 ? Nw : 1, NM = Ni + 1;
     double r, r1, x;
     geometry_of(a, gi, r, r1, x);
     if (!(r > 0.0) || !(r1 > 0.0) || (r == r1 && x == 0.0)) return;   // flagged by seed kernel
-    const int tid = threadIdx.x, nth = blockDim.x;
     const double *sd = a.seeds + gi * 4 * (int64_t)NM * D;
-    for (int e = tid; e < P1 * P1 * D; e += nth) T[e] = 0.0;
-    __syncthreads();
-#define TI(A, B, Cc) T[((A) * P1 + (B)) * D + (Cc)]
-    for (int c = tid; c < D; c += nth) {
-        TI(0, 0, c) = sd[(0 * NM + n) * D + c];
-        if (c <= C - 1) {
-            if (p >= 1) {
-                TI(1, 0, c) = sd[(1 * NM + n) * D + c];
-                TI(0, 1, c) = sd[(2 * NM + n) * D + c];
-            }
-        }
-        if (c <= C - 2 && p >= 1) TI(1, 1, c) = sd[(3 * NM + n) * D + c];
-    }
-    __syncthreads();
     const double n2 = (double)n * n;
-    // Laplace in r: Gbar_{a+2,b,c}, b in {0,1}, a = 0..p-2, all c with a+2+b+c <= 2p
-    for (int aa = 0; aa + 2 <= p; ++aa) {
-        const double inv = -1.0 / (r * r * (aa + 1.0) * (aa + 2.0));
-        for (int e = tid; e < 2 * D; e += nth) {
-            int b = e / D, c = e % D;
-            if (aa + 2 + b + c > C) continue;
-            double lap = r * r * TI(aa, b, c + 2);
-            if (aa >= 1) lap = fma(2.0 * r, TI(aa - 1, b, c + 2), lap);
-            if (aa >= 2) lap += TI(aa - 2, b, c + 2);
-            double num = r * (aa + 1) * (2.0 * aa + 1) * TI(aa + 1, b, c) +
-                         (aa * (double)aa - n2) * TI(aa, b, c) + (c + 1.0) * (c + 2.0) * lap;
-            TI(aa + 2, b, c) = num * inv;
-        }
-        __syncthreads();
-    }
-    // Laplace in r1: Gbar_{a,b+2,c}, b = 0..p-2, all a <= p, c with a+b+2+c <= 2p
-    for (int bb = 0; bb + 2 <= p; ++bb) {
-        const double inv = -1.0 / (r1 * r1 * (bb + 1.0) * (bb + 2.0));
-        for (int e = tid; e < P1 * D; e += nth) {
-            int aa = e / D, c = e % D;
-            if (aa + bb + 2 + c > C) continue;
-            double lap = r1 * r1 * TI(aa, bb, c + 2);
-            if (bb >= 1) lap = fma(2.0 * r1, TI(aa, bb - 1, c + 2), lap);
-            if (bb >= 2) lap += TI(aa, bb - 2, c + 2);
-            double num = r1 * (bb + 1) * (2.0 * bb + 1) * TI(aa, bb + 1, c) +
-                         (bb * (double)bb - n2) * TI(aa, bb, c) + (c + 1.0) * (c + 2.0) * lap;
-            TI(aa, bb + 2, c) = num * inv;
-        }
-        __syncthreads();
-    }
-    // write out
+    const int c0 = lane, c1 = lane + 32;
+    // packed (FMM) layout stores H_ab(c) = c! Gbar_abc (the S2L Hankel form); dense: Gbar_abc
+    double f0 = 1.0, f1 = 1.0;
     if (a.packed) {
-        const int64_t TP = (int64_t)P1 * P1 * P1, TPp = TP + (TP & 1);   // padded: 16-B blocks
-        double *o = a.out + (gi * KW + (n - a.m0)) * TPp;
-        for (int e = tid; e < P1 * P1; e += nth) {
-            int aa = e / P1, b = e % P1;
-            const int off = packed_off(aa, b, p);
-            double f = 1.0;   // packed (FMM) layout stores H_ab(c) = c! Gbar_abc (S2L Hankel form)
-            for (int c = 0; c <= C - aa - b; ++c) {
-                if (c >= 2) f *= c;
-                o[off + c] = TI(aa, b, c) * f;
-            }
+        for (int t = 2; t <= c0; ++t) f0 *= t;
+        f1 = f0;
+        for (int t = c0 + 1; t <= c1; ++t) f1 *= t;
+    }
+    const int64_t TP = (int64_t)P1 * P1 * P1, TPp = TP + (TP & 1);   // packed: padded 16-B blocks
+    double *o = a.out + (gi * KW + (n - a.m0)) * (a.packed ? TPp : (int64_t)P1 * P1 * D);
+    auto store = [&](int aa, int b, const Row &v) {
+        const int cmax = C - aa - b;
+        if (a.packed) {
+            double *q = o + packed_off(aa, b, p);
+            if (c0 <= cmax) q[c0] = v.lo * f0;
+            if (c1 <= cmax) q[c1] = v.hi * f1;
+        } else {
+            double *q = o + ((int64_t)aa * P1 + b) * D;
+            if (c0 < D) q[c0] = c0 <= cmax ? v.lo : 0.0;
+            if (c1 < D) q[c1] = c1 <= cmax ? v.hi : 0.0;
         }
-    } else {
-        double *o = a.out + (gi * KW + (n - a.m0)) * (int64_t)P1 * P1 * D;
-        for (int e = tid; e < P1 * P1 * D; e += nth) {
-            int aa = e / (P1 * D), b = (e / D) % P1, c = e % D;
-            o[e] = (aa + b + c <= C) ? T[e] : 0.0;
+    };
+    auto seed = [&](int k, int cmax) {
+        Row v;
+        v.lo = c0 <= cmax ? sd[(k * NM + n) * D + c0] : 0.0;
+        v.hi = c1 <= cmax ? sd[(k * NM + n) * D + c1] : 0.0;
+        return v;
+    };
+    // one Laplace step: new = [ s (k+1)(2k+1) cur + (k^2 - n^2) prev
+    //                         + (c+1)(c+2) (s^2 prev[c+2] + 2 s prev2[c+2] + prev3[c+2]) ] * inv
+    // (r: s = r, rows a = k+1, k, k-1, k-2 at fixed b; r1: s = r1, rows b = k+1, k, k-1, k-2)
+    auto lap_step = [&](double sc, int k, const Row &cur, const Row &prv, const Row &pm1,
+                        const Row &pm2) {
+        const double inv = -1.0 / (sc * sc * (k + 1.0) * (k + 2.0));
+        const double t0 = col_plus2(prv, lane), t1 = k >= 1 ? col_plus2(pm1, lane) : 0.0;
+        const double t2 = k >= 2 ? col_plus2(pm2, lane) : 0.0;
+        Row nw;
+        {
+            double lap = sc * sc * t0;
+            if (k >= 1) lap = fma(2.0 * sc, t1, lap);
+            if (k >= 2) lap += t2;
+            const double num = sc * (k + 1) * (2.0 * k + 1) * cur.lo + (k * (double)k - n2) * prv.lo +
+                               (c0 + 1.0) * (c0 + 2.0) * lap;
+            nw.lo = num * inv;
+        }
+        // column c + 32 (only c = 32 at p = 16, row (0, 0), never recursed into): not needed
+        nw.hi = 0.0;
+        return nw;
+    };
+    // b = 0, 1 rows of a = 0, 1 from the seeds
+    Row ra0[4] = {}, ra1[4] = {};   // rows a-4 .. a-1 of the b = 0 (ra0) and b = 1 (ra1) planes
+    Row b0 = seed(0, C), b1 = p >= 1 ? seed(2, C - 1) : Row{};
+    Row a1b0 = p >= 1 ? seed(1, C - 1) : Row{}, a1b1 = p >= 1 ? seed(3, C - 2) : Row{};
+    for (int aa = 0; aa <= p; ++aa) {
+        Row rb0, rb1;   // rows (aa, 0) and (aa, 1)
+        if (aa == 0) {
+            rb0 = b0;
+            rb1 = b1;
+        } else if (aa == 1) {
+            rb0 = a1b0;
+            rb1 = a1b1;
+        } else {   // Laplace in r (k = aa - 2): rows k+1, k, k-1, k-2 = aa-1 .. aa-4
+            const int k = aa - 2;
+            rb0 = lap_step(r, k, ra0[3], ra0[2], ra0[1], ra0[0]);
+            rb1 = lap_step(r, k, ra1[3], ra1[2], ra1[1], ra1[0]);
+        }
+#pragma unroll
+        for (int h = 0; h < 3; ++h) {
+            ra0[h] = ra0[h + 1];
+            ra1[h] = ra1[h + 1];
+        }
+        ra0[3] = rb0;
+        ra1[3] = rb1;
+        store(aa, 0, rb0);
+        if (p >= 1) store(aa, 1, rb1);
+        // Laplace in r1 for this a: rows b + 2 from b + 1, b, b - 1, b - 2
+        Row hb[4] = {Row{}, Row{}, rb0, rb1};   // rows b-2, b-1, b, b+1 (b = 0)
+        for (int bb = 0; bb + 2 <= p && aa + bb + 2 <= C; ++bb) {
+            const Row nb = lap_step(r1, bb, hb[3], hb[2], hb[1], hb[0]);
+            hb[0] = hb[1];
+            hb[1] = hb[2];
+            hb[2] = hb[3];
+            hb[3] = nb;
+            store(aa, bb + 2, nb);
         }
     }
-#undef TI
 }
 
 }  // namespace cyl
