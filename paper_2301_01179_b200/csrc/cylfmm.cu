@@ -179,7 +179,8 @@ static cudaError_t launch_p2pw(const P2PArgs &a, cudaStream_t st, bool direct = 
     const int KW = a.m1 - a.m0;
     const int kt = p2pw_kt(a.m0 > 0 ? kP2PWWindow : a.K);
     const bool wsm = false;
-    const bool win = a.m0 > 0;
+    const bool win = a.m0 > 0;   // windows after the first (the first runs the exact-33 kernel:
+                                 // measured C5 near field 48.2 ms vs 60.0 ms with the windowed one)
     const bool exact = !win && KW == kt;
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);

@@ -72,8 +72,8 @@ __device__ __forceinline__ double2 cfma(double2 s, double g, double2 acc)
 // of the task's source list; the four partial sums are added in warp order at the end
 // (deterministic).  Persistent CTAs fetch tasks from *a.task_ctr (zeroed before the launch).
 // EXACT: the mode count equals KT (no per-mode guards).
-// WIN: a mode window [m0, m0 + KW) with m0 > 0 (K > KT: the recursions still start at mode 0;
-// only the window's modes are accumulated).
+// WIN: a mode window [m0, m0 + KW) of a K > KT solve (the recursions start at mode 0, only the
+// window's modes are accumulated; forward pairs run two per lane in lockstep; m0 = 0 works too).
 // DIRECT: the direct sum: task = (tile of 32 targets, source partition), the
 // partition's partial sums written to out + part * part_stride (reduced in fixed order after).
 template <int KT, bool EXACT, bool WSM, bool WIN = false, bool DIRECT = false>
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
                 u0B = G0B;
                 u1B = G0B * fma(-(1.0 + chB), EB * rcp_nr(KB), chB);
             }
-            if constexpr (WIN) {                        // M0 >= 2: advance to the window
+            if constexpr (WIN) {                        // advance to the window (M0 >= 2)
 #pragma unroll 4
                 for (int n = 2; n < M0; ++n) {
                     const double e = c_rec.eps[n];
@@ -279,6 +279,12 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
                 for (int j = 0; j < KT; ++j) {
                     if (j < KW) {
                         const int n = M0 + j;
+                        if (n < 2) {                    // the first window: the seeds
+                            const double gA = n == 0 ? u0A : u1A, gB = n == 0 ? u0B : u1B;
+                            acc[j] = cfma(SA[j], gA, acc[j]);
+                            if constexpr (TWO) acc[j] = cfma(SB[j], gB, acc[j]);
+                            continue;
+                        }
                         const double e = c_rec.eps[n], R = c_rec.Rn[n];
                         const double u2A = fma(dA, u1A, fma(-e, u0A, u1A));
                         acc[j] = cfma(SA[j], u2A * R, acc[j]);
@@ -408,8 +414,10 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
                         xlA = wA;
                         xnB = xlB;
                         xlB = wB;
-                        cvA *= i2A;
-                        cvB *= i2B;
+                        if (M0 + j > 0) {               // w_{M0+j} produced: (2 chi)^-1 unless n = 0
+                            cvA *= i2A;
+                            cvB *= i2B;
+                        }
                     }
                     for (int m = M0 + 1; m >= 2; --m) {
                         const double d = c_rec.delta[m];
@@ -503,10 +511,10 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
     }   // task loop
     my_skipped = __reduce_add_sync(0xffffffffu, my_skipped);
     my_pairs = __reduce_add_sync(0xffffffffu, my_pairs);
-    if (WIN) my_skipped = my_pairs = 0;                  // counted by the first window
+    if (a.m0 > 0) my_skipped = my_pairs = 0;            // counted by the first window
     if (lane == 0 && a.n_skipped && my_skipped) atomicAdd(a.n_skipped, (unsigned long long)my_skipped);
     if (lane == 0 && a.n_pairs && my_pairs) atomicAdd(a.n_pairs, (unsigned long long)my_pairs);
-    if (!WIN && a.n_branch) {
+    if (a.m0 == 0 && a.n_branch) {
         my_fwd = __reduce_add_sync(0xffffffffu, my_fwd);
         my_far = __reduce_add_sync(0xffffffffu, my_far);
         my_mil = __reduce_add_sync(0xffffffffu, my_mil);
