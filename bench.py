@@ -251,8 +251,10 @@ def main():
         fidx = dd.my_fields(part, rank)
     else:
         fidx = np.arange(len(pr.fr))
-    # sources: each rank owns a contiguous shard; N > 1 replicates them with an all-gather
-    # (NCCL over NVLink) inside every timed step -- the north_star's source replication
+    # sources: each rank owns a contiguous shard; N > 1: the library replicates them inside every
+    # timed step (cylfmm_fmm_solve_dist: NCCL all-gather of the shard sizes, grouped broadcasts of
+    # the shards, P2M split across the ranks + leaf-moment broadcasts) -- the north_star's
+    # replication of the sources and the upper tree
     sl = dd.source_shard(len(pr.sr), rank, world)
     sr_loc = torch.as_tensor(pr.sr[sl], device=dev)
     sz_loc = torch.as_tensor(pr.sz[sl], device=dev)
@@ -262,17 +264,21 @@ def main():
     fr_d = torch.as_tensor(np.ascontiguousarray(fr), device=dev)
     fz_d = torch.as_tensor(np.ascontiguousarray(fz), device=dev)
     out = torch.empty((len(fr), pr.K), dtype=torch.complex128, device=dev)
-    plan = g.Plan(cfg)
+    if world > 1:   # the library-owned NCCL communicator (id from rank 0)
+        from paper_2301_01179_b200.cylfmm import comm_unique_id
+        uid = [comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        plan = g.Plan(cfg, dist=(world, rank, uid[0]))
+    else:
+        plan = g.Plan(cfg)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
     stream = torch.cuda.current_stream()
 
     def step(timings=False):
         if world > 1:
-            sr, sz, S = dd.allgather_sources((sr_loc, sz_loc, S_loc))
-        else:
-            sr, sz, S = sr_loc, sz_loc, S_loc
-        a, bb = (sr, sz) if same else (fr_d, fz_d)
-        return plan.solve(sr, sz, S, a, bb, out=out, timings=timings)
+            return plan.solve_dist(sr_loc, sz_loc, S_loc, fr_d, fz_d, out=out, timings=timings)
+        a, bb = (sr_loc, sz_loc) if same else (fr_d, fz_d)
+        return plan.solve(sr_loc, sz_loc, S_loc, a, bb, out=out, timings=timings)
 
     # warm-up, then one synchronising timings solve outside the timed region for the counts
     # (near-field branch mix, skipped pairs); the phase times come from the timed region
@@ -316,28 +322,46 @@ def main():
     if not args.no_e2e:
         # e2e through the host-buffer C-ABI call (pinned host memory, H2D + D2H inside the region):
         # the full source set and this rank's field points in, this rank's potentials out
-        hs = [torch.as_tensor(a).pin_memory() for a in (pr.sr, pr.sz)]
-        hS = torch.as_tensor(pr.S).pin_memory()
-        hf = hs if same else [torch.as_tensor(np.ascontiguousarray(a)).pin_memory() for a in (fr, fz)]
-        hout = torch.empty((len(fr), pr.K), dtype=torch.complex128).pin_memory()
+        if world > 1:
+            # this rank's source shard and field points from pinned host memory, the solve, its
+            # potentials back to pinned host memory (the copies inside the timed region)
+            hsh = [torch.as_tensor(np.ascontiguousarray(a)).pin_memory()
+                   for a in (pr.sr[sl], pr.sz[sl])]
+            hSh = torch.as_tensor(np.ascontiguousarray(pr.S[sl])).pin_memory()
+            hf = [torch.as_tensor(np.ascontiguousarray(a)).pin_memory() for a in (fr, fz)]
+            hout = torch.empty((len(fr), pr.K), dtype=torch.complex128).pin_memory()
+
+            def e2e_step():
+                d = [x.to(dev, non_blocking=True) for x in (hsh[0], hsh[1], hSh, hf[0], hf[1])]
+                o = plan.solve_dist(d[0], d[1], d[2], d[3], d[4], out=out)
+                hout.copy_(o, non_blocking=True)
+                torch.cuda.synchronize()
+        else:
+            hs = [torch.as_tensor(a).pin_memory() for a in (pr.sr, pr.sz)]
+            hS = torch.as_tensor(pr.S).pin_memory()
+            hf = hs if same else [torch.as_tensor(np.ascontiguousarray(a)).pin_memory() for a in (fr, fz)]
+            hout = torch.empty((len(fr), pr.K), dtype=torch.complex128).pin_memory()
+
+            def e2e_step():
+                plan.solve_host(hs[0].numpy(), hs[1].numpy(), hS.numpy(), hf[0].numpy(),
+                                hf[1].numpy(), out=hout.numpy())
         for _ in range(2):
-            plan.solve_host(hs[0].numpy(), hs[1].numpy(), hS.numpy(), hf[0].numpy(), hf[1].numpy(),
-                            out=hout.numpy())
+            e2e_step()
         barrier()
         e2e_ms = []
         for _ in range(args.steps):
             flush.zero_()
-            torch.cuda.synchronize()
+            barrier()
             t0 = time.perf_counter()
-            plan.solve_host(hs[0].numpy(), hs[1].numpy(), hS.numpy(), hf[0].numpy(), hf[1].numpy(),
-                            out=hout.numpy())
+            e2e_step()
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
         t_e2e = sum(e2e_ms) / len(e2e_ms)
         if world > 1:
             tt = torch.tensor([t_e2e], device=dev, dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             t_e2e = float(tt.item())
-        h2d = len(pr.sr) * (16 + 16 * pr.K) + (0 if same else len(fr) * 16)
+        nsl = sl.stop - sl.start if world > 1 else len(pr.sr)
+        h2d = nsl * (16 + 16 * pr.K) + (0 if same else len(fr) * 16)
         d2h = len(fr) * pr.K * 16
         e2e = {"value": inter_total / (t_e2e * 1e-3), "unit": "interactions/s",
                "ms_per_step": t_e2e, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
@@ -371,8 +395,9 @@ def main():
                 "config": {"workload": f"{args.config}: {pr.name}", "n_src": len(pr.sr),
                            "n_fld": len(pr.fr), "modes": pr.K, "order": pr.p, "depth": pr.depth,
                            "truncation": "double", "miller": "accurate", "l2": "flushed",
-                           "parallelism": (f"field-partition x{world} (cost-weighted Morton ranges, "
-                                           "source all-gather)") if world > 1 else "single GPU"},
+                           "parallelism": (f"field-partition x{world} (cost-weighted Morton ranges; "
+                                           "library NCCL: source broadcast-all-gather, P2M split + "
+                                           "leaf-moment broadcast)") if world > 1 else "single GPU"},
                 "phase_ms": {k: round(v, 4) for k, v in phase.items() if k.startswith("ms_")},
                 "near_branches": {k: tm[k] for k in ("n_forward", "n_far", "n_miller", "miller_steps")},
                 "near_pairs": tm["n_near_pairs"], "s2l_box_pairs": tm["n_s2l_pairs"],

@@ -44,7 +44,7 @@ typedef enum {
     CYLFMM_EDOMAIN = 2,  /* r <= 0, non-finite coordinate, point outside the FMM domain */
     CYLFMM_ENUMERIC = 3, /* unexcluded coincident pair, non-finite result */
     CYLFMM_ECUDA = 4,    /* CUDA runtime error (message in cylfmm_last_error) */
-    CYLFMM_ENCCL = 5,    /* reserved: collective failure */
+    CYLFMM_ENCCL = 5,    /* NCCL missing or a collective failed (multi-device entry points) */
     CYLFMM_ENOMEM = 6    /* device allocation failed */
 } cylfmm_status;
 
@@ -195,6 +195,37 @@ cylfmm_status cylfmm_fmm_solve_grad(cylfmm_plan plan, const double *src_r, const
                                     const double *src_S, int64_t n_src, const double *fld_r,
                                     const double *fld_z, int64_t n_fld, double *out_Phi,
                                     double *out_dPhi_dr, double *out_dPhi_dz,
+                                    cylfmm_stream_t stream, cylfmm_timings *timings);
+
+/* ---------------------------------------------------------------------------------------
+ * Multi-device solves (BASELINE north_star: "field points are partitioned across the GPUs of one
+ * 8xB200 box, with sources and the upper tree replicated via NCCL all-gather over NVLink";
+ * SURVEY 8(b), 8(e)).  One process per GPU; the library owns the NCCL communicator (NCCL is
+ * loaded at run time: libnccl.so.2 of the process, else the system one).
+ *
+ * cylfmm_comm_unique_id: HOST out, CYLFMM_UNIQUE_ID_BYTES bytes; called on one rank, shared with
+ *   the others by the caller (e.g. a torch.distributed broadcast).  Errors: EINVAL, ENCCL.
+ * cylfmm_plan_create_dist: a plan (as cylfmm_plan_create, on the current device) with an NCCL
+ *   communicator of nranks ranks; collective (every rank calls it with the same id).  Errors:
+ *   EINVAL (bad rank/nranks/params), ENCCL (NCCL missing or init failed), as plan_create.
+ * cylfmm_fmm_solve_dist: collective solve.  Rank r passes its shard of the sources (DEVICE,
+ *   n_src_local rows; the shards in rank order form the global source set) and its own field
+ *   points (DEVICE, typically its part of cylfmm_partition_fields); out_Phi (DEVICE) receives
+ *   the potentials of ALL sources at its field points, in its input order.  Steps: shard sizes
+ *   by ncclAllGather, the shards by grouped ncclBroadcast (one per rank) into plan-owned
+ *   replicated arrays; every rank builds the identical source tree; P2M is split by contiguous
+ *   source-leaf ranges across the ranks and the leaf moments are replicated by grouped
+ *   ncclBroadcast before M2M; the rest runs for the rank's own field points.  Results equal the
+ *   single-device solve of the same field points bit for bit.  Timings: ms_allgather is the
+ *   collective time.  Errors: as cylfmm_fmm_solve, EINVAL (no communicator), ENCCL.
+ * --------------------------------------------------------------------------------------- */
+#define CYLFMM_UNIQUE_ID_BYTES 128
+cylfmm_status cylfmm_comm_unique_id(void *unique_id);
+cylfmm_status cylfmm_plan_create_dist(cylfmm_plan *plan, const cylfmm_params *prm, int nranks,
+                                      int rank, const void *unique_id);
+cylfmm_status cylfmm_fmm_solve_dist(cylfmm_plan plan, const double *src_r, const double *src_z,
+                                    const double *src_S, int64_t n_src_local, const double *fld_r,
+                                    const double *fld_z, int64_t n_fld_local, double *out_Phi,
                                     cylfmm_stream_t stream, cylfmm_timings *timings);
 
 /* Field-point partition for a multi-GPU solve (BASELINE north_star: "field points are

@@ -3,6 +3,8 @@
 #include "../../include/cylfmm.h"
 
 #include <cuda_runtime.h>
+#include <nccl.h>
+#include <dlfcn.h>
 #include <nvtx3/nvToolsExt.h>
 #include <stdarg.h>
 #include <stdio.h>
@@ -49,6 +51,52 @@ static void set_err(const char *fmt, ...)
     do {                                                                                      \
         cylfmm_status s_ = (st);                                                              \
         if (s_ != CYLFMM_OK) return s_;                                                       \
+    } while (0)
+
+// ------------------------------------------------------------------------------------------
+// NCCL, loaded at run time (only the multi-device entry points need it): the process's
+// libnccl.so.2 (PyTorch's when torch.distributed is up, else the system one).  Types from nccl.h.
+struct NcclApi {
+    bool ok = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *);
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int);
+    ncclResult_t (*CommDestroy)(ncclComm_t);
+    ncclResult_t (*Broadcast)(const void *, void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
+    ncclResult_t (*GroupStart)();
+    ncclResult_t (*GroupEnd)();
+    const char *(*GetErrorString)(ncclResult_t);
+};
+static NcclApi g_nccl;
+static std::mutex g_nccl_mu;
+static bool load_nccl()
+{
+    std::lock_guard<std::mutex> lk(g_nccl_mu);
+    if (g_nccl.ok) return true;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return false;
+#define SYM(F) g_nccl.F = reinterpret_cast<decltype(g_nccl.F)>(dlsym(h, "nccl" #F))
+    SYM(GetUniqueId);
+    SYM(CommInitRank);
+    SYM(CommDestroy);
+    SYM(Broadcast);
+    SYM(AllGather);
+    SYM(GroupStart);
+    SYM(GroupEnd);
+    SYM(GetErrorString);
+#undef SYM
+    g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.Broadcast &&
+                g_nccl.AllGather && g_nccl.GroupStart && g_nccl.GroupEnd && g_nccl.GetErrorString;
+    return g_nccl.ok;
+}
+#define NC(call)                                                                              \
+    do {                                                                                      \
+        ncclResult_t r_ = (call);                                                             \
+        if (r_ != ncclSuccess) {                                                              \
+            set_err("%s:%d %s: %s", __FILE__, __LINE__, #call, g_nccl.GetErrorString(r_));    \
+            return CYLFMM_ENCCL;                                                              \
+        }                                                                                     \
     } while (0)
 
 extern "C" const char *cylfmm_status_string(cylfmm_status s)
@@ -430,10 +478,10 @@ struct DevBuf {
 
 // Phase timing: CUDA events recorded on the stream each phase runs on (no synchronisation),
 // summed when the timings are read (after the solve has completed), plus NVTX ranges.
-enum { PH_SORT, PH_LISTS, PH_TENSOR, PH_P2M, PH_M2M, PH_S2L, PH_L2L, PH_L2P, PH_P2P, PH_TOTAL, PH_N };
+enum { PH_SORT, PH_LISTS, PH_TENSOR, PH_P2M, PH_M2M, PH_S2L, PH_L2L, PH_L2P, PH_P2P, PH_TOTAL, PH_ALLGATHER, PH_N };
 static const char *kPhaseName[PH_N] = {"cylfmm.sort", "cylfmm.lists", "cylfmm.tensor", "cylfmm.p2m",
                                        "cylfmm.m2m", "cylfmm.s2l", "cylfmm.l2l", "cylfmm.l2p",
-                                       "cylfmm.near", "cylfmm.solve"};
+                                       "cylfmm.near", "cylfmm.solve", "cylfmm.allgather"};
 struct PhaseMark {
     int ph;
     cudaEvent_t a, b;
@@ -486,6 +534,10 @@ struct cylfmm_plan_s {
     int prof_solves = 0;
     bool prof_on = false;
     int64_t last_npairs = 0, last_launches = 0;
+    // multi-device (cylfmm_plan_create_dist): the library-owned NCCL communicator
+    ncclComm_t comm = nullptr;
+    int nranks = 1, rank = 0;
+    DevBuf g_r, g_z, g_S, g_cnt;          // gathered sources, shard counts
 };
 
 static cudaEvent_t pool_event(cylfmm_plan p)
@@ -538,7 +590,7 @@ static cylfmm_status read_phases(cylfmm_plan p, cylfmm_timings *t)
     t->ms_p2p = acc[PH_P2P] / n;
     t->ms_total = acc[PH_TOTAL] / n;
     t->ms_unpermute = 0.0;   // fused into the L2P / near-field row writes (a13)
-    t->ms_allgather = 0.0;
+    t->ms_allgather = acc[PH_ALLGATHER] / n;
     t->n_solves = p->prof_solves;
     p->marks.clear();
     p->evused = 0;
@@ -554,7 +606,7 @@ static void free_plan_bufs(cylfmm_plan p)
                      &p->slstart, &p->flstart, &p->flags, &p->smap, &p->skeys, &p->tmap,
                      &p->tkeys, &p->counts, &p->M, &p->Lc, &p->tens, &p->seeds, &p->tasks,
                      &p->ntasks, &p->tcnt, &p->toff, &p->written, &p->pcnt, &p->poff, &p->khist, &p->kstart, &p->kcur, &p->bstart, &p->pairs, &p->batches, &p->wlist, &p->pairbuf, &p->need, &p->lrow, &p->stflag, &p->stlist, &p->l2pown, &p->l2pflag, &p->l2ppos, &p->l2ptask, &p->l2pntask, &p->err, &p->ctr, &p->rtab, &p->h_sr, &p->h_sz,
-                     &p->h_S, &p->h_fr, &p->h_fz, &p->h_out};
+                     &p->h_S, &p->h_fr, &p->h_fz, &p->h_out, &p->g_r, &p->g_z, &p->g_S, &p->g_cnt};
     for (DevBuf *b : all) b->release();
 }
 
@@ -644,6 +696,7 @@ extern "C" void cylfmm_plan_destroy(cylfmm_plan plan)
     for (cudaEvent_t e : plan->aev)
         if (e) cudaEventDestroy(e);
     if (plan->hcp) cudaStreamDestroy(plan->hcp);
+    if (plan->comm && g_nccl.ok) g_nccl.CommDestroy(plan->comm);
     for (cudaEvent_t e : plan->hev)
         if (e) cudaEventDestroy(e);
     delete plan;
@@ -839,9 +892,12 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
                                     const double *fld_z, int64_t nf, double *out_Phi,
                                     cudaStream_t st, cylfmm_timings *tm,
                                     double *out_dr = nullptr, double *out_dz = nullptr,
-                                    cudaEvent_t s_ready = nullptr)
+                                    cudaEvent_t s_ready = nullptr, bool dist = false)
 {
     const bool grad = out_dr != nullptr && out_dz != nullptr;
+    // multi-device solve: the leaf moments are split across the ranks (P2M of a contiguous
+    // range of source leaves each) and replicated by NCCL broadcasts (one per rank, grouped)
+    const bool split = dist && p->comm && p->nranks > 1;
     const cylfmm_params &q = p->prm;
     const int d = q.depth, K = q.n_modes, pp = q.order, P = (pp + 1) * (pp + 2) / 2;
     // local order (0 = the source order) and the tensor order max(p, pl)
@@ -850,11 +906,12 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     int KW = q.mode_chunk > 0 ? std::min(q.mode_chunk, K) : K;
     p->launches = 0;
     // phase events: always in the synchronised timings path, on request (plan profiling) else
-    if (tm) {
+    if (tm && !dist) {
         p->marks.clear();
         p->evused = 0;
         p->prof_solves = 0;
     }
+    if (tm && dist) p->prof_solves = 0;
     Phases T{p, tm != nullptr || p->prof_on, {}};
     if (T.on) p->prof_solves++;
     RET_IF(p->err.need(sizeof(int)));
@@ -1154,6 +1211,17 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             KW = p->auto_kw > 0 ? std::min(p->auto_kw, K) : K;
         }
     }
+    if (split) {   // the moment broadcasts run per mode chunk: every rank takes the smallest chunk
+        RET_IF(p->g_cnt.need(sizeof(int64_t) * (p->nranks + 1)));
+        int64_t *dkw = p->g_cnt.as<int64_t>();
+        const int64_t mine = KW;
+        CK(cudaMemcpyAsync(dkw + p->nranks, &mine, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        NC(g_nccl.AllGather(dkw + p->nranks, dkw, 1, ncclInt64, p->comm, st));
+        std::vector<int64_t> kws((size_t)p->nranks);
+        CK(cudaMemcpyAsync(kws.data(), dkw, sizeof(int64_t) * p->nranks, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        for (int64_t v : kws) KW = (int)std::min<int64_t>(KW, v);
+    }
     RET_IF(p->M.need(sizeof(double2) * (size_t)std::max<int64_t>(stot, 1) * KW * P));
     RET_IF(p->Lc.need(sizeof(double2) * (size_t)std::max<int64_t>(nlc, 1) * KW * Pl));
     RET_IF(p->tens.need(sizeof(double) * (size_t)std::max<int64_t>(nstat_used, 1) * KW * TP));
@@ -1319,13 +1387,29 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         }
         if (ns > 0) {
             T.beg(PH_P2M, st);
-            if (fa.scount[d] > 0) {
+            const int nl = fa.scount[d];
+            auto leaf0 = [&](int r) { return (int)((int64_t)nl * r / (split ? p->nranks : 1)); };
+            const int a0 = split ? leaf0(p->rank) : 0, a1 = split ? leaf0(p->rank + 1) : nl;
+            if (a1 > a0) {
                 const int nmb = (kw + kP2MModes - 1) / kP2MModes;
-                p2m_kernel<<<(unsigned)((int64_t)fa.scount[d] * nmb), kP2MThreads, p2m_smem(P, pp), st>>>(fa);
+                fa.p2m_slot0 = a0;
+                p2m_kernel<<<(unsigned)((int64_t)(a1 - a0) * nmb), kP2MThreads, p2m_smem(P, pp), st>>>(fa);
                 CKL();
                 p->launches++;
             }
             T.end(PH_P2M, st);
+            if (split && nl > 0) {   // every rank's leaf moments to every rank
+                T.beg(PH_ALLGATHER, st);
+                NC(g_nccl.GroupStart());
+                for (int r = 0; r < p->nranks; ++r) {
+                    const int b0 = leaf0(r), b1 = leaf0(r + 1);
+                    if (b1 <= b0) continue;
+                    double *base = reinterpret_cast<double *>(fa.M + (fa.soff[d] + b0) * (int64_t)kw * P);
+                    NC(g_nccl.Broadcast(base, base, (size_t)(b1 - b0) * kw * P * 2, ncclFloat64, r, p->comm, st));
+                }
+                NC(g_nccl.GroupEnd());
+                T.end(PH_ALLGATHER, st);
+            }
             T.beg(PH_M2M, st);
             for (int l = d - 1; l >= 2; --l) {
                 if (fa.scount[l] == 0) continue;
@@ -1532,6 +1616,109 @@ extern "C" cylfmm_status cylfmm_fmm_solve_host(cylfmm_plan plan, const double *s
         CK(cudaMemcpyAsync(out_Phi, plan->h_out.p, 16 * (size_t)n_fld * K, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     return check_err_flag(plan, st);
+}
+
+// ------------------------------------------------------------------------------------------
+// multi-device solves (one process per GPU, a library-owned NCCL communicator)
+extern "C" cylfmm_status cylfmm_comm_unique_id(void *unique_id)
+{
+    if (!unique_id) {
+        set_err("cylfmm_comm_unique_id: null pointer");
+        return CYLFMM_EINVAL;
+    }
+    if (!load_nccl()) {
+        set_err("cylfmm_comm_unique_id: libnccl.so.2 not found");
+        return CYLFMM_ENCCL;
+    }
+    ncclUniqueId id;
+    NC(g_nccl.GetUniqueId(&id));
+    memcpy(unique_id, &id, sizeof id);
+    return CYLFMM_OK;
+}
+
+extern "C" cylfmm_status cylfmm_plan_create_dist(cylfmm_plan *plan, const cylfmm_params *prm,
+                                                 int nranks, int rank, const void *unique_id)
+{
+    if (!plan || !prm || !unique_id || nranks < 1 || rank < 0 || rank >= nranks) {
+        set_err("cylfmm_plan_create_dist: bad arguments (nranks=%d rank=%d)", nranks, rank);
+        return CYLFMM_EINVAL;
+    }
+    if (!load_nccl()) {
+        set_err("cylfmm_plan_create_dist: libnccl.so.2 not found");
+        return CYLFMM_ENCCL;
+    }
+    RET_IF(cylfmm_plan_create(plan, prm));
+    cylfmm_plan p = *plan;
+    ncclUniqueId id;
+    memcpy(&id, unique_id, sizeof id);
+    const ncclResult_t r = g_nccl.CommInitRank(&p->comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+        set_err("cylfmm_plan_create_dist: ncclCommInitRank: %s", g_nccl.GetErrorString(r));
+        p->comm = nullptr;
+        cylfmm_plan_destroy(p);
+        *plan = nullptr;
+        return CYLFMM_ENCCL;
+    }
+    p->nranks = nranks;
+    p->rank = rank;
+    return CYLFMM_OK;
+}
+
+extern "C" cylfmm_status cylfmm_fmm_solve_dist(cylfmm_plan plan, const double *src_r,
+                                               const double *src_z, const double *src_S,
+                                               int64_t n_src_local, const double *fld_r,
+                                               const double *fld_z, int64_t n_fld_local,
+                                               double *out_Phi, cylfmm_stream_t stream,
+                                               cylfmm_timings *timings)
+{
+    RET_IF(validate_solve(plan, src_r, src_z, src_S, n_src_local, fld_r, fld_z, n_fld_local, out_Phi));
+    if (!plan->comm) {
+        set_err("cylfmm_fmm_solve_dist: the plan has no communicator (cylfmm_plan_create_dist)");
+        return CYLFMM_EINVAL;
+    }
+    CK(cudaSetDevice(plan->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const int R = plan->nranks, K = plan->prm.n_modes;
+    // shard sizes of every rank (all-gather), then the shards themselves: one broadcast per
+    // rank, grouped (NCCL over NVLink / NVSwitch), into the plan's replicated source arrays
+    RET_IF(plan->g_cnt.need(sizeof(int64_t) * (R + 1)));
+    int64_t *dcnt = plan->g_cnt.as<int64_t>();
+    CK(cudaMemcpyAsync(dcnt + R, &n_src_local, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    NC(g_nccl.AllGather(dcnt + R, dcnt, 1, ncclInt64, plan->comm, st));
+    std::vector<int64_t> cnt((size_t)R), off((size_t)R + 1, 0);
+    CK(cudaMemcpyAsync(cnt.data(), dcnt, sizeof(int64_t) * R, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int r = 0; r < R; ++r) off[r + 1] = off[r] + cnt[r];
+    const int64_t ns = off[R];
+    if (ns > INT32_MAX) {
+        set_err("cylfmm_fmm_solve_dist: %lld sources in total", (long long)ns);
+        return CYLFMM_EINVAL;
+    }
+    RET_IF(plan->g_r.need(8 * (size_t)std::max<int64_t>(ns, 1)));
+    RET_IF(plan->g_z.need(8 * (size_t)std::max<int64_t>(ns, 1)));
+    RET_IF(plan->g_S.need(16 * (size_t)std::max<int64_t>(ns, 1) * K));
+    double *gr = plan->g_r.as<double>(), *gz = plan->g_z.as<double>(), *gS = plan->g_S.as<double>();
+    Phases T{plan, timings != nullptr || plan->prof_on, {}};
+    if (timings) {
+        plan->marks.clear();
+        plan->evused = 0;
+    }
+    T.beg(PH_ALLGATHER, st);
+    NC(g_nccl.GroupStart());
+    for (int r = 0; r < R; ++r) {
+        if (cnt[r] == 0) continue;
+        const bool me = r == plan->rank;
+        NC(g_nccl.Broadcast(me ? src_r : gr + off[r], gr + off[r], cnt[r], ncclFloat64, r, plan->comm, st));
+        NC(g_nccl.Broadcast(me ? src_z : gz + off[r], gz + off[r], cnt[r], ncclFloat64, r, plan->comm, st));
+        NC(g_nccl.Broadcast(me ? src_S : gS + 2 * off[r] * K, gS + 2 * off[r] * K, 2 * cnt[r] * K,
+                            ncclFloat64, r, plan->comm, st));
+    }
+    NC(g_nccl.GroupEnd());
+    T.end(PH_ALLGATHER, st);
+    // the gathered-source marks stay in the plan's list: the solve adds its own (a timings
+    // solve keeps them, see fmm_solve_impl) and the moment broadcasts
+    return fmm_solve_impl(plan, gr, gz, gS, ns, fld_r, fld_z, n_fld_local, out_Phi, st, timings,
+                          nullptr, nullptr, nullptr, true);
 }
 
 // ------------------------------------------------------------------------------------------

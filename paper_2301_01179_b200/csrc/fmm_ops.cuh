@@ -50,6 +50,7 @@ struct FarArgs {
     int l2p_accumulate;                 // L2P adds onto out (the near field wrote it first)
     int64_t tfield;                     // field points (L2P)
     int l2p_tp;                         // L2P task size (points)
+    int p2m_slot0;                      // P2M: first leaf slot (multi-device split)
     // recentring tables (host-built once per plan, recentre_tables_host): [cm | cl] 4 (p+1)^2
     // doubles and [tri_i | tri_j] 2 P ints, for the source order (M2M) and the local order (L2L)
     const double *rtab_m, *rtab_l;
@@ -91,7 +92,7 @@ __global__ void __launch_bounds__(kP2MThreads) p2m_kernel(FarArgs a)
     extern __shared__ double sm[];
     const int p = a.p, P = a.P, KW = a.m1 - a.m0, d = a.depth;
     const int nmb = (KW + kP2MModes - 1) / kP2MModes;
-    const int slot = blockIdx.x / nmb, n0 = (blockIdx.x % nmb) * kP2MModes;
+    const int slot = a.p2m_slot0 + blockIdx.x / nmb, n0 = (blockIdx.x % nmb) * kP2MModes;
     const int nm = min(kP2MModes, KW - n0);
     double *mono = sm;                                                  // [kP2MSrc][P]
     double2 *Sx = reinterpret_cast<double2 *>(mono + kP2MSrc * P);      // [kP2MSrc][kP2MModes]

@@ -82,6 +82,13 @@ def lib():
     L.cylfmm_plan_destroy.argtypes = [vp]
     L.cylfmm_plan_sync.restype = i
     L.cylfmm_plan_sync.argtypes = [vp]
+    L.cylfmm_comm_unique_id.restype = i
+    L.cylfmm_comm_unique_id.argtypes = [vp]
+    L.cylfmm_plan_create_dist.restype = i
+    L.cylfmm_plan_create_dist.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(Params), i, i, vp]
+    L.cylfmm_fmm_solve_dist.restype = i
+    L.cylfmm_fmm_solve_dist.argtypes = [vp, vp, vp, vp, i64, vp, vp, i64, vp, vp,
+                                         ctypes.POINTER(Timings)]
     L.cylfmm_plan_set_profiling.restype = i
     L.cylfmm_plan_set_profiling.argtypes = [vp, i]
     L.cylfmm_plan_read_timings.restype = i
@@ -203,17 +210,32 @@ class FMMConfig:
     order_local: int = 0      # local-expansion order (0: = order)
 
 
-class Plan:
-    """An FMM plan (cylfmm_plan_create); owns its device workspace."""
+def comm_unique_id() -> bytes:
+    """An NCCL unique id for cylfmm_plan_create_dist (cylfmm_comm_unique_id), 128 bytes."""
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().cylfmm_comm_unique_id(buf), "cylfmm_comm_unique_id")
+    return buf.raw
 
-    def __init__(self, cfg: FMMConfig):
+
+class Plan:
+    """An FMM plan (cylfmm_plan_create); owns its device workspace.  With dist=(nranks, rank,
+    unique_id) the plan also owns an NCCL communicator (cylfmm_plan_create_dist, collective) and
+    solve_dist runs the multi-device solve."""
+
+    def __init__(self, cfg: FMMConfig, dist=None):
         _torch()
         self.cfg = cfg
         prm = Params(cfg.n_modes, cfg.order, cfg.depth, cfg.truncation, cfg.miller,
                      int(bool(cfg.exclude_coincident)), float(cfg.z0), float(cfg.L),
                      cfg.mode_chunk, cfg.order_local)
         h = ctypes.c_void_p()
-        _check(lib().cylfmm_plan_create(ctypes.byref(h), ctypes.byref(prm)), "cylfmm_plan_create")
+        if dist is None:
+            _check(lib().cylfmm_plan_create(ctypes.byref(h), ctypes.byref(prm)), "cylfmm_plan_create")
+        else:
+            nranks, rank, uid = dist
+            ub = ctypes.create_string_buffer(bytes(uid), 128)
+            _check(lib().cylfmm_plan_create_dist(ctypes.byref(h), ctypes.byref(prm), int(nranks),
+                                                 int(rank), ub), "cylfmm_plan_create_dist")
         self._h = h
 
     def close(self):
@@ -242,6 +264,22 @@ class Plan:
                                       nf, _ptr(out), _stream(torch),
                                       ctypes.byref(tm) if tm is not None else None),
                "cylfmm_fmm_solve")
+        return (out, tm.as_dict()) if timings else out
+
+    def solve_dist(self, src_r, src_z, src_S, fld_r, fld_z, out=None, timings=False):
+        """Collective multi-device solve (cylfmm_fmm_solve_dist): this rank's source shard and
+        field points in, the potentials of all sources at its field points out (cuda)."""
+        torch = _torch()
+        sr, sz, fr, fz = (_dev_f64(a, torch) for a in (src_r, src_z, fld_r, fld_z))
+        S = _dev_c128(src_S, torch)
+        ns, nf = S.shape[0], fr.shape[0]
+        if out is None:
+            out = torch.empty((nf, self.cfg.n_modes), dtype=torch.complex128, device="cuda")
+        tm = Timings() if timings else None
+        _check(lib().cylfmm_fmm_solve_dist(self._h, _ptr(sr), _ptr(sz), _ptr(S), ns, _ptr(fr),
+                                           _ptr(fz), nf, _ptr(out), _stream(torch),
+                                           ctypes.byref(tm) if tm is not None else None),
+               "cylfmm_fmm_solve_dist")
         return (out, tm.as_dict()) if timings else out
 
     def solve_grad(self, src_r, src_z, src_S, fld_r, fld_z, timings=False):

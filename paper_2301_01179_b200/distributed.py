@@ -1,8 +1,9 @@
-"""Multi-GPU driver logic (BASELINE north_star): one process per GPU, field points
+"""Multi-GPU host helpers (BASELINE north_star): one process per GPU, field points
 partitioned across ranks by cost-weighted contiguous Morton ranges (cylfmm_partition_fields),
-sources replicated by an all-gather of the per-rank source shards, outputs optionally gathered
-back.  torch.distributed supplies the collectives (NCCL over NVLink on the GPU box; gloo in the
-CPU tests); every compute step runs in libcylfmm.so.
+the rank's contiguous source shard, and the optional gather of the per-rank outputs.  The
+device solve replicates the sources and the leaf moments itself (cylfmm_fmm_solve_dist, a
+library-owned NCCL communicator: Plan(cfg, dist=(nranks, rank, comm_unique_id()))); the
+torch.distributed all-gather helpers below serve the output gather and the gloo CPU tests.
 
 The FMM result at a field point depends only on the sources and on its own box chain, so each
 rank's solve over its own field points reproduces the single-GPU values bitwise."""

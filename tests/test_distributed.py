@@ -1,9 +1,12 @@
-"""Multi-rank host logic of the field-partitioned solve (paper_2301_01179_b200/distributed.py,
-SURVEY 8(e)) with world_size 2 over gloo on the CPU: source all-gather, the cost-weighted Morton
-field partition (cylfmm_partition_fields, host-only), per-rank solves and the output gather.
-The per-rank solve here is the oracle FMM (test infrastructure) standing in for the device
-solve: the assembled result must equal the single-process result bit for bit, because the FMM
-value at a field point depends only on the sources and on its own box chain."""
+"""Multi-rank host logic of the field-partitioned solve with world_size 2 over gloo
+on the CPU: source shards replicated by all-gather (the library does it with NCCL inside
+cylfmm_fmm_solve_dist), the cost-weighted Morton field partition (cylfmm_partition_fields,
+host-only, identical on every rank), per-rank solves over the rank's own field points and the
+output gather.  There is no GPU here, so the per-rank solve is the oracle FMM (test
+infrastructure) standing in for the device solve; the device side of the same claim -- each
+part solved through libcylfmm equals the one-solve result bit for bit -- is
+tests/test_gpu_parity.py::test_partitioned_solve_bitwise, and the library's NCCL path is
+test_dist_solve_single_rank_bitwise."""
 import os
 import socket
 

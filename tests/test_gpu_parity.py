@@ -480,3 +480,27 @@ def test_fmm_gradients_vs_oracle_fmm(gpu, orc, n, K, p, depth, same):
     # and Phi from the gradient solve equals the plain solve (the plain solve may run the
     # warp-task near-field kernel: same pairs, another summation order)
     assert eps_modes(F.cpu().numpy(), plan.solve(sr, sz, S, fr, fz).cpu().numpy()).max() <= 1e-13
+
+
+@pytest.mark.parametrize("name", ["C2", "sparse"])
+def test_dist_solve_single_rank_bitwise(gpu, name):
+    """The library-owned NCCL path (cylfmm_plan_create_dist / cylfmm_fmm_solve_dist) on a
+    one-rank communicator: shard-size all-gather, shard broadcasts into the replicated source
+    arrays, the P2M leaf split and moment broadcast, then the solve -- equal to the plain
+    device solve bit for bit.  (This box has one GPU; NCCL does not run two ranks on one device.)"""
+    import torch
+    sr, sz, S, fr, fz, p, depth, L, z0 = _partition_case(name)
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=dev)  # noqa: E731
+    cfg = gpu.FMMConfig(n_modes=S.shape[1], order=p, depth=depth, L=L, z0=z0)
+    plan = gpu.Plan(cfg)
+    ref = plan.solve(t(sr), t(sz), t(S), t(fr), t(fz)).cpu().numpy()
+    plan.close()
+    from paper_2301_01179_b200.cylfmm import comm_unique_id
+    dplan = gpu.Plan(cfg, dist=(1, 0, comm_unique_id()))
+    out, tm = dplan.solve_dist(t(sr), t(sz), t(S), t(fr), t(fz), timings=True)
+    assert np.array_equal(out.cpu().numpy(), ref)
+    assert tm["ms_allgather"] >= 0.0 and tm["n_near_pairs"] > 0
+    out2 = dplan.solve_dist(t(sr), t(sz), t(S), t(fr), t(fz)).cpu().numpy()
+    assert np.array_equal(out2, ref)
+    dplan.close()
