@@ -1,22 +1,16 @@
 #!/bin/bash
-# One gpurun call: GPU tests, the C5 diagnostic, a bench line, the ncu launch list, one --set
-# full capture of the top kernels, and the C2..C5 full-size configs with oracle parity.
+# Round evidence in one gpurun call: GPU tests, smoke, bench lines (C5 headline, C2), the ncu
+# launch list of the C5 bench command, and --set full captures of the two top C5 kernels.
+#   tools/gpu_round.sh <tag>
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
-rm -f gpurun_out/cfg_*.json
-nvidia-smi > gpurun_out/nvsmi.txt 2>&1
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
-CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline"
-timeout 300 $CMD > gpurun_out/plain.log 2>&1 && \
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
-   --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
-echo "ncu1 rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"s2l_kernel|p2p_warp" -s 6 -c 2 \
-   -o gpurun_out/prof $CMD > gpurun_out/ncu_full.log 2>&1
-echo "ncu2 rc=$?"
-timeout 900 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
-timeout 900 python tools/direct_speedup.py C2 C3 > gpurun_out/speedup.jsonl 2> gpurun_out/speedup.err
-for c in C2 C3 C4 C5; do
-  timeout 1200 python tools/run_config.py $c --sample 96 > gpurun_out/cfg_$c.json 2> gpurun_out/cfg_$c.err; echo "$c rc=$?"
+TAG=${1:-r}
+nvidia-smi > gpurun_out/${TAG}_nvsmi.txt 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/${TAG}_pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/${TAG}_pytest_gpu.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/${TAG}_smoke.log
+bash tools/gpu_bench.sh ${TAG}
+for k in "p2p_warp:2" "s2l_batch:1"; do
+  KR=${k%%:*}; N=${k##*:}
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"$KR" -s $N -c $N \
+     -o gpurun_out/${TAG}_full_${KR}_C5 -f python tools/solve_once.py C5 > gpurun_out/${TAG}_full_${KR}_C5.log 2>&1; echo "ncu full $KR rc=$?"
 done

@@ -34,6 +34,8 @@ def launches(path):
             data.append(dict(zip(hdr, r)))
     agg = defaultdict(lambda: [0, 0.0])
     for d in data:
+        if d.get("Metric Name", "gpu__time_duration.sum") != "gpu__time_duration.sum":
+            continue
         k = d["Kernel Name"].split("(")[0]
         agg[k][0] += 1
         agg[k][1] += float(d["Metric Value"])
