@@ -506,7 +506,7 @@ struct cylfmm_plan_s {
     DevBuf tasks, ntasks, tcnt, toff;
     DevBuf written;                       // per-box 'local written by S2L' flags
     DevBuf pcnt, poff, khist, kstart, kcur, bstart, pairs, batches, wlist, pairbuf;   // S2L lists
-    DevBuf need, lrow;                    // lazy L2L flags, compact local rows
+    DevBuf need, lrow, rowkey, lvoffd;    // lazy L2L flags, compact local rows, row -> box
     DevBuf stflag, stlist;                // stations with an S2L pair
     DevBuf l2pown, l2pflag, l2ppos, l2ptask, l2pntask;   // L2P evaluating boxes and tasks
     DevBuf err, ctr;
@@ -605,7 +605,7 @@ static void free_plan_bufs(cylfmm_plan p)
                      &p->scan_tmp[3], &p->sr_s, &p->sz_s, &p->S_s, &p->fr_s, &p->fz_s,
                      &p->slstart, &p->flstart, &p->flags, &p->smap, &p->skeys, &p->tmap,
                      &p->tkeys, &p->counts, &p->M, &p->Lc, &p->tens, &p->seeds, &p->tasks,
-                     &p->ntasks, &p->tcnt, &p->toff, &p->written, &p->pcnt, &p->poff, &p->khist, &p->kstart, &p->kcur, &p->bstart, &p->pairs, &p->batches, &p->wlist, &p->pairbuf, &p->need, &p->lrow, &p->stflag, &p->stlist, &p->l2pown, &p->l2pflag, &p->l2ppos, &p->l2ptask, &p->l2pntask, &p->err, &p->ctr, &p->rtab, &p->h_sr, &p->h_sz,
+                     &p->ntasks, &p->tcnt, &p->toff, &p->written, &p->pcnt, &p->poff, &p->khist, &p->kstart, &p->kcur, &p->bstart, &p->pairs, &p->batches, &p->wlist, &p->pairbuf, &p->need, &p->lrow, &p->rowkey, &p->lvoffd, &p->stflag, &p->stlist, &p->l2pown, &p->l2pflag, &p->l2ppos, &p->l2ptask, &p->l2pntask, &p->err, &p->ctr, &p->rtab, &p->h_sr, &p->h_sz,
                      &p->h_S, &p->h_fr, &p->h_fz, &p->h_out, &p->g_r, &p->g_z, &p->g_S, &p->g_cnt};
     for (DevBuf *b : all) b->release();
 }
@@ -1007,7 +1007,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     RET_IF(p->skeys.need(sizeof(int) * ltot));
     RET_IF(p->tmap.need(sizeof(int) * ltot));
     RET_IF(p->tkeys.need(sizeof(int) * ltot));
-    RET_IF(p->counts.need(sizeof(int) * (2 * kMaxLevels + 6)));
+    RET_IF(p->counts.need(sizeof(int) * (3 * kMaxLevels + 8)));
     int *tmap_b = same ? p->smap.as<int>() : p->tmap.as<int>();
     int *tkeys_b = same ? p->skeys.as<int>() : p->tkeys.as<int>();
     const int nside = same ? 1 : 2;
@@ -1059,7 +1059,8 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     int *cnt_ex = p->counts.as<int>() + 2 * kMaxLevels;   // [0] written targets, [1] max source
                                                           // column, [2] pairs, [3] batches,
                                                           // [4] materialised locals,
-                                                          // [5] stations with a pair
+                                                          // [5] stations with a pair,
+                                                          // [6 + l] first local row of level l
     CK(cudaMemsetAsync(cnt_ex, 0, 6 * sizeof(int), st));
     if (ns > 0) {   // the largest source column at the leaf level bounds the stations S2L reads
         max_col_kernel<<<nblk(std::min<int64_t>(ns, pow4(d)), 256), 256, 0, st>>>(
@@ -1137,10 +1138,20 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         count_total_kernel<<<1, 32, 0, st>>>(p->lrow.as<int>(), p->need.as<unsigned char>(), ltot,
                                              cnt_ex + 4);
         CKL();
-        p->launches++;
+        // row -> dense position, first row of each level (L2L walks materialised boxes only)
+        RET_IF(p->rowkey.need(sizeof(int64_t) * std::max<int64_t>(ltot, 1)));
+        RET_IF(p->lvoffd.need(sizeof(int64_t) * (kMaxLevels + 2)));
+        CK(cudaMemcpyAsync(p->lvoffd.p, lvoff, sizeof(int64_t) * (d + 2), cudaMemcpyHostToDevice, st));
+        need_rows_kernel<<<nblk(ltot, 256), 256, 0, st>>>(p->lrow.as<int>(), p->need.as<unsigned char>(),
+                                                         ltot, p->rowkey.as<int64_t>());
+        CKL();
+        level_rows_kernel<<<1, 32, 0, st>>>(p->lrow.as<int>(), p->need.as<unsigned char>(),
+                                            p->lvoffd.as<int64_t>(), d, cnt_ex + 6);
+        CKL();
+        p->launches += 3;
     }
-    int hcnt[2 * kMaxLevels + 6] = {0};
-    CK(cudaMemcpyAsync(hcnt, p->counts.p, sizeof(int) * (2 * kMaxLevels + 6), cudaMemcpyDeviceToHost, st));
+    int hcnt[3 * kMaxLevels + 8] = {0};
+    CK(cudaMemcpyAsync(hcnt, p->counts.p, sizeof(int) * (3 * kMaxLevels + 8), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     RET_IF(check_err_flag(p, st));
     if (same)
@@ -1282,6 +1293,8 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     fa.outz = grad ? reinterpret_cast<double2 *>(out_dz) : nullptr;
     fa.need = p->need.as<unsigned char>();
     fa.lrow = p->lrow.as<int>();
+    fa.rowkey = p->rowkey.as<int64_t>();
+    for (int l = 2; l <= d + 1; ++l) fa.lrow_lev[l] = hcnt[2 * kMaxLevels + 6 + l];
     // tree done: the near field and the tensors start behind it on their own streams
     if (overlap) {
         CK(cudaEventRecord(p->aev[1], st));
@@ -1442,8 +1455,9 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         if (overlap) CK(cudaEventRecord(p->aev[4], st));
         T.beg(PH_L2L, st);
         for (int l = 3; l <= d; ++l) {
-            if (fa.tcount[l] == 0) continue;
-            int64_t items = (int64_t)fa.tcount[l] * kw;
+            const int64_t nrow = fa.lrow_lev[l + 1] - fa.lrow_lev[l];
+            if (nrow == 0) continue;
+            int64_t items = nrow * kw;
             unsigned g = (unsigned)std::min<int64_t>((items + kL2LWarps - 1) / kL2LWarps,
                                                      (int64_t)p->nsm * 8);
             l2l_kernel<<<g, 32 * kL2LWarps, l2l_smem(pl), st>>>(fa, l);

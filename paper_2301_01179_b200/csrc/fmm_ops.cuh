@@ -47,6 +47,8 @@ struct FarArgs {
     int64_t lvoff[kMaxLevels];          // dense per-level offsets (level maps, s2l_written)
     const unsigned char *need;          // dense per level: local materialised (see need_kernel)
     const int *lrow;                    // dense per level: Lc row of a materialised local
+    const int64_t *rowkey;              // Lc row -> dense position (lvoff[l] + key)
+    int lrow_lev[kMaxLevels + 1];       // first Lc row of each level (rows are level-major)
     int l2p_accumulate;                 // L2P adds onto out (the near field wrote it first)
     int64_t tfield;                     // field points (L2P)
     int l2p_tp;                         // L2P task size (points)
@@ -91,9 +93,11 @@ __global__ void __launch_bounds__(kP2MThreads) p2m_kernel(FarArgs a)
 {
     extern __shared__ double sm[];
     const int p = a.p, P = a.P, KW = a.m1 - a.m0, d = a.depth;
+    // balanced mode blocks of <= kP2MModes (K = 65: 5 x 13, not 4 x 16 + 1)
     const int nmb = (KW + kP2MModes - 1) / kP2MModes;
-    const int slot = a.p2m_slot0 + blockIdx.x / nmb, n0 = (blockIdx.x % nmb) * kP2MModes;
-    const int nm = min(kP2MModes, KW - n0);
+    const int mb = blockIdx.x % nmb;
+    const int slot = a.p2m_slot0 + blockIdx.x / nmb, n0 = (KW * mb) / nmb;
+    const int nm = (KW * (mb + 1)) / nmb - n0;
     double *mono = sm;                                                  // [kP2MSrc][P]
     double2 *Sx = reinterpret_cast<double2 *>(mono + kP2MSrc * P);      // [kP2MSrc][kP2MModes]
     double *pw = reinterpret_cast<double *>(Sx + kP2MSrc * kP2MModes);  // [kP2MSrc][2][p+1]
@@ -112,7 +116,7 @@ __global__ void __launch_bounds__(kP2MThreads) p2m_kernel(FarArgs a)
     const int q0 = a.slstart[key], q1 = a.slstart[key + 1];
     const int tn = threadIdx.x % (kP2MModes / 2), tc = threadIdx.x / (kP2MModes / 2);
     const int c0 = tc * kP2MRC;
-    const bool active = c0 < P;
+    const bool active = c0 < P && 2 * tn < nm;
     double2 acc[2][kP2MRC];
 #pragma unroll
     for (int v = 0; v < 2; ++v)
@@ -309,6 +313,23 @@ __global__ void __launch_bounds__(256) m2m_kernel(FarArgs a, int level)
 // inputs (C2, C3) need every box; surface inputs (C5) skip L2L for most of the 700k boxes.
 // Dense form (thread per position of the level, before the host knows the level counts):
 // need[g] for g = lvoff[l] + key, and needi[g] = need as int (scanned into the compact Lc row).
+// Lc row -> dense position, and the first row of every level (lrow is an exclusive scan of the
+// dense need flags, so the rows of a level are contiguous)
+__global__ void need_rows_kernel(const int *lrow, const unsigned char *need, int64_t n, int64_t *rowkey)
+{
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < n && need[g]) rowkey[lrow[g]] = g;
+}
+__global__ void level_rows_kernel(const int *lrow, const unsigned char *need, const int64_t *lvoff,
+                                  int depth, int *out)
+{
+    // out[l] = first row of level l (l = 2..depth), out[depth + 1] = total rows
+    const int l = threadIdx.x + 2;
+    if (l > depth + 1) return;
+    if (l <= depth) out[l] = lrow[lvoff[l]];
+    else out[l] = lrow[lvoff[l] - 1] + (need[lvoff[l] - 1] ? 1 : 0);
+}
+
 struct NeedArgs {
     int depth;
     const int *tmap[kMaxLevels];
@@ -347,13 +368,13 @@ __global__ void __launch_bounds__(32 * kL2LWarps) l2l_kernel(FarArgs a, int leve
     double2 *par = wbuf + warp * 2 * P, *T = par + P;
     load_recentre_tables(p, a.rtab_l, a.tritab_l, cm, tri_i, tri_j);   // local order
     __syncthreads();
-    const int64_t items = (int64_t)a.tcount[level] * KW;
+    // the level's materialised boxes only: local rows [row0, row1), row -> dense position
+    const int row0 = a.lrow_lev[level], row1 = a.lrow_lev[level + 1];
+    const int64_t items = (int64_t)(row1 - row0) * KW;
     for (int64_t it = (int64_t)blockIdx.x * kL2LWarps + warp; it < items;
          it += (int64_t)gridDim.x * kL2LWarps) {
-        const int slot = (int)(it / KW), n = (int)(it % KW);
-        const uint32_t key = (uint32_t)a.tkeys[level][slot];
-        if (!a.need[a.lvoff[level] + key]) continue;
-        const int ps = a.tmap[level - 1][key >> 2];
+        const int row = row0 + (int)(it / KW), n = (int)(it % KW);
+        const uint32_t key = (uint32_t)(a.rowkey[row] - a.lvoff[level]);
         const int sr = key & 1, sz = (key >> 1) & 1;
         const bool child_w = a.s2l_written[a.lvoff[level] + key] != 0;
         const bool par_ok = level - 1 > 2 || a.s2l_written[a.lvoff[level - 1] + (key >> 2)] != 0;
@@ -372,7 +393,7 @@ __global__ void __launch_bounds__(32 * kL2LWarps) l2l_kernel(FarArgs a, int leve
             T[e] = acc;
         }
         __syncwarp();
-        double2 *o = a.Lc + ((int64_t)a.lrow[a.lvoff[level] + key] * KW + n) * P;
+        double2 *o = a.Lc + ((int64_t)row * KW + n) * P;
         for (int e = lane; e < P; e += 32) {
             const int i = tri_i[e], j = tri_j[e];
             const double *co = cl + (sz * P1 + j) * P1;
