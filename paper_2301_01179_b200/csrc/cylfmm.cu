@@ -126,12 +126,14 @@ static cudaError_t allow_smem(F *kernel)
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
 }
 
-#define P2PW_INSTANCES(X) X(9, true, false, false, false) X(17, true, false, false, false)              \
-    X(33, true, false, false, false) X(9, false, false, false, false) \
-    X(17, false, false, false, false) X(33, false, false, false, false) X(33, false, false, true, false) \
-    X(9, true, false, false, true) X(17, true, false, false, true) X(33, true, false, false, true)     \
-    X(9, false, false, false, true) X(17, false, false, false, true) X(33, false, false, false, true) \
-    X(33, false, false, true, true)
+#define P2PW_INSTANCES(X) X(9, true, false, false, false, false) X(17, true, false, false, false, false) \
+    X(33, true, false, false, false, false) X(9, false, false, false, false, false)                    \
+    X(17, false, false, false, false, false) X(33, false, false, false, false, false)                  \
+    X(33, false, false, true, false, false) X(9, true, false, false, true, false)                      \
+    X(17, true, false, false, true, false) X(33, true, false, false, true, false)                      \
+    X(9, false, false, false, true, false) X(17, false, false, false, true, false)                     \
+    X(33, false, false, false, true, false) X(33, false, false, true, true, false)                     \
+    X(33, true, false, false, false, true) X(33, false, false, true, false, true)
 #define P2P_INSTANCES(X)                                                                       \
     X(8, 16, 2) X(8, 16, 5) X(16, 8, 3) X(16, 8, 9) X(32, 4, 6) X(32, 4, 18)
 
@@ -153,7 +155,7 @@ static cylfmm_status ensure_init()
     cudaError_t e = cudaMemcpyToSymbol(c_rec, t, sizeof(RecTables));
     delete t;
     CK(e);
-#define X(KT, E, W, N, DR) CK(allow_smem(p2p_warp_kernel<KT, E, W, N, DR>));
+#define X(KT, E, W, N, DR, SV) CK(allow_smem(p2p_warp_kernel<KT, E, W, N, DR, SV>));
     P2PW_INSTANCES(X)
 #undef X
 #define X(TT, SC, MT)                                                                          \
@@ -237,10 +239,11 @@ static cudaError_t launch_p2pw(const P2PArgs &a, cudaStream_t st, bool direct = 
         cudaError_t err = cudaMemsetAsync(a.task_ctr, 0, sizeof(int), st);
         if (err != cudaSuccess) return err;
     }
-#define X(KT, E, W, N, DR)                                                                     \
-    if (kt == KT && exact == E && wsm == W && win == N && direct == DR) {                      \
-        p2p_warp_kernel<KT, E, W, N, DR><<<nsm * p2pw_min_blocks<KT, W>(), 128,                \
-                                           p2pw_smem_bytes<KT, W>(), st>>>(a);                 \
+    const bool sv = a.save != 0;   // window state saved / restored (K in (33, 66])
+#define X(KT, E, W, N, DR, SV)                                                                 \
+    if (kt == KT && exact == E && wsm == W && win == N && direct == DR && sv == SV) {          \
+        p2p_warp_kernel<KT, E, W, N, DR, SV><<<nsm * p2pw_min_blocks<KT, W>(), 128,            \
+                                               p2pw_smem_bytes<KT, W>(), st>>>(a);             \
         return cudaGetLastError();                                                             \
     }
     P2PW_INSTANCES(X)
@@ -499,7 +502,7 @@ struct cylfmm_plan_s {
     int device = 0;
     int nsm = 148;
     // tree buffers
-    DevBuf skey, sidx, skey2, sidx2, fkey, fidx, fkey2, fidx2, hist, scan_tmp[4];
+    DevBuf skey, sidx, skey2, sidx2, fkey, fidx, fkey2, fidx2, hist, scan_tmp[4], scan_tmp_n[4];
     DevBuf sr_s, sz_s, S_s, fr_s, fz_s;
     DevBuf slstart, flstart, flags, smap, skeys, tmap, tkeys, counts;
     DevBuf M, Lc, tens, seeds;
@@ -507,6 +510,7 @@ struct cylfmm_plan_s {
     DevBuf written;                       // per-box 'local written by S2L' flags
     DevBuf pcnt, poff, khist, kstart, kcur, bstart, pairs, batches, wlist, pairbuf;   // S2L lists
     DevBuf need, lrow, rowkey, lvoffd;    // lazy L2L flags, compact local rows, row -> box
+    DevBuf pbase, pcnt64, sv2, sv1;       // near-field window state (K in (33, 66])
     DevBuf stflag, stlist;                // stations with an S2L pair
     DevBuf l2pown, l2pflag, l2ppos, l2ptask, l2pntask;   // L2P evaluating boxes and tasks
     DevBuf err, ctr;
@@ -602,10 +606,11 @@ static void free_plan_bufs(cylfmm_plan p)
 {
     DevBuf *all[] = {&p->skey, &p->sidx, &p->skey2, &p->sidx2, &p->fkey, &p->fidx, &p->fkey2,
                      &p->fidx2, &p->hist, &p->scan_tmp[0], &p->scan_tmp[1], &p->scan_tmp[2],
-                     &p->scan_tmp[3], &p->sr_s, &p->sz_s, &p->S_s, &p->fr_s, &p->fz_s,
+                     &p->scan_tmp[3], &p->scan_tmp_n[0], &p->scan_tmp_n[1], &p->scan_tmp_n[2],
+                     &p->scan_tmp_n[3], &p->sr_s, &p->sz_s, &p->S_s, &p->fr_s, &p->fz_s,
                      &p->slstart, &p->flstart, &p->flags, &p->smap, &p->skeys, &p->tmap,
                      &p->tkeys, &p->counts, &p->M, &p->Lc, &p->tens, &p->seeds, &p->tasks,
-                     &p->ntasks, &p->tcnt, &p->toff, &p->written, &p->pcnt, &p->poff, &p->khist, &p->kstart, &p->kcur, &p->bstart, &p->pairs, &p->batches, &p->wlist, &p->pairbuf, &p->need, &p->lrow, &p->rowkey, &p->lvoffd, &p->stflag, &p->stlist, &p->l2pown, &p->l2pflag, &p->l2ppos, &p->l2ptask, &p->l2pntask, &p->err, &p->ctr, &p->rtab, &p->h_sr, &p->h_sz,
+                     &p->ntasks, &p->tcnt, &p->toff, &p->written, &p->pcnt, &p->poff, &p->khist, &p->kstart, &p->kcur, &p->bstart, &p->pairs, &p->batches, &p->wlist, &p->pairbuf, &p->need, &p->lrow, &p->rowkey, &p->lvoffd, &p->pbase, &p->pcnt64, &p->sv2, &p->sv1, &p->stflag, &p->stlist, &p->l2pown, &p->l2pflag, &p->l2ppos, &p->l2ptask, &p->l2pntask, &p->err, &p->ctr, &p->rtab, &p->h_sr, &p->h_sz,
                      &p->h_S, &p->h_fr, &p->h_fz, &p->h_out, &p->g_r, &p->g_z, &p->g_S, &p->g_cnt};
     for (DevBuf *b : all) b->release();
 }
@@ -754,8 +759,11 @@ extern "C" cylfmm_status cylfmm_plan_sync(cylfmm_plan plan)
     return CYLFMM_OK;
 }
 
-// exclusive scan in place on d (n ints), scratch from plan->scan_tmp[depth]
-static cylfmm_status scan_excl(cylfmm_plan p, int *d, int64_t n, cudaStream_t st, int lvl = 0)
+// exclusive scan in place on d (n ints or int64s), scratch from plan->scan_tmp[depth] (set 0,
+// the caller's stream) or plan->scan_tmp_n[depth] (set 1, the near-field stream)
+template <typename T>
+static cylfmm_status scan_excl(cylfmm_plan p, T *d, int64_t n, cudaStream_t st, int lvl = 0,
+                               int set = 0)
 {
     if (n <= 0) return CYLFMM_OK;
     int64_t nt = (n + kScanTile - 1) / kScanTile;
@@ -763,14 +771,15 @@ static cylfmm_status scan_excl(cylfmm_plan p, int *d, int64_t n, cudaStream_t st
         set_err("scan: too deep");
         return CYLFMM_EINVAL;
     }
-    RET_IF(p->scan_tmp[lvl].need(sizeof(int) * (size_t)std::max<int64_t>(nt, 1)));
-    int *sums = p->scan_tmp[lvl].as<int>();
-    scan_tile_kernel<<<(unsigned)nt, kScanThreads, 0, st>>>(d, n, d, sums);
+    DevBuf &tmp = set ? p->scan_tmp_n[lvl] : p->scan_tmp[lvl];
+    RET_IF(tmp.need(sizeof(T) * (size_t)std::max<int64_t>(nt, 1)));
+    T *sums = tmp.as<T>();
+    scan_tile_kernel<T><<<(unsigned)nt, kScanThreads, 0, st>>>(d, n, d, sums);
     CKL();
     p->launches++;
     if (nt > 1) {
-        RET_IF(scan_excl(p, sums, nt, st, lvl + 1));
-        scan_add_kernel<<<nblk(n, 256), 256, 0, st>>>(d, n, sums);
+        RET_IF(scan_excl(p, sums, nt, st, lvl + 1, set));
+        scan_add_kernel<T><<<nblk(n, 256), 256, 0, st>>>(d, n, sums);
         CKL();
         p->launches++;
     }
@@ -1150,8 +1159,27 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         CKL();
         p->launches += 3;
     }
+    // near-field window state (K in (33, 66], two mode windows): pair slots by target leaf
+    const bool wsave = ns > 0 && !grad && K > kP2PWWindow && K <= 2 * kP2PWWindow &&
+                       p2pw_enabled(K, grad);
+    if (wsave) {
+        const int64_t nl = pow4(d);
+        RET_IF(p->pbase.need(sizeof(int64_t) * (nl + 2)));
+        RET_IF(p->pcnt64.need(sizeof(int64_t) * nl));
+        int64_t *pb = p->pbase.as<int64_t>(), *pc = p->pcnt64.as<int64_t>();
+        CK(cudaMemsetAsync(pc, 0, sizeof(int64_t) * nl, st));
+        near_leaf_pairs_kernel<<<nblk(nl, 256), 256, 0, st>>>(tmap_b + lvoff[d], flstart, p->slstart.as<int>(), d, pc);
+        CKL();
+        CK(cudaMemcpyAsync(pb, pc, sizeof(int64_t) * nl, cudaMemcpyDeviceToDevice, st));
+        RET_IF(scan_excl(p, pb, nl, st));
+        total64_kernel<<<1, 32, 0, st>>>(pb, pc, nl, pb + nl);
+        CKL();
+        p->launches += 3;
+    }
+    int64_t nslots = 0;
     int hcnt[3 * kMaxLevels + 8] = {0};
     CK(cudaMemcpyAsync(hcnt, p->counts.p, sizeof(int) * (3 * kMaxLevels + 8), cudaMemcpyDeviceToHost, st));
+    if (wsave) CK(cudaMemcpyAsync(&nslots, p->pbase.as<int64_t>() + pow4(d), sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     RET_IF(check_err_flag(p, st));
     if (same)
@@ -1331,7 +1359,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             near_tasks_count_kernel<<<nblk(ntl, 256), 256, 0, st_n>>>(fa.tkeys[d], ntl, fa.flstart, TT,
                                                                    p->tcnt.as<int>());
             CKL();
-            RET_IF(scan_excl(p, p->tcnt.as<int>(), ntl, st_n));
+            RET_IF(scan_excl(p, p->tcnt.as<int>(), ntl, st_n, 0, 1));
             near_tasks_emit_kernel<<<nblk(ntl, 256), 256, 0, st_n>>>(fa.tkeys[d], ntl, fa.flstart, TT,
                                                                   p->tcnt.as<int>(), p->tasks.as<int4>(),
                                                                   p->ntasks.as<int>());
@@ -1340,6 +1368,10 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         p->launches += 2;
         unsigned long long *ctr = p->ctr.as<unsigned long long>();
         const int win = wk ? kP2PWWindow : kP2PWindow;
+        if (wsave) {
+            RET_IF(p->sv2.need(sizeof(double2) * (size_t)std::max<int64_t>(nslots, 1)));
+            RET_IF(p->sv1.need(sizeof(double) * (size_t)std::max<int64_t>(nslots, 1)));
+        }
         for (int m0 = 0; m0 < K; m0 += win) {
             P2PArgs a = {};
             a.sr = fa.sr;
@@ -1368,6 +1400,14 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             a.n_pairs = ctr + 1;
             a.n_branch = ctr + 3;
             a.err_flag = p->err.as<int>();
+            if (wsave) {   // first window saves the chain state, the second restarts from it
+                a.save = m0 == 0 ? 1 : 2;
+                a.sv2 = p->sv2.as<double2>();
+                a.sv1 = p->sv1.as<double>();
+                a.pbase = p->pbase.as<int64_t>();
+                a.tmap_leaf = fa.tmap[d];
+                a.fleafstart = fa.flstart;
+            }
             const dim3 grid((unsigned)maxtasks);
             a.task_ctr = p->ntasks.as<int>() + 1;
             if (wk) CK(launch_p2pw(a, st_n));

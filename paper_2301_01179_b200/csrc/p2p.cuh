@@ -43,6 +43,17 @@ struct P2PArgs {
     unsigned long long *n_skipped;
     unsigned long long *n_pairs;
     unsigned long long *n_branch;   // nullable: [0] forward, [1] far, [2] Miller pairs, [3] sum S - N
+    // window state (K in (33, 66]: two mode windows): save = 1 in the first window writes, per
+    // pair, the forward chain state (u_31, u_32) or the Miller state (w_66, w_65, c (2 chi)^-64)
+    // in the final scaling; save = 2 in the second window reads it instead of re-running the
+    // setup and the chain below / above the window.  Pair slot = pbase[leaf slot] + (target index
+    // in its leaf) * (sources of the leaf's 9 neighbours) + (source index in that list).
+    int save;
+    double2 *sv2;
+    double *sv1;
+    const int64_t *pbase;
+    const int *tmap_leaf;         // target leaf key -> slot
+    const int *fleafstart;        // dense target leaf starts
     int *err_flag;
 };
 

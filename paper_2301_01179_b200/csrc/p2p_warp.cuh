@@ -36,8 +36,8 @@ template <int KT, bool WSM>
 inline size_t p2pw_smem_bytes()
 {
     return (size_t)kWarps * (sizeof(double2) * kWarpCH * p2pw_row<KT>() + sizeof(double) * 2 * kWarpCH +
-                             sizeof(int) * kWarpCH) +
-           sizeof(int) * 19;
+                             2 * sizeof(int) * kWarpCH) +
+           sizeof(int) * 20;
 }
 template <int KT, bool WSM>
 __host__ __device__ constexpr int p2pw_min_blocks()
@@ -76,7 +76,7 @@ __device__ __forceinline__ double2 cfma(double2 s, double g, double2 acc)
 // window's modes are accumulated; forward pairs run two per lane in lockstep; m0 = 0 works too).
 // DIRECT: the direct sum: task = (tile of 32 targets, source partition), the
 // partition's partial sums written to out + part * part_stride (reduced in fixed order after).
-template <int KT, bool EXACT, bool WSM, bool WIN = false, bool DIRECT = false>
+template <int KT, bool EXACT, bool WSM, bool WIN = false, bool DIRECT = false, bool SV = false>
 __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_kernel(P2PArgs a)
 {
     constexpr int CH = kWarpCH, ROW = p2pw_row<KT>();
@@ -92,6 +92,7 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
     int *stG = reinterpret_cast<int *>(wbase) + warp * CH;
     int *segS0 = reinterpret_cast<int *>(wbase) + kWarps * CH;
     int *segPre = segS0 + 9;
+    int *stV = segS0 + 20 + warp * CH;                   // source index in the task's list
 
     unsigned my_skipped = 0, my_pairs = 0, my_fwd = 0, my_far = 0, my_mil = 0;
     unsigned long long my_msteps = 0;
@@ -164,6 +165,12 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
     const int vb = 0, ve = ICH * (total / (kWarps * ICH)) + min(max(rem - ICH * warp, 0), ICH);
 
     const double tr = a.fr[t0 + min(tl, nt - 1)], tz = a.fz[t0 + min(tl, nt - 1)];
+    // window-state slots of this lane's target (see P2PArgs::save)
+    int64_t tslot = 0;
+    if (SV && !DIRECT && a.save) {
+        const int lkey = tk.z;
+        tslot = a.pbase[a.tmap_leaf[lkey]] + (int64_t)(t0 + tl - a.fleafstart[lkey]) * total;
+    }
     double2 acc[KT];
 #pragma unroll
     for (int j = 0; j < KT; ++j) acc[j] = make_double2(0.0, 0.0);
@@ -181,6 +188,7 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
             for (int kk = 1; kk < 9; ++kk) k += (v >= segPre[kk]);
             const int gi = segS0[k] + (v - segPre[k]);
             stG[lane] = gi;
+            if (SV) stV[lane] = v;
             pw_async8(stR + lane, a.sr + gi);
             pw_async8(stZ + lane, a.sz + gi);
         }
@@ -231,40 +239,64 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
         // also advances to the window) two pairs per lane run in lockstep to hide its latency;
         // a missing second pair runs with zero seeds (the recursion is linear: exact zeros).
         constexpr bool TWO = WIN;
+        const bool load = SV && WIN && a.save == 2;   // (u_31, u_32) from the first window
+        // load mode: the states of the next iteration's pairs are fetched one iteration ahead
+        double2 pfA = make_double2(0.0, 0.0), pfB = make_double2(0.0, 0.0);
+        auto prefetch = [&](unsigned m) {
+            if (!m) return;
+            pfA = a.sv2[tslot + stV[sl + SL * (__ffs(m) - 1)]];
+            const unsigned m2 = m & (m - 1);
+            if (TWO && m2) pfB = a.sv2[tslot + stV[sl + SL * (__ffs(m2) - 1)]];
+        };
+        if (load) prefetch(mF);
         const int itF = __reduce_max_sync(0xffffffffu, TWO ? (nF + 1) >> 1 : nF);
         for (int it = 0; it < itF; ++it) {
             int ia = -1, ib = -1;
             if (mF) { ia = __ffs(mF) - 1; mF &= mF - 1; }
             if (TWO && mF) { ib = __ffs(mF) - 1; mF &= mF - 1; }
             if (ia < 0) continue;
+            const double2 sA = pfA, sBp = pfB;
+            if (load) prefetch(mF);
             const int ca = sl + SL * ia, cb = ib >= 0 ? sl + SL * ib : ca;
             const double wb = ib >= 0 ? 1.0 : 0.0;
             const PairGeo gA = pair_geo(tr, stR[ca], tz - stZ[ca], fwd2);
             const double2 *SA = stS + ca * ROW, *SB = stS + cb * ROW;
-            const double ipA = rsqrt_nr(gA.rp2);
-            double KA, EA;
-            ke_small(gA.rm2 * ipA * ipA, KA, EA);
-            const double G0A = KA * ipA * (1.0 / kPi);
             const double irA = rcp_nr(gA.rr1);
-            const double chA = 0.25 * (gA.rp2 + gA.rm2) * irA;
             const double dA = 0.5 * gA.rm2 * irA;   // chi - 1, exact to rounding (R#24)
-            double u0A = G0A, u1A = G0A * fma(-(1.0 + chA), EA * rcp_nr(KA), chA);
-            double u0B = 0.0, u1B = 0.0, dB = 0.0;
+            double u0A, u1A, u0B = 0.0, u1B = 0.0, dB = 0.0;
+            if (load) {
+                u0A = sA.x;
+                u1A = sA.y;
+            } else {
+                const double ipA = rsqrt_nr(gA.rp2);
+                double KA, EA;
+                ke_small(gA.rm2 * ipA * ipA, KA, EA);
+                const double G0A = KA * ipA * (1.0 / kPi);
+                const double chA = 0.25 * (gA.rp2 + gA.rm2) * irA;
+                u0A = G0A;
+                u1A = G0A * fma(-(1.0 + chA), EA * rcp_nr(KA), chA);
+            }
             if constexpr (TWO) {
                 const PairGeo gB = pair_geo(tr, stR[cb], tz - stZ[cb], fwd2);
-                const double ipB = rsqrt_nr(gB.rp2);
-                double KB, EB;
-                ke_small(gB.rm2 * ipB * ipB, KB, EB);
-                const double G0B = KB * ipB * (wb / kPi);
                 const double irB = rcp_nr(gB.rr1);
-                const double chB = 0.25 * (gB.rp2 + gB.rm2) * irB;
                 dB = 0.5 * gB.rm2 * irB;
-                u0B = G0B;
-                u1B = G0B * fma(-(1.0 + chB), EB * rcp_nr(KB), chB);
+                if (load) {
+                    const double2 sB = ib >= 0 ? sBp : make_double2(0.0, 0.0);
+                    u0B = sB.x;
+                    u1B = sB.y;
+                } else {
+                    const double ipB = rsqrt_nr(gB.rp2);
+                    double KB, EB;
+                    ke_small(gB.rm2 * ipB * ipB, KB, EB);
+                    const double G0B = KB * ipB * (wb / kPi);
+                    const double chB = 0.25 * (gB.rp2 + gB.rm2) * irB;
+                    u0B = G0B;
+                    u1B = G0B * fma(-(1.0 + chB), EB * rcp_nr(KB), chB);
+                }
             }
             if constexpr (WIN) {                        // advance to the window (M0 >= 2)
 #pragma unroll 4
-                for (int n = 2; n < M0; ++n) {
+                for (int n = load ? M0 : 2; n < M0; ++n) {
                     const double e = c_rec.eps[n];
                     const double u2A = fma(dA, u1A, fma(-e, u0A, u1A));
                     u0A = u1A;
@@ -310,6 +342,7 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
                         u1A = u2A;
                     }
                 }
+                if (SV && a.save == 1) a.sv2[tslot + stV[ca]] = make_double2(u0A, u1A);   // (u_31, u_32)
             }
         }
         // far pairs (chi >= 1000), one per lane and iteration: hypergeometric form (DLMF
@@ -363,6 +396,20 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
             my_msteps += (unsigned)(eA + eB);
             const int S_warp = __reduce_max_sync(0xffffffffu, S_lane);
             if (va) {
+                const double sumA = 0.5 * (gA.rp2 + gA.rm2), sumB = 0.5 * (gB.rp2 + gB.rm2);
+                const double i2A = gA.rr1 * rcp_nr(sumA), i2B = gB.rr1 * rcp_nr(sumB);   // 1/(2 chi)
+                const double qA = i2A * i2A, qB = i2B * i2B;
+                double wnA, wlA, wnB, wlB, cvA, cvB;
+                if (SV && WIN && a.save == 2) {   // the first window's chain state (see P2PArgs::save)
+                    const double2 sA = a.sv2[tslot + stV[ca]];
+                    wnA = sA.x;
+                    wlA = sA.y;
+                    cvA = a.sv1[tslot + stV[ca]];
+                    const double2 sB = vb ? a.sv2[tslot + stV[cb]] : make_double2(0.0, 0.0);
+                    wnB = sB.x;
+                    wlB = sB.y;
+                    cvB = vb ? a.sv1[tslot + stV[cb]] : 0.0;
+                } else {
                 const double ipA = rsqrt_nr(gA.rp2), ipB = rsqrt_nr(gB.rp2);
                 // AGM(1, k') of both pairs (K = pi / (2 AGM)); a converged pair is frozen
                 double a1 = 1.0, b1 = sqrt_nr(gA.rm2) * ipA, a2 = 1.0, b2 = sqrt_nr(gB.rm2) * ipB;
@@ -377,13 +424,19 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
                     if (uB) { a2 = nB; b2 = sB; }
                 }
                 const double G0A = 0.5 * ipA * rcp_nr(a1), G0B = 0.5 * ipB * rcp_nr(a2);
-                const double sumA = 0.5 * (gA.rp2 + gA.rm2), sumB = 0.5 * (gB.rp2 + gB.rm2);
-                const double i2A = gA.rr1 * rcp_nr(sumA), i2B = gB.rr1 * rcp_nr(sumB);   // 1/(2 chi)
-                const double qA = i2A * i2A, qB = i2B * i2B;
-                double wnA = 0.0, wlA = 1.0, wnB = 0.0, wlB = 1.0;
+                wnA = 0.0;
+                wlA = 1.0;
+                wnB = 0.0;
+                wlB = 1.0;
+                // first window of a two-window solve: the chain state at (K + 1, K), kept in the
+                // final scaling, is what the second window's contraction restarts from (the
+                // start S >= K - 1 + 7 lies above it)
+                const int ncap = (SV && !WIN && a.save == 1) ? a.K + 1 : -1;
+                double cnA = 0.0, clA = 0.0, cnB = 0.0, clB = 0.0;
                 int n = S_warp;
                 while (n > M1 + 1) {
-                    const int nstop = max(M1 + 1, n - 64);
+                    int nstop = max(M1 + 1, n - 64);
+                    if (ncap > nstop && n > ncap) nstop = ncap;
 #pragma unroll 4
                     for (; n > nstop; --n) {
                         const double d = c_rec.delta[n];
@@ -394,17 +447,31 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
                         wnB = wlB;
                         wlB = wB;
                     }
-                    int ex;
-                    frexp(wlA, &ex);
-                    wnA = ldexp(wnA, -ex);
-                    wlA = ldexp(wlA, -ex);
-                    frexp(wlB, &ex);
-                    wnB = ldexp(wnB, -ex);
-                    wlB = ldexp(wlB, -ex);
+                    int exA, exB;
+                    frexp(wlA, &exA);
+                    wnA = ldexp(wnA, -exA);
+                    wlA = ldexp(wlA, -exA);
+                    frexp(wlB, &exB);
+                    wnB = ldexp(wnB, -exB);
+                    wlB = ldexp(wlB, -exB);
+                    if (ncap > 0) {
+                        if (n == ncap) {               // captured after this block's rescaling
+                            cnA = wnA;
+                            clA = wlA;
+                            cnB = wnB;
+                            clB = wlB;
+                        } else if (n < ncap) {         // later rescalings apply to the capture
+                            cnA = ldexp(cnA, -exA);
+                            clA = ldexp(clA, -exA);
+                            cnB = ldexp(cnB, -exB);
+                            clB = ldexp(clB, -exB);
+                        }
+                    }
                 }
                 // pass 1: w_0 of both chains (wl = w_M1, wn = w_{M1+1} here)
                 double xnA = wnA, xlA = wlA, xnB = wnB, xlB = wlB;
-                double cvA = 1.0, cvB = 1.0;
+                cvA = 1.0;
+                cvB = 1.0;
                 if constexpr (WIN) {                    // steps below the window (n = M0 + 1 .. 2)
                     for (int j = KW - 1; j >= 0; --j) {
                         const double d = c_rec.delta[M0 + j + 2];
@@ -451,6 +518,20 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
                 }
                 cvA *= G0A * rcp_nr(xlA);                // c (2 chi)^-(M1-1)
                 cvB = vb ? cvB * (G0B * rcp_nr(xlB)) : 0.0;
+                if (ncap > 0) {   // second window's start: (w_{K+1}, w_K), c (2 chi)^-(K-1)
+                    double pA = 1.0, pB = 1.0;        // (2 chi)^-((K - 1) - (M1 - 1))
+                    for (int t = M1; t < a.K; ++t) {
+                        pA *= i2A;
+                        pB *= i2B;
+                    }
+                    a.sv2[tslot + stV[ca]] = make_double2(cnA, clA);
+                    a.sv1[tslot + stV[ca]] = cvA * pA;
+                    if (vb) {
+                        a.sv2[tslot + stV[cb]] = make_double2(cnB, clB);
+                        a.sv1[tslot + stV[cb]] = cvB * pB;
+                    }
+                }
+                }
                 const double tcA = sumA * rcp_nr(gA.rr1), tcB = sumB * rcp_nr(gB.rr1);   // 2 chi
                 // pass 2: G_n = w_n P_n c (2 chi)^-n, n = M0 + j, j = KW-1 .. 0
 #pragma unroll
@@ -554,6 +635,21 @@ __device__ __forceinline__ int near_sources(int key, const int *slstart, int dep
         }
     return tot;
 }
+// window-state slots: pairs per target leaf (targets x sources of the 9 neighbours), by leaf slot
+__global__ void near_leaf_pairs_kernel(const int *tmap_leaf, const int *flstart, const int *slstart,
+                                       int depth, int64_t *cnt)
+{
+    const int64_t key = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (key >= ((int64_t)1 << (2 * depth))) return;
+    const int s = tmap_leaf[key];
+    if (s < 0) return;
+    cnt[s] = (int64_t)(flstart[key + 1] - flstart[key]) * near_sources((int)key, slstart, depth);
+}
+__global__ void total64_kernel(const int64_t *scan, const int64_t *v, int64_t n, int64_t *out)
+{
+    if (threadIdx.x == 0) *out = n > 0 ? scan[n - 1] + v[n - 1] : 0;
+}
+
 __device__ __forceinline__ int task_bucket(int nt, int nsrc)
 {
     const int tw = nt <= 1 ? 1 : 1 << (32 - __clz(nt - 1));

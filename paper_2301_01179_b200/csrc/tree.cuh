@@ -105,49 +105,51 @@ constexpr int kScanThreads = 512;
 constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
-__device__ __forceinline__ int block_excl_scan(int v, int *sh, int &total)
+template <typename T>
+__device__ __forceinline__ T block_excl_scan(T v, T *sh, T &total)
 {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int x = v;
+    T x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(0xffffffffu, x, o);
+        T y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
     }
     if (lane == 31) sh[warp] = x;
     __syncthreads();
     if (warp == 0) {
-        int w = lane < (int)(blockDim.x / 32) ? sh[lane] : 0;
-        int ws = w;
+        T w = lane < (int)(blockDim.x / 32) ? sh[lane] : 0;
+        T ws = w;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            int y = __shfl_up_sync(0xffffffffu, ws, o);
+            T y = __shfl_up_sync(0xffffffffu, ws, o);
             if (lane >= o) ws += y;
         }
         sh[lane] = ws - w;
         if (lane == 31) sh[32] = ws;
     }
     __syncthreads();
-    int res = sh[warp] + x - v;
+    T res = sh[warp] + x - v;
     total = sh[32];
     __syncthreads();
     return res;
 }
 
-// out[i] = sum_{k<i} in[i]; sums[b] = tile total.  in may equal out.
-__global__ void __launch_bounds__(kScanThreads) scan_tile_kernel(const int *in, int64_t n, int *out,
-                                                                 int *sums)
+// out[i] = sum_{k<i} in[i]; sums[b] = tile total.  in may equal out.  T = int or int64_t.
+template <typename T>
+__global__ void __launch_bounds__(kScanThreads) scan_tile_kernel(const T *in, int64_t n, T *out,
+                                                                 T *sums)
 {
-    __shared__ int sh[33];
+    __shared__ T sh[33];
     int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
-    int v[kScanItems], s = 0;
+    T v[kScanItems], s = 0;
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
         v[k] = base + k < n ? in[base + k] : 0;
         s += v[k];
     }
-    int total;
-    int pre = block_excl_scan(s, sh, total);
+    T total;
+    T pre = block_excl_scan(s, sh, total);
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
         if (base + k < n) out[base + k] = pre;
@@ -156,7 +158,8 @@ __global__ void __launch_bounds__(kScanThreads) scan_tile_kernel(const int *in, 
     if (threadIdx.x == 0 && sums) sums[blockIdx.x] = total;
 }
 
-__global__ void scan_add_kernel(int *out, int64_t n, const int *offs)
+template <typename T>
+__global__ void scan_add_kernel(T *out, int64_t n, const T *offs)
 {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) out[i] += offs[i / kScanTile];
