@@ -177,3 +177,48 @@ def test_tensor_all_modes_vs_exact_recursion(orc, geom):
     for n in range(nmax + 1):
         err = np.abs((O[n] - E[n]) * w).max() / np.abs(E[n] * w).max()
         assert err <= 2e-12, (n, err)
+
+
+def _x_taylor_by_quadrature(r, r1, x, n, cmax, npts=None, dps=30):
+    """Gbar^n_{00c} = (1/c!) d^c G^(n)/dx^c for c = 0..cmax from the DEFINITION
+    G^(n) = int_0^2pi cos(n t) / (4 pi R) dt, R^2 = s^2 + ..., by the Legendre
+    generating function: 1 / sqrt(s^2 + 2 x h + h^2) = sum_c P_c(-x / s) h^c / s^(c+1) with
+    s^2 = r^2 + r1^2 - 2 r r1 cos t + x^2.  Trapezoid rule over t (spectrally accurate for
+    separated rings), mpmath at `dps` digits.  Independent of the tensor recursions."""
+    if npts is None:   # trapezoid error ~ exp(-alpha N), alpha ~ (closest distance) / sqrt(r r1)
+        alpha = math.hypot(r - r1, x) / math.sqrt(r * r1)
+        npts = max(512, 256 * math.ceil(44.0 / alpha / 256))
+    mp.mp.dps = dps
+    r, r1, x = mp.mpf(r), mp.mpf(r1), mp.mpf(x)
+    acc = [mp.mpf(0)] * (cmax + 1)
+    for k in range(npts):
+        t = 2 * mp.pi * k / npts
+        s = mp.sqrt(r * r + r1 * r1 - 2 * r * r1 * mp.cos(t) + x * x)
+        u = -x / s
+        w = mp.cos(n * t) / (4 * mp.pi * s)
+        p0, p1 = mp.mpf(1), u            # Legendre P_c(u) by the three-term recursion
+        for c in range(cmax + 1):
+            pc = p0 if c == 0 else p1
+            acc[c] += w * pc
+            w /= s
+            if c >= 1:
+                p0, p1 = p1, ((2 * c + 1) * u * p1 - c * p0) / (c + 1)
+    return [float(a * 2 * mp.pi / npts) for a in acc]
+
+
+@pytest.mark.parametrize("geom", [(300.5, 298.5, 2.0), (50.5, 47.5, 3.0), (10.5, 10.5, 2.0)])
+def test_tensor_x_derivatives_c5_regime_vs_definition(orc, geom):
+    """Step 2b (reading R#22) in the C5 regime -- K = 65 modes, p = 16 (x-derivatives to order
+    2p = 32) at normalised stations of the C5 tree (far from the axis, mid, and same-column) --
+    against the definition of G^(n) as an angular integral of the 3-D kernel, whose
+    x-Taylor coefficients follow from the Legendre generating function
+    (_x_taylor_by_quadrature): an independent method, not the paper's recursions.  Per mode,
+    relative to the largest coefficient of that mode."""
+    r, r1, x = geom
+    p, nmax = 16, 64
+    T = orc.tensor(r, r1, x, nmax, p)
+    for n in (2, 17, 33, 48, 64):
+        ref = _x_taylor_by_quadrature(r, r1, x, n, 2 * p)
+        scale = max(abs(v) for v in ref)
+        err = max(abs(T[n, 0, 0, c] - ref[c]) for c in range(2 * p + 1)) / scale
+        assert err <= 1e-12, (geom, n, err)
