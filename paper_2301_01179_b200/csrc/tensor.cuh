@@ -364,6 +364,21 @@ inline size_t tensor_seed_smem(int K, int m1, int p)
     return sizeof(double) * (NM + 8 * Q + 3 * (size_t)NM * D + g11 + (size_t)NM * D + 2 * D + 6);
 }
 
+// closed form of packed_off
+__host__ __device__ inline int packed_row_t(int a, int b, int p)
+{
+    return a * ((p + 1) * (2 * p + 1) - p * (p + 1) / 2) - (p + 1) * (a * (a - 1) / 2) +
+           b * (2 * p + 1 - a) - b * (b - 1) / 2;
+}
+// 1 / ((k + 1)(k + 2)) for the Laplace steps (k <= 2 CYLFMM_MAX_ORDER)
+__constant__ double c_lapinv[40] = {
+#define LI(k) 1.0 / (((k) + 1.0) * ((k) + 2.0))
+    LI(0), LI(1), LI(2), LI(3), LI(4), LI(5), LI(6), LI(7), LI(8), LI(9), LI(10), LI(11), LI(12),
+    LI(13), LI(14), LI(15), LI(16), LI(17), LI(18), LI(19), LI(20), LI(21), LI(22), LI(23), LI(24),
+    LI(25), LI(26), LI(27), LI(28), LI(29), LI(30), LI(31), LI(32), LI(33), LI(34), LI(35), LI(36),
+    LI(37), LI(38), LI(39)
+#undef LI
+};
 // packed offset of (a, b) for order p (host/device helper used by S2L)
 __host__ __device__ inline int packed_off(int aa, int b, int p)
 {
@@ -385,11 +400,12 @@ __host__ __device__ inline int packed_off(int aa, int b, int p)
 struct Row {                 // column c (lo) and c + 32 (hi) of one tensor row
     double lo, hi;
 };
-__device__ __forceinline__ double col_plus2(const Row &v, int lane)
+// column c + 2 of a row from lane c + 2; the one entry past lane 31 any valid entry reads is
+// (0, 0, 2p = 32) at p = 16 (by lane 30 when forming rows (2, 0) and (0, 2)): hi00, a register
+__device__ __forceinline__ double col_plus2(const Row &v, int lane, bool row00, double hi00)
 {
     const double a = __shfl_down_sync(0xffffffffu, v.lo, 2);
-    const double b = __shfl_sync(0xffffffffu, v.hi, lane - 30);   // lanes 30, 31: c + 2 >= 32
-    return lane < 30 ? a : b;
+    return (row00 && lane == 30) ? hi00 : a;
 }
 
 __global__ void __launch_bounds__(128) tensor_fill_kernel(TensorGeomArgs a)
@@ -420,7 +436,7 @@ __global__ void __launch_bounds__(128) tensor_fill_kernel(TensorGeomArgs a)
     auto store = [&](int aa, int b, const Row &v) {
         const int cmax = C - aa - b;
         if (a.packed) {
-            double *q = o + packed_off(aa, b, p);
+            double *q = o + packed_row_t(aa, b, p);
             if (c0 <= cmax) q[c0] = v.lo * f0;
             if (c1 <= cmax) q[c1] = v.hi * f1;
         } else {
@@ -438,11 +454,14 @@ __global__ void __launch_bounds__(128) tensor_fill_kernel(TensorGeomArgs a)
     // one Laplace step: new = [ s (k+1)(2k+1) cur + (k^2 - n^2) prev
     //                         + (c+1)(c+2) (s^2 prev[c+2] + 2 s prev2[c+2] + prev3[c+2]) ] * inv
     // (r: s = r, rows a = k+1, k, k-1, k-2 at fixed b; r1: s = r1, rows b = k+1, k, k-1, k-2)
-    auto lap_step = [&](double sc, int k, const Row &cur, const Row &prv, const Row &pm1,
-                        const Row &pm2) {
-        const double inv = -1.0 / (sc * sc * (k + 1.0) * (k + 2.0));
-        const double t0 = col_plus2(prv, lane), t1 = k >= 1 ? col_plus2(pm1, lane) : 0.0;
-        const double t2 = k >= 2 ? col_plus2(pm2, lane) : 0.0;
+    double hi00 = 0.0;   // (0, 0, 32) at p = 16, set from the seeds below
+    // 1/(s^2 (k+1)(k+2)) from 1/s^2 and a table: no division per step
+    auto lap_step = [&](double isc2, double sc, int k, const Row &cur, const Row &prv,
+                        const Row &pm1, const Row &pm2, bool prv00) {
+        const double inv = -isc2 * c_lapinv[k];
+        const double t0 = col_plus2(prv, lane, prv00, hi00);
+        const double t1 = k >= 1 ? col_plus2(pm1, lane, false, 0.0) : 0.0;
+        const double t2 = k >= 2 ? col_plus2(pm2, lane, false, 0.0) : 0.0;
         Row nw;
         {
             double lap = sc * sc * t0;
@@ -459,6 +478,8 @@ __global__ void __launch_bounds__(128) tensor_fill_kernel(TensorGeomArgs a)
     // b = 0, 1 rows of a = 0, 1 from the seeds
     Row ra0[4] = {}, ra1[4] = {};   // rows a-4 .. a-1 of the b = 0 (ra0) and b = 1 (ra1) planes
     Row b0 = seed(0, C), b1 = p >= 1 ? seed(2, C - 1) : Row{};
+    hi00 = __shfl_sync(0xffffffffu, b0.hi, 0);
+    const double ir2 = 1.0 / (r * r), ir12 = 1.0 / (r1 * r1);
     Row a1b0 = p >= 1 ? seed(1, C - 1) : Row{}, a1b1 = p >= 1 ? seed(3, C - 2) : Row{};
     for (int aa = 0; aa <= p; ++aa) {
         Row rb0, rb1;   // rows (aa, 0) and (aa, 1)
@@ -470,8 +491,8 @@ __global__ void __launch_bounds__(128) tensor_fill_kernel(TensorGeomArgs a)
             rb1 = a1b1;
         } else {   // Laplace in r (k = aa - 2): rows k+1, k, k-1, k-2 = aa-1 .. aa-4
             const int k = aa - 2;
-            rb0 = lap_step(r, k, ra0[3], ra0[2], ra0[1], ra0[0]);
-            rb1 = lap_step(r, k, ra1[3], ra1[2], ra1[1], ra1[0]);
+            rb0 = lap_step(ir2, r, k, ra0[3], ra0[2], ra0[1], ra0[0], aa == 2);
+            rb1 = lap_step(ir2, r, k, ra1[3], ra1[2], ra1[1], ra1[0], false);
         }
 #pragma unroll
         for (int h = 0; h < 3; ++h) {
@@ -485,7 +506,7 @@ __global__ void __launch_bounds__(128) tensor_fill_kernel(TensorGeomArgs a)
         // Laplace in r1 for this a: rows b + 2 from b + 1, b, b - 1, b - 2
         Row hb[4] = {Row{}, Row{}, rb0, rb1};   // rows b-2, b-1, b, b+1 (b = 0)
         for (int bb = 0; bb + 2 <= p && aa + bb + 2 <= C; ++bb) {
-            const Row nb = lap_step(r1, bb, hb[3], hb[2], hb[1], hb[0]);
+            const Row nb = lap_step(ir12, r1, bb, hb[3], hb[2], hb[1], hb[0], aa == 0 && bb == 0);
             hb[0] = hb[1];
             hb[1] = hb[2];
             hb[2] = hb[3];
