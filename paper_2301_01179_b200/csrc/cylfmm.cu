@@ -1310,7 +1310,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     ra.pcnt = p->pcnt.as<int>();
     ra.pairbuf = sa.pairbuf;
     ra.Lc = fa.Lc;
-    fa.l2p_accumulate = ns > 0;   // L2P adds the far field onto the near field's rows
+    fa.l2p_accumulate = ns > 0 && overlap;   // L2P adds onto the near field's rows (overlapped)
     fa.tfield = nf;
     RET_IF(p->l2pown.need(sizeof(int) * std::max(hcnt[kMaxLevels + d], 1)));
     RET_IF(p->l2pflag.need(sizeof(int) * nf));
@@ -1334,90 +1334,98 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         p->launches++;
         T.end(PH_TENSOR, st_t);
     }
-    // ---- near field: writes every field row (the far field is added by L2P)
-    if (ns > 0) {
-        if (overlap) CK(cudaStreamWaitEvent(st_n, p->aev[1], 0));
-        T.beg(PH_P2P, st_n);
-        const int ntl = fa.tcount[d];
-        double avg = (double)nf / std::max(ntl, 1);
-        const int TT = avg <= 10.0 ? 8 : (avg <= 24.0 ? 16 : 32);
-        const bool wk = p2pw_enabled(K, grad);
-        RET_IF(p->tcnt.need(sizeof(int) * (ntl + 1)));
-        RET_IF(p->ntasks.need(kTaskCtrInts * sizeof(int)));
-        // warp tasks: <= nf/32 full pieces + <= 5 power-of-two pieces per leaf
-        int64_t maxtasks = wk ? nf / 32 + 6 * (int64_t)ntl + 1 : nf / TT + ntl + 1;
-        RET_IF(p->tasks.need(sizeof(int4) * maxtasks));
-        if (wk) {
-            CK(cudaMemsetAsync(p->ntasks.as<int>(), 0, kTaskCtrInts * sizeof(int), st_n));
-            near_wtasks_count_kernel<<<nblk(ntl, 256), 256, 0, st_n>>>(fa.tkeys[d], ntl, fa.flstart,
-                                                                    fa.slstart, d, p->ntasks.as<int>());
-            CKL();
-            near_wtasks_emit_kernel<<<nblk(ntl, 256), 256, 0, st_n>>>(fa.tkeys[d], ntl, fa.flstart,
-                                                                   fa.slstart, d, p->tasks.as<int4>(),
-                                                                   p->ntasks.as<int>());
-        } else {
-            near_tasks_count_kernel<<<nblk(ntl, 256), 256, 0, st_n>>>(fa.tkeys[d], ntl, fa.flstart, TT,
-                                                                   p->tcnt.as<int>());
-            CKL();
-            RET_IF(scan_excl(p, p->tcnt.as<int>(), ntl, st_n, 0, 1));
-            near_tasks_emit_kernel<<<nblk(ntl, 256), 256, 0, st_n>>>(fa.tkeys[d], ntl, fa.flstart, TT,
-                                                                  p->tcnt.as<int>(), p->tasks.as<int4>(),
-                                                                  p->ntasks.as<int>());
-        }
-        CKL();
-        p->launches += 2;
-        unsigned long long *ctr = p->ctr.as<unsigned long long>();
-        const int win = wk ? kP2PWWindow : kP2PWindow;
-        if (wsave) {
-            RET_IF(p->sv2.need(sizeof(double2) * (size_t)std::max<int64_t>(nslots, 1)));
-            RET_IF(p->sv1.need(sizeof(double) * (size_t)std::max<int64_t>(nslots, 1)));
-        }
-        for (int m0 = 0; m0 < K; m0 += win) {
-            P2PArgs a = {};
-            a.sr = fa.sr;
-            a.sz = fa.sz;
-            a.S = fa.S;
-            a.fr = fa.fr;
-            a.fz = fa.fz;
-            a.ns = ns;
-            a.nf = nf;
-            a.K = K;
-            a.m0 = m0;
-            a.m1 = std::min(K, m0 + win);
-            a.miller = q.miller;
-            a.fwd2 = forward_coef(K - 1, q.miller);
-            a.exclude = q.exclude_coincident;
-            a.out = fa.out;
-            a.outr = fa.outr;
-            a.outz = fa.outz;
-            a.out_row = fperm;
-            a.accumulate = 0;
-            a.tasks = p->tasks.as<int4>();
-            a.ntasks = p->ntasks.as<int>();
-            a.leafstart = fa.slstart;
-            a.depth = d;
-            a.n_skipped = ctr + 0;
-            a.n_pairs = ctr + 1;
-            a.n_branch = ctr + 3;
-            a.err_flag = p->err.as<int>();
-            if (wsave) {   // first window saves the chain state, the second restarts from it
-                a.save = m0 == 0 ? 1 : 2;
-                a.sv2 = p->sv2.as<double2>();
-                a.sv1 = p->sv1.as<double>();
-                a.pbase = p->pbase.as<int64_t>();
-                a.tmap_leaf = fa.tmap[d];
-                a.fleafstart = fa.flstart;
+    // ---- near field.  Overlapped (small) solves: first, on its own stream, writing
+    // every field row, and L2P adds the far field; serial (large) solves: after L2P, adding onto
+    // the rows L2P wrote (the read-modify-write then sits at the end of long near-field tasks
+    // instead of inside the short L2P items)
+    const bool near_first = overlap;
+    auto run_near = [&](int accumulate) -> cylfmm_status {
+        if (ns > 0) {
+            if (overlap) CK(cudaStreamWaitEvent(st_n, p->aev[1], 0));
+            T.beg(PH_P2P, st_n);
+            const int ntl = fa.tcount[d];
+            double avg = (double)nf / std::max(ntl, 1);
+            const int TT = avg <= 10.0 ? 8 : (avg <= 24.0 ? 16 : 32);
+            const bool wk = p2pw_enabled(K, grad);
+            RET_IF(p->tcnt.need(sizeof(int) * (ntl + 1)));
+            RET_IF(p->ntasks.need(kTaskCtrInts * sizeof(int)));
+            // warp tasks: <= nf/32 full pieces + <= 5 power-of-two pieces per leaf
+            int64_t maxtasks = wk ? nf / 32 + 6 * (int64_t)ntl + 1 : nf / TT + ntl + 1;
+            RET_IF(p->tasks.need(sizeof(int4) * maxtasks));
+            if (wk) {
+                CK(cudaMemsetAsync(p->ntasks.as<int>(), 0, kTaskCtrInts * sizeof(int), st_n));
+                near_wtasks_count_kernel<<<nblk(ntl, 256), 256, 0, st_n>>>(fa.tkeys[d], ntl, fa.flstart,
+                                                                        fa.slstart, d, p->ntasks.as<int>());
+                CKL();
+                near_wtasks_emit_kernel<<<nblk(ntl, 256), 256, 0, st_n>>>(fa.tkeys[d], ntl, fa.flstart,
+                                                                       fa.slstart, d, p->tasks.as<int4>(),
+                                                                       p->ntasks.as<int>());
+            } else {
+                near_tasks_count_kernel<<<nblk(ntl, 256), 256, 0, st_n>>>(fa.tkeys[d], ntl, fa.flstart, TT,
+                                                                       p->tcnt.as<int>());
+                CKL();
+                RET_IF(scan_excl(p, p->tcnt.as<int>(), ntl, st_n, 0, 1));
+                near_tasks_emit_kernel<<<nblk(ntl, 256), 256, 0, st_n>>>(fa.tkeys[d], ntl, fa.flstart, TT,
+                                                                      p->tcnt.as<int>(), p->tasks.as<int4>(),
+                                                                      p->ntasks.as<int>());
             }
-            const dim3 grid((unsigned)maxtasks);
-            a.task_ctr = p->ntasks.as<int>() + 1;
-            if (wk) CK(launch_p2pw(a, st_n));
-            else if (grad) CK((launch_p2p<true, true>(TT, a, grid, st_n)));
-            else CK(launch_p2p<true>(TT, a, grid, st_n));
-            p->launches++;
+            CKL();
+            p->launches += 2;
+            unsigned long long *ctr = p->ctr.as<unsigned long long>();
+            const int win = wk ? kP2PWWindow : kP2PWindow;
+            if (wsave) {
+                RET_IF(p->sv2.need(sizeof(double2) * (size_t)std::max<int64_t>(nslots, 1)));
+                RET_IF(p->sv1.need(sizeof(double) * (size_t)std::max<int64_t>(nslots, 1)));
+            }
+            for (int m0 = 0; m0 < K; m0 += win) {
+                P2PArgs a = {};
+                a.sr = fa.sr;
+                a.sz = fa.sz;
+                a.S = fa.S;
+                a.fr = fa.fr;
+                a.fz = fa.fz;
+                a.ns = ns;
+                a.nf = nf;
+                a.K = K;
+                a.m0 = m0;
+                a.m1 = std::min(K, m0 + win);
+                a.miller = q.miller;
+                a.fwd2 = forward_coef(K - 1, q.miller);
+                a.exclude = q.exclude_coincident;
+                a.out = fa.out;
+                a.outr = fa.outr;
+                a.outz = fa.outz;
+                a.out_row = fperm;
+                a.accumulate = accumulate;
+                a.tasks = p->tasks.as<int4>();
+                a.ntasks = p->ntasks.as<int>();
+                a.leafstart = fa.slstart;
+                a.depth = d;
+                a.n_skipped = ctr + 0;
+                a.n_pairs = ctr + 1;
+                a.n_branch = ctr + 3;
+                a.err_flag = p->err.as<int>();
+                if (wsave) {   // first window saves the chain state, the second restarts from it
+                    a.save = m0 == 0 ? 1 : 2;
+                    a.sv2 = p->sv2.as<double2>();
+                    a.sv1 = p->sv1.as<double>();
+                    a.pbase = p->pbase.as<int64_t>();
+                    a.tmap_leaf = fa.tmap[d];
+                    a.fleafstart = fa.flstart;
+                }
+                const dim3 grid((unsigned)maxtasks);
+                a.task_ctr = p->ntasks.as<int>() + 1;
+                if (wk) CK(launch_p2pw(a, st_n));
+                else if (grad) CK((launch_p2p<true, true>(TT, a, grid, st_n)));
+                else CK(launch_p2p<true>(TT, a, grid, st_n));
+                p->launches++;
+            }
+            T.end(PH_P2P, st_n);
+            if (overlap) CK(cudaEventRecord(p->aev[3], st_n));
         }
-        T.end(PH_P2P, st_n);
-        if (overlap) CK(cudaEventRecord(p->aev[3], st_n));
-    }
+        return CYLFMM_OK;
+    };
+    if (near_first) RET_IF(run_near(0));
     for (int m0 = 0; m0 < K; m0 += KW) {
         fa.m0 = m0;
         fa.m1 = std::min(K, m0 + KW);
@@ -1505,7 +1513,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             p->launches++;
         }
         T.end(PH_L2L, st);
-        if (overlap && ns > 0 && m0 == 0) CK(cudaStreamWaitEvent(st, p->aev[3], 0));  // near field
+        if (near_first && ns > 0 && m0 == 0) CK(cudaStreamWaitEvent(st, p->aev[3], 0));  // near field
         T.beg(PH_L2P, st);
         {
             // tasks: runs of <= TP sorted field points sharing their evaluating box; TP from the
@@ -1549,6 +1557,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         }
         T.end(PH_L2P, st);
     }
+    if (!near_first) RET_IF(run_near(1));   // onto the far field L2P wrote
     T.end(PH_TOTAL, st);
     if (tm) {
         unsigned long long c[8] = {0, 0, 0, 0, 0, 0, 0, 0};

@@ -139,10 +139,11 @@ __global__ void __launch_bounds__(kP2MThreads) p2m_kernel(FarArgs a)
             }
         }
         __syncthreads();
-        // monomials dr^i dz^j, all threads
-        for (int e = threadIdx.x; e < nc * P; e += kP2MThreads) {
-            const int qq = e / P, c = e - qq * P;
-            mono[qq * P + c] = pw[(qq * 2) * (p + 1) + mi[c]] * pw[(qq * 2 + 1) * (p + 1) + mj[c]];
+        // monomials dr^i dz^j: thread per coefficient c (its (i, j) in registers), all sources
+        for (int c = threadIdx.x; c < P; c += kP2MThreads) {
+            const int ci = mi[c], cj = mj[c];
+            for (int qq = 0; qq < nc; ++qq)
+                mono[qq * P + c] = pw[(qq * 2) * (p + 1) + ci] * pw[(qq * 2 + 1) * (p + 1) + cj];
         }
         // coefficient rows by asynchronous copies (in flight while the monomials are formed)
         for (int e = threadIdx.x; e < nc * kP2MModes; e += kP2MThreads) {
