@@ -77,10 +77,11 @@ __device__ __forceinline__ void box_centre(uint32_t key, int level, double L, do
 // CTA per (source leaf, block of kP2MModes modes); sources streamed through shared memory in
 // chunks of kP2MSrc (monomials computed once per chunk); thread tile = 2 modes x kP2MRC
 // coefficients in registers (20 DFMA per 7 shared loads per source).
-constexpr int kP2MThreads = 256;
 constexpr int kP2MSrc = 32;
 constexpr int kP2MModes = 16;
-constexpr int kP2MRC = 5;
+constexpr int kP2MTM = 4;                                    // modes per thread
+constexpr int kP2MRC = 5;                                    // coefficients per thread
+constexpr int kP2MThreads = (kP2MModes / kP2MTM) * 32;       // 32 x 5 >= P (p <= 16)
 
 // 16-byte asynchronous global -> shared copy (zero fill when !valid)
 __device__ __forceinline__ void p2m_async16(void *smem, const void *gmem, bool valid)
@@ -114,12 +115,12 @@ __global__ void __launch_bounds__(kP2MThreads) p2m_kernel(FarArgs a)
     box_centre(key, d, a.L, a.z0, rc, zc, h);
     const double inv_h = 1.0 / h;
     const int q0 = a.slstart[key], q1 = a.slstart[key + 1];
-    const int tn = threadIdx.x % (kP2MModes / 2), tc = threadIdx.x / (kP2MModes / 2);
+    const int tn = threadIdx.x % (kP2MModes / kP2MTM), tc = threadIdx.x / (kP2MModes / kP2MTM);
     const int c0 = tc * kP2MRC;
-    const bool active = c0 < P && 2 * tn < nm;
-    double2 acc[2][kP2MRC];
+    const bool active = c0 < P && kP2MTM * tn < nm;
+    double2 acc[kP2MTM][kP2MRC];
 #pragma unroll
-    for (int v = 0; v < 2; ++v)
+    for (int v = 0; v < kP2MTM; ++v)
 #pragma unroll
         for (int u = 0; u < kP2MRC; ++u) acc[v][u] = make_double2(0.0, 0.0);
     for (int s0 = q0; s0 < q1; s0 += kP2MSrc) {
@@ -155,15 +156,18 @@ __global__ void __launch_bounds__(kP2MThreads) p2m_kernel(FarArgs a)
         __syncthreads();
         if (active) {
             for (int q = 0; q < nc; ++q) {
-                const double2 sa = Sx[q * kP2MModes + 2 * tn], sb = Sx[q * kP2MModes + 2 * tn + 1];
+                double2 sv[kP2MTM];
+#pragma unroll
+                for (int v = 0; v < kP2MTM; ++v) sv[v] = Sx[q * kP2MModes + kP2MTM * tn + v];
                 const double *mq = mono + q * P + c0;
 #pragma unroll
                 for (int u = 0; u < kP2MRC; ++u) {
                     const double m = c0 + u < P ? mq[u] : 0.0;
-                    acc[0][u].x = fma(sa.x, m, acc[0][u].x);
-                    acc[0][u].y = fma(sa.y, m, acc[0][u].y);
-                    acc[1][u].x = fma(sb.x, m, acc[1][u].x);
-                    acc[1][u].y = fma(sb.y, m, acc[1][u].y);
+#pragma unroll
+                    for (int v = 0; v < kP2MTM; ++v) {
+                        acc[v][u].x = fma(sv[v].x, m, acc[v][u].x);
+                        acc[v][u].y = fma(sv[v].y, m, acc[v][u].y);
+                    }
                 }
             }
         }
@@ -171,9 +175,9 @@ __global__ void __launch_bounds__(kP2MThreads) p2m_kernel(FarArgs a)
     if (active) {
         double2 *Mo = a.M + (a.soff[d] + slot) * (int64_t)KW * P;
 #pragma unroll
-        for (int v = 0; v < 2; ++v) {
-            const int n = n0 + 2 * tn + v;
-            if (2 * tn + v >= nm) continue;
+        for (int v = 0; v < kP2MTM; ++v) {
+            const int n = n0 + kP2MTM * tn + v;
+            if (kP2MTM * tn + v >= nm) continue;
 #pragma unroll
             for (int u = 0; u < kP2MRC; ++u)
                 if (c0 + u < P) Mo[(int64_t)n * P + c0 + u] = acc[v][u];
