@@ -236,6 +236,8 @@ cylfmm_status cylfmm_fmm_solve_dist(cylfmm_plan plan, const double *src_r, const
  *     cost(leaf) = n_t * [ (sum over the 9 neighbour leaves of n_s) * (200 + 9 K)   near field
  *                          + 4 P K ]                                                L2P
  *                + (non-empty source boxes in the leaf's S2L list) * 4 P^2 K        S2L
+ *                + sum over its ancestors A (levels 2..d-1) of the S2L work of A times
+ *                  n_t / (field points in A)                          ancestors' S2L
  * (P = (p+1)(p+2)/2; SURVEY 8(d) work per unit), and every field point gets the part of its
  * leaf.  part (HOST, int32 [n_fld], out): part index in [0, n_parts) of each field point, input
  * order.  part_cost (HOST, double [n_parts], out, nullable): estimated flops per part.

@@ -1861,6 +1861,32 @@ extern "C" cylfmm_status cylfmm_partition_fields(const double *src_r, const doub
                 }
             cost[k] = (double)nt[k] * (near * wpair + wl2p) + far;
         }
+    // the ancestors' S2L (levels 2..d-1), shared among a box's target leaves by field count
+    for (int l = 2; l < d; ++l) {
+        const int nbl = 1 << l, sh = 2 * (d - l);
+        std::vector<int64_t> nsl((size_t)nbl * nbl, 0), ntl((size_t)nbl * nbl, 0);
+        for (size_t k = 0; k < nleaf; ++k) {
+            nsl[k >> sh] += ns[k];
+            ntl[k >> sh] += nt[k];
+        }
+        std::vector<double> share((size_t)nbl * nbl, 0.0);   // S2L flops per field point
+        for (int ix = 0; ix < nbl; ++ix)
+            for (int iz = 0; iz < nbl; ++iz) {
+                const uint32_t k = host_morton((uint32_t)ix, (uint32_t)iz);
+                if (!ntl[k]) continue;
+                int pairs = 0;
+                const int px = ix >> 1, pz = iz >> 1;
+                for (int x = 2 * px - 2; x <= 2 * px + 3; ++x)
+                    for (int z = 2 * pz - 2; z <= 2 * pz + 3; ++z) {
+                        if (x < 0 || z < 0 || x >= nbl || z >= nbl) continue;
+                        if (std::abs(x - ix) <= 1 && std::abs(z - iz) <= 1) continue;
+                        if (nsl[host_morton((uint32_t)x, (uint32_t)z)]) ++pairs;
+                    }
+                share[k] = pairs * ws2l / (double)ntl[k];
+            }
+        for (size_t k = 0; k < nleaf; ++k)
+            if (nt[k]) cost[k] += share[k >> sh] * (double)nt[k];
+    }
     double total = 0.0;
     for (double c : cost) total += c;
     // contiguous Morton ranges: leaf k goes to part floor(n_parts * (prefix before k + c/2) / total)
