@@ -137,6 +137,18 @@ cylfmm_status cylfmm_plan_sync(cylfmm_plan plan);
  * the S2L pair count / kernel launches of the last solve.  Errors: EINVAL (null argument),
  * ECUDA. */
 cylfmm_status cylfmm_plan_set_profiling(cylfmm_plan plan, int on);
+
+/* Geometry cache.  on != 0: a solve whose coordinate arrays (src_r, src_z, fld_r, fld_z pointers
+ * and sizes) are those of the previous solve on this plan reuses everything that depends only on
+ * the coordinates -- the Morton orders, leaf ranges and level maps, the S2L pair lists and
+ * batches, the lazy-L2L rows, the near-field and L2P task lists, and (when all modes fit one
+ * chunk) the derivative tensors -- and runs only the coefficient-dependent passes (gather of the
+ * coefficient rows, P2M, M2M, S2L, L2L, L2P, near field).  Such a solve has NO host
+ * synchronisation and allocates nothing, so it can be captured into a CUDA graph.  The caller
+ * guarantees that the coordinates themselves did not change (the coefficients src_S may).
+ * Switching the cache on (or off) invalidates the remembered geometry.  Results are bitwise those
+ * of an uncached solve.  Errors: EINVAL (null plan). */
+cylfmm_status cylfmm_plan_set_geometry_cache(cylfmm_plan plan, int on);
 cylfmm_status cylfmm_plan_read_timings(cylfmm_plan plan, cylfmm_timings *timings);
 
 /* FMM solve, Algorithm 1 of the paper:

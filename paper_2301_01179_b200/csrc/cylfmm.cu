@@ -538,6 +538,17 @@ struct cylfmm_plan_s {
     int prof_solves = 0;
     bool prof_on = false;
     int64_t last_npairs = 0, last_launches = 0;
+    // geometry cache (cylfmm_plan_set_geometry_cache): the coordinate-only results of the last
+    // solve (sorted orders, lists, tensors, task lists live in the plan's buffers)
+    bool geo_cache = false;
+    struct {
+        bool valid = false, grad = false;
+        const double *sr = nullptr, *sz = nullptr, *fr = nullptr, *fz = nullptr;
+        int64_t ns = 0, nf = 0, nslots = 0;
+        int *sperm = nullptr, *fperm = nullptr;
+        uint32_t *skey_s = nullptr, *fkey_s = nullptr;
+        int hcnt[3 * kMaxLevels + 8];
+    } geo;
     // multi-device (cylfmm_plan_create_dist): the library-owned NCCL communicator
     ncclComm_t comm = nullptr;
     int nranks = 1, rank = 0;
@@ -733,6 +744,17 @@ extern "C" cylfmm_status cylfmm_plan_set_profiling(cylfmm_plan plan, int on)
     plan->marks.clear();
     plan->evused = 0;
     plan->prof_solves = 0;
+    return CYLFMM_OK;
+}
+
+extern "C" cylfmm_status cylfmm_plan_set_geometry_cache(cylfmm_plan plan, int on)
+{
+    if (!plan) {
+        set_err("cylfmm_plan_set_geometry_cache: null plan");
+        return CYLFMM_EINVAL;
+    }
+    plan->geo_cache = on != 0;
+    plan->geo.valid = false;   // the next solve builds (and remembers) its geometry
     return CYLFMM_OK;
 }
 
@@ -955,12 +977,41 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     ta.seeds = p->seeds.as<double>();
     ta.packed = 1;
     ta.err = p->err.as<int>();
-    // ---- tree
-    T.beg(PH_SORT, st);
-    int *sperm = nullptr, *fperm = nullptr;
-    uint32_t *skey_s = nullptr, *fkey_s = nullptr;
-    // fields == sources (C2-C4: "field points equal to source points"): one tree serves both
+    // ---- tree and lists (geometry).  With the plan's geometry cache on and the same coordinate
+    // arrays as the previous solve (the caller guarantees unchanged coordinates), everything
+    // below that depends only on the coordinates is reused: no sort, no lists, no tensors and no
+    // host synchronisation, so the solve can be captured into a CUDA graph.
     const bool same = fld_r == src_r && fld_z == src_z && nf == ns;
+    const bool reuse = p->geo_cache && p->geo.valid && p->geo.sr == src_r && p->geo.sz == src_z &&
+                       p->geo.fr == fld_r && p->geo.fz == fld_z && p->geo.ns == ns &&
+                       p->geo.nf == nf && p->geo.grad == grad && !dist;
+    int *sperm = reuse ? p->geo.sperm : nullptr, *fperm = reuse ? p->geo.fperm : nullptr;
+    uint32_t *skey_s = reuse ? p->geo.skey_s : nullptr, *fkey_s = reuse ? p->geo.fkey_s : nullptr;
+    const int64_t nleaf = pow4(d);
+    int64_t lvoff[kMaxLevels + 1];
+    lvoff[0] = lvoff[1] = lvoff[2] = 0;
+    for (int l = 2; l <= d; ++l) lvoff[l + 1] = lvoff[l] + pow4(l);
+    const int64_t ltot = lvoff[d + 1];
+    // buffer pointers: set after the buffers are sized (geometry pass) or taken as they are (reuse)
+    const int *flstart = nullptr;
+    int *tmap_b = nullptr, *tkeys_b = nullptr;
+    auto set_ptrs = [&]() {
+        flstart = same ? p->slstart.as<int>() : p->flstart.as<int>();
+        tmap_b = same ? p->smap.as<int>() : p->tmap.as<int>();
+        tkeys_b = same ? p->skeys.as<int>() : p->tkeys.as<int>();
+    };
+    if (reuse) set_ptrs();
+    const int nkeys = 2 * 12 * (1 << d), JT = s2l_jt(pl);
+    const bool wsave = ns > 0 && !grad && K > kP2PWWindow && K <= 2 * kP2PWWindow &&
+                       p2pw_enabled(K, grad);
+    int64_t nslots = reuse ? p->geo.nslots : 0;
+    int hcnt[3 * kMaxLevels + 8] = {0};
+    if (reuse) memcpy(hcnt, p->geo.hcnt, sizeof hcnt);
+    S2LListArgs la = {};
+    int *cnt_ex = nullptr;
+    T.beg(PH_SORT, st);
+    if (!reuse) {
+    // fields == sources (C2-C4: "field points equal to source points"): one tree serves both
     RET_IF(build_tree(p, src_r, src_z, ns, true, st, &sperm, &skey_s));
     if (same) {
         fperm = sperm;
@@ -973,52 +1024,33 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     RET_IF(p->S_s.need(16 * (size_t)std::max<int64_t>(ns, 1) * K));
     RET_IF(p->fr_s.need(8 * nf));
     RET_IF(p->fz_s.need(8 * nf));
-    if (ns > 0) {
-        if (s_ready) CK(cudaStreamWaitEvent(st, s_ready, 0));   // host solve: S copied behind the sort
-        gather_points_kernel<<<nblk(ns * std::max(K, 1), 256), 256, 0, st>>>(
-            src_r, src_z, reinterpret_cast<const double2 *>(src_S), sperm, ns, K,
-            p->sr_s.as<double>(), p->sz_s.as<double>(), p->S_s.as<double2>());
-        CKL();
-        p->launches++;
-    }
-    const double *fr_sorted = p->sr_s.as<double>(), *fz_sorted = p->sz_s.as<double>();
     if (!same) {
         gather_points_kernel<<<nblk(nf, 256), 256, 0, st>>>(fld_r, fld_z, nullptr, fperm, nf, 0,
                                                             p->fr_s.as<double>(), p->fz_s.as<double>(),
                                                             nullptr);
         CKL();
         p->launches++;
-        fr_sorted = p->fr_s.as<double>();
-        fz_sorted = p->fz_s.as<double>();
     }
     T.end(PH_SORT, st);
     T.beg(PH_LISTS, st);
-    const int64_t nleaf = pow4(d);
     RET_IF(p->slstart.need(sizeof(int) * (nleaf + 1)));
     RET_IF(p->flstart.need(sizeof(int) * (nleaf + 1)));
     leaf_start_kernel<<<nblk(nleaf + 1, 256), 256, 0, st>>>(skey_s, ns, nleaf, p->slstart.as<int>());
     CKL();
     p->launches++;
-    const int *flstart = p->slstart.as<int>();
     if (!same) {
         leaf_start_kernel<<<nblk(nleaf + 1, 256), 256, 0, st>>>(fkey_s, nf, nleaf, p->flstart.as<int>());
         CKL();
         p->launches++;
-        flstart = p->flstart.as<int>();
     }
     // level maps
-    int64_t lvoff[kMaxLevels + 1];
-    lvoff[0] = lvoff[1] = lvoff[2] = 0;
-    for (int l = 2; l <= d; ++l) lvoff[l + 1] = lvoff[l] + pow4(l);
-    const int64_t ltot = lvoff[d + 1];
     RET_IF(p->flags.need(sizeof(int) * ltot));
     RET_IF(p->smap.need(sizeof(int) * ltot));
     RET_IF(p->skeys.need(sizeof(int) * ltot));
     RET_IF(p->tmap.need(sizeof(int) * ltot));
     RET_IF(p->tkeys.need(sizeof(int) * ltot));
     RET_IF(p->counts.need(sizeof(int) * (3 * kMaxLevels + 8)));
-    int *tmap_b = same ? p->smap.as<int>() : p->tmap.as<int>();
-    int *tkeys_b = same ? p->skeys.as<int>() : p->tkeys.as<int>();
+    set_ptrs();
     const int nside = same ? 1 : 2;
     int lsmall = 1;   // levels 2..lsmall in one launch (4^l <= kSmallLevelBoxes)
     while (lsmall + 1 <= d && pow4(lsmall + 1) <= kSmallLevelBoxes) ++lsmall;
@@ -1056,7 +1088,6 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     // S2L interaction lists (s2l.cuh): every (target box, source box) pair of every level,
     // counted per target (dense index) and per station key; the per-box "written by S2L" flags
     // that L2L / L2P use instead of zero-initialised locals
-    const int nkeys = 2 * 12 * (1 << d), JT = s2l_jt(pl);
     RET_IF(p->written.need(std::max<int64_t>(ltot, 1)));
     RET_IF(p->pcnt.need(sizeof(int) * std::max<int64_t>(ltot, 1)));
     RET_IF(p->poff.need(sizeof(int) * std::max<int64_t>(ltot, 1)));
@@ -1065,7 +1096,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     RET_IF(p->kstart.need(sizeof(int) * nkeys));
     RET_IF(p->kcur.need(sizeof(int) * nkeys));
     RET_IF(p->bstart.need(sizeof(int) * nkeys));
-    int *cnt_ex = p->counts.as<int>() + 2 * kMaxLevels;   // [0] written targets, [1] max source
+    cnt_ex = p->counts.as<int>() + 2 * kMaxLevels;   // [0] written targets, [1] max source
                                                           // column, [2] pairs, [3] batches,
                                                           // [4] materialised locals,
                                                           // [5] stations with a pair,
@@ -1077,7 +1108,6 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         CKL();
         p->launches++;
     }
-    S2LListArgs la = {};
     la.depth = d;
     for (int l = 2; l <= d; ++l) {
         la.smap[l] = p->smap.as<int>() + lvoff[l];
@@ -1160,8 +1190,6 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         p->launches += 3;
     }
     // near-field window state (K in (33, 66], two mode windows): pair slots by target leaf
-    const bool wsave = ns > 0 && !grad && K > kP2PWWindow && K <= 2 * kP2PWWindow &&
-                       p2pw_enabled(K, grad);
     if (wsave) {
         const int64_t nl = pow4(d);
         RET_IF(p->pbase.need(sizeof(int64_t) * (nl + 2)));
@@ -1176,14 +1204,26 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         CKL();
         p->launches += 3;
     }
-    int64_t nslots = 0;
-    int hcnt[3 * kMaxLevels + 8] = {0};
     CK(cudaMemcpyAsync(hcnt, p->counts.p, sizeof(int) * (3 * kMaxLevels + 8), cudaMemcpyDeviceToHost, st));
     if (wsave) CK(cudaMemcpyAsync(&nslots, p->pbase.as<int64_t>() + pow4(d), sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     RET_IF(check_err_flag(p, st));
-    if (same)
-        for (int l = 0; l < kMaxLevels; ++l) hcnt[kMaxLevels + l] = hcnt[l];
+        if (same)
+            for (int l = 0; l < kMaxLevels; ++l) hcnt[kMaxLevels + l] = hcnt[l];
+    } else {
+        T.end(PH_SORT, st);
+        T.beg(PH_LISTS, st);
+    }
+    if (ns > 0) {
+        if (s_ready) CK(cudaStreamWaitEvent(st, s_ready, 0));   // host solve: S copied behind the sort
+        gather_points_kernel<<<nblk(ns * std::max(K, 1), 256), 256, 0, st>>>(
+            src_r, src_z, reinterpret_cast<const double2 *>(src_S), sperm, ns, K,
+            p->sr_s.as<double>(), p->sz_s.as<double>(), p->S_s.as<double2>());
+        CKL();
+        p->launches++;
+    }
+    const double *fr_sorted = same ? p->sr_s.as<double>() : p->fr_s.as<double>();
+    const double *fz_sorted = same ? p->sz_s.as<double>() : p->fz_s.as<double>();
     // the pair lists, now that their sizes are known
     const int64_t npairs = hcnt[2 * kMaxLevels + 2], nbatches = hcnt[2 * kMaxLevels + 3];
     const int nwritten = hcnt[2 * kMaxLevels];
@@ -1196,12 +1236,29 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     RET_IF(p->batches.need(sizeof(int4) * std::max<int64_t>(nbatches, 1)));
     la.pairs = p->pairs.as<int4>();
     la.batches = p->batches.as<int4>();
+    if (!reuse) {
     if (npairs > 0) {
         s2l_emit_kernel<<<nblk(ltot, 256), 256, 0, st>>>(la);
         CKL();
         s2l_batch_emit_kernel<<<nblk(nkeys, 256), 256, 0, st>>>(la);
         CKL();
         p->launches += 2;
+    }
+        // remember the geometry for the next solve with the same coordinate arrays
+        p->geo.valid = true;
+        p->geo.sr = src_r;
+        p->geo.sz = src_z;
+        p->geo.fr = fld_r;
+        p->geo.fz = fld_z;
+        p->geo.ns = ns;
+        p->geo.nf = nf;
+        p->geo.grad = grad;
+        p->geo.sperm = sperm;
+        p->geo.fperm = fperm;
+        p->geo.skey_s = skey_s;
+        p->geo.fkey_s = fkey_s;
+        p->geo.nslots = nslots;
+        memcpy(p->geo.hcnt, hcnt, sizeof hcnt);
     }
     T.end(PH_LISTS, st);
     // ---- far-field storage
@@ -1328,7 +1385,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         CK(cudaEventRecord(p->aev[1], st));
         CK(cudaStreamWaitEvent(st_t, p->aev[1], 0));
     }
-    if (nstu > 0) {   // seeds of all modes once, for the stations with a pair
+    if (nstu > 0 && !(reuse && KW == K)) {   // seeds of all modes once, stations with a pair
         T.beg(PH_TENSOR, st_t);
         RET_IF(run_seeds(ta, nstu, st_t));
         p->launches++;
@@ -1352,7 +1409,9 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             // warp tasks: <= nf/32 full pieces + <= 5 power-of-two pieces per leaf
             int64_t maxtasks = wk ? nf / 32 + 6 * (int64_t)ntl + 1 : nf / TT + ntl + 1;
             RET_IF(p->tasks.need(sizeof(int4) * maxtasks));
-            if (wk) {
+            if (wk && reuse) {   // the task list is the previous solve's: rewind the fetch counter
+                CK(cudaMemsetAsync(p->ntasks.as<int>() + 1, 0, sizeof(int), st_n));
+            } else if (wk) {
                 CK(cudaMemsetAsync(p->ntasks.as<int>(), 0, kTaskCtrInts * sizeof(int), st_n));
                 near_wtasks_count_kernel<<<nblk(ntl, 256), 256, 0, st_n>>>(fa.tkeys[d], ntl, fa.flstart,
                                                                         fa.slstart, d, p->ntasks.as<int>());
@@ -1441,7 +1500,8 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             T.beg(PH_TENSOR, st_t);
             // the stations with a pair are the only ones S2L reads (dense layout, i_in <= the
             // largest source column)
-            if (nstu > 0) RET_IF(run_fill(ta, nstu, st_t));
+            // (reused with the geometry when all modes fit one chunk: the tensors are still there)
+            if (nstu > 0 && !(reuse && KW == K)) RET_IF(run_fill(ta, nstu, st_t));
             p->launches++;
             T.end(PH_TENSOR, st_t);
             if (overlap) CK(cudaEventRecord(p->aev[2], st_t));
@@ -1523,7 +1583,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             fa.l2p_tp = ppl < 8 ? 128 : (int)std::min<int64_t>(128, std::max<int64_t>(16, (int64_t)1 << (63 - __builtin_clzll(ppl))));
             const int gpc = kL2PThreads / fa.l2p_tp;
             const int64_t ub_tasks = nf / fa.l2p_tp + ntl + 1;
-            if (m0 == 0) {   // evaluating box of every target leaf (written flags are per solve)
+            if (m0 == 0 && !reuse) {   // evaluating box of every target leaf and the L2P runs
                 l2p_owner_kernel<<<nblk(ntl, 256), 256, 0, st>>>(fa, p->l2pown.as<int>());
                 CKL();
                 int *flag = p->l2pflag.as<int>(), *pos = p->l2ppos.as<int>();

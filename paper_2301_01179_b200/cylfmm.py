@@ -89,6 +89,8 @@ def lib():
     L.cylfmm_fmm_solve_dist.restype = i
     L.cylfmm_fmm_solve_dist.argtypes = [vp, vp, vp, vp, i64, vp, vp, i64, vp, vp,
                                          ctypes.POINTER(Timings)]
+    L.cylfmm_plan_set_geometry_cache.restype = i
+    L.cylfmm_plan_set_geometry_cache.argtypes = [vp, i]
     L.cylfmm_plan_set_profiling.restype = i
     L.cylfmm_plan_set_profiling.argtypes = [vp, i]
     L.cylfmm_plan_read_timings.restype = i
@@ -316,6 +318,12 @@ class Plan:
 
     def sync(self):
         _check(lib().cylfmm_plan_sync(self._h), "cylfmm_plan_sync")
+
+    def set_geometry_cache(self, on: bool):
+        """Reuse the coordinate-only work of the previous solve when the coordinate arrays are the
+        same (cylfmm_plan_set_geometry_cache): sync-free, graph-capturable solves."""
+        _check(lib().cylfmm_plan_set_geometry_cache(self._h, int(bool(on))),
+               "cylfmm_plan_set_geometry_cache")
 
     def set_profiling(self, on: bool):
         """Record phase events in the following (asynchronous) solves (cylfmm_plan_set_profiling)."""

@@ -504,3 +504,48 @@ def test_dist_solve_single_rank_bitwise(gpu, name):
     out2 = dplan.solve_dist(t(sr), t(sz), t(S), t(fr), t(fz)).cpu().numpy()
     assert np.array_equal(out2, ref)
     dplan.close()
+
+
+@pytest.mark.parametrize("name", ["C2", "sparse"])
+def test_geometry_cache_and_cuda_graph(gpu, name):
+    """cylfmm_plan_set_geometry_cache: a second solve on the same coordinate arrays reuses the
+    sort, lists, tensors and task lists (no host synchronisation) and equals an uncached solve bit
+    for bit, also with new coefficients; captured into a CUDA graph it replays to the same
+    values."""
+    import torch
+    sr, sz, S, fr, fz, p, depth, L, z0 = _partition_case(name)
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=dev)  # noqa: E731
+    cfg = gpu.FMMConfig(n_modes=S.shape[1], order=p, depth=depth, L=L, z0=z0)
+    r_s, z_s, f_r, f_z = t(sr), t(sz), t(fr), t(fz)
+    S1 = t(S)
+    S2 = t(S[::-1].copy() * (0.5 - 0.25j))
+    fresh = gpu.Plan(cfg)
+    ref1 = fresh.solve(r_s, z_s, S1, f_r, f_z).cpu().numpy()
+    ref2 = fresh.solve(r_s, z_s, S2, f_r, f_z).cpu().numpy()
+    fresh.close()
+    plan = gpu.Plan(cfg)
+    plan.set_geometry_cache(True)
+    out = torch.empty((len(fr), S.shape[1]), dtype=torch.complex128, device=dev)
+    plan.solve(r_s, z_s, S1, f_r, f_z, out=out)            # builds and remembers the geometry
+    assert np.array_equal(out.cpu().numpy(), ref1)
+    plan.solve(r_s, z_s, S2, f_r, f_z, out=out)            # reuses it
+    assert np.array_equal(out.cpu().numpy(), ref2)
+    Sg = S1.clone()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        plan.solve(r_s, z_s, Sg, f_r, f_z, out=out)        # warm on the capture stream
+        with torch.cuda.graph(g, stream=s):
+            plan.solve(r_s, z_s, Sg, f_r, f_z, out=out)
+    torch.cuda.current_stream().wait_stream(s)
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), ref1)
+    Sg.copy_(S2)
+    g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), ref2)
+    plan.close()
