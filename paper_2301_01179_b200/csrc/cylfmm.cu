@@ -1414,10 +1414,12 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             } else if (wk) {
                 CK(cudaMemsetAsync(p->ntasks.as<int>(), 0, kTaskCtrInts * sizeof(int), st_n));
                 near_wtasks_count_kernel<<<nblk(ntl, 256), 256, 0, st_n>>>(fa.tkeys[d], ntl, fa.flstart,
-                                                                        fa.slstart, d, p->ntasks.as<int>());
+                                                                        fa.slstart, d, accumulate,
+                                                                        p->ntasks.as<int>());
                 CKL();
                 near_wtasks_emit_kernel<<<nblk(ntl, 256), 256, 0, st_n>>>(fa.tkeys[d], ntl, fa.flstart,
-                                                                       fa.slstart, d, p->tasks.as<int4>(),
+                                                                       fa.slstart, d, accumulate,
+                                                                       p->tasks.as<int4>(),
                                                                        p->ntasks.as<int>());
             } else {
                 near_tasks_count_kernel<<<nblk(ntl, 256), 256, 0, st_n>>>(fa.tkeys[d], ntl, fa.flstart, TT,

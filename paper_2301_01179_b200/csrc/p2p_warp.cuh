@@ -656,13 +656,16 @@ __device__ __forceinline__ int task_bucket(int nt, int nsrc)
     const unsigned cost = (unsigned)tw * (unsigned)max(nsrc, 1);
     return 31 - __clz(cost);
 }
+// skip_empty: leaves without a source in their 9 neighbours get no task (the near field only
+// adds onto rows the far field wrote: an empty task would add zeros)
 __global__ void near_wtasks_count_kernel(const int *tkeys, int nleaf, const int *flstart,
-                                         const int *slstart, int depth, int *ctr)
+                                         const int *slstart, int depth, int skip_empty, int *ctr)
 {
     int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= nleaf) return;
     const int key = tkeys[s];
     const int nsrc = near_sources(key, slstart, depth);
+    if (skip_empty && nsrc == 0) return;
     for (int nt = flstart[key + 1] - flstart[key]; nt > 0;) {
         const int take = piece_size(nt);
         atomicAdd(&ctr[2 + task_bucket(take, nsrc)], 1);
@@ -670,7 +673,8 @@ __global__ void near_wtasks_count_kernel(const int *tkeys, int nleaf, const int 
     }
 }
 __global__ void near_wtasks_emit_kernel(const int *tkeys, int nleaf, const int *flstart,
-                                        const int *slstart, int depth, int4 *tasks, int *ctr)
+                                        const int *slstart, int depth, int skip_empty, int4 *tasks,
+                                        int *ctr)
 {
     __shared__ int off[32];
     if (threadIdx.x < 32) {
@@ -684,6 +688,7 @@ __global__ void near_wtasks_emit_kernel(const int *tkeys, int nleaf, const int *
     if (s >= nleaf) return;
     const int key = tkeys[s];
     const int nsrc = near_sources(key, slstart, depth);
+    if (skip_empty && nsrc == 0) return;
     int t = flstart[key], nt = flstart[key + 1] - t;
     while (nt > 0) {
         const int take = piece_size(nt);
