@@ -141,7 +141,7 @@ static cudaError_t allow_smem(F *kernel)
 // groups) per local-order class; JT = CG C pairs per batch
 #define S2L_P8 4, 4, 16, 8
 #define S2L_P12 4, 4, 32, 8
-#define S2L_P16 4, 4, 48, 4
+#define S2L_P16 4, 3, 48, 4
 #define S2L_ALL(X) X(S2L_P8) X(S2L_P12) X(S2L_P16)
 
 static cylfmm_status ensure_init()
@@ -1292,7 +1292,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         // chunk must fit in a third of the free device memory (C5: 1.8 GB per mode).  The free
         // memory is queried only when the current allocations cannot hold all modes (the query
         // is slow; steady-state solves reuse the plan's workspace).
-        size_t per_mode = sizeof(double2) * ((size_t)stot * P + (size_t)(nlc + npairs) * Pl) +
+        size_t per_mode = sizeof(double2) * ((size_t)2 * stot * P + (size_t)(nlc + npairs) * Pl) +
                           sizeof(double) * nstat_used * TP;
         size_t have = p->M.cap + p->Lc.cap + p->tens.cap + p->pairbuf.cap;   // reusable allocations
         if (per_mode * (size_t)K > have) {
@@ -1318,7 +1318,8 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         CK(cudaStreamSynchronize(st));
         for (int64_t v : kws) KW = (int)std::min<int64_t>(KW, v);
     }
-    RET_IF(p->M.need(sizeof(double2) * (size_t)std::max<int64_t>(stot, 1) * KW * P));
+    // moments, then their S2L copy for backward pairs (prescale_moments_kernel)
+    RET_IF(p->M.need(sizeof(double2) * (size_t)std::max<int64_t>(stot, 1) * KW * P * 2));
     RET_IF(p->Lc.need(sizeof(double2) * (size_t)std::max<int64_t>(nlc, 1) * KW * Pl));
     RET_IF(p->tens.need(sizeof(double) * (size_t)std::max<int64_t>(nstat_used, 1) * KW * TP));
     RET_IF(p->pairbuf.need(sizeof(double2) * (size_t)std::max<int64_t>(npairs, 1) * KW * Pl));
@@ -1351,6 +1352,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     sa.K = K;
     sa.tens = p->tens.as<double>();
     sa.M = p->M.as<double2>();
+    sa.Mb = sa.M + (size_t)std::max<int64_t>(stot, 1) * KW * P;
     sa.pairs = p->pairs.as<int4>();
     sa.batches = p->batches.as<int4>();
     for (int l = 2; l <= d; ++l) sa.soff[l] = fa.soff[l];
@@ -1542,7 +1544,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
                 p->launches++;
             }
             // S2L consumes the moments pre-scaled by (-1)^j / j! (fmm_ops.cuh)
-            prescale_moments_kernel<<<nblk(stot * kw * P, 256), 256, 0, st>>>(fa.M, stot * kw, P, fa.pscale);
+            prescale_moments_kernel<<<nblk(stot * kw * P, 256), 256, 0, st>>>(fa.M, const_cast<double2 *>(sa.Mb), stot * kw, P, fa.pscale);
             CKL();
             p->launches++;
             T.end(PH_M2M, st);

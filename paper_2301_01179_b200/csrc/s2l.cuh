@@ -12,8 +12,8 @@
 //     key = ((i_in * 12 + class) << 1) | inward,
 // and each bucket is cut into batches of JT pairs: one CTA applies ONE staged operator to JT
 // pairs (a full register-tiled FP64 GEMM, however sparse the inputs are: C5's sources lie on two
-// curves, so a target column sees ~2 of them per offset).  Backward pairs negate their odd-j
-// moment coefficients and odd-l result rows around the GEMM (exact).  Each pair's contribution
+// curves, so a target column sees ~2 of them per offset).  Backward pairs read a moment copy
+// with their odd-j sign flip folded in and negate their odd-l result rows (exact).  Each pair's contribution
 // goes to its own slot of a pair buffer (target-major), and a reduction sums every target box's
 // slots in the fixed offset order: results are bitwise reproducible, independent of how pairs are
 // batched and of which other target boxes exist (a field-partitioned solve equals the full one).
@@ -153,7 +153,8 @@ __global__ void s2l_totals_kernel(S2LListArgs a)
 // ring of R tensor values in registers, H[T(k,i) + j + l0 + r], loading ONE new value per step
 // (the window slides by one), so a step is 1 scalar + C vector shared loads for 2 R C DFMA.
 // Results are post-scaled by 1/l! (and (-1)^l for backward pairs) and written as contiguous runs
-// of the pair's row in the pair buffer.  Single truncation (i+j+k+l <= p, R#8) zeroes the tensor
+// of the pair's row in the pair buffer.  Backward pairs read moments pre-scaled without the
+// (-1)^j (their sign flip on j is folded into the second copy).  Single truncation (i+j+k+l <= p, R#8) zeroes the tensor
 // entries with a + b + c > p in shared memory first.
 template <int R, int C, int NU, int CG>
 struct S2LCfg {
@@ -166,7 +167,8 @@ struct S2LArgs {
     int p, P, pl, Pl, pt, K, m0, m1;
     int truncation;
     const double *tens;        // [stations][KW][TPp] packed
-    const double2 *M;          // pre-scaled moments [row][KW][P]
+    const double2 *M;          // pre-scaled moments [row][KW][P]: (-1)^j / j! (forward pairs)
+    const double2 *Mb;         // the same with 1 / j! (backward pairs: (-1)^j folded in)
     const int4 *pairs, *batches;
     int64_t soff[kMaxLevels];  // per level: first moment row
     double2 *pairbuf;          // [slot][KW][Pl]
@@ -219,8 +221,12 @@ __device__ __forceinline__ int packed_row(int a, int b, int pt)
            b * (2 * pt + 1 - a) - b * (b - 1) / 2;
 }
 
+// resident CTAs per SM the shape is built for (shared memory at p = 16: tensor 39 KB + JT rows)
+template <int C>
+__host__ __device__ constexpr int s2l_min_blocks() { return C <= 3 ? 3 : 1; }
+
 template <int R, int C, int NU, int CG>
-__global__ void __launch_bounds__(NU * CG) s2l_batch_kernel(S2LArgs a)
+__global__ void __launch_bounds__(NU * CG, s2l_min_blocks<C>()) s2l_batch_kernel(S2LArgs a)
 {
     constexpr int NT = NU * CG, JT = CG * C;
     extern __shared__ double sm[];
@@ -240,50 +246,46 @@ __global__ void __launch_bounds__(NU * CG) s2l_batch_kernel(S2LArgs a)
     const int cnt = bt.y, skey = bt.z, inward = skey & 1;
     const int64_t station = skey >> 1;
     const int tid = threadIdx.x;
-    if (tid < JT) rec[tid] = tid < cnt ? a.pairs[bt.x + tid] : make_int4(0, -1, 0, 0);
-    for (int q = tid; q < (pl + 1) * (p + 1); q += NT) {
-        const int k = q / (p + 1), i = q - k * (p + 1);
-        Tk[q] = inward ? packed_row(i, k, pt) : packed_row(k, i, pt);
-    }
-    if (tid == 0) {
-        int u = 0;
-        for (int k = 0; k <= pl; ++k)
-            for (int l0 = 0; l0 <= pl - k; l0 += R) ukl[u++] = (k << 8) | l0;
-        for (; u < NU; ++u) ukl[u] = -1;
-        for (int e = 0; e < R + 2; ++e) Hs[TPp + e] = 0.0;
-        mbar_init(bar, 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-    // TMA: the tensor block and one moment row per pair on one mbarrier
+    // warp 0 starts the copies at once (barrier, tensor block, one moment row per pair: backward
+    // pairs read the copy with (-1)^j folded in) while the other warps build the index tables
     if (tid < 32) {
         if (tid == 0) {
+            mbar_init(bar, 1);
+            fence_mbar_init();
             mbar_arrive_expect_tx(bar, (unsigned)(TPp * 8 + cnt * P * 16));
             bulk_g2s(Hs, a.tens + (station * KW + nloc) * (int64_t)TPp, (unsigned)(TPp * 8), bar);
         }
         __syncwarp();
-        for (int b = tid; b < cnt; b += 32)
-            bulk_g2s(Xs + b * BPS, a.M + ((a.soff[rec[b].w] + rec[b].x) * KW + nloc) * P,
-                     (unsigned)(P * 16), bar);
-    }
-    mbar_wait(bar, 0);
-    // backward pairs: (-1)^j on the moment coefficients (i, j)
-    for (int q = tid; q < cnt * (p + 1); q += NT) {
-        const int b = q / (p + 1), i = q - b * (p + 1);
-        if (!rec[b].z) continue;
-        const int q0 = i * (p + 1) - i * (i - 1) / 2;
-        for (int j = 1; i + j <= p; j += 2) {
-            const double2 v = Xs[b * BPS + q0 + j];
-            Xs[b * BPS + q0 + j] = make_double2(-v.x, -v.y);
+        for (int b = tid; b < JT; b += 32) {
+            const int4 pr = b < cnt ? a.pairs[bt.x + b] : make_int4(0, -1, 0, 0);
+            rec[b] = pr;
+            if (b < cnt)
+                bulk_g2s(Xs + b * BPS, (pr.z ? a.Mb : a.M) + ((a.soff[pr.w] + pr.x) * KW + nloc) * P,
+                         (unsigned)(P * 16), bar);
+        }
+    } else {
+        for (int q = tid - 32; q < (pl + 1) * (p + 1); q += NT - 32) {
+            const int k = q / (p + 1), i = q - k * (p + 1);
+            Tk[q] = inward ? packed_row(i, k, pt) : packed_row(k, i, pt);
+        }
+        if (tid == 32) {
+            int u = 0;
+            for (int k = 0; k <= pl; ++k)
+                for (int l0 = 0; l0 <= pl - k; l0 += R) ukl[u++] = (k << 8) | l0;
+            for (; u < NU; ++u) ukl[u] = -1;
+            for (int e = 0; e < R + 2; ++e) Hs[TPp + e] = 0.0;
         }
     }
-    if (a.truncation == 1)   // single truncation: H(a, b, c) = 0 for a + b + c > p
+    __syncthreads();   // tables, records and the initialised barrier
+    mbar_wait(bar, 0);
+    if (a.truncation == 1) {   // single truncation: H(a, b, c) = 0 for a + b + c > p
         for (int q = tid; q < (pt + 1) * (pt + 1); q += NT) {
             const int aa = q / (pt + 1), bb = q - aa * (pt + 1);
             const int o = packed_row(aa, bb, pt);
             for (int c = max(p - aa - bb + 1, 0); c <= 2 * pt - aa - bb; ++c) Hs[o + c] = 0.0;
         }
-    __syncthreads();
+        __syncthreads();
+    }
 
     const int u = tid % NU, cg = tid / NU;
     const int kl = ukl[u];
@@ -403,14 +405,17 @@ __global__ void __launch_bounds__(256) s2l_reduce_kernel(S2LReduceArgs a)
     }
 }
 
-// Source moments pre-scaled once for S2L: M'_ij = (-1)^j M^_ij / j! (all levels, after M2M).
-__global__ void prescale_moments_kernel(double2 *M, int64_t nrows, int P, const double *pscale)
+// Source moments pre-scaled once for S2L: M'_ij = (-1)^j M^_ij / j! (all levels, after M2M),
+// and Mb = M^_ij / j! for backward pairs (their (-1)^j, cancels the forward sign).
+__global__ void prescale_moments_kernel(double2 *M, double2 *Mb, int64_t nrows, int P,
+                                        const double *pscale)
 {
     int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= nrows * P) return;
     const double f = __ldg(pscale + (int)(e % P));   // (-1)^j / j! of coefficient (i, j)
-    double2 v = M[e];
+    const double2 v = M[e];
     M[e] = make_double2(v.x * f, v.y * f);
+    Mb[e] = make_double2(v.x * fabs(f), v.y * fabs(f));
 }
 
 }  // namespace cyl
