@@ -84,7 +84,7 @@ def lib():
         L.or_s2l.restype = i
         L.or_s2l.argtypes = [pd, i, i, i, d, d, d, d, i, i, pd]
         L.or_fmm.restype = i64
-        L.or_fmm.argtypes = [pd, pd, pd, i64, pd, pd, i64, i, i, i, i, d, d, i, i, pd, pd, pd, i]
+        L.or_fmm.argtypes = [pd, pd, pd, i64, pd, pd, i64, i, i, i, i, d, d, i, i, pd, pd, pd, i, i64]
         L.or_greens_grad.restype = i
         L.or_greens_grad.argtypes = [d, d, d, i, i, pd, pd, pd]
         L.or_direct_grad.restype = i64
@@ -250,9 +250,11 @@ def s2l(M, p, rs, zs, rt, zt, truncation=TRUNC_DOUBLE, miller=MILLER_ACCURATE, p
 
 
 def fmm(sr, sz, S, fr, fz, p, depth, L, z0=0.0, truncation=TRUNC_DOUBLE,
-        miller=MILLER_ACCURATE, nthreads: int = 0, pl=None, grad=False):
+        miller=MILLER_ACCURATE, nthreads: int = 0, pl=None, grad=False, leaf_src: int = 0):
     """Algorithm 1: source/moment order p, local order pl (default p).
-    grad=True also returns the field gradients dPhi/dr, dPhi/dz: (Phi, dPr, dPz, skipped)."""
+    grad=True also returns the field gradients dPhi/dr, dPhi/dz: (Phi, dPr, dPz, skipped).
+    leaf_src > 0: the adaptive source tree of R#26 (a source box with <= leaf_src sources is a
+    leaf); 0 = the uniform tree."""
     sr, sz, fr, fz = _f64(sr), _f64(sz), _f64(fr), _f64(fz)
     S = _c128(S)
     ns, K = S.shape
@@ -265,7 +267,7 @@ def fmm(sr, sz, S, fr, fz, p, depth, L, z0=0.0, truncation=TRUNC_DOUBLE,
     sk = lib().or_fmm(_pd(sr), _pd(sz), _pd(S.view(np.float64)), ns, _pd(fr), _pd(fz), nf, K, p,
                       0 if pl is None else pl, depth, L, z0, truncation, miller,
                       _pd(Phi.view(np.float64)), _pd(Gr.view(np.float64)) if grad else nul,
-                      _pd(Gz.view(np.float64)) if grad else nul, nthreads)
+                      _pd(Gz.view(np.float64)) if grad else nul, nthreads, int(leaf_src))
     if sk < 0:
         raise ValueError("or_fmm: invalid input")
     return (Phi, Gr, Gz, int(sk)) if grad else (Phi, int(sk))

@@ -13,6 +13,16 @@
  *   L2P:       Phi(r,z) += sum Phi_kl (r-r_c)^k (z-z_c)^l.
  *   near:      direct sum over the 9 neighbour leaves, coincident pairs skipped.
  * Every ordered (source box, target box) pair computes its own tensor (no 12-class reuse).
+ *
+ * Adaptive source tree (reading R#26; leaf_src = sigma > 0): a source box with
+ * <= sigma sources is a leaf, its subtree is not descended.  An ordered pair of adjacent boxes
+ * (T, S) at level l whose parent pair was descended (l = 2, or S's parent holds > sigma sources)
+ * is evaluated directly when S is a leaf or l = d: every target of T against every source of S
+ * (P:647-651 applied at level l).  An S2L pair at level l > 2 exists only if S's
+ * parent holds > sigma sources (otherwise the parent pair was evaluated directly).  Every
+ * (target, source) pair is then covered exactly once, by the first level at which its boxes
+ * separate or its source box becomes a leaf; sigma = 0 is the uniform tree above, operation for
+ * operation.  Only the paper's operators are used (same-level S2L, M2M, L2L, L2P, direct sum).
  */
 #include <math.h>
 #include <stdlib.h>
@@ -266,13 +276,13 @@ static void demorton(uint32_t key, uint32_t *ix, uint32_t *iz)
 int64_t or_fmm(const double *sr, const double *sz, const double *S, int64_t ns,
                const double *fr, const double *fz, int64_t nf, int nmodes, int p, int pl,
                int depth, double L, double z0, int truncation, int miller, double *Phi,
-               double *dPr, double *dPz, int nthreads)
+               double *dPr, double *dPz, int nthreads, int64_t leaf_src)
 {
     /* dPr, dPz (nullable, both or neither): the field gradients, from the gradient of the local
      * expansion at the point plus the near field with the derivative relations of G (or_greens_grad) */
     const int grad = dPr != NULL && dPz != NULL;
     if (pl <= 0) pl = p; /* local order defaults to the source order */
-    if (depth < 2 || depth > 15 || p < 1 || nmodes < 1 || !(L > 0.0)) return -1;
+    if (depth < 2 || depth > 15 || p < 1 || nmodes < 1 || !(L > 0.0) || leaf_src < 0) return -1;
 #ifdef _OPENMP
     if (nthreads > 0) omp_set_num_threads(nthreads);
 #else
@@ -283,6 +293,7 @@ int64_t or_fmm(const double *sr, const double *sz, const double *S, int64_t ns,
     for (int64_t j = 0; j < nf; ++j)
         if (!(fr[j] > 0.0) || !(fr[j] <= L) || !(fz[j] >= z0) || !(fz[j] <= z0 + L)) return -1;
 
+    int64_t *scnt[16] = {0}, *sfirst[16] = {0};   /* per level: sources per box, first source */
     int P = tri_size(p), Pl = tri_size(pl);
     size_t per_box = (size_t)2 * nmodes * P;     /* source boxes: moments of order p */
     size_t per_tbox = (size_t)2 * nmodes * Pl;   /* target boxes: locals of order pl */
@@ -322,6 +333,20 @@ int64_t or_fmm(const double *sr, const double *sz, const double *S, int64_t ns,
         }
         lstart[nleaf] = ns;
     }
+    /* sources per box and first sorted source of each box, every level (a box's sources are
+     * contiguous in Morton order) */
+    for (int l = 2; l <= depth; ++l) {
+        int64_t nb_ = src[l].count > 0 ? src[l].count : 1;
+        scnt[l] = (int64_t *)calloc((size_t)nb_, sizeof(int64_t));
+        sfirst[l] = (int64_t *)calloc((size_t)nb_, sizeof(int64_t));
+        if (!scnt[l] || !sfirst[l]) err = 1;
+    }
+    if (!err)
+        for (int64_t i = 0; i < ns; ++i)
+            for (int l = 2; l <= depth; ++l) {
+                int32_t s = src[l].map[skey_sorted[i] >> (2 * (depth - l))];
+                if (scnt[l][s]++ == 0) sfirst[l][s] = i;
+            }
     if (err) goto cleanup;
 
     double hd = L / (double)(1u << depth);
@@ -386,6 +411,10 @@ int64_t or_fmm(const double *sr, const double *sz, const double *S, int64_t ns,
                             if (abs(di) <= 1 && abs(dj) <= 1) continue;
                             int32_t ss = src[l].map[morton((uint32_t)ci, (uint32_t)cj)];
                             if (ss < 0) continue;
+                            /* adaptive: the parent pair was evaluated directly (R#26) */
+                            if (leaf_src > 0 && l > 2 &&
+                                scnt[l - 1][src[l - 1].map[morton((uint32_t)a, (uint32_t)c)]] <= leaf_src)
+                                continue;
                             double sr0 = (ci + 0.5) * h, sz0 = z0 + (cj + 0.5) * h;
                             if (or_s2l(src[l].data + (size_t)ss * per_box, nmodes, p, pl, sr0, sz0,
                                        tr, tz, truncation, miller, Lb) != 0)
@@ -420,12 +449,23 @@ int64_t or_fmm(const double *sr, const double *sz, const double *S, int64_t ns,
                 if (grad)
                     or_l2p_grad(tgt[depth].data + (size_t)ts * per_tbox, nmodes, pl, rc, zc, fr[j],
                                 fz[j], outr, outz);
-                for (int a = (int)ix - 1; a <= (int)ix + 1; ++a)
-                    for (int c = (int)iz - 1; c <= (int)iz + 1; ++c) {
-                        if (a < 0 || c < 0 || a >= (int)nb || c >= (int)nb) continue;
-                        int32_t ls = src[depth].map[morton((uint32_t)a, (uint32_t)c)];
+                /* uniform: the 9 neighbour leaves; adaptive: at every level, the neighbours S of
+                 * the target's box whose pair is evaluated directly (R#26) */
+                for (int l = leaf_src > 0 ? 2 : depth; l <= depth; ++l) {
+                    const int sh = depth - l, nbl = (int)(nb >> sh);
+                    const int bx = (int)(ix >> sh), bz = (int)(iz >> sh);
+                for (int a = bx - 1; a <= bx + 1; ++a)
+                    for (int c = bz - 1; c <= bz + 1; ++c) {
+                        if (a < 0 || c < 0 || a >= nbl || c >= nbl) continue;
+                        int32_t ls = src[l].map[morton((uint32_t)a, (uint32_t)c)];
                         if (ls < 0) continue;
-                        for (int64_t q = lstart[ls]; q < lstart[ls + 1]; ++q) {
+                        if (leaf_src > 0) {
+                            const int active = l == 2 ||
+                                scnt[l - 1][src[l - 1].map[morton((uint32_t)a >> 1, (uint32_t)c >> 1)]] > leaf_src;
+                            const int direct = l == depth || scnt[l][ls] <= leaf_src;
+                            if (!active || !direct) continue;
+                        }
+                        for (int64_t q = sfirst[l][ls]; q < sfirst[l][ls] + scnt[l][ls]; ++q) {
                             int64_t i = sperm[q];
                             if (sr[i] == fr[j] && sz[i] == fz[j]) {
                                 ++skipped;
@@ -451,6 +491,7 @@ int64_t or_fmm(const double *sr, const double *sz, const double *S, int64_t ns,
                             }
                         }
                     }
+                }
             }
             free(G);
         }
@@ -459,6 +500,8 @@ cleanup:
     for (int l = 0; l < 16; ++l) {
         level_free(&src[l]);
         level_free(&tgt[l]);
+        free(scnt[l]);
+        free(sfirst[l]);
     }
     free(lstart);
     free(skey);

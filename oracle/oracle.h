@@ -84,7 +84,7 @@ int or_s2l(const double *M, int nmodes, int p, int pl, double rs, double zs, dou
 int64_t or_fmm(const double *sr, const double *sz, const double *S, int64_t ns,
                const double *fr, const double *fz, int64_t nf, int nmodes, int p, int pl,
                int depth, double L, double z0, int truncation, int miller, double *Phi,
-               double *dPr, double *dPz, int nthreads);
+               double *dPr, double *dPz, int nthreads, int64_t leaf_src);
 /* potential gradients: G and its field-point derivatives d/dr, d/dx by the
  * paper's first-order relations; direct sum with gradients; local-expansion
  * gradient */

@@ -300,3 +300,75 @@ def test_s2l_truncation_order_by_scaling(orc, p):
             rates = [math.log2(e[k] / e[k + 1]) for k in range(2)]
             assert all(abs(r - (p + 1)) < tol for r in rates), ((si, sj, ti, tj), p, trunc, e, rates)
         assert all(a > b for a, b in zip(errs[1], errs[0])), (errs[1], errs[0])
+
+
+# ---- adaptive source tree (reading R#26) ------------------------------------
+def _clustered(n, K, seed):
+    from tests.inputs import config_c4
+    pr = config_c4(n=n, K=K, p=8, depth=6, seed=seed, clusters=8)
+    return pr.sr, pr.sz, pr.S
+
+
+def test_adaptive_sigma0_is_uniform(orc):
+    """leaf_src = 0 is the uniform tree, operation for operation (bitwise)."""
+    sr, sz, S = _clustered(1600, 3, 31)
+    A, sa = orc.fmm(sr, sz, S, sr, sz, 6, 5, 1.0)
+    B, sb = orc.fmm(sr, sz, S, sr, sz, 6, 5, 1.0, leaf_src=0)
+    assert sa == sb and np.array_equal(A, B)
+
+
+@pytest.mark.parametrize("leaf_src", [8, 40])
+def test_adaptive_converges_to_direct(orc, leaf_src):
+    """Pinned against the plain direct sum: with the adaptive lists every (target,
+    source) pair must be covered exactly once -- a missing or doubled pair would leave an O(1)
+    error floor -- so the error falls geometrically with the order (~0.4 decade per order, P:680,
+    714-718) to the uniform tree's level; clustered C4-like input, depth 6."""
+    sr, sz, S = _clustered(2400, 3, 32)
+    D, _ = orc.direct(sr, sz, S, sr, sz)
+    eps, uni = {}, {}
+    for p in [4, 8, 12, 16]:
+        F, sk = orc.fmm(sr, sz, S, sr, sz, p, 6, 1.0, leaf_src=leaf_src)
+        assert sk >= 2400
+        eps[p] = orc.eps_per_mode(F, D)
+        U, _ = orc.fmm(sr, sz, S, sr, sz, p, 6, 1.0)
+        uni[p] = orc.eps_per_mode(U, D)
+    slope = np.log10(eps[4].max() / eps[16].max()) / 12
+    assert 0.25 < slope < 0.8, slope
+    for p in [4, 8, 12]:
+        assert np.all(eps[p] > eps[p + 4])
+    # same accuracy class as the uniform tree (the direct sums it adds are exact)
+    assert np.all(eps[16] < 1e-8), eps[16]
+    assert eps[16].max() < 10 * uni[16].max()
+
+
+def test_adaptive_all_leaves_at_level2(orc):
+    """leaf_src >= N: every level-2 source box is a leaf, so every target sums its level-2
+    neighbourhood directly and takes S2L only from the non-adjacent level-2 boxes:
+    the FMM equals that split, assembled here from the direct sum and single-box operators."""
+    rng = np.random.default_rng(33)
+    sr, sz, S = uniform_rings(rng, 300, 2)
+    fr, fz, _ = uniform_rings(rng, 9, 1)
+    p, d, L = 8, 4, 1.0
+    F, _ = orc.fmm(sr, sz, S, fr, fz, p, d, L, leaf_src=10 ** 6)
+    six = np.minimum(np.floor(sr * 4 / L), 3).astype(int)
+    siz = np.minimum(np.floor(sz * 4 / L), 3).astype(int)
+    h = L / 4
+    out = np.zeros_like(F)
+    for t in range(len(fr)):
+        tx, tz = min(int(fr[t] * 4 / L), 3), min(int(fz[t] * 4 / L), 3)
+        rt, zt = (tx + 0.5) * h, (tz + 0.5) * h
+        for a in range(4):
+            for c in range(4):
+                sel = (six == a) & (siz == c)
+                if not np.any(sel):
+                    continue
+                if abs(a - tx) <= 1 and abs(c - tz) <= 1:
+                    Dn, _ = orc.direct(sr[sel], sz[sel], S[sel], fr[t:t + 1], fz[t:t + 1])
+                    out[t] += Dn[0]
+                else:
+                    rs, zs = (a + 0.5) * h, (c + 0.5) * h
+                    M = orc.p2m(sr[sel], sz[sel], S[sel], p, rs, zs)
+                    Lc = orc.s2l(M, p, rs, zs, rt, zt)
+                    # the level-2 local reaches the leaf by exact L2L re-centrings (P:428-438)
+                    out[t] += orc.l2p(Lc, p, rt, zt, fr[t], fz[t])
+    assert np.max(np.abs(out - F)) <= 1e-12 * np.max(np.abs(F))
