@@ -103,8 +103,22 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def make_problem(name):
+# adaptive source tree per config (DESIGN R#26): (depth, leaf sources).  C4's
+# clusters leave most of a uniform depth-8 tree's leaves either crowded or nearly empty; C5 (sources
+# on curves, fields on a full grid) keeps the uniform depth-10 tree (pruning only adds S2L pairs).
+ADAPTIVE = {"C4": (11, 224)}
+
+
+def make_problem(name, args=None):
+    """The config's synthetic inputs, with its tree: depth and adaptive leaf size (pr.leaf_src,
+    0 = uniform) from ADAPTIVE unless --adaptive / --depth override them."""
     pr = CONFIGS[name]()
+    a = getattr(args, "adaptive", None)
+    pr.leaf_src = ADAPTIVE.get(name, (0, 0))[1] if a is None else a
+    if getattr(args, "depth", 0):
+        pr.depth = args.depth
+    elif pr.leaf_src > 0 and name in ADAPTIVE:
+        pr.depth = ADAPTIVE[name][0]
     return pr
 
 
@@ -125,7 +139,7 @@ def oracle_sample(pr, budget_s, cores):
         idx = np.sort(order[:m])
         t0 = time.perf_counter()
         _, sk = oracle.fmm(pr.sr, pr.sz, pr.S, pr.fr[idx], pr.fz[idx], pr.p, pr.depth, pr.L,
-                           pr.z0, nthreads=cores)
+                           pr.z0, nthreads=cores, leaf_src=pr.leaf_src)
         return time.perf_counter() - t0, sk, idx
 
     m0, m1 = min(nf, 16), min(nf, 64)
@@ -145,17 +159,19 @@ def run_reference(args):
     if rank != 0:
         return
     import oracle
-    pr = make_problem(args.config)
+    pr = make_problem(args.config, args)
     cores = os.cpu_count() or 1
     m, _, _, idx, fixed = oracle_sample(pr, 4.0, cores)   # each step a bounded sample (~4 s)
     fr, fz = pr.fr[idx], pr.fz[idx]
     for _ in range(args.warmup):
-        oracle.fmm(pr.sr, pr.sz, pr.S, fr, fz, pr.p, pr.depth, pr.L, pr.z0, nthreads=cores)
+        oracle.fmm(pr.sr, pr.sz, pr.S, fr, fz, pr.p, pr.depth, pr.L, pr.z0, nthreads=cores,
+                   leaf_src=pr.leaf_src)
     ts = []
     sk = 0
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        _, sk = oracle.fmm(pr.sr, pr.sz, pr.S, fr, fz, pr.p, pr.depth, pr.L, pr.z0, nthreads=cores)
+        _, sk = oracle.fmm(pr.sr, pr.sz, pr.S, fr, fz, pr.p, pr.depth, pr.L, pr.z0, nthreads=cores,
+                           leaf_src=pr.leaf_src)
         ts.append(time.perf_counter() - t0)
     t = sum(ts) / len(ts)
     inter = (len(pr.sr) * m - sk) * pr.K
@@ -168,7 +184,8 @@ def run_reference(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": f"{args.config}: {pr.name}", "n_src": len(pr.sr),
-                       "n_fld": m, "modes": pr.K, "order": pr.p, "depth": pr.depth},
+                       "n_fld": m, "modes": pr.K, "order": pr.p, "depth": pr.depth,
+                       "adaptive_leaf": pr.leaf_src},
             "cpu_baseline": {"value": v, "unit": "interactions/s", "cores": cores,
                              "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": "interactions/s", "h2d_bytes_per_step": 0,
@@ -217,6 +234,10 @@ def main():
     ap.add_argument("--config", default="C5")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg (profiling runs)")
+    ap.add_argument("--adaptive", type=int, default=None, metavar="SIGMA",
+                    help="adaptive source tree (leaf <= SIGMA sources, SURVEY 8(f)-4); "
+                         "0 = uniform; default: the config's (C4: 224 at depth 11)")
+    ap.add_argument("--depth", type=int, default=0, help="override the config's depth")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "cylfmm" else args.warmup
     if args.impl == "reference":
@@ -241,9 +262,10 @@ def main():
     from paper_2301_01179_b200 import distributed as dd
     if not b.up_to_date():
         b.build()
-    pr = make_problem(args.config)
+    pr = make_problem(args.config, args)
     dev = torch.device("cuda", local)
-    cfg = g.FMMConfig(n_modes=pr.K, order=pr.p, depth=pr.depth, L=pr.L, z0=pr.z0)
+    cfg = g.FMMConfig(n_modes=pr.K, order=pr.p, depth=pr.depth, L=pr.L, z0=pr.z0,
+                      adaptive_leaf=pr.leaf_src)
     # fields: all of them on one GPU; on N GPUs the cost-weighted contiguous Morton range of this
     # rank (cylfmm_partition_fields, identical on every rank: planning, outside the timed region)
     if world > 1:
@@ -430,6 +452,8 @@ def main():
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": f"{args.config}: {pr.name}", "n_src": len(pr.sr),
                            "n_fld": len(pr.fr), "modes": pr.K, "order": pr.p, "depth": pr.depth,
+                           "tree": (f"adaptive source tree, leaf <= {pr.leaf_src} sources"
+                                    if pr.leaf_src > 0 else "uniform"),
                            "truncation": "double", "miller": "accurate", "l2": "flushed",
                            "parallelism": (f"field-partition x{world} (cost-weighted Morton ranges; "
                                            "library NCCL: source broadcast-all-gather, P2M split + "

@@ -73,6 +73,12 @@ typedef struct {
                                (all modes if the workspace fits a third of free memory) */
     int order_local;        /* local-expansion order pl (the source and local orders
                                may differ); 0 = the source order `order`.  1 <= pl <= 16 */
+    int adaptive_leaf;      /* adaptive source tree (DESIGN R#26): a source box
+                               holding <= adaptive_leaf sources is a leaf; an adjacent box pair
+                               stops there with a direct sum (P:647-651 at that level) and the
+                               S2L pairs below it are dropped.  0 = the uniform tree of
+                               Algorithm 1.  >= 0; > 0 needs n_modes <= 33 and is not available
+                               to cylfmm_fmm_solve_grad (CYLFMM_EINVAL) */
 } cylfmm_params;
 
 /* Per-phase device times, milliseconds: CUDA events recorded on the stream each phase runs on

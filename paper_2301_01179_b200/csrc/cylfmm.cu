@@ -640,7 +640,7 @@ extern "C" cylfmm_status cylfmm_plan_create(cylfmm_plan *plan, const cylfmm_para
         q.order_local < 0 || q.order_local > CYLFMM_MAX_ORDER ||
         q.depth < 2 || q.depth > CYLFMM_MAX_DEPTH || (q.truncation != 0 && q.truncation != 1) ||
         (q.miller != 0 && q.miller != 1) || !(q.domain_L > 0.0) || !(q.domain_z0 == q.domain_z0) ||
-        q.mode_chunk < 0) {
+        q.mode_chunk < 0 || q.adaptive_leaf < 0 || (q.adaptive_leaf > 0 && q.n_modes > kP2PWWindow)) {
         set_err("cylfmm_plan_create: bad parameters (K=%d p=%d d=%d trunc=%d miller=%d L=%g)",
                 q.n_modes, q.order, q.depth, q.truncation, q.miller, q.domain_L);
         return CYLFMM_EINVAL;
@@ -928,7 +928,8 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     const bool grad = out_dr != nullptr && out_dz != nullptr;
     // multi-device solve: the leaf moments are split across the ranks (P2M of a contiguous
     // range of source leaves each) and replicated by NCCL broadcasts (one per rank, grouped)
-    const bool split = dist && p->comm && p->nranks > 1;
+    // (the adaptive source tree computes its leaf moments on every rank)
+    const bool split = dist && p->comm && p->nranks > 1 && p->prm.adaptive_leaf == 0;
     const cylfmm_params &q = p->prm;
     const int d = q.depth, K = q.n_modes, pp = q.order, P = (pp + 1) * (pp + 2) / 2;
     // local order (0 = the source order) and the tensor order max(p, pl)
@@ -960,7 +961,8 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     // auxiliary streams, joined by events; large ones (C4, C5) keep every kernel on `st`, where
     // each already fills the GPU (measured: C5 162.6 ms overlapped vs 163.0 ms serialised) and
     // the per-phase events stay clean.
-    const bool overlap = tm == nullptr && p->aux_ok && ns + nf <= ((int64_t)1 << 20);
+    // (the adaptive tree's near field runs one accumulating launch per level: serial)
+    const bool overlap = tm == nullptr && p->aux_ok && ns + nf <= ((int64_t)1 << 20) && q.adaptive_leaf == 0;
     cudaStream_t st_t = overlap ? p->aux[0] : st, st_n = overlap ? p->aux[1] : st;
     const int64_t nstat = (int64_t)12 << d;
     const int NM = std::max(K - 1, 1) + 1, D = 2 * pt + 1;
@@ -995,10 +997,14 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     // buffer pointers: set after the buffers are sized (geometry pass) or taken as they are (reuse)
     const int *flstart = nullptr;
     int *tmap_b = nullptr, *tkeys_b = nullptr;
+    // fields == sources: one sort and one set of leaf ranges; the level maps are shared too
+    // unless the source tree is adaptive (its maps omit the boxes below source leaves)
+    const int sigma = q.adaptive_leaf;
+    const bool share = same && sigma == 0;
     auto set_ptrs = [&]() {
         flstart = same ? p->slstart.as<int>() : p->flstart.as<int>();
-        tmap_b = same ? p->smap.as<int>() : p->tmap.as<int>();
-        tkeys_b = same ? p->skeys.as<int>() : p->tkeys.as<int>();
+        tmap_b = share ? p->smap.as<int>() : p->tmap.as<int>();
+        tkeys_b = share ? p->skeys.as<int>() : p->tkeys.as<int>();
     };
     if (reuse) set_ptrs();
     const int nkeys = 2 * 12 * (1 << d), JT = s2l_jt(pl);
@@ -1051,7 +1057,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     RET_IF(p->tkeys.need(sizeof(int) * ltot));
     RET_IF(p->counts.need(sizeof(int) * (3 * kMaxLevels + 8)));
     set_ptrs();
-    const int nside = same ? 1 : 2;
+    const int nside = share ? 1 : 2;
     int lsmall = 1;   // levels 2..lsmall in one launch (4^l <= kSmallLevelBoxes)
     while (lsmall + 1 <= d && pow4(lsmall + 1) <= kSmallLevelBoxes) ++lsmall;
     if (lsmall >= 2) {
@@ -1061,6 +1067,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             sa.map[side] = side == 0 ? p->smap.as<int>() : p->tmap.as<int>();
             sa.keys[side] = side == 0 ? p->skeys.as<int>() : p->tkeys.as<int>();
             sa.count[side] = p->counts.as<int>() + side * kMaxLevels;
+            sa.sigma[side] = side == 0 ? sigma : 0;
         }
         for (int l = 0; l <= d + 1 && l < 17; ++l) sa.lvoff[l] = lvoff[l];
         sa.depth = d;
@@ -1076,11 +1083,12 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         int *keys = side == 0 ? p->skeys.as<int>() : p->tkeys.as<int>();
         for (int l = lsmall + 1; l <= d; ++l) {
             int *fl = p->flags.as<int>() + lvoff[l];
-            level_flags_kernel<<<nblk(pow4(l), 256), 256, 0, st>>>(ls, d, l, fl);
+            const int sg = side == 0 ? sigma : 0;
+            level_flags_kernel<<<nblk(pow4(l), 256), 256, 0, st>>>(ls, d, l, sg, fl);
             CKL();
             RET_IF(scan_excl(p, fl, pow4(l), st));
             level_map_kernel<<<nblk(pow4(l), 256), 256, 0, st>>>(
-                ls, d, l, fl, map + lvoff[l], keys + lvoff[l], p->counts.as<int>() + side * kMaxLevels + l);
+                ls, d, l, sg, fl, map + lvoff[l], keys + lvoff[l], p->counts.as<int>() + side * kMaxLevels + l);
             CKL();
             p->launches += 2;
         }
@@ -1102,11 +1110,15 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
                                                           // [5] stations with a pair,
                                                           // [6 + l] first local row of level l
     CK(cudaMemsetAsync(cnt_ex, 0, 6 * sizeof(int), st));
-    if (ns > 0) {   // the largest source column at the leaf level bounds the stations S2L reads
-        max_col_kernel<<<nblk(std::min<int64_t>(ns, pow4(d)), 256), 256, 0, st>>>(
-            p->skeys.as<int>() + lvoff[d], p->counts.as<int>() + d, cnt_ex + 1);
-        CKL();
-        p->launches++;
+    if (ns > 0) {   // the largest source column bounds the stations S2L reads: uniform tree,
+                    // at the leaf level; adaptive source tree, over the levels (its leaves sit
+                    // at every level)
+        for (int l = sigma > 0 ? 2 : d; l <= d; ++l) {
+            max_col_kernel<<<nblk(std::min<int64_t>(ns, pow4(l)), 256), 256, 0, st>>>(
+                p->skeys.as<int>() + lvoff[l], p->counts.as<int>() + l, cnt_ex + 1);
+            CKL();
+            p->launches++;
+        }
     }
     la.depth = d;
     for (int l = 2; l <= d; ++l) {
@@ -1208,7 +1220,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     if (wsave) CK(cudaMemcpyAsync(&nslots, p->pbase.as<int64_t>() + pow4(d), sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     RET_IF(check_err_flag(p, st));
-        if (same)
+        if (share)
             for (int l = 0; l < kMaxLevels; ++l) hcnt[kMaxLevels + l] = hcnt[l];
     } else {
         T.end(PH_SORT, st);
@@ -1327,6 +1339,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     fa.Lc = p->Lc.as<double2>();
     fa.tens = p->tens.as<double>();
     fa.slstart = p->slstart.as<int>();
+    fa.sigma = sigma;
     fa.flstart = flstart;
     fa.sr = p->sr_s.as<double>();
     fa.sz = p->sz_s.as<double>();
@@ -1406,21 +1419,76 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             double avg = (double)nf / std::max(ntl, 1);
             const int TT = avg <= 10.0 ? 8 : (avg <= 24.0 ? 16 : 32);
             const bool wk = p2pw_enabled(K, grad);
+            const int sigma = q.adaptive_leaf;
             RET_IF(p->tcnt.need(sizeof(int) * (ntl + 1)));
             RET_IF(p->ntasks.need(kTaskCtrInts * sizeof(int)));
-            // warp tasks: <= nf/32 full pieces + <= 5 power-of-two pieces per leaf
+            // warp tasks: <= nf/32 full pieces + <= 5 power-of-two pieces per leaf (per box of a
+            // level under the adaptive tree)
             int64_t maxtasks = wk ? nf / 32 + 6 * (int64_t)ntl + 1 : nf / TT + ntl + 1;
+            if (sigma > 0)
+                for (int l = 2; l < d; ++l) maxtasks = std::max<int64_t>(maxtasks, nf / 32 + 6 * (int64_t)fa.tcount[l] + 1);
             RET_IF(p->tasks.need(sizeof(int4) * maxtasks));
+            if (sigma > 0) {
+                // adaptive source tree (R#26): one accumulating launch per level, over the target
+                // boxes with a neighbour pair that stops there (each launch owns its rows)
+                unsigned long long *ctr = p->ctr.as<unsigned long long>();
+                for (int l = 2; l <= d; ++l) {
+                    const int nbx = fa.tcount[l];
+                    if (nbx == 0) continue;
+                    CK(cudaMemsetAsync(p->ntasks.as<int>(), 0, kTaskCtrInts * sizeof(int), st_n));
+                    near_wtasks_count_kernel<<<nblk(nbx, 256), 256, 0, st_n>>>(fa.tkeys[l], nbx, fa.flstart,
+                                                                            fa.slstart, d, 1, l, sigma,
+                                                                            p->ntasks.as<int>());
+                    CKL();
+                    near_wtasks_emit_kernel<<<nblk(nbx, 256), 256, 0, st_n>>>(fa.tkeys[l], nbx, fa.flstart,
+                                                                           fa.slstart, d, 1, l, sigma,
+                                                                           p->tasks.as<int4>(),
+                                                                           p->ntasks.as<int>());
+                    CKL();
+                    P2PArgs a = {};
+                    a.sr = fa.sr;
+                    a.sz = fa.sz;
+                    a.S = fa.S;
+                    a.fr = fa.fr;
+                    a.fz = fa.fz;
+                    a.ns = ns;
+                    a.nf = nf;
+                    a.K = K;
+                    a.m0 = 0;
+                    a.m1 = K;
+                    a.miller = q.miller;
+                    a.fwd2 = forward_coef(K - 1, q.miller);
+                    a.exclude = q.exclude_coincident;
+                    a.out = fa.out;
+                    a.out_row = fperm;
+                    a.accumulate = 1;
+                    a.tasks = p->tasks.as<int4>();
+                    a.ntasks = p->ntasks.as<int>();
+                    a.task_ctr = p->ntasks.as<int>() + 1;
+                    a.leafstart = fa.slstart;
+                    a.depth = d;
+                    a.level = l;
+                    a.adaptive_leaf = sigma;
+                    a.n_skipped = ctr + 0;
+                    a.n_pairs = ctr + 1;
+                    a.n_branch = ctr + 3;
+                    a.err_flag = p->err.as<int>();
+                    CK(launch_p2pw(a, st_n));
+                    p->launches += 3;
+                }
+                T.end(PH_P2P, st_n);
+                return CYLFMM_OK;
+            }
             if (wk && reuse) {   // the task list is the previous solve's: rewind the fetch counter
                 CK(cudaMemsetAsync(p->ntasks.as<int>() + 1, 0, sizeof(int), st_n));
             } else if (wk) {
                 CK(cudaMemsetAsync(p->ntasks.as<int>(), 0, kTaskCtrInts * sizeof(int), st_n));
                 near_wtasks_count_kernel<<<nblk(ntl, 256), 256, 0, st_n>>>(fa.tkeys[d], ntl, fa.flstart,
-                                                                        fa.slstart, d, accumulate,
+                                                                        fa.slstart, d, accumulate, 0, 0,
                                                                         p->ntasks.as<int>());
                 CKL();
                 near_wtasks_emit_kernel<<<nblk(ntl, 256), 256, 0, st_n>>>(fa.tkeys[d], ntl, fa.flstart,
-                                                                       fa.slstart, d, accumulate,
+                                                                       fa.slstart, d, accumulate, 0, 0,
                                                                        p->tasks.as<int4>(),
                                                                        p->ntasks.as<int>());
             } else {
@@ -1511,6 +1579,22 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             if (overlap) CK(cudaEventRecord(p->aev[2], st_t));
         }
         if (ns > 0) {
+        if (sigma > 0) {
+            // adaptive source tree: P2M at every source leaf, whatever its level (the kernel
+            // skips the boxes above the leaves: M2M forms them), then M2M over the boxes above
+            T.beg(PH_P2M, st);
+            const int nmb = (kw + kP2MModes - 1) / kP2MModes;
+            fa.p2m_slot0 = 0;
+            for (int l = 2; l <= d; ++l) {
+                if (fa.scount[l] == 0) continue;
+                fa.p2m_level = l;
+                p2m_kernel<<<(unsigned)((int64_t)fa.scount[l] * nmb), kP2MThreads, p2m_smem(P, pp), st>>>(fa);
+                CKL();
+                p->launches++;
+            }
+            fa.p2m_level = 0;
+            T.end(PH_P2M, st);
+        } else {
             T.beg(PH_P2M, st);
             const int nl = fa.scount[d];
             auto leaf0 = [&](int r) { return (int)((int64_t)nl * r / (split ? p->nranks : 1)); };
@@ -1535,6 +1619,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
                 NC(g_nccl.GroupEnd());
                 T.end(PH_ALLGATHER, st);
             }
+        }
             T.beg(PH_M2M, st);
             for (int l = d - 1; l >= 2; --l) {
                 if (fa.scount[l] == 0) continue;
@@ -1692,6 +1777,10 @@ extern "C" cylfmm_status cylfmm_fmm_solve_grad(cylfmm_plan plan, const double *s
     }
     if (plan->prm.n_modes > kP2PWindow) {
         set_err("cylfmm_fmm_solve_grad: gradients support n_modes <= %d", kP2PWindow);
+        return CYLFMM_EINVAL;
+    }
+    if (plan->prm.adaptive_leaf > 0) {
+        set_err("cylfmm_fmm_solve_grad: gradients use the uniform tree (adaptive_leaf = 0)");
         return CYLFMM_EINVAL;
     }
     CK(cudaSetDevice(plan->device));

@@ -53,6 +53,8 @@ struct FarArgs {
     int64_t tfield;                     // field points (L2P)
     int l2p_tp;                         // L2P task size (points)
     int p2m_slot0;                      // P2M: first leaf slot (multi-device split)
+    int p2m_level;                      // P2M: level of the boxes (0: the leaf level d)
+    int sigma;                          // adaptive source tree leaf size (R#26), 0 = uniform
     // recentring tables (host-built once per plan, recentre_tables_host): [cm | cl] 4 (p+1)^2
     // doubles and [tri_i | tri_j] 2 P ints, for the source order (M2M) and the local order (L2L)
     const double *rtab_m, *rtab_l;
@@ -110,11 +112,14 @@ __global__ void __launch_bounds__(kP2MThreads) p2m_kernel(FarArgs a)
         mi[c] = i;
         mj[c] = c - (i * (p + 1) - i * (i - 1) / 2);
     }
-    const uint32_t key = (uint32_t)a.skeys[d][slot];
+    // level lv (adaptive source tree: every level, leaves only; uniform: the leaf level d)
+    const int lv = a.p2m_level ? a.p2m_level : d, sh = 2 * (d - lv);
+    const uint32_t key = (uint32_t)a.skeys[lv][slot];
+    const int q0 = a.slstart[(int64_t)key << sh], q1 = a.slstart[(int64_t)(key + 1) << sh];
+    if (lv < d && q1 - q0 > a.sigma) return;   // above the source leaves: M2M forms it (uniform CTA)
     double rc, zc, h;
-    box_centre(key, d, a.L, a.z0, rc, zc, h);
+    box_centre(key, lv, a.L, a.z0, rc, zc, h);
     const double inv_h = 1.0 / h;
-    const int q0 = a.slstart[key], q1 = a.slstart[key + 1];
     const int tn = threadIdx.x % (kP2MModes / kP2MTM), tc = threadIdx.x / (kP2MModes / kP2MTM);
     const int c0 = tc * kP2MRC;
     const bool active = c0 < P && kP2MTM * tn < nm;
@@ -173,7 +178,7 @@ __global__ void __launch_bounds__(kP2MThreads) p2m_kernel(FarArgs a)
         }
     }
     if (active) {
-        double2 *Mo = a.M + (a.soff[d] + slot) * (int64_t)KW * P;
+        double2 *Mo = a.M + (a.soff[lv] + slot) * (int64_t)KW * P;
 #pragma unroll
         for (int v = 0; v < kP2MTM; ++v) {
             const int n = n0 + kP2MTM * tn + v;
@@ -268,6 +273,10 @@ __global__ void __launch_bounds__(256) m2m_kernel(FarArgs a, int level)
     int *tri_i = reinterpret_cast<int *>(T + 4 * kMMG * P);
     int *tri_j = tri_i + P;
     const uint32_t key = (uint32_t)a.skeys[level][slot];
+    if (a.sigma > 0) {   // an adaptive source leaf: P2M formed its moments (CTA-uniform)
+        const int sh = 2 * (a.depth - level);
+        if (a.slstart[(int64_t)(key + 1) << sh] - a.slstart[(int64_t)key << sh] <= a.sigma) return;
+    }
     int cs[4];
 #pragma unroll
     for (int c = 0; c < 4; ++c) cs[c] = a.smap[level + 1][4 * key + c];

@@ -40,6 +40,8 @@ struct P2PArgs {
     int *task_ctr;              // near, warp-task kernel: dynamic task counter (zeroed)
     const int *leafstart;       // near: dense source leaf starts [4^d + 1]
     int depth;
+    int level;                  // near: level of the task boxes (0: the leaf level d)
+    int adaptive_leaf;          // near: adaptive source tree sigma (R#26), 0 = uniform
     unsigned long long *n_skipped;
     unsigned long long *n_pairs;
     unsigned long long *n_branch;   // nullable: [0] forward, [1] far, [2] Miller pairs, [3] sum S - N
@@ -77,6 +79,32 @@ __device__ __forceinline__ uint32_t compact1(uint32_t v)
     v = (v | (v >> 4)) & 0x00ff00ffu;
     v = (v | (v >> 8)) & 0x0000ffffu;
     return v;
+}
+
+// Sources of neighbour k (0..8, (dx, dz) = (k / 3 - 1, k % 3 - 1)) of the level-lv box `key` that
+// the near field sums directly: (first sorted source, count).  Every box at every
+// level owns the contiguous sorted range [slstart[b 4^(d-lv)], slstart[(b+1) 4^(d-lv)]).
+// Uniform tree (sigma = 0): the whole neighbour (lv = d).  Adaptive source tree (sigma > 0, R#26):
+// the pair (box, neighbour S) is evaluated directly at level lv iff it was descended into (lv = 2
+// or S's parent holds > sigma sources) and stops here (S holds <= sigma sources, or lv = d).
+__device__ __forceinline__ int2 near_segment(const int *slstart, int depth, int lv, int sigma,
+                                             uint32_t key, int k)
+{
+    const int x = (int)compact1(key) + k / 3 - 1, z = (int)compact1(key >> 1) + k % 3 - 1;
+    const int nb = 1 << lv;
+    if (x < 0 || z < 0 || x >= nb || z >= nb) return make_int2(0, 0);
+    const int sh = 2 * (depth - lv);
+    const uint32_t m = morton2((uint32_t)x, (uint32_t)z);
+    const int s0 = slstart[(int64_t)m << sh], len = slstart[(int64_t)(m + 1) << sh] - s0;
+    if (sigma > 0 && len > 0) {
+        if (lv < depth && len > sigma) return make_int2(s0, 0);   // S is descended into
+        if (lv > 2) {
+            const int64_t pm = m >> 2;
+            if (slstart[(pm + 1) << (sh + 2)] - slstart[pm << (sh + 2)] <= sigma)
+                return make_int2(s0, 0);                            // the parent pair stopped
+        }
+    }
+    return make_int2(s0, len);
 }
 
 // GRAD (near field, one mode window from mode 0): also the field gradients, from the paper's

@@ -131,15 +131,11 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
         if (lane == 8) segS0[18] = (int)(s1 - s0);
     } else if (warp == 0) {
         int s0 = 0, len = 0;
-        const uint32_t key = (uint32_t)tk.z;
-        const int ix = (int)compact1(key), iz = (int)compact1(key >> 1), nb = 1 << a.depth;
         if (lane < 9) {
-            const int x = ix + lane / 3 - 1, z = iz + lane % 3 - 1;
-            if (x >= 0 && z >= 0 && x < nb && z < nb) {
-                const uint32_t m = morton2((uint32_t)x, (uint32_t)z);
-                s0 = a.leafstart[m];
-                len = a.leafstart[m + 1] - s0;
-            }
+            const int2 sg = near_segment(a.leafstart, a.depth, a.level ? a.level : a.depth,
+                                         a.adaptive_leaf, (uint32_t)tk.z, lane);
+            s0 = sg.x;
+            len = sg.y;
         }
         int incl = len;
 #pragma unroll
@@ -622,17 +618,12 @@ __device__ __forceinline__ int piece_size(int nt)
     return (4 * nt >= 3 * p) ? nt : p / 2;
 }
 constexpr int kTaskCtrInts = 66;
-__device__ __forceinline__ int near_sources(int key, const int *slstart, int depth)
+__device__ __forceinline__ int near_sources(int key, const int *slstart, int depth, int level = 0,
+                                            int sigma = 0)
 {
-    const int ix = (int)compact1((uint32_t)key), iz = (int)compact1((uint32_t)key >> 1), nb = 1 << depth;
     int tot = 0;
-    for (int da = -1; da <= 1; ++da)
-        for (int dc = -1; dc <= 1; ++dc) {
-            const int x = ix + da, z = iz + dc;
-            if (x < 0 || z < 0 || x >= nb || z >= nb) continue;
-            const uint32_t m = morton2((uint32_t)x, (uint32_t)z);
-            tot += slstart[m + 1] - slstart[m];
-        }
+    for (int k = 0; k < 9; ++k)
+        tot += near_segment(slstart, depth, level ? level : depth, sigma, (uint32_t)key, k).y;
     return tot;
 }
 // window-state slots: pairs per target leaf (targets x sources of the 9 neighbours), by leaf slot
@@ -658,23 +649,27 @@ __device__ __forceinline__ int task_bucket(int nt, int nsrc)
 }
 // skip_empty: leaves without a source in their 9 neighbours get no task (the near field only
 // adds onto rows the far field wrote: an empty task would add zeros)
+// level, sigma: tasks for the target boxes of one level under the adaptive source tree (R#26;
+// level 0 = the leaf level, sigma 0 = uniform)
 __global__ void near_wtasks_count_kernel(const int *tkeys, int nleaf, const int *flstart,
-                                         const int *slstart, int depth, int skip_empty, int *ctr)
+                                         const int *slstart, int depth, int skip_empty, int level,
+                                         int sigma, int *ctr)
 {
     int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= nleaf) return;
     const int key = tkeys[s];
-    const int nsrc = near_sources(key, slstart, depth);
+    const int nsrc = near_sources(key, slstart, depth, level, sigma);
     if (skip_empty && nsrc == 0) return;
-    for (int nt = flstart[key + 1] - flstart[key]; nt > 0;) {
+    const int sh = 2 * (depth - (level ? level : depth));
+    for (int nt = flstart[(int64_t)(key + 1) << sh] - flstart[(int64_t)key << sh]; nt > 0;) {
         const int take = piece_size(nt);
         atomicAdd(&ctr[2 + task_bucket(take, nsrc)], 1);
         nt -= take;
     }
 }
 __global__ void near_wtasks_emit_kernel(const int *tkeys, int nleaf, const int *flstart,
-                                        const int *slstart, int depth, int skip_empty, int4 *tasks,
-                                        int *ctr)
+                                        const int *slstart, int depth, int skip_empty, int level,
+                                        int sigma, int4 *tasks, int *ctr)
 {
     __shared__ int off[32];
     if (threadIdx.x < 32) {
@@ -687,9 +682,10 @@ __global__ void near_wtasks_emit_kernel(const int *tkeys, int nleaf, const int *
     int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= nleaf) return;
     const int key = tkeys[s];
-    const int nsrc = near_sources(key, slstart, depth);
+    const int nsrc = near_sources(key, slstart, depth, level, sigma);
     if (skip_empty && nsrc == 0) return;
-    int t = flstart[key], nt = flstart[key + 1] - t;
+    const int sh = 2 * (depth - (level ? level : depth));
+    int t = flstart[(int64_t)key << sh], nt = flstart[(int64_t)(key + 1) << sh] - t;
     while (nt > 0) {
         const int take = piece_size(nt);
         const int b = task_bucket(take, nsrc);

@@ -58,7 +58,7 @@ __device__ __forceinline__ void for_each_s2l(const S2LListArgs &a, int l, uint32
             const int js = jt + dj;
             if (js < 0 || js >= nb) continue;
             const int s = smap[morton2((uint32_t)is, (uint32_t)js)];
-            if (s < 0) continue;
+            if (s < 0) continue;   // empty, or below an adaptive source leaf (R#26)
             const int iin = min(it, is), dI = di < 0 ? -di : di, dJ = dj < 0 ? -dj : dj;
             f(s, ((iin * 12 + class_of(dI, dJ)) << 1) | (di > 0 ? 1 : 0), dj > 0 ? 1 : 0);
         }

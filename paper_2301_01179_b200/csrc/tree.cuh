@@ -181,24 +181,37 @@ __global__ void leaf_start_kernel(const uint32_t *skey, int64_t n, int64_t nleaf
 }
 
 // flags[b] = box b of level l non-empty (b in [0, 4^l))
-__global__ void level_flags_kernel(const int *lstart, int depth, int level, int *flags)
+// A box of the tree at `level`: non-empty and, for the adaptive source tree (sigma > 0, R#26),
+// below no leaf (level 2, or the parent holds > sigma points).  Boxes below a source leaf take
+// part in nothing (no moments, no S2L), so they get no slot.
+__device__ __forceinline__ bool box_in_tree(const int *lstart, int depth, int level, int64_t b,
+                                            int sigma)
+{
+    const int sh = 2 * (depth - level);
+    if (lstart[(b + 1) << sh] <= lstart[b << sh]) return false;
+    if (sigma > 0 && level > 2) {
+        const int64_t pb = b >> 2;
+        return lstart[(pb + 1) << (sh + 2)] - lstart[pb << (sh + 2)] > sigma;
+    }
+    return true;
+}
+
+__global__ void level_flags_kernel(const int *lstart, int depth, int level, int sigma, int *flags)
 {
     int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int64_t nbox = (int64_t)1 << (2 * level);
     if (b >= nbox) return;
-    int sh = 2 * (depth - level);
-    flags[b] = lstart[(b + 1) << sh] > lstart[b << sh] ? 1 : 0;
+    flags[b] = box_in_tree(lstart, depth, level, b, sigma) ? 1 : 0;
 }
 
 // map[b] = slot or -1; keys[slot] = b; count written by the last box.
-__global__ void level_map_kernel(const int *lstart, int depth, int level, const int *scan,
+__global__ void level_map_kernel(const int *lstart, int depth, int level, int sigma, const int *scan,
                                  int *map, int *keys, int *count)
 {
     int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int64_t nbox = (int64_t)1 << (2 * level);
     if (b >= nbox) return;
-    int sh = 2 * (depth - level);
-    bool ne = lstart[(b + 1) << sh] > lstart[b << sh];
+    bool ne = box_in_tree(lstart, depth, level, b, sigma);
     int s = scan[b];
     map[b] = ne ? s : -1;
     if (ne) keys[s] = (int)b;
@@ -240,12 +253,13 @@ struct SmallLevelArgs {
     int *count[2];             // per side: count[l]
     int64_t lvoff[17];
     int depth, lmin, nlev;     // levels lmin .. lmin + nlev - 1
+    int sigma[2];              // per side: adaptive leaf size (box_in_tree), 0 = uniform
 };
 __global__ void __launch_bounds__(1024) level_maps_small_kernel(SmallLevelArgs a)
 {
     __shared__ int wsum[32];
     const int side = blockIdx.x / a.nlev, level = a.lmin + blockIdx.x % a.nlev;
-    const int nbox = 1 << (2 * level), sh = 2 * (a.depth - level);
+    const int nbox = 1 << (2 * level);
     const int *ls = a.ls[side];
     int *map = a.map[side] + a.lvoff[level], *keys = a.keys[side] + a.lvoff[level];
     constexpr int PER = kSmallLevelBoxes / 1024;
@@ -254,7 +268,7 @@ __global__ void __launch_bounds__(1024) level_maps_small_kernel(SmallLevelArgs a
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
         const int b = b0 + k;
-        f[k] = b < nbox && ls[(int64_t)(b + 1) << sh] > ls[(int64_t)b << sh];
+        f[k] = b < nbox && box_in_tree(ls, a.depth, level, b, a.sigma[side]);
         c += f[k];
     }
     // block exclusive scan of c

@@ -34,7 +34,7 @@ class Params(ctypes.Structure):
                 ("truncation", ctypes.c_int), ("miller", ctypes.c_int),
                 ("exclude_coincident", ctypes.c_int), ("domain_z0", ctypes.c_double),
                 ("domain_L", ctypes.c_double), ("mode_chunk", ctypes.c_int),
-                ("order_local", ctypes.c_int)]
+                ("order_local", ctypes.c_int), ("adaptive_leaf", ctypes.c_int)]
 
 
 class Timings(ctypes.Structure):
@@ -210,6 +210,7 @@ class FMMConfig:
     exclude_coincident: bool = True
     mode_chunk: int = 0
     order_local: int = 0      # local-expansion order (0: = order)
+    adaptive_leaf: int = 0    # adaptive source tree: leaf if <= this many sources (0: uniform)
 
 
 def comm_unique_id() -> bytes:
@@ -229,7 +230,7 @@ class Plan:
         self.cfg = cfg
         prm = Params(cfg.n_modes, cfg.order, cfg.depth, cfg.truncation, cfg.miller,
                      int(bool(cfg.exclude_coincident)), float(cfg.z0), float(cfg.L),
-                     cfg.mode_chunk, cfg.order_local)
+                     cfg.mode_chunk, cfg.order_local, cfg.adaptive_leaf)
         h = ctypes.c_void_p()
         if dist is None:
             _check(lib().cylfmm_plan_create(ctypes.byref(h), ctypes.byref(prm)), "cylfmm_plan_create")
@@ -346,7 +347,7 @@ def partition_fields(src_r, src_z, fld_r, fld_z, cfg: "FMMConfig", n_parts: int)
     cost = np.empty(n_parts, dtype=np.float64)
     prm = Params(cfg.n_modes, cfg.order, cfg.depth, cfg.truncation, cfg.miller,
                  int(bool(cfg.exclude_coincident)), float(cfg.z0), float(cfg.L), cfg.mode_chunk,
-                 cfg.order_local)
+                 cfg.order_local, cfg.adaptive_leaf)
     p = lambda x: ctypes.c_void_p(x.ctypes.data) if x.size else ctypes.c_void_p(0)  # noqa: E731
     _check(lib().cylfmm_partition_fields(p(a[0]), p(a[1]), a[0].shape[0], p(a[2]), p(a[3]),
                                          a[2].shape[0], ctypes.byref(prm), int(n_parts), p(part),

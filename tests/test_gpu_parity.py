@@ -223,13 +223,17 @@ def test_tree_sort_bit_exact(gpu, orc, n, depth, L, z0):
     assert np.array_equal(perm.cpu().numpy(), p_ref)
 
 
+C4_ADAPTIVE = (11, 224)   # (depth, leaf sources) of the adaptive C4 run (bench.py ADAPTIVE)
+
+
 def _fmm_case(gpu, orc, sr, sz, S, fr, fz, p, depth, L, z0=0.0, truncation=0, miller=0,
-              mode_chunk=0, pl=0):
+              mode_chunk=0, pl=0, leaf_src=0):
     K = S.shape[1]
-    ref, sk = orc.fmm(sr, sz, S, fr, fz, p, depth, L, z0, truncation, miller, pl=pl or None)
+    ref, sk = orc.fmm(sr, sz, S, fr, fz, p, depth, L, z0, truncation, miller, pl=pl or None,
+                      leaf_src=leaf_src)
     plan = gpu.Plan(gpu.FMMConfig(n_modes=K, order=p, depth=depth, L=L, z0=z0,
                                   truncation=truncation, miller=miller, mode_chunk=mode_chunk,
-                                  order_local=pl))
+                                  order_local=pl, adaptive_leaf=leaf_src))
     out, tm = plan.solve(sr, sz, S, fr, fz, timings=True)
     assert tm["n_skipped"] == sk
     return out.cpu().numpy(), ref, plan
@@ -549,3 +553,80 @@ def test_geometry_cache_and_cuda_graph(gpu, name):
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy(), ref2)
     plan.close()
+
+
+# ---- adaptive source tree (DESIGN R#26) ------------------------------------
+@pytest.mark.parametrize("n,K,p,depth,sigma,sep", [
+    (30000, 9, 8, 7, 16, False), (30000, 17, 12, 7, 64, False), (20000, 33, 6, 6, 32, True),
+    (12000, 3, 16, 8, 8, False), (20000, 5, 8, 8, 400, True)])
+def test_fmm_adaptive_vs_oracle(gpu, orc, n, K, p, depth, sigma, sep):
+    """Adaptive source tree (per-level accumulating near-field launches, S2L lists pruned below
+    source leaves) against the oracle's adaptive Algorithm 1 on clustered C4-like input, fields =
+    sources (coincident pairs) or a separate ragged field set."""
+    from tests.inputs import config_c4
+    pr = config_c4(n=n, K=K, p=p, depth=depth, seed=40 + K, clusters=8)
+    if sep:
+        rng = np.random.default_rng(41)
+        fr, fz, _ = uniform_rings(rng, 3001, 1)
+    else:
+        fr, fz = pr.sr, pr.sz
+    out, ref, _ = _fmm_case(gpu, orc, pr.sr, pr.sz, pr.S, fr, fz, p, depth, 1.0, leaf_src=sigma)
+    assert eps_modes(out, ref).max() <= TOL
+
+
+def test_fmm_adaptive_full_size_c4(gpu, orc):
+    """C4 at full size on the adaptive tree the bench runs (depth 11, leaf 128 sources): GPU at a
+    seeded sample plus targeted points (_targeted_fields) against the oracle's adaptive FMM at
+    those points, and against the GPU direct sum within 10x eps(16) (R#25)."""
+    import torch
+    from paper_2301_01179_b200.inputs import CONFIGS
+    pr = CONFIGS["C4"]()
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.as_tensor(a, device=dev)  # noqa: E731
+    d, sigma = C4_ADAPTIVE
+    plan = gpu.Plan(gpu.FMMConfig(n_modes=pr.K, order=pr.p, depth=d, L=pr.L, z0=pr.z0,
+                                  adaptive_leaf=sigma))
+    out = plan.solve(t(pr.sr), t(pr.sz), t(pr.S), t(pr.fr), t(pr.fz))
+    rng = np.random.default_rng(8)
+    idx = rng.choice(len(pr.fr), size=48, replace=False)
+    idx = np.unique(np.concatenate([idx, _targeted_fields("C4", pr, rng)]))
+    F = out[t(idx)].cpu().numpy()
+    del out
+    plan.close()
+    ref, _ = orc.fmm(pr.sr, pr.sz, pr.S, pr.fr[idx], pr.fz[idx], pr.p, d, pr.L, pr.z0,
+                     leaf_src=sigma)
+    assert eps_modes(F, ref).max() <= TOL
+    D = gpu.direct(t(pr.sr), t(pr.sz), t(pr.S), t(pr.fr[idx]), t(pr.fz[idx])).cpu().numpy()
+    assert eps_modes(F, D).max() <= 10 * 0.1 * 10.0 ** (-0.4 * pr.p)
+
+
+def test_partitioned_solve_adaptive(gpu):
+    """The adaptive tree's choices depend on the sources only, so every field point of a
+    field-partitioned solve takes the same interactions as in the one-GPU solve (C4, the bench's
+    adaptive configuration).  Not bit for bit: the direct sums of a coarse level run in pieces of
+    the box's targets, and a partition cut through a coarse box changes the pieces' lane layout,
+    hence the summation order -- agreement to rounding (eps <= 1e-14 per mode)."""
+    import torch
+    from paper_2301_01179_b200.inputs import CONFIGS
+    pr = CONFIGS["C4"]()
+    d, sigma = C4_ADAPTIVE
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=dev)  # noqa: E731
+    cfg = gpu.FMMConfig(n_modes=pr.K, order=pr.p, depth=d, L=pr.L, z0=pr.z0, adaptive_leaf=sigma)
+    plan = gpu.Plan(cfg)
+    full = plan.solve(t(pr.sr), t(pr.sz), t(pr.S), t(pr.fr), t(pr.fz)).cpu().numpy()
+    part, _ = gpu.partition_fields(pr.sr, pr.sz, pr.fr, pr.fz, cfg, 2)
+    for q in range(2):
+        idx = np.nonzero(part == q)[0]
+        out = plan.solve(t(pr.sr), t(pr.sz), t(pr.S), t(pr.fr[idx]), t(pr.fz[idx])).cpu().numpy()
+        assert eps_modes(out, full[idx]).max() <= 1e-14, q
+    plan.close()
+
+
+def test_adaptive_limits(gpu):
+    """adaptive_leaf > 0 needs n_modes <= 33 (one near-field mode window) and the potential
+    solve (cylfmm_fmm_solve_grad keeps the uniform tree): CYLFMM_EINVAL otherwise."""
+    with pytest.raises(Exception):
+        gpu.Plan(gpu.FMMConfig(n_modes=34, order=4, depth=4, adaptive_leaf=8))
+    with pytest.raises(Exception):
+        gpu.Plan(gpu.FMMConfig(n_modes=3, order=4, depth=4, adaptive_leaf=-1))
