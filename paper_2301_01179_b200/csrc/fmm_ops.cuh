@@ -152,10 +152,13 @@ __global__ void __launch_bounds__(kP2MThreads) p2m_kernel(FarArgs a)
                 mono[qq * P + c] = pw[(qq * 2) * (p + 1) + ci] * pw[(qq * 2 + 1) * (p + 1) + cj];
         }
         // coefficient rows by asynchronous copies (in flight while the monomials are formed)
+        // (mode n = kP2MTM tn + v of source q at Sx[q][v][tn]: a warp's four tn of one v are 64
+        // contiguous bytes, one conflict-free wavefront)
         for (int e = threadIdx.x; e < nc * kP2MModes; e += kP2MThreads) {
             const int q = e / kP2MModes, n = e % kP2MModes;
             const bool v = n < nm;
-            p2m_async16(Sx + e, v ? a.S + (int64_t)(s0 + q) * a.K + a.m0 + n0 + n : a.S, v);
+            p2m_async16(Sx + q * kP2MModes + (n % kP2MTM) * (kP2MModes / kP2MTM) + n / kP2MTM,
+                        v ? a.S + (int64_t)(s0 + q) * a.K + a.m0 + n0 + n : a.S, v);
         }
         asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
         __syncthreads();
@@ -163,7 +166,7 @@ __global__ void __launch_bounds__(kP2MThreads) p2m_kernel(FarArgs a)
             for (int q = 0; q < nc; ++q) {
                 double2 sv[kP2MTM];
 #pragma unroll
-                for (int v = 0; v < kP2MTM; ++v) sv[v] = Sx[q * kP2MModes + kP2MTM * tn + v];
+                for (int v = 0; v < kP2MTM; ++v) sv[v] = Sx[q * kP2MModes + v * (kP2MModes / kP2MTM) + tn];
                 const double *mq = mono + q * P + c0;
 #pragma unroll
                 for (int u = 0; u < kP2MRC; ++u) {
