@@ -180,6 +180,23 @@ cylfmm_status cylfmm_fmm_solve_host(cylfmm_plan plan, const double *src_r, const
                                     const double *fld_z, int64_t n_fld, double *out_Phi,
                                     cylfmm_stream_t stream, cylfmm_timings *timings);
 
+/* Pipelined variant of cylfmm_fmm_solve_host for a stream of solves: returns as soon as the
+ * work is queued.  The inputs are uploaded into one of two plan-owned device staging slots
+ * (alternating between calls) on a plan copy stream, the solve runs on `stream` behind them, and
+ * out_Phi is downloaded on a second plan copy stream; so the next call's upload and the previous
+ * call's download overlap the current solve (PCIe is full duplex).  Host buffers (HOST pointers,
+ * same layouts as cylfmm_fmm_solve) should be pinned (cudaHostAlloc / cudaHostRegister) for the
+ * copies to be asynchronous; the caller keeps them valid and the inputs unmodified, and reads
+ * out_Phi, only after cylfmm_plan_sync() (which waits for every queued call).  Argument errors
+ * (EINVAL / EDOMAIN) return before any work is queued; device-side errors (ENUMERIC, domain
+ * flags) are reported by cylfmm_plan_sync().  The geometry cache does not apply (the staging
+ * slots alternate).  Errors: as cylfmm_fmm_solve_host, ENOMEM for the staging slots. */
+cylfmm_status cylfmm_fmm_solve_host_async(cylfmm_plan plan, const double *src_r,
+                                          const double *src_z, const double *src_S,
+                                          int64_t n_src, const double *fld_r,
+                                          const double *fld_z, int64_t n_fld, double *out_Phi,
+                                          cylfmm_stream_t stream);
+
 /* ---------------------------------------------------------------------------------------
  * Test entry points (batched, DEVICE pointers, asynchronous on `stream`).
  * --------------------------------------------------------------------------------------- */

@@ -497,6 +497,19 @@ struct Phases {
     void end(int ph, cudaStream_t s);
 };
 
+// mailbox layout (ints): [0, 3 kMaxLevels + 8) level counts, [kMboxErr] error flag,
+// [kMboxSlots, +2) the near-field window-slot count (int64)
+constexpr int kMboxErr = 3 * kMaxLevels + 8, kMboxSlots = kMboxErr + 2, kMboxInts = kMboxSlots + 2;
+__global__ void mailbox_kernel(const int *counts, int nc, const int *err, const int64_t *slots,
+                               volatile int *out)
+{
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) out[i] = counts[i];
+    if (threadIdx.x == 0) {
+        out[kMboxErr] = *err;
+        if (slots) *reinterpret_cast<volatile int64_t *>(out + kMboxSlots) = *slots;
+    }
+}
+
 struct cylfmm_plan_s {
     cylfmm_params prm;
     int device = 0;
@@ -509,7 +522,7 @@ struct cylfmm_plan_s {
     DevBuf tasks, ntasks, tcnt, toff;
     DevBuf written;                       // per-box 'local written by S2L' flags
     DevBuf pcnt, poff, khist, kstart, kcur, bstart, pairs, batches, wlist, pairbuf;   // S2L lists
-    DevBuf need, lrow, rowkey, lvoffd;    // lazy L2L flags, compact local rows, row -> box
+    DevBuf need, lrow, rowkey;            // lazy L2L flags, compact local rows, row -> box
     DevBuf pbase, pcnt64, sv2, sv1;       // near-field window state (K in (33, 66])
     DevBuf stflag, stlist;                // stations with an S2L pair
     DevBuf l2pown, l2pflag, l2ppos, l2ptask, l2pntask;   // L2P evaluating boxes and tasks
@@ -531,6 +544,17 @@ struct cylfmm_plan_s {
     // build (hev: previous work on the caller's stream done, coefficients resident)
     cudaStream_t hcp = nullptr;
     cudaEvent_t hev[2] = {};
+    // pipelined host-buffer solves (cylfmm_fmm_solve_host_async): two device staging slots used
+    // alternately; uploads on hcp, downloads on hdn; per slot: coordinates / coefficients
+    // resident, solve done (inputs free, result ready), download done (result buffer free)
+    struct HostSlot {
+        DevBuf sr, sz, S, fr, fz, out;
+        cudaEvent_t coords = nullptr, coef = nullptr, done = nullptr, down = nullptr;
+    } hs[2];
+    int hslot = 0;
+    cudaStream_t hdn = nullptr;
+    // mapped pinned mailbox: the mid-solve counts the host needs, written by mailbox_kernel
+    int *mbox = nullptr, *mbox_dev = nullptr;
     // phase events (Phases): pool reused across solves, marks of the solves since the last read
     std::vector<cudaEvent_t> evpool;
     size_t evused = 0;
@@ -621,7 +645,7 @@ static void free_plan_bufs(cylfmm_plan p)
                      &p->scan_tmp_n[3], &p->sr_s, &p->sz_s, &p->S_s, &p->fr_s, &p->fz_s,
                      &p->slstart, &p->flstart, &p->flags, &p->smap, &p->skeys, &p->tmap,
                      &p->tkeys, &p->counts, &p->M, &p->Lc, &p->tens, &p->seeds, &p->tasks,
-                     &p->ntasks, &p->tcnt, &p->toff, &p->written, &p->pcnt, &p->poff, &p->khist, &p->kstart, &p->kcur, &p->bstart, &p->pairs, &p->batches, &p->wlist, &p->pairbuf, &p->need, &p->lrow, &p->rowkey, &p->lvoffd, &p->pbase, &p->pcnt64, &p->sv2, &p->sv1, &p->stflag, &p->stlist, &p->l2pown, &p->l2pflag, &p->l2ppos, &p->l2ptask, &p->l2pntask, &p->err, &p->ctr, &p->rtab, &p->h_sr, &p->h_sz,
+                     &p->ntasks, &p->tcnt, &p->toff, &p->written, &p->pcnt, &p->poff, &p->khist, &p->kstart, &p->kcur, &p->bstart, &p->pairs, &p->batches, &p->wlist, &p->pairbuf, &p->need, &p->lrow, &p->rowkey, &p->pbase, &p->pcnt64, &p->sv2, &p->sv1, &p->stflag, &p->stlist, &p->l2pown, &p->l2pflag, &p->l2ppos, &p->l2ptask, &p->l2pntask, &p->err, &p->ctr, &p->rtab, &p->h_sr, &p->h_sz,
                      &p->h_S, &p->h_fr, &p->h_fz, &p->h_out, &p->g_r, &p->g_z, &p->g_S, &p->g_cnt};
     for (DevBuf *b : all) b->release();
 }
@@ -667,6 +691,12 @@ static cylfmm_status plan_init(cylfmm_plan p, const cylfmm_params &q)
     for (int i = 0; i < 5; ++i) CK(cudaEventCreateWithFlags(&p->aev[i], cudaEventDisableTiming));
     CK(cudaStreamCreateWithFlags(&p->hcp, cudaStreamNonBlocking));
     for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&p->hev[i], cudaEventDisableTiming));
+    CK(cudaStreamCreateWithFlags(&p->hdn, cudaStreamNonBlocking));
+    CK(cudaHostAlloc(reinterpret_cast<void **>(&p->mbox), sizeof(int) * kMboxInts, cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void **>(&p->mbox_dev), p->mbox, 0));
+    for (auto &h : p->hs)
+        for (cudaEvent_t *e : {&h.coords, &h.coef, &h.done, &h.down})
+            CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     p->aux_ok = true;
     {
         const int pl = q.order_local > 0 ? q.order_local : q.order;
@@ -715,14 +745,18 @@ extern "C" void cylfmm_plan_destroy(cylfmm_plan plan)
     if (plan->comm && g_nccl.ok) g_nccl.CommDestroy(plan->comm);
     for (cudaEvent_t e : plan->hev)
         if (e) cudaEventDestroy(e);
+    if (plan->hdn) cudaStreamDestroy(plan->hdn);
+    if (plan->mbox) cudaFreeHost(plan->mbox);
+    for (auto &h : plan->hs) {
+        for (cudaEvent_t e : {h.coords, h.coef, h.done, h.down})
+            if (e) cudaEventDestroy(e);
+        for (DevBuf *b : {&h.sr, &h.sz, &h.S, &h.fr, &h.fz, &h.out}) b->release();
+    }
     delete plan;
 }
 
-static cylfmm_status check_err_flag(cylfmm_plan p, cudaStream_t st)
+static cylfmm_status err_status(int h)
 {
-    int h = 0;
-    CK(cudaMemcpyAsync(&h, p->err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
     if (h & 4) {
         set_err("cylfmm: point outside the domain [0,L]x[z0,z0+L] or r <= 0 / non-finite");
         return CYLFMM_EDOMAIN;
@@ -732,6 +766,15 @@ static cylfmm_status check_err_flag(cylfmm_plan p, cudaStream_t st)
         return CYLFMM_ENUMERIC;
     }
     return CYLFMM_OK;
+}
+// the plan's error flag after the work queued on `st` (through the mapped mailbox: no copy
+// engine, see mailbox_kernel)
+static cylfmm_status check_err_flag(cylfmm_plan p, cudaStream_t st)
+{
+    mailbox_kernel<<<1, 32, 0, st>>>(nullptr, 0, p->err.as<int>(), nullptr, p->mbox_dev);
+    CKL();
+    CK(cudaStreamSynchronize(st));
+    return err_status(p->mbox[kMboxErr]);
 }
 
 extern "C" cylfmm_status cylfmm_plan_set_profiling(cylfmm_plan plan, int on)
@@ -1191,13 +1234,14 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         CKL();
         // row -> dense position, first row of each level (L2L walks materialised boxes only)
         RET_IF(p->rowkey.need(sizeof(int64_t) * std::max<int64_t>(ltot, 1)));
-        RET_IF(p->lvoffd.need(sizeof(int64_t) * (kMaxLevels + 2)));
-        CK(cudaMemcpyAsync(p->lvoffd.p, lvoff, sizeof(int64_t) * (d + 2), cudaMemcpyHostToDevice, st));
+        LevelOffsets lo = {};   // by value: no host-to-device copy on the solve's stream (it
+                                // would queue behind a pipelined solve's upload)
+        for (int l = 0; l <= d + 1; ++l) lo.v[l] = lvoff[l];
         need_rows_kernel<<<nblk(ltot, 256), 256, 0, st>>>(p->lrow.as<int>(), p->need.as<unsigned char>(),
                                                          ltot, p->rowkey.as<int64_t>());
         CKL();
-        level_rows_kernel<<<1, 32, 0, st>>>(p->lrow.as<int>(), p->need.as<unsigned char>(),
-                                            p->lvoffd.as<int64_t>(), d, cnt_ex + 6);
+        level_rows_kernel<<<1, 32, 0, st>>>(p->lrow.as<int>(), p->need.as<unsigned char>(), lo, d,
+                                            cnt_ex + 6);
         CKL();
         p->launches += 3;
     }
@@ -1216,10 +1260,16 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         CKL();
         p->launches += 3;
     }
-    CK(cudaMemcpyAsync(hcnt, p->counts.p, sizeof(int) * (3 * kMaxLevels + 8), cudaMemcpyDeviceToHost, st));
-    if (wsave) CK(cudaMemcpyAsync(&nslots, p->pbase.as<int64_t>() + pow4(d), sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    // the level counts, the error flag and the window-slot count reach the host through mapped
+    // pinned memory written by a kernel (a device-to-host copy on this stream would queue behind
+    // a pipelined solve's multi-GB download on the copy engine)
+    mailbox_kernel<<<1, 64, 0, st>>>(p->counts.as<int>(), 3 * kMaxLevels + 8, p->err.as<int>(),
+                                     wsave ? p->pbase.as<int64_t>() + pow4(d) : nullptr, p->mbox_dev);
+    CKL();
     CK(cudaStreamSynchronize(st));
-    RET_IF(check_err_flag(p, st));
+    memcpy(hcnt, p->mbox, sizeof(int) * (3 * kMaxLevels + 8));
+    if (wsave) memcpy(&nslots, p->mbox + kMboxSlots, sizeof(int64_t));
+    RET_IF(err_status(p->mbox[kMboxErr]));
         if (share)
             for (int l = 0; l < kMaxLevels; ++l) hcnt[kMaxLevels + l] = hcnt[l];
     } else {
@@ -1832,6 +1882,61 @@ extern "C" cylfmm_status cylfmm_fmm_solve_host(cylfmm_plan plan, const double *s
         CK(cudaMemcpyAsync(out_Phi, plan->h_out.p, 16 * (size_t)n_fld * K, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     return check_err_flag(plan, st);
+}
+
+extern "C" cylfmm_status cylfmm_fmm_solve_host_async(cylfmm_plan plan, const double *src_r,
+                                                     const double *src_z, const double *src_S,
+                                                     int64_t n_src, const double *fld_r,
+                                                     const double *fld_z, int64_t n_fld,
+                                                     double *out_Phi, cylfmm_stream_t stream)
+{
+    RET_IF(validate_solve(plan, src_r, src_z, src_S, n_src, fld_r, fld_z, n_fld, out_Phi));
+    CK(cudaSetDevice(plan->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const int K = plan->prm.n_modes;
+    auto &h = plan->hs[plan->hslot];
+    plan->hslot ^= 1;
+    const bool same = fld_r == src_r && fld_z == src_z && n_fld == n_src;
+    size_t bs = 8 * (size_t)std::max<int64_t>(n_src, 1), bf = 8 * (size_t)std::max<int64_t>(n_fld, 1);
+    // the slot's previous solve has read its inputs and its download has left the result
+    // buffer before either is overwritten (events never recorded: no wait).  (Growing a slot
+    // reallocates: the host waits for that slot's previous work first.)
+    if (h.sr.cap < bs || h.S.cap < bs * 2 * K || h.fr.cap < bf || h.out.cap < bf * 2 * K) {
+        CK(cudaEventSynchronize(h.done));
+        CK(cudaEventSynchronize(h.down));
+    }
+    RET_IF(h.sr.need(bs));
+    RET_IF(h.sz.need(bs));
+    RET_IF(h.S.need(bs * 2 * K));
+    RET_IF(h.fr.need(bf));
+    RET_IF(h.fz.need(bf));
+    RET_IF(h.out.need(bf * 2 * K));
+    CK(cudaStreamWaitEvent(plan->hcp, h.done, 0));
+    if (n_src > 0) {
+        CK(cudaMemcpyAsync(h.sr.p, src_r, 8 * n_src, cudaMemcpyHostToDevice, plan->hcp));
+        CK(cudaMemcpyAsync(h.sz.p, src_z, 8 * n_src, cudaMemcpyHostToDevice, plan->hcp));
+    }
+    if (n_fld > 0 && !same) {
+        CK(cudaMemcpyAsync(h.fr.p, fld_r, 8 * n_fld, cudaMemcpyHostToDevice, plan->hcp));
+        CK(cudaMemcpyAsync(h.fz.p, fld_z, 8 * n_fld, cudaMemcpyHostToDevice, plan->hcp));
+    }
+    CK(cudaEventRecord(h.coords, plan->hcp));
+    // the coefficient rows last: first read by the gather after the Morton sort
+    if (n_src > 0) CK(cudaMemcpyAsync(h.S.p, src_S, 16 * (size_t)n_src * K, cudaMemcpyHostToDevice, plan->hcp));
+    CK(cudaEventRecord(h.coef, plan->hcp));
+    CK(cudaStreamWaitEvent(st, h.coords, 0));
+    CK(cudaStreamWaitEvent(st, h.down, 0));
+    const double *dfr = same ? h.sr.as<double>() : h.fr.as<double>();
+    const double *dfz = same ? h.sz.as<double>() : h.fz.as<double>();
+    RET_IF(fmm_solve_impl(plan, h.sr.as<double>(), h.sz.as<double>(), h.S.as<double>(), n_src,
+                          dfr, dfz, n_fld, h.out.as<double>(), st, nullptr, nullptr, nullptr,
+                          n_src > 0 ? h.coef : nullptr));
+    CK(cudaEventRecord(h.done, st));
+    CK(cudaStreamWaitEvent(plan->hdn, h.done, 0));
+    if (n_fld > 0)
+        CK(cudaMemcpyAsync(out_Phi, h.out.p, 16 * (size_t)n_fld * K, cudaMemcpyDeviceToHost, plan->hdn));
+    CK(cudaEventRecord(h.down, plan->hdn));
+    return CYLFMM_OK;
 }
 
 // ------------------------------------------------------------------------------------------

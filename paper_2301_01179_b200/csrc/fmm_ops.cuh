@@ -337,9 +337,13 @@ __global__ void need_rows_kernel(const int *lrow, const unsigned char *need, int
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g < n && need[g]) rowkey[lrow[g]] = g;
 }
-__global__ void level_rows_kernel(const int *lrow, const unsigned char *need, const int64_t *lvoff,
+struct LevelOffsets {
+    int64_t v[kMaxLevels + 2];
+};
+__global__ void level_rows_kernel(const int *lrow, const unsigned char *need, LevelOffsets lo,
                                   int depth, int *out)
 {
+    const int64_t *lvoff = lo.v;
     // out[l] = first row of level l (l = 2..depth), out[depth + 1] = total rows
     const int l = threadIdx.x + 2;
     if (l > depth + 1) return;

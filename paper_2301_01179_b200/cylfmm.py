@@ -100,6 +100,8 @@ def lib():
                                    ctypes.POINTER(Timings)]
     L.cylfmm_fmm_solve_host.restype = i
     L.cylfmm_fmm_solve_host.argtypes = L.cylfmm_fmm_solve.argtypes
+    L.cylfmm_fmm_solve_host_async.restype = i
+    L.cylfmm_fmm_solve_host_async.argtypes = [vp, vp, vp, vp, i64, vp, vp, i64, vp, vp]
     L.cylfmm_fmm_solve_grad.restype = i
     L.cylfmm_fmm_solve_grad.argtypes = [vp, vp, vp, vp, i64, vp, vp, i64, vp, vp, vp, vp,
                                         ctypes.POINTER(Timings)]
@@ -316,6 +318,22 @@ class Plan:
                                            ctypes.byref(tm) if tm is not None else None),
                "cylfmm_fmm_solve_host")
         return (out, tm.as_dict()) if timings else out
+
+    def solve_host_async(self, src_r, src_z, src_S, fld_r, fld_z, out):
+        """Pipelined host-buffer solve (cylfmm_fmm_solve_host_async): queues the upload, the solve
+        and the download and returns; `out` (and the inputs, which must stay unmodified) are
+        valid after sync().  Arrays must be C-contiguous float64 / complex128, ideally pinned."""
+        torch = _torch()
+        arrs = (src_r, src_z, src_S, fld_r, fld_z, out)
+        for a in arrs:
+            if not (isinstance(a, np.ndarray) and a.flags.c_contiguous):
+                raise ValueError("solve_host_async: C-contiguous numpy arrays required")
+        ns, nf = src_S.shape[0], fld_r.shape[0]
+        p = lambda a: ctypes.c_void_p(a.ctypes.data) if a.size else ctypes.c_void_p(0)  # noqa: E731
+        _check(lib().cylfmm_fmm_solve_host_async(self._h, p(src_r), p(src_z), p(src_S), ns,
+                                                 p(fld_r), p(fld_z), nf, p(out), _stream(torch)),
+               "cylfmm_fmm_solve_host_async")
+        return out
 
     def sync(self):
         _check(lib().cylfmm_plan_sync(self._h), "cylfmm_plan_sync")
