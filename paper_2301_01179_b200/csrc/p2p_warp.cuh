@@ -118,7 +118,9 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
     const int tl = lane & (TW - 1), sl = lane >> lgTW;
     const bool tvalid = tl < nt;
     const int KW = EXACT ? KT : a.m1 - a.m0;
-    const int M0 = WIN ? a.m0 : 0, M1 = M0 + KW;
+    // (the saved-state second window of a K in (33, 66] solve starts at mode KT = 33: a
+    // compile-time window start turns the recursion and Miller constants into immediates)
+    const int M0 = WIN ? (SV ? KT : a.m0) : 0, M1 = M0 + KW;
 
     // neighbour source segments (warp 0, lane k < 9 = neighbour k), prefix by shuffles; the
     // direct sum has one segment, the partition
