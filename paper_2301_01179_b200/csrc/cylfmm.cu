@@ -133,7 +133,8 @@ static cudaError_t allow_smem(F *kernel)
     X(17, true, false, false, true, false) X(33, true, false, false, true, false)                      \
     X(9, false, false, false, true, false) X(17, false, false, false, true, false)                     \
     X(33, false, false, false, true, false) X(33, false, false, true, true, false)                     \
-    X(33, true, false, false, false, true) X(33, false, false, true, false, true)
+    X(33, true, false, false, false, true) X(33, false, false, true, false, true)                      \
+    X(32, true, false, true, false, true)
 #define P2P_INSTANCES(X)                                                                       \
     X(8, 16, 2) X(8, 16, 5) X(16, 8, 3) X(16, 8, 9) X(32, 4, 6) X(32, 4, 18)
 
@@ -227,11 +228,15 @@ static bool p2pw_enabled(int K, bool grad) { return !grad && K <= kP2PWindow * 8
 static cudaError_t launch_p2pw(const P2PArgs &a, cudaStream_t st, bool direct = false)
 {
     const int KW = a.m1 - a.m0;
-    const int kt = p2pw_kt(a.m0 > 0 ? kP2PWWindow : a.K);
+    int kt = p2pw_kt(a.m0 > 0 ? kP2PWWindow : a.K);
     const bool wsm = false;
     const bool win = a.m0 > 0;   // windows after the first (the first runs the exact-33 kernel:
                                  // measured C5 near field 48.2 ms vs 60.0 ms with the windowed one)
-    const bool exact = !win && KW == kt;
+    bool exact = !win && KW == kt;
+    if (win && a.save == 2 && KW == 32) {   // K = 65 (C5): the second window exactly 32 modes
+        kt = 32;
+        exact = true;
+    }
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);

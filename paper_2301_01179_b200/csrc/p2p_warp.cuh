@@ -26,6 +26,7 @@
 namespace cyl {
 
 constexpr int kWarpCH = 32;   // sources per warp stage
+constexpr int kWinStart = 33; // first mode of the second window of a K in (33, 66] solve
 constexpr int kWarps = 4;     // warps per CTA (one task per CTA, the source list split in four)
 
 template <int KT>
@@ -120,7 +121,7 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
     const int KW = EXACT ? KT : a.m1 - a.m0;
     // (the saved-state second window of a K in (33, 66] solve starts at mode KT = 33: a
     // compile-time window start turns the recursion and Miller constants into immediates)
-    const int M0 = WIN ? (SV ? KT : a.m0) : 0, M1 = M0 + KW;
+    const int M0 = WIN ? (SV ? kWinStart : a.m0) : 0, M1 = M0 + KW;
 
     // neighbour source segments (warp 0, lane k < 9 = neighbour k), prefix by shuffles; the
     // direct sum has one segment, the partition
