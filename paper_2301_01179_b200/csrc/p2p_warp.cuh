@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
         // recursion is a chain of dependent FMAs: in the windowed pass (K > KT, where the chain
         // also advances to the window) two pairs per lane run in lockstep to hide its latency;
         // a missing second pair runs with zero seeds (the recursion is linear: exact zeros).
-        constexpr bool TWO = WIN;
+        constexpr bool TWO = WIN || SV;   // (SV: both windows of a K in (33, 66] solve)
         const bool load = SV && WIN && a.save == 2;   // (u_31, u_32) from the first window
         // load mode: the states of the next iteration's pairs are fetched one iteration ahead
         double2 pfA = make_double2(0.0, 0.0), pfB = make_double2(0.0, 0.0);
@@ -332,6 +332,10 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
             } else {
                 acc[0] = cfma(SA[0], u0A, acc[0]);
                 if (KW > 1) acc[1] = cfma(SA[1], u1A, acc[1]);
+                if constexpr (TWO) {
+                    acc[0] = cfma(SB[0], u0B, acc[0]);
+                    if (KW > 1) acc[1] = cfma(SB[1], u1B, acc[1]);
+                }
 #pragma unroll
                 for (int n = 2; n < KT; ++n) {
                     if (n < KW) {
@@ -339,9 +343,18 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
                         acc[n] = cfma(SA[n], u2A * c_rec.Rn[n], acc[n]);
                         u0A = u1A;
                         u1A = u2A;
+                        if constexpr (TWO) {
+                            const double u2B = fma(dB, u1B, fma(-c_rec.eps[n], u0B, u1B));
+                            acc[n] = cfma(SB[n], u2B * c_rec.Rn[n], acc[n]);
+                            u0B = u1B;
+                            u1B = u2B;
+                        }
                     }
                 }
-                if (SV && a.save == 1) a.sv2[tslot + stV[ca]] = make_double2(u0A, u1A);   // (u_31, u_32)
+                if (SV && a.save == 1) {   // (u_31, u_32) for the second window
+                    a.sv2[tslot + stV[ca]] = make_double2(u0A, u1A);
+                    if (TWO && ib >= 0) a.sv2[tslot + stV[cb]] = make_double2(u0B, u1B);
+                }
             }
         }
         // far pairs (chi >= 1000), one per lane and iteration: hypergeometric form (DLMF
