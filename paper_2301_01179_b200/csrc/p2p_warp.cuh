@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
         // recursion is a chain of dependent FMAs: in the windowed pass (K > KT, where the chain
         // also advances to the window) two pairs per lane run in lockstep to hide its latency;
         // a missing second pair runs with zero seeds (the recursion is linear: exact zeros).
-        constexpr bool TWO = WIN || SV;   // (SV: both windows of a K in (33, 66] solve)
+        constexpr bool TWO = WIN || SV || (!DIRECT && KT <= 17);   // (SV: both windows of a K in (33, 66] solve)
         const bool load = SV && WIN && a.save == 2;   // (u_31, u_32) from the first window
         // load mode: the states of the next iteration's pairs are fetched one iteration ahead
         double2 pfA = make_double2(0.0, 0.0), pfB = make_double2(0.0, 0.0);
