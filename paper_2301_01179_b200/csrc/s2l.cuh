@@ -221,12 +221,14 @@ __device__ __forceinline__ int packed_row(int a, int b, int pt)
            b * (2 * pt + 1 - a) - b * (b - 1) / 2;
 }
 
-// resident CTAs per SM the shape is built for (shared memory at p = 16: tensor 39 KB + JT rows)
-template <int C>
-__host__ __device__ constexpr int s2l_min_blocks() { return C <= 3 ? 3 : 1; }
+// resident CTAs per SM each shape is built for (<= 128 registers at 128 / 256 threads, 96 at
+// 192: p = 16's three CTAs, whose shared memory is the tensor 39 KB + 12 moment rows; measured:
+// the p <= 12 shape at 140 registers fit one CTA per SM, C3 S2L 29.0 vs 22.9 ms)
+template <int NT>
+__host__ __device__ constexpr int s2l_min_blocks() { return NT <= 128 ? 4 : (NT <= 192 ? 3 : 2); }
 
 template <int R, int C, int NU, int CG>
-__global__ void __launch_bounds__(NU * CG, s2l_min_blocks<C>()) s2l_batch_kernel(S2LArgs a)
+__global__ void __launch_bounds__(NU * CG, s2l_min_blocks<NU * CG>()) s2l_batch_kernel(S2LArgs a)
 {
     constexpr int NT = NU * CG, JT = CG * C;
     extern __shared__ double sm[];
