@@ -776,6 +776,12 @@ static cylfmm_status err_status(int h)
 // engine, see mailbox_kernel)
 static cylfmm_status check_err_flag(cylfmm_plan p, cudaStream_t st)
 {
+    if (!p->mbox) {   // a scratch plan without a mailbox (cylfmm_tree_sort)
+        int h = 0;
+        CK(cudaMemcpyAsync(&h, p->err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        return err_status(h);
+    }
     mailbox_kernel<<<1, 32, 0, st>>>(nullptr, 0, p->err.as<int>(), nullptr, p->mbox_dev);
     CKL();
     CK(cudaStreamSynchronize(st));
