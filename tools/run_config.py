@@ -3,7 +3,7 @@
 seeded sample of field points against the oracle FMM (parity, 1e-12) and the GPU direct sum
 (eps vs direct, the paper's metric P:697-703).  Diagnostic tool (GPU box); prints one JSON line.
 
-  python tools/run_config.py C4 [--sample 128] [--depth D] [--chunk KW] [--no-oracle]
+  python tools/run_config.py C4 [--sample 128] [--depth D] [--adaptive SIGMA] [--chunk KW] [--no-oracle]
 """
 import argparse
 import json
@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--sample", type=int, default=128)
     ap.add_argument("--depth", type=int, default=0)
     ap.add_argument("--chunk", type=int, default=0)
+    ap.add_argument("--adaptive", type=int, default=0, help="adaptive source tree leaf size (R#26)")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--no-oracle", action="store_true")
     a = ap.parse_args()
@@ -37,13 +38,13 @@ def main():
     pr = CONFIGS[a.config]()
     d = a.depth or pr.depth
     rec = {"config": a.config, "n_src": len(pr.sr), "n_fld": len(pr.fr), "K": pr.K, "p": pr.p,
-           "depth": d, "gen_s": round(time.time() - t0, 1)}
+           "depth": d, "adaptive_leaf": a.adaptive, "gen_s": round(time.time() - t0, 1)}
     dev = torch.device("cuda", 0)
     sr, sz = torch.as_tensor(pr.sr, device=dev), torch.as_tensor(pr.sz, device=dev)
     S = torch.as_tensor(pr.S, device=dev)
     fr, fz = torch.as_tensor(pr.fr, device=dev), torch.as_tensor(pr.fz, device=dev)
     plan = g.Plan(g.FMMConfig(n_modes=pr.K, order=pr.p, depth=d, L=pr.L, z0=pr.z0,
-                              mode_chunk=a.chunk))
+                              mode_chunk=a.chunk, adaptive_leaf=a.adaptive))
     out, tm = plan.solve(sr, sz, S, fr, fz, timings=True)
     torch.cuda.synchronize()
     ts = []
@@ -68,7 +69,8 @@ def main():
         import oracle
         oracle.build()
         t0 = time.time()
-        O, sk = oracle.fmm(pr.sr, pr.sz, pr.S, pr.fr[idx], pr.fz[idx], pr.p, d, pr.L, pr.z0)
+        O, sk = oracle.fmm(pr.sr, pr.sz, pr.S, pr.fr[idx], pr.fz[idx], pr.p, d, pr.L, pr.z0,
+                           leaf_src=a.adaptive)
         rec["oracle_s"] = round(time.time() - t0, 1)
         e = eps(F, O)
         rec["eps_vs_oracle_fmm_max"] = float(e.max())
