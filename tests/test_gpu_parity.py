@@ -654,3 +654,29 @@ def test_solve_host_async_pipelined(gpu):
             ref = plan.solve(sr, sz, Ss[k], f_r, f_z).cpu().numpy()
             assert np.array_equal(outs[k], ref), k
     plan.close()
+
+
+def test_adaptive_mode_chunks_and_geometry_cache(gpu, orc):
+    """The adaptive source tree under mode chunking (the far field in chunks of 2 modes: per-level
+    P2M and M2M per chunk) against the oracle, and a geometry-cached re-solve (no sort, no lists,
+    per-level near-field tasks re-emitted) bitwise equal to the uncached solve."""
+    import torch
+    from tests.inputs import config_c4
+    pr = config_c4(n=24000, K=5, p=10, depth=7, seed=91, clusters=8)
+    out, ref, _ = _fmm_case(gpu, orc, pr.sr, pr.sz, pr.S, pr.sr, pr.sz, 10, 7, 1.0, mode_chunk=2,
+                            leaf_src=48)
+    assert eps_modes(out, ref).max() <= TOL
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.as_tensor(a, device=dev)  # noqa: E731
+    sr, sz, S = t(pr.sr), t(pr.sz), t(pr.S)
+    plan = gpu.Plan(gpu.FMMConfig(n_modes=5, order=10, depth=7, adaptive_leaf=48))
+    a = plan.solve(sr, sz, S, sr, sz).cpu().numpy()
+    plan.set_geometry_cache(True)
+    plan.solve(sr, sz, S, sr, sz)
+    S2 = t(pr.S * 0.5)
+    b = plan.solve(sr, sz, S2, sr, sz).cpu().numpy()
+    plan.set_geometry_cache(False)
+    c = plan.solve(sr, sz, S2, sr, sz).cpu().numpy()
+    assert np.array_equal(b, c)
+    assert not np.array_equal(a, c)
+    plan.close()
