@@ -1,6 +1,6 @@
 #!/usr/bin/env python
 """Top CUDA source lines by warp-stall samples of an ncu report (--page source, cuda,sass).
-   python tools/ncu_lines.py report.ncu-rep [N]"""
+   python tools/ncu_lines.py report.ncu-rep [N] [launch index]"""
 import csv
 import io
 import subprocess
@@ -9,7 +9,8 @@ from collections import defaultdict
 
 rep = sys.argv[1]
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 25
-txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+sel = ["--launch-skip", sys.argv[3], "--launch-count", "1"] if len(sys.argv) > 3 else []
+txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"] + sel,
                      capture_output=True, text=True).stdout
 agg = defaultdict(lambda: [0, 0, ""])
 fname = ""
