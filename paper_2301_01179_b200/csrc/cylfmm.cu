@@ -142,7 +142,7 @@ static cudaError_t allow_smem(F *kernel)
 // groups) per local-order class; JT = CG C pairs per batch
 #define S2L_P8 4, 4, 16, 8
 #define S2L_P12 4, 4, 32, 8
-#define S2L_P16 4, 3, 48, 4
+#define S2L_P16 3, 4, 57, 3
 #define S2L_ALL(X) X(S2L_P8) X(S2L_P12) X(S2L_P16)
 
 static cylfmm_status ensure_init()
