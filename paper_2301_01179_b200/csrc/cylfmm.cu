@@ -140,8 +140,8 @@ static cudaError_t allow_smem(F *kernel)
 
 // S2L batch shapes (R rows per unit, C pairs per thread, NU units >= units(pl, R), CG column
 // groups) per local-order class; JT = CG C pairs per batch
-#define S2L_P8 4, 4, 16, 8
-#define S2L_P12 4, 4, 32, 8
+#define S2L_P8 3, 4, 18, 8
+#define S2L_P12 3, 4, 35, 8
 #define S2L_P16 3, 4, 57, 3
 #define S2L_ALL(X) X(S2L_P8) X(S2L_P12) X(S2L_P16)
 
