@@ -1,6 +1,6 @@
 #!/usr/bin/env python
-"""Per-phase solve timings (median over reps) for one config; used to compare kernel variants
-(CYLFMM_S2L_VARIANT etc.) on the GPU box.  Prints one JSON line."""
+"""Per-phase solve timings (median over reps) for one config at a chosen depth / mode chunk;
+used to compare builds on the GPU box.  Prints one JSON line."""
 import argparse
 import json
 import os
