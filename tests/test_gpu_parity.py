@@ -680,3 +680,30 @@ def test_adaptive_mode_chunks_and_geometry_cache(gpu, orc):
     assert np.array_equal(b, c)
     assert not np.array_equal(a, c)
     plan.close()
+
+
+def test_adaptive_and_async_edge_cases(gpu, orc):
+    """Edge cases of the round-2 entry points: the adaptive tree with no sources (zeros), a
+    single source, and a leaf size above the source count (every level-2 box a leaf); the
+    pipelined host solve with no field points and with no sources."""
+    import torch
+    plan = gpu.Plan(gpu.FMMConfig(n_modes=3, order=6, depth=5, adaptive_leaf=16))
+    fr, fz = np.array([0.25, 0.75, 0.5]), np.array([0.5, 0.1, 0.9])
+    out = plan.solve(np.zeros(0), np.zeros(0), np.zeros((0, 3), dtype=np.complex128), fr, fz)
+    assert np.all(out.cpu().numpy() == 0)
+    plan.close()
+    rng = np.random.default_rng(5)
+    sr, sz, S = uniform_rings(rng, 700, 3)
+    for n, sigma in [(1, 16), (700, 10 ** 6)]:
+        o, ref, _ = _fmm_case(gpu, orc, sr[:n], sz[:n], S[:n], fr, fz, 6, 5, 1.0, leaf_src=sigma)
+        assert eps_modes(o, ref).max() <= TOL, (n, sigma)
+    plan = gpu.Plan(gpu.FMMConfig(n_modes=3, order=6, depth=4))
+    pin = lambda a: torch.as_tensor(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+    hr, hz, hS = pin(sr), pin(sz), pin(S)
+    e = np.zeros(0)
+    plan.solve_host_async(hr, hz, hS, e, e, np.zeros((0, 3), dtype=np.complex128))
+    o = pin(np.ones((3, 3), dtype=np.complex128))
+    plan.solve_host_async(e, e, np.zeros((0, 3), dtype=np.complex128), pin(fr), pin(fz), o)
+    plan.sync()
+    assert np.all(o == 0)
+    plan.close()
