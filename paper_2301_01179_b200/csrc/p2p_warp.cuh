@@ -16,7 +16,9 @@
 //     the warp runs the same branch on as many lanes as the per-lane class counts allow);
 //   * G^(n) is produced in registers and contracted at once into the lane's register
 //     accumulators acc[n] (forward and far upward in n; Miller downward into w[n], normalised
-//     upward by G^(0) = K/(pi rho_+) from the AGM);
+//     upward by G^(0) = K/(pi rho_+) from the AGM), all in the forward recursion's units
+//     u_n = G^(n) / R_n: the forward pairs add S u_n with no per-pair scaling, the far and Miller
+//     factors carry 1 / R_n, and each (target, mode) sum is multiplied by R_n once at the end;
 //   * the SL partial sums of a target are combined by a fixed xor-shuffle tree, so results are
 //     bitwise reproducible.
 // Mode window: all K <= KT modes in one pass (KT compile-time: register arrays).
@@ -36,7 +38,8 @@ __host__ __device__ constexpr int p2pw_row() { return KT | 1; }   // odd double2
 template <int KT, bool WSM>
 inline size_t p2pw_smem_bytes()
 {
-    return (size_t)kWarps * (sizeof(double2) * kWarpCH * p2pw_row<KT>() + sizeof(double) * 2 * kWarpCH +
+    return 4 * sizeof(double) +                          // one mbarrier per warp
+           (size_t)kWarps * (sizeof(double2) * kWarpCH * p2pw_row<KT>() + sizeof(double) * 2 * kWarpCH +
                              2 * sizeof(int) * kWarpCH) +
            sizeof(int) * 20;
 }
@@ -52,14 +55,38 @@ __device__ __forceinline__ void pw_async8(void *smem, const void *gmem)
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
                  "l"(gmem));
 }
-__device__ __forceinline__ void pw_async16(void *smem, const void *gmem)
-{
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
-                 "l"(gmem));
-}
 __device__ __forceinline__ void pw_async_wait()
 {
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+// a stage's coefficient rows arrive by one TMA bulk copy per source row on the warp's mbarrier
+// (one instruction per row instead of a 16-byte cp.async per element with its address arithmetic)
+__device__ __forceinline__ void pw_mbar_init(uint64_t *bar)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void pw_mbar_expect(uint64_t *bar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void pw_bulk(void *dst, const void *src, unsigned bytes, uint64_t *bar)
+{
+    asm volatile("fence.proxy.async.shared::cta;\n"
+                 "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(dst)),
+                 "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void pw_mbar_wait(uint64_t *bar, unsigned phase)
+{
+    asm volatile("{\n.reg .pred p;\nPW_WAIT_%=:\n"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                 "@!p bra PW_WAIT_%=;\n}\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+                 "r"(phase)
+                 : "memory");
 }
 
 __device__ __forceinline__ double2 cfma(double2 s, double g, double2 acc)
@@ -83,18 +110,21 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
     constexpr int CH = kWarpCH, ROW = p2pw_row<KT>();
     extern __shared__ double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // layout: S rows [kWarps][CH][ROW] double2 | r, z [kWarps][2 CH] | source index [kWarps][CH] |
-    //         segments: starts [9], prefixes [9], total
-    double2 *stS0 = reinterpret_cast<double2 *>(smem);
+    // layout: mbarriers [4] | S rows [kWarps][CH][ROW] double2 | r, z [kWarps][2 CH] |
+    //         source index [kWarps][CH] | segments: starts [9], prefixes [9], total
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem) + warp;
+    double2 *stS0 = reinterpret_cast<double2 *>(smem + 4);
     double2 *stS = stS0 + (size_t)warp * CH * ROW;
     double *stR = reinterpret_cast<double *>(stS0 + (size_t)kWarps * CH * ROW) + warp * 2 * CH;
     double *stZ = stR + CH;
     double *wbase = reinterpret_cast<double *>(stS0 + (size_t)kWarps * CH * ROW) + kWarps * 2 * CH;
-    int *stG = reinterpret_cast<int *>(wbase) + warp * CH;
     int *segS0 = reinterpret_cast<int *>(wbase) + kWarps * CH;
     int *segPre = segS0 + 9;
     int *stV = segS0 + 20 + warp * CH;                   // source index in the task's list
 
+    if (lane == 0) pw_mbar_init(bar);
+    __syncwarp();
+    unsigned ph = 0;                                     // the warp's mbarrier phase
     unsigned my_skipped = 0, my_pairs = 0, my_fwd = 0, my_far = 0, my_mil = 0;
     unsigned long long my_msteps = 0;
     const int nparts = DIRECT ? (int)((a.ns + a.src_per_part - 1) / a.src_per_part) : 1;
@@ -179,6 +209,7 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
     for (int v0 = vb; v0 < ve; v0 += CH) {
         const int nch = min(CH, ve - v0);
         __syncwarp();
+        if (lane == 0) pw_mbar_expect(bar, (unsigned)(nch * KW) * (unsigned)sizeof(double2));
         if (lane < nch) {
             const int uu = v0 + lane;
             const int v = (kWarps * (uu / ICH) + warp) * ICH + uu % ICH;
@@ -186,28 +217,15 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
 #pragma unroll
             for (int kk = 1; kk < 9; ++kk) k += (v >= segPre[kk]);
             const int gi = segS0[k] + (v - segPre[k]);
-            stG[lane] = gi;
             if (SV) stV[lane] = v;
             pw_async8(stR + lane, a.sr + gi);
             pw_async8(stZ + lane, a.sz + gi);
-        }
-        __syncwarp();
-        // coefficient rows: element e = s KW + n, lanes stride 32 elements
-        {
-            int s = lane / KW, n = lane - s * KW;
-            const int ds = 32 / KW, dn = 32 - ds * KW;
-#pragma unroll 4
-            for (int e = lane; e < nch * KW; e += 32) {
-                pw_async16(stS + s * ROW + n, a.S + (int64_t)stG[s] * a.K + M0 + n);
-                s += ds;
-                n += dn;
-                if (n >= KW) {
-                    n -= KW;
-                    ++s;
-                }
-            }
+            // the source's coefficient row (modes M0 .. M0 + KW - 1): one bulk copy
+            pw_bulk(stS + lane * ROW, a.S + (int64_t)gi * a.K + M0, (unsigned)(KW * sizeof(double2)), bar);
         }
         pw_async_wait();
+        pw_mbar_wait(bar, ph);
+        ph ^= 1u;
         __syncwarp();
         // classify this lane's pairs c = sl + SL i
         unsigned mF = 0, mX = 0, mM = 0, mL = 0;     // forward, far, Miller short / long
@@ -316,14 +334,14 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
                             if constexpr (TWO) acc[j] = cfma(SB[j], gB, acc[j]);
                             continue;
                         }
-                        const double e = c_rec.eps[n], R = c_rec.Rn[n];
+                        const double e = c_rec.eps[n];
                         const double u2A = fma(dA, u1A, fma(-e, u0A, u1A));
-                        acc[j] = cfma(SA[j], u2A * R, acc[j]);
+                        acc[j] = cfma(SA[j], u2A, acc[j]);
                         u0A = u1A;
                         u1A = u2A;
                         if constexpr (TWO) {
                             const double u2B = fma(dB, u1B, fma(-e, u0B, u1B));
-                            acc[j] = cfma(SB[j], u2B * R, acc[j]);
+                            acc[j] = cfma(SB[j], u2B, acc[j]);
                             u0B = u1B;
                             u1B = u2B;
                         }
@@ -340,12 +358,12 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
                 for (int n = 2; n < KT; ++n) {
                     if (n < KW) {
                         const double u2A = fma(dA, u1A, fma(-c_rec.eps[n], u0A, u1A));
-                        acc[n] = cfma(SA[n], u2A * c_rec.Rn[n], acc[n]);
+                        acc[n] = cfma(SA[n], u2A, acc[n]);
                         u0A = u1A;
                         u1A = u2A;
                         if constexpr (TWO) {
                             const double u2B = fma(dB, u1B, fma(-c_rec.eps[n], u0B, u1B));
-                            acc[n] = cfma(SB[n], u2B * c_rec.Rn[n], acc[n]);
+                            acc[n] = cfma(SB[n], u2B, acc[n]);
                             u0B = u1B;
                             u1B = u2B;
                         }
@@ -383,7 +401,7 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
                     t = z * c_rec.farT[n][2] * (1.0 + t);
                     t = z * c_rec.farT[n][1] * (1.0 + t);
                     t = z * c_rec.farT[n][0] * (1.0 + t);
-                    acc[j] = cfma(Srow[j], c_rec.farA[n] * qn * (1.0 + t), acc[j]);
+                    acc[j] = cfma(Srow[j], c_rec.farAR[n] * qn * (1.0 + t), acc[j]);
                 }
             }
         }
@@ -558,8 +576,8 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
                         wnB = wlB;
                         wlB = wB;
                         const double2 SA = stS[ca * ROW + j], SB = stS[cb * ROW + j];
-                        acc[j] = cfma(SA, wA * c_rec.Pn[nn] * cvA, acc[j]);
-                        acc[j] = cfma(SB, wB * c_rec.Pn[nn] * cvB, acc[j]);
+                        acc[j] = cfma(SA, wA * c_rec.PnR[nn] * cvA, acc[j]);
+                        acc[j] = cfma(SB, wB * c_rec.PnR[nn] * cvB, acc[j]);
                         cvA *= tcA;
                         cvB *= tcB;
                     }
@@ -592,6 +610,9 @@ __global__ void __launch_bounds__(128, (p2pw_min_blocks<KT, WSM>())) p2p_warp_ke
             v.x += p.x;
             v.y += p.y;
         }
+        const double Rn = c_rec.Rn[M0 + j];             // u units -> G (see RecTables::farAR)
+        v.x *= Rn;
+        v.y *= Rn;
         const int64_t row = a.out_row ? a.out_row[t0 + t] : (t0 + t);
         double2 *o = a.out + (DIRECT ? tk.z * a.part_stride : 0) + row * a.K + a.m0 + j;
         if (a.accumulate) {

@@ -50,6 +50,11 @@ struct RecTables {
     // of 2F1((2n+1)/4, (2n+3)/4; n+1; 1/chi^2)
     double farA[kMaxModes + 2];
     double farT[kMaxModes + 2][4];
+    // the near-field kernel accumulates every branch in forward units u_n = G_n / R_n and
+    // multiplies by R_n once per (target, mode) at the end: the far and Miller factors carry
+    // the 1 / R_n (one multiply fewer per forward pair and mode)
+    double farAR[kMaxModes + 2];   // farA_n / R_n
+    double PnR[kMaxModes + 2];     // P_n / R_n
 };
 constexpr double kFarChi = 1.0e3;        // far branch from chi = 1000 (4 hypergeometric terms)
 __constant__ RecTables c_rec;
@@ -91,6 +96,10 @@ inline void build_rec_tables(RecTables *t)
         const long double a = (2.0L * n + 1.0L) / 4.0L, b = (2.0L * n + 3.0L) / 4.0L, c = n + 1.0L;
         for (int k = 0; k < 4; ++k)
             t->farT[n][k] = (double)((a + k) * (b + k) / ((c + k) * (k + 1.0L)));
+    }
+    for (int n = 0; n < kMaxModes + 2; ++n) {
+        t->farAR[n] = t->farA[n] / t->Rn[n];
+        t->PnR[n] = t->Pn[n] / t->Rn[n];
     }
 }
 
