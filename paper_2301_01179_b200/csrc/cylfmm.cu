@@ -399,7 +399,12 @@ static cylfmm_status run_fill(TensorGeomArgs ta, int64_t ngeom, cudaStream_t st)
 {
     // warp per (station, mode), 4 warps per CTA (tensor.cuh)
     ta.nwork = ngeom * (ta.m1 - ta.m0);
-    tensor_fill_kernel<<<nblk(ta.nwork, 4), 128, 0, st>>>(ta);
+    switch (ta.p) {   // compile-time orders for the BASELINE configurations
+    case 8: tensor_fill_kernel<8><<<nblk(ta.nwork, 4), 128, 0, st>>>(ta); break;
+    case 12: tensor_fill_kernel<12><<<nblk(ta.nwork, 4), 128, 0, st>>>(ta); break;
+    case 16: tensor_fill_kernel<16><<<nblk(ta.nwork, 4), 128, 0, st>>>(ta); break;
+    default: tensor_fill_kernel<0><<<nblk(ta.nwork, 4), 128, 0, st>>>(ta); break;
+    }
     CKL();
     return CYLFMM_OK;
 }

@@ -410,9 +410,21 @@ __device__ __forceinline__ double col_plus2(const Row &v, int lane, bool row00, 
     return (row00 && lane == 30) ? hi00 : a;
 }
 
-__global__ void __launch_bounds__(128) tensor_fill_kernel(TensorGeomArgs a)
+// PT > 0: the order as a compile-time constant (the BASELINE orders 8, 12, 16): every loop below
+// unrolls, so the packed row offsets, the per-step coefficients' rational factors and the
+// k >= 1 / k >= 2 cases become constants (the runtime-order loop spent ~100 instructions per
+// row on index arithmetic, integer -> FP64 conversions and branches; now ~15).  PT = 0: any p.
+//
+// One Laplace step, written so that the newest row enters last through ONE FMA (the row-to-row
+// dependency chain is a single DFMA; everything else is formed off the chain):
+//   new = A_k cur + B_k prv + L_k(c) (s^2 prv[c+2] + 2 s pm1[c+2] + pm2[c+2]),
+//   A_k = -(2k+1) / ((k+2) s),  B_k = (n^2 - k^2) / (s^2 (k+1)(k+2)),
+//   L_k(c) = -(c+1)(c+2) / (s^2 (k+1)(k+2))
+// (the same recursion as  s^2 (k+1)(k+2) new + s (k+1)(2k+1) cur + (k^2 - n^2) prv + ... = 0).
+template <int PT>
+__global__ void __launch_bounds__(128, PT ? 4 : 1) tensor_fill_kernel(TensorGeomArgs a)
 {
-    const int p = a.p, C = 2 * p, D = C + 1, P1 = p + 1;
+    const int p = PT ? PT : a.p, C = 2 * p, D = C + 1, P1 = p + 1;
     const int KW = a.m1 - a.m0;
     const int lane = threadIdx.x & 31;
     const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -453,26 +465,32 @@ __global__ void __launch_bounds__(128) tensor_fill_kernel(TensorGeomArgs a)
         v.hi = c1 <= cmax ? sd[(k * NM + n) * D + c1] : 0.0;
         return v;
     };
-    // one Laplace step: new = [ s (k+1)(2k+1) cur + (k^2 - n^2) prev
-    //                         + (c+1)(c+2) (s^2 prev[c+2] + 2 s prev2[c+2] + prev3[c+2]) ] * inv
-    // (r: s = r, rows a = k+1, k, k-1, k-2 at fixed b; r1: s = r1, rows b = k+1, k, k-1, k-2)
     double hi00 = 0.0;   // (0, 0, 32) at p = 16, set from the seeds below
-    // 1/(s^2 (k+1)(k+2)) from 1/s^2 and a table: no division per step
-    auto lap_step = [&](double isc2, double sc, int k, const Row &cur, const Row &prv,
-                        const Row &pm1, const Row &pm2, bool prv00) {
-        const double inv = -isc2 * c_lapinv[k];
+    const double cc = -(c0 + 1.0) * (c0 + 2.0);
+    // per direction (r: s = r; r1: s = r1): 1/s, 1/s^2, s^2, 2 s
+    struct Dir {
+        double is, is2, s2, s2x;
+    };
+    auto mkdir = [](double sc) {
+        Dir d;
+        d.is = 1.0 / sc;
+        d.is2 = d.is * d.is;
+        d.s2 = sc * sc;
+        d.s2x = 2.0 * sc;
+        return d;
+    };
+    const Dir dr = mkdir(r), dr1 = mkdir(r1);
+    auto lap_step = [&](const Dir &d, int k, const Row &cur, const Row &prv, const Row &pm1,
+                        const Row &pm2, bool prv00) {
+        const double li = c_lapinv[k] * d.is2;                 // 1 / (s^2 (k+1)(k+2))
+        const double A = (-(2.0 * k + 1.0) / (k + 2.0)) * d.is;
+        const double B = (n2 - (double)(k * k)) * li;
         const double t0 = col_plus2(prv, lane, prv00, hi00);
-        const double t1 = k >= 1 ? col_plus2(pm1, lane, false, 0.0) : 0.0;
-        const double t2 = k >= 2 ? col_plus2(pm2, lane, false, 0.0) : 0.0;
+        double lap = d.s2 * t0;
+        if (k >= 1) lap = fma(d.s2x, col_plus2(pm1, lane, false, 0.0), lap);
+        if (k >= 2) lap += col_plus2(pm2, lane, false, 0.0);
         Row nw;
-        {
-            double lap = sc * sc * t0;
-            if (k >= 1) lap = fma(2.0 * sc, t1, lap);
-            if (k >= 2) lap += t2;
-            const double num = sc * (k + 1) * (2.0 * k + 1) * cur.lo + (k * (double)k - n2) * prv.lo +
-                               (c0 + 1.0) * (c0 + 2.0) * lap;
-            nw.lo = num * inv;
-        }
+        nw.lo = fma(A, cur.lo, fma(B, prv.lo, (cc * li) * lap));
         // column c + 32 (only c = 32 at p = 16, row (0, 0), never recursed into): not needed
         nw.hi = 0.0;
         return nw;
@@ -481,8 +499,8 @@ __global__ void __launch_bounds__(128) tensor_fill_kernel(TensorGeomArgs a)
     Row ra0[4] = {}, ra1[4] = {};   // rows a-4 .. a-1 of the b = 0 (ra0) and b = 1 (ra1) planes
     Row b0 = seed(0, C), b1 = p >= 1 ? seed(2, C - 1) : Row{};
     hi00 = __shfl_sync(0xffffffffu, b0.hi, 0);
-    const double ir2 = 1.0 / (r * r), ir12 = 1.0 / (r1 * r1);
     Row a1b0 = p >= 1 ? seed(1, C - 1) : Row{}, a1b1 = p >= 1 ? seed(3, C - 2) : Row{};
+#pragma unroll
     for (int aa = 0; aa <= p; ++aa) {
         Row rb0, rb1;   // rows (aa, 0) and (aa, 1)
         if (aa == 0) {
@@ -493,8 +511,8 @@ __global__ void __launch_bounds__(128) tensor_fill_kernel(TensorGeomArgs a)
             rb1 = a1b1;
         } else {   // Laplace in r (k = aa - 2): rows k+1, k, k-1, k-2 = aa-1 .. aa-4
             const int k = aa - 2;
-            rb0 = lap_step(ir2, r, k, ra0[3], ra0[2], ra0[1], ra0[0], aa == 2);
-            rb1 = lap_step(ir2, r, k, ra1[3], ra1[2], ra1[1], ra1[0], false);
+            rb0 = lap_step(dr, k, ra0[3], ra0[2], ra0[1], ra0[0], aa == 2);
+            rb1 = lap_step(dr, k, ra1[3], ra1[2], ra1[1], ra1[0], false);
         }
 #pragma unroll
         for (int h = 0; h < 3; ++h) {
@@ -507,8 +525,9 @@ __global__ void __launch_bounds__(128) tensor_fill_kernel(TensorGeomArgs a)
         if (p >= 1) store(aa, 1, rb1);
         // Laplace in r1 for this a: rows b + 2 from b + 1, b, b - 1, b - 2
         Row hb[4] = {Row{}, Row{}, rb0, rb1};   // rows b-2, b-1, b, b+1 (b = 0)
+#pragma unroll
         for (int bb = 0; bb + 2 <= p && aa + bb + 2 <= C; ++bb) {
-            const Row nb = lap_step(ir12, r1, bb, hb[3], hb[2], hb[1], hb[0], aa == 0 && bb == 0);
+            const Row nb = lap_step(dr1, bb, hb[3], hb[2], hb[1], hb[0], aa == 0 && bb == 0);
             hb[0] = hb[1];
             hb[1] = hb[2];
             hb[2] = hb[3];
