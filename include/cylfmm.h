@@ -102,6 +102,10 @@ typedef struct {
      * (chi < 1.008), the far series (chi >= 1000) and Miller's backward recursion
      * (P:868-874), and the sum over Miller pairs of the start offset S - N (R#4) */
     int64_t n_forward, n_far, n_miller, miller_steps;
+    /* the tensor seed kernel's span (included in ms_tensor).  Solves without `timings` on large
+     * problems run it on the plan's auxiliary stream, overlapping P2M / M2M, so this is a span
+     * shared with those phases, not an exclusive time */
+    double ms_seeds;
 } cylfmm_timings;
 
 typedef struct cylfmm_plan_s *cylfmm_plan;

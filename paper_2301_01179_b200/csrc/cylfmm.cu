@@ -491,10 +491,11 @@ struct DevBuf {
 
 // Phase timing: CUDA events recorded on the stream each phase runs on (no synchronisation),
 // summed when the timings are read (after the solve has completed), plus NVTX ranges.
-enum { PH_SORT, PH_LISTS, PH_TENSOR, PH_P2M, PH_M2M, PH_S2L, PH_L2L, PH_L2P, PH_P2P, PH_TOTAL, PH_ALLGATHER, PH_N };
+enum { PH_SORT, PH_LISTS, PH_TENSOR, PH_P2M, PH_M2M, PH_S2L, PH_L2L, PH_L2P, PH_P2P, PH_TOTAL, PH_ALLGATHER, PH_SEEDS, PH_N };
 static const char *kPhaseName[PH_N] = {"cylfmm.sort", "cylfmm.lists", "cylfmm.tensor", "cylfmm.p2m",
                                        "cylfmm.m2m", "cylfmm.s2l", "cylfmm.l2l", "cylfmm.l2p",
-                                       "cylfmm.near", "cylfmm.solve", "cylfmm.allgather"};
+                                       "cylfmm.near", "cylfmm.solve", "cylfmm.allgather",
+                                       "cylfmm.tensor_seeds"};
 struct PhaseMark {
     int ph;
     cudaEvent_t a, b;
@@ -630,7 +631,8 @@ static cylfmm_status read_phases(cylfmm_plan p, cylfmm_timings *t)
     t->ms_sort = acc[PH_SORT] / n;
     t->ms_lists = acc[PH_LISTS] / n;
     t->ms_tree = t->ms_sort + t->ms_lists;
-    t->ms_tensor = acc[PH_TENSOR] / n;
+    t->ms_tensor = (acc[PH_TENSOR] + acc[PH_SEEDS]) / n;
+    t->ms_seeds = acc[PH_SEEDS] / n;
     t->ms_p2m = acc[PH_P2M] / n;
     t->ms_m2m = acc[PH_M2M] / n;
     t->ms_s2l = acc[PH_S2L] / n;
@@ -1023,6 +1025,12 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     // (the adaptive tree's near field runs one accumulating launch per level: serial)
     const bool overlap = tm == nullptr && p->aux_ok && ns + nf <= ((int64_t)1 << 20) && q.adaptive_leaf == 0;
     cudaStream_t st_t = overlap ? p->aux[0] : st, st_n = overlap ? p->aux[1] : st;
+    // large solves: the tensor seeds alone on the auxiliary stream, overlapping P2M / M2M.  The
+    // seed kernel's duration is set by its few longest Miller stations (a sequential series
+    // recursion of up to ~10^3 steps in one thread; C5: 3.3 ms with most SMs idle at the end);
+    // the fill follows behind M2M on `st`, joined by an event.
+    const bool seeds_aside = !overlap && tm == nullptr && p->aux_ok;
+    cudaStream_t st_s = (overlap || seeds_aside) ? p->aux[0] : st;
     const int64_t nstat = (int64_t)12 << d;
     const int NM = std::max(K - 1, 1) + 1, D = 2 * pt + 1;
     RET_IF(p->seeds.need(sizeof(double) * (size_t)nstat * 4 * NM * D));
@@ -1462,16 +1470,17 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
     fa.rowkey = p->rowkey.as<int64_t>();
     for (int l = 2; l <= d + 1; ++l) fa.lrow_lev[l] = hcnt[2 * kMaxLevels + 6 + l];
     // tree done: the near field and the tensors start behind it on their own streams
-    if (overlap) {
+    if (overlap || seeds_aside) {
         CK(cudaEventRecord(p->aev[1], st));
-        CK(cudaStreamWaitEvent(st_t, p->aev[1], 0));
+        CK(cudaStreamWaitEvent(st_s, p->aev[1], 0));
     }
     if (nstu > 0 && !(reuse && KW == K)) {   // seeds of all modes once, stations with a pair
-        T.beg(PH_TENSOR, st_t);
-        RET_IF(run_seeds(ta, nstu, st_t));
+        T.beg(PH_SEEDS, st_s);
+        RET_IF(run_seeds(ta, nstu, st_s));
         p->launches++;
-        T.end(PH_TENSOR, st_t);
+        T.end(PH_SEEDS, st_s);
     }
+    if (seeds_aside) CK(cudaEventRecord(p->aev[2], st_s));
     // ---- near field.  Overlapped (small) solves: first, on its own stream, writing
     // every field row, and L2P adds the far field; serial (large) solves: after L2P, adding onto
     // the rows L2P wrote (the read-modify-write then sits at the end of long near-field tasks
@@ -1628,8 +1637,8 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
         fa.m1 = std::min(K, m0 + KW);
         const int kw = fa.m1 - fa.m0;
         // tensors for the normalised stations (shared by all levels): seeds of all modes once,
-        // the Laplace fill per mode chunk
-        {
+        // the Laplace fill per mode chunk (behind M2M when the seeds run aside)
+        auto run_fill_chunk = [&]() -> cylfmm_status {
             ta.out = p->tens.as<double>();
             ta.m0 = fa.m0;
             ta.m1 = fa.m1;
@@ -1643,7 +1652,9 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             p->launches++;
             T.end(PH_TENSOR, st_t);
             if (overlap) CK(cudaEventRecord(p->aev[2], st_t));
-        }
+            return CYLFMM_OK;
+        };
+        if (!seeds_aside) RET_IF(run_fill_chunk());
         if (ns > 0) {
         if (sigma > 0) {
             // adaptive source tree: P2M at every source leaf, whatever its level (the kernel
@@ -1699,6 +1710,10 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             CKL();
             p->launches++;
             T.end(PH_M2M, st);
+        }
+        if (seeds_aside) {
+            if (m0 == 0) CK(cudaStreamWaitEvent(st, p->aev[2], 0));   // seeds done
+            RET_IF(run_fill_chunk());
         }
         // S2L of every level in one launch (each level's contribution), then the L2L chain
         if (overlap) CK(cudaStreamWaitEvent(st, p->aev[2], 0));   // tensors of this chunk ready

@@ -119,14 +119,15 @@ __global__ void __launch_bounds__(128) tensor_seed_kernel(TensorGeomArgs a)
     const int Nw = a.m1 - 1;                 // highest mode needed
     const int Ni = Nw > 1 ? Nw : 1;          // + mode 1 for n = 0
     const int NM = Ni + 1;
+    // shared: G, the tables, g00 and g01 (read by later steps); g10 and g11 go straight to the
+    // output (54 KB at p = 16, K = 65: four CTAs per SM instead of two)
     double *G = sm;                          // [NM]
     double *tab = G + NM;                    // 8 tables x Q: tsum tdif usum udif ssum sdif vp vm
     double *g00 = tab + 8 * Q;               // [NM][D]
-    double *g10 = g00 + NM * D;
-    double *g01 = g10 + NM * D;
-    double *g11 = g01 + NM * D;
-    double *rat = g11 + (NM * D > 8 * Q ? NM * D : 8 * Q);   // [NM][D] Miller ratio series
-    double *rho = rat + NM * D;                              // [D]
+    double *g01 = g00 + NM * D;
+    double *rat = g01 + NM * D;              // [NM][D] Miller ratio series; first the raw tables
+    double *raw = rat;                       // [2][4][Q] (consumed before the Miller step)
+    double *rho = rat + (NM * D > 8 * Q ? NM * D : 8 * Q);   // [D]
     double *den = rho + D;                                   // [D + 4]
     int *sS = reinterpret_cast<int *>(den + D + 4);          // [2]
     const int64_t gi = a.glist ? a.glist[blockIdx.x] : blockIdx.x;
@@ -162,11 +163,11 @@ __global__ void __launch_bounds__(128) tensor_seed_kernel(TensorGeomArgs a)
             double us = (q == 0 ? -1.0 : 0.0) + 2.0 * r1 * vi;
             double w2r = wr * zr - wi * zi;       // (-1)^q z^{q+2}
             double v = sg * 2.0 * r * (q + 1) * w2r;
-            // store raw per sign in scratch: [s][4][Q] at g11 (reused later)
-            g11[(s * 4 + 0) * Q + q] = t;
-            g11[(s * 4 + 1) * Q + q] = u;
-            g11[(s * 4 + 2) * Q + q] = us;
-            g11[(s * 4 + 3) * Q + q] = v;
+            // store raw per sign in scratch: [s][4][Q] (the Miller series area, reused later)
+            raw[(s * 4 + 0) * Q + q] = t;
+            raw[(s * 4 + 1) * Q + q] = u;
+            raw[(s * 4 + 2) * Q + q] = us;
+            raw[(s * 4 + 3) * Q + q] = v;
             double nwr = -(wr * zr - wi * zi), nwi = -(wr * zi + wi * zr);
             wr = nwr;
             wi = nwi;
@@ -178,14 +179,14 @@ __global__ void __launch_bounds__(128) tensor_seed_kernel(TensorGeomArgs a)
     __syncthreads();
     // raw tables per sign: t+- u+- us+- v+-
     for (int q = tid; q < Q; q += blockDim.x) {
-        tab[0 * Q + q] = g11[0 * Q + q];  // t+
-        tab[1 * Q + q] = g11[4 * Q + q];  // t-
-        tab[2 * Q + q] = g11[1 * Q + q];  // u+
-        tab[3 * Q + q] = g11[5 * Q + q];  // u-
-        tab[4 * Q + q] = g11[2 * Q + q];  // us+
-        tab[5 * Q + q] = g11[6 * Q + q];  // us-
-        tab[6 * Q + q] = g11[3 * Q + q];  // v+
-        tab[7 * Q + q] = g11[7 * Q + q];  // v-
+        tab[0 * Q + q] = raw[0 * Q + q];  // t+
+        tab[1 * Q + q] = raw[4 * Q + q];  // t-
+        tab[2 * Q + q] = raw[1 * Q + q];  // u+
+        tab[3 * Q + q] = raw[5 * Q + q];  // u-
+        tab[4 * Q + q] = raw[2 * Q + q];  // us+
+        tab[5 * Q + q] = raw[6 * Q + q];  // us-
+        tab[6 * Q + q] = raw[3 * Q + q];  // v+
+        tab[7 * Q + q] = raw[7 * Q + q];  // v-
     }
     for (int n = tid; n < NM; n += blockDim.x) g00[n * D] = G[n];
     __syncthreads();
@@ -318,6 +319,8 @@ __global__ void __launch_bounds__(128) tensor_seed_kernel(TensorGeomArgs a)
             }
         }
     }
+    // seeds out: [4][NM][D]
+    double *so = a.seeds + gi * 4 * (int64_t)NM * D;
     // r and r1 derivatives
     for (int e = tid; e < NM * C; e += blockDim.x) {
         int n = e / C, k = e % C, m = n == 0 ? 1 : n - 1;
@@ -328,7 +331,7 @@ __global__ void __launch_bounds__(128) tensor_seed_kernel(TensorGeomArgs a)
             s1 = fma(gp, up[q], fma(gd, um[q], s1));
             s2 = fma(gp, sp[q], fma(gd, smn[q], s2));
         }
-        g10[n * D + k] = (-g00[n * D + k] + (n - 0.5) * s1) / (2.0 * r);
+        so[NM * D + n * D + k] = (-g00[n * D + k] + (n - 0.5) * s1) / (2.0 * r);
         g01[n * D + k] = (-g00[n * D + k] + (n - 0.5) * s2) / (2.0 * r1);
     }
     __syncthreads();
@@ -341,29 +344,24 @@ __global__ void __launch_bounds__(128) tensor_seed_kernel(TensorGeomArgs a)
             double hn = g01[n * D + k - q], hm = g01[m * D + k - q];
             s = fma(gn + gm, vp[q], fma(hn + hm, up[q], fma(gn - gm, vm[q], fma(hn - hm, um[q], s))));
         }
-        // g11 overlaps the raw tables, consumed before the previous __syncthreads
-        g11[n * D + k] = (-g01[n * D + k] + (n - 0.5) * s) / (2.0 * r);
+        so[3 * NM * D + n * D + k] = (-g01[n * D + k] + (n - 0.5) * s) / (2.0 * r);
     }
-    __syncthreads();
-    // seeds out: [4][NM][D]
-    double *so = a.seeds + gi * 4 * (int64_t)NM * D;
     for (int e = tid; e < NM * D; e += blockDim.x) {
-        int n = e / D, c = e % D;
+        const int c = e % D;
         so[e] = g00[e];
-        so[NM * D + e] = c < C ? g10[e] : 0.0;
         so[2 * NM * D + e] = c < C ? g01[e] : 0.0;
-        so[3 * NM * D + e] = c < C - 1 ? g11[e] : 0.0;
-        (void)n;
+        if (c == C) so[NM * D + e] = 0.0;               // (g10, g11 beyond their last column)
+        if (c >= C - 1) so[3 * NM * D + e] = 0.0;
     }
 }
 
 inline size_t tensor_seed_smem(int K, int m1, int p)
 {
     int Nw = m1 - 1, Ni = Nw > 1 ? Nw : 1, NM = Ni + 1, Q = 2 * p + 2, D = 2 * p + 1;
-    size_t g11 = (size_t)NM * D;
-    if (g11 < (size_t)8 * Q) g11 = 8 * Q;
+    size_t ratsz = (size_t)NM * D;
+    if (ratsz < (size_t)8 * Q) ratsz = 8 * Q;
     (void)K;
-    return sizeof(double) * (NM + 8 * Q + 3 * (size_t)NM * D + g11 + (size_t)NM * D + 2 * D + 6);
+    return sizeof(double) * (NM + 8 * Q + 2 * (size_t)NM * D + ratsz + 2 * D + 6);
 }
 
 // closed form of packed_off

@@ -44,7 +44,8 @@ class Timings(ctypes.Structure):
                                               "kernel_launches")] + \
                [(n, ctypes.c_double) for n in ("ms_sort", "ms_lists", "ms_unpermute", "ms_allgather")] + \
                [(n, ctypes.c_int64) for n in ("n_solves", "n_forward", "n_far", "n_miller",
-                                              "miller_steps")]
+                                              "miller_steps")] + \
+               [("ms_seeds", ctypes.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
