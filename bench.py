@@ -159,8 +159,32 @@ def run_reference(args):
     if rank != 0:
         return
     import oracle
-    pr = make_problem(args.config, args)
     cores = os.cpu_count() or 1
+    if args.config == "C1":   # the oracle's direct sum, whole (about 0.1 s per step)
+        oracle.build()
+        pr = CONFIGS["C1"]()
+        K = pr.S.shape[1]
+        ts = []
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            oracle.direct(pr.sr, pr.sz, pr.S, pr.fr, pr.fz, nthreads=cores)
+            if i >= args.warmup:
+                ts.append(time.perf_counter() - t0)
+        t = sum(ts) / len(ts)
+        v = len(pr.sr) * len(pr.fr) * K / t
+        print(json.dumps({
+            "metric": "FP64 modal source-field interactions/s (direct sum)", "value": v,
+            "unit": "interactions/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "replicas only", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"C1: {pr.name}", "n_src": len(pr.sr), "n_fld": len(pr.fr), "modes": K},
+            "cpu_baseline": {"value": v, "unit": "interactions/s", "cores": cores, "kind": "oracle",
+                             "sample": "the whole C1 direct sum per step"},
+            "e2e": {"value": v, "unit": "interactions/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}), flush=True)
+        return
+    pr = make_problem(args.config, args)
     m, _, _, idx, fixed = oracle_sample(pr, 4.0, cores)   # each step a bounded sample (~4 s)
     fr, fz = pr.fr[idx], pr.fz[idx]
     for _ in range(args.warmup):
@@ -225,6 +249,123 @@ NCU_NAME = {"s2l": "s2l_batch_kernel", "p2p": "p2p_warp_kernel", "l2p": "l2p_ker
             "p2m": "p2m_kernel"}
 
 
+def run_direct(args):
+    """C1 (BASELINE configs[0]): the direct modal sum, I_direct = (N_s N_f - skipped) K / t
+    (SURVEY 8(d)).  The sum is ~16 us of FP64 work, so a call is launch-latency bound: the step
+    is one replay of a CUDA graph captured from cylfmm_direct_enqueue (launches only), timed
+    with the L2 flushed between replays, plus 1000 replays back to back (inputs L2-resident:
+    0.3 MB)."""
+    import torch
+    import paper_2301_01179_b200 as g
+    from paper_2301_01179_b200 import build as b
+    if not b.up_to_date():
+        b.build()
+    pr = CONFIGS["C1"]()
+    K = pr.S.shape[1]
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
+    torch.cuda.set_device(dev)
+    d = [torch.as_tensor(np.ascontiguousarray(a), device=dev) for a in (pr.sr, pr.sz, pr.S, pr.fr, pr.fz)]
+    ns, nf = len(pr.sr), len(pr.fr)
+    out = torch.empty((nf, K), dtype=torch.complex128, device=dev)
+    ws = torch.empty(g.direct_workspace_bytes(ns, nf, K), dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        g.direct_enqueue(*d, out, ws)
+    torch.cuda.synchronize()
+    assert int(ws[:4].view(torch.int32).item()) == 0
+    gr = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream()
+    cs.wait_stream(stream)
+    with torch.cuda.stream(cs):
+        with torch.cuda.graph(gr, stream=cs):
+            g.direct_enqueue(*d, out, ws)
+    stream.wait_stream(cs)
+    for _ in range(args.warmup):
+        gr.replay()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(dev.index)
+    clocks.start()
+    time.sleep(0.4)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        gr.replay()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    t_step = sum(a.elapsed_time(bb) for a, bb in ev) / args.steps
+    R = 1000
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(R):
+        gr.replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t_rep = e0.elapsed_time(e1) / R
+    # the plain synchronising call (allocation + flag read-back per call), for comparison
+    e0.record(stream)
+    for _ in range(50):
+        g.direct(*d, out=out)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t_call = e0.elapsed_time(e1) / 50
+    clk = clocks.stop()
+    inter = ns * nf * K     # independent field draws: no coincident pair (flag checked above)
+    # e2e: host buffers in, potentials back, through the graph (pinned memory, copies timed)
+    hs = [torch.as_tensor(np.ascontiguousarray(a)).pin_memory() for a in (pr.sr, pr.sz, pr.S, pr.fr, pr.fz)]
+    hout = torch.empty((nf, K), dtype=torch.complex128).pin_memory()
+
+    def e2e_step():
+        for x, y in zip(d, hs):
+            x.copy_(y, non_blocking=True)
+        gr.replay()
+        hout.copy_(out, non_blocking=True)
+        torch.cuda.synchronize()
+    for _ in range(3):
+        e2e_step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_step()
+    t_e2e = (time.perf_counter() - t0) * 1e3 / args.steps
+    flops = 600.0 * ns * nf   # SURVEY 8(d): W_pair ~ 600 flops at K = 9 (backward branch), 6e8 per sum
+    ach = flops / (t_rep * 1e-3) / 1e12
+    line = {"metric": "FP64 modal source-field interactions/s (direct sum)",
+            "value": inter / (t_rep * 1e-3), "unit": "interactions/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_rep,
+            "higher_is_better": True, "scaling": "replicas only", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C1: {pr.name}", "n_src": ns, "n_fld": nf, "modes": K,
+                       "miller": "accurate", "l2": "resident (1000 CUDA-graph replays back to back; "
+                       "the flushed single-replay time is ms_per_step_l2_flushed)"},
+            "ms_per_step_l2_flushed": t_step, "value_l2_flushed": inter / (t_step * 1e-3),
+            "ms_per_call_synchronous_api": t_call,
+            "roofline": {"bound": "alu", "kernel": "p2p_warp_kernel + reduce_parts_kernel (direct sum)",
+                         "achieved": ach, "peak": FP64_NOMINAL_TFLOPS, "unit": "TFLOP/s",
+                         "frac": ach / FP64_NOMINAL_TFLOPS, "traffic": None,
+                         "algorithmic_flops": flops,
+                         "note": "one sum is 6e8 flops = 16 us at the FP64 nominal: launch / tail bound"},
+            "clocks": clk,
+            "e2e": {"value": inter / (t_e2e * 1e-3), "unit": "interactions/s", "ms_per_step": t_e2e,
+                    "h2d_bytes_per_step": ns * (16 + 16 * K) + nf * 16, "d2h_bytes_per_step": nf * K * 16,
+                    "api": "pinned copies + CUDA-graph replay of cylfmm_direct_enqueue"},
+            "gpu_launches": 3 * R}
+    if not args.no_cpu_baseline:
+        import oracle
+        oracle.build()
+        cores = os.cpu_count() or 1
+        t0 = time.perf_counter()
+        reps = 0
+        while time.perf_counter() - t0 < 10.0:
+            oracle.direct(pr.sr, pr.sz, pr.S, pr.fr, pr.fz, nthreads=cores)
+            reps += 1
+        t = (time.perf_counter() - t0) / reps
+        line["cpu_baseline"] = {"value": inter / t, "unit": "interactions/s", "cores": cores,
+                                "kind": "oracle", "sample": f"the whole C1 direct sum, {reps} repeats"}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -242,6 +383,8 @@ def main():
     args.warmup = max(args.warmup, 3) if args.impl == "cylfmm" else args.warmup
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == "C1":
+        return run_direct(args)
 
     import torch
     import torch.distributed as dist

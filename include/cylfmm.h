@@ -132,6 +132,24 @@ cylfmm_status cylfmm_direct(const double *src_r, const double *src_z, const doub
                             int64_t n_fld, int n_modes, int miller, int exclude_coincident,
                             double *out_Phi, cylfmm_stream_t stream);
 
+/* The same direct sum as launches only: no allocation, no synchronisation and no
+ * host read, so the call can be captured into a CUDA graph and replayed (the C1-sized sum is
+ * launch-latency bound otherwise).  Arguments as for cylfmm_direct, plus
+ *   workspace : DEVICE, 16-byte aligned, at least cylfmm_direct_workspace_bytes(...) bytes,
+ *               owned by the caller and in use until the work queued here has completed.
+ *               Its first int is the error flag, zeroed by the call: non-zero after completion
+ *               iff an unexcluded coincident pair was met (what cylfmm_direct reports as
+ *               CYLFMM_ENUMERIC); the rest holds per-partition partial sums.
+ * Results are bitwise those of cylfmm_direct.  Errors: EINVAL (sizes, null pointers, workspace
+ * too small or misaligned), ECUDA. */
+cylfmm_status cylfmm_direct_workspace_bytes(int64_t n_src, int64_t n_fld, int n_modes,
+                                            int64_t *bytes);
+cylfmm_status cylfmm_direct_enqueue(const double *src_r, const double *src_z, const double *src_S,
+                                    int64_t n_src, const double *fld_r, const double *fld_z,
+                                    int64_t n_fld, int n_modes, int miller, int exclude_coincident,
+                                    double *out_Phi, void *workspace, int64_t workspace_bytes,
+                                    cylfmm_stream_t stream);
+
 /* ---------------------------------------------------------------------------------------
  * FMM plan.  The plan owns its device workspace (grown on demand, freed by destroy).
  * One plan serves one device and one solve at a time.

@@ -258,35 +258,20 @@ static cudaError_t launch_p2pw(const P2PArgs &a, cudaStream_t st, bool direct = 
 
 // ------------------------------------------------------------------------------------------
 // direct modal sum
-extern "C" cylfmm_status cylfmm_direct(const double *src_r, const double *src_z,
-                                       const double *src_S, int64_t n_src, const double *fld_r,
-                                       const double *fld_z, int64_t n_fld, int n_modes,
-                                       int miller, int exclude_coincident, double *out_Phi,
-                                       cylfmm_stream_t stream)
+// Direct sum: partition of the sources among the CTAs of one target tile, and the launches.
+struct DirectShape {
+    bool wk;          // warp-task kernel (p2p_warp.cuh)
+    int nparts;       // source partitions per target tile (partial sums reduced afterwards)
+    int64_t per;      // sources per partition
+    int64_t tiles;    // 32-target tiles
+};
+static cylfmm_status direct_shape(int64_t n_src, int64_t n_fld, int K, DirectShape *sh)
 {
-    if (n_src < 0 || n_fld < 0 || n_modes < 1 || n_modes > CYLFMM_MAX_MODES ||
-        (miller != 0 && miller != 1) || n_src > INT32_MAX || n_fld > INT32_MAX) {
-        set_err("cylfmm_direct: bad sizes (n_src=%lld n_fld=%lld n_modes=%d miller=%d)",
-                (long long)n_src, (long long)n_fld, n_modes, miller);
-        return CYLFMM_EINVAL;
-    }
-    if ((n_src > 0 && (!src_r || !src_z || !src_S)) || (n_fld > 0 && (!fld_r || !fld_z || !out_Phi))) {
-        set_err("cylfmm_direct: null pointer");
-        return CYLFMM_EINVAL;
-    }
-    RET_IF(ensure_init());
-    cudaStream_t st = (cudaStream_t)stream;
-    if (n_fld == 0) return CYLFMM_OK;
-    const int K = n_modes;
-    if (n_src == 0) {
-        CK(cudaMemsetAsync(out_Phi, 0, sizeof(double) * 2 * K * n_fld, st));
-        return CYLFMM_OK;
-    }
     int dev = 0, nsm = 148;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    // warp-task kernel (p2p_warp.cuh): tasks = (32-target tile, source partition of >= 128),
-    // ~12 tasks per resident CTA slot; CYLFMM_P2P_VARIANT=1 keeps the CTA-wide kernel
+    // warp-task kernel: tasks = (32-target tile, source partition of >= 128), ~12 tasks per
+    // resident CTA slot; the CTA-wide kernel serves the mode counts the warp kernel does not
     const bool wk = p2pw_enabled(K, false);
     const int TT = 32, SC = 4;
     int64_t tiles = (n_fld + TT - 1) / TT;
@@ -296,21 +281,19 @@ extern "C" cylfmm_status cylfmm_direct(const double *src_r, const double *src_z,
     int64_t per = (n_src + nparts - 1) / nparts;
     per = (per + SC - 1) / SC * SC;
     nparts = (int)((n_src + per - 1) / per);
-    int *d_err = nullptr;
-    double2 *ws = nullptr;
-    // stream-ordered frees on every return path (including CK failures below)
-    struct AsyncFree {
-        void **q;
-        cudaStream_t s;
-        ~AsyncFree()
-        {
-            if (*q) cudaFreeAsync(*q, s);
-        }
-    } free_err{(void **)&d_err, st}, free_ws{(void **)&ws, st};
-    CK(cudaMallocAsync((void **)&d_err, 2 * sizeof(int), st));
+    *sh = {wk, nparts, per, tiles};
+    return CYLFMM_OK;
+}
+// d_err: DEVICE int[2] (error flag, task counter), zeroed here; ws: DEVICE double2[nparts][n_fld][K]
+// when sh.nparts > 1.  Launches only: no allocation, no synchronisation.
+static cylfmm_status direct_launch(const DirectShape &sh, const double *src_r, const double *src_z,
+                                   const double *src_S, int64_t n_src, const double *fld_r,
+                                   const double *fld_z, int64_t n_fld, int K, int miller,
+                                   int exclude_coincident, double *out_Phi, int *d_err, double2 *ws,
+                                   cudaStream_t st)
+{
     CK(cudaMemsetAsync(d_err, 0, 2 * sizeof(int), st));
-    if (nparts > 1) CK(cudaMallocAsync((void **)&ws, sizeof(double2) * (size_t)nparts * n_fld * K, st));
-    const int win = wk ? kP2PWWindow : kP2PWindow;
+    const int win = sh.wk ? kP2PWWindow : kP2PWindow;
     for (int m0 = 0; m0 < K; m0 += win) {
         P2PArgs a = {};
         a.sr = src_r;
@@ -326,22 +309,75 @@ extern "C" cylfmm_status cylfmm_direct(const double *src_r, const double *src_z,
         a.miller = miller;
         a.fwd2 = forward_coef(K - 1, miller);
         a.exclude = exclude_coincident;
-        a.out = nparts > 1 ? ws : reinterpret_cast<double2 *>(out_Phi);
+        a.out = sh.nparts > 1 ? ws : reinterpret_cast<double2 *>(out_Phi);
         a.out_row = nullptr;
         a.accumulate = 0;
         a.part_stride = n_fld * K;
-        a.src_per_part = per;
+        a.src_per_part = sh.per;
         a.err_flag = d_err;
         a.task_ctr = d_err + 1;
-        if (wk) CK(launch_p2pw(a, st, true));
-        else CK(launch_p2p<false>(TT, a, dim3((unsigned)tiles, nparts), st));
+        if (sh.wk) CK(launch_p2pw(a, st, true));
+        else CK(launch_p2p<false>(32, a, dim3((unsigned)sh.tiles, sh.nparts), st));
     }
-    if (nparts > 1) {
+    if (sh.nparts > 1) {
         int64_t ne = n_fld * K;
-        reduce_parts_kernel<<<nblk(ne, 256), 256, 0, st>>>(ws, ne, nparts,
+        reduce_parts_kernel<<<nblk(ne, 256), 256, 0, st>>>(ws, ne, sh.nparts,
                                                           reinterpret_cast<double2 *>(out_Phi));
         CKL();
     }
+    return CYLFMM_OK;
+}
+static cylfmm_status direct_check_args(const char *who, const double *src_r, const double *src_z,
+                                       const double *src_S, int64_t n_src, const double *fld_r,
+                                       const double *fld_z, int64_t n_fld, int n_modes, int miller,
+                                       const double *out_Phi)
+{
+    if (n_src < 0 || n_fld < 0 || n_modes < 1 || n_modes > CYLFMM_MAX_MODES ||
+        (miller != 0 && miller != 1) || n_src > INT32_MAX || n_fld > INT32_MAX) {
+        set_err("%s: bad sizes (n_src=%lld n_fld=%lld n_modes=%d miller=%d)", who,
+                (long long)n_src, (long long)n_fld, n_modes, miller);
+        return CYLFMM_EINVAL;
+    }
+    if ((n_src > 0 && (!src_r || !src_z || !src_S)) || (n_fld > 0 && (!fld_r || !fld_z || !out_Phi))) {
+        set_err("%s: null pointer", who);
+        return CYLFMM_EINVAL;
+    }
+    return CYLFMM_OK;
+}
+
+extern "C" cylfmm_status cylfmm_direct(const double *src_r, const double *src_z,
+                                       const double *src_S, int64_t n_src, const double *fld_r,
+                                       const double *fld_z, int64_t n_fld, int n_modes,
+                                       int miller, int exclude_coincident, double *out_Phi,
+                                       cylfmm_stream_t stream)
+{
+    RET_IF(direct_check_args("cylfmm_direct", src_r, src_z, src_S, n_src, fld_r, fld_z, n_fld,
+                             n_modes, miller, out_Phi));
+    RET_IF(ensure_init());
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n_fld == 0) return CYLFMM_OK;
+    const int K = n_modes;
+    if (n_src == 0) {
+        CK(cudaMemsetAsync(out_Phi, 0, sizeof(double) * 2 * K * n_fld, st));
+        return CYLFMM_OK;
+    }
+    DirectShape sh;
+    RET_IF(direct_shape(n_src, n_fld, K, &sh));
+    int *d_err = nullptr;
+    double2 *ws = nullptr;
+    // stream-ordered frees on every return path (including CK failures below)
+    struct AsyncFree {
+        void **q;
+        cudaStream_t s;
+        ~AsyncFree()
+        {
+            if (*q) cudaFreeAsync(*q, s);
+        }
+    } free_err{(void **)&d_err, st}, free_ws{(void **)&ws, st};
+    CK(cudaMallocAsync((void **)&d_err, 2 * sizeof(int), st));
+    if (sh.nparts > 1) CK(cudaMallocAsync((void **)&ws, sizeof(double2) * (size_t)sh.nparts * n_fld * K, st));
+    RET_IF(direct_launch(sh, src_r, src_z, src_S, n_src, fld_r, fld_z, n_fld, K, miller,
+                         exclude_coincident, out_Phi, d_err, ws, st));
     int h_err = 0;
     CK(cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -350,6 +386,55 @@ extern "C" cylfmm_status cylfmm_direct(const double *src_r, const double *src_z,
         return CYLFMM_ENUMERIC;
     }
     return CYLFMM_OK;
+}
+
+extern "C" cylfmm_status cylfmm_direct_workspace_bytes(int64_t n_src, int64_t n_fld, int n_modes,
+                                                       int64_t *bytes)
+{
+    if (!bytes || n_src < 0 || n_fld < 0 || n_modes < 1 || n_modes > CYLFMM_MAX_MODES ||
+        n_src > INT32_MAX || n_fld > INT32_MAX) {
+        set_err("cylfmm_direct_workspace_bytes: bad arguments");
+        return CYLFMM_EINVAL;
+    }
+    RET_IF(ensure_init());
+    *bytes = 16;   // the two flag words, padded
+    if (n_src == 0 || n_fld == 0) return CYLFMM_OK;
+    DirectShape sh;
+    RET_IF(direct_shape(n_src, n_fld, n_modes, &sh));
+    if (sh.nparts > 1) *bytes += (int64_t)sizeof(double2) * sh.nparts * n_fld * n_modes;
+    return CYLFMM_OK;
+}
+
+extern "C" cylfmm_status cylfmm_direct_enqueue(const double *src_r, const double *src_z,
+                                               const double *src_S, int64_t n_src,
+                                               const double *fld_r, const double *fld_z,
+                                               int64_t n_fld, int n_modes, int miller,
+                                               int exclude_coincident, double *out_Phi,
+                                               void *workspace, int64_t workspace_bytes,
+                                               cylfmm_stream_t stream)
+{
+    RET_IF(direct_check_args("cylfmm_direct_enqueue", src_r, src_z, src_S, n_src, fld_r, fld_z,
+                             n_fld, n_modes, miller, out_Phi));
+    int64_t need = 0;
+    RET_IF(cylfmm_direct_workspace_bytes(n_src, n_fld, n_modes, &need));
+    if (!workspace || workspace_bytes < need || ((uintptr_t)workspace & 15)) {
+        set_err("cylfmm_direct_enqueue: workspace of %lld bytes (16-byte aligned) needed, %lld given",
+                (long long)need, (long long)workspace_bytes);
+        return CYLFMM_EINVAL;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    int *d_err = (int *)workspace;
+    const int K = n_modes;
+    if (n_fld == 0 || n_src == 0) {
+        CK(cudaMemsetAsync(d_err, 0, 2 * sizeof(int), st));
+        if (n_fld > 0) CK(cudaMemsetAsync(out_Phi, 0, sizeof(double) * 2 * K * n_fld, st));
+        return CYLFMM_OK;
+    }
+    DirectShape sh;
+    RET_IF(direct_shape(n_src, n_fld, K, &sh));
+    return direct_launch(sh, src_r, src_z, src_S, n_src, fld_r, fld_z, n_fld, K, miller,
+                         exclude_coincident, out_Phi, d_err,
+                         reinterpret_cast<double2 *>((char *)workspace + 16), st);
 }
 
 // ------------------------------------------------------------------------------------------

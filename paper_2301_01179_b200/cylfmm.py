@@ -77,6 +77,10 @@ def lib():
     L.cylfmm_version.argtypes = []
     L.cylfmm_direct.restype = i
     L.cylfmm_direct.argtypes = [vp, vp, vp, i64, vp, vp, i64, i, i, i, vp, vp]
+    L.cylfmm_direct_workspace_bytes.restype = i
+    L.cylfmm_direct_workspace_bytes.argtypes = [i64, i64, i, ctypes.POINTER(i64)]
+    L.cylfmm_direct_enqueue.restype = i
+    L.cylfmm_direct_enqueue.argtypes = [vp, vp, vp, i64, vp, vp, i64, i, i, i, vp, vp, i64, vp]
     L.cylfmm_plan_create.restype = i
     L.cylfmm_plan_create.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(Params)]
     L.cylfmm_plan_destroy.restype = None
@@ -167,6 +171,29 @@ def direct(src_r, src_z, src_S, fld_r, fld_z, miller=MILLER_ACCURATE, exclude_co
     _check(lib().cylfmm_direct(_ptr(sr), _ptr(sz), _ptr(S), ns, _ptr(fr), _ptr(fz), nf, K, miller,
                                int(bool(exclude_coincident)), _ptr(out), _stream(torch)),
            "cylfmm_direct")
+    return out
+
+
+def direct_workspace_bytes(n_src, n_fld, n_modes):
+    """Bytes of caller-owned device workspace cylfmm_direct_enqueue needs."""
+    n = ctypes.c_int64(0)
+    _check(lib().cylfmm_direct_workspace_bytes(n_src, n_fld, n_modes, ctypes.byref(n)),
+           "cylfmm_direct_workspace_bytes")
+    return n.value
+
+
+def direct_enqueue(src_r, src_z, src_S, fld_r, fld_z, out, workspace, miller=MILLER_ACCURATE,
+                   exclude_coincident=True):
+    """cylfmm_direct_enqueue: the direct sum as launches only (CUDA-graph capturable).  All
+    arguments are CUDA tensors; `workspace` is a uint8 tensor of direct_workspace_bytes(...)
+    bytes whose first int32 is the error flag after completion.  Returns `out`."""
+    torch = _torch()
+    ns, K = src_S.shape
+    nf = fld_r.shape[0]
+    _check(lib().cylfmm_direct_enqueue(_ptr(src_r), _ptr(src_z), _ptr(src_S), ns, _ptr(fld_r),
+                                       _ptr(fld_z), nf, K, miller, int(bool(exclude_coincident)),
+                                       _ptr(out), _ptr(workspace), workspace.numel(),
+                                       _stream(torch)), "cylfmm_direct_enqueue")
     return out
 
 

@@ -22,7 +22,7 @@ def libso():
 
 def test_header_declares_the_boundary():
     names = set(cylfmm.header_functions())
-    for f in ("cylfmm_direct", "cylfmm_plan_create", "cylfmm_fmm_solve", "cylfmm_fmm_solve_host",
+    for f in ("cylfmm_direct", "cylfmm_direct_enqueue", "cylfmm_direct_workspace_bytes", "cylfmm_plan_create", "cylfmm_fmm_solve", "cylfmm_fmm_solve_host",
               "cylfmm_plan_sync", "cylfmm_plan_destroy", "cylfmm_greens_batch",
               "cylfmm_tensor_batch", "cylfmm_tree_sort", "cylfmm_status_string",
               "cylfmm_last_error", "cylfmm_version"):
@@ -53,6 +53,9 @@ def test_invalid_arguments_rejected_before_any_work(libso):
     # negative sizes / bad mode counts are argument errors, detected on the host
     st = L.cylfmm_direct(None, None, None, -1, None, None, 0, 3, 0, 1, None, None)
     assert st == cylfmm.EINVAL
+    st = L.cylfmm_direct_enqueue(None, None, None, 4, None, None, 4, 3, 0, 1, None, None, 0, None)
+    assert st == cylfmm.EINVAL
+    assert L.cylfmm_direct_workspace_bytes(4, 4, 0, None) == cylfmm.EINVAL
     st = L.cylfmm_greens_batch(None, None, None, 4, 0, 0, None, None)
     assert st == cylfmm.EINVAL
     prm = cylfmm.Params(3, 0, 4, 0, 0, 1, 0.0, 1.0, 0)   # order 0 is invalid

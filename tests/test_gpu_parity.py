@@ -210,6 +210,50 @@ def test_direct_bitwise_deterministic(gpu):
     assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("ns,nf,K", [(1000, 1000, 9), (37, 5, 3), (4100, 77, 33), (300, 90, 65), (0, 10, 4)])
+def test_direct_enqueue_graph_replay_bitwise(gpu, ns, nf, K):
+    """cylfmm_direct_enqueue (launches only, caller workspace) equals cylfmm_direct bit for bit,
+    directly and replayed from a CUDA graph on new coefficients; its flag word reports an
+    unexcluded coincident pair."""
+    import torch
+    rng = np.random.default_rng(ns + nf + K)
+    sr, sz, S = uniform_rings(rng, ns, K)
+    fr, fz, _ = uniform_rings(rng, nf, 1)
+    dev = "cuda"
+    d = [torch.as_tensor(a, device=dev) for a in (sr, sz, S.reshape(ns, K), fr, fz)]
+    ref = gpu.direct(*d).cpu().numpy()
+    ws = torch.empty(gpu.direct_workspace_bytes(ns, nf, K), dtype=torch.uint8, device=dev)
+    out = torch.full((nf, K), float("nan"), dtype=torch.complex128, device=dev)
+    gpu.direct_enqueue(*d, out, ws)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), ref)
+    assert int(ws[:4].view(torch.int32).item()) == 0
+    if ns == 0:
+        return
+    gr = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream()
+    cs.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(cs):
+        with torch.cuda.graph(gr, stream=cs):
+            gpu.direct_enqueue(*d, out, ws)
+    torch.cuda.current_stream().wait_stream(cs)
+    S2 = torch.as_tensor(rng.standard_normal((ns, K)) + 1j * rng.standard_normal((ns, K)), device=dev)
+    d[2].copy_(S2)
+    out.fill_(float("nan"))
+    gr.replay()
+    torch.cuda.synchronize()
+    ref2 = gpu.direct(*d).cpu().numpy()
+    assert np.array_equal(out.cpu().numpy(), ref2)
+    # an unexcluded coincident pair raises the flag word (cylfmm_direct: CYLFMM_ENUMERIC)
+    d[3][0], d[4][0] = d[0][0], d[1][0]
+    gpu.direct_enqueue(*d, out, ws, exclude_coincident=False)
+    torch.cuda.synchronize()
+    assert int(ws[:4].view(torch.int32).item()) != 0
+    # workspace too small: argument error before any launch
+    with pytest.raises(gpu.CylFMMError):
+        gpu.direct_enqueue(*d, out, ws[:8])
+
+
 @pytest.mark.parametrize("n,depth,L,z0", [(1000, 4, 1.0, 0.0), (70000, 6, 2.0, -1.0), (5, 2, 1.0, 0.0)])
 def test_tree_sort_bit_exact(gpu, orc, n, depth, L, z0):
     rng = np.random.default_rng(n)
