@@ -145,6 +145,20 @@ static cudaError_t allow_smem(F *kernel)
 #define S2L_P16 3, 4, 57, 3
 #define S2L_ALL(X) X(S2L_P8) X(S2L_P12) X(S2L_P16)
 
+// Stream-ordered scratch of the plan-less entry points (direct sum, test batches) comes from a
+// library-owned pool that keeps up to 64 MB cached: the device's default pool returns its memory
+// to the driver at every synchronisation, which made each small synchronising call re-map its
+// scratch (9 ms per C1 direct sum against 0.12 ms of work).
+static cudaMemPool_t g_pool[64];
+static cylfmm_status scratch_alloc(void **ptr, size_t bytes, cudaStream_t st)
+{
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (dev < 64 && g_pool[dev]) CK(cudaMallocFromPoolAsync(ptr, bytes, g_pool[dev], st));
+    else CK(cudaMallocAsync(ptr, bytes, st));
+    return CYLFMM_OK;
+}
+
 static cylfmm_status ensure_init()
 {
     int dev = 0;
@@ -166,18 +180,45 @@ static cylfmm_status ensure_init()
     P2P_INSTANCES(X)
 #undef X
     CK(allow_smem(tensor_seed_kernel));
-    CK(allow_smem(p2m_kernel));
+    CK(allow_smem(p2m_kernel<2>));
+    CK(allow_smem(p2m_kernel<3>));
+    CK(allow_smem(p2m_kernel<5>));
     CK(allow_smem(m2m_kernel));
     CK(allow_smem(l2l_kernel));
     CK(allow_smem(l2p_kernel<4, false>));
     CK(allow_smem(l2p_kernel<9, false>));
     CK(allow_smem(l2p_kernel<13, false>));
     CK(allow_smem(l2p_kernel<16, false>));
+    CK(allow_smem(l2p_kernel<4, false, 2>));
+    CK(allow_smem(l2p_kernel<9, false, 2>));
+    CK(allow_smem(l2p_kernel<13, false, 2>));
+    CK((allow_smem(l2p_kernel<13, false, 2, 16, true>)));
+    CK(allow_smem(l2p_kernel<16, false, 2>));
     CK(allow_smem(l2p_kernel<16, true>));
 #define X(...) CK(allow_smem(s2l_batch_kernel<__VA_ARGS__>));
     S2L_ALL(X)
 #undef X
-    if (dev < 64) g_init_done[dev] = true;
+    if (dev < 64) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        CK(cudaMemPoolCreate(&g_pool[dev], &props));
+        uint64_t keep = 64ull << 20;
+        CK(cudaMemPoolSetAttribute(g_pool[dev], cudaMemPoolAttrReleaseThreshold, &keep));
+        g_init_done[dev] = true;
+    }
+    return CYLFMM_OK;
+}
+
+static cylfmm_status launch_p2m(const FarArgs &fa, unsigned grid, int P, int pp, cudaStream_t st)
+{
+    switch (p2m_rc(P)) {
+    case 2: p2m_kernel<2><<<grid, kP2MThreads, p2m_smem(P, pp), st>>>(fa); break;
+    case 3: p2m_kernel<3><<<grid, kP2MThreads, p2m_smem(P, pp), st>>>(fa); break;
+    default: p2m_kernel<5><<<grid, kP2MThreads, p2m_smem(P, pp), st>>>(fa); break;
+    }
     return CYLFMM_OK;
 }
 
@@ -270,14 +311,16 @@ static cylfmm_status direct_shape(int64_t n_src, int64_t n_fld, int K, DirectSha
     int dev = 0, nsm = 148;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    // warp-task kernel: tasks = (32-target tile, source partition of >= 128), ~12 tasks per
-    // resident CTA slot; the CTA-wide kernel serves the mode counts the warp kernel does not
+    // warp-task kernel: tasks = (32-target tile, source partition of >= 32: 8 per warp), ~12
+    // tasks per resident CTA slot (a lane walks its pairs one after another, so the C1-sized sum
+    // is bound by that chain: more, shorter partitions); the CTA-wide kernel serves the mode
+    // counts the warp kernel does not
     const bool wk = p2pw_enabled(K, false);
     const int TT = 32, SC = 4;
     int64_t tiles = (n_fld + TT - 1) / TT;
     int64_t want = (int64_t)nsm * (wk ? 12 * 3 : 4);
     int nparts = (int)std::max<int64_t>(1, std::min<int64_t>((want + tiles - 1) / tiles,
-                                                             (n_src + (wk ? 127 : 63)) / (wk ? 128 : 64)));
+                                                             (n_src + (wk ? 31 : 63)) / (wk ? 32 : 64)));
     int64_t per = (n_src + nparts - 1) / nparts;
     per = (per + SC - 1) / SC * SC;
     nparts = (int)((n_src + per - 1) / per);
@@ -374,8 +417,8 @@ extern "C" cylfmm_status cylfmm_direct(const double *src_r, const double *src_z,
             if (*q) cudaFreeAsync(*q, s);
         }
     } free_err{(void **)&d_err, st}, free_ws{(void **)&ws, st};
-    CK(cudaMallocAsync((void **)&d_err, 2 * sizeof(int), st));
-    if (sh.nparts > 1) CK(cudaMallocAsync((void **)&ws, sizeof(double2) * (size_t)sh.nparts * n_fld * K, st));
+    RET_IF(scratch_alloc((void **)&d_err, 2 * sizeof(int), st));
+    if (sh.nparts > 1) RET_IF(scratch_alloc((void **)&ws, sizeof(double2) * (size_t)sh.nparts * n_fld * K, st));
     RET_IF(direct_launch(sh, src_r, src_z, src_S, n_src, fld_r, fld_z, n_fld, K, miller,
                          exclude_coincident, out_Phi, d_err, ws, st));
     int h_err = 0;
@@ -452,7 +495,7 @@ extern "C" cylfmm_status cylfmm_greens_batch(const double *r, const double *r1, 
     if (n == 0) return CYLFMM_OK;
     cudaStream_t st = (cudaStream_t)stream;
     int *d_err;
-    CK(cudaMallocAsync((void **)&d_err, sizeof(int), st));
+    RET_IF(scratch_alloc((void **)&d_err, sizeof(int), st));
     CK(cudaMemsetAsync(d_err, 0, sizeof(int), st));
     greens_batch_kernel<<<nblk(n, 128), 128, 0, st>>>(r, r1, x, n, n_modes, miller,
                                                       forward_coef(n_modes - 1, miller), out_G, d_err);
@@ -514,8 +557,8 @@ extern "C" cylfmm_status cylfmm_tensor_batch(const double *r, const double *r1, 
     int Ni = std::max(n_modes - 1, 1), NM = Ni + 1, D = 2 * p + 1;
     double *seeds;
     int *d_err;
-    CK(cudaMallocAsync((void **)&seeds, sizeof(double) * (size_t)n * 4 * NM * D, st));
-    CK(cudaMallocAsync((void **)&d_err, sizeof(int), st));
+    RET_IF(scratch_alloc((void **)&seeds, sizeof(double) * (size_t)n * 4 * NM * D, st));
+    RET_IF(scratch_alloc((void **)&d_err, sizeof(int), st));
     CK(cudaMemsetAsync(d_err, 0, sizeof(int), st));
     TensorGeomArgs ta = {};
     ta.r = r;
@@ -1750,7 +1793,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             for (int l = 2; l <= d; ++l) {
                 if (fa.scount[l] == 0) continue;
                 fa.p2m_level = l;
-                p2m_kernel<<<(unsigned)((int64_t)fa.scount[l] * nmb), kP2MThreads, p2m_smem(P, pp), st>>>(fa);
+                RET_IF(launch_p2m(fa, (unsigned)((int64_t)fa.scount[l] * nmb), P, pp, st));
                 CKL();
                 p->launches++;
             }
@@ -1764,7 +1807,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             if (a1 > a0) {
                 const int nmb = (kw + kP2MModes - 1) / kP2MModes;
                 fa.p2m_slot0 = a0;
-                p2m_kernel<<<(unsigned)((int64_t)(a1 - a0) * nmb), kP2MThreads, p2m_smem(P, pp), st>>>(fa);
+                RET_IF(launch_p2m(fa, (unsigned)((int64_t)(a1 - a0) * nmb), P, pp, st));
                 CKL();
                 p->launches++;
             }
@@ -1837,7 +1880,10 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             const int64_t ppl = nf / std::max(ntl, 1);
             fa.l2p_tp = ppl < 8 ? 128 : (int)std::min<int64_t>(128, std::max<int64_t>(16, (int64_t)1 << (63 - __builtin_clzll(ppl))));
             const int gpc = kL2PThreads / fa.l2p_tp;
-            const int64_t ub_tasks = nf / fa.l2p_tp + ntl + 1;
+            // CTA-wide tasks (coarse evaluating boxes, C5) take two points per thread
+            const bool two = !grad && fa.l2p_tp == kL2PThreads;
+            fa.l2p_run = fa.l2p_tp * (two ? 2 : 1);
+            const int64_t ub_tasks = nf / fa.l2p_run + ntl + 1;
             if (m0 == 0 && !reuse) {   // evaluating box of every target leaf and the L2P runs
                 l2p_owner_kernel<<<nblk(ntl, 256), 256, 0, st>>>(fa, p->l2pown.as<int>());
                 CKL();
@@ -1862,11 +1908,16 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             const uint32_t *fk = fkey_s;
             const int *own = p->l2pown.as<int>(), *tst = p->l2ptask.as<int>(), *ntk = p->l2pntask.as<int>();
             const int tp = fa.l2p_tp;
-            if (grad) l2p_kernel<16, true><<<grid, kL2PThreads, l2p_smem<16>(Pl, kw, tp), st>>>(fa, fk, own, tst, ntk, ngrp);
-            else if (mb <= 4) l2p_kernel<4, false><<<grid, kL2PThreads, l2p_smem<4>(Pl, kw, tp), st>>>(fa, fk, own, tst, ntk, ngrp);
-            else if (mb <= 9) l2p_kernel<9, false><<<grid, kL2PThreads, l2p_smem<9>(Pl, kw, tp), st>>>(fa, fk, own, tst, ntk, ngrp);
-            else if (mb <= 13) l2p_kernel<13, false><<<grid, kL2PThreads, l2p_smem<13>(Pl, kw, tp), st>>>(fa, fk, own, tst, ntk, ngrp);
-            else l2p_kernel<16, false><<<grid, kL2PThreads, l2p_smem<16>(Pl, kw, tp), st>>>(fa, fk, own, tst, ntk, ngrp);
+#define L2P_GO(MBV, GR, PTV) \
+    l2p_kernel<MBV, GR, PTV><<<grid, kL2PThreads, l2p_smem<MBV>(Pl, kw, tp), st>>>(fa, fk, own, tst, ntk, ngrp)
+            if (grad) L2P_GO(16, true, 1);
+            else if (mb <= 4) { if (two) L2P_GO(4, false, 2); else L2P_GO(4, false, 1); }
+            else if (mb <= 9) { if (two) L2P_GO(9, false, 2); else L2P_GO(9, false, 1); }
+            else if (mb == 13 && two && Pl == 153 && kw % ngrp == 0)   // C5: order 16, 65 = 5 x 13
+                l2p_kernel<13, false, 2, 16, true><<<grid, kL2PThreads, l2p_smem<13>(Pl, kw, tp), st>>>(fa, fk, own, tst, ntk, ngrp);
+            else if (mb <= 13) { if (two) L2P_GO(13, false, 2); else L2P_GO(13, false, 1); }
+            else { if (two) L2P_GO(16, false, 2); else L2P_GO(16, false, 1); }
+#undef L2P_GO
             CKL();
             p->launches++;
         }

@@ -51,7 +51,8 @@ struct FarArgs {
     int lrow_lev[kMaxLevels + 1];       // first Lc row of each level (rows are level-major)
     int l2p_accumulate;                 // L2P adds onto out (the near field wrote it first)
     int64_t tfield;                     // field points (L2P)
-    int l2p_tp;                         // L2P task size (points)
+    int l2p_tp;                         // L2P threads per task
+    int l2p_run;                        // L2P task size (points): l2p_tp x points per thread
     int p2m_slot0;                      // P2M: first leaf slot (multi-device split)
     int p2m_level;                      // P2M: level of the boxes (0: the leaf level d)
     int sigma;                          // adaptive source tree leaf size (R#26), 0 = uniform
@@ -76,14 +77,20 @@ __device__ __forceinline__ void box_centre(uint32_t key, int level, double L, do
 // ---------------------------------------------------------------------------------------------
 // P2M at the leaves, as a small complex-by-real GEMM per leaf:
 //   M^(n)_ij = sum_q S_q^(n) mono_q[ij],  mono_q[ij] = ((r_q - r_c)/h)^i ((z_q - z_c)/h)^j.
-// CTA per (source leaf, block of kP2MModes modes); sources streamed through shared memory in
-// chunks of kP2MSrc (monomials computed once per chunk); thread tile = 2 modes x kP2MRC
-// coefficients in registers (20 DFMA per 7 shared loads per source).
+// CTA per (source leaf, block of <= kP2MModes modes); sources streamed through shared memory in
+// chunks of kP2MSrc (monomials computed once per chunk).  Warp w owns nv_w of the block's modes
+// (the nm modes dealt as evenly as 4 warps allow: 13 = 4 + 3 + 3 + 3, a compile-time count per
+// warp: no mode slot multiplies zeros), lane = RC coefficients: thread tile nv x RC in registers,
+// the coefficient row read as warp broadcasts, the monomials from a lane-major layout
+// (slot(c) = (c % RC) * 32 + c / RC: conflict-free).  (Before: every warp held 4 x 4 mode slots,
+// 16 for K = 65's blocks of 13, 19% of the FP64 issue on zero rows; ncu FP64 pipe 50%.)
 constexpr int kP2MSrc = 32;
 constexpr int kP2MModes = 16;
-constexpr int kP2MTM = 4;                                    // modes per thread
-constexpr int kP2MRC = 5;                                    // coefficients per thread
-constexpr int kP2MThreads = (kP2MModes / kP2MTM) * 32;       // 32 x 5 >= P (p <= 16)
+constexpr int kP2MTM = 4;                                    // modes per thread (at most)
+constexpr int kP2MThreads = (kP2MModes / kP2MTM) * 32;
+// coefficients per lane RC = 2 / 3 / 5 by order (32 RC >= P: p <= 9 / 12 / 16), so that most
+// lanes hold coefficients at every order (RC = 5 at p = 8 left 23 of 32 lanes idle)
+__host__ __device__ constexpr int p2m_rc(int P) { return P <= 64 ? 2 : (P <= 96 ? 3 : 5); }
 
 // 16-byte asynchronous global -> shared copy (zero fill when !valid)
 __device__ __forceinline__ void p2m_async16(void *smem, const void *gmem, bool valid)
@@ -92,8 +99,32 @@ __device__ __forceinline__ void p2m_async16(void *smem, const void *gmem, bool v
                  "l"(gmem), "r"(valid ? 16 : 0));
 }
 
-__global__ void __launch_bounds__(kP2MThreads) p2m_kernel(FarArgs a)
+template <int NV, int kP2MRC>
+__device__ __forceinline__ void p2m_chunk(const double2 *Sx, const double *mono, int nc, int lane,
+                                          double2 (&acc)[kP2MTM][kP2MRC])
 {
+    constexpr int kP2MRow = 32 * kP2MRC;
+    for (int q = 0; q < nc; ++q) {
+        double2 sv[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) sv[v] = Sx[q * kP2MModes + v];
+        const double *mq = mono + q * kP2MRow + lane;
+#pragma unroll
+        for (int u = 0; u < kP2MRC; ++u) {
+            const double m = mq[u * 32];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                acc[v][u].x = fma(sv[v].x, m, acc[v][u].x);
+                acc[v][u].y = fma(sv[v].y, m, acc[v][u].y);
+            }
+        }
+    }
+}
+
+template <int kP2MRC>
+__global__ void __launch_bounds__(kP2MThreads, 4) p2m_kernel(FarArgs a)
+{
+    constexpr int kP2MRow = 32 * kP2MRC, NE = (kP2MRow + kP2MThreads - 1) / kP2MThreads;
     extern __shared__ double sm[];
     const int p = a.p, P = a.P, KW = a.m1 - a.m0, d = a.depth;
     // balanced mode blocks of <= kP2MModes (K = 65: 5 x 13, not 4 x 16 + 1)
@@ -101,16 +132,25 @@ __global__ void __launch_bounds__(kP2MThreads) p2m_kernel(FarArgs a)
     const int mb = blockIdx.x % nmb;
     const int slot = a.p2m_slot0 + blockIdx.x / nmb, n0 = (KW * mb) / nmb;
     const int nm = (KW * (mb + 1)) / nmb - n0;
-    double *mono = sm;                                                  // [kP2MSrc][P]
-    double2 *Sx = reinterpret_cast<double2 *>(mono + kP2MSrc * P);      // [kP2MSrc][kP2MModes]
+    double *mono = sm;                                                  // [kP2MSrc][kP2MRow]
+    double2 *Sx = reinterpret_cast<double2 *>(mono + kP2MSrc * kP2MRow);   // [kP2MSrc][kP2MModes]
     double *pw = reinterpret_cast<double *>(Sx + kP2MSrc * kP2MModes);  // [kP2MSrc][2][p+1]
-    int *mi = reinterpret_cast<int *>(pw + kP2MSrc * 2 * (p + 1));      // [P] i, then [P] j
-    int *mj = mi + P;
-    for (int c = threadIdx.x; c < P; c += kP2MThreads) {
-        int i = 0;
-        while (i < p && c >= (i + 1) * (p + 1) - (i + 1) * i / 2) ++i;
-        mi[c] = i;
-        mj[c] = c - (i * (p + 1) - i * (i - 1) / 2);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // this thread's monomial slots s = tid, tid + 128 (coefficient c = RC (s % 32) + s / 32)
+    int ci[NE], cj[NE];
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+        const int sl = threadIdx.x + e * kP2MThreads;
+        const int c = kP2MRC * (sl % 32) + sl / 32;
+        ci[e] = cj[e] = -1;
+        if (sl < kP2MRow && c < P) {
+            int i = 0;
+            while (i < p && c >= (i + 1) * (p + 1) - (i + 1) * i / 2) ++i;
+            ci[e] = i;
+            cj[e] = c - (i * (p + 1) - i * (i - 1) / 2);
+        } else if (sl < kP2MRow) {
+            for (int qq = 0; qq < kP2MSrc; ++qq) mono[qq * kP2MRow + sl] = 0.0;   // slots past P
+        }
     }
     // level lv (adaptive source tree: every level, leaves only; uniform: the leaf level d)
     const int lv = a.p2m_level ? a.p2m_level : d, sh = 2 * (d - lv);
@@ -120,9 +160,10 @@ __global__ void __launch_bounds__(kP2MThreads) p2m_kernel(FarArgs a)
     double rc, zc, h;
     box_centre(key, lv, a.L, a.z0, rc, zc, h);
     const double inv_h = 1.0 / h;
-    const int tn = threadIdx.x % (kP2MModes / kP2MTM), tc = threadIdx.x / (kP2MModes / kP2MTM);
-    const int c0 = tc * kP2MRC;
-    const bool active = c0 < P && kP2MTM * tn < nm;
+    // the warp's modes [w0, w0 + nv) of the block
+    const int nv = nm / 4 + (warp < nm % 4 ? 1 : 0);
+    const int w0 = warp * (nm / 4) + min(warp, nm % 4);
+    const int c0 = lane * kP2MRC;
     double2 acc[kP2MTM][kP2MRC];
 #pragma unroll
     for (int v = 0; v < kP2MTM; ++v)
@@ -144,59 +185,47 @@ __global__ void __launch_bounds__(kP2MThreads) p2m_kernel(FarArgs a)
                 }
             }
         }
-        __syncthreads();
-        // monomials dr^i dz^j: thread per coefficient c (its (i, j) in registers), all sources
-        for (int c = threadIdx.x; c < P; c += kP2MThreads) {
-            const int ci = mi[c], cj = mj[c];
-            for (int qq = 0; qq < nc; ++qq)
-                mono[qq * P + c] = pw[(qq * 2) * (p + 1) + ci] * pw[(qq * 2 + 1) * (p + 1) + cj];
-        }
         // coefficient rows by asynchronous copies (in flight while the monomials are formed)
-        // (mode n = kP2MTM tn + v of source q at Sx[q][v][tn]: a warp's four tn of one v are 64
-        // contiguous bytes, one conflict-free wavefront)
         for (int e = threadIdx.x; e < nc * kP2MModes; e += kP2MThreads) {
             const int q = e / kP2MModes, n = e % kP2MModes;
             const bool v = n < nm;
-            p2m_async16(Sx + q * kP2MModes + (n % kP2MTM) * (kP2MModes / kP2MTM) + n / kP2MTM,
-                        v ? a.S + (int64_t)(s0 + q) * a.K + a.m0 + n0 + n : a.S, v);
+            p2m_async16(Sx + q * kP2MModes + n, v ? a.S + (int64_t)(s0 + q) * a.K + a.m0 + n0 + n : a.S, v);
+        }
+        __syncthreads();
+        // monomials dr^i dz^j: thread per slot (its (i, j) in registers), all sources
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+            if (ci[e] < 0) continue;
+            const int sl = threadIdx.x + e * kP2MThreads;
+            for (int qq = 0; qq < nc; ++qq)
+                mono[qq * kP2MRow + sl] = pw[(qq * 2) * (p + 1) + ci[e]] * pw[(qq * 2 + 1) * (p + 1) + cj[e]];
         }
         asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
         __syncthreads();
-        if (active) {
-            for (int q = 0; q < nc; ++q) {
-                double2 sv[kP2MTM];
-#pragma unroll
-                for (int v = 0; v < kP2MTM; ++v) sv[v] = Sx[q * kP2MModes + v * (kP2MModes / kP2MTM) + tn];
-                const double *mq = mono + q * P + c0;
-#pragma unroll
-                for (int u = 0; u < kP2MRC; ++u) {
-                    const double m = c0 + u < P ? mq[u] : 0.0;
-#pragma unroll
-                    for (int v = 0; v < kP2MTM; ++v) {
-                        acc[v][u].x = fma(sv[v].x, m, acc[v][u].x);
-                        acc[v][u].y = fma(sv[v].y, m, acc[v][u].y);
-                    }
-                }
-            }
+        const double2 *Sw = Sx + w0;
+        switch (nv) {   // warp-uniform
+        case 4: p2m_chunk<4, kP2MRC>(Sw, mono, nc, lane, acc); break;
+        case 3: p2m_chunk<3, kP2MRC>(Sw, mono, nc, lane, acc); break;
+        case 2: p2m_chunk<2, kP2MRC>(Sw, mono, nc, lane, acc); break;
+        case 1: p2m_chunk<1, kP2MRC>(Sw, mono, nc, lane, acc); break;
+        default: break;
         }
     }
-    if (active) {
-        double2 *Mo = a.M + (a.soff[lv] + slot) * (int64_t)KW * P;
+    double2 *Mo = a.M + (a.soff[lv] + slot) * (int64_t)KW * P;
 #pragma unroll
-        for (int v = 0; v < kP2MTM; ++v) {
-            const int n = n0 + kP2MTM * tn + v;
-            if (kP2MTM * tn + v >= nm) continue;
+    for (int v = 0; v < kP2MTM; ++v) {
+        if (v >= nv) break;
+        const int n = n0 + w0 + v;
 #pragma unroll
-            for (int u = 0; u < kP2MRC; ++u)
-                if (c0 + u < P) Mo[(int64_t)n * P + c0 + u] = acc[v][u];
-        }
+        for (int u = 0; u < kP2MRC; ++u)
+            if (c0 + u < P) Mo[(int64_t)n * P + c0 + u] = acc[v][u];
     }
 }
 
 inline size_t p2m_smem(int P, int p)
 {
-    return sizeof(double) * kP2MSrc * P + sizeof(double2) * kP2MSrc * kP2MModes +
-           sizeof(double) * kP2MSrc * 2 * (p + 1) + sizeof(int) * 2 * P;
+    return sizeof(double) * kP2MSrc * 32 * p2m_rc(P) + sizeof(double2) * kP2MSrc * kP2MModes +
+           sizeof(double) * kP2MSrc * 2 * (p + 1);
 }
 
 // binomial C(n, k) for n <= 2 * 20 (exact in FP64)
@@ -513,7 +542,7 @@ __global__ void l2p_task_flags_kernel(FarArgs a, const uint32_t *fkey, const int
 {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= a.tfield) return;
-    flag[t] = (t % a.l2p_tp == 0 || point_owner(a, fkey, owner, t) != point_owner(a, fkey, owner, t - 1)) ? 1 : 0;
+    flag[t] = (t % a.l2p_run == 0 || point_owner(a, fkey, owner, t) != point_owner(a, fkey, owner, t - 1)) ? 1 : 0;
 }
 __global__ void l2p_task_emit_kernel(int64_t nf, const int *flag, const int *pos, int *tstart)
 {
@@ -528,12 +557,21 @@ __global__ void l2p_task_emit_kernel(int64_t nf, const int *flag, const int *pos
 // shared-memory broadcasts (the points of a task evaluate the same box): MB vector loads for
 // 2 MB DFMA per coefficient.  GRAD: also d/dr and d/dz of the local polynomial (SURVEY 8(f)
 // item 3), from k dr^(k-1) dz^l and l dr^k dz^(l-1).
-template <int MB, bool GRAD>
-__global__ void __launch_bounds__(kL2PThreads) l2p_kernel(FarArgs a, const uint32_t *fkey, const int *owner,
+// PT = 2 (tasks of 2 TP points, thread = points ip and ip + TP): the inner loop is bound by the
+// shared-memory pipe (one 16-byte coefficient broadcast per 2 DFMA: ncu lsu wavefronts 83%, FP64
+// pipe 43% at C5), so a coefficient read serves two points (4 DFMA); warps without a second
+// point run the one-point loop.
+// PL > 0: compile-time local order (the row stride P becomes an immediate: one address register
+// for the MB coefficient loads of a step, which the compiler then issues as a batch); EXACT:
+// every mode group holds exactly MB modes (no per-mode predicates).
+template <int MB, bool GRAD, int PT = 1, int PL = 0, bool EXACT = false>
+__global__ void __launch_bounds__(kL2PThreads, PT == 2 ? 3 : 1) l2p_kernel(FarArgs a, const uint32_t *fkey, const int *owner,
                                                           const int *tstart, const int *ntasks, int ngrp)
 {
+    static_assert(PT == 1 || !GRAD, "two points per thread: potential only");
     extern __shared__ double sm[];
-    const int p = a.pl, P = a.Pl, KW = a.m1 - a.m0, d = a.depth;   // local order
+    const int p = PL ? PL : a.pl, P = PL ? (PL + 1) * (PL + 2) / 2 : a.Pl;   // local order
+    const int KW = a.m1 - a.m0, d = a.depth;
     const int TP = a.l2p_tp, gpc = kL2PThreads / TP;
     const int ngi = (ngrp + gpc - 1) / gpc;                          // CTA items per task
     double2 *loc = reinterpret_cast<double2 *>(sm);                 // [staged modes][Pl]
@@ -553,7 +591,8 @@ __global__ void __launch_bounds__(kL2PThreads) l2p_kernel(FarArgs a, const uint3
     const int n0 = (KW * g) / ngrp, nm = jg < nG ? (KW * (g + 1)) / ngrp - n0 : 0;   // <= MB
     const int own = point_owner(a, fkey, owner, t0);
     const int64_t t = t0 + ip;
-    double inv_h = 0.0, dr = 0.0, dz = 0.0;
+    double inv_h = 0.0, dr = 0.0, dz = 0.0, dr2 = 0.0, dz2 = 0.0;
+    const bool two = PT == 2 && __any_sync(0xffffffffu, t + TP < t1);   // warp-uniform
     if (own >= 0) {
         if (threadIdx.x == 0) {
             l2p_fence_proxy();
@@ -567,11 +606,60 @@ __global__ void __launch_bounds__(kL2PThreads) l2p_kernel(FarArgs a, const uint3
             dr = (a.fr[t] - rc) * inv_h;
             dz = (a.fz[t] - zc) * inv_h;
         }
+        if (PT == 2 && t + TP < t1) {
+            dr2 = (a.fr[t + TP] - rc) * inv_h;
+            dz2 = (a.fz[t + TP] - zc) * inv_h;
+        }
         l2p_mbar_wait(bar, phase);
         phase ^= 1u;
     }
     const double2 *lg = loc + (size_t)(n0 - nA) * P;
-    if (t < t1 && nm > 0) {
+    if (PT == 2 && two) {
+    if (nm > 0) {   // (a warp with a second point: every lane has its first)
+    double2 acc[MB], acc2[MB];
+#pragma unroll
+    for (int m = 0; m < MB; ++m) acc[m] = acc2[m] = make_double2(0.0, 0.0);
+    if (own >= 0) {
+        double pr = 1.0, pr2 = 1.0;
+        int q = 0;
+        for (int k = 0; k <= p; ++k) {
+            double pz = pr, pz2 = pr2;
+            for (int l = 0; k + l <= p; ++l, ++q) {
+#pragma unroll
+                for (int m = 0; m < MB; ++m) {
+                    if (EXACT || m < nm) {
+                        const double2 c = lg[m * P + q];
+                        acc[m].x = fma(c.x, pz, acc[m].x);
+                        acc[m].y = fma(c.y, pz, acc[m].y);
+                        acc2[m].x = fma(c.x, pz2, acc2[m].x);
+                        acc2[m].y = fma(c.y, pz2, acc2[m].y);
+                    }
+                }
+                pz *= dz;
+                pz2 *= dz2;
+            }
+            pr *= dr;
+            pr2 *= dr2;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        if (j == 1 && t + TP >= t1) break;
+        double2 *o = a.out + a.fperm[t + j * TP] * a.K + a.m0 + n0;
+#pragma unroll
+        for (int m = 0; m < MB; ++m) {
+            if (m >= nm) break;
+            const double2 s = j ? acc2[m] : acc[m];
+            double2 v = make_double2(s.x * inv_h, s.y * inv_h);
+            if (a.l2p_accumulate) {
+                const double2 cur = o[m];
+                v = make_double2(fma(s.x, inv_h, cur.x), fma(s.y, inv_h, cur.y));
+            }
+            o[m] = v;
+        }
+    }
+    }
+    } else if (t < t1 && nm > 0) {
     const int64_t row = a.fperm[t];
     double2 acc[MB], accr[GRAD ? MB : 1], accz[GRAD ? MB : 1];
 #pragma unroll
