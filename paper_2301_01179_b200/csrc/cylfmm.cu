@@ -198,6 +198,7 @@ static cylfmm_status ensure_init()
 #define X(...) CK(allow_smem(s2l_batch_kernel<__VA_ARGS__>));
     S2L_ALL(X)
 #undef X
+    CK((allow_smem(s2l_batch_units_kernel<S2L_P16, 2>)));
     if (dev < 64) {
         cudaMemPoolProps props = {};
         props.allocType = cudaMemAllocationTypePinned;
@@ -1069,20 +1070,29 @@ extern "C" cylfmm_status cylfmm_tree_sort(const double *r, const double *z, int6
 // FMM solve
 static int64_t pow4(int l) { return (int64_t)1 << (2 * l); }
 
-template <int R, int C, int NU, int CG>
+template <int R, int C, int NU, int CG, int U = 1>
 static cudaError_t launch_s2l_t(const S2LArgs &sa, int64_t nbatches, cudaStream_t st)
 {
     const int KW = sa.m1 - sa.m0;
     if (nbatches == 0) return cudaSuccess;
     size_t sm = s2l_smem_bytes<R, C, NU, CG>(sa.p, sa.pl);
-    s2l_batch_kernel<R, C, NU, CG><<<(unsigned)(nbatches * KW), NU * CG, sm, st>>>(sa);
+    if (U > 1)
+        s2l_batch_units_kernel<R, C, NU, CG, U><<<(unsigned)(nbatches * KW), ((NU + U - 1) / U) * CG, sm, st>>>(sa);
+    else
+        s2l_batch_kernel<R, C, NU, CG><<<(unsigned)(nbatches * KW), NU * CG, sm, st>>>(sa);
     return cudaGetLastError();
 }
 // class by the local order (units(pl, R) <= NU)
-static cudaError_t launch_s2l(const S2LArgs &sa, int64_t nbatches, cudaStream_t st)
+// p > 12 with well-filled batches (>= 90% of the JT pair slots, C4's clusters): two units per
+// thread (C4 S2L 37.3 -> 35.9 ms).  Sparse stations (C5: 8.5 pairs per batch of 12, a third of
+// the column groups idle) keep one unit per thread, whose CTAs hold twice the warps (C5 S2L 36.0
+// vs 37.7 ms with two).  The p <= 12 shape with two units (144 threads, 136 registers): C3 S2L
+// 34.0 vs 20.9 ms, not kept.
+static cudaError_t launch_s2l(const S2LArgs &sa, int64_t nbatches, int64_t npairs, cudaStream_t st)
 {
     if (sa.pl <= 8) return launch_s2l_t<S2L_P8>(sa, nbatches, st);
     if (sa.pl <= 12) return launch_s2l_t<S2L_P12>(sa, nbatches, st);
+    if (10 * npairs >= 9 * nbatches * S2LCfg<S2L_P16>::JT) return launch_s2l_t<S2L_P16, 2>(sa, nbatches, st);
     return launch_s2l_t<S2L_P16>(sa, nbatches, st);
 }
 
@@ -1850,7 +1860,7 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             sa.m0 = fa.m0;
             sa.m1 = fa.m1;
             ra.KW = kw;
-            CK(launch_s2l(sa, nbatches, st));
+            CK(launch_s2l(sa, nbatches, npairs, st));
             const int64_t witems = (int64_t)nwritten * kw;
             s2l_reduce_kernel<<<(unsigned)std::min<int64_t>((witems + 7) / 8, (int64_t)p->nsm * 16), 256, 0, st>>>(ra);
             CKL();
@@ -1880,7 +1890,8 @@ static cylfmm_status fmm_solve_impl(cylfmm_plan p, const double *src_r, const do
             const int64_t ppl = nf / std::max(ntl, 1);
             fa.l2p_tp = ppl < 8 ? 128 : (int)std::min<int64_t>(128, std::max<int64_t>(16, (int64_t)1 << (63 - __builtin_clzll(ppl))));
             const int gpc = kL2PThreads / fa.l2p_tp;
-            // CTA-wide tasks (coarse evaluating boxes, C5) take two points per thread
+            // CTA-wide tasks (coarse evaluating boxes, C5) take two points per thread (four points
+            // on groups of 5 modes measured slower: C5 10.05 vs 9.73 ms)
             const bool two = !grad && fa.l2p_tp == kL2PThreads;
             fa.l2p_run = fa.l2p_tp * (two ? 2 : 1);
             const int64_t ub_tasks = nf / fa.l2p_run + ntl + 1;

@@ -550,6 +550,41 @@ __global__ void l2p_task_emit_kernel(int64_t nf, const int *flag, const int *pos
     if (t < nf && flag[t]) tstart[pos[t]] = (int)t;
 }
 
+// NP points of one thread against the MB modes of a staged local (potential only): a coefficient
+// broadcast feeds 2 NP DFMA.  dr, dz: the points' normalised offsets (absent points: zeros).
+template <int MB, int NP, bool EXACT, int NPA>
+__device__ __forceinline__ void l2p_points(const double2 *lg, int P, int p, int nm,
+                                           const double (&dr)[NPA], const double (&dz)[NPA],
+                                           double2 (&acc)[NPA][MB])
+{
+    double pr[NP];
+#pragma unroll
+    for (int j = 0; j < NP; ++j) pr[j] = 1.0;
+    int q = 0;
+    for (int k = 0; k <= p; ++k) {
+        double pz[NP];
+#pragma unroll
+        for (int j = 0; j < NP; ++j) pz[j] = pr[j];
+        for (int l = 0; k + l <= p; ++l, ++q) {
+#pragma unroll
+            for (int m = 0; m < MB; ++m) {
+                if (EXACT || m < nm) {
+                    const double2 c = lg[m * P + q];
+#pragma unroll
+                    for (int j = 0; j < NP; ++j) {
+                        acc[j][m].x = fma(c.x, pz[j], acc[j][m].x);
+                        acc[j][m].y = fma(c.y, pz[j], acc[j][m].y);
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < NP; ++j) pz[j] *= dz[j];
+        }
+#pragma unroll
+        for (int j = 0; j < NP; ++j) pr[j] *= dr[j];
+    }
+}
+
 // CTA item = (task, gpc = 128 / TP consecutive groups of <= MB modes): the evaluating box's
 // local (the groups' modes, one contiguous block of the compact local storage) arrives by one TMA
 // bulk copy; thread = (field point, mode group), monomials (r - r_c)^k (z - z_c)^l / h^(k+l)
@@ -557,18 +592,20 @@ __global__ void l2p_task_emit_kernel(int64_t nf, const int *flag, const int *pos
 // shared-memory broadcasts (the points of a task evaluate the same box): MB vector loads for
 // 2 MB DFMA per coefficient.  GRAD: also d/dr and d/dz of the local polynomial (SURVEY 8(f)
 // item 3), from k dr^(k-1) dz^l and l dr^k dz^(l-1).
-// PT = 2 (tasks of 2 TP points, thread = points ip and ip + TP): the inner loop is bound by the
-// shared-memory pipe (one 16-byte coefficient broadcast per 2 DFMA: ncu lsu wavefronts 83%, FP64
-// pipe 43% at C5), so a coefficient read serves two points (4 DFMA); warps without a second
-// point run the one-point loop.
+// PT = 2, 4 (tasks of PT TP points, thread = points ip + j TP): the inner loop is bound by the
+// shared-memory pipe (a 16-byte coefficient broadcast is 2 wavefronts of the SM's one per clock,
+// 2 DFMA are 4 clocks of one of its four FP64 pipes: ncu lsu wavefronts 83%, FP64 pipe 43% at C5
+// with one point per thread, 65% / 52% with two), so a coefficient read serves PT points; warps
+// with fewer points run the loop for 2 or 1.
 // PL > 0: compile-time local order (the row stride P becomes an immediate: one address register
 // for the MB coefficient loads of a step, which the compiler then issues as a batch); EXACT:
 // every mode group holds exactly MB modes (no per-mode predicates).
 template <int MB, bool GRAD, int PT = 1, int PL = 0, bool EXACT = false>
-__global__ void __launch_bounds__(kL2PThreads, PT == 2 ? 3 : 1) l2p_kernel(FarArgs a, const uint32_t *fkey, const int *owner,
+__global__ void __launch_bounds__(kL2PThreads, PT >= 2 ? 3 : 1) l2p_kernel(FarArgs a, const uint32_t *fkey, const int *owner,
                                                           const int *tstart, const int *ntasks, int ngrp)
 {
-    static_assert(PT == 1 || !GRAD, "two points per thread: potential only");
+    static_assert(PT == 1 || !GRAD, "several points per thread: potential only");
+    static_assert(PT == 1 || PT == 2 || PT == 4, "points per thread");
     extern __shared__ double sm[];
     const int p = PL ? PL : a.pl, P = PL ? (PL + 1) * (PL + 2) / 2 : a.Pl;   // local order
     const int KW = a.m1 - a.m0, d = a.depth;
@@ -591,8 +628,16 @@ __global__ void __launch_bounds__(kL2PThreads, PT == 2 ? 3 : 1) l2p_kernel(FarAr
     const int n0 = (KW * g) / ngrp, nm = jg < nG ? (KW * (g + 1)) / ngrp - n0 : 0;   // <= MB
     const int own = point_owner(a, fkey, owner, t0);
     const int64_t t = t0 + ip;
-    double inv_h = 0.0, dr = 0.0, dz = 0.0, dr2 = 0.0, dz2 = 0.0;
-    const bool two = PT == 2 && __any_sync(0xffffffffu, t + TP < t1);   // warp-uniform
+    double inv_h = 0.0, dr = 0.0, dz = 0.0;
+    double drs[PT], dzs[PT];   // points t + j TP (PT > 1)
+#pragma unroll
+    for (int j = 0; j < PT; ++j) drs[j] = dzs[j] = 0.0;
+    // points per thread this warp needs (warp-uniform): 1 runs the one-point loop below
+    int np = 1;
+    if (PT > 1) {
+        np = __any_sync(0xffffffffu, t + TP < t1) ? 2 : 1;
+        if (PT > 2 && __any_sync(0xffffffffu, t + 2 * TP < t1)) np = 4;
+    }
     if (own >= 0) {
         if (threadIdx.x == 0) {
             l2p_fence_proxy();
@@ -606,54 +651,42 @@ __global__ void __launch_bounds__(kL2PThreads, PT == 2 ? 3 : 1) l2p_kernel(FarAr
             dr = (a.fr[t] - rc) * inv_h;
             dz = (a.fz[t] - zc) * inv_h;
         }
-        if (PT == 2 && t + TP < t1) {
-            dr2 = (a.fr[t + TP] - rc) * inv_h;
-            dz2 = (a.fz[t + TP] - zc) * inv_h;
+        if (PT > 1) {
+#pragma unroll
+            for (int j = 0; j < PT; ++j) {
+                if (t + j * TP < t1) {
+                    drs[j] = (a.fr[t + j * TP] - rc) * inv_h;
+                    dzs[j] = (a.fz[t + j * TP] - zc) * inv_h;
+                }
+            }
         }
         l2p_mbar_wait(bar, phase);
         phase ^= 1u;
     }
     const double2 *lg = loc + (size_t)(n0 - nA) * P;
-    if (PT == 2 && two) {
+    if (PT > 1 && np > 1) {
     if (nm > 0) {   // (a warp with a second point: every lane has its first)
-    double2 acc[MB], acc2[MB];
+    double2 acc[PT][MB];
 #pragma unroll
-    for (int m = 0; m < MB; ++m) acc[m] = acc2[m] = make_double2(0.0, 0.0);
+    for (int j = 0; j < PT; ++j)
+#pragma unroll
+        for (int m = 0; m < MB; ++m) acc[j][m] = make_double2(0.0, 0.0);
     if (own >= 0) {
-        double pr = 1.0, pr2 = 1.0;
-        int q = 0;
-        for (int k = 0; k <= p; ++k) {
-            double pz = pr, pz2 = pr2;
-            for (int l = 0; k + l <= p; ++l, ++q) {
-#pragma unroll
-                for (int m = 0; m < MB; ++m) {
-                    if (EXACT || m < nm) {
-                        const double2 c = lg[m * P + q];
-                        acc[m].x = fma(c.x, pz, acc[m].x);
-                        acc[m].y = fma(c.y, pz, acc[m].y);
-                        acc2[m].x = fma(c.x, pz2, acc2[m].x);
-                        acc2[m].y = fma(c.y, pz2, acc2[m].y);
-                    }
-                }
-                pz *= dz;
-                pz2 *= dz2;
-            }
-            pr *= dr;
-            pr2 *= dr2;
-        }
+        if (PT > 2 && np > 2) l2p_points<MB, PT, EXACT, PT>(lg, P, p, nm, drs, dzs, acc);
+        else l2p_points<MB, 2, EXACT, PT>(lg, P, p, nm, drs, dzs, acc);
     }
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        if (j == 1 && t + TP >= t1) break;
+    for (int j = 0; j < PT; ++j) {
+        if (j >= np || t + j * TP >= t1) break;
         double2 *o = a.out + a.fperm[t + j * TP] * a.K + a.m0 + n0;
 #pragma unroll
         for (int m = 0; m < MB; ++m) {
             if (m >= nm) break;
-            const double2 s = j ? acc2[m] : acc[m];
-            double2 v = make_double2(s.x * inv_h, s.y * inv_h);
+            const double2 sv = acc[j][m];
+            double2 v = make_double2(sv.x * inv_h, sv.y * inv_h);
             if (a.l2p_accumulate) {
                 const double2 cur = o[m];
-                v = make_double2(fma(s.x, inv_h, cur.x), fma(s.y, inv_h, cur.y));
+                v = make_double2(fma(sv.x, inv_h, cur.x), fma(sv.y, inv_h, cur.y));
             }
             o[m] = v;
         }

@@ -365,6 +365,177 @@ __global__ void __launch_bounds__(NU * CG, s2l_min_blocks<NU * CG>()) s2l_batch_
     }
 }
 
+// s2l_batch_units_kernel, U = 2: the same batch with two units per thread (u and u + NUT) on the
+// same C pairs (the one-unit kernel above is kept as it is: the generalised source compiled to a
+// slower one-unit kernel, C5 S2L 38.6 vs 36.0 ms).  The loop is bound by the
+// shared-memory pipe as much as by the FP64 pipe (per step C 16-byte moment loads, 2 clocks each
+// of the SM's register write-back, and one tensor value for 2 R C DFMA = 4 R C clocks of one of
+// four FP64 pipes: (2 C + 1) / (R C) = 0.75 at 3 x 4, plus bank conflicts on the tensor loads;
+// ncu: FP64 pipe 58%, memory pipes 79%); two units share the moment loads, halving them, without
+// the row-slot waste of longer units (units of 6 rows: 198 slots for p = 16's 153 rows).
+template <int R, int C, int NU, int CG, int U>
+__global__ void __launch_bounds__(((NU + U - 1) / U) * CG, 3)
+    s2l_batch_units_kernel(S2LArgs a)
+{
+    constexpr int NUT = (NU + U - 1) / U;   // unit slots (threads per column group)
+    constexpr int NT = NUT * CG, JT = CG * C;
+    extern __shared__ double sm[];
+    const int p = a.p, P = a.P, pl = a.pl, Pl = a.Pl, pt = a.pt;
+    const int KW = a.m1 - a.m0;
+    const int TP = (pt + 1) * (pt + 1) * (pt + 1), TPp = TP + (TP & 1);
+    const int BPS = P | 1;                            // moment row stride (complex, odd)
+    double2 *Xs = reinterpret_cast<double2 *>(sm);   // [JT][BPS] moments
+    double *Hs = reinterpret_cast<double *>(Xs + JT * BPS);   // [TPp + R + 2] (zero tail)
+    uint64_t *bar = reinterpret_cast<uint64_t *>(Hs + TPp + R + 2 + ((R + 2) & 1));
+    int4 *rec = reinterpret_cast<int4 *>(bar + 2);   // [JT]
+    int *Tk = reinterpret_cast<int *>(rec + JT);     // [(pl+1) * (p+1)] row offsets T(k, i)
+    int *ukl = Tk + 17 * 17;                         // [NU] units (k << 8 | l0), -1 = none
+
+    const int nloc = (int)(blockIdx.x % KW);
+    const int4 bt = a.batches[blockIdx.x / KW];
+    const int cnt = bt.y, skey = bt.z, inward = skey & 1;
+    const int64_t station = skey >> 1;
+    const int tid = threadIdx.x;
+    // warp 0 starts the copies at once (barrier, tensor block, one moment row per pair: backward
+    // pairs read the copy with (-1)^j folded in) while the other warps build the index tables
+    if (tid < 32) {
+        if (tid == 0) {
+            mbar_init(bar, 1);
+            fence_mbar_init();
+            mbar_arrive_expect_tx(bar, (unsigned)(TPp * 8 + cnt * P * 16));
+            bulk_g2s(Hs, a.tens + (station * KW + nloc) * (int64_t)TPp, (unsigned)(TPp * 8), bar);
+        }
+        __syncwarp();
+        for (int b = tid; b < JT; b += 32) {
+            const int4 pr = b < cnt ? a.pairs[bt.x + b] : make_int4(0, -1, 0, 0);
+            rec[b] = pr;
+            if (b < cnt)
+                bulk_g2s(Xs + b * BPS, (pr.z ? a.Mb : a.M) + ((a.soff[pr.w] + pr.x) * KW + nloc) * P,
+                         (unsigned)(P * 16), bar);
+        }
+    } else {
+        for (int q = tid - 32; q < (pl + 1) * (p + 1); q += NT - 32) {
+            const int k = q / (p + 1), i = q - k * (p + 1);
+            Tk[q] = inward ? packed_row(i, k, pt) : packed_row(k, i, pt);
+        }
+        if (tid == 32) {
+            int u = 0;
+            for (int k = 0; k <= pl; ++k)
+                for (int l0 = 0; l0 <= pl - k; l0 += R) ukl[u++] = (k << 8) | l0;
+            for (; u < NU; ++u) ukl[u] = -1;
+            for (int e = 0; e < R + 2; ++e) Hs[TPp + e] = 0.0;
+        }
+    }
+    __syncthreads();   // tables, records and the initialised barrier
+    mbar_wait(bar, 0);
+    if (a.truncation == 1) {   // single truncation: H(a, b, c) = 0 for a + b + c > p
+        for (int q = tid; q < (pt + 1) * (pt + 1); q += NT) {
+            const int aa = q / (pt + 1), bb = q - aa * (pt + 1);
+            const int o = packed_row(aa, bb, pt);
+            for (int c = max(p - aa - bb + 1, 0); c <= 2 * pt - aa - bb; ++c) Hs[o + c] = 0.0;
+        }
+        __syncthreads();
+    }
+
+    const int ut = tid % NUT, cg = tid / NUT;
+    int uk[U], ul0[U];
+    bool uv[U];
+#pragma unroll
+    for (int e = 0; e < U; ++e) {
+        const int u = ut + e * NUT;
+        const int kl = u < NU ? ukl[u] : -1;
+        uv[e] = kl >= 0;
+        uk[e] = uv[e] ? kl >> 8 : 0;      // (an absent second unit walks unit (0, 0): discarded)
+        ul0[e] = uv[e] ? kl & 0xff : 0;
+    }
+    if (!uv[0] || cg * C >= cnt) return;
+    double2 acc[U][R][C];
+#pragma unroll
+    for (int e = 0; e < U; ++e)
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int c = 0; c < C; ++c) acc[e][r][c] = make_double2(0.0, 0.0);
+    const double2 *X0 = Xs + cg * C * BPS;
+    // one step j of the Hankel product: rows r use H[T(k,i) + l0 + j + r] = w[(j + r) % R]
+    // (ring slot of H[.. + s] is s % R); x holds M'_(i,j) of the C pairs, xn is prefetched
+    auto step = [&](const double *const (&h)[U], const double2 *X, int j, int t, double (&w)[U][R],
+                    double2 (&xn)[C]) {
+        double2 x[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) x[c] = xn[c];
+#pragma unroll
+        for (int c = 0; c < C; ++c) xn[c] = X[c * BPS + j + 1];   // next step (may run one past)
+#pragma unroll
+        for (int e = 0; e < U; ++e) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const double hv = w[e][(t + r) % R];
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                    acc[e][r][c].x = fma(hv, x[c].x, acc[e][r][c].x);
+                    acc[e][r][c].y = fma(hv, x[c].y, acc[e][r][c].y);
+                }
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < U; ++e) w[e][t] = h[e][j + R];
+    };
+    for (int i = 0; i <= p; ++i) {
+        const int jn = p + 1 - i;   // steps j = 0 .. p - i
+        const double *h[U];
+#pragma unroll
+        for (int e = 0; e < U; ++e) h[e] = Hs + Tk[uk[e] * (p + 1) + i] + ul0[e];
+        const double2 *X = X0 + i * (p + 1) - i * (i - 1) / 2;
+        double w[U][R];
+        double2 xn[C];
+#pragma unroll
+        for (int e = 0; e < U; ++e)
+#pragma unroll
+            for (int r = 0; r < R; ++r) w[e][r] = h[e][r];
+#pragma unroll
+        for (int c = 0; c < C; ++c) xn[c] = X[c * BPS];
+        int j0 = 0;
+        for (; j0 + R <= jn; j0 += R) {   // full blocks: straight-line, loads run ahead
+#pragma unroll
+            for (int t = 0; t < R; ++t) step(h, X, j0 + t, t, w, xn);
+        }
+#pragma unroll
+        for (int t = 0; t < R - 1; ++t)   // remainder (warp-uniform)
+            if (j0 + t < jn) step(h, X, j0 + t, t, w, xn);
+    }
+    // rows (k, l0 + r): post-scale 1/l! (and (-1)^l for backward pairs), contiguous runs
+#pragma unroll
+    for (int e = 0; e < U; ++e) {
+        if (!uv[e]) break;
+        const int k = uk[e], l0 = ul0[e];
+        const int m0 = k * (pl + 1) - k * (k - 1) / 2 + l0;
+        double f[R];
+        {
+            double fl = 1.0;
+            for (int t = 2; t <= l0; ++t) fl *= t;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                if (r > 0) fl *= (l0 + r);
+                f[r] = 1.0 / fl;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            const int b = cg * C + c;
+            if (b >= cnt) break;
+            const int4 rc = rec[b];
+            double2 *dst = a.pairbuf + ((int64_t)rc.y * KW + nloc) * Pl + m0;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                if (l0 + r > pl - k) break;
+                const double sgn = (rc.z && ((l0 + r) & 1)) ? -f[r] : f[r];
+                dst[r] = make_double2(acc[e][r][c].x * sgn, acc[e][r][c].y * sgn);
+            }
+        }
+    }
+}
+
 template <int R, int C, int NU, int CG>
 inline size_t s2l_smem_bytes(int p, int pl)
 {
