@@ -300,6 +300,18 @@ def test_fmm_small_vs_oracle_fmm(gpu, orc, n, K, p, depth, L, z0, trunc, miller)
     assert e.max() <= TOL, e
 
 
+@pytest.mark.parametrize("n,p,pl,trunc", [(5000, 16, 0, 0), (5000, 16, 0, 1), (4000, 12, 14, 0)])
+def test_fmm_p16_full_batches_two_unit_s2l(gpu, orc, n, p, pl, trunc):
+    """S2L with two units per thread (s2l_batch_units_kernel: local order > 12 and >= 90% of the
+    batches' pair slots taken).  Uniform rings at depth 6 give 84k pairs in 7.5k batches of 12
+    (93% full; tools/s2l_buckets.py counts the same way), with ragged tail batches on every
+    station; the small p = 16 cases above (depth 3: 71% full) run the one-unit kernel."""
+    rng = np.random.default_rng(n + 2)
+    sr, sz, S = uniform_rings(rng, n, 2)
+    out, ref, _ = _fmm_case(gpu, orc, sr, sz, S, sr, sz, p, 6, 1.0, truncation=trunc, pl=pl)
+    assert eps_modes(out, ref).max() <= TOL
+
+
 @pytest.mark.parametrize("K", [1, 2, 9, 17, 20, 33, 34, 66])
 def test_near_field_warp_kernel_modes_and_pieces(gpu, orc, K):
     """Warp-task near field (p2p_warp.cuh): every compile-time mode bound (9, 17, 33, exact or

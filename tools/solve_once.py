@@ -13,6 +13,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("config")
     ap.add_argument("--warm", type=int, default=1)
+    ap.add_argument("--adaptive", type=int, nargs=2, metavar=("DEPTH", "LEAF"),
+                    help="adaptive source tree (bench.py's C4: 11 224)")
     a = ap.parse_args()
     import torch
     import paper_2301_01179_b200 as g
@@ -25,7 +27,9 @@ def main():
         fr, fz = sr, sz
     else:
         fr, fz = torch.as_tensor(pr.fr, device=dev), torch.as_tensor(pr.fz, device=dev)
-    plan = g.Plan(g.FMMConfig(n_modes=pr.K, order=pr.p, depth=pr.depth, L=pr.L, z0=pr.z0))
+    depth, leaf = a.adaptive if a.adaptive else (pr.depth, 0)
+    plan = g.Plan(g.FMMConfig(n_modes=pr.K, order=pr.p, depth=depth, L=pr.L, z0=pr.z0,
+                              adaptive_leaf=leaf))
     out = torch.empty((len(pr.fr), pr.K), dtype=torch.complex128, device=dev)
     for _ in range(a.warm + 1):
         plan.solve(sr, sz, S, fr, fz, out=out)
