@@ -51,8 +51,11 @@ def launches(path):
 
 
 def full(rep):
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    if rep.endswith(".csv"):   # a raw page exported on the GPU box (large reports stay there)
+        txt = open(rep).read()
+    else:
+        txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     if len(rows) < 3:
         return "(no --set full data)"
