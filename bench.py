@@ -242,7 +242,7 @@ def phase_flops(pr, tm):
             "p2m": ns * 4 * P * K}
 
 
-KERNEL_OF = {"s2l": "s2l_batch_kernel + s2l_reduce_kernel (S2L phase)",
+KERNEL_OF = {"s2l": "s2l_batch_kernel (full batches at p > 12: s2l_batch_units_kernel) + s2l_reduce_kernel (S2L phase)",
              "p2p": "p2p_warp_kernel (near-field phase)",
              "l2p": "l2p_kernel (L2P phase)", "p2m": "p2m_kernel (P2M phase)"}
 NCU_NAME = {"s2l": "s2l_batch_kernel", "p2p": "p2p_warp_kernel", "l2p": "l2p_kernel",
@@ -595,7 +595,10 @@ def main():
     traffic = None
     try:   # dram read + write bytes per step of the dominant kernel(s), committed ncu capture
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f)["per_step_dram_bytes"][args.config].get(NCU_NAME[dom])
+            per = json.load(f)["per_step_dram_bytes"][args.config]
+            traffic = per.get(NCU_NAME[dom])
+            if traffic is None and dom == "s2l":
+                traffic = per.get("s2l_batch_units_kernel")
     except Exception:
         pass
     roof = {"bound": "alu", "kernel": KERNEL_OF[dom], "achieved": ach, "peak": FP64_NOMINAL_TFLOPS,
